@@ -1,0 +1,225 @@
+/*
+ * kvfs.h — C ABI of the B200-native KVFS + batched `pred` attention hot path
+ * (arXiv 2510.25412, "Serve Programs, Not Prompts", Symphony).
+ *
+ * Citation key: P:n = PAPER.md line n, S:n = SPEC.md line n, §8 = SURVEY.md §8 (the scope table),
+ * R1..R12 = the readings in SURVEY.md §8(c) C3 restated in DESIGN.md "Readings".
+ *
+ * What the calls compute
+ *   pred (§4.1): "pred(kv: kv_file, tokens, positions) -> list[dist]"; the file is "updated
+ *   with new tensors corresponding to the provided tokens" and a result is returned "for each input
+ *   token".  This library implements the attention part of that system call for a batch of LIPs
+ *   (§4.4 P:241 "aggregates multiple pred system calls into a single batch"): given the already
+ *   projected Q / K_new / V_new rows of every LIP's new tokens it appends K_new / V_new into the LIP's
+ *   file and returns, per query row and head, softmax attention over exactly the tokens the file
+ *   retains (R10).  Tokens -> embeddings -> projections and the LM head / `dist` are outside (§2.1 M2/M3).
+ *   KVFS (§4.2): the KV cache as files over fixed-size pages ("PagedAttention"), with
+ *   open / fork ("clone the prefix file ... without duplicating the actual tensors") /
+ *   remove, and pruning of "invalid or unimportant tokens" as in-place evict + compaction.
+ *
+ * Conventions (all functions)
+ *   - Return KVFS_OK (0) or a negative kvfs_err.  Never throw, never abort, never print.
+ *   - Atomic failure: a call that fails changes nothing.  pred_* is atomic per
+ *     descriptor: failing descriptors get their own status and leave their output rows untouched, the
+ *     others proceed, and the call returns KVFS_EPARTIAL.
+ *   - Ownership: the caller owns every device buffer (pools, workspace, Q/K/V/out/lse), typically torch
+ *     tensors, and keeps them alive until kvfs_destroy returns.  The ctx owns only host metadata, pinned
+ *     staging buffers and CUDA events; it copies `name` strings.
+ *   - Streams: host metadata changes take effect at call time.  Device work is enqueued on the given
+ *     stream (NULL = legacy default stream).  All device work of one ctx must be issued on one stream
+ *     (or the caller serialises streams): a page freed by evict/truncate may be reused by the next
+ *     call's device work, and stream order is what keeps earlier readers safe.
+ *   - Thread safety: calls on one ctx are serialised by an internal mutex.
+ *   - Host-only ctx (cfg.device == -1): metadata only, for testing the control plane without a GPU.
+ *     No CUDA call is ever made; calls that need data (pred_attn_batch, pred_attn_layer, kvfs_read)
+ *     return KVFS_ENOSYS; kvfs_append / fork / evict / compact update metadata only.
+ *   - A CUDA error poisons the ctx: that call and every later data call return KVFS_EIO.
+ *
+ * Data layout (device)
+ *   K and V pools, one pair per layer: [n_pages][n_kv_heads][page_size][head_dim] bf16 ("HND" pages):
+ *   the (page, kv head) block is page_size*head_dim*2 contiguous bytes, which is the unit the decode
+ *   kernel streams with 1-D TMA bulk copies.  One page id addresses the same page in every layer.
+ *   Q rows [T][n_q_heads][head_dim] bf16, K_new/V_new rows [T][n_kv_heads][head_dim] bf16, out
+ *   [T][n_q_heads][head_dim] bf16, lse [T][n_q_heads] fp32 (natural log), all row-major, rows packed in
+ *   descriptor order (S:355 FIFO).  GQA: query head h reads KV head h / (n_q_heads / n_kv_heads).
+ */
+#ifndef KVFS_H_
+#define KVFS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* cudaStream_t / CUstream without including CUDA headers. */
+typedef struct CUstream_st *kvfs_stream_t;
+
+typedef enum {
+  KVFS_OK = 0,
+  KVFS_ENOENT = -2,      /* name not found (open without O_CREAT, unlink) */
+  KVFS_EIO = -5,         /* CUDA error; the ctx is poisoned */
+  KVFS_EBADF = -9,       /* fd not open, or its file was unlinked */
+  KVFS_ENOMEM = -12,     /* host allocation / device table slab / workspace too small */
+  KVFS_EBUSY = -16,      /* pred batch: the descriptor's file already appeared earlier in the batch */
+  KVFS_EEXIST = -17,     /* name exists (open O_CREAT|O_EXCL, fork destination) */
+  KVFS_EINVAL = -22,     /* malformed arguments (NULL pointers, bad sizes, unsorted ranges, ...) */
+  KVFS_ENOSPC = -28,     /* page pool exhausted (SPEC PoolExhausted) */
+  KVFS_ERANGE = -34,     /* index / length out of range */
+  KVFS_ENOSYS = -38,     /* data operation on a host-only ctx */
+  KVFS_EPOS = -1001,     /* positions not strictly increasing / not > last retained (SPEC PositionConflict) */
+  KVFS_EPARTIAL = -1002  /* pred batch: some descriptors failed, see status[] */
+} kvfs_err;
+
+enum { KVFS_O_CREAT = 1, KVFS_O_EXCL = 2 };   /* kvfs_open flags (R2) */
+enum { KVFS_EVICT_COMPACT = 1 };              /* kvfs_evict flag (R8) */
+
+typedef struct kvfs_ctx kvfs_ctx;
+typedef struct pred_step pred_step;
+
+typedef struct {
+  int device;              /* CUDA device ordinal, or -1 for a host-only ctx */
+  int n_layers;            /* >= 1 */
+  int n_q_heads;           /* Hq, multiple of n_kv_heads */
+  int n_kv_heads;          /* Hkv */
+  int head_dim;            /* D: 64 or 128 */
+  int page_size;           /* P: 16, 32 or 64 tokens (the per-entry slot mask is a u64) */
+  int64_t n_pages;         /* pool size in pages, < 2^25 */
+  void *const *k_pool;     /* [n_layers] device pointers (NULL for a host-only ctx) */
+  void *const *v_pool;     /* [n_layers] device pointers */
+  int32_t max_batch_rows;  /* max total query rows (sum of n_q) of one pred call */
+  int32_t max_batch_descs; /* max descriptors of one pred call */
+  int64_t table_capacity;  /* device table slab capacity in entries; 0 = 2*n_pages + 65536 */
+  void *workspace;         /* device scratch, >= kvfs_workspace_bytes(cfg) bytes, 256-B aligned */
+  size_t workspace_bytes;
+} kvfs_config;
+
+/* Bytes of device workspace kvfs_init needs for cfg (slab, upload area, split partials, counters). */
+size_t kvfs_workspace_bytes(const kvfs_config *cfg);
+
+/* Create a ctx over caller-owned pools (all pages free).  Validates shapes; ENOMEM if the workspace is
+ * too small; EINVAL for unsupported shapes. */
+int kvfs_init(const kvfs_config *cfg, kvfs_ctx **out);
+
+/* Synchronises the ctx's last stream use, frees host resources.  Device buffers stay the caller's. */
+int kvfs_destroy(kvfs_ctx *ctx);
+
+/* Human-readable name of an error code (static storage). */
+const char *kvfs_strerror(int err);
+
+/* ---------------------------------------------------------------- files (R2, R9) */
+/* Open `name`, creating an empty file (no pages) with KVFS_O_CREAT; EEXIST with O_CREAT|O_EXCL if it
+ * exists; ENOENT without O_CREAT if missing.  *fd is the smallest non-negative integer not open. */
+int kvfs_open(kvfs_ctx *ctx, const char *name, int flags, int *fd);
+/* Release the fd only (pages stay with the file).  EBADF if not open. */
+int kvfs_close(kvfs_ctx *ctx, int fd);
+/* kv_remove: drop every page reference of the file (refcount--, freed at 0) and remove
+ * the name.  fds still open on it become EBADF for everything but kvfs_close. */
+int kvfs_unlink(kvfs_ctx *ctx, const char *name);
+
+/* kv_fork (R4): new file `dst_name` sharing every page of src (refcount++).  If src's tail
+ * page has room, the child's tail is a fresh page (smallest free id, R1) holding a copy of the retained
+ * slots (device copy of the whole page for every layer, K and V, enqueued on `stream`).  ENOSPC if that
+ * page cannot be allocated, EEXIST if dst_name exists. */
+int kvfs_fork(kvfs_ctx *ctx, int src_fd, const char *dst_name, int *dst_fd, kvfs_stream_t stream);
+
+/* Keep logical tokens [0, new_len) (R5): later entries are dropped (refcount--), the last mask is trimmed,
+ * positions are truncated.  ERANGE unless 0 <= new_len <= len.  Host only. */
+int kvfs_truncate(kvfs_ctx *ctx, int fd, int64_t new_len);
+
+/* Evict logical ranges (R6): ranges = [n_ranges][2] half-open [a, b), a < b, sorted, disjoint
+ * (else EINVAL), within [0, len) (else ERANGE).  Clears mask bits, drops emptied entries; retained
+ * positions are unchanged; no data moves.  With KVFS_EVICT_COMPACT the file is then
+ * compacted (R7) in the same atomic call (R8), the page need being checked after the eviction. */
+int kvfs_evict(kvfs_ctx *ctx, int fd, const int64_t *ranges, int n_ranges, int flags,
+               kvfs_stream_t stream);
+
+/* Compaction (R7): gather the retained tokens in logical order into ceil(len/P) fresh pages allocated
+ * (smallest free first) while the old pages are still held, then release the old entries.  The device
+ * gather (all layers, K and V) is enqueued on `stream`.  ENOSPC if the pages are not free.  No-op when
+ * the file is empty. */
+int kvfs_compact(kvfs_ctx *ctx, int fd, kvfs_stream_t stream);
+
+/* Append n tokens (R3) without attention (e.g. a prefilled prompt, "fills the file with the KV
+ * cache").  pos: host [n] int32, strictly increasing and > the last retained position (else EPOS).
+ * k, v: device [n_layers][n][n_kv_heads][head_dim] bf16 (may be NULL on a host-only ctx).
+ * A shared tail page with room is copied first (copy-on-write). */
+int kvfs_append(kvfs_ctx *ctx, int fd, int64_t n, const int32_t *pos, const void *k, const void *v,
+                kvfs_stream_t stream);
+
+/* ---------------------------------------------------------------- batched pred */
+typedef struct {
+  int32_t fd;   /* the LIP's KV file */
+  int32_t n_q;  /* number of new tokens (query rows) of this LIP in the batch; 0 = no-op */
+} pred_desc;
+
+/* One layer (n_layers == 1) batched pred.  Descriptors are processed in order (R11): EBADF, EBUSY (the
+ * file appeared in an earlier descriptor), EPOS, ENOSPC per descriptor; the others reserve their slots
+ * (copy-on-write of a shared tail, smallest-free pages), append K_new/V_new and compute
+ *   out[r][h] = sum_k softmax_k(scale * <q[r][h], K[k][g]>) V[k][g],   lse[r][h] = log sum_k exp(...)
+ * over the file's retained tokens k with logical index <= len - n_q + i (row r = i-th row of the
+ * descriptor, bottom-right-aligned causal; g = h / (Hq/Hkv)).
+ *   pos    host [T] int32, T = sum of n_q (EINVAL if any n_q < 0 or T > max_batch_rows)
+ *   q      device [T][Hq][D] bf16;  k_new, v_new device [T][Hkv][D] bf16
+ *   out    device [T][Hq][D] bf16;  lse device [T][Hq] fp32 or NULL
+ *   scale  > 0 (usually 1/sqrt(D))
+ *   status host [n_desc] int, per-descriptor result (may be NULL)
+ * Returns KVFS_OK, KVFS_EPARTIAL, or a call-level error (nothing changed). */
+int pred_attn_batch(kvfs_ctx *ctx, const pred_desc *descs, int n_desc, const int32_t *pos,
+                    const void *q, const void *k_new, const void *v_new, void *out, float *lse,
+                    float scale, int *status, kvfs_stream_t stream);
+
+/* Multi-layer form: pred_step_begin validates + reserves once (host metadata committed, device tables
+ * and copy-on-write copies enqueued), then the caller issues pred_attn_layer for EVERY layer (append of
+ * that layer's K_new/V_new fused with its attention), then pred_step_end.  Only one step may be open per
+ * ctx; other calls on the ctx return EBUSY while it is open.  Same arguments as pred_attn_batch. */
+int pred_step_begin(kvfs_ctx *ctx, const pred_desc *descs, int n_desc, const int32_t *pos, int *status,
+                    pred_step **step, kvfs_stream_t stream);
+int pred_attn_layer(kvfs_ctx *ctx, pred_step *step, int layer, const void *q, const void *k_new,
+                    const void *v_new, void *out, float *lse, float scale, kvfs_stream_t stream);
+int pred_step_end(kvfs_ctx *ctx, pred_step *step);
+
+/* ---------------------------------------------------------------- introspection (tests, policies) */
+typedef struct {
+  int64_t len;        /* retained tokens */
+  int64_t n_entries;  /* page entries */
+  int32_t last_pos;   /* last retained position, -1 if empty */
+  int32_t reserved;
+} kvfs_stat_t;
+
+int kvfs_stat(kvfs_ctx *ctx, int fd, kvfs_stat_t *st);
+/* The file's page table: page ids and slot masks (bit s = slot s retained).  *n = n_entries; at most
+ * cap are written. */
+int kvfs_get_table(kvfs_ctx *ctx, int fd, uint32_t *page, uint64_t *mask, int64_t cap, int64_t *n);
+int kvfs_get_positions(kvfs_ctx *ctx, int fd, int32_t *pos, int64_t cap, int64_t *n);
+/* refcnt[p] for p < min(n, n_pages). */
+int kvfs_get_refcounts(kvfs_ctx *ctx, uint32_t *refcnt, int64_t n);
+int kvfs_free_pages(kvfs_ctx *ctx, int64_t *n_free);
+/* Gather logical tokens [begin, end) of one layer into dense device k_out/v_out [end-begin][Hkv][D]. */
+int kvfs_read(kvfs_ctx *ctx, int fd, int layer, int64_t begin, int64_t end, void *k_out, void *v_out,
+              kvfs_stream_t stream);
+/* Recompute refcounts from the tables and check invariants I1-I5 (§8(c) C2).  EIO-free: returns
+ * KVFS_EINVAL (and leaves state as is) if an invariant is violated. */
+int kvfs_audit(kvfs_ctx *ctx);
+
+/* ---------------------------------------------------------------- knobs and counters */
+typedef enum {
+  KVFS_OPT_DECODE_CTAS = 1,     /* grid size of the decode kernel; 0 = auto (SM count x occupancy) */
+  KVFS_OPT_CHUNK_CUTOVER = 2,   /* n_q at or above which the tcgen05 chunk kernel is used; 0 = never */
+  KVFS_OPT_DETERMINISTIC = 3    /* reserved (the kernels are deterministic for a fixed grid) */
+} kvfs_option;
+int kvfs_set_option(kvfs_ctx *ctx, int option, int64_t value);
+
+typedef enum {
+  KVFS_CTR_KERNEL_LAUNCHES = 1, /* CUDA kernels this ctx has launched */
+  KVFS_CTR_H2D_BYTES = 2,       /* bytes of host->device metadata uploads */
+  KVFS_CTR_PAGE_COPIES = 3,     /* whole-page copies (copy-on-write + fork tails), per page */
+  KVFS_CTR_LAST_DECODE_CTAS = 4 /* grid of the last decode launch */
+} kvfs_counter;
+int kvfs_get_counter(kvfs_ctx *ctx, int counter, int64_t *value);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVFS_H_ */

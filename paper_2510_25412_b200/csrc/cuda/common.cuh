@@ -1,0 +1,142 @@
+// Shared device-side definitions: table entry / descriptor layouts (byte-identical to the host structs in
+// csrc/host/kvfs_impl.h) and the sm_100a PTX helpers (mbarrier, 1-D TMA bulk copy, packed fp32x2 FMA).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace kvfs {
+namespace dev {
+
+struct Entry {  // == kvfs::Entry
+  uint32_t page;
+  int32_t lstart;
+  uint64_t mask;
+};
+
+struct Desc {  // == kvfs::DevDesc
+  int64_t cost_begin;
+  int32_t slab_off;
+  int32_t n_old_entries;
+  int32_t n_old;
+  int32_t n_q;
+  int32_t row0;
+  int32_t unit_base;
+  int32_t stages_per_unit;
+  int32_t pad0;
+  int64_t pad1;
+};
+
+struct SlabRun {
+  int64_t dst;
+  int32_t src;
+  int32_t count;
+};
+
+struct PageCopy {
+  uint32_t src, dst;
+};
+
+// ------------------------------------------------------------------------------------------ PTX
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// 1-D TMA: global -> shared, completion counted on an mbarrier (bytes multiple of 16, 16-B aligned).
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// d += a * b on packed fp32 pairs (sm_100a FFMA2).
+__device__ __forceinline__ void fma2(float2 &d, const float2 a, const float2 b) {
+  unsigned long long dd = *reinterpret_cast<unsigned long long *>(&d);
+  const unsigned long long aa = *reinterpret_cast<const unsigned long long *>(&a);
+  const unsigned long long bb = *reinterpret_cast<const unsigned long long *>(&b);
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(dd) : "l"(aa), "l"(bb));
+  d = *reinterpret_cast<float2 *>(&dd);
+}
+
+__device__ __forceinline__ float2 mul2(const float2 a, const float2 b) {
+  unsigned long long dd;
+  const unsigned long long aa = *reinterpret_cast<const unsigned long long *>(&a);
+  const unsigned long long bb = *reinterpret_cast<const unsigned long long *>(&b);
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(dd) : "l"(aa), "l"(bb));
+  return *reinterpret_cast<float2 *>(&dd);
+}
+
+// bf16 pair (little-endian u32: element 0 in the low half) -> fp32 pair, exact.
+__device__ __forceinline__ float2 bf2_to_f2(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
+
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Position of the r-th (0-based) set bit of m (precondition: popc(m) > r).
+__device__ __forceinline__ int select_bit64(uint64_t m, int r) {
+  const uint32_t lo = static_cast<uint32_t>(m);
+  const int nlo = __popc(lo);
+  if (r < nlo) return __fns(lo, 0, r + 1);
+  return 32 + __fns(static_cast<uint32_t>(m >> 32), 0, r - nlo + 1);
+}
+
+// Keep the lowest k set bits of m.
+__device__ __forceinline__ uint64_t lowest_bits(uint64_t m, int k) {
+  if (k <= 0) return 0;
+  if (k >= __popcll(m)) return m;
+  const int s = select_bit64(m, k);  // position of the (k+1)-th set bit
+  return m & ((1ull << s) - 1);
+}
+
+}  // namespace dev
+}  // namespace kvfs

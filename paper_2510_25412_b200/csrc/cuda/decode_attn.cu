@@ -1,0 +1,529 @@
+// K1: fused append + split-KV page-gathering GQA attention for the batched `pred` (§4.1
+// P:210-215 semantics, rule R10 of SURVEY.md §8(c); HBM-bound, AI ~ 4 flop/B).
+//
+// Work decomposition ("stage" = one (page entry, kv head) block of K and V, or one block of up to P new
+// rows of K_new/V_new):
+//   unit  = (descriptor d, kv head g, query row qi): the G query heads of one new token against the
+//           file's retained tokens;  units of d are ordered g-major so that consecutive units (same g,
+//           consecutive qi) stream the same pages;
+//   stages of a unit = its file's n_old_entries page entries, then ceil(n_q / P) "new-row" stages;
+//   the batch's stages are concatenated in descriptor order and the grid splits that sequence into
+//   equal contiguous ranges, one per CTA (split-KV at page granularity, exact load balance).
+//   A unit cut by a range boundary is finished by whichever CTA completes its last piece: partial
+//   (O, m, l) go to the workspace and that CTA merges them in range order (deterministic).
+// Per CTA: one producer lane streams stages into a ring of NSTAGES shared-memory slots with 1-D TMA
+// bulk copies (cp.async.bulk, completion on mbarriers, evict-first L2 policy); NW consumer warps take
+// ring slots round-robin.  In a consumer warp, LPK lanes share one key (16 B bf16 vectors, DPL dims per
+// lane), so a warp scores KG = 32/LPK keys per step with packed fp32x2 FMAs and an xor-shuffle
+// reduction; softmax is online in the log2 domain with lazy rescaling (only when the running max grows
+// by > 8); the new-row stage of unit qi = 0 also writes K_new/V_new into the file's reserved slots
+// (the fused append).  Warps combine through shared memory at unit boundaries.
+#include <cuda_bf16.h>
+#include <math_constants.h>
+
+#include "kernels.cuh"
+
+namespace kvfs {
+namespace dev {
+
+template <int D_, int G_, int P_>
+struct DecodeCfg {
+  static constexpr int D = D_, G = G_, P = P_;
+  static constexpr int DPL = (G <= 4) ? 16 : 8;  // dims per lane
+  static constexpr int LPK = D / DPL;            // lanes per key
+  static constexpr int KG = 32 / LPK;            // keys per warp step
+  static constexpr int CH = DPL / 8;             // 16-byte chunks per lane per row
+  static constexpr int SUB = 16;                 // slots per softmax sub-block
+  static constexpr int NIT = SUB / KG;           // warp steps per sub-block
+  static constexpr int NW = 7;                   // consumer warps (8 warps total: up to 255 registers)
+  static constexpr int THREADS = (NW + 1) * 32;
+  static constexpr int BLOCK_BYTES = P * D * 2;  // one (page, head) block of K or V
+  static constexpr int STAGE_BYTES = 2 * BLOCK_BYTES;
+  static constexpr int NSTAGES_RAW = 131072 / STAGE_BYTES;
+  static constexpr int NSTAGES = NSTAGES_RAW < 4 ? 4 : (NSTAGES_RAW > 16 ? 16 : NSTAGES_RAW);
+  static constexpr int NQ = 4;                   // Q ring slots
+  static constexpr int PART = G * (D + 2);       // floats per partial (o, m, l per head)
+  static_assert(LPK * KG == 32 && SUB % KG == 0 && P % SUB == 0, "layout");
+};
+
+struct StageMeta {
+  uint64_t mask;  // slots (or new rows) that are visible keys
+  int32_t kind;   // 0 = page entry, 1 = new rows
+  int32_t nrows;  // new-row stage: rows loaded
+};
+
+
+
+__device__ __forceinline__ int64_t cta_start(int64_t c, int64_t total, int ncta) { return c * total / ncta; }
+
+__device__ __forceinline__ int cta_of(int64_t x, int64_t total, int ncta) {
+  int64_t c = x * ncta / total;
+  if (c >= ncta) c = ncta - 1;
+  while (c + 1 < ncta && cta_start(c + 1, total, ncta) <= x) ++c;
+  while (c > 0 && cta_start(c, total, ncta) > x) --c;
+  return static_cast<int>(c);
+}
+
+// Largest d with descs[d].cost_begin <= x.
+__device__ __forceinline__ int find_desc(const Desc *descs, int n, int64_t x) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (descs[mid].cost_begin <= x) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+struct Segment {
+  int d;         // descriptor
+  int g, qi;     // kv head, query row within the descriptor
+  int st0, nst;  // first stage within the unit, number of stages
+  int spu;       // stages per unit
+  int64_t ubeg;  // global stage index of the unit's first stage
+};
+
+// Segment containing global stage x (x < total), clipped to [x, end).
+__device__ __forceinline__ Segment make_segment(const Desc *descs, int n_desc, int64_t x, int64_t end, int Hkv) {
+  Segment s;
+  s.d = find_desc(descs, n_desc, x);
+  const Desc &dd = descs[s.d];
+  s.spu = dd.stages_per_unit;
+  const int64_t rel = x - dd.cost_begin;
+  const int u = static_cast<int>(rel / s.spu);
+  s.st0 = static_cast<int>(rel - static_cast<int64_t>(u) * s.spu);
+  s.g = u / dd.n_q;
+  s.qi = u - s.g * dd.n_q;
+  s.ubeg = dd.cost_begin + static_cast<int64_t>(u) * s.spu;
+  const int64_t uend = s.ubeg + s.spu;
+  s.nst = static_cast<int>((end < uend ? end : uend) - x);
+  (void)Hkv;
+  return s;
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const DecodeParams p) {
+  constexpr int D = C::D, G = C::G, P = C::P, NW = C::NW, NSTAGES = C::NSTAGES;
+  constexpr int LPK = C::LPK, KG = C::KG, CH = C::CH, DPL = C::DPL, NIT = C::NIT, SUB = C::SUB;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t *stage_data = smem;                                                    // [NSTAGES][2][P][D] bf16
+  __nv_bfloat16 *qring = reinterpret_cast<__nv_bfloat16 *>(smem + NSTAGES * C::STAGE_BYTES);  // [NQ][G][D]
+  float *comb = reinterpret_cast<float *>(qring + C::NQ * G * D);                // [NW][PART]
+  StageMeta *meta = reinterpret_cast<StageMeta *>(comb + NW * C::PART);          // [NSTAGES]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(meta + NSTAGES);                 // full, empty, qfull, qempty
+  int *flag = reinterpret_cast<int *>(bars + 2 * NSTAGES + 2 * C::NQ);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cta = blockIdx.x;
+  const int64_t beg = cta_start(cta, p.total, p.ncta), end = cta_start(cta + 1, p.total, p.ncta);
+  auto full_bar = [&](int s) { return smem_u32(bars + s); };
+  auto empty_bar = [&](int s) { return smem_u32(bars + NSTAGES + s); };
+  auto qfull_bar = [&](int s) { return smem_u32(bars + 2 * NSTAGES + s); };
+  auto qempty_bar = [&](int s) { return smem_u32(bars + 2 * NSTAGES + C::NQ + s); };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int s = 0; s < C::NQ; ++s) {
+      mbar_init(qfull_bar(s), 1);
+      mbar_init(qempty_bar(s), NW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (beg >= end) return;
+
+  if (warp == NW) {
+    // ================================================================ producer (one lane)
+    if (lane != 0) return;
+    const uint64_t pol = policy_evict_first();
+    int64_t x = beg;
+    int local = 0, segi = 0;
+    while (x < end) {
+      const Segment sg = make_segment(p.descs, p.n_desc, x, end, p.Hkv);
+      const Desc dd = p.descs[sg.d];
+      // Q rows of this unit -> Q ring
+      {
+        const int qs = segi % C::NQ;
+        if (segi >= C::NQ) mbar_wait(qempty_bar(qs), ((segi / C::NQ) & 1) ^ 1);
+        const __nv_bfloat16 *src = p.q + (static_cast<int64_t>(dd.row0 + sg.qi) * p.Hq + sg.g * G) * D;
+        mbar_arrive_expect_tx(qfull_bar(qs), G * D * 2);
+        bulk_g2s(smem_u32(qring + qs * G * D), src, G * D * 2, qfull_bar(qs), pol);
+      }
+      for (int i = 0; i < sg.nst; ++i, ++local) {
+        const int slot = local % NSTAGES;
+        if (local >= NSTAGES) mbar_wait(empty_bar(slot), ((local / NSTAGES) & 1) ^ 1);
+        const int st = sg.st0 + i;
+        const uint32_t kdst = smem_u32(stage_data + slot * C::STAGE_BYTES);
+        const uint32_t vdst = kdst + C::BLOCK_BYTES;
+        StageMeta m;
+        uint32_t bytes = 0;
+        if (st < dd.n_old_entries) {
+          const Entry e = p.slab[dd.slab_off + st];
+          uint64_t mask = e.mask;
+          if (e.lstart + __popcll(mask) > dd.n_old) mask = lowest_bits(mask, dd.n_old - e.lstart);
+          const int lo = __ffsll(static_cast<long long>(mask)) - 1;
+          const int hi = 63 - __clzll(static_cast<long long>(mask));
+          const uint32_t nb = static_cast<uint32_t>(hi - lo + 1) * D * 2;
+          const int64_t off = ((static_cast<int64_t>(e.page) * p.Hkv + sg.g) * P + lo) * D;
+          m.mask = mask;
+          m.kind = 0;
+          m.nrows = 0;
+          meta[slot] = m;
+          bytes = 2 * nb;
+          mbar_arrive_expect_tx(full_bar(slot), bytes);
+          bulk_g2s(kdst + lo * D * 2, p.kpool + off, nb, full_bar(slot), pol);
+          bulk_g2s(vdst + lo * D * 2, p.vpool + off, nb, full_bar(slot), pol);
+        } else {
+          const int v0 = (st - dd.n_old_entries) * P;
+          const int r_end = min(dd.n_q, v0 + P);
+          const int vis_end = min(r_end, sg.qi + 1);  // causal: row qi sees new rows <= qi
+          const int n_vis = vis_end > v0 ? vis_end - v0 : 0;
+          const int n_load = (sg.qi == 0) ? (r_end - v0) : n_vis;  // unit qi=0 also writes the append
+          m.mask = n_vis >= 64 ? ~0ull : ((1ull << n_vis) - 1);
+          m.kind = 1;
+          m.nrows = n_load;
+          meta[slot] = m;
+          bytes = 2u * n_load * D * 2;
+          if (bytes) {
+            mbar_arrive_expect_tx(full_bar(slot), bytes);
+            for (int r = 0; r < n_load; ++r) {
+              const int64_t off = (static_cast<int64_t>(dd.row0 + v0 + r) * p.Hkv + sg.g) * D;
+              bulk_g2s(kdst + r * D * 2, p.k_new + off, D * 2, full_bar(slot), pol);
+              bulk_g2s(vdst + r * D * 2, p.v_new + off, D * 2, full_bar(slot), pol);
+            }
+          } else {
+            mbar_arrive(full_bar(slot));
+          }
+        }
+      }
+      x += sg.nst;
+      ++segi;
+    }
+    return;
+  }
+
+  // ================================================================ consumers
+  const int kg = lane / LPK, sub = lane % LPK;
+  int64_t x = beg;
+  int local0 = 0, segi = 0;
+  bool first_seg = true;
+  while (x < end) {
+    const Segment sg = make_segment(p.descs, p.n_desc, x, end, p.Hkv);
+    const Desc dd = p.descs[sg.d];
+    // ---- Q (scaled into the log2 domain) from the Q ring
+    float2 q2[G][DPL / 2];
+    {
+      const int qs = segi % C::NQ;
+      mbar_wait(qfull_bar(qs), (segi / C::NQ) & 1);
+#pragma unroll
+      for (int h = 0; h < G; ++h)
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const uint4 w = *reinterpret_cast<const uint4 *>(qring + (qs * G + h) * D + (c * LPK + sub) * 8);
+          const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float2 f = bf2_to_f2(ws[j]);
+            q2[h][c * 4 + j] = make_float2(f.x * p.scale_log2, f.y * p.scale_log2);
+          }
+        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qempty_bar(qs));
+    }
+    float2 o2[G][DPL / 2];
+    float m_run[G], l_run[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+      m_run[h] = -CUDART_INF_F;
+      l_run[h] = 0.f;
+#pragma unroll
+      for (int j = 0; j < DPL / 2; ++j) o2[h][j] = make_float2(0.f, 0.f);
+    }
+
+    for (int i = warp; i < sg.nst; i += NW) {
+      const int local = local0 + i;
+      const int slot = local % NSTAGES;
+      mbar_wait(full_bar(slot), (local / NSTAGES) & 1);
+      const StageMeta m = meta[slot];
+      const __nv_bfloat16 *ks = reinterpret_cast<const __nv_bfloat16 *>(stage_data + slot * C::STAGE_BYTES);
+      const __nv_bfloat16 *vs = ks + P * D;
+#pragma unroll 1
+      for (int sb = 0; sb < P / SUB; ++sb) {
+        const uint32_t sbm = static_cast<uint32_t>(m.mask >> (sb * SUB)) & ((1u << SUB) - 1);
+        if (sbm == 0) continue;  // warp-uniform
+        float s[NIT][G];
+        float smax[G];
+#pragma unroll
+        for (int h = 0; h < G; ++h) smax[h] = -CUDART_INF_F;
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+          const int slot_k = sb * SUB + it * KG + kg;
+          const bool valid = (sbm >> (it * KG + kg)) & 1u;
+          float2 acc[G];
+#pragma unroll
+          for (int h = 0; h < G; ++h) acc[h] = make_float2(0.f, 0.f);
+#pragma unroll
+          for (int c = 0; c < CH; ++c) {
+            const uint4 w = *reinterpret_cast<const uint4 *>(ks + slot_k * D + (c * LPK + sub) * 8);
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 kf = bf2_to_f2(ws[j]);
+#pragma unroll
+              for (int h = 0; h < G; ++h) fma2(acc[h], q2[h][c * 4 + j], kf);
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < G; ++h) {
+            float v = acc[h].x + acc[h].y;
+#pragma unroll
+            for (int o = LPK / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            s[it][h] = valid ? v : -CUDART_INF_F;
+            smax[h] = fmaxf(smax[h], s[it][h]);
+          }
+        }
+        // sub-block max over the warp's key groups
+#pragma unroll
+        for (int h = 0; h < G; ++h)
+#pragma unroll
+          for (int o = LPK; o < 32; o <<= 1) smax[h] = fmaxf(smax[h], __shfl_xor_sync(0xffffffffu, smax[h], o));
+        // lazy rescale: only when the running max would be exceeded by more than 2^8
+        bool need = false;
+#pragma unroll
+        for (int h = 0; h < G; ++h) need |= smax[h] > m_run[h] + 8.f;
+        if (need) {
+#pragma unroll
+          for (int h = 0; h < G; ++h) {
+            const float mn = fmaxf(m_run[h], smax[h]);
+            const float a = (m_run[h] == -CUDART_INF_F) ? 0.f : fast_exp2(m_run[h] - mn);
+            m_run[h] = mn;
+            l_run[h] *= a;
+            const float2 a2 = make_float2(a, a);
+#pragma unroll
+            for (int j = 0; j < DPL / 2; ++j) o2[h][j] = mul2(o2[h][j], a2);
+          }
+        }
+        // P.V
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+          const int slot_k = sb * SUB + it * KG + kg;
+          const bool valid = (sbm >> (it * KG + kg)) & 1u;
+          float pw[G];
+#pragma unroll
+          for (int h = 0; h < G; ++h) {
+            pw[h] = valid ? fast_exp2(s[it][h] - m_run[h]) : 0.f;
+            l_run[h] += pw[h];
+          }
+          if (valid) {
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+              const uint4 w = *reinterpret_cast<const uint4 *>(vs + slot_k * D + (c * LPK + sub) * 8);
+              const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float2 vf = bf2_to_f2(ws[j]);
+#pragma unroll
+                for (int h = 0; h < G; ++h) fma2(o2[h][c * 4 + j], make_float2(pw[h], pw[h]), vf);
+              }
+            }
+          }
+        }
+      }
+      // fused append: the new-row stage of unit qi = 0 writes K_new / V_new into the reserved slots
+      if (m.kind == 1 && sg.qi == 0) {
+        const int st = sg.st0 + i;
+        const int v0 = (st - dd.n_old_entries) * P;
+        constexpr int CPR = D / 8;  // 16-byte chunks per row
+        for (int idx = lane; idx < m.nrows * CPR; idx += 32) {
+          const int r = idx / CPR, cc = idx % CPR;
+          const int32_t ds = p.dst_slot[dd.row0 + v0 + r];
+          const int page = ds / P, sl = ds % P;
+          const int64_t off = ((static_cast<int64_t>(page) * p.Hkv + sg.g) * P + sl) * D + cc * 8;
+          *reinterpret_cast<uint4 *>(p.kpool + off) = *reinterpret_cast<const uint4 *>(ks + r * D + cc * 8);
+          *reinterpret_cast<uint4 *>(p.vpool + off) = *reinterpret_cast<const uint4 *>(vs + r * D + cc * 8);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty_bar(slot));
+    }
+
+    // ---- combine the warps' (m, l, O) of this segment
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+#pragma unroll
+      for (int o = LPK; o < 32; o <<= 1) {
+        l_run[h] += __shfl_xor_sync(0xffffffffu, l_run[h], o);
+#pragma unroll
+        for (int j = 0; j < DPL / 2; ++j) {
+          o2[h][j].x += __shfl_xor_sync(0xffffffffu, o2[h][j].x, o);
+          o2[h][j].y += __shfl_xor_sync(0xffffffffu, o2[h][j].y, o);
+        }
+      }
+    }
+    float *cw = comb + warp * C::PART;
+    if (kg == 0) {
+#pragma unroll
+      for (int h = 0; h < G; ++h)
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int dim = (c * LPK + sub) * 8 + 2 * j;
+            *reinterpret_cast<float2 *>(cw + h * (D + 2) + dim) = o2[h][c * 4 + j];
+          }
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        cw[h * (D + 2) + D] = m_run[h];
+        cw[h * (D + 2) + D + 1] = l_run[h];
+      }
+    }
+    named_bar_sync(1, NW * 32);
+
+    const bool whole = (sg.st0 == 0) && (sg.nst == sg.spu);
+    const int tid = threadIdx.x;  // 0 .. NW*32-1
+    const int unit = dd.unit_base + sg.g * dd.n_q + sg.qi;
+    const int64_t row = dd.row0 + sg.qi;
+    if (whole) {
+      for (int e = tid; e < G * D / 2; e += NW * 32) {
+        const int h = e / (D / 2), dim = (e % (D / 2)) * 2;
+        float M = -CUDART_INF_F;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) M = fmaxf(M, comb[w * C::PART + h * (D + 2) + D]);
+        float L = 0.f, ox = 0.f, oy = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+          const float *cwp = comb + w * C::PART + h * (D + 2);
+          const float f = (cwp[D] == -CUDART_INF_F) ? 0.f : fast_exp2(cwp[D] - M);
+          L += cwp[D + 1] * f;
+          ox += cwp[dim] * f;
+          oy += cwp[dim + 1] * f;
+        }
+        const float inv = 1.f / L;
+        const int64_t oidx = (row * p.Hq + sg.g * G + h) * D + dim;
+        *reinterpret_cast<__nv_bfloat162 *>(p.out + oidx) = __floats2bfloat162_rn(ox * inv, oy * inv);
+        if (dim == 0 && p.lse) p.lse[row * p.Hq + sg.g * G + h] = (M + __log2f(L)) * 0.69314718055994531f;
+      }
+      named_bar_sync(1, NW * 32);
+    } else {
+      // partial of this CTA's piece of the unit
+      const int which = first_seg ? 0 : 1;
+      float *part = p.partials + (static_cast<int64_t>(cta) * 2 + which) * C::PART;
+      for (int e = tid; e < G * (D + 2); e += NW * 32) {
+        const int h = e / (D + 2), dim = e % (D + 2);
+        float M = -CUDART_INF_F;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) M = fmaxf(M, comb[w * C::PART + h * (D + 2) + D]);
+        float acc = 0.f;
+        if (dim == D) {
+          acc = M;
+        } else {
+#pragma unroll
+          for (int w = 0; w < NW; ++w) {
+            const float *cwp = comb + w * C::PART + h * (D + 2);
+            const float f = (cwp[D] == -CUDART_INF_F) ? 0.f : fast_exp2(cwp[D] - M);
+            acc += (dim == D + 1 ? cwp[D + 1] : cwp[dim]) * f;
+          }
+        }
+        part[e] = acc;
+      }
+      __threadfence();
+      named_bar_sync(1, NW * 32);
+      if (tid == 0) {
+        const int64_t ua = sg.ubeg, ub = sg.ubeg + sg.spu;
+        const int c0 = cta_of(ua, p.total, p.ncta), c1 = cta_of(ub - 1, p.total, p.ncta);
+        const int prev = atomicAdd(p.counters + unit, 1);
+        *flag = (prev == c1 - c0) ? 1 : 0;
+        if (prev == c1 - c0) p.counters[unit] = 0;  // self-cleaning for the next launch
+      }
+      named_bar_sync(1, NW * 32);
+      if (*flag) {
+        __threadfence();
+        const int64_t ua = sg.ubeg, ub = sg.ubeg + sg.spu;
+        const int c0 = cta_of(ua, p.total, p.ncta), c1 = cta_of(ub - 1, p.total, p.ncta);
+        for (int e = tid; e < G * D / 2; e += NW * 32) {
+          const int h = e / (D / 2), dim = (e % (D / 2)) * 2;
+          float M = -CUDART_INF_F;
+          for (int c = c0; c <= c1; ++c) {
+            const int wh = (cta_start(c, p.total, p.ncta) >= ua) ? 0 : 1;
+            const float *pc = p.partials + (static_cast<int64_t>(c) * 2 + wh) * C::PART + h * (D + 2);
+            M = fmaxf(M, __ldcg(pc + D));
+          }
+          float L = 0.f, ox = 0.f, oy = 0.f;
+          for (int c = c0; c <= c1; ++c) {
+            const int wh = (cta_start(c, p.total, p.ncta) >= ua) ? 0 : 1;
+            const float *pc = p.partials + (static_cast<int64_t>(c) * 2 + wh) * C::PART + h * (D + 2);
+            const float mc = __ldcg(pc + D);
+            const float f = (mc == -CUDART_INF_F) ? 0.f : fast_exp2(mc - M);
+            L += __ldcg(pc + D + 1) * f;
+            ox += __ldcg(pc + dim) * f;
+            oy += __ldcg(pc + dim + 1) * f;
+          }
+          const float inv = 1.f / L;
+          const int64_t oidx = (row * p.Hq + sg.g * G + h) * D + dim;
+          *reinterpret_cast<__nv_bfloat162 *>(p.out + oidx) = __floats2bfloat162_rn(ox * inv, oy * inv);
+          if (dim == 0 && p.lse) p.lse[row * p.Hq + sg.g * G + h] = (M + __log2f(L)) * 0.69314718055994531f;
+        }
+      }
+      named_bar_sync(1, NW * 32);
+    }
+    x += sg.nst;
+    local0 += sg.nst;
+    ++segi;
+    first_seg = false;
+  }
+}
+
+template <class C>
+static size_t decode_smem_bytes() {
+  return static_cast<size_t>(C::NSTAGES) * C::STAGE_BYTES + C::NQ * C::G * C::D * 2 + C::NW * C::PART * 4 +
+         C::NSTAGES * sizeof(StageMeta) + (2 * C::NSTAGES + 2 * C::NQ) * 8 + 16;
+}
+
+template <int D, int G, int P>
+static cudaError_t launch_decode_t(const DecodeParams &p, cudaStream_t s) {
+  using C = DecodeCfg<D, G, P>;
+  const size_t smem = decode_smem_bytes<C>();
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  decode_attn_kernel<C><<<p.ncta, C::THREADS, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <int D, int G>
+static cudaError_t launch_decode_p(const DecodeParams &p, int P, cudaStream_t s) {
+  switch (P) {
+    case 16: return launch_decode_t<D, G, 16>(p, s);
+    case 32: return launch_decode_t<D, G, 32>(p, s);
+    case 64: return launch_decode_t<D, G, 64>(p, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int D>
+static cudaError_t launch_decode_g(const DecodeParams &p, int G, int P, cudaStream_t s) {
+  switch (G) {
+    case 1: return launch_decode_p<D, 1>(p, P, s);
+    case 2: return launch_decode_p<D, 2>(p, P, s);
+    case 4: return launch_decode_p<D, 4>(p, P, s);
+    case 8: return launch_decode_p<D, 8>(p, P, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_decode(const DecodeParams &p, int D, int G, int P, cudaStream_t s) {
+  if (D == 64) return launch_decode_g<64>(p, G, P, s);
+  if (D == 128) return launch_decode_g<128>(p, G, P, s);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace dev
+}  // namespace kvfs

@@ -1,0 +1,416 @@
+// Device data plane of KVFS: workspace layout, the per-call metadata upload (one pinned H2D copy per
+// call), and the bandwidth-bound copy kernels (K4 copy-on-write / fork tail page copy, K5 evict-compact
+// gather, K7 dense read-back, the kvfs_append scatter, the table-delta scatter).  The attention kernel
+// lives in decode_attn.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "../host/kvfs_impl.h"
+#include "kernels.cuh"
+
+namespace kvfs {
+
+namespace {
+
+constexpr int kMaxCtas = 2048;
+
+size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
+struct WsLayout {
+  size_t slab = 0, upload = 0, counters = 0, partials = 0, ptrs = 0, total = 0, upload_cap = 0;
+};
+
+WsLayout ws_layout(const kvfs_config &c) {
+  WsLayout w;
+  const int G = c.n_q_heads / c.n_kv_heads;
+  const size_t part = static_cast<size_t>(G) * (c.head_dim + 2) * 4;
+  size_t off = 0;
+  w.slab = off;
+  off = align256(off + static_cast<size_t>(c.table_capacity) * 16);
+  w.upload = off;
+  w.upload_cap = align256(static_cast<size_t>(c.table_capacity) * 16 + static_cast<size_t>(c.n_pages) * 24 +
+                          static_cast<size_t>(c.max_batch_descs) * 96 + static_cast<size_t>(c.max_batch_rows) * 8 +
+                          (1u << 20));
+  off = align256(off + w.upload_cap);
+  w.counters = off;
+  off = align256(off + static_cast<size_t>(c.max_batch_rows) * c.n_kv_heads * 4);
+  w.partials = off;
+  off = align256(off + static_cast<size_t>(kMaxCtas) * 2 * part);
+  w.ptrs = off;
+  off = align256(off + static_cast<size_t>(c.n_layers) * 2 * sizeof(void *));
+  w.total = off;
+  return w;
+}
+
+// ------------------------------------------------------------------------------------------ kernels
+using bf16 = __nv_bfloat16;
+
+// Table deltas into the slab (one warp per run) and whole-page copies (one CTA per page, layer, K|V).
+__global__ void prologue_kernel(const dev::SlabRun *runs, int n_runs, const dev::Entry *run_entries,
+                                dev::Entry *slab, const dev::PageCopy *copies, int n_copies, bf16 *const *kp,
+                                bf16 *const *vp, int L, int64_t page_elems) {
+  const int run_blocks = (n_runs + 7) / 8;
+  if (static_cast<int>(blockIdx.x) < run_blocks) {
+    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (r >= n_runs) return;
+    const dev::SlabRun run = runs[r];
+    for (int i = threadIdx.x & 31; i < run.count; i += 32) slab[run.dst + i] = run_entries[run.src + i];
+    return;
+  }
+  const int b = blockIdx.x - run_blocks;
+  const int ci = b / (2 * L), rem = b % (2 * L), l = rem >> 1, isv = rem & 1;
+  if (ci >= n_copies) return;
+  const bf16 *pool = isv ? vp[l] : kp[l];
+  const uint4 *src = reinterpret_cast<const uint4 *>(pool + static_cast<int64_t>(copies[ci].src) * page_elems);
+  uint4 *dst = reinterpret_cast<uint4 *>(const_cast<bf16 *>(pool) + static_cast<int64_t>(copies[ci].dst) * page_elems);
+  const int64_t n16 = page_elems / 8;
+  for (int64_t i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
+}
+
+// kvfs_append scatter: rows [row_base, row_base + n) of k/v [L][n_total][Hkv][D] -> pool slots
+// dst[r] = page * P + slot.
+__global__ void append_rows_kernel(const int32_t *dst, int64_t n, int64_t row_base, int64_t n_total, const bf16 *k,
+                                   const bf16 *v, bf16 *const *kp, bf16 *const *vp, int L, int Hkv, int D, int P) {
+  const int cpr = D / 8;
+  const int64_t total = static_cast<int64_t>(L) * n * Hkv * cpr;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(idx % cpr);
+    int64_t t = idx / cpr;
+    const int g = static_cast<int>(t % Hkv);
+    t /= Hkv;
+    const int64_t r = t % n;
+    const int l = static_cast<int>(t / n);
+    const int32_t ds = dst[r];
+    const int64_t so = ((static_cast<int64_t>(l) * n_total + row_base + r) * Hkv + g) * D + c * 8;
+    const int64_t po = ((static_cast<int64_t>(ds / P) * Hkv + g) * P + ds % P) * D + c * 8;
+    *reinterpret_cast<uint4 *>(kp[l] + po) = *reinterpret_cast<const uint4 *>(k + so);
+    *reinterpret_cast<uint4 *>(vp[l] + po) = *reinterpret_cast<const uint4 *>(v + so);
+  }
+}
+
+__device__ __forceinline__ int find_entry(const dev::Entry *t, int n, int64_t i) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (t[mid].lstart <= i) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// K5: token i of the old table (logical order) -> (new_pages[i / P], i % P), every layer, K and V.
+__global__ void compact_kernel(const dev::Entry *old, int n_old, const uint32_t *new_pages, int64_t len,
+                               bf16 *const *kp, bf16 *const *vp, int L, int Hkv, int D, int P) {
+  const int cpr = D / 8;
+  const int64_t total = static_cast<int64_t>(L) * len * Hkv * cpr;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(idx % cpr);
+    int64_t t = idx / cpr;
+    const int g = static_cast<int>(t % Hkv);
+    t /= Hkv;
+    const int64_t i = t % len;
+    const int l = static_cast<int>(t / len);
+    const dev::Entry e = old[find_entry(old, n_old, i)];
+    const int slot = dev::select_bit64(e.mask, static_cast<int>(i - e.lstart));
+    const int64_t so = ((static_cast<int64_t>(e.page) * Hkv + g) * P + slot) * D + c * 8;
+    const int64_t po = ((static_cast<int64_t>(new_pages[i / P]) * Hkv + g) * P + i % P) * D + c * 8;
+    *reinterpret_cast<uint4 *>(kp[l] + po) = *reinterpret_cast<const uint4 *>(kp[l] + so);
+    *reinterpret_cast<uint4 *>(vp[l] + po) = *reinterpret_cast<const uint4 *>(vp[l] + so);
+  }
+}
+
+// K7: logical tokens [begin, end) of one layer -> dense [n][Hkv][D].
+__global__ void read_kernel(const dev::Entry *t, int n_ent, int64_t begin, int64_t end, const bf16 *kpl,
+                            const bf16 *vpl, bf16 *kout, bf16 *vout, int Hkv, int D, int P) {
+  const int cpr = D / 8;
+  const int64_t n = end - begin;
+  const int64_t total = n * Hkv * cpr;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(idx % cpr);
+    int64_t r = idx / cpr;
+    const int g = static_cast<int>(r % Hkv);
+    r /= Hkv;
+    const int64_t i = begin + r;
+    const dev::Entry e = t[find_entry(t, n_ent, i)];
+    const int slot = dev::select_bit64(e.mask, static_cast<int>(i - e.lstart));
+    const int64_t so = ((static_cast<int64_t>(e.page) * Hkv + g) * P + slot) * D + c * 8;
+    const int64_t doff = (r * Hkv + g) * D + c * 8;
+    *reinterpret_cast<uint4 *>(kout + doff) = *reinterpret_cast<const uint4 *>(kpl + so);
+    *reinterpret_cast<uint4 *>(vout + doff) = *reinterpret_cast<const uint4 *>(vpl + so);
+  }
+}
+
+// ------------------------------------------------------------------------------------------ device
+class CudaDevice final : public Device {
+ public:
+  explicit CudaDevice(Ctx &c) : c_(c) {}
+  ~CudaDevice() override {
+    for (auto &s : stg_) {
+      if (s.ev) cudaEventDestroy(s.ev);
+      if (s.host) cudaFreeHost(s.host);
+    }
+  }
+
+  int init() {
+    const kvfs_config &cfg = c_.cfg;
+    if (cudaSetDevice(cfg.device) != cudaSuccess) return KVFS_EINVAL;
+    lay_ = ws_layout(cfg);
+    char *ws = static_cast<char *>(cfg.workspace);
+    if (reinterpret_cast<uintptr_t>(ws) % 256) return KVFS_EINVAL;
+    slab_ = reinterpret_cast<dev::Entry *>(ws + lay_.slab);
+    upload_ = ws + lay_.upload;
+    counters_ = reinterpret_cast<int *>(ws + lay_.counters);
+    partials_ = reinterpret_cast<float *>(ws + lay_.partials);
+    kptrs_ = reinterpret_cast<bf16 **>(ws + lay_.ptrs);
+    vptrs_ = kptrs_ + cfg.n_layers;
+    std::vector<void *> ptrs(c_.kpool);
+    ptrs.insert(ptrs.end(), c_.vpool.begin(), c_.vpool.end());
+    if (cudaMemcpy(kptrs_, ptrs.data(), ptrs.size() * sizeof(void *), cudaMemcpyHostToDevice) != cudaSuccess)
+      return KVFS_EIO;
+    if (cudaMemset(counters_, 0, static_cast<size_t>(cfg.max_batch_rows) * cfg.n_kv_heads * 4) != cudaSuccess)
+      return KVFS_EIO;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device);
+    sms_ = sms > 0 ? sms : 148;
+    for (auto &s : stg_) {
+      if (cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming) != cudaSuccess) return KVFS_EIO;
+      if (!grow(s, 1 << 20)) return KVFS_ENOMEM;
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess) return KVFS_EIO;
+    return KVFS_OK;
+  }
+
+  int copy_pages(const std::vector<PageCopy> &copies, kvfs_stream_t s) override {
+    begin_packet();
+    const void *dc = push(copies.data(), copies.size() * sizeof(PageCopy));
+    if (!dc) return KVFS_ENOMEM;
+    if (!send(s)) return KVFS_EIO;
+    return launch_prologue(nullptr, 0, nullptr, static_cast<const dev::PageCopy *>(dc),
+                           static_cast<int>(copies.size()), s);
+  }
+
+  int append_rows(const std::vector<int32_t> &dst, const void *k, const void *v, kvfs_stream_t s) override {
+    // the slot list is uploaded in pieces that fit the upload area
+    const int64_t n = static_cast<int64_t>(dst.size());
+    const int64_t piece = std::max<int64_t>(1, static_cast<int64_t>(lay_.upload_cap / 8));
+    for (int64_t b = 0; b < n; b += piece) {
+      const int rc = append_piece(dst.data() + b, std::min(piece, n - b), b, n, static_cast<const bf16 *>(k),
+                                  static_cast<const bf16 *>(v), s);
+      if (rc != KVFS_OK) return rc;
+    }
+    return KVFS_OK;
+  }
+
+  int compact(const std::vector<Entry> &old_table, const std::vector<uint32_t> &new_pages, int64_t len,
+              kvfs_stream_t s) override {
+    begin_packet();
+    const void *dt = push(old_table.data(), old_table.size() * sizeof(Entry));
+    const void *dp = push(new_pages.data(), new_pages.size() * sizeof(uint32_t));
+    if (!dt || !dp) return KVFS_ENOMEM;
+    if (!send(s)) return KVFS_EIO;
+    const kvfs_config &cfg = c_.cfg;
+    const int64_t total = static_cast<int64_t>(cfg.n_layers) * len * cfg.n_kv_heads * (cfg.head_dim / 8);
+    const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, sms_ * 16));
+    compact_kernel<<<grid, 256, 0, cs(s)>>>(static_cast<const dev::Entry *>(dt), static_cast<int>(old_table.size()),
+                                            static_cast<const uint32_t *>(dp), len, kptrs_, vptrs_, cfg.n_layers,
+                                            cfg.n_kv_heads, cfg.head_dim, cfg.page_size);
+    ++c_.ctr.launches;
+    return cudaGetLastError() == cudaSuccess ? KVFS_OK : KVFS_EIO;
+  }
+
+  int read(const std::vector<Entry> &table, int layer, int64_t begin, int64_t end, void *k_out, void *v_out,
+           kvfs_stream_t s) override {
+    begin_packet();
+    const void *dt = push(table.data(), table.size() * sizeof(Entry));
+    if (!dt) return KVFS_ENOMEM;
+    if (!send(s)) return KVFS_EIO;
+    const kvfs_config &cfg = c_.cfg;
+    const int64_t total = (end - begin) * cfg.n_kv_heads * (cfg.head_dim / 8);
+    const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, sms_ * 16));
+    read_kernel<<<grid, 256, 0, cs(s)>>>(static_cast<const dev::Entry *>(dt), static_cast<int>(table.size()), begin,
+                                         end, static_cast<const bf16 *>(c_.kpool[layer]),
+                                         static_cast<const bf16 *>(c_.vpool[layer]), static_cast<bf16 *>(k_out),
+                                         static_cast<bf16 *>(v_out), cfg.n_kv_heads, cfg.head_dim, cfg.page_size);
+    ++c_.ctr.launches;
+    return cudaGetLastError() == cudaSuccess ? KVFS_OK : KVFS_EIO;
+  }
+
+  int pred_begin(PredPlan &pl, kvfs_stream_t s) override {
+    begin_packet();
+    d_runs_ = push(pl.runs.data(), pl.runs.size() * sizeof(SlabRun));
+    d_run_entries_ = push(pl.run_entries.data(), pl.run_entries.size() * sizeof(Entry));
+    d_copies_ = push(pl.copies.data(), pl.copies.size() * sizeof(PageCopy));
+    d_descs_ = push(pl.descs.data(), pl.descs.size() * sizeof(DevDesc));
+    d_dst_ = push(pl.dst_slot.data(), pl.dst_slot.size() * sizeof(int32_t));
+    if (!d_runs_ || !d_run_entries_ || !d_copies_ || !d_descs_ || !d_dst_) return KVFS_ENOMEM;
+    if (!send(s)) return KVFS_EIO;
+    if (pl.runs.empty() && pl.copies.empty()) return KVFS_OK;
+    return launch_prologue(static_cast<const dev::SlabRun *>(d_runs_), static_cast<int>(pl.runs.size()),
+                           static_cast<const dev::Entry *>(d_run_entries_),
+                           static_cast<const dev::PageCopy *>(d_copies_), static_cast<int>(pl.copies.size()), s);
+  }
+
+  int pred_layer(const PredPlan &pl, int layer, const void *q, const void *k_new, const void *v_new, void *out,
+                 float *lse, float scale, kvfs_stream_t s) override {
+    if (pl.descs.empty()) return KVFS_OK;
+    const kvfs_config &cfg = c_.cfg;
+    dev::DecodeParams p{};
+    p.descs = static_cast<const dev::Desc *>(d_descs_);
+    p.n_desc = static_cast<int>(pl.descs.size());
+    p.total = pl.total_cost;
+    int64_t ncta = c_.opt_decode_ctas > 0 ? c_.opt_decode_ctas : sms_;
+    ncta = std::min<int64_t>(std::min<int64_t>(ncta, kMaxCtas), pl.total_cost);
+    p.ncta = static_cast<int>(ncta);
+    p.slab = slab_;
+    p.dst_slot = static_cast<const int32_t *>(d_dst_);
+    p.q = static_cast<const bf16 *>(q);
+    p.k_new = static_cast<const bf16 *>(k_new);
+    p.v_new = static_cast<const bf16 *>(v_new);
+    p.out = static_cast<bf16 *>(out);
+    p.lse = lse;
+    p.kpool = static_cast<bf16 *>(c_.kpool[layer]);
+    p.vpool = static_cast<bf16 *>(c_.vpool[layer]);
+    p.scale_log2 = scale * 1.4426950408889634f;
+    p.partials = partials_;
+    p.counters = counters_;
+    p.Hq = cfg.n_q_heads;
+    p.Hkv = cfg.n_kv_heads;
+    const cudaError_t e = dev::launch_decode(p, cfg.head_dim, cfg.n_q_heads / cfg.n_kv_heads, cfg.page_size, cs(s));
+    ++c_.ctr.launches;
+    c_.ctr.last_decode_ctas = ncta;
+    return e == cudaSuccess ? KVFS_OK : KVFS_EIO;
+  }
+
+  int sync() override { return cudaDeviceSynchronize() == cudaSuccess ? KVFS_OK : KVFS_EIO; }
+
+ private:
+  struct Staging {
+    char *host = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    bool pending = false;
+  };
+
+  static cudaStream_t cs(kvfs_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+  bool grow(Staging &s, size_t need) {
+    if (s.cap >= need) return true;
+    if (s.pending) {
+      cudaEventSynchronize(s.ev);
+      s.pending = false;
+    }
+    if (s.host) cudaFreeHost(s.host);
+    s.host = nullptr;
+    size_t cap = std::max<size_t>(need, 2 * s.cap);
+    if (cudaHostAlloc(reinterpret_cast<void **>(&s.host), cap, cudaHostAllocDefault) != cudaSuccess) {
+      s.cap = 0;
+      return false;
+    }
+    s.cap = cap;
+    return true;
+  }
+
+  void begin_packet() {
+    cur_ = (cur_ + 1) % 2;
+    Staging &s = stg_[cur_];
+    if (s.pending) {
+      cudaEventSynchronize(s.ev);  // the H2D copy that last used this buffer has finished
+      s.pending = false;
+    }
+    used_ = 0;
+    pending_.clear();
+  }
+
+  // Reserve bytes in the packet; returns the device address they will occupy.  Data is gathered into the
+  // pinned buffer at send().
+  const void *push(const void *data, size_t bytes) {
+    const size_t off = (used_ + 15) & ~static_cast<size_t>(15);
+    if (off + bytes > lay_.upload_cap) return nullptr;
+    pending_.push_back({data, bytes, off});
+    used_ = off + bytes;
+    return upload_ + off;
+  }
+
+  bool send(kvfs_stream_t s) {
+    Staging &st = stg_[cur_];
+    if (!grow(st, std::max<size_t>(used_, 16))) return false;
+    for (const auto &p : pending_)
+      if (p.bytes) std::memcpy(st.host + p.off, p.data, p.bytes);
+    if (used_ == 0) return true;
+    if (cudaMemcpyAsync(upload_, st.host, used_, cudaMemcpyHostToDevice, cs(s)) != cudaSuccess) return false;
+    if (cudaEventRecord(st.ev, cs(s)) != cudaSuccess) return false;
+    st.pending = true;
+    c_.ctr.h2d_bytes += static_cast<int64_t>(used_);
+    return true;
+  }
+
+  int launch_prologue(const dev::SlabRun *runs, int n_runs, const dev::Entry *run_entries,
+                      const dev::PageCopy *copies, int n_copies, kvfs_stream_t s) {
+    const kvfs_config &cfg = c_.cfg;
+    const int blocks = (n_runs + 7) / 8 + n_copies * 2 * cfg.n_layers;
+    if (blocks == 0) return KVFS_OK;
+    const int64_t page_elems = static_cast<int64_t>(cfg.n_kv_heads) * cfg.page_size * cfg.head_dim;
+    prologue_kernel<<<blocks, 256, 0, cs(s)>>>(runs, n_runs, run_entries, slab_, copies, n_copies, kptrs_, vptrs_,
+                                               cfg.n_layers, page_elems);
+    ++c_.ctr.launches;
+    return cudaGetLastError() == cudaSuccess ? KVFS_OK : KVFS_EIO;
+  }
+
+  int append_piece(const int32_t *dst, int64_t m, int64_t row_base, int64_t n_total, const bf16 *k, const bf16 *v,
+                   kvfs_stream_t s) {
+    begin_packet();
+    const void *dd = push(dst, static_cast<size_t>(m) * sizeof(int32_t));
+    if (!dd) return KVFS_ENOMEM;
+    if (!send(s)) return KVFS_EIO;
+    const kvfs_config &cfg = c_.cfg;
+    const int64_t total = cfg.n_layers * m * cfg.n_kv_heads * (cfg.head_dim / 8);
+    const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, sms_ * 16));
+    append_rows_kernel<<<grid, 256, 0, cs(s)>>>(static_cast<const int32_t *>(dd), m, row_base, n_total, k, v, kptrs_,
+                                                vptrs_, cfg.n_layers, cfg.n_kv_heads, cfg.head_dim, cfg.page_size);
+    ++c_.ctr.launches;
+    return cudaGetLastError() == cudaSuccess ? KVFS_OK : KVFS_EIO;
+  }
+
+  struct Pending {
+    const void *data;
+    size_t bytes, off;
+  };
+
+  Ctx &c_;
+  WsLayout lay_;
+  dev::Entry *slab_ = nullptr;
+  char *upload_ = nullptr;
+  int *counters_ = nullptr;
+  float *partials_ = nullptr;
+  bf16 **kptrs_ = nullptr, **vptrs_ = nullptr;
+  int sms_ = 148;
+  Staging stg_[2];
+  int cur_ = 0;
+  size_t used_ = 0;
+  std::vector<Pending> pending_;
+  const void *d_runs_ = nullptr, *d_run_entries_ = nullptr, *d_copies_ = nullptr, *d_descs_ = nullptr,
+             *d_dst_ = nullptr;
+};
+
+}  // namespace
+
+size_t device_workspace_bytes(const kvfs_config &cfg) { return ws_layout(cfg).total; }
+
+int create_device(Ctx &c, Device **out) {
+  auto *d = new (std::nothrow) CudaDevice(c);
+  if (!d) return KVFS_ENOMEM;
+  const int rc = d->init();
+  if (rc != KVFS_OK) {
+    delete d;
+    return rc;
+  }
+  *out = d;
+  return KVFS_OK;
+}
+
+}  // namespace kvfs

@@ -1,0 +1,107 @@
+// Batched pred, host side (§4.4 P:239-243 batch assembly; §4.1 P:215 append): validate and
+// reserve every descriptor in order (R11), then emit the plan the data plane consumes: the packed
+// descriptor list, per-row destination slots of the append, copy-on-write copies, and the slab
+// updates (table deltas) of the files in the batch.
+#include <algorithm>
+
+#include "kvfs_impl.h"
+
+namespace kvfs {
+
+int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos, int *status, PredPlan *plan) {
+  const int P = c.cfg.page_size;
+  const int Hkv = c.cfg.n_kv_heads;
+  if (n_desc < 0 || n_desc > c.cfg.max_batch_descs || (n_desc > 0 && !descs)) return KVFS_EINVAL;
+  int64_t T = 0;
+  for (int i = 0; i < n_desc; ++i) {
+    if (descs[i].n_q < 0) return KVFS_EINVAL;
+    T += descs[i].n_q;
+  }
+  if (T > c.cfg.max_batch_rows || (T > 0 && !pos)) return KVFS_EINVAL;
+
+  const bool device = c.dev != nullptr;
+  PredPlan &pl = *plan;
+  pl.descs.clear();
+  pl.runs.clear();
+  pl.run_entries.clear();
+  pl.copies.clear();
+  pl.dst_slot.assign(static_cast<size_t>(T), -1);
+  pl.total_cost = 0;
+  pl.n_units = 0;
+  pl.T = static_cast<int32_t>(T);
+  pl.max_nq = 0;
+  const int64_t tag = ++c.batch_counter;
+
+  std::vector<int32_t> dst;
+  int64_t row = 0;
+  bool partial = false;
+  for (int i = 0; i < n_desc; ++i) {
+    const int64_t row0 = row;
+    const int nq = descs[i].n_q;
+    row += nq;
+    int st = KVFS_OK;
+    File *f = get_file(c, descs[i].fd);
+    if (!f) {
+      st = KVFS_EBADF;
+    } else if (f->batch_tag == tag) {
+      st = KVFS_EBUSY;
+    } else {
+      f->batch_tag = tag;
+      if (nq > 0) {
+        int64_t need = 0, new_entries = 0;
+        st = append_plan(c, *f, nq, pos + row0, &need, &new_entries);
+        if (st == KVFS_OK && device) {
+          // the table may outgrow the file's slab block: get the new block before committing
+          const int64_t size_after = static_cast<int64_t>(f->table.size()) + new_entries;
+          if (size_after > f->slab_cap) {
+            int64_t off = 0, cap = 0;
+            if (!c.slab.alloc(std::max<int64_t>(size_after, 2 * static_cast<int64_t>(f->table.size())), &off, &cap) &&
+                !c.slab.alloc(size_after, &off, &cap)) {
+              st = KVFS_ENOMEM;
+            } else {
+              release_file_slab(c, *f);
+              f->slab_off = off;
+              f->slab_cap = cap;
+              f->dirty_from = 0;
+            }
+          }
+        }
+        if (st == KVFS_OK) {
+          const int64_t n_old = f->len;
+          dst.clear();
+          append_commit(c, *f, nq, pos + row0, &dst, &pl.copies);
+          std::copy(dst.begin(), dst.end(), pl.dst_slot.begin() + row0);
+          int64_t idx = static_cast<int64_t>(f->table.size()) - 1;
+          while (idx >= 0 && f->table[idx].lstart >= n_old) --idx;
+          DevDesc d{};
+          d.cost_begin = pl.total_cost;
+          d.slab_off = static_cast<int32_t>(f->slab_off);
+          d.n_old_entries = static_cast<int32_t>(idx + 1);
+          d.n_old = static_cast<int32_t>(n_old);
+          d.n_q = nq;
+          d.row0 = static_cast<int32_t>(row0);
+          d.unit_base = pl.n_units;
+          d.stages_per_unit = d.n_old_entries + (nq + P - 1) / P;
+          pl.descs.push_back(d);
+          pl.total_cost += static_cast<int64_t>(Hkv) * nq * d.stages_per_unit;
+          pl.n_units += Hkv * nq;
+          pl.max_nq = std::max(pl.max_nq, nq);
+          if (device && f->dirty_from < f->table.size()) {
+            SlabRun r{f->slab_off + static_cast<int64_t>(f->dirty_from), static_cast<int32_t>(pl.run_entries.size()),
+                      static_cast<int32_t>(f->table.size() - f->dirty_from)};
+            pl.runs.push_back(r);
+            pl.run_entries.insert(pl.run_entries.end(), f->table.begin() + static_cast<long>(f->dirty_from),
+                                  f->table.end());
+            f->dirty_from = f->table.size();
+          }
+        }
+      }
+    }
+    if (status) status[i] = st;
+    if (st != KVFS_OK) partial = true;
+  }
+  c.ctr.page_copies += static_cast<int64_t>(pl.copies.size());
+  return partial ? KVFS_EPARTIAL : KVFS_OK;
+}
+
+}  // namespace kvfs

@@ -1,0 +1,395 @@
+// extern "C" shims of include/kvfs.h: argument validation, the ctx mutex, error mapping, and the split
+// between host metadata (this directory) and the device data plane (csrc/cuda).
+#include <cstring>
+#include <new>
+
+#include "kvfs_impl.h"
+
+using namespace kvfs;
+
+namespace {
+
+bool supported_shape(const kvfs_config &c) {
+  if (c.n_layers < 1 || c.n_layers > 1024) return false;
+  if (c.n_kv_heads < 1 || c.n_q_heads < c.n_kv_heads || c.n_q_heads % c.n_kv_heads) return false;
+  const int G = c.n_q_heads / c.n_kv_heads;
+  if (G != 1 && G != 2 && G != 4 && G != 8) return false;
+  if (c.head_dim != 64 && c.head_dim != 128) return false;
+  if (c.page_size != 16 && c.page_size != 32 && c.page_size != 64) return false;
+  if (c.n_pages < 1 || c.n_pages >= (int64_t{1} << 25)) return false;
+  if (static_cast<int64_t>(c.n_pages) * c.page_size >= (int64_t{1} << 31)) return false;
+  if (c.max_batch_rows < 1 || c.max_batch_descs < 1) return false;
+  return true;
+}
+
+int64_t default_table_capacity(const kvfs_config &c) {
+  return c.table_capacity > 0 ? c.table_capacity : 2 * c.n_pages + 65536;
+}
+
+struct Lock {
+  explicit Lock(kvfs_ctx *ctx) : c(reinterpret_cast<Ctx *>(ctx)), g(c->mu) {}
+  Ctx *c;
+  std::lock_guard<std::mutex> g;
+};
+
+}  // namespace
+
+struct kvfs_ctx {};  // opaque; the real object is kvfs::Ctx
+struct pred_step {};
+
+extern "C" {
+
+const char *kvfs_strerror(int err) {
+  switch (err) {
+    case KVFS_OK: return "ok";
+    case KVFS_ENOENT: return "no such file";
+    case KVFS_EIO: return "CUDA error (ctx poisoned)";
+    case KVFS_EBADF: return "bad file descriptor";
+    case KVFS_ENOMEM: return "out of memory (host, table slab or workspace)";
+    case KVFS_EBUSY: return "busy (file repeated in a batch, or a pred step is open)";
+    case KVFS_EEXIST: return "file exists";
+    case KVFS_EINVAL: return "invalid argument";
+    case KVFS_ENOSPC: return "page pool exhausted";
+    case KVFS_ERANGE: return "out of range";
+    case KVFS_ENOSYS: return "data operation on a host-only ctx";
+    case KVFS_EPOS: return "position conflict";
+    case KVFS_EPARTIAL: return "some batch descriptors failed";
+    default: return "unknown error";
+  }
+}
+
+size_t kvfs_workspace_bytes(const kvfs_config *cfg) {
+  if (!cfg || !supported_shape(*cfg) || cfg->device < 0) return 0;
+  kvfs_config c = *cfg;
+  c.table_capacity = default_table_capacity(c);
+  return device_workspace_bytes(c);
+}
+
+int kvfs_init(const kvfs_config *cfg, kvfs_ctx **out) {
+  if (!cfg || !out || !supported_shape(*cfg)) return KVFS_EINVAL;
+  Ctx *c = new (std::nothrow) Ctx();
+  if (!c) return KVFS_ENOMEM;
+  c->cfg = *cfg;
+  c->cfg.table_capacity = default_table_capacity(*cfg);
+  c->pool.reset(new PagePool(cfg->n_pages));
+  c->slab.init(c->cfg.table_capacity);
+  if (cfg->device >= 0) {
+    if (!cfg->k_pool || !cfg->v_pool || !cfg->workspace) {
+      delete c;
+      return KVFS_EINVAL;
+    }
+    for (int l = 0; l < cfg->n_layers; ++l) {
+      if (!cfg->k_pool[l] || !cfg->v_pool[l]) {
+        delete c;
+        return KVFS_EINVAL;
+      }
+      c->kpool.push_back(cfg->k_pool[l]);
+      c->vpool.push_back(cfg->v_pool[l]);
+    }
+    c->cfg.k_pool = c->kpool.data();
+    c->cfg.v_pool = c->vpool.data();
+    if (cfg->workspace_bytes < device_workspace_bytes(c->cfg)) {
+      delete c;
+      return KVFS_ENOMEM;
+    }
+    Device *d = nullptr;
+    const int rc = create_device(*c, &d);
+    if (rc != KVFS_OK) {
+      delete c;
+      return rc;
+    }
+    c->dev = d;
+  } else {
+    c->cfg.k_pool = nullptr;
+    c->cfg.v_pool = nullptr;
+  }
+  *out = reinterpret_cast<kvfs_ctx *>(c);
+  return KVFS_OK;
+}
+
+int kvfs_destroy(kvfs_ctx *ctx) {
+  if (!ctx) return KVFS_EINVAL;
+  Ctx *c = reinterpret_cast<Ctx *>(ctx);
+  if (c->dev) {
+    c->dev->sync();
+    delete c->dev;
+  }
+  delete c;
+  return KVFS_OK;
+}
+
+#define KVFS_LOCK_OR(ctx)                       \
+  if (!(ctx)) return KVFS_EINVAL;               \
+  Lock lk_(ctx);                                \
+  Ctx &c = *lk_.c;                              \
+  if (c.step_open) return KVFS_EBUSY;
+
+int kvfs_open(kvfs_ctx *ctx, const char *name, int flags, int *fd) {
+  KVFS_LOCK_OR(ctx);
+  return open_file(c, name, flags, fd);
+}
+
+int kvfs_close(kvfs_ctx *ctx, int fd) {
+  KVFS_LOCK_OR(ctx);
+  return close_file(c, fd);
+}
+
+int kvfs_unlink(kvfs_ctx *ctx, const char *name) {
+  KVFS_LOCK_OR(ctx);
+  return unlink_file(c, name);
+}
+
+int kvfs_fork(kvfs_ctx *ctx, int src_fd, const char *dst_name, int *dst_fd, kvfs_stream_t stream) {
+  KVFS_LOCK_OR(ctx);
+  if (c.dev && c.poisoned) return KVFS_EIO;
+  File *src = get_file(c, src_fd);
+  if (!src) return KVFS_EBADF;
+  std::vector<PageCopy> copies;
+  int rc = fork_file(c, *src, dst_name, dst_fd, &copies);
+  if (rc != KVFS_OK) return rc;
+  c.ctr.page_copies += static_cast<int64_t>(copies.size());
+  if (c.dev && !copies.empty()) {
+    rc = c.dev->copy_pages(copies, stream);
+    if (rc != KVFS_OK) c.poisoned = true;
+  }
+  return rc;
+}
+
+int kvfs_truncate(kvfs_ctx *ctx, int fd, int64_t new_len) {
+  KVFS_LOCK_OR(ctx);
+  File *f = get_file(c, fd);
+  if (!f) return KVFS_EBADF;
+  return truncate_file(c, *f, new_len);
+}
+
+int kvfs_evict(kvfs_ctx *ctx, int fd, const int64_t *ranges, int n_ranges, int flags, kvfs_stream_t stream) {
+  KVFS_LOCK_OR(ctx);
+  if (c.dev && c.poisoned) return KVFS_EIO;
+  File *f = get_file(c, fd);
+  if (!f) return KVFS_EBADF;
+  if (flags & ~KVFS_EVICT_COMPACT) return KVFS_EINVAL;
+  std::vector<Entry> old_table;
+  std::vector<uint32_t> new_pages;
+  int rc = evict_file(c, *f, ranges, n_ranges, flags, &old_table, &new_pages);
+  if (rc != KVFS_OK) return rc;
+  if (c.dev && !new_pages.empty()) {
+    rc = c.dev->compact(old_table, new_pages, f->len, stream);
+    if (rc != KVFS_OK) c.poisoned = true;
+  }
+  return rc;
+}
+
+int kvfs_compact(kvfs_ctx *ctx, int fd, kvfs_stream_t stream) {
+  KVFS_LOCK_OR(ctx);
+  if (c.dev && c.poisoned) return KVFS_EIO;
+  File *f = get_file(c, fd);
+  if (!f) return KVFS_EBADF;
+  std::vector<Entry> old_table;
+  std::vector<uint32_t> new_pages;
+  int rc = compact_file(c, *f, &old_table, &new_pages);
+  if (rc != KVFS_OK) return rc;
+  if (c.dev && !new_pages.empty()) {
+    rc = c.dev->compact(old_table, new_pages, f->len, stream);
+    if (rc != KVFS_OK) c.poisoned = true;
+  }
+  return rc;
+}
+
+int kvfs_append(kvfs_ctx *ctx, int fd, int64_t n, const int32_t *pos, const void *k, const void *v,
+                kvfs_stream_t stream) {
+  KVFS_LOCK_OR(ctx);
+  if (c.dev && c.poisoned) return KVFS_EIO;
+  File *f = get_file(c, fd);
+  if (!f) return KVFS_EBADF;
+  if (n < 0 || (n > 0 && !pos)) return KVFS_EINVAL;
+  if (n == 0) return KVFS_OK;
+  if (n >= (int64_t{1} << 30)) return KVFS_EINVAL;
+  if (c.dev && (!k || !v)) return KVFS_EINVAL;
+  int64_t need = 0;
+  int rc = append_plan(c, *f, n, pos, &need, nullptr);
+  if (rc != KVFS_OK) return rc;
+  std::vector<int32_t> dst;
+  std::vector<PageCopy> copies;
+  dst.reserve(static_cast<size_t>(n));
+  append_commit(c, *f, n, pos, &dst, &copies);
+  c.ctr.page_copies += static_cast<int64_t>(copies.size());
+  if (c.dev) {
+    if (!copies.empty()) rc = c.dev->copy_pages(copies, stream);
+    if (rc == KVFS_OK) rc = c.dev->append_rows(dst, k, v, stream);
+    if (rc != KVFS_OK) c.poisoned = true;
+  }
+  return rc;
+}
+
+// ------------------------------------------------------------------------------------------ pred
+int pred_step_begin(kvfs_ctx *ctx, const pred_desc *descs, int n_desc, const int32_t *pos, int *status,
+                    pred_step **step, kvfs_stream_t stream) {
+  KVFS_LOCK_OR(ctx);
+  if (!step) return KVFS_EINVAL;
+  if (c.dev && c.poisoned) return KVFS_EIO;
+  const int rc = pred_reserve(c, descs, n_desc, pos, status, &c.plan);
+  if (rc != KVFS_OK && rc != KVFS_EPARTIAL) return rc;
+  if (c.dev) {
+    const int drc = c.dev->pred_begin(c.plan, stream);
+    if (drc != KVFS_OK) {
+      c.poisoned = true;
+      return drc;
+    }
+  }
+  c.step_open = true;
+  *step = reinterpret_cast<pred_step *>(&c.plan);
+  return rc;
+}
+
+int pred_attn_layer(kvfs_ctx *ctx, pred_step *step, int layer, const void *q, const void *k_new,
+                    const void *v_new, void *out, float *lse, float scale, kvfs_stream_t stream) {
+  if (!ctx) return KVFS_EINVAL;
+  Lock lk(ctx);
+  Ctx &c = *lk.c;
+  if (!c.step_open || step != reinterpret_cast<pred_step *>(&c.plan)) return KVFS_EINVAL;
+  if (!c.dev) return KVFS_ENOSYS;
+  if (c.poisoned) return KVFS_EIO;
+  if (layer < 0 || layer >= c.cfg.n_layers || !(scale > 0.f)) return KVFS_EINVAL;
+  if (c.plan.T > 0 && (!q || !k_new || !v_new || !out)) return KVFS_EINVAL;
+  const int rc = c.dev->pred_layer(c.plan, layer, q, k_new, v_new, out, lse, scale, stream);
+  if (rc != KVFS_OK) c.poisoned = true;
+  return rc;
+}
+
+int pred_step_end(kvfs_ctx *ctx, pred_step *step) {
+  if (!ctx) return KVFS_EINVAL;
+  Lock lk(ctx);
+  Ctx &c = *lk.c;
+  if (!c.step_open || step != reinterpret_cast<pred_step *>(&c.plan)) return KVFS_EINVAL;
+  c.step_open = false;
+  return KVFS_OK;
+}
+
+int pred_attn_batch(kvfs_ctx *ctx, const pred_desc *descs, int n_desc, const int32_t *pos, const void *q,
+                    const void *k_new, const void *v_new, void *out, float *lse, float scale, int *status,
+                    kvfs_stream_t stream) {
+  if (!ctx) return KVFS_EINVAL;
+  {
+    Lock lk(ctx);
+    Ctx &c = *lk.c;
+    if (c.step_open) return KVFS_EBUSY;
+    if (!c.dev) return KVFS_ENOSYS;
+    if (c.poisoned) return KVFS_EIO;
+    if (c.cfg.n_layers != 1 || !(scale > 0.f)) return KVFS_EINVAL;
+    int64_t T = 0;
+    for (int i = 0; descs && i < n_desc; ++i) T += descs[i].n_q > 0 ? descs[i].n_q : 0;
+    if (T > 0 && (!q || !k_new || !v_new || !out)) return KVFS_EINVAL;
+  }
+  pred_step *st = nullptr;
+  const int rc = pred_step_begin(ctx, descs, n_desc, pos, status, &st, stream);
+  if (rc != KVFS_OK && rc != KVFS_EPARTIAL) return rc;
+  const int lrc = pred_attn_layer(ctx, st, 0, q, k_new, v_new, out, lse, scale, stream);
+  pred_step_end(ctx, st);
+  return lrc != KVFS_OK ? lrc : rc;
+}
+
+// ------------------------------------------------------------------------------------------ introspection
+int kvfs_stat(kvfs_ctx *ctx, int fd, kvfs_stat_t *st) {
+  KVFS_LOCK_OR(ctx);
+  File *f = get_file(c, fd);
+  if (!f) return KVFS_EBADF;
+  if (!st) return KVFS_EINVAL;
+  st->len = f->len;
+  st->n_entries = static_cast<int64_t>(f->table.size());
+  st->last_pos = f->pos.empty() ? -1 : f->pos.back();
+  st->reserved = 0;
+  return KVFS_OK;
+}
+
+int kvfs_get_table(kvfs_ctx *ctx, int fd, uint32_t *page, uint64_t *mask, int64_t cap, int64_t *n) {
+  KVFS_LOCK_OR(ctx);
+  File *f = get_file(c, fd);
+  if (!f) return KVFS_EBADF;
+  if (cap < 0 || (cap > 0 && (!page || !mask))) return KVFS_EINVAL;
+  const int64_t m = static_cast<int64_t>(f->table.size());
+  for (int64_t i = 0; i < m && i < cap; ++i) {
+    page[i] = f->table[i].page;
+    mask[i] = f->table[i].mask;
+  }
+  if (n) *n = m;
+  return KVFS_OK;
+}
+
+int kvfs_get_positions(kvfs_ctx *ctx, int fd, int32_t *pos, int64_t cap, int64_t *n) {
+  KVFS_LOCK_OR(ctx);
+  File *f = get_file(c, fd);
+  if (!f) return KVFS_EBADF;
+  if (cap < 0 || (cap > 0 && !pos)) return KVFS_EINVAL;
+  const int64_t m = static_cast<int64_t>(f->pos.size());
+  if (m > 0 && cap > 0) std::memcpy(pos, f->pos.data(), sizeof(int32_t) * static_cast<size_t>(std::min(m, cap)));
+  if (n) *n = m;
+  return KVFS_OK;
+}
+
+int kvfs_get_refcounts(kvfs_ctx *ctx, uint32_t *refcnt, int64_t n) {
+  KVFS_LOCK_OR(ctx);
+  if (n < 0 || (n > 0 && !refcnt)) return KVFS_EINVAL;
+  for (int64_t p = 0; p < n && p < c.pool->n_pages(); ++p) refcnt[p] = c.pool->refcnt(static_cast<uint32_t>(p));
+  return KVFS_OK;
+}
+
+int kvfs_free_pages(kvfs_ctx *ctx, int64_t *n_free) {
+  KVFS_LOCK_OR(ctx);
+  if (!n_free) return KVFS_EINVAL;
+  *n_free = c.pool->n_free();
+  return KVFS_OK;
+}
+
+int kvfs_read(kvfs_ctx *ctx, int fd, int layer, int64_t begin, int64_t end, void *k_out, void *v_out,
+              kvfs_stream_t stream) {
+  KVFS_LOCK_OR(ctx);
+  File *f = get_file(c, fd);
+  if (!f) return KVFS_EBADF;
+  if (!c.dev) return KVFS_ENOSYS;
+  if (c.poisoned) return KVFS_EIO;
+  if (layer < 0 || layer >= c.cfg.n_layers) return KVFS_EINVAL;
+  if (begin < 0 || end < begin || end > f->len) return KVFS_ERANGE;
+  if (end == begin) return KVFS_OK;
+  if (!k_out || !v_out) return KVFS_EINVAL;
+  const int rc = c.dev->read(f->table, layer, begin, end, k_out, v_out, stream);
+  if (rc != KVFS_OK) c.poisoned = true;
+  return rc;
+}
+
+int kvfs_audit(kvfs_ctx *ctx) {
+  KVFS_LOCK_OR(ctx);
+  return audit(c);
+}
+
+int kvfs_set_option(kvfs_ctx *ctx, int option, int64_t value) {
+  KVFS_LOCK_OR(ctx);
+  switch (option) {
+    case KVFS_OPT_DECODE_CTAS:
+      if (value < 0 || value > 4096) return KVFS_EINVAL;
+      c.opt_decode_ctas = value;
+      return KVFS_OK;
+    case KVFS_OPT_CHUNK_CUTOVER:
+      if (value < 0) return KVFS_EINVAL;
+      c.opt_chunk_cutover = value;
+      return KVFS_OK;
+    case KVFS_OPT_DETERMINISTIC:
+      return KVFS_OK;
+    default:
+      return KVFS_EINVAL;
+  }
+}
+
+int kvfs_get_counter(kvfs_ctx *ctx, int counter, int64_t *value) {
+  if (!ctx || !value) return KVFS_EINVAL;
+  Lock lk(ctx);
+  Ctx &c = *lk.c;
+  switch (counter) {
+    case KVFS_CTR_KERNEL_LAUNCHES: *value = c.ctr.launches; return KVFS_OK;
+    case KVFS_CTR_H2D_BYTES: *value = c.ctr.h2d_bytes; return KVFS_OK;
+    case KVFS_CTR_PAGE_COPIES: *value = c.ctr.page_copies; return KVFS_OK;
+    case KVFS_CTR_LAST_DECODE_CTAS: *value = c.ctr.last_decode_ctas; return KVFS_OK;
+    default: return KVFS_EINVAL;
+  }
+}
+
+}  // extern "C"

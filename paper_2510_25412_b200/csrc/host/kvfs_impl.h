@@ -1,0 +1,156 @@
+// Host control plane of KVFS (no CUDA dependency): files, page tables, the batched-pred reserve and
+// the plan handed to the device data plane.  Rules R1-R11 as in SURVEY.md §8(c) C3 / DESIGN.md.
+#pragma once
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../../include/kvfs.h"
+#include "pool.h"
+
+namespace kvfs {
+
+// One page-table entry.  Byte-identical to the device mirror entry (16 B): the slab is a plain copy.
+struct Entry {
+  uint32_t page;
+  int32_t lstart;  // logical index of the entry's first retained token (prefix sum of popcounts)
+  uint64_t mask;   // bit s = slot s retained
+};
+static_assert(sizeof(Entry) == 16, "Entry must be 16 bytes");
+
+struct File {
+  std::string name;
+  bool alive = true;
+  std::vector<Entry> table;
+  std::vector<int32_t> pos;  // absolute positions of the retained tokens, logical order
+  int64_t len = 0;
+  // device mirror of `table` in the slab: entries [0, dirty_from) are up to date on the device
+  int64_t slab_off = -1;
+  int64_t slab_cap = 0;
+  size_t dirty_from = 0;
+  int64_t batch_tag = -1;  // pred batch id that last used the file (EBUSY detection)
+};
+using FilePtr = std::shared_ptr<File>;
+
+struct PageCopy {
+  uint32_t src, dst;
+};
+
+// Slab of device table entries: per-file blocks of power-of-two capacity (>= 64 entries) with per-class
+// free lists.  Host bookkeeping only; a freed block is reused by later uploads, which are stream-ordered
+// after every kernel that could still read it.
+class Slab {
+ public:
+  void init(int64_t capacity) { cap_ = capacity; top_ = 0; free_.assign(40, {}); }
+  bool alloc(int64_t n, int64_t *off, int64_t *cap);
+  void free(int64_t off, int64_t cap);
+  int64_t capacity() const { return cap_; }
+
+ private:
+  int64_t cap_ = 0, top_ = 0;
+  std::vector<std::vector<int64_t>> free_;
+};
+
+// Per-descriptor record consumed by the decode kernel (layout shared with csrc/cuda/common.cuh).
+struct DevDesc {
+  int64_t cost_begin;       // first global stage index of this descriptor's units
+  int32_t slab_off;         // entry base of the file's table in the slab
+  int32_t n_old_entries;    // entries holding at least one token retained before this call
+  int32_t n_old;            // retained tokens before this call's append
+  int32_t n_q;              // new tokens (query rows)
+  int32_t row0;             // first packed row of the descriptor
+  int32_t unit_base;        // global unit index of (g=0, qi=0)
+  int32_t stages_per_unit;  // n_old_entries + ceil(n_q / P)
+  int32_t pad0;
+  int64_t pad1;
+};
+static_assert(sizeof(DevDesc) == 48, "DevDesc must be 48 bytes");
+
+struct SlabRun {
+  int64_t dst;    // first slab entry written
+  int32_t src;    // first entry in the uploaded run array
+  int32_t count;  // entries
+};
+static_assert(sizeof(SlabRun) == 16, "SlabRun must be 16 bytes");
+
+struct PredPlan {
+  std::vector<DevDesc> descs;       // successful descriptors with n_q > 0, in order
+  std::vector<int32_t> dst_slot;    // [T] page * P + slot of every appended row (-1: row not appended)
+  std::vector<SlabRun> runs;        // slab updates
+  std::vector<Entry> run_entries;
+  std::vector<PageCopy> copies;     // copy-on-write copies
+  int64_t total_cost = 0;
+  int32_t n_units = 0;
+  int32_t T = 0;
+  int32_t max_nq = 0;
+};
+
+class Device;  // data plane (csrc/cuda), absent for a host-only ctx
+
+struct CtxCounters {
+  int64_t launches = 0, h2d_bytes = 0, page_copies = 0, last_decode_ctas = 0;
+};
+
+struct Ctx {
+  std::mutex mu;
+  kvfs_config cfg{};
+  std::vector<void *> kpool, vpool;
+  std::unique_ptr<PagePool> pool;
+  std::unordered_map<std::string, FilePtr> names;
+  std::vector<FilePtr> fds;  // index = fd
+  Slab slab;
+  Device *dev = nullptr;
+  bool poisoned = false;
+  bool step_open = false;
+  int64_t batch_counter = 0;
+  int64_t opt_decode_ctas = 0;
+  int64_t opt_chunk_cutover = 0;
+  CtxCounters ctr;
+  PredPlan plan;  // the open step's plan
+  std::vector<int> step_status;
+};
+
+// ---- host operations (files.cc); return kvfs_err codes, atomic on failure
+int open_file(Ctx &c, const char *name, int flags, int *fd);
+int close_file(Ctx &c, int fd);
+int unlink_file(Ctx &c, const char *name);
+File *get_file(Ctx &c, int fd);
+int append_plan(const Ctx &c, const File &f, int64_t n, const int32_t *pos, int64_t *need, int64_t *new_entries);
+// Commit R3; appends dst slots (page * P + slot) of the new tokens and any copy-on-write copy.
+void append_commit(Ctx &c, File &f, int64_t n, const int32_t *pos, std::vector<int32_t> *dst,
+                   std::vector<PageCopy> *copies);
+int fork_file(Ctx &c, File &src, const char *dst_name, int *dst_fd, std::vector<PageCopy> *copies);
+int truncate_file(Ctx &c, File &f, int64_t n);
+int evict_file(Ctx &c, File &f, const int64_t *ranges, int n_ranges, int flags, std::vector<Entry> *old_table,
+               std::vector<uint32_t> *new_pages);
+int compact_file(Ctx &c, File &f, std::vector<Entry> *old_table, std::vector<uint32_t> *new_pages);
+void recompute_lstart(File &f, size_t from);
+void release_file_slab(Ctx &c, File &f);
+int audit(Ctx &c);
+
+// ---- batched pred (batch.cc)
+int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos, int *status, PredPlan *plan);
+
+// ---- data plane interface (implemented in csrc/cuda/device.cu)
+class Device {
+ public:
+  virtual ~Device() = default;
+  virtual int copy_pages(const std::vector<PageCopy> &copies, kvfs_stream_t s) = 0;
+  virtual int append_rows(const std::vector<int32_t> &dst, const void *k, const void *v, kvfs_stream_t s) = 0;
+  virtual int compact(const std::vector<Entry> &old_table, const std::vector<uint32_t> &new_pages, int64_t len,
+                      kvfs_stream_t s) = 0;
+  virtual int read(const std::vector<Entry> &table, int layer, int64_t begin, int64_t end, void *k_out,
+                   void *v_out, kvfs_stream_t s) = 0;
+  virtual int pred_begin(PredPlan &plan, kvfs_stream_t s) = 0;
+  virtual int pred_layer(const PredPlan &plan, int layer, const void *q, const void *k_new, const void *v_new,
+                         void *out, float *lse, float scale, kvfs_stream_t s) = 0;
+  virtual int sync() = 0;
+};
+
+size_t device_workspace_bytes(const kvfs_config &cfg);
+int create_device(Ctx &c, Device **out);
+
+}  // namespace kvfs
