@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Benchmark of the batched `pred` hot path (BASELINE.json metric: pred decode tokens/s at the Llama-3-8B
+attention shape and KV-attention HBM GB/s vs peak).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+
+One step = one batched pred over the workload's batch: batch assembly + validate/reserve
+(host C++), one metadata H2D copy, the table-delta/copy-on-write prologue kernel, and the fused
+append + split-KV decode attention kernel, through the C ABI.  N > 1: one process per GPU (torchrun),
+each rank runs its own LIPs (weak scaling, no collective on the step); the time is the max over ranks.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "pred decode tokens/s (8B-attn shape) and KV-attn HBM GB/s vs peak at 1/2/4/8 GPU"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample for cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs: copy bandwidth)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md recipe)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _one(self):
+        try:
+            r = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+            if r.returncode == 0 and r.stdout.strip():
+                self.samples.append([x.strip() for x in r.stdout.strip().split(",")])
+        except Exception:
+            pass
+
+    def _run(self):
+        while not self._stop.is_set():
+            self._one()
+            self._stop.wait(0.1)
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+        if not self.samples:
+            self._one()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for n, v in zip(names, s[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------------------------------ CPU oracle
+def oracle_sample(cfg_name: str, seconds: float, max_steps: int = None, n_sample: int = 8):
+    """Time the oracle (as it stands) on a bounded sample of the workload: n_sample of the LIPs with their
+    full files, one decode pred per step, repeated until `seconds` elapse (or max_steps)."""
+    import numpy as np
+
+    from oracle import Oracle
+    from paper_2510_25412_b200.workloads import CONFIGS, STEP_OWNER
+    from synth.workloads import TAG_K, TAG_Q, TAG_V, rows_np
+
+    c = CONFIGS[cfg_name]
+    s = c["shape"]
+    n_sample = min(n_sample, c["n_files"])
+    steps_cap = max_steps if max_steps is not None else 10 ** 9
+    per_file = (c["file_len"] + 1024 + s.P) // s.P + 2
+    o = Oracle(n_sample * per_file, s.P, 1, s.Hkv, s.D)
+    fds, lens = [], []
+    for f in range(n_sample):
+        fd = o.open(f"lip{f}")
+        k = rows_np(c["seed"], TAG_K, 0, f, 0, c["file_len"], s.Hkv * s.D).reshape(1, -1, s.Hkv, s.D)
+        v = rows_np(c["seed"], TAG_V, 0, f, 0, c["file_len"], s.Hkv * s.D).reshape(1, -1, s.Hkv, s.D)
+        o.append(fd, list(range(c["file_len"])), k, v)
+        fds.append(fd)
+        lens.append(c["file_len"])
+    try:
+        from threadpoolctl import threadpool_info
+        blas_threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        blas_threads = None
+    cores = len(os.sched_getaffinity(0))
+    rows = 0
+    steps = 0
+    t0 = time.perf_counter()
+    while steps < steps_cap and (max_steps is not None or time.perf_counter() - t0 < seconds or steps == 0):
+        T = n_sample * c["n_q"]
+        owner = STEP_OWNER + steps
+        q = rows_np(c["seed"], TAG_Q, 0, owner, 0, T, s.Hq * s.D).reshape(1, T, s.Hq, s.D)
+        k = rows_np(c["seed"], TAG_K, 0, owner, 0, T, s.Hkv * s.D).reshape(1, T, s.Hkv, s.D)
+        v = rows_np(c["seed"], TAG_V, 0, owner, 0, T, s.Hkv * s.D).reshape(1, T, s.Hkv, s.D)
+        pos = []
+        for ln in lens:
+            pos.extend(range(ln, ln + c["n_q"]))
+        st, _, _ = o.pred_batch([(fd, c["n_q"]) for fd in fds], pos, q, k, v, s.D ** -0.5)
+        assert all(x == 0 for x in st)
+        lens = [ln + c["n_q"] for ln in lens]
+        rows += T
+        steps += 1
+    el = time.perf_counter() - t0
+    return {"value": rows / el, "unit": "tokens/s", "cores": cores, "blas_threads": blas_threads,
+            "kind": "oracle",
+            "sample": f"{n_sample} of {c['n_files']} LIPs ({c['file_len']}-token files, n_q={c['n_q']}), "
+                      f"{steps} decode preds in {el:.1f} s via oracle.Oracle.pred_batch (numpy fp64)",
+            "steps": steps, "seconds": el}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2510_25412_b200.workloads import CONFIGS
+
+    c = CONFIGS[args.config]
+    # warm-up steps are run untimed, then exactly K timed steps (each a bounded 4-LIP sample)
+    oracle_sample(args.config, 0.0, max_steps=args.warmup, n_sample=4)
+    cb = oracle_sample(args.config, 0.0, max_steps=args.steps, n_sample=4)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * cb["seconds"] / cb["steps"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (counter-based generator, DESIGN.md input recipe)",
+        "config": {"workload": c["workload"], "reference_sample": cb["sample"]},
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------ ours
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_25412_b200 import kvfs as K
+    from paper_2510_25412_b200.workloads import DecodeWorkload
+
+    world, rank, local = dist_env()
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    W, Kst = args.warmup, args.steps
+    n_e2e = 0 if args.no_e2e else Kst
+    wl = DecodeWorkload(args.config, steps_total=W + Kst + n_e2e + 1, device=local)
+    s = wl.shape
+    kv = wl.kv
+    T = wl.n_files * wl.n_q
+    inputs = [wl.make_inputs(i) for i in range(W + Kst)]
+    out = torch.empty((T, s.Hq, s.D), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((T, s.Hq), dtype=torch.float32, device="cuda")
+    descs = np.array([[fd, wl.n_q] for fd in wl.fds], dtype=np.int32)
+    lens = np.array(wl.lens, dtype=np.int64)
+    offs = np.arange(wl.n_q, dtype=np.int64)
+
+    def positions():
+        return (lens[:, None] + offs[None, :]).reshape(-1).astype(np.int32)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    alg_bytes = []
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(Kst)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(Kst)]
+    for i in range(W):
+        q, k, v = inputs[i]
+        st = kv.pred_attn_batch(descs, positions(), q, k, v, out, lse)
+        assert all(x == 0 for x in st), st
+        wl.lens = list(lens + wl.n_q)
+        lens += wl.n_q
+    torch.cuda.synchronize()
+    barrier()
+    launches0 = kv.counter(K.CTR_KERNEL_LAUNCHES)
+    h2d0 = kv.counter(K.CTR_H2D_BYTES)
+    sampler = ClockSampler(local)
+    sampler.start()
+    torch.cuda.synchronize()
+    barrier()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    host_t0 = time.perf_counter()
+    t_start.record()
+    for i in range(Kst):
+        q, k, v = inputs[W + i]
+        wl.lens = lens.tolist()
+        alg_bytes.append(wl.algorithmic_bytes())
+        step, st = kv.pred_step_begin(descs, positions())
+        ev0[i].record()
+        kv.pred_attn_layer(step, 0, q, k, v, out, lse)
+        ev1[i].record()
+        kv.pred_step_end(step)
+        lens += wl.n_q
+    t_end.record()
+    host_s = time.perf_counter() - host_t0
+    torch.cuda.synchronize()
+    barrier()
+    sampler.stop()
+    ms_total = t_start.elapsed_time(t_end)
+    kernel_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    launches = kv.counter(K.CTR_KERNEL_LAUNCHES) - launches0
+    h2d = kv.counter(K.CTR_H2D_BYTES) - h2d0
+    wl.lens = lens.tolist()
+    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / Kst
+    value = world * T * Kst / (ms_max / 1000.0)
+
+    # ---- end to end: host (pinned) inputs -> H2D -> pred through the C ABI -> D2H of out + lse, every step
+    e2e = None
+    if n_e2e:
+        ring = [tuple(x.cpu().pin_memory() for x in inputs[i % len(inputs)]) for i in range(4)]
+        qd, kd, vd = (torch.empty_like(x) for x in inputs[0])
+        out_h = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+        lse_h = torch.empty(lse.shape, dtype=lse.dtype, pin_memory=True)
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(n_e2e):
+            hq, hk, hv = ring[i % 4]
+            qd.copy_(hq, non_blocking=True)
+            kd.copy_(hk, non_blocking=True)
+            vd.copy_(hv, non_blocking=True)
+            kv.pred_attn_batch(descs, positions(), qd, kd, vd, out, lse)
+            out_h.copy_(out, non_blocking=True)
+            lse_h.copy_(lse, non_blocking=True)
+            lens += wl.n_q
+        e1.record()
+        torch.cuda.synchronize()
+        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        h2d_b = sum(x.numel() * x.element_size() for x in ring[0])
+        d2h_b = out_h.numel() * out_h.element_size() + lse_h.numel() * lse_h.element_size()
+        e2e = {"value": world * T * n_e2e / (float(et.item()) / 1000.0), "unit": "tokens/s",
+               "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b, "steps": n_e2e,
+               "note": "pinned host Q/K_new/V_new -> device, pred_attn_batch via the C ABI, out+lse -> pinned host"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = peaks()
+    k_ms = statistics.mean(kernel_ms)
+    achieved = statistics.mean(alg_bytes) / (k_ms / 1000.0) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "decode_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(args.config)
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": Kst, "warmup": W,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (counter-based generator seed %d, DESIGN.md input recipe)" % wl.seed,
+        "config": {"workload": wl.desc, "lips_per_gpu": wl.n_files, "file_len_start": wl.file_len,
+                   "n_q": wl.n_q, "n_q_heads": s.Hq, "n_kv_heads": s.Hkv, "head_dim": s.D, "page_size": s.P,
+                   "layers_per_step": 1, "parallelism": f"dp{world} (LIPs partitioned by process, no collective)",
+                   "l2": "inputs larger than L2 (K/V read per step %.2f GB > 126 MB L2)" % (alg_bytes[0] / 1e9)},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "decode_attn_kernel (K1, fused append + split-KV attention)",
+                     "kernel_ms_mean": k_ms, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": statistics.mean(alg_bytes)},
+        "gpu_launches": launches,
+        "clocks": sampler.summary(),
+        "extra": {"kv_attn_gbs_step": statistics.mean(alg_bytes) / (ms_step / 1000.0) / 1e9,
+                  "tok_s_32_layer_equiv": value / 32.0, "host_s_per_step": host_s / Kst,
+                  "h2d_metadata_bytes_per_step": h2d / Kst,
+                  "decode_ctas": kv.counter(K.CTR_LAST_DECODE_CTAS)},
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = oracle_sample(args.config, args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -35,15 +35,18 @@ struct DecodeCfg {
   static constexpr int CH = DPL / 8;             // 16-byte chunks per lane per row
   static constexpr int SUB = 16;                 // slots per softmax sub-block
   static constexpr int NIT = SUB / KG;           // warp steps per sub-block
-  static constexpr int NW = 7;                   // consumer warps (8 warps total: up to 255 registers)
-  static constexpr int THREADS = (NW + 1) * 32;
   static constexpr int BLOCK_BYTES = P * D * 2;  // one (page, head) block of K or V
   static constexpr int STAGE_BYTES = 2 * BLOCK_BYTES;
   static constexpr int NSTAGES_RAW = 131072 / STAGE_BYTES;
   static constexpr int NSTAGES = NSTAGES_RAW < 4 ? 4 : (NSTAGES_RAW > 16 ? 16 : NSTAGES_RAW);
+  // consumer warps (<= 7: 8 warps in total keep the 255-register budget).  NW <= NSTAGES is required:
+  // a warp never waits on a ring slot more than one phase ahead (mbarrier parity waits are ambiguous
+  // beyond that).
+  static constexpr int NW = NSTAGES < 7 ? NSTAGES : 7;
+  static constexpr int THREADS = (NW + 1) * 32;
   static constexpr int NQ = 4;                   // Q ring slots
   static constexpr int PART = G * (D + 2);       // floats per partial (o, m, l per head)
-  static_assert(LPK * KG == 32 && SUB % KG == 0 && P % SUB == 0, "layout");
+  static_assert(LPK * KG == 32 && SUB % KG == 0 && P % SUB == 0 && NW <= NSTAGES, "layout");
 };
 
 struct StageMeta {

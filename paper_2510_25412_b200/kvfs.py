@@ -235,17 +235,21 @@ class KVFS:
 
     # ------------------------------------------------------------------ pred
     @staticmethod
-    def _descs(descs: Iterable[Tuple[int, int]]):
+    def _descs(descs):
+        """descs: list of (fd, n_q) or an int32 numpy array [n][2] (fast path, no per-item Python work)."""
+        if isinstance(descs, np.ndarray):
+            a = np.ascontiguousarray(descs, dtype=np.int32).reshape(-1, 2)
+            return a.ctypes.data_as(ctypes.POINTER(PredDesc)), a.shape[0], a
         descs = list(descs)
         arr = (PredDesc * max(1, len(descs)))()
         for i, (fd, nq) in enumerate(descs):
             arr[i].fd, arr[i].n_q = fd, nq
-        return arr, len(descs)
+        return arr, len(descs), None
 
     def pred_attn_batch(self, descs, pos, q, k_new, v_new, out, lse=None, scale: Optional[float] = None,
                         stream=None) -> List[int]:
         """Batched pred (one layer). Returns the per-descriptor status list; raises on call-level errors."""
-        arr, n = self._descs(descs)
+        arr, n, _keep = self._descs(descs)
         p = _i32(pos)
         status = (ctypes.c_int * max(1, n))()
         scale = float(scale if scale is not None else self.D ** -0.5)
@@ -256,7 +260,7 @@ class KVFS:
         return list(status[:n])
 
     def pred_step_begin(self, descs, pos, stream=None):
-        arr, n = self._descs(descs)
+        arr, n, _keep = self._descs(descs)
         p = _i32(pos)
         status = (ctypes.c_int * max(1, n))()
         step = ctypes.c_void_p()
