@@ -68,6 +68,18 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
+// Same wait with a suspend-time hint (ns): the waiting thread sleeps in the barrier instead of
+// re-issuing try_wait, which would steal issue slots from the warps sharing its SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAITS_%=;\n\t}" ::"r"(bar),
+      "r"(parity), "r"(1000000)
+      : "memory");
+}
+
 // 1-D TMA: global -> shared, completion counted on an mbarrier (bytes multiple of 16, 16-B aligned).
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar,
                                          uint64_t policy) {

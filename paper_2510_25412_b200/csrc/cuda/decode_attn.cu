@@ -21,6 +21,8 @@
 #include <cuda_bf16.h>
 #include <math_constants.h>
 
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace kvfs {
@@ -37,16 +39,25 @@ struct DecodeCfg {
   static constexpr int NIT = SUB / KG;           // warp steps per sub-block
   static constexpr int BLOCK_BYTES = P * D * 2;  // one (page, head) block of K or V
   static constexpr int STAGE_BYTES = 2 * BLOCK_BYTES;
-  static constexpr int NSTAGES_RAW = 131072 / STAGE_BYTES;
-  static constexpr int NSTAGES = NSTAGES_RAW < 4 ? 4 : (NSTAGES_RAW > 16 ? 16 : NSTAGES_RAW);
-  // consumer warps (<= 7: 8 warps in total keep the 255-register budget).  NW <= NSTAGES is required:
-  // a warp never waits on a ring slot more than one phase ahead (mbarrier parity waits are ambiguous
-  // beyond that).
-  static constexpr int NW = NSTAGES < 7 ? NSTAGES : 7;
-  static constexpr int THREADS = (NW + 1) * 32;
+  // One CTA per SM holding R independent rings; ring = 1 producer warp (1-D TMA) + NW consumer warps.
+  // An SM's TMA bandwidth grows with the number of independent producer streams (tools/bw_probe.cu:
+  // 1 stream/SM ~2.5 TB/s, 3-4 streams/SM ~6.4-6.9 TB/s), so the rings are what feeds HBM; one CTA of
+  // 12 warps lets setmaxnreg move registers from the 4-warp producer warpgroup to the 8 consumers.
+  static constexpr int NSTAGES_RAW = 49152 / STAGE_BYTES;
+  static constexpr int NSTAGES = NSTAGES_RAW < 2 ? 2 : (NSTAGES_RAW > 8 ? 8 : NSTAGES_RAW);
+  // NW <= NSTAGES is required: a warp never waits on a ring slot more than one phase ahead (mbarrier
+  // parity waits are ambiguous beyond that).
+  static constexpr int NW = 2;                   // consumer warps per ring
+  static constexpr int THREADS = 12 * 32;        // producer warpgroup (4 warps) + 2 consumer warpgroups
+  static constexpr int PRODUCER_REGS = 56, CONSUMER_REGS = 224;
   static constexpr int NQ = 4;                   // Q ring slots
   static constexpr int PART = G * (D + 2);       // floats per partial (o, m, l per head)
-  static_assert(LPK * KG == 32 && SUB % KG == 0 && P % SUB == 0 && NW <= NSTAGES, "layout");
+  static constexpr int RING_BYTES_RAW = NSTAGES * STAGE_BYTES + NQ * G * D * 2 + NW * PART * 4 + NSTAGES * 16 +
+                                        (2 * NSTAGES + 2 * NQ) * 8 + 16;
+  static constexpr int RING_BYTES = (RING_BYTES_RAW + 127) / 128 * 128;
+  static constexpr int R_RAW = 232448 / RING_BYTES;  // 227 KB of dynamic shared memory per CTA
+  static constexpr int R = R_RAW > 4 ? 4 : R_RAW;    // rings per CTA
+  static_assert(LPK * KG == 32 && SUB % KG == 0 && P % SUB == 0 && NW <= NSTAGES && NW * R <= 8 && R >= 1, "layout");
 };
 
 struct StageMeta {
@@ -107,7 +118,12 @@ template <class C>
 __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const DecodeParams p) {
   constexpr int D = C::D, G = C::G, P = C::P, NW = C::NW, NSTAGES = C::NSTAGES;
   constexpr int LPK = C::LPK, KG = C::KG, CH = C::CH, DPL = C::DPL, NIT = C::NIT, SUB = C::SUB;
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem_all[];
+  const int warp_all = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool is_producer = warp_all < 4;
+  const int ring = is_producer ? warp_all : (warp_all - 4) / NW;
+  const int warp = is_producer ? NW : (warp_all - 4) % NW;  // consumer index in the ring (NW = producer)
+  uint8_t *smem = smem_all + ring * C::RING_BYTES;
   uint8_t *stage_data = smem;                                                    // [NSTAGES][2][P][D] bf16
   __nv_bfloat16 *qring = reinterpret_cast<__nv_bfloat16 *>(smem + NSTAGES * C::STAGE_BYTES);  // [NQ][G][D]
   float *comb = reinterpret_cast<float *>(qring + C::NQ * G * D);                // [NW][PART]
@@ -115,90 +131,111 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
   uint64_t *bars = reinterpret_cast<uint64_t *>(meta + NSTAGES);                 // full, empty, qfull, qempty
   int *flag = reinterpret_cast<int *>(bars + 2 * NSTAGES + 2 * C::NQ);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cta = blockIdx.x;
-  const int64_t beg = cta_start(cta, p.total, p.ncta), end = cta_start(cta + 1, p.total, p.ncta);
+  const int cta = blockIdx.x * C::R + ring;  // virtual CTA: one contiguous stage range per ring
   auto full_bar = [&](int s) { return smem_u32(bars + s); };
   auto empty_bar = [&](int s) { return smem_u32(bars + NSTAGES + s); };
   auto qfull_bar = [&](int s) { return smem_u32(bars + 2 * NSTAGES + s); };
   auto qempty_bar = [&](int s) { return smem_u32(bars + 2 * NSTAGES + C::NQ + s); };
 
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < C::R) {  // thread r initialises ring r's barriers
+    uint64_t *rb = reinterpret_cast<uint64_t *>(
+        reinterpret_cast<uint8_t *>(bars) + (static_cast<int>(threadIdx.x) - ring) * C::RING_BYTES);
     for (int s = 0; s < NSTAGES; ++s) {
-      mbar_init(full_bar(s), 1);
-      mbar_init(empty_bar(s), 1);
+      mbar_init(smem_u32(rb + s), 1);
+      mbar_init(smem_u32(rb + NSTAGES + s), 1);
     }
     for (int s = 0; s < C::NQ; ++s) {
-      mbar_init(qfull_bar(s), 1);
-      mbar_init(qempty_bar(s), NW);
+      mbar_init(smem_u32(rb + 2 * NSTAGES + s), 1);
+      mbar_init(smem_u32(rb + 2 * NSTAGES + C::NQ + s), NW);
     }
     fence_mbar_init();
   }
   __syncthreads();
-  if (beg >= end) return;
+  const int64_t beg = cta < p.ncta ? cta_start(cta, p.total, p.ncta) : 0;
+  const int64_t end = cta < p.ncta ? cta_start(cta + 1, p.total, p.ncta) : 0;
 
-  if (warp == NW) {
-    // ================================================================ producer (one lane)
-    if (lane != 0) return;
+  if (is_producer) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::PRODUCER_REGS));
+    if (ring >= C::R || beg >= end) return;
+    // ================================================================ producer warp
+    // Lanes prepare up to 32 stages at once (one coalesced load of their page-table entries), then lane 0
+    // issues them in order: wait for the ring slot, publish the stage meta, arm the barrier, 1-D TMA.
     const uint64_t pol = policy_evict_first();
     int64_t x = beg;
     int local = 0, segi = 0;
     while (x < end) {
       const Segment sg = make_segment(p.descs, p.n_desc, x, end, p.Hkv);
       const Desc dd = p.descs[sg.d];
-      // Q rows of this unit -> Q ring
-      {
+      if (lane == 0) {  // Q rows of this unit -> Q ring
         const int qs = segi % C::NQ;
-        if (segi >= C::NQ) mbar_wait(qempty_bar(qs), ((segi / C::NQ) & 1) ^ 1);
+        if (segi >= C::NQ) mbar_wait_sleep(qempty_bar(qs), ((segi / C::NQ) & 1) ^ 1);
         const __nv_bfloat16 *src = p.q + (static_cast<int64_t>(dd.row0 + sg.qi) * p.Hq + sg.g * G) * D;
         mbar_arrive_expect_tx(qfull_bar(qs), G * D * 2);
         bulk_g2s(smem_u32(qring + qs * G * D), src, G * D * 2, qfull_bar(qs), pol);
       }
-      for (int i = 0; i < sg.nst; ++i, ++local) {
-        const int slot = local % NSTAGES;
-        if (local >= NSTAGES) mbar_wait(empty_bar(slot), ((local / NSTAGES) & 1) ^ 1);
-        const int st = sg.st0 + i;
-        const uint32_t kdst = smem_u32(stage_data + slot * C::STAGE_BYTES);
-        const uint32_t vdst = kdst + C::BLOCK_BYTES;
-        StageMeta m;
-        uint32_t bytes = 0;
-        if (st < dd.n_old_entries) {
-          const Entry e = p.slab[dd.slab_off + st];
-          uint64_t mask = e.mask;
-          if (e.lstart + __popcll(mask) > dd.n_old) mask = lowest_bits(mask, dd.n_old - e.lstart);
-          const int lo = __ffsll(static_cast<long long>(mask)) - 1;
-          const int hi = 63 - __clzll(static_cast<long long>(mask));
-          const uint32_t nb = static_cast<uint32_t>(hi - lo + 1) * D * 2;
-          const int64_t off = ((static_cast<int64_t>(e.page) * p.Hkv + sg.g) * P + lo) * D;
-          m.mask = mask;
-          m.kind = 0;
-          m.nrows = 0;
-          meta[slot] = m;
-          bytes = 2 * nb;
-          mbar_arrive_expect_tx(full_bar(slot), bytes);
-          bulk_g2s(kdst + lo * D * 2, p.kpool + off, nb, full_bar(slot), pol);
-          bulk_g2s(vdst + lo * D * 2, p.vpool + off, nb, full_bar(slot), pol);
-        } else {
-          const int v0 = (st - dd.n_old_entries) * P;
-          const int r_end = min(dd.n_q, v0 + P);
-          const int vis_end = min(r_end, sg.qi + 1);  // causal: row qi sees new rows <= qi
-          const int n_vis = vis_end > v0 ? vis_end - v0 : 0;
-          const int n_load = (sg.qi == 0) ? (r_end - v0) : n_vis;  // unit qi=0 also writes the append
-          m.mask = n_vis >= 64 ? ~0ull : ((1ull << n_vis) - 1);
-          m.kind = 1;
-          m.nrows = n_load;
-          meta[slot] = m;
-          bytes = 2u * n_load * D * 2;
-          if (bytes) {
-            mbar_arrive_expect_tx(full_bar(slot), bytes);
-            for (int r = 0; r < n_load; ++r) {
-              const int64_t off = (static_cast<int64_t>(dd.row0 + v0 + r) * p.Hkv + sg.g) * D;
-              bulk_g2s(kdst + r * D * 2, p.k_new + off, D * 2, full_bar(slot), pol);
-              bulk_g2s(vdst + r * D * 2, p.v_new + off, D * 2, full_bar(slot), pol);
-            }
+      for (int base = 0; base < sg.nst; base += 32) {
+        const int n = min(32, sg.nst - base);
+        uint64_t mask = 0;
+        int64_t off = 0;
+        int lo = 0, nrows = 0;
+        const int st = sg.st0 + base + lane;
+        if (lane < n) {
+          if (st < dd.n_old_entries) {
+            const Entry e = p.slab[dd.slab_off + st];
+            mask = e.mask;
+            if (e.lstart + __popcll(mask) > dd.n_old) mask = lowest_bits(mask, dd.n_old - e.lstart);
+            lo = __ffsll(static_cast<long long>(mask)) - 1;
+            const int hi = 63 - __clzll(static_cast<long long>(mask));
+            nrows = hi - lo + 1;
+            off = ((static_cast<int64_t>(e.page) * p.Hkv + sg.g) * P + lo) * D;
           } else {
-            mbar_arrive(full_bar(slot));
+            const int v0 = (st - dd.n_old_entries) * P;
+            const int r_end = min(dd.n_q, v0 + P);
+            const int vis_end = min(r_end, sg.qi + 1);  // causal: row qi sees new rows <= qi
+            const int n_vis = vis_end > v0 ? vis_end - v0 : 0;
+            mask = n_vis >= 64 ? ~0ull : ((1ull << n_vis) - 1);
+            nrows = (sg.qi == 0) ? (r_end - v0) : n_vis;  // unit qi = 0 also writes the append
+            lo = -1;                                        // marks a new-row stage
+            off = static_cast<int64_t>(v0);
           }
+        }
+        for (int j = 0; j < n; ++j, ++local) {
+          const uint64_t mj = __shfl_sync(0xffffffffu, mask, j);
+          const int64_t offj = __shfl_sync(0xffffffffu, off, j);
+          const int loj = __shfl_sync(0xffffffffu, lo, j);
+          const int nrj = __shfl_sync(0xffffffffu, nrows, j);
+          if (lane == 0) {
+            const int slot = local % NSTAGES;
+            if (local >= NSTAGES) mbar_wait_sleep(empty_bar(slot), ((local / NSTAGES) & 1) ^ 1);
+            const uint32_t kdst = smem_u32(stage_data + slot * C::STAGE_BYTES);
+            const uint32_t vdst = kdst + C::BLOCK_BYTES;
+            StageMeta m;
+            m.mask = mj;
+            if (loj >= 0) {
+              m.kind = 0;
+              m.nrows = 0;
+              meta[slot] = m;
+              const uint32_t nb = static_cast<uint32_t>(nrj) * D * 2;
+              mbar_arrive_expect_tx(full_bar(slot), 2 * nb);
+              bulk_g2s(kdst + loj * D * 2, p.kpool + offj, nb, full_bar(slot), pol);
+              bulk_g2s(vdst + loj * D * 2, p.vpool + offj, nb, full_bar(slot), pol);
+            } else {
+              m.kind = 1;
+              m.nrows = nrj;
+              meta[slot] = m;
+              if (nrj) {
+                mbar_arrive_expect_tx(full_bar(slot), 2u * nrj * D * 2);
+                for (int r = 0; r < nrj; ++r) {
+                  const int64_t o = (static_cast<int64_t>(dd.row0 + offj + r) * p.Hkv + sg.g) * D;
+                  bulk_g2s(kdst + r * D * 2, p.k_new + o, D * 2, full_bar(slot), pol);
+                  bulk_g2s(vdst + r * D * 2, p.v_new + o, D * 2, full_bar(slot), pol);
+                }
+              } else {
+                mbar_arrive(full_bar(slot));
+              }
+            }
+          }
+          __syncwarp();
         }
       }
       x += sg.nst;
@@ -207,8 +244,17 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
     return;
   }
 
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::CONSUMER_REGS));
+  if (ring >= C::R || beg >= end) return;
   // ================================================================ consumers
+  // Lane (kg, sub): key group kg = lane / LPK scores key kg of every warp step; sub = lane % LPK owns
+  // dims {(c*LPK + sub)*8 .. +8} for c < CH.  After the transposing xor-reduction of the G partial dot
+  // products, lane holds the full score of head hm = sub / (LPK/G) (its "own" head): exp / max / l are
+  // per own head, then the G probabilities of the key are gathered back with G shuffles for P.V.
+  constexpr int LG = (G == 1) ? 0 : (G == 2 ? 1 : (G == 4 ? 2 : 3));
+  constexpr int SPH = LPK / G;  // lanes per head within a key group
   const int kg = lane / LPK, sub = lane % LPK;
+  const int hm = sub / SPH;
   int64_t x = beg;
   int local0 = 0, segi = 0;
   bool first_seg = true;
@@ -236,14 +282,11 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
       if (lane == 0) mbar_arrive(qempty_bar(qs));
     }
     float2 o2[G][DPL / 2];
-    float m_run[G], l_run[G];
+    float m_own = -CUDART_INF_F, l_own = 0.f;  // running max / sum of the lane's own head
 #pragma unroll
-    for (int h = 0; h < G; ++h) {
-      m_run[h] = -CUDART_INF_F;
-      l_run[h] = 0.f;
+    for (int h = 0; h < G; ++h)
 #pragma unroll
       for (int j = 0; j < DPL / 2; ++j) o2[h][j] = make_float2(0.f, 0.f);
-    }
 
     for (int i = warp; i < sg.nst; i += NW) {
       const int local = local0 + i;
@@ -252,18 +295,16 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
       const StageMeta m = meta[slot];
       const __nv_bfloat16 *ks = reinterpret_cast<const __nv_bfloat16 *>(stage_data + slot * C::STAGE_BYTES);
       const __nv_bfloat16 *vs = ks + P * D;
-#pragma unroll 1
-      for (int sb = 0; sb < P / SUB; ++sb) {
-        const uint32_t sbm = static_cast<uint32_t>(m.mask >> (sb * SUB)) & ((1u << SUB) - 1);
-        if (sbm == 0) continue;  // warp-uniform
-        float s[NIT][G];
-        float smax[G];
-#pragma unroll
-        for (int h = 0; h < G; ++h) smax[h] = -CUDART_INF_F;
+      // one softmax sub-block of SUB slots; FULL = every slot is a visible key (the common case: no
+      // per-key predicates or divergent branches)
+      auto sub_block = [&](auto full_tag, const uint32_t sbm, const int sb) {
+        constexpr bool FULL = decltype(full_tag)::value;
+        float s[NIT];
+        float smax = -CUDART_INF_F;
 #pragma unroll
         for (int it = 0; it < NIT; ++it) {
           const int slot_k = sb * SUB + it * KG + kg;
-          const bool valid = (sbm >> (it * KG + kg)) & 1u;
+          const bool valid = FULL || ((sbm >> (it * KG + kg)) & 1u);
           float2 acc[G];
 #pragma unroll
           for (int h = 0; h < G; ++h) acc[h] = make_float2(0.f, 0.f);
@@ -278,32 +319,40 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
               for (int h = 0; h < G; ++h) fma2(acc[h], q2[h][c * 4 + j], kf);
             }
           }
+          float v[G];
 #pragma unroll
-          for (int h = 0; h < G; ++h) {
-            float v = acc[h].x + acc[h].y;
+          for (int h = 0; h < G; ++h) v[h] = acc[h].x + acc[h].y;
+          // transposing reduction: each level halves the values a lane carries
 #pragma unroll
-            for (int o = LPK / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            s[it][h] = valid ? v : -CUDART_INF_F;
-            smax[h] = fmaxf(smax[h], s[it][h]);
+          for (int lvl = 0, cnt = G; lvl < LG; ++lvl, cnt >>= 1) {
+            const int o = LPK >> (lvl + 1);
+            const bool up = (sub & o) != 0;
+#pragma unroll
+            for (int t = 0; t < cnt / 2; ++t) {
+              const float send = up ? v[t] : v[t + cnt / 2];
+              const float keep = up ? v[t + cnt / 2] : v[t];
+              v[t] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
           }
+          float sc = v[0];
+#pragma unroll
+          for (int o = SPH / 2; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
+          s[it] = FULL ? sc : (valid ? sc : -CUDART_INF_F);
+          smax = fmaxf(smax, s[it]);
         }
-        // sub-block max over the warp's key groups
+        // sub-block max of the own head over the warp's key groups
 #pragma unroll
-        for (int h = 0; h < G; ++h)
-#pragma unroll
-          for (int o = LPK; o < 32; o <<= 1) smax[h] = fmaxf(smax[h], __shfl_xor_sync(0xffffffffu, smax[h], o));
-        // lazy rescale: only when the running max would be exceeded by more than 2^8
-        bool need = false;
-#pragma unroll
-        for (int h = 0; h < G; ++h) need |= smax[h] > m_run[h] + 8.f;
-        if (need) {
+        for (int o = LPK; o < 32; o <<= 1) smax = fmaxf(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+        // lazy rescale: only when some running max would be exceeded by more than 2^8
+        if (__any_sync(0xffffffffu, smax > m_own + 8.f)) {
+          const float mn = fmaxf(m_own, smax);
+          const float a = (m_own == -CUDART_INF_F) ? 0.f : fast_exp2(m_own - mn);
+          m_own = mn;
+          l_own *= a;
 #pragma unroll
           for (int h = 0; h < G; ++h) {
-            const float mn = fmaxf(m_run[h], smax[h]);
-            const float a = (m_run[h] == -CUDART_INF_F) ? 0.f : fast_exp2(m_run[h] - mn);
-            m_run[h] = mn;
-            l_run[h] *= a;
-            const float2 a2 = make_float2(a, a);
+            const float ah = __shfl_sync(0xffffffffu, a, h * SPH);
+            const float2 a2 = make_float2(ah, ah);
 #pragma unroll
             for (int j = 0; j < DPL / 2; ++j) o2[h][j] = mul2(o2[h][j], a2);
           }
@@ -312,13 +361,12 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
 #pragma unroll
         for (int it = 0; it < NIT; ++it) {
           const int slot_k = sb * SUB + it * KG + kg;
-          const bool valid = (sbm >> (it * KG + kg)) & 1u;
+          const bool valid = FULL || ((sbm >> (it * KG + kg)) & 1u);
+          const float pown = FULL ? fast_exp2(s[it] - m_own) : (valid ? fast_exp2(s[it] - m_own) : 0.f);
+          l_own += pown;
           float pw[G];
 #pragma unroll
-          for (int h = 0; h < G; ++h) {
-            pw[h] = valid ? fast_exp2(s[it][h] - m_run[h]) : 0.f;
-            l_run[h] += pw[h];
-          }
+          for (int h = 0; h < G; ++h) pw[h] = __shfl_sync(0xffffffffu, pown, kg * LPK + h * SPH);
           if (valid) {
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
@@ -333,6 +381,12 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
             }
           }
         }
+      };
+#pragma unroll 1
+      for (int sb = 0; sb < P / SUB; ++sb) {
+        const uint32_t sbm = static_cast<uint32_t>(m.mask >> (sb * SUB)) & ((1u << SUB) - 1);
+        if (sbm == (1u << SUB) - 1) sub_block(std::true_type{}, sbm, sb);
+        else if (sbm != 0) sub_block(std::false_type{}, sbm, sb);  // warp-uniform
       }
       // fused append: the new-row stage of unit qi = 0 writes K_new / V_new into the reserved slots
       if (m.kind == 1 && sg.qi == 0) {
@@ -354,16 +408,15 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
 
     // ---- combine the warps' (m, l, O) of this segment
 #pragma unroll
-    for (int h = 0; h < G; ++h) {
+    for (int o = LPK; o < 32; o <<= 1) {
+      l_own += __shfl_xor_sync(0xffffffffu, l_own, o);
 #pragma unroll
-      for (int o = LPK; o < 32; o <<= 1) {
-        l_run[h] += __shfl_xor_sync(0xffffffffu, l_run[h], o);
+      for (int h = 0; h < G; ++h)
 #pragma unroll
         for (int j = 0; j < DPL / 2; ++j) {
           o2[h][j].x += __shfl_xor_sync(0xffffffffu, o2[h][j].x, o);
           o2[h][j].y += __shfl_xor_sync(0xffffffffu, o2[h][j].y, o);
         }
-      }
     }
     float *cw = comb + warp * C::PART;
     if (kg == 0) {
@@ -376,18 +429,15 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
             const int dim = (c * LPK + sub) * 8 + 2 * j;
             *reinterpret_cast<float2 *>(cw + h * (D + 2) + dim) = o2[h][c * 4 + j];
           }
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int h = 0; h < G; ++h) {
-        cw[h * (D + 2) + D] = m_run[h];
-        cw[h * (D + 2) + D + 1] = l_run[h];
+      if (sub % SPH == 0) {
+        cw[hm * (D + 2) + D] = m_own;
+        cw[hm * (D + 2) + D + 1] = l_own;
       }
     }
-    named_bar_sync(1, NW * 32);
+    named_bar_sync(1 + ring, NW * 32);
 
     const bool whole = (sg.st0 == 0) && (sg.nst == sg.spu);
-    const int tid = threadIdx.x;  // 0 .. NW*32-1
+    const int tid = warp * 32 + lane;  // 0 .. NW*32-1 within the ring
     const int unit = dd.unit_base + sg.g * dd.n_q + sg.qi;
     const int64_t row = dd.row0 + sg.qi;
     if (whole) {
@@ -410,7 +460,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
         *reinterpret_cast<__nv_bfloat162 *>(p.out + oidx) = __floats2bfloat162_rn(ox * inv, oy * inv);
         if (dim == 0 && p.lse) p.lse[row * p.Hq + sg.g * G + h] = (M + __log2f(L)) * 0.69314718055994531f;
       }
-      named_bar_sync(1, NW * 32);
+      named_bar_sync(1 + ring, NW * 32);
     } else {
       // partial of this CTA's piece of the unit
       const int which = first_seg ? 0 : 1;
@@ -434,7 +484,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
         part[e] = acc;
       }
       __threadfence();
-      named_bar_sync(1, NW * 32);
+      named_bar_sync(1 + ring, NW * 32);
       if (tid == 0) {
         const int64_t ua = sg.ubeg, ub = sg.ubeg + sg.spu;
         const int c0 = cta_of(ua, p.total, p.ncta), c1 = cta_of(ub - 1, p.total, p.ncta);
@@ -442,7 +492,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
         *flag = (prev == c1 - c0) ? 1 : 0;
         if (prev == c1 - c0) p.counters[unit] = 0;  // self-cleaning for the next launch
       }
-      named_bar_sync(1, NW * 32);
+      named_bar_sync(1 + ring, NW * 32);
       if (*flag) {
         __threadfence();
         const int64_t ua = sg.ubeg, ub = sg.ubeg + sg.spu;
@@ -471,7 +521,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
           if (dim == 0 && p.lse) p.lse[row * p.Hq + sg.g * G + h] = (M + __log2f(L)) * 0.69314718055994531f;
         }
       }
-      named_bar_sync(1, NW * 32);
+      named_bar_sync(1 + ring, NW * 32);
     }
     x += sg.nst;
     local0 += sg.nst;
@@ -482,50 +532,65 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
 
 template <class C>
 static size_t decode_smem_bytes() {
-  return static_cast<size_t>(C::NSTAGES) * C::STAGE_BYTES + C::NQ * C::G * C::D * 2 + C::NW * C::PART * 4 +
-         C::NSTAGES * sizeof(StageMeta) + (2 * C::NSTAGES + 2 * C::NQ) * 8 + 16;
+  static_assert(sizeof(StageMeta) == 16, "StageMeta");
+  return static_cast<size_t>(C::R) * C::RING_BYTES;
 }
 
 template <int D, int G, int P>
-static cudaError_t launch_decode_t(const DecodeParams &p, cudaStream_t s) {
+static cudaError_t launch_decode_t(const DecodeParams &p, cudaStream_t s, int *per_sm) {
   using C = DecodeCfg<D, G, P>;
   const size_t smem = decode_smem_bytes<C>();
-  static bool attr = false;
-  if (!attr) {
+  static int occ = -1;
+  if (occ < 0) {
     cudaError_t e = cudaFuncSetAttribute(decode_attn_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    attr = true;
+    int o = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, decode_attn_kernel<C>, C::THREADS, smem);
+    if (e != cudaSuccess) return e;
+    occ = (o > 0 ? o : 1) * C::R;  // virtual CTAs (rings) per SM
   }
-  decode_attn_kernel<C><<<p.ncta, C::THREADS, smem, s>>>(p);
+  if (per_sm) {
+    *per_sm = occ;
+    return cudaSuccess;
+  }
+  decode_attn_kernel<C><<<(p.ncta + C::R - 1) / C::R, C::THREADS, smem, s>>>(p);
   return cudaGetLastError();
 }
 
 template <int D, int G>
-static cudaError_t launch_decode_p(const DecodeParams &p, int P, cudaStream_t s) {
+static cudaError_t launch_decode_p(const DecodeParams &p, int P, cudaStream_t s, int *per_sm) {
   switch (P) {
-    case 16: return launch_decode_t<D, G, 16>(p, s);
-    case 32: return launch_decode_t<D, G, 32>(p, s);
-    case 64: return launch_decode_t<D, G, 64>(p, s);
+    case 16: return launch_decode_t<D, G, 16>(p, s, per_sm);
+    case 32: return launch_decode_t<D, G, 32>(p, s, per_sm);
+    case 64: return launch_decode_t<D, G, 64>(p, s, per_sm);
     default: return cudaErrorInvalidValue;
   }
 }
 
 template <int D>
-static cudaError_t launch_decode_g(const DecodeParams &p, int G, int P, cudaStream_t s) {
+static cudaError_t launch_decode_g(const DecodeParams &p, int G, int P, cudaStream_t s, int *per_sm) {
   switch (G) {
-    case 1: return launch_decode_p<D, 1>(p, P, s);
-    case 2: return launch_decode_p<D, 2>(p, P, s);
-    case 4: return launch_decode_p<D, 4>(p, P, s);
-    case 8: return launch_decode_p<D, 8>(p, P, s);
+    case 1: return launch_decode_p<D, 1>(p, P, s, per_sm);
+    case 2: return launch_decode_p<D, 2>(p, P, s, per_sm);
+    case 4: return launch_decode_p<D, 4>(p, P, s, per_sm);
+    case 8: return launch_decode_p<D, 8>(p, P, s, per_sm);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_decode(const DecodeParams &p, int D, int G, int P, cudaStream_t s) {
-  if (D == 64) return launch_decode_g<64>(p, G, P, s);
-  if (D == 128) return launch_decode_g<128>(p, G, P, s);
+  if (D == 64) return launch_decode_g<64>(p, G, P, s, nullptr);
+  if (D == 128) return launch_decode_g<128>(p, G, P, s, nullptr);
   return cudaErrorInvalidValue;
+}
+
+int decode_ctas_per_sm(int D, int G, int P) {
+  int o = 1;
+  DecodeParams dummy{};
+  if (D == 64) launch_decode_g<64>(dummy, G, P, nullptr, &o);
+  if (D == 128) launch_decode_g<128>(dummy, G, P, nullptr, &o);
+  return o;
 }
 
 }  // namespace dev

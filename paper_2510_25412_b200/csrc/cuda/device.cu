@@ -263,7 +263,8 @@ class CudaDevice final : public Device {
     p.descs = static_cast<const dev::Desc *>(d_descs_);
     p.n_desc = static_cast<int>(pl.descs.size());
     p.total = pl.total_cost;
-    int64_t ncta = c_.opt_decode_ctas > 0 ? c_.opt_decode_ctas : sms_;
+    if (per_sm_ == 0) per_sm_ = dev::decode_ctas_per_sm(cfg.head_dim, cfg.n_q_heads / cfg.n_kv_heads, cfg.page_size);
+    int64_t ncta = c_.opt_decode_ctas > 0 ? c_.opt_decode_ctas : static_cast<int64_t>(sms_) * per_sm_;
     ncta = std::min<int64_t>(std::min<int64_t>(ncta, kMaxCtas), pl.total_cost);
     p.ncta = static_cast<int>(ncta);
     p.slab = slab_;
@@ -316,7 +317,7 @@ class CudaDevice final : public Device {
   }
 
   void begin_packet() {
-    cur_ = (cur_ + 1) % 2;
+    cur_ = (cur_ + 1) % 4;
     Staging &s = stg_[cur_];
     if (s.pending) {
       cudaEventSynchronize(s.ev);  // the H2D copy that last used this buffer has finished
@@ -389,7 +390,8 @@ class CudaDevice final : public Device {
   float *partials_ = nullptr;
   bf16 **kptrs_ = nullptr, **vptrs_ = nullptr;
   int sms_ = 148;
-  Staging stg_[2];
+  int per_sm_ = 0;
+  Staging stg_[4];
   int cur_ = 0;
   size_t used_ = 0;
   std::vector<Pending> pending_;

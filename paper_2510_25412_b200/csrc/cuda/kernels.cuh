@@ -23,6 +23,8 @@ struct DecodeParams {
 };
 
 cudaError_t launch_decode(const DecodeParams &p, int D, int G, int P, cudaStream_t s);
+// resident decode CTAs per SM for this shape (occupancy query; the default grid is SMs x this)
+int decode_ctas_per_sm(int D, int G, int P);
 
 }  // namespace dev
 }  // namespace kvfs
