@@ -308,11 +308,12 @@ def run_ours(args):
     peak, peak_src = peaks()
     k_ms = statistics.mean(kernel_ms)
     achieved = statistics.mean(alg_bytes) / (k_ms / 1000.0) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "decode_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.config)
+            t = json.load(open(tp)).get(args.config)
+            traffic, traffic_src = t["traffic_bytes_per_launch"], t["source"]
         except Exception:
             traffic = None
     line = {
@@ -325,7 +326,8 @@ def run_ours(args):
                    "layers_per_step": 1, "parallelism": f"dp{world} (LIPs partitioned by process, no collective)",
                    "l2": "inputs larger than L2 (K/V read per step %.2f GB > 126 MB L2)" % (alg_bytes[0] / 1e9)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "decode_attn_kernel (K1, fused append + split-KV attention)",
+                     "traffic": traffic, "traffic_source": traffic_src,
+                     "kernel": "decode_attn_kernel (K1, fused append + split-KV attention)",
                      "kernel_ms_mean": k_ms, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": statistics.mean(alg_bytes)},
         "gpu_launches": launches,
