@@ -99,7 +99,8 @@ typedef struct {
 size_t kvfs_workspace_bytes(const kvfs_config *cfg);
 
 /* Create a ctx over caller-owned pools (all pages free).  Validates shapes; ENOMEM if the workspace is
- * too small; EINVAL for unsupported shapes. */
+ * too small; EINVAL for unsupported shapes.  A device ctx zero-fills the pools once (synchronously), so
+ * every pool slot always holds finite bf16 (the tensor-core kernel multiplies masked keys' V by P = 0). */
 int kvfs_init(const kvfs_config *cfg, kvfs_ctx **out);
 
 /* Synchronises the ctx's last stream use, frees host resources.  Device buffers stay the caller's. */
@@ -206,7 +207,8 @@ int kvfs_audit(kvfs_ctx *ctx);
 /* ---------------------------------------------------------------- knobs and counters */
 typedef enum {
   KVFS_OPT_DECODE_CTAS = 1,     /* grid size of the decode kernel; 0 = auto (SM count x occupancy) */
-  KVFS_OPT_CHUNK_CUTOVER = 2,   /* n_q at or above which the tcgen05 chunk kernel is used; 0 = never */
+  KVFS_OPT_CHUNK_CUTOVER = 2,   /* n_q at or above which the tcgen05 chunk kernel is used (head_dim 128);
+                                   0 = never; default 8 */
   KVFS_OPT_DETERMINISTIC = 3    /* reserved (the kernels are deterministic for a fixed grid) */
 } kvfs_option;
 int kvfs_set_option(kvfs_ctx *ctx, int option, int64_t value);
@@ -215,7 +217,8 @@ typedef enum {
   KVFS_CTR_KERNEL_LAUNCHES = 1, /* CUDA kernels this ctx has launched */
   KVFS_CTR_H2D_BYTES = 2,       /* bytes of host->device metadata uploads */
   KVFS_CTR_PAGE_COPIES = 3,     /* whole-page copies (copy-on-write + fork tails), per page */
-  KVFS_CTR_LAST_DECODE_CTAS = 4 /* grid of the last decode launch */
+  KVFS_CTR_LAST_DECODE_CTAS = 4, /* grid (virtual CTAs = rings) of the last decode launch */
+  KVFS_CTR_LAST_CHUNK_UNITS = 5  /* CTAs of the last tcgen05 chunk launch (0: none) */
 } kvfs_counter;
 int kvfs_get_counter(kvfs_ctx *ctx, int counter, int64_t *value);
 

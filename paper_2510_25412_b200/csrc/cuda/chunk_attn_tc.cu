@@ -1,0 +1,444 @@
+// K2: multi-token (chunked prefill / speculative draft / keystroke re-append) attention on the 5th-gen
+// tensor cores: tcgen05.mma with TMEM accumulators, operands staged by TMA (§4.1 P:215-217;
+// rule R10 of SURVEY.md §8(c): each of the n_q new tokens attends to the file's retained tokens with
+// logical index <= len - n_q + i).
+//
+// Unit = (descriptor, kv head g, M-tile m): 128 query rows R = 128 m + r, row R <-> (qi = R / G, h = R % G),
+// so Q of the unit is a [rows][D] K-major tile loaded by one 4-D TMA box per 64-column half.
+// KV tiles = 128 keys = 128 / P consecutive page entries of the file (K and V blocks of the (page, g) pairs
+// loaded with 2-D TMA boxes of {64 cols, P rows}, 128-byte swizzle); the new tokens were scattered into the
+// pool by scatter_rows_kernel before this launch, so every key is read from the pool.
+//   S  = Q K^T      tcgen05.mma kind::f16, M = 128, N = 128, K = 16 x 8, A = Q (smem, K-major),
+//                   B = K tile (smem, K-major), D = S in TMEM (double-buffered: columns 0 / 128)
+//   softmax         4 warps, thread = row: tcgen05.ld of the S row, masks (retained slots, causality from
+//                   per-column "new-token index" metadata written by the TMA warp), online softmax in the
+//                   log2 domain with lazy rescale of O (tcgen05.ld/st, only when the row max grows > 8),
+//                   P -> bf16 into smem in the 128B-swizzled K-major layout
+//   O += P V        M = 128, N = 128 (D), K = 16 x 8, A = P (smem, K-major), B = V tile (smem, MN-major),
+//                   D = O in TMEM (columns 256..383)
+// Warp roles: 0 = TMA producer, 1 = MMA issuer (one elected lane), 2 = TMEM allocator, 3 = idle,
+// 4..7 = softmax / epilogue warpgroup.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <math_constants.h>
+
+#include "kernels.cuh"
+
+namespace kvfs {
+namespace dev {
+
+namespace tc {
+
+constexpr int BM = 128;   // rows per M-tile
+constexpr int BN = 128;   // keys per KV tile
+constexpr int HD = 128;   // head dim (K2 is specialised for D = 128)
+constexpr int HALF_BYTES = BM * 64 * 2;  // one 64-column half of a [128][64] bf16 SW128 tile = 16 KiB
+constexpr int TILE_BYTES = 2 * HALF_BYTES;  // [128][128] bf16 = 32 KiB
+constexpr int KV_STAGES = 2;
+constexpr int THREADS = 256;
+constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t S_COL0 = 0, O_COL = 256;
+
+// shared memory layout (all tiles 1024-B aligned for the 128B swizzle)
+constexpr int OFF_Q = 0;
+constexpr int OFF_P = OFF_Q + TILE_BYTES;
+constexpr int OFF_K = OFF_P + TILE_BYTES;                  // [KV_STAGES] K tiles
+constexpr int OFF_V = OFF_K + KV_STAGES * TILE_BYTES;      // [KV_STAGES] V tiles
+constexpr int OFF_JCOL = OFF_V + KV_STAGES * TILE_BYTES;   // [KV_STAGES][BN] int32 column metadata
+constexpr int OFF_BAR = OFF_JCOL + KV_STAGES * BN * 4;
+// barriers: q_full, kv_full[S], kv_empty[S], s_full[2], s_empty[2], p_full, o_full
+constexpr int N_BARS = 1 + 2 * KV_STAGES + 2 + 2 + 1 + 1;
+constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
+constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + alignment slack
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // version (Blackwell)
+  d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// kind::f16 instruction descriptor: bf16 x bf16 -> f32, M = 128, N = 128
+__host__ __device__ constexpr uint32_t idesc_bf16(bool b_mn_major) {
+  return (1u << 4)                                  // c_format = F32
+         | (1u << 7)                                // a_format = BF16
+         | (1u << 10)                               // b_format = BF16
+         | (0u << 15)                               // a K-major
+         | ((b_mn_major ? 1u : 0u) << 16)           // b major
+         | ((static_cast<uint32_t>(BN) >> 3) << 17)  // N >> 3
+         | ((static_cast<uint32_t>(BM) >> 4) << 24); // M >> 4
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
+      "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
+      "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
+      "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
+      "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31])));
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint32_t bar,
+                                            uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar), "l"(pol)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+}  // namespace tc
+
+template <int G>
+__global__ void __launch_bounds__(tc::THREADS, 1)
+    chunk_attn_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
+                         const __grid_constant__ CUtensorMap qmap, const ChunkParams p) {
+  using namespace tc;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = smem_u32(smem);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
+  const uint32_t q_full = smem_u32(bars + 0);
+  auto kv_full = [&](int s) { return smem_u32(bars + 1 + s); };
+  auto kv_empty = [&](int s) { return smem_u32(bars + 1 + KV_STAGES + s); };
+  auto s_full = [&](int b) { return smem_u32(bars + 1 + 2 * KV_STAGES + b); };
+  auto s_empty = [&](int b) { return smem_u32(bars + 3 + 2 * KV_STAGES + b); };
+  const uint32_t p_full = smem_u32(bars + 5 + 2 * KV_STAGES);
+  const uint32_t o_full = smem_u32(bars + 6 + 2 * KV_STAGES);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + OFF_TMEM);
+  int32_t *jcol_all = reinterpret_cast<int32_t *>(smem + OFF_JCOL);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const ChunkUnit u = p.units[blockIdx.x];
+  const ChunkDesc cd = p.descs[u.desc];
+  const int epb = BN / p.P;  // page entries per KV tile
+  const int n_tiles = (cd.n_entries + epb - 1) / epb;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < KV_STAGES; ++s) {
+      mbar_init(kv_full(s), 1);
+      mbar_init(kv_empty(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(s_full(b), 1);
+      mbar_init(s_empty(b), 4);  // one arrive per softmax warp
+    }
+    mbar_init(p_full, 4);
+    mbar_init(o_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ================================================================ TMA producer
+    const uint64_t pol = policy_evict_first();
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, TILE_BYTES);
+      const int qrow = cd.row0 + (u.m * BM) / G;
+      tma_load_4d(sbase + OFF_Q, &qmap, 0, 0, u.g, qrow, q_full);
+      tma_load_4d(sbase + OFF_Q + HALF_BYTES, &qmap, 64, 0, u.g, qrow, q_full);
+    }
+    for (int t = 0; t < n_tiles; ++t) {
+      const int s = t % KV_STAGES;
+      if (t >= KV_STAGES) mbar_wait_sleep(kv_empty(s), ((t / KV_STAGES) & 1) ^ 1);
+      // column metadata: j = logical index - n_old for a retained slot (<= qi is visible), INT_MAX otherwise
+      int32_t *jcol = jcol_all + s * BN;
+      for (int c = lane; c < BN; c += 32) {
+        const int e = t * epb + c / p.P, slot = c % p.P;
+        int32_t j = 0x7fffffff;
+        if (e < cd.n_entries) {
+          const Entry en = p.slab[cd.slab_off + e];
+          if ((en.mask >> slot) & 1ull) {
+            const int lg = en.lstart + __popcll(en.mask & ((1ull << slot) - 1ull));
+            j = lg - cd.n_old;
+          }
+        }
+        jcol[c] = j;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_expect_tx(kv_full(s), 2 * TILE_BYTES);
+        for (int i = 0; i < epb; ++i) {
+          const int e = t * epb + i;
+          // rows past the table: an out-of-bounds box (zero-filled by TMA)
+          const int row = e < cd.n_entries ? (static_cast<int>(p.slab[cd.slab_off + e].page) * p.Hkv + u.g) * p.P
+                                           : p.pool_rows;
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t off = h * HALF_BYTES + i * p.P * 128;
+            tma_load_2d(sbase + OFF_K + s * TILE_BYTES + off, &kmap, h * 64, row, kv_full(s), pol);
+            tma_load_2d(sbase + OFF_V + s * TILE_BYTES + off, &vmap, h * 64, row, kv_full(s), pol);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    // ================================================================ MMA issuer
+    constexpr uint32_t ID_S = idesc_bf16(false), ID_O = idesc_bf16(true);
+    mbar_wait(q_full, 0);
+    auto issue_s = [&](int t) {
+      const int s = t % KV_STAGES, b = t & 1;
+      mbar_wait(kv_full(s), (t / KV_STAGES) & 1);
+      if (t >= 2) mbar_wait(s_empty(b), ((t >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t koff = (k >> 2) * HALF_BYTES + (k & 3) * 32;
+          mma_bf16(tmem + S_COL0 + b * BN, umma_desc(sbase + OFF_Q + koff, 16, 1024),
+                   umma_desc(sbase + OFF_K + s * TILE_BYTES + koff, 16, 1024), ID_S, k > 0);
+        }
+        mma_commit(s_full(b));
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    for (int t = 0; t < n_tiles; ++t) {
+      if (t + 1 < n_tiles) issue_s(t + 1);
+      const int s = t % KV_STAGES;
+      mbar_wait(p_full, t & 1);  // softmax wrote P_t (and corrected O)
+      tc_fence_after();
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < BN / 16; ++k) {
+          const uint32_t poff = (k >> 2) * HALF_BYTES + (k & 3) * 32;
+          mma_bf16(tmem + O_COL, umma_desc(sbase + OFF_P + poff, 16, 1024),
+                   umma_desc(sbase + OFF_V + s * TILE_BYTES + k * 2048, HALF_BYTES, 1024), ID_O, (t > 0 || k > 0));
+        }
+        mma_commit(o_full);
+        mma_commit(kv_empty(s));
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    // ================================================================ softmax + epilogue (thread = row)
+    const int wq = warp - 4;                 // TMEM lane quarter
+    const int r = wq * 32 + lane;            // row within the M-tile
+    const int R = u.m * BM + r;
+    const int qi = R / G, h = R % G;
+    const bool live = qi < cd.n_q;
+    const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
+    float m_run = -CUDART_INF_F, l_run = 0.f;
+    uint8_t *prow = smem + OFF_P + r * 128;  // row r of both 64-column halves (+HALF_BYTES)
+    for (int t = 0; t < n_tiles; ++t) {
+      const int b = t & 1, s = t % KV_STAGES;
+      mbar_wait(s_full(b), (t >> 1) & 1);
+      tc_fence_after();
+      float x[BN];
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        tmem_ld32(tmem + lane_addr + S_COL0 + b * BN + c * 32, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[c * 32 + i] = v[i];
+      }
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_empty(b));
+      const int32_t *jcol = jcol_all + s * BN;
+      float mx = -CUDART_INF_F;
+#pragma unroll
+      for (int c = 0; c < BN; ++c) {
+        const float v = (jcol[c] <= qi) ? x[c] * p.scale_log2 : -CUDART_INF_F;
+        x[c] = v;
+        mx = fmaxf(mx, v);
+      }
+      // P_{t-1}.V must be complete before O is corrected and P is overwritten
+      if (t > 0) mbar_wait(o_full, (t - 1) & 1);
+      tc_fence_after();
+      const bool need = mx > m_run + 8.f;
+      if (__any_sync(0xffffffffu, need)) {
+        const float mn = need ? mx : m_run;
+        const float a = (need && m_run != -CUDART_INF_F) ? fast_exp2(m_run - mn) : (need ? 0.f : 1.f);
+        if (t > 0) {
+#pragma unroll
+          for (int c = 0; c < HD / 32; ++c) {
+            float v[32];
+            tmem_ld32(tmem + lane_addr + O_COL + c * 32, v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] *= a;
+            tmem_st32(tmem + lane_addr + O_COL + c * 32, v);
+          }
+          tmem_wait_st();
+        }
+        l_run *= a;
+        m_run = mn;
+      }
+      // P = exp2(x - m) -> bf16, 128B-swizzled K-major rows
+      float ls = 0.f;
+#pragma unroll
+      for (int c8 = 0; c8 < BN / 8; ++c8) {
+        uint32_t w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float p0 = fast_exp2(x[c8 * 8 + 2 * i] - m_run);
+          const float p1 = fast_exp2(x[c8 * 8 + 2 * i + 1] - m_run);
+          ls += p0 + p1;
+          __nv_bfloat162 pr = __floats2bfloat162_rn(p0, p1);
+          w[i] = *reinterpret_cast<uint32_t *>(&pr);
+        }
+        const int half = c8 >> 3, chunk = c8 & 7;
+        uint4 *dst = reinterpret_cast<uint4 *>(prow + half * HALF_BYTES + ((chunk ^ (r & 7)) << 4));
+        *dst = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      l_run += ls;
+      fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core (async proxy)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    // epilogue: O / l -> bf16 out, lse
+    mbar_wait(o_full, (n_tiles - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l_run;
+    const int64_t orow = (static_cast<int64_t>(cd.row0 + qi) * p.Hq + u.g * G + h) * HD;
+#pragma unroll
+    for (int c = 0; c < HD / 32; ++c) {
+      float v[32];
+      tmem_ld32(tmem + lane_addr + O_COL + c * 32, v);
+      tmem_wait_ld();
+      if (live) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint32_t w[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            __nv_bfloat162 pr = __floats2bfloat162_rn(v[i + 2 * j] * inv, v[i + 2 * j + 1] * inv);
+            w[j] = *reinterpret_cast<uint32_t *>(&pr);
+          }
+          *reinterpret_cast<uint4 *>(p.out + orow + c * 32 + i) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+    }
+    if (live && p.lse) p.lse[static_cast<int64_t>(cd.row0 + qi) * p.Hq + u.g * G + h] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// Scatter the new rows of the chunk descriptors into their reserved pool slots (K and V of one layer).
+__global__ void scatter_rows_kernel(const int32_t *dst, int T, const __nv_bfloat16 *k, const __nv_bfloat16 *v,
+                                    __nv_bfloat16 *kp, __nv_bfloat16 *vp, int Hkv, int D, int P) {
+  const int cpr = D / 8;
+  const int64_t total = static_cast<int64_t>(T) * Hkv * cpr;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int c = static_cast<int>(idx % cpr);
+    const int64_t t = idx / cpr;
+    const int g = static_cast<int>(t % Hkv);
+    const int r = static_cast<int>(t / Hkv);
+    const int32_t ds = dst[r];
+    if (ds < 0) continue;
+    const int64_t so = (static_cast<int64_t>(r) * Hkv + g) * D + c * 8;
+    const int64_t po = ((static_cast<int64_t>(ds / P) * Hkv + g) * P + ds % P) * D + c * 8;
+    *reinterpret_cast<uint4 *>(kp + po) = *reinterpret_cast<const uint4 *>(k + so);
+    *reinterpret_cast<uint4 *>(vp + po) = *reinterpret_cast<const uint4 *>(v + so);
+  }
+}
+
+cudaError_t launch_scatter_rows(const int32_t *dst, int T, const __nv_bfloat16 *k, const __nv_bfloat16 *v,
+                                __nv_bfloat16 *kp, __nv_bfloat16 *vp, int Hkv, int D, int P, int sms,
+                                cudaStream_t s) {
+  const int64_t total = static_cast<int64_t>(T) * Hkv * (D / 8);
+  const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, static_cast<int64_t>(sms) * 16));
+  if (grid <= 0) return cudaSuccess;
+  scatter_rows_kernel<<<grid, 256, 0, s>>>(dst, T, k, v, kp, vp, Hkv, D, P);
+  return cudaGetLastError();
+}
+
+int chunk_smem_bytes() { return tc::SMEM_BYTES; }
+
+template <int G>
+static cudaError_t launch_chunk_g(const CUtensorMap &km, const CUtensorMap &vm, const CUtensorMap &qm,
+                                  const ChunkParams &p, int n_units, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(chunk_attn_tc_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         tc::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  chunk_attn_tc_kernel<G><<<n_units, tc::THREADS, tc::SMEM_BYTES, s>>>(km, vm, qm, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chunk(const CUtensorMap &km, const CUtensorMap &vm, const CUtensorMap &qm, const ChunkParams &p,
+                         int n_units, int G, cudaStream_t s) {
+  switch (G) {
+    case 1: return launch_chunk_g<1>(km, vm, qm, p, n_units, s);
+    case 2: return launch_chunk_g<2>(km, vm, qm, p, n_units, s);
+    case 4: return launch_chunk_g<4>(km, vm, qm, p, n_units, s);
+    case 8: return launch_chunk_g<8>(km, vm, qm, p, n_units, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace dev
+}  // namespace kvfs

@@ -2,7 +2,9 @@
 // call), and the bandwidth-bound copy kernels (K4 copy-on-write / fork tail page copy, K5 evict-compact
 // gather, K7 dense read-back, the kvfs_append scatter, the table-delta scatter).  The attention kernel
 // lives in decode_attn.cu.
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cstring>
@@ -174,6 +176,26 @@ class CudaDevice final : public Device {
       return KVFS_EIO;
     if (cudaMemset(counters_, 0, static_cast<size_t>(cfg.max_batch_rows) * cfg.n_kv_heads * 4) != cudaSuccess)
       return KVFS_EIO;
+    // Zero-fill the pools once: every slot then always holds finite bf16 (only finite rows are ever
+    // written), so the tensor-core kernel can multiply masked-out keys' V rows by P = 0 safely.
+    const size_t pool_bytes = static_cast<size_t>(cfg.n_pages) * cfg.n_kv_heads * cfg.page_size * cfg.head_dim * 2;
+    for (int l = 0; l < cfg.n_layers; ++l) {
+      if (cudaMemset(c_.kpool[l], 0, pool_bytes) != cudaSuccess) return KVFS_EIO;
+      if (cudaMemset(c_.vpool[l], 0, pool_bytes) != cudaSuccess) return KVFS_EIO;
+    }
+    if (cfg.head_dim == 128) {
+      void *fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess || !fn)
+        return KVFS_EIO;
+      encode_ = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+      kmaps_.resize(cfg.n_layers);
+      vmaps_.resize(cfg.n_layers);
+      for (int l = 0; l < cfg.n_layers; ++l) {
+        if (!pool_map(c_.kpool[l], &kmaps_[l]) || !pool_map(c_.vpool[l], &vmaps_[l])) return KVFS_EIO;
+      }
+    }
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device);
     sms_ = sms > 0 ? sms : 148;
@@ -247,7 +269,11 @@ class CudaDevice final : public Device {
     d_copies_ = push(pl.copies.data(), pl.copies.size() * sizeof(PageCopy));
     d_descs_ = push(pl.descs.data(), pl.descs.size() * sizeof(DevDesc));
     d_dst_ = push(pl.dst_slot.data(), pl.dst_slot.size() * sizeof(int32_t));
-    if (!d_runs_ || !d_run_entries_ || !d_copies_ || !d_descs_ || !d_dst_) return KVFS_ENOMEM;
+    d_cdescs_ = push(pl.chunk_descs.data(), pl.chunk_descs.size() * sizeof(ChunkDesc));
+    d_cunits_ = push(pl.chunk_units.data(), pl.chunk_units.size() * sizeof(ChunkUnit));
+    d_cdst_ = push(pl.chunk_dst.data(), pl.chunk_dst.size() * sizeof(int32_t));
+    if (!d_runs_ || !d_run_entries_ || !d_copies_ || !d_descs_ || !d_dst_ || !d_cdescs_ || !d_cunits_ || !d_cdst_)
+      return KVFS_ENOMEM;
     if (!send(s)) return KVFS_EIO;
     if (pl.runs.empty() && pl.copies.empty()) return KVFS_OK;
     return launch_prologue(static_cast<const dev::SlabRun *>(d_runs_), static_cast<int>(pl.runs.size()),
@@ -257,6 +283,11 @@ class CudaDevice final : public Device {
 
   int pred_layer(const PredPlan &pl, int layer, const void *q, const void *k_new, const void *v_new, void *out,
                  float *lse, float scale, kvfs_stream_t s) override {
+    c_.ctr.last_chunk_units = static_cast<int64_t>(pl.chunk_units.size());
+    if (!pl.chunk_units.empty()) {
+      const int rc = chunk_layer(pl, layer, q, k_new, v_new, out, lse, scale, s);
+      if (rc != KVFS_OK) return rc;
+    }
     if (pl.descs.empty()) return KVFS_OK;
     const kvfs_config &cfg = c_.cfg;
     dev::DecodeParams p{};
@@ -288,6 +319,47 @@ class CudaDevice final : public Device {
   }
 
   int sync() override { return cudaDeviceSynchronize() == cudaSuccess ? KVFS_OK : KVFS_EIO; }
+
+  // K2: scatter the chunk descriptors' new rows into the pool, then tcgen05 attention from the pool.
+  int chunk_layer(const PredPlan &pl, int layer, const void *q, const void *k_new, const void *v_new, void *out,
+                  float *lse, float scale, kvfs_stream_t s) {
+    const kvfs_config &cfg = c_.cfg;
+    cudaError_t e = dev::launch_scatter_rows(static_cast<const int32_t *>(d_cdst_), pl.T,
+                                             static_cast<const bf16 *>(k_new), static_cast<const bf16 *>(v_new),
+                                             static_cast<bf16 *>(c_.kpool[layer]), static_cast<bf16 *>(c_.vpool[layer]),
+                                             cfg.n_kv_heads, cfg.head_dim, cfg.page_size, sms_, cs(s));
+    ++c_.ctr.launches;
+    if (e != cudaSuccess) return KVFS_EIO;
+    const int G = cfg.n_q_heads / cfg.n_kv_heads;
+    alignas(64) CUtensorMap qmap;
+    {
+      const cuuint64_t dims[4] = {static_cast<cuuint64_t>(cfg.head_dim), static_cast<cuuint64_t>(G),
+                                  static_cast<cuuint64_t>(cfg.n_kv_heads), static_cast<cuuint64_t>(pl.T)};
+      const cuuint64_t strides[3] = {static_cast<cuuint64_t>(cfg.head_dim) * 2,
+                                     static_cast<cuuint64_t>(G) * cfg.head_dim * 2,
+                                     static_cast<cuuint64_t>(cfg.n_q_heads) * cfg.head_dim * 2};
+      const cuuint32_t box[4] = {64, static_cast<cuuint32_t>(G), 1, static_cast<cuuint32_t>(128 / G)};
+      const cuuint32_t es[4] = {1, 1, 1, 1};
+      if (encode_(&qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(q), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return KVFS_EINVAL;
+    }
+    dev::ChunkParams p{};
+    p.units = static_cast<const dev::ChunkUnit *>(d_cunits_);
+    p.descs = static_cast<const dev::ChunkDesc *>(d_cdescs_);
+    p.slab = slab_;
+    p.out = static_cast<bf16 *>(out);
+    p.lse = lse;
+    p.scale_log2 = scale * 1.4426950408889634f;
+    p.P = cfg.page_size;
+    p.Hkv = cfg.n_kv_heads;
+    p.Hq = cfg.n_q_heads;
+    p.pool_rows = static_cast<int>(cfg.n_pages * cfg.n_kv_heads * cfg.page_size);
+    e = dev::launch_chunk(kmaps_[layer], vmaps_[layer], qmap, p, static_cast<int>(pl.chunk_units.size()), G, cs(s));
+    ++c_.ctr.launches;
+    return e == cudaSuccess ? KVFS_OK : KVFS_EIO;
+  }
 
  private:
   struct Staging {
@@ -377,6 +449,18 @@ class CudaDevice final : public Device {
     return cudaGetLastError() == cudaSuccess ? KVFS_OK : KVFS_EIO;
   }
 
+  bool pool_map(void *pool, CUtensorMap *m) {
+    const kvfs_config &cfg = c_.cfg;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cfg.head_dim),
+                                static_cast<cuuint64_t>(cfg.n_pages) * cfg.n_kv_heads * cfg.page_size};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cfg.head_dim) * 2};
+    const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(cfg.page_size)};
+    const cuuint32_t es[2] = {1, 1};
+    return encode_(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, pool, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+
   struct Pending {
     const void *data;
     size_t bytes, off;
@@ -396,7 +480,9 @@ class CudaDevice final : public Device {
   size_t used_ = 0;
   std::vector<Pending> pending_;
   const void *d_runs_ = nullptr, *d_run_entries_ = nullptr, *d_copies_ = nullptr, *d_descs_ = nullptr,
-             *d_dst_ = nullptr;
+             *d_dst_ = nullptr, *d_cdescs_ = nullptr, *d_cunits_ = nullptr, *d_cdst_ = nullptr;
+  PFN_cuTensorMapEncodeTiled_v12000 encode_ = nullptr;
+  std::vector<CUtensorMap> kmaps_, vmaps_;
 };
 
 }  // namespace

@@ -1,5 +1,7 @@
 // Kernel parameter blocks and launchers shared by csrc/cuda/*.cu.
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace kvfs {
@@ -23,6 +25,29 @@ struct DecodeParams {
 };
 
 cudaError_t launch_decode(const DecodeParams &p, int D, int G, int P, cudaStream_t s);
+// ---- K2 (tcgen05 chunk attention, D = 128)
+struct ChunkDesc {  // == kvfs::ChunkDesc
+  int32_t slab_off, n_entries, n_old, n_q, row0, pad;
+};
+struct ChunkUnit {  // == kvfs::ChunkUnit
+  int32_t desc, g, m, pad;
+};
+struct ChunkParams {
+  const ChunkUnit *units;
+  const ChunkDesc *descs;
+  const Entry *slab;
+  __nv_bfloat16 *out;
+  float *lse;
+  float scale_log2;
+  int P, Hkv, Hq;
+  int pool_rows;  // n_pages * Hkv * P: a row coordinate out of the pool tensor (zero-filled TMA box)
+};
+cudaError_t launch_chunk(const CUtensorMap &km, const CUtensorMap &vm, const CUtensorMap &qm, const ChunkParams &p,
+                         int n_units, int G, cudaStream_t s);
+cudaError_t launch_scatter_rows(const int32_t *dst, int T, const __nv_bfloat16 *k, const __nv_bfloat16 *v,
+                                __nv_bfloat16 *kp, __nv_bfloat16 *vp, int Hkv, int D, int P, int sms, cudaStream_t s);
+int chunk_smem_bytes();
+
 // resident decode CTAs per SM for this shape (occupancy query; the default grid is SMs x this)
 int decode_ctas_per_sm(int D, int G, int P);
 

@@ -32,6 +32,9 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
   pl.max_nq = 0;
   const int64_t tag = ++c.batch_counter;
 
+  pl.chunk_descs.clear();
+  pl.chunk_units.clear();
+  pl.chunk_dst.clear();
   std::vector<int32_t> dst;
   int64_t row = 0;
   bool partial = false;
@@ -74,6 +77,7 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
           int64_t idx = static_cast<int64_t>(f->table.size()) - 1;
           while (idx >= 0 && f->table[idx].lstart >= n_old) --idx;
           DevDesc d{};
+          d.pad0 = static_cast<int32_t>(f->table.size());  // entries after the append (used by K2)
           d.cost_begin = pl.total_cost;
           d.slab_off = static_cast<int32_t>(f->slab_off);
           d.n_old_entries = static_cast<int32_t>(idx + 1);
@@ -102,6 +106,42 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
   }
   c.ctr.page_copies += static_cast<int64_t>(pl.copies.size());
   return partial ? KVFS_EPARTIAL : KVFS_OK;
+}
+
+}  // namespace kvfs
+
+namespace kvfs {
+
+void pred_split(const Ctx &c, int64_t cutover, PredPlan *plan) {
+  PredPlan &pl = *plan;
+  if (cutover <= 0 || c.cfg.head_dim != 128) return;
+  const int P = c.cfg.page_size, Hkv = c.cfg.n_kv_heads, G = c.cfg.n_q_heads / c.cfg.n_kv_heads;
+  std::vector<DevDesc> keep;
+  int64_t cost = 0;
+  int32_t units = 0;
+  for (const DevDesc &d : pl.descs) {
+    if (d.n_q >= cutover) {
+      if (pl.chunk_dst.empty()) pl.chunk_dst.assign(static_cast<size_t>(pl.T), -1);
+      ChunkDesc cd{d.slab_off, d.pad0, d.n_old, d.n_q, d.row0, 0};
+      const int32_t di = static_cast<int32_t>(pl.chunk_descs.size());
+      pl.chunk_descs.push_back(cd);
+      const int mt = (d.n_q * G + 127) / 128;
+      for (int g = 0; g < Hkv; ++g)
+        for (int m = 0; m < mt; ++m) pl.chunk_units.push_back({di, g, m, 0});
+      for (int r = 0; r < d.n_q; ++r) pl.chunk_dst[d.row0 + r] = pl.dst_slot[d.row0 + r];
+      continue;
+    }
+    DevDesc k = d;
+    k.cost_begin = cost;
+    k.unit_base = units;
+    cost += static_cast<int64_t>(Hkv) * d.n_q * d.stages_per_unit;
+    units += Hkv * d.n_q;
+    keep.push_back(k);
+  }
+  (void)P;
+  pl.descs.swap(keep);
+  pl.total_cost = cost;
+  pl.n_units = units;
 }
 
 }  // namespace kvfs

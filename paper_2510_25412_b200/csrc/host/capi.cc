@@ -229,6 +229,7 @@ int pred_step_begin(kvfs_ctx *ctx, const pred_desc *descs, int n_desc, const int
   if (c.dev && c.poisoned) return KVFS_EIO;
   const int rc = pred_reserve(c, descs, n_desc, pos, status, &c.plan);
   if (rc != KVFS_OK && rc != KVFS_EPARTIAL) return rc;
+  if (c.dev) pred_split(c, c.opt_chunk_cutover, &c.plan);
   if (c.dev) {
     const int drc = c.dev->pred_begin(c.plan, stream);
     if (drc != KVFS_OK) {
@@ -388,6 +389,7 @@ int kvfs_get_counter(kvfs_ctx *ctx, int counter, int64_t *value) {
     case KVFS_CTR_H2D_BYTES: *value = c.ctr.h2d_bytes; return KVFS_OK;
     case KVFS_CTR_PAGE_COPIES: *value = c.ctr.page_copies; return KVFS_OK;
     case KVFS_CTR_LAST_DECODE_CTAS: *value = c.ctr.last_decode_ctas; return KVFS_OK;
+    case KVFS_CTR_LAST_CHUNK_UNITS: *value = c.ctr.last_chunk_units; return KVFS_OK;
     default: return KVFS_EINVAL;
   }
 }

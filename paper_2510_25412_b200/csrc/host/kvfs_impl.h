@@ -76,6 +76,14 @@ struct SlabRun {
 };
 static_assert(sizeof(SlabRun) == 16, "SlabRun must be 16 bytes");
 
+// K2 (tcgen05 chunk kernel) records (layouts shared with csrc/cuda/kernels.cuh)
+struct ChunkDesc {
+  int32_t slab_off, n_entries, n_old, n_q, row0, pad;
+};
+struct ChunkUnit {
+  int32_t desc, g, m, pad;
+};
+
 struct PredPlan {
   std::vector<DevDesc> descs;       // successful descriptors with n_q > 0, in order
   std::vector<int32_t> dst_slot;    // [T] page * P + slot of every appended row (-1: row not appended)
@@ -86,12 +94,16 @@ struct PredPlan {
   int32_t n_units = 0;
   int32_t T = 0;
   int32_t max_nq = 0;
+  // split by n_q (pred_split): descriptors with n_q >= cutover go to K2
+  std::vector<ChunkDesc> chunk_descs;
+  std::vector<ChunkUnit> chunk_units;
+  std::vector<int32_t> chunk_dst;  // [T] dst slot of rows of K2 descriptors, -1 otherwise
 };
 
 class Device;  // data plane (csrc/cuda), absent for a host-only ctx
 
 struct CtxCounters {
-  int64_t launches = 0, h2d_bytes = 0, page_copies = 0, last_decode_ctas = 0;
+  int64_t launches = 0, h2d_bytes = 0, page_copies = 0, last_decode_ctas = 0, last_chunk_units = 0;
 };
 
 struct Ctx {
@@ -107,7 +119,7 @@ struct Ctx {
   bool step_open = false;
   int64_t batch_counter = 0;
   int64_t opt_decode_ctas = 0;
-  int64_t opt_chunk_cutover = 0;
+  int64_t opt_chunk_cutover = 8;
   CtxCounters ctr;
   PredPlan plan;  // the open step's plan
   std::vector<int> step_status;
@@ -133,6 +145,8 @@ int audit(Ctx &c);
 
 // ---- batched pred (batch.cc)
 int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos, int *status, PredPlan *plan);
+// Move descriptors with n_q >= cutover (0: none) from the K1 list to the K2 list (D = 128 only).
+void pred_split(const Ctx &c, int64_t cutover, PredPlan *plan);
 
 // ---- data plane interface (implemented in csrc/cuda/device.cu)
 class Device {

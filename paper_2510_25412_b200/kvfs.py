@@ -22,7 +22,7 @@ EPOS, EPARTIAL = -1001, -1002
 O_CREAT, O_EXCL = 1, 2
 EVICT_COMPACT = 1
 OPT_DECODE_CTAS, OPT_CHUNK_CUTOVER, OPT_DETERMINISTIC = 1, 2, 3
-CTR_KERNEL_LAUNCHES, CTR_H2D_BYTES, CTR_PAGE_COPIES, CTR_LAST_DECODE_CTAS = 1, 2, 3, 4
+CTR_KERNEL_LAUNCHES, CTR_H2D_BYTES, CTR_PAGE_COPIES, CTR_LAST_DECODE_CTAS, CTR_LAST_CHUNK_UNITS = 1, 2, 3, 4, 5
 
 # every symbol include/kvfs.h declares (tests check the library exports all of them)
 EXPORTS = [

@@ -176,3 +176,60 @@ def test_partial_batch_and_edge_cases():
     assert st == []
     h.check_meta()
     h.check_data()
+
+
+@pytest.mark.parametrize("P,Hq,Hkv", [(16, 32, 8), (16, 8, 8), (32, 16, 8), (64, 16, 2), (16, 16, 8)])
+def test_chunk_tcgen05_kernel(P, Hq, Hkv):
+    """K2 (tcgen05) for descriptors with n_q >= cutover, mixed with K1 rows in the same batch; holes from
+    eviction, truncation + re-append (autocompletion), a fresh file, several 128-row M-tiles."""
+    D = 128
+    h = Harness(3000, P, Hq, Hkv, D, seed=P + Hq + 7)
+    h.c.set_option(2, 8)  # KVFS_OPT_CHUNK_CUTOVER (the default)
+    lens = [300, 1000, 77, 513, 0, 2048]
+    for i, n in enumerate(lens):
+        h.open(f"f{i}")
+        if n:
+            h.append(f"f{i}", list(range(n)))
+    h.evict("f1", [(10, 200), (500, 517)])
+    h.truncate("f5", 2000)
+    rows = []
+    for i, nq in enumerate([64, 17, 8, 100, 40, 48]):
+        last = h.o.stat(h.fds[f"f{i}"][1])[2]
+        rows.append((f"f{i}", list(range(last + 1, last + 1 + nq))))
+    rows.append(("f0", [999]))  # EBUSY: repeated file
+    h.open("d")
+    h.append("d", list(range(50)))
+    rows.append(("d", [50, 51]))  # K1 row in the same batch
+    st, *_ = h.pred(rows, qstd=4.0)
+    assert st[:6] == [0] * 6 and st[6] == -16 and st[7] == 0
+    G = Hq // Hkv
+    assert h.c.counter(5) == Hkv * sum((nq * G + 127) // 128 for nq in [64, 17, 8, 100, 40, 48])  # K2 CTAs
+    # second step: decode + another chunk on the grown files
+    rows = []
+    for i, nq in enumerate([1, 64, 1, 16, 3, 64]):
+        last = h.o.stat(h.fds[f"f{i}"][1])[2]
+        rows.append((f"f{i}", list(range(last + 1, last + 1 + nq))))
+    h.pred(rows)
+    h.check_meta()
+    h.check_data()
+
+
+def test_chunk_autocompletion_shape():
+    """Config-4 shape in miniature: 8 LIPs x 1024 tokens, truncate-to-cursor then a 64-token re-append."""
+    h = Harness(1200, 16, 32, 8, 128, seed=1004)
+    h.c.set_option(2, 8)
+    for i in range(8):
+        h.open(f"f{i}")
+        h.append(f"f{i}", list(range(1024)))
+    import random as _r
+    rnd = _r.Random(1004)
+    for step in range(3):
+        rows = []
+        for i in range(8):
+            r = rnd.randint(1, 64) if step else 64
+            n = h.o.stat(h.fds[f"f{i}"][1])[0]
+            h.truncate(f"f{i}", n - r)
+            last = h.o.stat(h.fds[f"f{i}"][1])[2]
+            rows.append((f"f{i}", list(range(last + 1, last + 65))))
+        h.pred(rows, qstd=1.0)
+    h.check_meta()
