@@ -33,7 +33,11 @@ CONFIGS: Dict[str, dict] = {
     # BASELINE.json configs[1]: Llama-3-8B attention shape, 256 LIPs decoding from 2k-token files
     "cfg2": dict(workload="cfg2: Llama-3-8B attn (32q/8kv, hd128, bf16, P=16), 256 LIPs decode (n_q=1) "
                           "from 2048-token KVFS files, 1 layer per step",
-                 shape=Shape(32, 8, 128, 16), n_files=256, file_len=2048, n_q=1, seed=1002),
+                 shape=Shape(32, 8, 128, 16), n_files=256, file_len=2048, n_q=1, seed=1002, rewind=0),
+    # BASELINE.json configs[3]: live code autocompletion, truncate-to-cursor (r = 64) + 64-token re-append
+    "cfg4": dict(workload="cfg4: autocompletion, 128 LIPs x 8192-token files (32q/8kv, hd128, P=16); each step "
+                          "truncates every file to 8192-64 and re-appends 64 tokens (n_q=64, tcgen05 chunk kernel)",
+                 shape=Shape(32, 8, 128, 16), n_files=128, file_len=8192, n_q=64, seed=1004, rewind=64),
 }
 
 
@@ -50,10 +54,12 @@ class DecodeWorkload:
         self.n_files = n_files or c["n_files"]
         self.file_len = c["file_len"]
         self.n_q = c["n_q"]
+        self.rewind = c.get("rewind", 0)  # truncate-to-cursor before every step (autocompletion)
         self.steps_total = steps_total
         s = self.shape
         self.dev = torch.device("cuda", device)
-        per_file = math.ceil((self.file_len + steps_total * self.n_q + s.P) / s.P) + 1
+        grow = 0 if self.rewind else steps_total * self.n_q
+        per_file = math.ceil((self.file_len + grow + s.P) / s.P) + 1
         self.n_pages = self.n_files * per_file + 64
         rows = self.n_files * self.n_q
         self.kv = KVFS(1, s.Hq, s.Hkv, s.D, s.P, self.n_pages, max_batch_rows=max(rows, 16),
@@ -82,6 +88,13 @@ class DecodeWorkload:
         v = rows_torch(self.seed, TAG_V, 0, owner, 0, T, s.Hkv * s.D, device=self.dev).view(T, s.Hkv, s.D)
         return q, k, v
 
+    def pre_step(self) -> None:
+        """Host-side LIP policy before a step: truncate-to-cursor for the autocompletion workload."""
+        if self.rewind:
+            for i, fd in enumerate(self.fds):
+                self.lens[i] -= self.rewind
+                self.kv.truncate(fd, self.lens[i])
+
     def descs_and_pos(self) -> Tuple[List[Tuple[int, int]], List[int]]:
         descs, pos = [], []
         for fd, ln in zip(self.fds, self.lens):
@@ -108,8 +121,9 @@ class DecodeWorkload:
 
     def flops(self) -> int:
         s = self.shape
-        tot = 0
-        for ln in self.lens:
-            for i in range(self.n_q):
-                tot += 4 * s.Hq * s.D * (ln + i + 1)
-        return tot
+        n = self.n_q
+        return sum(4 * s.Hq * s.D * (n * ln + n * (n + 1) // 2) for ln in self.lens)
+
+    def dominant_kernel(self) -> str:
+        return ("chunk_attn_tc_kernel (K2, tcgen05 QK^T / PV with TMEM accumulators)" if self.n_q >= 8
+                else "decode_attn_kernel (K1, fused append + split-KV attention)")

@@ -125,6 +125,51 @@ __global__ void __launch_bounds__(R * (CPR + 1) * 32) multi_ring(const uint8_t *
   if (acc == 0x12345678) sink[0] = acc;
 }
 
+
+// One ring; each stage's copies split across NPW producer warps (lanes [0, NL) of each issue a part).
+// Stage i is fully issued by all producers before the next (all wait the same empty barrier).
+template <int NPW, int NL>
+__global__ void __launch_bounds__((NPW + 7) * 32) split_ring(const uint8_t *buf, int64_t n_blocks, int blk, int nstages,
+                                                             int *sink) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(sm + (size_t)nstages * blk);
+  uint64_t *empty = full + nstages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t per = (n_blocks + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = blockIdx.x * per, b1 = min(n_blocks, b0 + per);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nstages; ++s) { mbar_init(smem_u32(full + s), NPW * NL); mbar_init(smem_u32(empty + s), 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t n = b1 - b0;
+  constexpr int NW = 7;
+  if (warp >= NW) {
+    const int pw = warp - NW;
+    if (lane >= NL) return;
+    const int part = pw * NL + lane, nparts = NPW * NL;
+    for (int64_t i = 0; i < n; ++i) {
+      const int slot = i % nstages;
+      if (i >= nstages) mbar_wait(smem_u32(empty + slot), ((i / nstages) & 1) ^ 1);
+      const int64_t b = b0 + i;
+      const int64_t pb = (b % 8) * (n_blocks / 8) + b / 8;
+      const int chunk = blk / nparts;
+      mbar_expect(smem_u32(full + slot), chunk);
+      bulk(smem_u32(sm + (size_t)slot * blk + part * chunk), buf + pb * blk + part * chunk, chunk, smem_u32(full + slot));
+    }
+    return;
+  }
+  int acc = 0;
+  for (int64_t i = warp; i < n; i += NW) {
+    const int slot = i % nstages;
+    mbar_wait(smem_u32(full + slot), (i / nstages) & 1);
+    acc += reinterpret_cast<const int *>(sm + (size_t)slot * blk)[lane];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(empty + slot));
+  }
+  if (acc == 0x12345678) sink[0] = acc;
+}
+
 __global__ void ldg_stream(const int4 *buf, int64_t n16, int *sink) {
   int acc = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -166,6 +211,21 @@ int main(int argc, char **argv) {
   if (only < 0)
     printf("ldg_stream (LDG.128 x8 unroll, 148x1024 thr): %.0f GB/s\n",
            timeit([&] { ldg_stream<<<148 * 2, 1024>>>((const int4 *)buf, bytes / 16, sink); }));
+  if (only >= 200) {
+    const int k = only - 200;
+    const size_t smem = (size_t)16 * 8192 + 2 * 16 * 8;
+    const int64_t nb = bytes / 8192;
+    double gbs = 0;
+    const char *name = "";
+#define SR(NPW_, NL_)                                                                                        \
+  cudaFuncSetAttribute(split_ring<NPW_, NL_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
+  gbs = timeit([&] { split_ring<NPW_, NL_><<<148, (NPW_ + 7) * 32, smem>>>(buf, nb, 8192, 16, sink); }); \
+  name = #NPW_ " producer warps x " #NL_ " lanes";
+    switch (k) { case 0: SR(1, 1) break; case 1: SR(1, 4) break; case 2: SR(4, 1) break; case 3: SR(2, 2) break; case 4: SR(1, 8) break; }
+    cudaError_t e = cudaGetLastError();
+    printf("split_ring 16 x 8 KiB, %s: %.0f GB/s %s\n", name, gbs, e ? cudaGetErrorString(e) : "");
+    return 0;
+  }
   if (only >= 100) {
     const int k = only - 100;
     struct M { int R, CPR, nst, ctas; } ms[] = {{2, 3, 8, 1}, {3, 2, 8, 1}, {4, 2, 6, 1}, {4, 1, 6, 1}, {1, 1, 6, 4}, {2, 1, 6, 2}};
