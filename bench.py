@@ -121,59 +121,32 @@ def dist_env():
 # ------------------------------------------------------------------------------------------ CPU oracle
 def oracle_sample(cfg_name: str, seconds: float, max_steps: int = None, n_sample: int = 8):
     """Time the oracle (as it stands) on a bounded sample of the workload: n_sample of the LIPs with their
-    full files, one decode pred per step, repeated until `seconds` elapse (or max_steps)."""
-    import numpy as np
-
-    from oracle import Oracle
-    from paper_2510_25412_b200.workloads import CONFIGS, STEP_OWNER
-    from synth.workloads import TAG_K, TAG_Q, TAG_V, rows_np
+    full files and per-step policies, one pred per step, repeated until `seconds` elapse (or max_steps)."""
+    from oracle.workload import OracleWorkload
+    from synth.configs import CONFIGS
 
     c = CONFIGS[cfg_name]
-    s = c["shape"]
     n_sample = min(n_sample, c["n_files"])
-    steps_cap = max_steps if max_steps is not None else 10 ** 9
-    per_file = (c["file_len"] + 1024 + s.P) // s.P + 2
-    o = Oracle(n_sample * per_file, s.P, 1, s.Hkv, s.D)
-    fds, lens = [], []
-    for f in range(n_sample):
-        fd = o.open(f"lip{f}")
-        k = rows_np(c["seed"], TAG_K, 0, f, 0, c["file_len"], s.Hkv * s.D).reshape(1, -1, s.Hkv, s.D)
-        v = rows_np(c["seed"], TAG_V, 0, f, 0, c["file_len"], s.Hkv * s.D).reshape(1, -1, s.Hkv, s.D)
-        o.append(fd, list(range(c["file_len"])), k, v)
-        fds.append(fd)
-        lens.append(c["file_len"])
+    cap = max_steps if max_steps is not None else 10 ** 9
+    ow = OracleWorkload(cfg_name, range(n_sample), max_steps=min(cap, 256))
     try:
         from threadpoolctl import threadpool_info
         blas_threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
         blas_threads = None
     cores = len(os.sched_getaffinity(0))
-    rows = 0
-    steps = 0
+    rows = steps = 0
     t0 = time.perf_counter()
-    while steps < steps_cap and (max_steps is not None or time.perf_counter() - t0 < seconds or steps == 0):
-        T = n_sample * c["n_q"]
-        owner = STEP_OWNER + steps
-        q = rows_np(c["seed"], TAG_Q, 0, owner, 0, T, s.Hq * s.D).reshape(1, T, s.Hq, s.D)
-        k = rows_np(c["seed"], TAG_K, 0, owner, 0, T, s.Hkv * s.D).reshape(1, T, s.Hkv, s.D)
-        v = rows_np(c["seed"], TAG_V, 0, owner, 0, T, s.Hkv * s.D).reshape(1, T, s.Hkv, s.D)
-        if c.get("rewind"):
-            lens = [ln - c["rewind"] for ln in lens]
-            for fd, ln in zip(fds, lens):
-                o.truncate(fd, ln)
-        pos = []
-        for ln in lens:
-            pos.extend(range(ln, ln + c["n_q"]))
-        st, _, _ = o.pred_batch([(fd, c["n_q"]) for fd in fds], pos, q, k, v, s.D ** -0.5)
-        assert all(x == 0 for x in st)
-        lens = [ln + c["n_q"] for ln in lens]
-        rows += T
+    while steps < cap and (max_steps is not None or time.perf_counter() - t0 < seconds or steps == 0):
+        st, _, _ = ow.run_step()
+        assert all(x == 0 for x in st), st
+        rows += n_sample * c["n_q"]
         steps += 1
     el = time.perf_counter() - t0
     return {"value": rows / el, "unit": "tokens/s", "cores": cores, "blas_threads": blas_threads,
             "kind": "oracle",
-            "sample": f"{n_sample} of {c['n_files']} LIPs ({c['file_len']}-token files, n_q={c['n_q']}), "
-                      f"{steps} decode preds in {el:.1f} s via oracle.Oracle.pred_batch (numpy fp64)",
+            "sample": f"{n_sample} of {c['n_files']} LIPs (full files, n_q={c['n_q']}, same per-step policy), "
+                      f"{steps} preds in {el:.1f} s via oracle.Oracle.pred_batch (numpy fp64)",
             "steps": steps, "seconds": el}
 
 
@@ -181,7 +154,7 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    from paper_2510_25412_b200.workloads import CONFIGS
+    from synth.configs import CONFIGS
 
     c = CONFIGS[args.config]
     # warm-up steps are run untimed, then exactly K timed steps (each a bounded 4-LIP sample)
@@ -222,32 +195,17 @@ def run_ours(args):
     inputs = [wl.make_inputs(i) for i in range(W + Kst)]
     out = torch.empty((T, s.Hq, s.D), dtype=torch.bfloat16, device="cuda")
     lse = torch.empty((T, s.Hq), dtype=torch.float32, device="cuda")
-    descs = np.array([[fd, wl.n_q] for fd in wl.fds], dtype=np.int32)
-    lens = np.array(wl.lens, dtype=np.int64)
-    offs = np.arange(wl.n_q, dtype=np.int64)
-
-    def positions():
-        return (lens[:, None] + offs[None, :]).reshape(-1).astype(np.int32)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    alg_bytes = []
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(Kst)]
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(Kst)]
-    def rewind():
-        if wl.rewind:
-            lens[:] -= wl.rewind
-            for fd, ln in zip(wl.fds, lens.tolist()):
-                kv.truncate(fd, ln)
-
     for i in range(W):
         q, k, v = inputs[i]
-        rewind()
-        st = kv.pred_attn_batch(descs, positions(), q, k, v, out, lse)
+        wl.pre_step()
+        st = kv.pred_attn_batch(wl.descs, wl.positions(), q, k, v, out, lse)
         assert all(x == 0 for x in st), st
-        lens += wl.n_q
+        wl.advance()
     torch.cuda.synchronize()
     barrier()
     launches0 = kv.counter(K.CTR_KERNEL_LAUNCHES)
@@ -256,23 +214,25 @@ def run_ours(args):
     sampler.start()
     torch.cuda.synchronize()
     barrier()
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(Kst)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(Kst)]
+    alg_bytes, alg_flops, logical = [], [], []
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     host_t0 = time.perf_counter()
     t_start.record()
-    alg_flops = []
     for i in range(Kst):
         q, k, v = inputs[W + i]
-        rewind()
-        wl.lens = lens.tolist()
+        wl.pre_step()
         alg_bytes.append(wl.algorithmic_bytes())
         alg_flops.append(wl.flops())
-        step, st = kv.pred_step_begin(descs, positions())
+        logical.append(wl.logical_kv_bytes())
+        step, st = kv.pred_step_begin(wl.descs, wl.positions())
         ev0[i].record()
         kv.pred_attn_layer(step, 0, q, k, v, out, lse)
         ev1[i].record()
         kv.pred_step_end(step)
-        lens += wl.n_q
+        wl.advance()
     t_end.record()
     host_s = time.perf_counter() - host_t0
     torch.cuda.synchronize()
@@ -282,7 +242,6 @@ def run_ours(args):
     kernel_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
     launches = kv.counter(K.CTR_KERNEL_LAUNCHES) - launches0
     h2d = kv.counter(K.CTR_H2D_BYTES) - h2d0
-    wl.lens = lens.tolist()
     t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -304,14 +263,14 @@ def run_ours(args):
         e0.record()
         for i in range(n_e2e):
             hq, hk, hv = ring[i % 4]
-            rewind()
+            wl.pre_step()
             qd.copy_(hq, non_blocking=True)
             kd.copy_(hk, non_blocking=True)
             vd.copy_(hv, non_blocking=True)
-            kv.pred_attn_batch(descs, positions(), qd, kd, vd, out, lse)
+            kv.pred_attn_batch(wl.descs, wl.positions(), qd, kd, vd, out, lse)
             out_h.copy_(out, non_blocking=True)
             lse_h.copy_(lse, non_blocking=True)
-            lens += wl.n_q
+            wl.advance()
         e1.record()
         torch.cuda.synchronize()
         et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
@@ -358,10 +317,12 @@ def run_ours(args):
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16",
         "data": "synthetic (counter-based generator seed %d, DESIGN.md input recipe)" % wl.seed,
-        "config": {"workload": wl.desc, "lips_per_gpu": wl.n_files, "file_len_start": wl.file_len,
+        "config": {"workload": wl.desc, "lips_per_gpu": wl.n_files, "file_len_start": wl.file_len + wl.prefix_len,
                    "n_q": wl.n_q, "n_q_heads": s.Hq, "n_kv_heads": s.Hkv, "head_dim": s.D, "page_size": s.P,
                    "layers_per_step": 1, "parallelism": f"dp{world} (LIPs partitioned by process, no collective)",
-                   "l2": "inputs larger than L2 (K/V read per step %.2f GB > 126 MB L2)" % (alg_bytes[0] / 1e9)},
+                   "l2": ("inputs larger than L2 (K/V read per step %.2f GB > 126 MB L2)" % (logical[0] / 1e9)
+                          if logical[0] > 126e6 * 4 else
+                          "unique K/V %.0f MB per step; the CoW-shared prefix is L2-resident by design" % (alg_bytes[0] / 1e6))},
         "roofline": dict(roof, traffic=traffic, traffic_source=traffic_src, kernel=wl.dominant_kernel(),
                          kernel_ms_mean=k_ms, peak_source=peak_src,
                          algorithmic_bytes_per_launch=statistics.mean(alg_bytes),
@@ -369,6 +330,8 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": sampler.summary(),
         "extra": {"kv_attn_gbs_step": statistics.mean(alg_bytes) / (ms_step / 1000.0) / 1e9,
+                  "logical_kv_bytes_per_step": statistics.mean(logical),
+                  "logical_gbs_kernel": statistics.mean(logical) / (k_ms / 1000.0) / 1e9,
                   "tok_s_32_layer_equiv": value / 32.0, "host_s_per_step": host_s / Kst,
                   "h2d_metadata_bytes_per_step": h2d / Kst,
                   "decode_ctas": kv.counter(K.CTR_LAST_DECODE_CTAS)},

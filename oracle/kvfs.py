@@ -195,11 +195,12 @@ class Oracle:
         if not (0 <= begin <= end <= f.length()):
             raise KvfsError(ERANGE, "read range")
         lg = f.logical()[begin:end]
-        k = np.stack([self.K[layer, p, :, s, :] for p, s in lg]) if lg else \
-            np.zeros((0, self.Hkv, self.D), np.uint16)
-        v = np.stack([self.V[layer, p, :, s, :] for p, s in lg]) if lg else \
-            np.zeros((0, self.Hkv, self.D), np.uint16)
-        return k, v
+        if not lg:
+            z = np.zeros((0, self.Hkv, self.D), np.uint16)
+            return z, z.copy()
+        pages = np.array([p for p, _ in lg])
+        sl = np.array([x for _, x in lg])
+        return self.K[layer, pages, :, sl, :], self.V[layer, pages, :, sl, :]
 
     def audit(self) -> None:
         """Invariants I1-I5. Raises AssertionError on violation."""
@@ -266,11 +267,13 @@ class Oracle:
 
     def _write_rows(self, slots, k_rows, v_rows) -> None:
         """k_rows / v_rows: [L][n][Hkv][D] bf16 bits."""
-        if not self.store:
+        if not self.store or not slots:
             return
-        for i, (page, slot) in enumerate(slots):
-            self.K[:, page, :, slot, :] = k_rows[:, i]
-            self.V[:, page, :, slot, :] = v_rows[:, i]
+        pages = np.array([p for p, _ in slots])
+        sl = np.array([x for _, x in slots])
+        # advanced indices split by a slice put the row axis first: [n][L][Hkv][D]
+        self.K[:, pages, :, sl, :] = np.asarray(k_rows).transpose(1, 0, 2, 3)
+        self.V[:, pages, :, sl, :] = np.asarray(v_rows).transpose(1, 0, 2, 3)
 
     def append(self, fd: int, pos: Sequence[int], k_rows=None, v_rows=None) -> None:
         f = self._file(fd)

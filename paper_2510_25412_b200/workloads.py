@@ -2,48 +2,32 @@
 
 Inputs follow DESIGN.md "Input recipe" (synth/, counter-based, bit-identical on host and device):
   * initial K/V of file f, token serial t:  rows(seed, TAG_K|TAG_V, layer, owner=f, serial=t)
-  * new K/V of decode step s, row r:       rows(seed, TAG_K|TAG_V, layer, owner=STEP_OWNER+s, serial=r)
-  * Q of decode step s, row r:             rows(seed, TAG_Q, layer, owner=STEP_OWNER+s, serial=r)
+  * the shared prefix (cfg3):              rows(seed, TAG_K|TAG_V, layer, owner=PREFIX_OWNER, serial=t)
+  * new K/V of step s, row r:              rows(seed, TAG_K|TAG_V, layer, owner=STEP_OWNER+s, serial=r)
+  * Q of step s, row r:                    rows(seed, TAG_Q, layer, owner=STEP_OWNER+s, serial=r)
 so a test can regenerate any file's or step's inputs on the host for the oracle.
 """
 from __future__ import annotations
 
 import math
-from dataclasses import dataclass, field
-from typing import Dict, List, Tuple
+from typing import Tuple
 
+import numpy as np
 import torch
 
 from synth.workloads import TAG_K, TAG_Q, TAG_V, rows_torch
 
 from .kvfs import KVFS
 
-STEP_OWNER = 1_000_000
-
-
-@dataclass
-class Shape:
-    Hq: int = 32
-    Hkv: int = 8
-    D: int = 128
-    P: int = 16
-
-
-CONFIGS: Dict[str, dict] = {
-    # BASELINE.json configs[1]: Llama-3-8B attention shape, 256 LIPs decoding from 2k-token files
-    "cfg2": dict(workload="cfg2: Llama-3-8B attn (32q/8kv, hd128, bf16, P=16), 256 LIPs decode (n_q=1) "
-                          "from 2048-token KVFS files, 1 layer per step",
-                 shape=Shape(32, 8, 128, 16), n_files=256, file_len=2048, n_q=1, seed=1002, rewind=0),
-    # BASELINE.json configs[3]: live code autocompletion, truncate-to-cursor (r = 64) + 64-token re-append
-    "cfg4": dict(workload="cfg4: autocompletion, 128 LIPs x 8192-token files (32q/8kv, hd128, P=16); each step "
-                          "truncates every file to 8192-64 and re-appends 64 tokens (n_q=64, tcgen05 chunk kernel)",
-                 shape=Shape(32, 8, 128, 16), n_files=128, file_len=8192, n_q=64, seed=1004, rewind=64),
-}
+from synth.configs import CONFIGS, PREFIX_OWNER, STEP_OWNER, Shape  # noqa: F401
 
 
 class DecodeWorkload:
-    """n_files LIPs, each owning one file of file_len tokens; every step is one batched pred with n_q rows
-    per LIP (positions continue the file)."""
+    """n_files LIPs, each owning one file; every step is one batched pred with n_q rows per LIP.
+
+    Per-step LIP policies (host, through the C ABI): `rewind` truncates every file by r tokens before the
+    step (autocompletion); `evict_sink` evicts logical [sink, sink+1) (attention sink + sliding
+    window); `prefix_len` builds every file as a fork of one shared prefix."""
 
     def __init__(self, name: str, steps_total: int, device: int = 0, n_files: int = None):
         c = CONFIGS[name]
@@ -54,32 +38,46 @@ class DecodeWorkload:
         self.n_files = n_files or c["n_files"]
         self.file_len = c["file_len"]
         self.n_q = c["n_q"]
-        self.rewind = c.get("rewind", 0)  # truncate-to-cursor before every step (autocompletion)
+        self.rewind = c.get("rewind", 0)
+        self.prefix_len = c.get("prefix_len", 0)
+        self.evict_sink = c.get("evict_sink", 0)
         self.steps_total = steps_total
         s = self.shape
         self.dev = torch.device("cuda", device)
         grow = 0 if self.rewind else steps_total * self.n_q
-        per_file = math.ceil((self.file_len + grow + s.P) / s.P) + 1
-        self.n_pages = self.n_files * per_file + 64
+        per_file = math.ceil((self.file_len + grow + s.P) / s.P) + 2
+        self.n_pages = self.n_files * per_file + math.ceil(self.prefix_len / s.P) + 64
         rows = self.n_files * self.n_q
         self.kv = KVFS(1, s.Hq, s.Hkv, s.D, s.P, self.n_pages, max_batch_rows=max(rows, 16),
                        max_batch_descs=max(self.n_files, 16), device=device)
-        self.fds: List[int] = []
-        self.lens: List[int] = []
         width = s.Hkv * s.D
+        fds = []
+        self.prefix_fd = None
+        if self.prefix_len:
+            self.prefix_fd = self.kv.open("prefix")
+            k = rows_torch(self.seed, TAG_K, 0, PREFIX_OWNER, 0, self.prefix_len, width, device=self.dev)
+            v = rows_torch(self.seed, TAG_V, 0, PREFIX_OWNER, 0, self.prefix_len, width, device=self.dev)
+            self.kv.append(self.prefix_fd, list(range(self.prefix_len)), k.view(1, -1, s.Hkv, s.D),
+                           v.view(1, -1, s.Hkv, s.D))
         for f in range(self.n_files):
-            fd = self.kv.open(f"lip{f}")
+            fd = self.kv.fork(self.prefix_fd, f"lip{f}") if self.prefix_fd is not None else self.kv.open(f"lip{f}")
             k = rows_torch(self.seed, TAG_K, 0, f, 0, self.file_len, width, device=self.dev)
             v = rows_torch(self.seed, TAG_V, 0, f, 0, self.file_len, width, device=self.dev)
-            self.kv.append(fd, list(range(self.file_len)), k.view(1, self.file_len, s.Hkv, s.D),
+            p0 = self.prefix_len
+            self.kv.append(fd, list(range(p0, p0 + self.file_len)), k.view(1, self.file_len, s.Hkv, s.D),
                            v.view(1, self.file_len, s.Hkv, s.D))
-            self.fds.append(fd)
-            self.lens.append(self.file_len)
+            fds.append(fd)
         torch.cuda.synchronize(self.dev)
+        self.fds = fds
+        self.descs = np.array([[fd, self.n_q] for fd in fds], dtype=np.int32)
+        self.lens = np.full(self.n_files, self.prefix_len + self.file_len, dtype=np.int64)  # retained tokens
+        self.next_pos = self.lens.copy()  # next absolute position of every LIP
+        self._offs = np.arange(self.n_q, dtype=np.int64)
         self.step = 0
 
+    # ------------------------------------------------------------------ per step
     def make_inputs(self, step: int) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
-        """Device Q [T][Hq][D], K_new/V_new [T][Hkv][D] of decode step `step`."""
+        """Device Q [T][Hq][D], K_new/V_new [T][Hkv][D] of step `step`."""
         s = self.shape
         T = self.n_files * self.n_q
         owner = STEP_OWNER + step
@@ -89,40 +87,55 @@ class DecodeWorkload:
         return q, k, v
 
     def pre_step(self) -> None:
-        """Host-side LIP policy before a step: truncate-to-cursor for the autocompletion workload."""
+        """Host-side LIP policy before a step (through the C ABI)."""
         if self.rewind:
-            for i, fd in enumerate(self.fds):
-                self.lens[i] -= self.rewind
-                self.kv.truncate(fd, self.lens[i])
+            self.lens -= self.rewind
+            self.next_pos -= self.rewind
+            for fd, ln in zip(self.fds, self.lens.tolist()):
+                self.kv.truncate(fd, ln)
+        if self.evict_sink and self.step > 0:
+            e = self.evict_sink
+            for fd in self.fds:
+                self.kv.evict(fd, [(e, e + 1)])
+            self.lens -= 1
 
-    def descs_and_pos(self) -> Tuple[List[Tuple[int, int]], List[int]]:
-        descs, pos = [], []
-        for fd, ln in zip(self.fds, self.lens):
-            descs.append((fd, self.n_q))
-            pos.extend(range(ln, ln + self.n_q))
-        return descs, pos
+    def positions(self) -> np.ndarray:
+        return (self.next_pos[:, None] + self._offs[None, :]).reshape(-1).astype(np.int32)
+
+    def descs_and_pos(self):
+        return [(int(a), int(b)) for a, b in self.descs], self.positions().tolist()
 
     def advance(self) -> None:
-        self.lens = [ln + self.n_q for ln in self.lens]
+        self.lens += self.n_q
+        self.next_pos += self.n_q
         self.step += 1
 
-    def algorithmic_bytes(self) -> int:
-        """Bytes one pred step must move (SURVEY §8(d)): every retained K/V row read once (the old tokens;
-        the new rows are read from K_new), Q read, out + lse written, new K/V read once and written once."""
+    # ------------------------------------------------------------------ accounting (SURVEY §8(d))
+    def logical_kv_bytes(self) -> int:
         s = self.shape
-        row_kv = s.Hkv * s.D * 2  # one token's K (or V) bytes
+        return int(2 * self.lens.sum() * s.Hkv * s.D * 2)
+
+    def unique_kv_bytes(self) -> int:
+        """K/V bytes of the distinct retained rows the batch reads (a CoW-shared prefix counted once)."""
+        s = self.shape
+        row_kv = s.Hkv * s.D * 2
+        if not self.prefix_len:
+            return int(2 * self.lens.sum() * row_kv)
+        return int(2 * (self.prefix_len + (self.lens - self.prefix_len).sum()) * row_kv)
+
+    def algorithmic_bytes(self) -> int:
+        """Bytes one pred step must move: every unique retained K/V row read once (the old tokens; the new
+        rows come from K_new), Q read, out + lse written, new K/V read once and written once."""
+        s = self.shape
+        row_kv = s.Hkv * s.D * 2
         T = self.n_files * self.n_q
-        old = sum(self.lens)  # retained tokens before this step's append
-        return (2 * old * row_kv            # K and V of the retained tokens
-                + T * s.Hq * s.D * 2        # Q
-                + T * s.Hq * s.D * 2        # out
-                + T * s.Hq * 4              # lse
-                + 2 * 2 * T * row_kv)       # K_new, V_new: read + written into the pool
+        return (self.unique_kv_bytes() + T * s.Hq * s.D * 2 + T * s.Hq * s.D * 2 + T * s.Hq * 4
+                + 2 * 2 * T * row_kv)
 
     def flops(self) -> int:
         s = self.shape
         n = self.n_q
-        return sum(4 * s.Hq * s.D * (n * ln + n * (n + 1) // 2) for ln in self.lens)
+        return int(sum(4 * s.Hq * s.D * (n * int(ln) + n * (n + 1) // 2) for ln in self.lens))
 
     def dominant_kernel(self) -> str:
         return ("chunk_attn_tc_kernel (K2, tcgen05 QK^T / PV with TMEM accumulators)" if self.n_q >= 8
