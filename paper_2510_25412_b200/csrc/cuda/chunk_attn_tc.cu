@@ -210,8 +210,14 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         if (e < cd.n_entries) {
           const Entry en = p.slab[cd.slab_off + e];
           if ((en.mask >> slot) & 1ull) {
-            const int lg = en.lstart + __popcll(en.mask & ((1ull << slot) - 1ull));
-            j = lg - cd.n_old;
+            if (e < cd.first_new_entry) {
+              j = -1;  // an old token: visible to every query row
+            } else {
+              // logical index = first_new_lstart + tokens of the new-region entries before e + rank in e
+              int lg = cd.first_new_lstart + __popcll(en.mask & ((1ull << slot) - 1ull));
+              for (int e2 = cd.first_new_entry; e2 < e; ++e2) lg += __popcll(p.slab[cd.slab_off + e2].mask);
+              j = lg - cd.n_old;
+            }
           }
         }
         jcol[c] = j;

@@ -8,7 +8,7 @@
 namespace kvfs {
 namespace dev {
 
-struct Entry {  // == kvfs::Entry
+struct Entry {  // == kvfs::Entry (the slab copy's lstart is not maintained: kernels must not read it)
   uint32_t page;
   int32_t lstart;
   uint64_t mask;
@@ -23,8 +23,11 @@ struct Desc {  // == kvfs::DevDesc
   int32_t row0;
   int32_t unit_base;
   int32_t stages_per_unit;
-  int32_t pad0;
-  int64_t pad1;
+  int32_t n_entries;
+  int32_t tail_lstart;
+  int32_t first_new_entry;
+  int32_t first_new_lstart;
+  int32_t pad0, pad1, pad2;
 };
 
 struct SlabRun {

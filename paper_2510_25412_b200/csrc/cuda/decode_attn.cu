@@ -183,7 +183,8 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
           if (st < dd.n_old_entries) {
             const Entry e = p.slab[dd.slab_off + st];
             mask = e.mask;
-            if (e.lstart + __popcll(mask) > dd.n_old) mask = lowest_bits(mask, dd.n_old - e.lstart);
+            // only the last old entry can also hold new tokens (the device lstart is not maintained)
+            if (st == dd.n_old_entries - 1) mask = lowest_bits(mask, dd.n_old - dd.tail_lstart);
             lo = __ffsll(static_cast<long long>(mask)) - 1;
             const int hi = 63 - __clzll(static_cast<long long>(mask));
             nrows = hi - lo + 1;

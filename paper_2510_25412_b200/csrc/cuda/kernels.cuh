@@ -27,7 +27,7 @@ struct DecodeParams {
 cudaError_t launch_decode(const DecodeParams &p, int D, int G, int P, cudaStream_t s);
 // ---- K2 (tcgen05 chunk attention, D = 128)
 struct ChunkDesc {  // == kvfs::ChunkDesc
-  int32_t slab_off, n_entries, n_old, n_q, row0, pad;
+  int32_t slab_off, n_entries, n_old, n_q, row0, first_new_entry, first_new_lstart, pad;
 };
 struct ChunkUnit {  // == kvfs::ChunkUnit
   int32_t desc, g, m, pad;

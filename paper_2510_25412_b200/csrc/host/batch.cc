@@ -62,10 +62,9 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
                 !c.slab.alloc(size_after, &off, &cap)) {
               st = KVFS_ENOMEM;
             } else {
-              release_file_slab(c, *f);
+              release_file_slab(c, *f);  // resets dirty_from = 0: the whole table is uploaded
               f->slab_off = off;
               f->slab_cap = cap;
-              f->dirty_from = 0;
             }
           }
         }
@@ -76,8 +75,9 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
           std::copy(dst.begin(), dst.end(), pl.dst_slot.begin() + row0);
           int64_t idx = static_cast<int64_t>(f->table.size()) - 1;
           while (idx >= 0 && f->table[idx].lstart >= n_old) --idx;
+          int64_t fne = idx < 0 ? 0 : idx;  // entry holding logical token n_old
+          if (idx >= 0 && f->table[idx].lstart + __builtin_popcountll(f->table[idx].mask) <= n_old) fne = idx + 1;
           DevDesc d{};
-          d.pad0 = static_cast<int32_t>(f->table.size());  // entries after the append (used by K2)
           d.cost_begin = pl.total_cost;
           d.slab_off = static_cast<int32_t>(f->slab_off);
           d.n_old_entries = static_cast<int32_t>(idx + 1);
@@ -86,17 +86,36 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
           d.row0 = static_cast<int32_t>(row0);
           d.unit_base = pl.n_units;
           d.stages_per_unit = d.n_old_entries + (nq + P - 1) / P;
+          d.n_entries = static_cast<int32_t>(f->table.size());
+          d.tail_lstart = idx >= 0 ? f->table[idx].lstart : 0;
+          d.first_new_entry = static_cast<int32_t>(fne);
+          d.first_new_lstart = f->table[fne].lstart;
           pl.descs.push_back(d);
           pl.total_cost += static_cast<int64_t>(Hkv) * nq * d.stages_per_unit;
           pl.n_units += Hkv * nq;
           pl.max_nq = std::max(pl.max_nq, nq);
-          if (device && f->dirty_from < f->table.size()) {
-            SlabRun r{f->slab_off + static_cast<int64_t>(f->dirty_from), static_cast<int32_t>(pl.run_entries.size()),
-                      static_cast<int32_t>(f->table.size() - f->dirty_from)};
-            pl.runs.push_back(r);
-            pl.run_entries.insert(pl.run_entries.end(), f->table.begin() + static_cast<long>(f->dirty_from),
-                                  f->table.end());
-            f->dirty_from = f->table.size();
+          if (device) {
+            // device table deltas: in-place point updates below dirty_from, then the dirty suffix
+            const size_t n_ent = f->table.size();
+            for (uint32_t e : f->dirty_pts) {
+              if (e >= f->dirty_from || e >= n_ent) continue;
+              if (!pl.runs.empty() && pl.runs.back().dst + pl.runs.back().count == f->slab_off + e &&
+                  pl.runs.back().count < (1 << 30)) {
+                pl.runs.back().count += 1;
+              } else {
+                pl.runs.push_back({f->slab_off + e, static_cast<int32_t>(pl.run_entries.size()), 1});
+              }
+              pl.run_entries.push_back(f->table[e]);
+            }
+            f->dirty_pts.clear();
+            if (f->dirty_from < n_ent) {
+              SlabRun r{f->slab_off + static_cast<int64_t>(f->dirty_from), static_cast<int32_t>(pl.run_entries.size()),
+                        static_cast<int32_t>(n_ent - f->dirty_from)};
+              pl.runs.push_back(r);
+              pl.run_entries.insert(pl.run_entries.end(), f->table.begin() + static_cast<long>(f->dirty_from),
+                                    f->table.end());
+            }
+            f->dirty_from = n_ent;
           }
         }
       }
@@ -122,7 +141,7 @@ void pred_split(const Ctx &c, int64_t cutover, PredPlan *plan) {
   for (const DevDesc &d : pl.descs) {
     if (d.n_q >= cutover) {
       if (pl.chunk_dst.empty()) pl.chunk_dst.assign(static_cast<size_t>(pl.T), -1);
-      ChunkDesc cd{d.slab_off, d.pad0, d.n_old, d.n_q, d.row0, 0};
+      ChunkDesc cd{d.slab_off, d.n_entries, d.n_old, d.n_q, d.row0, d.first_new_entry, d.first_new_lstart, 0};
       const int32_t di = static_cast<int32_t>(pl.chunk_descs.size());
       pl.chunk_descs.push_back(cd);
       const int mt = (d.n_q * G + 127) / 128;

@@ -297,7 +297,7 @@ int kvfs_stat(kvfs_ctx *ctx, int fd, kvfs_stat_t *st) {
   if (!st) return KVFS_EINVAL;
   st->len = f->len;
   st->n_entries = static_cast<int64_t>(f->table.size());
-  st->last_pos = f->pos.empty() ? -1 : f->pos.back();
+  st->last_pos = last_pos(c, *f);
   st->reserved = 0;
   return KVFS_OK;
 }
@@ -321,8 +321,10 @@ int kvfs_get_positions(kvfs_ctx *ctx, int fd, int32_t *pos, int64_t cap, int64_t
   File *f = get_file(c, fd);
   if (!f) return KVFS_EBADF;
   if (cap < 0 || (cap > 0 && !pos)) return KVFS_EINVAL;
-  const int64_t m = static_cast<int64_t>(f->pos.size());
-  if (m > 0 && cap > 0) std::memcpy(pos, f->pos.data(), sizeof(int32_t) * static_cast<size_t>(std::min(m, cap)));
+  std::vector<int32_t> lp;
+  file_positions(c, *f, &lp);
+  const int64_t m = static_cast<int64_t>(lp.size());
+  if (m > 0 && cap > 0) std::memcpy(pos, lp.data(), sizeof(int32_t) * static_cast<size_t>(std::min(m, cap)));
   if (n) *n = m;
   return KVFS_OK;
 }

@@ -36,7 +36,12 @@ int64_t new_fd(Ctx &c, const FilePtr &f) {
   return static_cast<int64_t>(c.fds.size() - 1);
 }
 
-void mark_dirty(File &f, size_t i) { f.dirty_from = std::min(f.dirty_from, i); }
+// Entries at indices >= i moved or are new: the device copy of the whole suffix is stale.
+void mark_dirty_from(File &f, size_t i) { f.dirty_from = std::min(f.dirty_from, i); }
+// Entry i's page or mask changed in place.
+void mark_dirty_pt(File &f, size_t i) {
+  if (i < f.dirty_from) f.dirty_pts.push_back(static_cast<uint32_t>(i));
+}
 
 }  // namespace
 
@@ -70,6 +75,21 @@ void release_file_slab(Ctx &c, File &f) {
   f.slab_off = -1;
   f.slab_cap = 0;
   f.dirty_from = 0;
+  f.dirty_pts.clear();
+}
+
+int32_t last_pos(const Ctx &c, const File &f) {
+  if (f.table.empty()) return -1;
+  const Entry &t = f.table.back();
+  return f.spos[(f.table.size() - 1) * c.cfg.page_size + hi_slot(t.mask)];
+}
+
+void file_positions(const Ctx &c, const File &f, std::vector<int32_t> *out) {
+  const int P = c.cfg.page_size;
+  out->clear();
+  out->reserve(static_cast<size_t>(f.len));
+  for (size_t e = 0; e < f.table.size(); ++e)
+    for (uint64_t m = f.table[e].mask; m; m &= m - 1) out->push_back(f.spos[e * P + __builtin_ctzll(m)]);
 }
 
 // ------------------------------------------------------------------------------------------ helpers
@@ -119,7 +139,7 @@ int unlink_file(Ctx &c, const char *name) {
   File &f = *it->second;
   for (const Entry &e : f.table) c.pool->release(e.page);
   f.table.clear();
-  f.pos.clear();
+  f.spos.clear();
   f.len = 0;
   f.alive = false;
   release_file_slab(c, f);
@@ -130,7 +150,7 @@ int unlink_file(Ctx &c, const char *name) {
 // ------------------------------------------------------------------------------------------ R3
 int append_plan(const Ctx &c, const File &f, int64_t n, const int32_t *pos, int64_t *need, int64_t *new_entries) {
   const int P = c.cfg.page_size;
-  int64_t last = f.pos.empty() ? -1 : f.pos.back();
+  const int64_t last = last_pos(c, f);
   if (pos[0] <= last) return KVFS_EPOS;
   for (int64_t i = 1; i < n; ++i)
     if (pos[i] <= pos[i - 1]) return KVFS_EPOS;
@@ -154,7 +174,8 @@ void append_commit(Ctx &c, File &f, int64_t n, const int32_t *pos, std::vector<i
   int64_t i = 0;
   size_t first_changed = f.table.size();
   if (!f.table.empty()) {
-    Entry &t = f.table.back();
+    const size_t ti = f.table.size() - 1;
+    Entry &t = f.table[ti];
     const int hi = hi_slot(t.mask);
     const int room = P - 1 - hi;
     if (room > 0) {
@@ -167,23 +188,27 @@ void append_commit(Ctx &c, File &f, int64_t n, const int32_t *pos, std::vector<i
       const int take = static_cast<int>(std::min<int64_t>(n, room));
       for (int s = 0; s < take; ++s) {
         t.mask |= 1ull << (hi + 1 + s);
+        f.spos[ti * P + hi + 1 + s] = pos[s];
         if (dst) dst->push_back(static_cast<int32_t>(t.page) * P + hi + 1 + s);
       }
       i = take;
-      first_changed = f.table.size() - 1;
+      first_changed = ti;
+      mark_dirty_pt(f, ti);
     }
   }
+  mark_dirty_from(f, f.table.size());
   while (i < n) {
     const uint32_t q = c.pool->alloc();
     const int take = static_cast<int>(std::min<int64_t>(P, n - i));
     Entry e{q, 0, take == 64 ? ~0ull : ((1ull << take) - 1)};
     f.table.push_back(e);
-    if (dst)
-      for (int s = 0; s < take; ++s) dst->push_back(static_cast<int32_t>(q) * P + s);
+    f.spos.resize(f.table.size() * P, 0);
+    for (int s = 0; s < take; ++s) {
+      f.spos[(f.table.size() - 1) * P + s] = pos[i + s];
+      if (dst) dst->push_back(static_cast<int32_t>(q) * P + s);
+    }
     i += take;
   }
-  f.pos.insert(f.pos.end(), pos, pos + n);
-  mark_dirty(f, first_changed);
   recompute_lstart(f, first_changed);
 }
 
@@ -197,7 +222,7 @@ int fork_file(Ctx &c, File &src, const char *dst_name, int *dst_fd, std::vector<
   auto f = std::make_shared<File>();
   f->name = dst_name;
   f->table = src.table;
-  f->pos = src.pos;
+  f->spos = src.spos;
   f->len = src.len;
   for (const Entry &e : f->table) c.pool->incref(e.page);
   if (copy_tail) {
@@ -214,26 +239,29 @@ int fork_file(Ctx &c, File &src, const char *dst_name, int *dst_fd, std::vector<
 
 // ------------------------------------------------------------------------------------------ R5
 int truncate_file(Ctx &c, File &f, int64_t n) {
+  const int P = c.cfg.page_size;
   if (n < 0 || n > f.len) return KVFS_ERANGE;
   if (n == f.len) return KVFS_OK;
   if (n == 0) {
     for (const Entry &e : f.table) c.pool->release(e.page);
     f.table.clear();
-    f.pos.clear();
+    f.spos.clear();
     f.len = 0;
-    f.dirty_from = 0;
     return KVFS_OK;
   }
   // entry holding logical token n-1
   size_t i = 0;
   while (f.table[i].lstart + popc(f.table[i].mask) < n) ++i;
   Entry &e = f.table[i];
-  e.mask = rank_range_bits(e.mask, 0, static_cast<int>(n - e.lstart));
+  const uint64_t m = rank_range_bits(e.mask, 0, static_cast<int>(n - e.lstart));
+  if (m != e.mask) {
+    e.mask = m;
+    mark_dirty_pt(f, i);
+  }
   for (size_t j = i + 1; j < f.table.size(); ++j) c.pool->release(f.table[j].page);
   f.table.resize(i + 1);
-  f.pos.resize(static_cast<size_t>(n));
+  f.spos.resize((i + 1) * P);
   f.len = n;
-  mark_dirty(f, i);
   return KVFS_OK;
 }
 
@@ -245,8 +273,12 @@ static void compact_commit(Ctx &c, File &f, std::vector<Entry> *old_table, std::
   const int64_t k = (len + P - 1) / P;
   std::vector<uint32_t> np(static_cast<size_t>(k));
   for (int64_t j = 0; j < k; ++j) np[j] = c.pool->alloc();  // old pages still held: never destinations
+  std::vector<int32_t> lpos;
+  file_positions(c, f, &lpos);
   std::vector<Entry> old;
   old.swap(f.table);
+  f.spos.assign(static_cast<size_t>(k) * P, 0);
+  std::copy(lpos.begin(), lpos.end(), f.spos.begin());  // token i -> (new[i / P], i % P)
   const uint64_t full = P == 64 ? ~0ull : ((1ull << P) - 1);
   f.table.reserve(static_cast<size_t>(k));
   for (int64_t j = 0; j < k; ++j) {
@@ -254,7 +286,7 @@ static void compact_commit(Ctx &c, File &f, std::vector<Entry> *old_table, std::
     f.table.push_back({np[j], static_cast<int32_t>(j * P), cnt == 64 ? ~0ull : (cnt == P ? full : ((1ull << cnt) - 1))});
   }
   for (const Entry &e : old) c.pool->release(e.page);
-  f.dirty_from = 0;
+  mark_dirty_from(f, 0);
   recompute_lstart(f, 0);
   if (old_table) old_table->swap(old);
   if (new_pages) new_pages->swap(np);
@@ -270,10 +302,8 @@ int evict_file(Ctx &c, File &f, const int64_t *ranges, int n_ranges, int flags, 
     if (r > 0 && a < ranges[2 * r - 1]) return KVFS_EINVAL;
     if (a < 0 || b > f.len) return KVFS_ERANGE;
   }
-  // new masks (not yet committed)
-  std::vector<uint64_t> masks(f.table.size());
-  for (size_t i = 0; i < f.table.size(); ++i) masks[i] = f.table[i].mask;
-  size_t first_changed = f.table.size();
+  // new masks of the touched entries (not yet committed)
+  std::vector<std::pair<size_t, uint64_t>> touched;
   int64_t evicted = 0;
   size_t ei = 0;
   for (int r = 0; r < n_ranges; ++r) {
@@ -284,10 +314,10 @@ int evict_file(Ctx &c, File &f, const int64_t *ranges, int n_ranges, int flags, 
       const int64_t ls = f.table[i].lstart;
       const int r0 = static_cast<int>(std::max<int64_t>(0, a - ls));
       const int r1 = static_cast<int>(std::min<int64_t>(popc(f.table[i].mask), b - ls));
-      if (r0 < r1) {
-        masks[i] &= ~rank_range_bits(f.table[i].mask, r0, r1);
-        first_changed = std::min(first_changed, i);
-      }
+      if (r0 >= r1) continue;
+      const uint64_t clear = rank_range_bits(f.table[i].mask, r0, r1);
+      if (!touched.empty() && touched.back().first == i) touched.back().second &= ~clear;
+      else touched.push_back({i, f.table[i].mask & ~clear});
     }
   }
   const bool compact = (flags & KVFS_EVICT_COMPACT) != 0;
@@ -295,35 +325,37 @@ int evict_file(Ctx &c, File &f, const int64_t *ranges, int n_ranges, int flags, 
     const int64_t new_len = f.len - evicted;
     const int64_t k = (new_len + P - 1) / P;
     int64_t freed = 0;
-    for (size_t i = 0; i < masks.size(); ++i)
-      if (masks[i] == 0 && c.pool->refcnt(f.table[i].page) == 1) ++freed;
+    for (const auto &t : touched)
+      if (t.second == 0 && c.pool->refcnt(f.table[t.first].page) == 1) ++freed;
     if (k > c.pool->n_free() + freed) return KVFS_ENOSPC;
   }
-  if (n_ranges > 0) {
-    // positions: drop the evicted logical indices
-    std::vector<int32_t> np;
-    np.reserve(static_cast<size_t>(f.len - evicted));
-    int64_t idx = 0;
-    for (int r = 0; r < n_ranges; ++r) {
-      for (; idx < ranges[2 * r]; ++idx) np.push_back(f.pos[idx]);
-      idx = ranges[2 * r + 1];
-    }
-    for (; idx < f.len; ++idx) np.push_back(f.pos[idx]);
-    f.pos.swap(np);
-    std::vector<Entry> nt;
-    nt.reserve(f.table.size());
-    for (size_t i = 0; i < f.table.size(); ++i) {
-      if (masks[i]) {
-        Entry e = f.table[i];
-        e.mask = masks[i];
-        nt.push_back(e);
+  if (!touched.empty()) {
+    bool removed = false;
+    for (const auto &t : touched) {
+      f.table[t.first].mask = t.second;
+      if (t.second == 0) {
+        c.pool->release(f.table[t.first].page);
+        removed = true;
       } else {
-        c.pool->release(f.table[i].page);
+        mark_dirty_pt(f, t.first);
       }
     }
-    f.table.swap(nt);
-    mark_dirty(f, first_changed);
-    recompute_lstart(f, first_changed);
+    if (removed) {  // drop emptied entries (and their position slots) in place
+      size_t w = touched.front().first;
+      for (size_t i = w; i < f.table.size(); ++i) {
+        if (f.table[i].mask == 0) continue;
+        if (w != i) {
+          f.table[w] = f.table[i];
+          std::copy(f.spos.begin() + static_cast<long>(i * P), f.spos.begin() + static_cast<long>((i + 1) * P),
+                    f.spos.begin() + static_cast<long>(w * P));
+        }
+        ++w;
+      }
+      mark_dirty_from(f, touched.front().first);
+      f.table.resize(w);
+      f.spos.resize(w * P);
+    }
+    recompute_lstart(f, touched.front().first);
   }
   if (compact) compact_commit(c, f, old_table, new_pages);
   return KVFS_OK;
@@ -355,9 +387,11 @@ int audit(Ctx &c) {
     }
     std::sort(pages.begin(), pages.end());
     if (std::adjacent_find(pages.begin(), pages.end()) != pages.end()) return KVFS_EINVAL;  // I2
-    if (acc != f.len || static_cast<int64_t>(f.pos.size()) != f.len) return KVFS_EINVAL;
-    for (size_t i = 1; i < f.pos.size(); ++i)
-      if (f.pos[i] <= f.pos[i - 1]) return KVFS_EINVAL;  // I4
+    if (acc != f.len || f.spos.size() != f.table.size() * static_cast<size_t>(P)) return KVFS_EINVAL;
+    std::vector<int32_t> lp;
+    file_positions(c, f, &lp);
+    for (size_t i = 1; i < lp.size(); ++i)
+      if (lp[i] <= lp[i - 1]) return KVFS_EINVAL;  // I4
   }
   int64_t n_free = 0;
   for (int64_t p = 0; p < c.pool->n_pages(); ++p) {

@@ -25,12 +25,14 @@ struct File {
   std::string name;
   bool alive = true;
   std::vector<Entry> table;
-  std::vector<int32_t> pos;  // absolute positions of the retained tokens, logical order
+  std::vector<int32_t> spos;  // [n_entries * P]: absolute position of the token in (entry, slot)
   int64_t len = 0;
-  // device mirror of `table` in the slab: entries [0, dirty_from) are up to date on the device
+  // Device mirror of `table` (page and mask only; the kernels never read the device lstart): entries at
+  // indices >= dirty_from and the indices in dirty_pts may be stale on the device.
   int64_t slab_off = -1;
   int64_t slab_cap = 0;
   size_t dirty_from = 0;
+  std::vector<uint32_t> dirty_pts;
   int64_t batch_tag = -1;  // pred batch id that last used the file (EBUSY detection)
 };
 using FilePtr = std::shared_ptr<File>;
@@ -56,18 +58,21 @@ class Slab {
 
 // Per-descriptor record consumed by the decode kernel (layout shared with csrc/cuda/common.cuh).
 struct DevDesc {
-  int64_t cost_begin;       // first global stage index of this descriptor's units
-  int32_t slab_off;         // entry base of the file's table in the slab
-  int32_t n_old_entries;    // entries holding at least one token retained before this call
-  int32_t n_old;            // retained tokens before this call's append
-  int32_t n_q;              // new tokens (query rows)
-  int32_t row0;             // first packed row of the descriptor
-  int32_t unit_base;        // global unit index of (g=0, qi=0)
-  int32_t stages_per_unit;  // n_old_entries + ceil(n_q / P)
-  int32_t pad0;
-  int64_t pad1;
+  int64_t cost_begin;        // first global stage index of this descriptor's units
+  int32_t slab_off;          // entry base of the file's table in the slab
+  int32_t n_old_entries;     // entries holding at least one token retained before this call
+  int32_t n_old;             // retained tokens before this call's append
+  int32_t n_q;               // new tokens (query rows)
+  int32_t row0;              // first packed row of the descriptor
+  int32_t unit_base;         // global unit index of (g=0, qi=0)
+  int32_t stages_per_unit;   // n_old_entries + ceil(n_q / P)
+  int32_t n_entries;         // entries after the append
+  int32_t tail_lstart;       // logical index of the first token of entry n_old_entries - 1
+  int32_t first_new_entry;   // entry holding logical token n_old (the first new token)
+  int32_t first_new_lstart;  // logical index of that entry's first token
+  int32_t pad0, pad1, pad2;
 };
-static_assert(sizeof(DevDesc) == 48, "DevDesc must be 48 bytes");
+static_assert(sizeof(DevDesc) == 64, "DevDesc must be 64 bytes");
 
 struct SlabRun {
   int64_t dst;    // first slab entry written
@@ -78,7 +83,7 @@ static_assert(sizeof(SlabRun) == 16, "SlabRun must be 16 bytes");
 
 // K2 (tcgen05 chunk kernel) records (layouts shared with csrc/cuda/kernels.cuh)
 struct ChunkDesc {
-  int32_t slab_off, n_entries, n_old, n_q, row0, pad;
+  int32_t slab_off, n_entries, n_old, n_q, row0, first_new_entry, first_new_lstart, pad;
 };
 struct ChunkUnit {
   int32_t desc, g, m, pad;
@@ -140,6 +145,8 @@ int evict_file(Ctx &c, File &f, const int64_t *ranges, int n_ranges, int flags, 
                std::vector<uint32_t> *new_pages);
 int compact_file(Ctx &c, File &f, std::vector<Entry> *old_table, std::vector<uint32_t> *new_pages);
 void recompute_lstart(File &f, size_t from);
+int32_t last_pos(const Ctx &c, const File &f);
+void file_positions(const Ctx &c, const File &f, std::vector<int32_t> *out);
 void release_file_slab(Ctx &c, File &f);
 int audit(Ctx &c);
 
