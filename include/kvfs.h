@@ -204,6 +204,27 @@ int kvfs_read(kvfs_ctx *ctx, int fd, int layer, int64_t begin, int64_t end, void
  * KVFS_EINVAL (and leaves state as is) if an invariant is violated. */
 int kvfs_audit(kvfs_ctx *ctx);
 
+/* ---------------------------------------------------------------- migration */
+/* Pack a file set for transfer to another ctx (another GPU): the set's distinct pages, in ascending
+ * source page id (a page shared by several files of the set is packed once, so CoW sharing inside the
+ * set survives the move; pages shared with files outside the set are duplicated), are gathered into
+ * buf_dev as [n_layers][K, V][n_unique][n_kv_heads][page_size][head_dim] bf16 (device, K6 gather on
+ * `stream`), and hdr (host) receives the tables relative to that order plus positions:
+ *   u32 magic 'KVP1', u32 version 1, u32 n_files, u32 n_unique, u32 P, L, Hkv, D, u64 bytes per page
+ *   per layer per K|V; then per file: u32 n_entries, u32 n_tokens, n_entries x {u32 local page, u32 0,
+ *   u64 mask}, n_tokens x i32 positions (logical order).
+ * The source files are not modified (the caller unlinks them after the transfer).  ENOMEM with
+ * *buf_used / *hdr_used set to the sizes needed if a capacity is too small; EBADF for a bad fd; EBUSY
+ * if a file appears twice.  A host-only ctx packs the header only (buf_dev may be NULL). */
+int kvfs_pack(kvfs_ctx *ctx, const int *fds, int n_fds, void *buf_dev, size_t buf_cap, size_t *buf_used,
+              void *hdr, size_t hdr_cap, size_t *hdr_used, kvfs_stream_t stream);
+/* Create files names[i] from a packed set: n_unique pages are allocated smallest-free first in packed order
+ * (R1), buf_dev is scattered into them (device, on `stream`), tables and positions are rebuilt and the
+ * refcounts count the sharing within the set.  fds_out[i] receives the new fds.  EINVAL for a malformed
+ * header or a shape mismatch, EEXIST if a name exists, ENOSPC if the pages are not free (atomic). */
+int kvfs_unpack(kvfs_ctx *ctx, const void *buf_dev, const void *hdr, size_t hdr_bytes, const char *const *names,
+                int *fds_out, kvfs_stream_t stream);
+
 /* ---------------------------------------------------------------- knobs and counters */
 typedef enum {
   KVFS_OPT_DECODE_CTAS = 1,     /* grid size of the decode kernel; 0 = auto (SM count x occupancy) */

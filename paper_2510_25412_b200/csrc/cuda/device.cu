@@ -125,6 +125,22 @@ __global__ void compact_kernel(const dev::Entry *old, int n_old, const uint32_t 
   }
 }
 
+// K6: whole pages <-> a packed buffer [L][K, V][n][page_elems] (migration pack / unpack).
+__global__ void pack_kernel(const uint32_t *pages, int n, bf16 *const *kp, bf16 *const *vp, int L, int64_t page_elems,
+                            bf16 *buf, int unpack) {
+  const int b = blockIdx.x;
+  const int j = b % n, rem = b / n, isv = rem & 1, l = rem >> 1;
+  bf16 *pool = isv ? vp[l] : kp[l];
+  uint4 *pg = reinterpret_cast<uint4 *>(pool + static_cast<int64_t>(pages[j]) * page_elems);
+  uint4 *bb = reinterpret_cast<uint4 *>(buf + ((static_cast<int64_t>(l) * 2 + isv) * n + j) * page_elems);
+  const int64_t n16 = page_elems / 8;
+  if (unpack) {
+    for (int64_t i = threadIdx.x; i < n16; i += blockDim.x) pg[i] = bb[i];
+  } else {
+    for (int64_t i = threadIdx.x; i < n16; i += blockDim.x) bb[i] = pg[i];
+  }
+}
+
 // K7: logical tokens [begin, end) of one layer -> dense [n][Hkv][D].
 __global__ void read_kernel(const dev::Entry *t, int n_ent, int64_t begin, int64_t end, const bf16 *kpl,
                             const bf16 *vpl, bf16 *kout, bf16 *vout, int Hkv, int D, int P) {
@@ -319,6 +335,28 @@ class CudaDevice final : public Device {
   }
 
   int sync() override { return cudaDeviceSynchronize() == cudaSuccess ? KVFS_OK : KVFS_EIO; }
+
+  int pack_pages(const std::vector<uint32_t> &pages, void *buf, kvfs_stream_t s) override {
+    return pack_impl(pages, buf, 0, s);
+  }
+  int unpack_pages(const std::vector<uint32_t> &pages, const void *buf, kvfs_stream_t s) override {
+    return pack_impl(pages, const_cast<void *>(buf), 1, s);
+  }
+  int pack_impl(const std::vector<uint32_t> &pages, void *buf, int unpack, kvfs_stream_t s) {
+    begin_packet();
+    const void *dp = push(pages.data(), pages.size() * sizeof(uint32_t));
+    if (!dp) return KVFS_ENOMEM;
+    if (!send(s)) return KVFS_EIO;
+    const kvfs_config &cfg = c_.cfg;
+    const int64_t page_elems = static_cast<int64_t>(cfg.n_kv_heads) * cfg.page_size * cfg.head_dim;
+    const int64_t blocks = static_cast<int64_t>(pages.size()) * cfg.n_layers * 2;
+    pack_kernel<<<static_cast<unsigned>(blocks), 256, 0, cs(s)>>>(static_cast<const uint32_t *>(dp),
+                                                                  static_cast<int>(pages.size()), kptrs_, vptrs_,
+                                                                  cfg.n_layers, page_elems, static_cast<bf16 *>(buf),
+                                                                  unpack);
+    ++c_.ctr.launches;
+    return cudaGetLastError() == cudaSuccess ? KVFS_OK : KVFS_EIO;
+  }
 
   // K2: scatter the chunk descriptors' new rows into the pool, then tcgen05 attention from the pool.
   int chunk_layer(const PredPlan &pl, int layer, const void *q, const void *k_new, const void *v_new, void *out,

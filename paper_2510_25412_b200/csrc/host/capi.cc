@@ -364,6 +364,45 @@ int kvfs_audit(kvfs_ctx *ctx) {
   return audit(c);
 }
 
+int kvfs_pack(kvfs_ctx *ctx, const int *fds, int n_fds, void *buf_dev, size_t buf_cap, size_t *buf_used, void *hdr,
+              size_t hdr_cap, size_t *hdr_used, kvfs_stream_t stream) {
+  KVFS_LOCK_OR(ctx);
+  if (c.dev && c.poisoned) return KVFS_EIO;
+  std::vector<uint32_t> pages;
+  std::vector<uint8_t> h;
+  const int rc = pack_files(c, fds, n_fds, &pages, &h);
+  if (rc != KVFS_OK) return rc;
+  const size_t need = pages.size() * static_cast<size_t>(c.cfg.n_layers) * 2 * c.cfg.n_kv_heads * c.cfg.page_size *
+                      c.cfg.head_dim * 2;
+  if (buf_used) *buf_used = c.dev ? need : 0;
+  if (hdr_used) *hdr_used = h.size();
+  if (!hdr || hdr_cap < h.size()) return KVFS_ENOMEM;
+  if (c.dev && need > 0 && (!buf_dev || buf_cap < need)) return KVFS_ENOMEM;
+  std::memcpy(hdr, h.data(), h.size());
+  if (c.dev && !pages.empty()) {
+    const int drc = c.dev->pack_pages(pages, buf_dev, stream);
+    if (drc != KVFS_OK) c.poisoned = true;
+    return drc;
+  }
+  return KVFS_OK;
+}
+
+int kvfs_unpack(kvfs_ctx *ctx, const void *buf_dev, const void *hdr, size_t hdr_bytes, const char *const *names,
+                int *fds_out, kvfs_stream_t stream) {
+  KVFS_LOCK_OR(ctx);
+  if (c.dev && c.poisoned) return KVFS_EIO;
+  if (c.dev && !buf_dev) return KVFS_EINVAL;
+  std::vector<uint32_t> pages;
+  const int rc = unpack_files(c, hdr, hdr_bytes, names, fds_out, &pages);
+  if (rc != KVFS_OK) return rc;
+  if (c.dev && !pages.empty()) {
+    const int drc = c.dev->unpack_pages(pages, buf_dev, stream);
+    if (drc != KVFS_OK) c.poisoned = true;
+    return drc;
+  }
+  return KVFS_OK;
+}
+
 int kvfs_set_option(kvfs_ctx *ctx, int option, int64_t value) {
   KVFS_LOCK_OR(ctx);
   switch (option) {

@@ -150,6 +150,11 @@ void file_positions(const Ctx &c, const File &f, std::vector<int32_t> *out);
 void release_file_slab(Ctx &c, File &f);
 int audit(Ctx &c);
 
+// ---- migration (migrate.cc)
+int pack_files(Ctx &c, const int *fds, int n, std::vector<uint32_t> *pages, std::vector<uint8_t> *hdr);
+int unpack_files(Ctx &c, const void *hdr, size_t hdr_bytes, const char *const *names, int *fds_out,
+                 std::vector<uint32_t> *new_pages);
+
 // ---- batched pred (batch.cc)
 int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos, int *status, PredPlan *plan);
 // Move descriptors with n_q >= cutover (0: none) from the K1 list to the K2 list (D = 128 only).
@@ -168,6 +173,8 @@ class Device {
   virtual int pred_begin(PredPlan &plan, kvfs_stream_t s) = 0;
   virtual int pred_layer(const PredPlan &plan, int layer, const void *q, const void *k_new, const void *v_new,
                          void *out, float *lse, float scale, kvfs_stream_t s) = 0;
+  virtual int pack_pages(const std::vector<uint32_t> &pages, void *buf, kvfs_stream_t s) = 0;
+  virtual int unpack_pages(const std::vector<uint32_t> &pages, const void *buf, kvfs_stream_t s) = 0;
   virtual int sync() = 0;
 };
 

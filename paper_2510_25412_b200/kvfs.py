@@ -30,7 +30,7 @@ EXPORTS = [
     "kvfs_unlink", "kvfs_fork", "kvfs_truncate", "kvfs_evict", "kvfs_compact", "kvfs_append",
     "pred_attn_batch", "pred_step_begin", "pred_attn_layer", "pred_step_end", "kvfs_stat",
     "kvfs_get_table", "kvfs_get_positions", "kvfs_get_refcounts", "kvfs_free_pages", "kvfs_read",
-    "kvfs_audit", "kvfs_set_option", "kvfs_get_counter",
+    "kvfs_audit", "kvfs_set_option", "kvfs_get_counter", "kvfs_pack", "kvfs_unpack",
 ]
 
 
@@ -94,6 +94,9 @@ def lib():
             "kvfs_audit": (cint, [vp]),
             "kvfs_set_option": (cint, [vp, cint, i64]),
             "kvfs_get_counter": (cint, [vp, cint, P(i64)]),
+            "kvfs_pack": (cint, [vp, P(cint), cint, vp, ctypes.c_size_t, P(ctypes.c_size_t), vp, ctypes.c_size_t,
+                                 P(ctypes.c_size_t), vp]),
+            "kvfs_unpack": (cint, [vp, vp, vp, ctypes.c_size_t, P(ctypes.c_char_p), P(cint), vp]),
         }
         for name, (res, args) in sigs.items():
             f = getattr(L, name)
@@ -325,6 +328,32 @@ class KVFS:
 
     def set_option(self, option: int, value: int) -> None:
         _check(lib().kvfs_set_option(self._h, option, value), "set_option")
+
+    # ------------------------------------------------------------------ migration
+    def pack(self, fds: Sequence[int], stream=None):
+        """Pack a file set: returns (header bytes, device uint8 buffer or None on a host-only ctx)."""
+        arr = (ctypes.c_int * max(1, len(fds)))(*fds)
+        bu, hu = ctypes.c_size_t(), ctypes.c_size_t()
+        st = _stream(stream) if self.device >= 0 else None
+        rc = lib().kvfs_pack(self._h, arr, len(fds), None, 0, ctypes.byref(bu), None, 0, ctypes.byref(hu), st)
+        if rc not in (OK, ENOMEM):
+            raise KvfsError(rc, "pack")
+        hdr = ctypes.create_string_buffer(max(1, hu.value))
+        buf = None
+        if self.device >= 0:
+            import torch
+            buf = torch.empty(max(16, bu.value), dtype=torch.uint8, device=self.k_pool[0].device)
+        _check(lib().kvfs_pack(self._h, arr, len(fds), _dptr(buf), 0 if buf is None else buf.numel(),
+                               ctypes.byref(bu), hdr, len(hdr), ctypes.byref(hu), st), "pack")
+        return hdr.raw[:hu.value], buf
+
+    def unpack(self, hdr: bytes, buf, names: Sequence[str], stream=None) -> List[int]:
+        n = len(names)
+        nm = (ctypes.c_char_p * max(1, n))(*[x.encode() for x in names])
+        fds = (ctypes.c_int * max(1, n))()
+        st = _stream(stream) if self.device >= 0 else None
+        _check(lib().kvfs_unpack(self._h, _dptr(buf), hdr, len(hdr), nm, fds, st), "unpack")
+        return list(fds[:n])
 
     def counter(self, which: int) -> int:
         v = ctypes.c_int64()

@@ -233,3 +233,48 @@ def test_chunk_autocompletion_shape():
             rows.append((f"f{i}", list(range(last + 1, last + 65))))
         h.pred(rows, qstd=1.0)
     h.check_meta()
+
+
+def test_migration_pack_unpack_two_ctx():
+    """§8(e) data path with two ctxs on one GPU (the NCCL transport replaced by the buffer itself): the
+    moved files' K/V bits, masks and positions survive; decode on the destination matches the oracle."""
+    from paper_2510_25412_b200 import kvfs as K
+
+    h = Harness(600, 16, 32, 8, 128, seed=21)
+    h.open("base")
+    h.append("base", list(range(300)))
+    h.fork("base", "child")
+    h.pred([("child", [300, 301, 302])])
+    h.evict("base", [(10, 40)])
+    h.open("other")
+    h.append("other", list(range(77)))
+    names = ["base", "child", "other"]
+    hdr, buf = h.c.pack([h.fds[n][0] for n in names])
+    dst = K.KVFS(1, 32, 8, 128, 16, 500, device=0)
+    dst.open("pre-existing")  # the destination allocates smallest-free pages around its own state
+    fds = dst.unpack(hdr, buf, names)
+    torch.cuda.synchronize()
+    dst.audit()
+    for n, fd in zip(names, fds):
+        ofd = h.fds[n][1]
+        assert [m for _, m in dst.table(fd)] == [m for _, m in h.o.table(ofd)]
+        assert dst.positions(fd) == h.o.positions(ofd)
+        ln = h.o.stat(ofd)[0]
+        k, v = dst.read(fd, 0, 0, ln)
+        ko, vo = h.o.read(ofd, 0, 0, ln)
+        assert np.array_equal(to_bits(k), ko) and np.array_equal(to_bits(v), vo)
+    shared = {p for p, _ in dst.table(fds[0])} & {p for p, _ in dst.table(fds[1])}
+    rc = dst.refcounts()
+    assert shared and all(rc[p] == 2 for p in shared)  # CoW sharing preserved
+    # a decode step on the destination == the oracle (source state) on the same inputs
+    rows = [(n, [h.o.stat(h.fds[n][1])[2] + 1]) for n in names]
+    k_new, v_new = h._kv(3)
+    q = h._q(3, 4.0)
+    out = torch.empty((3, 32, 128), dtype=torch.bfloat16, device="cuda")
+    st = dst.pred_attn_batch([(fd, 1) for fd in fds], [r[1][0] for r in rows], to_dev(q[0]), to_dev(k_new[0]),
+                             to_dev(v_new[0]), out)
+    torch.cuda.synchronize()
+    assert st == [0, 0, 0]
+    _, ref, _ = h.o.pred_batch([(h.fds[n][1], 1) for n in names], [r[1][0] for r in rows], q, k_new, v_new,
+                               128 ** -0.5)
+    assert_close(to_bits(out), ref[0], "migrated decode")
