@@ -139,45 +139,74 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap *map
 
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// A operand from TMEM (P aliasing the S columns): D[tmem] (+)= A[tmem] * B[smem]
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+
 }  // namespace tc
 
+// v2 layout: one CTA = (descriptor, kv head, pair of 128-row M-tiles) sharing every K/V tile.
+// TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); P_m aliases the first 64 columns of S_m.
+namespace tc2 {
+constexpr int THREADS = 384;  // warps 0-3: K producer, MMA, TMEM alloc, V producer; 4-7, 8-11: softmax M-tiles
+constexpr int KV2 = 2;        // K stages and V stages (independent rings)
+constexpr int JR = 4;         // column-metadata ring
+constexpr uint32_t O_COL2 = 256;
+constexpr int OFF_Q2 = 0;                                   // 2 Q tiles
+constexpr int OFF_K2 = OFF_Q2 + 2 * tc::TILE_BYTES;         // KV2 K tiles
+constexpr int OFF_V2 = OFF_K2 + KV2 * tc::TILE_BYTES;       // KV2 V tiles
+constexpr int OFF_JCOL2 = OFF_V2 + KV2 * tc::TILE_BYTES;    // JR x BN int32
+constexpr int OFF_BAR2 = OFF_JCOL2 + JR * tc::BN * 4;
+constexpr int N_BARS2 = 1 + 4 * KV2 + 6 + JR;
+constexpr int OFF_TMEM2 = OFF_BAR2 + N_BARS2 * 8;
+constexpr int SMEM2 = OFF_TMEM2 + 16 + 1024;
+}  // namespace tc2
+
 template <int G>
-__global__ void __launch_bounds__(tc::THREADS, 1)
+__global__ void __launch_bounds__(tc2::THREADS, 1)
     chunk_attn_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                          const __grid_constant__ CUtensorMap qmap, const ChunkParams p) {
   using namespace tc;
+  using namespace tc2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
-  const uint32_t q_full = smem_u32(bars + 0);
-  auto kv_full = [&](int s) { return smem_u32(bars + 1 + s); };
-  auto kv_empty = [&](int s) { return smem_u32(bars + 1 + KV_STAGES + s); };
-  auto s_full = [&](int b) { return smem_u32(bars + 1 + 2 * KV_STAGES + b); };
-  auto s_empty = [&](int b) { return smem_u32(bars + 3 + 2 * KV_STAGES + b); };
-  const uint32_t p_full = smem_u32(bars + 5 + 2 * KV_STAGES);
-  const uint32_t o_full = smem_u32(bars + 6 + 2 * KV_STAGES);
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + OFF_TMEM);
-  int32_t *jcol_all = reinterpret_cast<int32_t *>(smem + OFF_JCOL);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR2);
+  auto bar = [&](int i) { return smem_u32(bars + i); };
+  // barrier indices
+  constexpr int B_Q = 0, B_KF = 1, B_KE = 1 + KV2, B_VF = 1 + 2 * KV2, B_VE = 1 + 3 * KV2, B_SF = 1 + 4 * KV2,
+                B_PF = B_SF + 2, B_OF = B_PF + 2, B_JF = B_OF + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + OFF_TMEM2);
+  int32_t *jcol_all = reinterpret_cast<int32_t *>(smem + OFF_JCOL2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const ChunkUnit u = p.units[blockIdx.x];
   const ChunkDesc cd = p.descs[u.desc];
   const int epb = BN / p.P;  // page entries per KV tile
   const int n_tiles = (cd.n_entries + epb - 1) / epb;
+  const int rows_total = cd.n_q * G;
+  const int m0 = 2 * u.m;                                     // first M-tile of this CTA
+  const int n_mt = min(2, (rows_total + BM - 1) / BM - m0);  // 1 or 2 M-tiles
 
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    for (int s = 0; s < KV_STAGES; ++s) {
-      mbar_init(kv_full(s), 1);
-      mbar_init(kv_empty(s), 1);
+    mbar_init(bar(B_Q), 1);
+    for (int s = 0; s < KV2; ++s) {
+      mbar_init(bar(B_KF + s), 1);
+      mbar_init(bar(B_KE + s), 1);
+      mbar_init(bar(B_VF + s), 1);
+      mbar_init(bar(B_VE + s), 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(s_full(b), 1);
-      mbar_init(s_empty(b), 4);  // one arrive per softmax warp
+    for (int m = 0; m < 2; ++m) {
+      mbar_init(bar(B_SF + m), 1);
+      mbar_init(bar(B_PF + m), 4);
+      mbar_init(bar(B_OF + m), 1);
     }
-    mbar_init(p_full, 4);
-    mbar_init(o_full, 1);
+    for (int j = 0; j < JR; ++j) mbar_init(bar(B_JF + j), 1);
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -190,196 +219,229 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    // ================================================================ TMA producer
-    const uint64_t pol = policy_evict_first();
-    if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, TILE_BYTES);
-      const int qrow = cd.row0 + (u.m * BM) / G;
-      tma_load_4d(sbase + OFF_Q, &qmap, 0, 0, u.g, qrow, q_full);
-      tma_load_4d(sbase + OFF_Q + HALF_BYTES, &qmap, 64, 0, u.g, qrow, q_full);
-    }
-    for (int t = 0; t < n_tiles; ++t) {
-      const int s = t % KV_STAGES;
-      if (t >= KV_STAGES) mbar_wait_sleep(kv_empty(s), ((t / KV_STAGES) & 1) ^ 1);
-      // column metadata: j = logical index - n_old for a retained slot (<= qi is visible), INT_MAX otherwise
-      int32_t *jcol = jcol_all + s * BN;
-      for (int c = lane; c < BN; c += 32) {
-        const int e = t * epb + c / p.P, slot = c % p.P;
-        int32_t j = 0x7fffffff;
-        if (e < cd.n_entries) {
-          const Entry en = p.slab[cd.slab_off + e];
-          if ((en.mask >> slot) & 1ull) {
-            if (e < cd.first_new_entry) {
-              j = -1;  // an old token: visible to every query row
-            } else {
-              // logical index = first_new_lstart + tokens of the new-region entries before e + rank in e
-              int lg = cd.first_new_lstart + __popcll(en.mask & ((1ull << slot) - 1ull));
-              for (int e2 = cd.first_new_entry; e2 < e; ++e2) lg += __popcll(p.slab[cd.slab_off + e2].mask);
-              j = lg - cd.n_old;
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    if (warp == 0) {
+      // ============================================================ K producer (+ Q, + column metadata)
+      const uint64_t pol = policy_evict_first();
+      if (lane == 0) {
+        mbar_arrive_expect_tx(bar(B_Q), n_mt * TILE_BYTES);
+        for (int m = 0; m < n_mt; ++m) {
+          const int qrow = cd.row0 + ((m0 + m) * BM) / G;
+          tma_load_4d(sbase + OFF_Q2 + m * TILE_BYTES, &qmap, 0, 0, u.g, qrow, bar(B_Q));
+          tma_load_4d(sbase + OFF_Q2 + m * TILE_BYTES + HALF_BYTES, &qmap, 64, 0, u.g, qrow, bar(B_Q));
+        }
+      }
+      for (int t = 0; t < n_tiles; ++t) {
+        const int s = t % KV2;
+        if (t >= KV2) mbar_wait_sleep(bar(B_KE + s), ((t / KV2) & 1) ^ 1);
+        // column metadata of tile t: j = logical index - n_old (visible iff j <= qi), INT_MAX = no key
+        int32_t *jcol = jcol_all + (t % JR) * BN;
+        for (int c = lane; c < BN; c += 32) {
+          const int e = t * epb + c / p.P, slot = c % p.P;
+          int32_t j = 0x7fffffff;
+          if (e < cd.n_entries) {
+            const Entry en = p.slab[cd.slab_off + e];
+            if ((en.mask >> slot) & 1ull) {
+              if (e < cd.first_new_entry) {
+                j = -1;
+              } else {
+                int lg = cd.first_new_lstart + __popcll(en.mask & ((1ull << slot) - 1ull));
+                for (int e2 = cd.first_new_entry; e2 < e; ++e2) lg += __popcll(p.slab[cd.slab_off + e2].mask);
+                j = lg - cd.n_old;
+              }
             }
           }
+          jcol[c] = j;
         }
-        jcol[c] = j;
-      }
-      __syncwarp();
-      if (lane == 0) {
-        mbar_arrive_expect_tx(kv_full(s), 2 * TILE_BYTES);
-        for (int i = 0; i < epb; ++i) {
-          const int e = t * epb + i;
-          // rows past the table: an out-of-bounds box (zero-filled by TMA)
-          const int row = e < cd.n_entries ? (static_cast<int>(p.slab[cd.slab_off + e].page) * p.Hkv + u.g) * p.P
-                                           : p.pool_rows;
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t off = h * HALF_BYTES + i * p.P * 128;
-            tma_load_2d(sbase + OFF_K + s * TILE_BYTES + off, &kmap, h * 64, row, kv_full(s), pol);
-            tma_load_2d(sbase + OFF_V + s * TILE_BYTES + off, &vmap, h * 64, row, kv_full(s), pol);
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(bar(B_JF + t % JR));
+          mbar_arrive_expect_tx(bar(B_KF + s), TILE_BYTES);
+          for (int i = 0; i < epb; ++i) {
+            const int e = t * epb + i;
+            const int row = e < cd.n_entries ? (static_cast<int>(p.slab[cd.slab_off + e].page) * p.Hkv + u.g) * p.P
+                                             : p.pool_rows;
+            for (int h = 0; h < 2; ++h)
+              tma_load_2d(sbase + OFF_K2 + s * TILE_BYTES + h * HALF_BYTES + i * p.P * 128, &kmap, h * 64, row,
+                          bar(B_KF + s), pol);
           }
         }
+        __syncwarp();
       }
-      __syncwarp();
-    }
-  } else if (warp == 1) {
-    // ================================================================ MMA issuer
-    constexpr uint32_t ID_S = idesc_bf16(false), ID_O = idesc_bf16(true);
-    mbar_wait(q_full, 0);
-    auto issue_s = [&](int t) {
-      const int s = t % KV_STAGES, b = t & 1;
-      mbar_wait(kv_full(s), (t / KV_STAGES) & 1);
-      if (t >= 2) mbar_wait(s_empty(b), ((t >> 1) & 1) ^ 1);
-      tc_fence_after();
-      if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < HD / 16; ++k) {
-          const uint32_t koff = (k >> 2) * HALF_BYTES + (k & 3) * 32;
-          mma_bf16(tmem + S_COL0 + b * BN, umma_desc(sbase + OFF_Q + koff, 16, 1024),
-                   umma_desc(sbase + OFF_K + s * TILE_BYTES + koff, 16, 1024), ID_S, k > 0);
+    } else if (warp == 3) {
+      // ============================================================ V producer
+      const uint64_t pol = policy_evict_first();
+      for (int t = 0; t < n_tiles; ++t) {
+        const int s = t % KV2;
+        if (t >= KV2) mbar_wait_sleep(bar(B_VE + s), ((t / KV2) & 1) ^ 1);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(bar(B_VF + s), TILE_BYTES);
+          for (int i = 0; i < epb; ++i) {
+            const int e = t * epb + i;
+            const int row = e < cd.n_entries ? (static_cast<int>(p.slab[cd.slab_off + e].page) * p.Hkv + u.g) * p.P
+                                             : p.pool_rows;
+            for (int h = 0; h < 2; ++h)
+              tma_load_2d(sbase + OFF_V2 + s * TILE_BYTES + h * HALF_BYTES + i * p.P * 128, &vmap, h * 64, row,
+                          bar(B_VF + s), pol);
+          }
         }
-        mma_commit(s_full(b));
+        __syncwarp();
       }
-      __syncwarp();
-    };
-    issue_s(0);
-    for (int t = 0; t < n_tiles; ++t) {
-      if (t + 1 < n_tiles) issue_s(t + 1);
-      const int s = t % KV_STAGES;
-      mbar_wait(p_full, t & 1);  // softmax wrote P_t (and corrected O)
-      tc_fence_after();
-      if (lane == 0) {
+    } else if (warp == 1) {
+      // ============================================================ MMA issuer
+      constexpr uint32_t ID_S = idesc_bf16(false), ID_O = idesc_bf16(true);
+      mbar_wait(bar(B_Q), 0);
+      auto issue_s = [&](int t, int m) {
+        tc_fence_after();
+        if (lane == 0) {
 #pragma unroll
-        for (int k = 0; k < BN / 16; ++k) {
-          const uint32_t poff = (k >> 2) * HALF_BYTES + (k & 3) * 32;
-          mma_bf16(tmem + O_COL, umma_desc(sbase + OFF_P + poff, 16, 1024),
-                   umma_desc(sbase + OFF_V + s * TILE_BYTES + k * 2048, HALF_BYTES, 1024), ID_O, (t > 0 || k > 0));
+          for (int k = 0; k < HD / 16; ++k) {
+            const uint32_t koff = (k >> 2) * HALF_BYTES + (k & 3) * 32;
+            mma_bf16(tmem + m * BN, umma_desc(sbase + OFF_Q2 + m * TILE_BYTES + koff, 16, 1024),
+                     umma_desc(sbase + OFF_K2 + (t % KV2) * TILE_BYTES + koff, 16, 1024), ID_S, k > 0);
+          }
+          mma_commit(bar(B_SF + m));
         }
-        mma_commit(o_full);
-        mma_commit(kv_empty(s));
-      }
-      __syncwarp();
-    }
-  } else if (warp >= 4) {
-    // ================================================================ softmax + epilogue (thread = row)
-    const int wq = warp - 4;                 // TMEM lane quarter
-    const int r = wq * 32 + lane;            // row within the M-tile
-    const int R = u.m * BM + r;
-    const int qi = R / G, h = R % G;
-    const bool live = qi < cd.n_q;
-    const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
-    float m_run = -CUDART_INF_F, l_run = 0.f;
-    uint8_t *prow = smem + OFF_P + r * 128;  // row r of both 64-column halves (+HALF_BYTES)
-    for (int t = 0; t < n_tiles; ++t) {
-      const int b = t & 1, s = t % KV_STAGES;
-      mbar_wait(s_full(b), (t >> 1) & 1);
-      tc_fence_after();
-      float x[BN];
+        __syncwarp();
+      };
+      auto issue_pv = [&](int t, int m) {
+        tc_fence_after();
+        if (lane == 0) {
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
+          for (int k = 0; k < BN / 16; ++k)
+            mma_bf16_ts(tmem + O_COL2 + m * HD, tmem + m * BN + k * 8,
+                        umma_desc(sbase + OFF_V2 + (t % KV2) * TILE_BYTES + k * 2048, HALF_BYTES, 1024), ID_O,
+                        (t > 0 || k > 0));
+          mma_commit(bar(B_OF + m));
+        }
+        __syncwarp();
+      };
+      mbar_wait(bar(B_KF + 0), 0);
+      for (int m = 0; m < n_mt; ++m) issue_s(0, m);
+      if (lane == 0) mma_commit(bar(B_KE + 0));
+      __syncwarp();
+      for (int t = 0; t < n_tiles; ++t) {
+        const int s = t % KV2;
+        mbar_wait(bar(B_VF + s), (t / KV2) & 1);
+        const bool more = t + 1 < n_tiles;
+        if (more) mbar_wait(bar(B_KF + (t + 1) % KV2), ((t + 1) / KV2) & 1);
+        for (int m = 0; m < n_mt; ++m) {
+          mbar_wait(bar(B_PF + m), t & 1);  // softmax m wrote P(t) into TMEM (and corrected O)
+          issue_pv(t, m);
+          if (more) issue_s(t + 1, m);      // in-order after PV(t): S(t+1) may overwrite P(t)'s columns
+        }
+        if (lane == 0) {
+          if (more) mma_commit(bar(B_KE + (t + 1) % KV2));
+          mma_commit(bar(B_VE + s));
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    // ============================================================ softmax warpgroups (thread = row)
+    const int m = (warp - 4) >> 2;          // M-tile of this warpgroup
+    const int wq = (warp - 4) & 3;          // TMEM lane quarter
+    if (m < n_mt) {
+      const int r = wq * 32 + lane;
+      const int R = (m0 + m) * BM + r;
+      const int qi = R / G, h = R % G;
+      const bool live = qi < cd.n_q;
+      const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
+      const uint32_t s_col = tmem + lane_addr + m * BN;
+      const uint32_t o_col = tmem + lane_addr + O_COL2 + m * HD;
+      float m_run = -CUDART_INF_F, l_run = 0.f;
+      for (int t = 0; t < n_tiles; ++t) {
+        mbar_wait(bar(B_SF + m), t & 1);
+        tc_fence_after();
+        float x[BN];
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) {
+          float v[32];
+          tmem_ld32(s_col + c * 32, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) x[c * 32 + i] = v[i];
+        }
+        tmem_wait_ld();
+        mbar_wait(bar(B_JF + t % JR), (t / JR) & 1);
+        const int32_t *jcol = jcol_all + (t % JR) * BN;
+        float mx = -CUDART_INF_F;
+#pragma unroll
+        for (int c = 0; c < BN; ++c) {
+          const float v = (jcol[c] <= qi) ? x[c] * p.scale_log2 : -CUDART_INF_F;
+          x[c] = v;
+          mx = fmaxf(mx, v);
+        }
+        if (t > 0) mbar_wait(bar(B_OF + m), (t - 1) & 1);  // PV(t-1) done: O stable
+        tc_fence_after();
+        const bool need = mx > m_run + 8.f;
+        if (__any_sync(0xffffffffu, need)) {
+          const float mn = need ? mx : m_run;
+          const float a = (need && m_run != -CUDART_INF_F) ? fast_exp2(m_run - mn) : (need ? 0.f : 1.f);
+          if (t > 0) {
+#pragma unroll
+            for (int c = 0; c < HD / 32; ++c) {
+              float v[32];
+              tmem_ld32(o_col + c * 32, v);
+              tmem_wait_ld();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] *= a;
+              tmem_st32(o_col + c * 32, v);
+            }
+          }
+          l_run *= a;
+          m_run = mn;
+        }
+        const float mref = m_run == -CUDART_INF_F ? 0.f : m_run;
+        // P = exp2(x - m) -> bf16 pairs into the first 64 columns of this tile's S (A operand of P.V)
+        float ls = 0.f;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          float w[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float p0 = fast_exp2(x[c * 64 + 2 * i] - mref);
+            const float p1 = fast_exp2(x[c * 64 + 2 * i + 1] - mref);
+            ls += p0 + p1;
+            __nv_bfloat162 pr = __floats2bfloat162_rn(p0, p1);
+            w[i] = __uint_as_float(*reinterpret_cast<uint32_t *>(&pr));
+          }
+          tmem_st32(s_col + c * 32, w);
+        }
+        l_run += ls;
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(B_PF + m));
+      }
+      // epilogue: O / l -> bf16 out, lse
+      mbar_wait(bar(B_OF + m), (n_tiles - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l_run;
+      const int64_t orow = (static_cast<int64_t>(cd.row0 + qi) * p.Hq + u.g * G + h) * HD;
+#pragma unroll
+      for (int c = 0; c < HD / 32; ++c) {
         float v[32];
-        tmem_ld32(tmem + lane_addr + S_COL0 + b * BN + c * 32, v);
+        tmem_ld32(o_col + c * 32, v);
+        tmem_wait_ld();
+        if (live) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) x[c * 32 + i] = v[i];
-      }
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(s_empty(b));
-      const int32_t *jcol = jcol_all + s * BN;
-      float mx = -CUDART_INF_F;
+          for (int i = 0; i < 32; i += 8) {
+            uint32_t w[4];
 #pragma unroll
-      for (int c = 0; c < BN; ++c) {
-        const float v = (jcol[c] <= qi) ? x[c] * p.scale_log2 : -CUDART_INF_F;
-        x[c] = v;
-        mx = fmaxf(mx, v);
-      }
-      // P_{t-1}.V must be complete before O is corrected and P is overwritten
-      if (t > 0) mbar_wait(o_full, (t - 1) & 1);
-      tc_fence_after();
-      const bool need = mx > m_run + 8.f;
-      if (__any_sync(0xffffffffu, need)) {
-        const float mn = need ? mx : m_run;
-        const float a = (need && m_run != -CUDART_INF_F) ? fast_exp2(m_run - mn) : (need ? 0.f : 1.f);
-        if (t > 0) {
-#pragma unroll
-          for (int c = 0; c < HD / 32; ++c) {
-            float v[32];
-            tmem_ld32(tmem + lane_addr + O_COL + c * 32, v);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] *= a;
-            tmem_st32(tmem + lane_addr + O_COL + c * 32, v);
+            for (int j = 0; j < 4; ++j) {
+              __nv_bfloat162 pr = __floats2bfloat162_rn(v[i + 2 * j] * inv, v[i + 2 * j + 1] * inv);
+              w[j] = *reinterpret_cast<uint32_t *>(&pr);
+            }
+            *reinterpret_cast<uint4 *>(p.out + orow + c * 32 + i) = make_uint4(w[0], w[1], w[2], w[3]);
           }
-          tmem_wait_st();
         }
-        l_run *= a;
-        m_run = mn;
       }
-      // P = exp2(x - m) -> bf16, 128B-swizzled K-major rows
-      float ls = 0.f;
-#pragma unroll
-      for (int c8 = 0; c8 < BN / 8; ++c8) {
-        uint32_t w[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float p0 = fast_exp2(x[c8 * 8 + 2 * i] - m_run);
-          const float p1 = fast_exp2(x[c8 * 8 + 2 * i + 1] - m_run);
-          ls += p0 + p1;
-          __nv_bfloat162 pr = __floats2bfloat162_rn(p0, p1);
-          w[i] = *reinterpret_cast<uint32_t *>(&pr);
-        }
-        const int half = c8 >> 3, chunk = c8 & 7;
-        uint4 *dst = reinterpret_cast<uint4 *>(prow + half * HALF_BYTES + ((chunk ^ (r & 7)) << 4));
-        *dst = make_uint4(w[0], w[1], w[2], w[3]);
-      }
-      l_run += ls;
-      fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor core (async proxy)
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (live && p.lse)
+        p.lse[static_cast<int64_t>(cd.row0 + qi) * p.Hq + u.g * G + h] =
+            (m_run + __log2f(l_run)) * 0.69314718055994531f;
     }
-    // epilogue: O / l -> bf16 out, lse
-    mbar_wait(o_full, (n_tiles - 1) & 1);
-    tc_fence_after();
-    const float inv = 1.f / l_run;
-    const int64_t orow = (static_cast<int64_t>(cd.row0 + qi) * p.Hq + u.g * G + h) * HD;
-#pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
-      float v[32];
-      tmem_ld32(tmem + lane_addr + O_COL + c * 32, v);
-      tmem_wait_ld();
-      if (live) {
-#pragma unroll
-        for (int i = 0; i < 32; i += 8) {
-          uint32_t w[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            __nv_bfloat162 pr = __floats2bfloat162_rn(v[i + 2 * j] * inv, v[i + 2 * j + 1] * inv);
-            w[j] = *reinterpret_cast<uint32_t *>(&pr);
-          }
-          *reinterpret_cast<uint4 *>(p.out + orow + c * 32 + i) = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-      }
-    }
-    if (live && p.lse) p.lse[static_cast<int64_t>(cd.row0 + qi) * p.Hq + u.g * G + h] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
   }
   tc_fence_before();
   __syncthreads();
@@ -419,7 +481,7 @@ cudaError_t launch_scatter_rows(const int32_t *dst, int T, const __nv_bfloat16 *
   return cudaGetLastError();
 }
 
-int chunk_smem_bytes() { return tc::SMEM_BYTES; }
+int chunk_smem_bytes() { return tc2::SMEM2; }
 
 template <int G>
 static cudaError_t launch_chunk_g(const CUtensorMap &km, const CUtensorMap &vm, const CUtensorMap &qm,
@@ -427,11 +489,11 @@ static cudaError_t launch_chunk_g(const CUtensorMap &km, const CUtensorMap &vm, 
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(chunk_attn_tc_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         tc::SMEM_BYTES);
+                                         tc2::SMEM2);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  chunk_attn_tc_kernel<G><<<n_units, tc::THREADS, tc::SMEM_BYTES, s>>>(km, vm, qm, p);
+  chunk_attn_tc_kernel<G><<<n_units, tc2::THREADS, tc2::SMEM2, s>>>(km, vm, qm, p);
   return cudaGetLastError();
 }
 

@@ -144,9 +144,9 @@ void pred_split(const Ctx &c, int64_t cutover, PredPlan *plan) {
       ChunkDesc cd{d.slab_off, d.n_entries, d.n_old, d.n_q, d.row0, d.first_new_entry, d.first_new_lstart, 0};
       const int32_t di = static_cast<int32_t>(pl.chunk_descs.size());
       pl.chunk_descs.push_back(cd);
-      const int mt = (d.n_q * G + 127) / 128;
+      const int mt = (d.n_q * G + 127) / 128;  // 128-row M-tiles; one CTA takes a pair (shared K/V tiles)
       for (int g = 0; g < Hkv; ++g)
-        for (int m = 0; m < mt; ++m) pl.chunk_units.push_back({di, g, m, 0});
+        for (int m = 0; m < (mt + 1) / 2; ++m) pl.chunk_units.push_back({di, g, m, 0});
       for (int r = 0; r < d.n_q; ++r) pl.chunk_dst[d.row0 + r] = pl.dst_slot[d.row0 + r];
       continue;
     }
