@@ -126,6 +126,14 @@ __device__ __forceinline__ float2 mul2(const float2 a, const float2 b) {
   return *reinterpret_cast<float2 *>(&dd);
 }
 
+__device__ __forceinline__ float2 add2(const float2 a, const float2 b) {
+  unsigned long long dd;
+  const unsigned long long aa = *reinterpret_cast<const unsigned long long *>(&a);
+  const unsigned long long bb = *reinterpret_cast<const unsigned long long *>(&b);
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(dd) : "l"(aa), "l"(bb));
+  return *reinterpret_cast<float2 *>(&dd);
+}
+
 // bf16 pair (little-endian u32: element 0 in the low half) -> fp32 pair, exact.
 __device__ __forceinline__ float2 bf2_to_f2(uint32_t w) {
   return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
