@@ -1,6 +1,8 @@
-"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (default grid, cfg2:
-256 LIPs x 2048-token files, Hq 32 / Hkv 8 / D 128 / P 16): sampled descriptors recomputed one by one by the
-oracle from the generator (no input or expected value read back from the CUDA path)."""
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times (default grids, the
+workloads' own per-step LIP policies): cfg2 (256 x 2048 decode), cfg3 (64 forks of a 4096-token CoW
+prefix), cfg4 (128 x 8192, truncate-to-cursor + 64-token re-append through the tcgen05 kernel), cfg5
+(128 x 32768 with sink + window eviction).  Sampled LIPs are recomputed one by one by the oracle from the
+generator (oracle/workload.py); nothing is read back from the CUDA path to build the expectation."""
 import numpy as np
 import pytest
 import torch
@@ -11,53 +13,42 @@ if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs a GPU", allow_module_level=True)
 
 from gpu_harness import assert_close, to_bits  # noqa: E402
-from oracle import Oracle  # noqa: E402
-from paper_2510_25412_b200.workloads import CONFIGS, STEP_OWNER, DecodeWorkload  # noqa: E402
-from synth.workloads import TAG_K, TAG_Q, TAG_V, rows_np  # noqa: E402
+from oracle.workload import OracleWorkload  # noqa: E402
+from paper_2510_25412_b200.workloads import DecodeWorkload  # noqa: E402
 
 
-def oracle_for_lip(cfg, f, n_steps):
-    """The oracle's output for LIP f at decode step n_steps-1 (files built exactly as DecodeWorkload does)."""
-    s = cfg["shape"]
-    L0 = cfg["file_len"]
-    o = Oracle((L0 + n_steps) // s.P + 4, s.P, 1, s.Hkv, s.D)
-    fd = o.open("f")
-    k = rows_np(cfg["seed"], TAG_K, 0, f, 0, L0, s.Hkv * s.D).reshape(1, L0, s.Hkv, s.D)
-    v = rows_np(cfg["seed"], TAG_V, 0, f, 0, L0, s.Hkv * s.D).reshape(1, L0, s.Hkv, s.D)
-    o.append(fd, list(range(L0)), k, v)
-    out = lse = None
-    for st in range(n_steps):
-        own = STEP_OWNER + st
-        q = rows_np(cfg["seed"], TAG_Q, 0, own, f, f + 1, s.Hq * s.D).reshape(1, 1, s.Hq, s.D)
-        kn = rows_np(cfg["seed"], TAG_K, 0, own, f, f + 1, s.Hkv * s.D).reshape(1, 1, s.Hkv, s.D)
-        vn = rows_np(cfg["seed"], TAG_V, 0, own, f, f + 1, s.Hkv * s.D).reshape(1, 1, s.Hkv, s.D)
-        _, out, lse = o.pred_batch([(fd, 1)], [L0 + st], q, kn, vn, s.D ** -0.5)
-    return out[0, 0], lse[0, 0]
-
-
-def test_cfg2_full_size_sampled_parity():
-    cfg = CONFIGS["cfg2"]
-    n_steps = 3
-    wl = DecodeWorkload("cfg2", steps_total=n_steps + 1)
+@pytest.mark.parametrize("cfg,steps,lips", [
+    ("cfg2", 3, [0, 1, 37, 127, 128, 200, 254, 255]),
+    ("cfg3", 3, [0, 31, 63]),
+    ("cfg4", 2, [0, 77, 127]),
+    ("cfg5", 2, [5]),
+])
+def test_full_size_sampled_parity(cfg, steps, lips):
+    wl = DecodeWorkload(cfg, steps_total=steps + 1)
     s = wl.shape
-    T = wl.n_files
+    T = wl.n_files * wl.n_q
     out = torch.empty((T, s.Hq, s.D), dtype=torch.bfloat16, device="cuda")
     lse = torch.empty((T, s.Hq), dtype=torch.float32, device="cuda")
-    for st in range(n_steps):
+    for st in range(steps):
         q, k, v = wl.make_inputs(st)
-        descs, pos = wl.descs_and_pos()
-        status = wl.kv.pred_attn_batch(descs, pos, q, k, v, out, lse)
-        assert status == [0] * T
+        wl.pre_step()
+        status = wl.kv.pred_attn_batch(wl.descs, wl.positions(), q, k, v, out, lse)
+        assert status == [0] * wl.n_files
         wl.advance()
     torch.cuda.synchronize()
-    ob = to_bits(out)
-    lb = lse.cpu().numpy()
+    ob = to_bits(out).reshape(wl.n_files, wl.n_q, s.Hq, s.D)
+    lb = lse.cpu().numpy().reshape(wl.n_files, wl.n_q, s.Hq)
     assert np.isfinite(lb).all()
-    for f in [0, 1, 37, 127, 128, 200, 254, 255]:
-        ref_out, ref_lse = oracle_for_lip(cfg, f, n_steps)
-        assert_close(ob[f], ref_out, f"cfg2 LIP {f}")
-        np.testing.assert_allclose(lb[f], ref_lse, atol=2e-3, rtol=0)
-    # every LIP's file holds exactly its 2048 + 3 positions
-    for f in [0, 255]:
-        assert wl.kv.positions(wl.fds[f]) == list(range(cfg["file_len"] + n_steps))
+    ow = OracleWorkload(cfg, lips, max_steps=steps + 1)
+    for _ in range(steps):
+        st, ref_out, ref_lse = ow.run_step()
+        assert st == [0] * len(lips)
+    for i, f in enumerate(lips):
+        assert_close(ob[f], ref_out[i], f"{cfg} LIP {f}")
+        np.testing.assert_allclose(lb[f], ref_lse[i], atol=2e-3, rtol=0)
+        assert wl.kv.positions(wl.fds[f]) == ow.o.positions(ow.fds[i])
+    if cfg == "cfg3":  # the fan-out shares the prefix: 256 pages referenced by the prefix + 64 forks
+        tab = wl.kv.table(wl.fds[0])
+        rc = wl.kv.refcounts()
+        assert all(rc[p] == 65 for p, _ in tab[:256])
     wl.kv.audit()
