@@ -345,10 +345,116 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def evict_ranges_heavy_hitter(seed: int, f: int, n: int, drop: int, sink: int = 4, recent: int = 1024):
+    """cfg5(ii) policy: evict the `drop` lowest Exp(1) synthetic scores of file f, protecting
+    the first `sink` and last `recent` tokens; ties -> lower index. Returns sorted disjoint [a, b) ranges."""
+    import numpy as np
+
+    from synth import exp1_scores_np, stream_key
+
+    sc = exp1_scores_np(stream_key(seed, 4, 0, f), 0, n)
+    sc[:sink] = np.inf
+    sc[n - recent:] = np.inf
+    idx = np.sort(np.argsort(sc, kind="stable")[:drop])
+    brk = np.nonzero(np.diff(idx) != 1)[0]
+    starts = np.concatenate([[idx[0]], idx[brk + 1]])
+    ends = np.concatenate([idx[brk], [idx[-1]]]) + 1
+    return np.stack([starts, ends], axis=1).astype(np.int64)
+
+
+def run_heavy_hitter(args):
+    """cfg5(ii): 128 LIPs x 65536 tokens, evict the 32768 lowest-score tokens (lazy holes, ~50%-dense pages),
+    time decode, compact every file (K5 gather), time decode again.  One JSON line."""
+    import numpy as np
+    import torch
+
+    from paper_2510_25412_b200 import kvfs as K
+    from paper_2510_25412_b200.workloads import STEP_OWNER
+    from synth.configs import Shape
+    from synth.workloads import TAG_K, TAG_Q, TAG_V, rows_torch
+
+    torch.cuda.set_device(0)
+    s, n_files, L0, seed = Shape(32, 8, 128, 16), 128, 65536, 1005
+    W, Kst = args.warmup, args.steps
+    n_pages = n_files * (L0 // 16 + 4) + n_files * (L0 // 32 + 8)
+    kv = K.KVFS(1, s.Hq, s.Hkv, s.D, s.P, n_pages, max_batch_rows=n_files, max_batch_descs=n_files, device=0)
+    dev = torch.device("cuda", 0)
+    fds = []
+    for f in range(n_files):
+        fd = kv.open(f"hh{f}")
+        k = rows_torch(seed, TAG_K, 0, f, 0, L0, s.Hkv * s.D, device=dev).view(1, L0, s.Hkv, s.D)
+        v = rows_torch(seed, TAG_V, 0, f, 0, L0, s.Hkv * s.D, device=dev).view(1, L0, s.Hkv, s.D)
+        kv.append(fd, list(range(L0)), k, v)
+        fds.append(fd)
+        del k, v
+    torch.cuda.synchronize()
+    for f, fd in enumerate(fds):
+        kv.evict(fd, evict_ranges_heavy_hitter(seed, f, L0, L0 // 2))
+    descs = np.array([[fd, 1] for fd in fds], dtype=np.int32)
+    next_pos = np.full(n_files, L0, dtype=np.int64)
+    lens = np.full(n_files, L0 // 2, dtype=np.int64)
+    out = torch.empty((n_files, s.Hq, s.D), dtype=torch.bfloat16, device=dev)
+    row_kv = s.Hkv * s.D * 2
+
+    def decode(steps, step0):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ins = []
+        for i in range(steps):
+            own = STEP_OWNER + step0 + i
+            ins.append(tuple(rows_torch(seed, t, 0, own, 0, n_files, w, device=dev).view(n_files, -1, s.D)
+                             for t, w in ((TAG_Q, s.Hq * s.D), (TAG_K, s.Hkv * s.D), (TAG_V, s.Hkv * s.D))))
+        torch.cuda.synchronize()
+        e0.record()
+        for q, k, v in ins:
+            st = kv.pred_attn_batch(descs, next_pos.astype(np.int32), q, k, v, out)
+            assert st == [0] * n_files
+            next_pos[:] += 1
+            lens[:] += 1
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
+
+    decode(W, 0)
+    alg_before = 2 * int(lens.sum()) * row_kv
+    ms_before = decode(Kst, W)
+    retained = int(lens.sum())
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record()
+    for fd in fds:
+        kv.compact(fd)
+    c1.record()
+    torch.cuda.synchronize()
+    ms_compact = c0.elapsed_time(c1)
+    compact_bytes = 2 * 2 * retained * row_kv  # K and V of every retained token: read + write
+    decode(W, W + Kst)
+    alg_after = 2 * int(lens.sum()) * row_kv
+    ms_after = decode(Kst, 2 * W + Kst)
+    peak, peak_src = peaks()
+    line = {
+        "metric": METRIC, "value": n_files / (ms_after / 1000.0), "unit": "tokens/s", "n_gpus": 1, "steps": Kst,
+        "warmup": W, "ms_per_step": ms_after, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (counter-based generator seed 1005, Exp(1) scores; DESIGN.md)",
+        "config": {"workload": "cfg5(ii): 128 LIPs x 65536-token files, heavy-hitter-like eviction of the 32768 "
+                               "lowest Exp(1) scores (first 4 and last 1024 protected), decode before / after "
+                               "kvfs_compact", "l2": "inputs larger than L2"},
+        "roofline": {"bound": "hbm", "achieved": compact_bytes / (ms_compact / 1000.0) / 1e9, "peak": peak,
+                     "unit": "GB/s", "frac": compact_bytes / (ms_compact / 1000.0) / 1e9 / peak,
+                     "kernel": "compact_kernel (K5, evict-compact gather, all files)", "peak_source": peak_src,
+                     "traffic": None, "algorithmic_bytes_per_launch": compact_bytes / n_files},
+        "extra": {"decode_ms_holes": ms_before, "decode_gbs_holes": alg_before / (ms_before / 1000.0) / 1e9,
+                  "decode_ms_compacted": ms_after, "decode_gbs_compacted": alg_after / (ms_after / 1000.0) / 1e9,
+                  "compact_ms_all_files": ms_compact, "compact_bytes": compact_bytes,
+                  "retained_tokens": retained},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "cfg5hh":
+        run_heavy_hitter(args)
     else:
         run_ours(args)
 

@@ -104,24 +104,53 @@ __device__ __forceinline__ int find_entry(const dev::Entry *t, int n, int64_t i)
 }
 
 // K5: token i of the old table (logical order) -> (new_pages[i / P], i % P), every layer, K and V.
-__global__ void compact_kernel(const dev::Entry *old, int n_old, const uint32_t *new_pages, int64_t len,
-                               bf16 *const *kp, bf16 *const *vp, int L, int Hkv, int D, int P) {
-  const int cpr = D / 8;
-  const int64_t total = static_cast<int64_t>(L) * len * Hkv * cpr;
-  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int c = static_cast<int>(idx % cpr);
-    int64_t t = idx / cpr;
-    const int g = static_cast<int>(t % Hkv);
-    t /= Hkv;
-    const int64_t i = t % len;
-    const int l = static_cast<int>(t / len);
+// One CTA per (destination page, layer): the P source (page, slot) pairs are resolved once into shared
+// memory, then the CTA streams the page's Hkv x P rows of K and V with 16-byte vectors (4 loads in flight
+// per thread before the stores).
+__global__ void __launch_bounds__(256) compact_kernel(const dev::Entry *old, int n_old, const uint32_t *new_pages,
+                                                      int64_t len, bf16 *const *kp, bf16 *const *vp, int L, int Hkv,
+                                                      int D, int P) {
+  __shared__ uint32_t src_page[64];
+  __shared__ int src_slot[64];
+  const int j = blockIdx.x, l = blockIdx.y;
+  const int64_t i0 = static_cast<int64_t>(j) * P;
+  const int ntok = static_cast<int>(len - i0 < P ? len - i0 : static_cast<int64_t>(P));
+  if (threadIdx.x < ntok) {
+    const int64_t i = i0 + threadIdx.x;
     const dev::Entry e = old[find_entry(old, n_old, i)];
-    const int slot = dev::select_bit64(e.mask, static_cast<int>(i - e.lstart));
-    const int64_t so = ((static_cast<int64_t>(e.page) * Hkv + g) * P + slot) * D + c * 8;
-    const int64_t po = ((static_cast<int64_t>(new_pages[i / P]) * Hkv + g) * P + i % P) * D + c * 8;
-    *reinterpret_cast<uint4 *>(kp[l] + po) = *reinterpret_cast<const uint4 *>(kp[l] + so);
-    *reinterpret_cast<uint4 *>(vp[l] + po) = *reinterpret_cast<const uint4 *>(vp[l] + so);
+    src_page[threadIdx.x] = e.page;
+    src_slot[threadIdx.x] = dev::select_bit64(e.mask, static_cast<int>(i - e.lstart));
+  }
+  __syncthreads();
+  const bf16 *ks = kp[l];
+  const bf16 *vs = vp[l];
+  bf16 *kd = kp[l];
+  bf16 *vd = vp[l];
+  const int cpr = D / 8;
+  const int total = Hkv * ntok * cpr;
+  const int64_t dpage = new_pages[j];
+  constexpr int U = 4;
+  for (int base = threadIdx.x; base < total; base += U * blockDim.x) {
+    uint4 kr[U], vr[U];
+    int64_t po[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int idx = base + u * blockDim.x;
+      if (idx < total) {
+        const int c = idx % cpr, r = idx / cpr, t = r % ntok, g = r / ntok;
+        const int64_t so = ((static_cast<int64_t>(src_page[t]) * Hkv + g) * P + src_slot[t]) * D + c * 8;
+        po[u] = ((dpage * Hkv + g) * P + t) * D + c * 8;
+        kr[u] = *reinterpret_cast<const uint4 *>(ks + so);
+        vr[u] = *reinterpret_cast<const uint4 *>(vs + so);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (base + u * static_cast<int>(blockDim.x) < total) {
+        *reinterpret_cast<uint4 *>(kd + po[u]) = kr[u];
+        *reinterpret_cast<uint4 *>(vd + po[u]) = vr[u];
+      }
+    }
   }
 }
 
@@ -252,8 +281,7 @@ class CudaDevice final : public Device {
     if (!dt || !dp) return KVFS_ENOMEM;
     if (!send(s)) return KVFS_EIO;
     const kvfs_config &cfg = c_.cfg;
-    const int64_t total = static_cast<int64_t>(cfg.n_layers) * len * cfg.n_kv_heads * (cfg.head_dim / 8);
-    const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, sms_ * 16));
+    const dim3 grid(static_cast<unsigned>(new_pages.size()), static_cast<unsigned>(cfg.n_layers));
     compact_kernel<<<grid, 256, 0, cs(s)>>>(static_cast<const dev::Entry *>(dt), static_cast<int>(old_table.size()),
                                             static_cast<const uint32_t *>(dp), len, kptrs_, vptrs_, cfg.n_layers,
                                             cfg.n_kv_heads, cfg.head_dim, cfg.page_size);

@@ -273,21 +273,23 @@ static void compact_commit(Ctx &c, File &f, std::vector<Entry> *old_table, std::
   const int64_t k = (len + P - 1) / P;
   std::vector<uint32_t> np(static_cast<size_t>(k));
   for (int64_t j = 0; j < k; ++j) np[j] = c.pool->alloc();  // old pages still held: never destinations
-  std::vector<int32_t> lpos;
-  file_positions(c, f, &lpos);
+  // positions in logical order, written straight into the new per-slot array: token i -> (new[i/P], i%P)
+  std::vector<int32_t> nspos(static_cast<size_t>(k) * P, 0);
+  size_t w = 0;
+  for (size_t e = 0; e < f.table.size(); ++e)
+    for (uint64_t m = f.table[e].mask; m; m &= m - 1) nspos[w++] = f.spos[e * P + __builtin_ctzll(m)];
   std::vector<Entry> old;
   old.swap(f.table);
-  f.spos.assign(static_cast<size_t>(k) * P, 0);
-  std::copy(lpos.begin(), lpos.end(), f.spos.begin());  // token i -> (new[i / P], i % P)
+  f.spos.swap(nspos);
   const uint64_t full = P == 64 ? ~0ull : ((1ull << P) - 1);
-  f.table.reserve(static_cast<size_t>(k));
+  f.table.resize(static_cast<size_t>(k));
   for (int64_t j = 0; j < k; ++j) {
     const int64_t cnt = std::min<int64_t>(P, len - j * P);
-    f.table.push_back({np[j], static_cast<int32_t>(j * P), cnt == 64 ? ~0ull : (cnt == P ? full : ((1ull << cnt) - 1))});
+    f.table[j] = {np[j], static_cast<int32_t>(j * P), cnt == P ? full : ((1ull << cnt) - 1)};
   }
   for (const Entry &e : old) c.pool->release(e.page);
   mark_dirty_from(f, 0);
-  recompute_lstart(f, 0);
+  f.len = len;
   if (old_table) old_table->swap(old);
   if (new_pages) new_pages->swap(np);
 }

@@ -1,5 +1,6 @@
 #include "pool.h"
 
+#include <algorithm>
 #include <cassert>
 
 namespace kvfs {
@@ -15,6 +16,7 @@ PagePool::PagePool(int64_t n_pages)
 void PagePool::set_free(uint32_t p) {
   l0_[p >> 6] |= 1ull << (p & 63);
   l1_[p >> 12] |= 1ull << ((p >> 6) & 63);
+  hint_ = std::min<size_t>(hint_, p >> 12);
 }
 
 void PagePool::clear_free(uint32_t p) {
@@ -25,8 +27,11 @@ void PagePool::clear_free(uint32_t p) {
 
 uint32_t PagePool::alloc() {
   assert(n_free_ > 0);
-  for (size_t i = 0; i < l1_.size(); ++i) {
-    if (!l1_[i]) continue;
+  for (size_t i = hint_; i < l1_.size(); ++i) {
+    if (!l1_[i]) {
+      hint_ = i + 1;
+      continue;
+    }
     const size_t w = i * 64 + static_cast<size_t>(__builtin_ctzll(l1_[i]));
     const uint32_t p = static_cast<uint32_t>(w * 64 + static_cast<size_t>(__builtin_ctzll(l0_[w])));
     clear_free(p);

@@ -31,6 +31,7 @@ class PagePool {
   std::vector<uint32_t> ref_;
   std::vector<uint64_t> l0_;  // bit = page free
   std::vector<uint64_t> l1_;  // bit = l0_ word non-zero
+  size_t hint_ = 0;           // every l1_ word below hint_ is zero (no free page below hint_ * 4096)
   int64_t n_free_ = 0;
 };
 
