@@ -83,6 +83,15 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 
+// One elected lane of a converged warp (elect.sync): the issue region of the single-thread tcgen05 ops.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .b32 rx;\n\t.reg .pred px;\n\telect.sync rx|px, 0xffffffff;\n\tselp.b32 %0, 1, 0, px;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -218,7 +227,10 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // The CTA owns all 512 TMEM columns (one CTA per SM), so the allocation starts at lane 0, column 0.  The
+  // constant keeps every tcgen05 operand a compile-time uniform value (no R2UR waterfall per MMA).
+  if (*tmem_slot != 0u) __trap();
+  constexpr uint32_t tmem = 0;
 
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
@@ -233,64 +245,91 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           tma_load_4d(sbase + OFF_Q2 + m * TILE_BYTES + HALF_BYTES, &qmap, 64, 0, u.g, qrow, bar(B_Q));
         }
       }
+      // Page-table entries are fetched 32 at a time with one coalesced load (lane i <-> entry 32 blk + i)
+      // and handed to the tile's columns by shuffles: no dependent global load on the per-tile path.
+      // jbase(e) = j of entry e's first retained token = first_new_lstart - n_old + sum of the popcounts
+      // of the entries fne .. e-1 (entries at or after the first new entry hold new tokens).
+      uint64_t emask = 0;
+      int32_t erow = p.pool_rows, jbase = 0, carry = cd.first_new_lstart - cd.n_old;
+      int cached = -1;
       for (int t = 0; t < n_tiles; ++t) {
         const int s = t % KV2;
         if (t >= KV2) mbar_wait_sleep(bar(B_KE + s), ((t / KV2) & 1) ^ 1);
+        const int e0 = t * epb, blk = e0 >> 5;
+        if (blk != cached) {
+          const int e = blk * 32 + lane;
+          emask = 0;
+          erow = p.pool_rows;
+          if (e < cd.n_entries) {
+            const Entry en = p.slab[cd.slab_off + e];
+            emask = en.mask;
+            erow = (static_cast<int>(en.page) * p.Hkv + u.g) * p.P;
+          }
+          const int cnt = (e >= cd.first_new_entry) ? __popcll(emask) : 0;
+          int incl = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          jbase = carry + incl - cnt;
+          carry += __shfl_sync(0xffffffffu, incl, 31);
+          cached = blk;
+        }
         // column metadata of tile t: j = logical index - n_old (visible iff j <= qi), INT_MAX = no key;
         // jflag = 1 when every column is an old retained token (visible to every row: no masking)
         int32_t *jcol = jcol_all + (t % JR) * BN;
         bool vis_all = true;
-        for (int c = lane; c < BN; c += 32) {
-          const int e = t * epb + c / p.P, slot = c % p.P;
+#pragma unroll
+        for (int k = 0; k < BN / 32; ++k) {
+          const int c = k * 32 + lane;
+          const int i = c / p.P, slot = c % p.P;
+          const int src = (e0 & 31) + i;
+          const uint64_t m = __shfl_sync(0xffffffffu, emask, src);
+          const int32_t jb = __shfl_sync(0xffffffffu, jbase, src);
+          const int e = e0 + i;
           int32_t j = 0x7fffffff;
-          if (e < cd.n_entries) {
-            const Entry en = p.slab[cd.slab_off + e];
-            if ((en.mask >> slot) & 1ull) {
-              if (e < cd.first_new_entry) {
-                j = -1;
-              } else {
-                int lg = cd.first_new_lstart + __popcll(en.mask & ((1ull << slot) - 1ull));
-                for (int e2 = cd.first_new_entry; e2 < e; ++e2) lg += __popcll(p.slab[cd.slab_off + e2].mask);
-                j = lg - cd.n_old;
-              }
-            }
-          }
+          if (e < cd.n_entries && ((m >> slot) & 1ull))
+            j = (e < cd.first_new_entry) ? -1 : jb + __popcll(m & ((1ull << slot) - 1ull));
           jcol[c] = j;
           vis_all &= (j < 0);
         }
         vis_all = __all_sync(0xffffffffu, vis_all);
-        if (lane == 0) jflag[t % JR] = vis_all ? 1 : 0;
-        __syncwarp();
+        const int32_t row = __shfl_sync(0xffffffffu, erow, (e0 & 31) + (lane % epb));
         if (lane == 0) {
+          jflag[t % JR] = vis_all ? 1 : 0;
           mbar_arrive(bar(B_JF + t % JR));
           mbar_arrive_expect_tx(bar(B_KF + s), TILE_BYTES);
-          for (int i = 0; i < epb; ++i) {
-            const int e = t * epb + i;
-            const int row = e < cd.n_entries ? (static_cast<int>(p.slab[cd.slab_off + e].page) * p.Hkv + u.g) * p.P
-                                             : p.pool_rows;
-            for (int h = 0; h < 2; ++h)
-              tma_load_2d(sbase + OFF_K2 + s * TILE_BYTES + h * HALF_BYTES + i * p.P * 128, &kmap, h * 64, row,
-                          bar(B_KF + s), pol);
-          }
+        }
+        __syncwarp();
+        if (lane < epb) {  // entry e0 + lane (rows past the table: out-of-bounds box, zero-filled)
+          for (int h = 0; h < 2; ++h)
+            tma_load_2d(sbase + OFF_K2 + s * TILE_BYTES + h * HALF_BYTES + lane * p.P * 128, &kmap, h * 64, row,
+                        bar(B_KF + s), pol);
         }
         __syncwarp();
       }
     } else if (warp == 3) {
       // ============================================================ V producer
       const uint64_t pol = policy_evict_first();
+      int32_t erow = p.pool_rows;
+      int cached = -1;
       for (int t = 0; t < n_tiles; ++t) {
         const int s = t % KV2;
         if (t >= KV2) mbar_wait_sleep(bar(B_VE + s), ((t / KV2) & 1) ^ 1);
-        if (lane == 0) {
-          mbar_arrive_expect_tx(bar(B_VF + s), TILE_BYTES);
-          for (int i = 0; i < epb; ++i) {
-            const int e = t * epb + i;
-            const int row = e < cd.n_entries ? (static_cast<int>(p.slab[cd.slab_off + e].page) * p.Hkv + u.g) * p.P
-                                             : p.pool_rows;
-            for (int h = 0; h < 2; ++h)
-              tma_load_2d(sbase + OFF_V2 + s * TILE_BYTES + h * HALF_BYTES + i * p.P * 128, &vmap, h * 64, row,
-                          bar(B_VF + s), pol);
-          }
+        const int e0 = t * epb, blk = e0 >> 5;
+        if (blk != cached) {
+          const int e = blk * 32 + lane;
+          erow = e < cd.n_entries ? (static_cast<int>(p.slab[cd.slab_off + e].page) * p.Hkv + u.g) * p.P : p.pool_rows;
+          cached = blk;
+        }
+        const int32_t row = __shfl_sync(0xffffffffu, erow, (e0 & 31) + (lane % epb));
+        if (lane == 0) mbar_arrive_expect_tx(bar(B_VF + s), TILE_BYTES);
+        __syncwarp();
+        if (lane < epb) {
+          for (int h = 0; h < 2; ++h)
+            tma_load_2d(sbase + OFF_V2 + s * TILE_BYTES + h * HALF_BYTES + lane * p.P * 128, &vmap, h * 64, row,
+                        bar(B_VF + s), pol);
         }
         __syncwarp();
       }
@@ -300,7 +339,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       mbar_wait(bar(B_Q), 0);
       auto issue_s = [&](int t, int m) {
         tc_fence_after();
-        if (lane == 0) {
+        if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < HD / 16; ++k) {
             const uint32_t koff = (k >> 2) * HALF_BYTES + (k & 3) * 32;
@@ -313,7 +352,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       };
       auto issue_pv = [&](int t, int m) {
         tc_fence_after();
-        if (lane == 0) {
+        if (elect_one()) {
 #pragma unroll
           for (int k = 0; k < BN / 16; ++k)
             mma_bf16_ts(tmem + O_COL2 + m * HD, tmem + m * BN + k * 8,
@@ -325,7 +364,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       };
       mbar_wait(bar(B_KF + 0), 0);
       for (int m = 0; m < n_mt; ++m) issue_s(0, m);
-      if (lane == 0) mma_commit(bar(B_KE + 0));
+      if (elect_one()) mma_commit(bar(B_KE + 0));
       __syncwarp();
       for (int t = 0; t < n_tiles; ++t) {
         const int s = t % KV2;
@@ -339,7 +378,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
             issue_s(t + 1, m);
           }
         }
-        if (lane == 0) {
+        if (elect_one()) {
           if (more) mma_commit(bar(B_KE + (t + 1) % KV2));
           mma_commit(bar(B_VE + s));
         }
