@@ -35,17 +35,17 @@ def _headers():
             + glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
-def _obj(src):
+def _obj(src, out_dir):
     rel = os.path.relpath(src, CSRC).replace(os.sep, "_")
-    return os.path.join(OUT_DIR, rel + ".o")
+    return os.path.join(out_dir, rel + ".o")
 
 
-def _compile(src, force, hdr_mtime):
-    obj = _obj(src)
+def _compile(src, force, hdr_mtime, out_dir=OUT_DIR, defines=()):
+    obj = _obj(src, out_dir)
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(src), hdr_mtime):
         return obj, ""
     if src.endswith(".cu"):
-        cmd = [NVCC] + NVFLAGS + ["-c", src, "-o", obj]
+        cmd = [NVCC] + NVFLAGS + ["-D" + d for d in defines] + ["-c", src, "-o", obj]
     else:
         cmd = ["g++"] + CXXFLAGS + ["-I" + os.path.join(ROOT, "include"), "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -54,12 +54,15 @@ def _compile(src, force, hdr_mtime):
     return obj, r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OUT_DIR, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), lib: str = LIB, out_dir: str = OUT_DIR) -> str:
+    """Build `lib` (default: the in-tree libkvfs.so).  `defines` (e.g. KVFS_EXP_EMU=2) and another
+    `lib`/`out_dir` are for tuning experiments only (loaded via KVFS_LIB_PATH)."""
+    LIB = lib
+    os.makedirs(out_dir, exist_ok=True)
     cc, cu = _sources()
     hdr_mtime = max([os.path.getmtime(h) for h in _headers()] + [0.0])
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        results = list(ex.map(lambda s: _compile(s, force, hdr_mtime), cc + cu))
+        results = list(ex.map(lambda s: _compile(s, force, hdr_mtime, out_dir, defines), cc + cu))
     objs = [o for o, _ in results]
     if verbose:
         for o, log in results:

@@ -30,26 +30,16 @@ namespace dev {
 namespace tc {
 
 constexpr int BM = 128;   // rows per M-tile
-constexpr int BN = 128;   // keys per KV tile
 constexpr int HD = 128;   // head dim (K2 is specialised for D = 128)
-constexpr int HALF_BYTES = BM * 64 * 2;  // one 64-column half of a [128][64] bf16 SW128 tile = 16 KiB
-constexpr int TILE_BYTES = 2 * HALF_BYTES;  // [128][128] bf16 = 32 KiB
-constexpr int KV_STAGES = 2;
-constexpr int THREADS = 256;
+#ifndef KVFS_EXP_EMU
+#define KVFS_EXP_EMU 2
+#endif
+constexpr int EXP_EMU = KVFS_EXP_EMU;  // of every 8 exp2 pairs in the softmax, how many run as a polynomial on the FMA pipe
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t S_COL0 = 0, O_COL = 256;
-
-// shared memory layout (all tiles 1024-B aligned for the 128B swizzle)
-constexpr int OFF_Q = 0;
-constexpr int OFF_P = OFF_Q + TILE_BYTES;
-constexpr int OFF_K = OFF_P + TILE_BYTES;                  // [KV_STAGES] K tiles
-constexpr int OFF_V = OFF_K + KV_STAGES * TILE_BYTES;      // [KV_STAGES] V tiles
-constexpr int OFF_JCOL = OFF_V + KV_STAGES * TILE_BYTES;   // [KV_STAGES][BN] int32 column metadata
-constexpr int OFF_BAR = OFF_JCOL + KV_STAGES * BN * 4;
-// barriers: q_full, kv_full[S], kv_empty[S], s_full[2], s_empty[2], p_full, o_full
-constexpr int N_BARS = 1 + 2 * KV_STAGES + 2 + 2 + 1 + 1;
-constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
-constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + alignment slack
+#ifndef KVFS_K2_ISSUERS
+#define KVFS_K2_ISSUERS 2
+#endif
+constexpr int K2_ISSUERS = KVFS_K2_ISSUERS;  // MMA-issuing warps (1: warp 1 issues both M-tiles)
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
   uint64_t d = 0;
@@ -59,17 +49,6 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes
   d |= static_cast<uint64_t>(1) << 46;  // version (Blackwell)
   d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
   return d;
-}
-
-// kind::f16 instruction descriptor: bf16 x bf16 -> f32, M = 128, N = 128
-__host__ __device__ constexpr uint32_t idesc_bf16(bool b_mn_major) {
-  return (1u << 4)                                  // c_format = F32
-         | (1u << 7)                                // a_format = BF16
-         | (1u << 10)                               // b_format = BF16
-         | (0u << 15)                               // a K-major
-         | ((b_mn_major ? 1u : 0u) << 16)           // b major
-         | ((static_cast<uint32_t>(BN) >> 3) << 17)  // N >> 3
-         | ((static_cast<uint32_t>(BM) >> 4) << 24); // M >> 4
 }
 
 __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -157,44 +136,124 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
 }
 
+
+// S_m = Q_m K^T for one 64-key tile: 8 MMAs (K = 16 each) in one asm block.  a / b are the SW128 K-major
+// descriptors of the Q tile (128 rows, halves 16 KiB apart) and the K tile (64 rows, halves 8 KiB apart);
+// step k advances the start address by (k / 4) * half + (k % 4) * 32 bytes (in 16-byte units below).
+__device__ __forceinline__ void mma_s_group(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .b64 a1, a2, a3, a4, a5, a6, a7, b1, b2, b3, b4, b5, b6, b7;\n\t"
+      "add.s64 a1, %1, 2;\n\tadd.s64 b1, %2, 2;\n\t"
+      "add.s64 a2, %1, 4;\n\tadd.s64 b2, %2, 4;\n\t"
+      "add.s64 a3, %1, 6;\n\tadd.s64 b3, %2, 6;\n\t"
+      "add.s64 a4, %1, 1024;\n\tadd.s64 b4, %2, 512;\n\t"
+      "add.s64 a5, %1, 1026;\n\tadd.s64 b5, %2, 514;\n\t"
+      "add.s64 a6, %1, 1028;\n\tadd.s64 b6, %2, 516;\n\t"
+      "add.s64 a7, %1, 1030;\n\tadd.s64 b7, %2, 518;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a1, b1, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a2, b2, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a3, b3, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a4, b4, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a5, b5, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a6, b6, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], a7, b7, %3, 1;\n\t}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc));
+}
+
+// O_m (+)= P_m V for one 64-key tile: 4 MMAs with A = P from TMEM (8 columns = 16 keys per step) and
+// B = the V tile (MN-major SW128, 16 key rows = 2048 B = 128 units per step).
+__device__ __forceinline__ void mma_pv_group(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                             uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b64 b1, b2, b3;\n\t.reg .b32 t1, t2, t3;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "add.s64 b1, %2, 128;\n\tadd.s64 b2, %2, 256;\n\tadd.s64 b3, %2, 384;\n\t"
+      "add.s32 t1, %1, 8;\n\tadd.s32 t2, %1, 16;\n\tadd.s32 t3, %1, 24;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [t1], b1, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [t2], b2, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [t3], b3, %3, 1;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
+}
+
 }  // namespace tc
 
-// v2 layout: one CTA = (descriptor, kv head, pair of 128-row M-tiles) sharing every K/V tile.
-// TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); P_m aliases the first 64 columns of S_m.
-namespace tc2 {
+// v3 layout: one CTA = (descriptor, kv head, pair of 128-row M-tiles) sharing every K/V tile; KV tiles of
+// 64 keys.  TMEM: S0 [0,64) S1 [64,128), P_m[b] at [128 + 32 (2m + b), +32) (double-buffered by tile
+// parity b), O0 [256,384) O1 [384,512).  P has its own columns, so S_m(t+1) is issued as soon as softmax m
+// has read S_m(t) into registers and runs on the tensor pipe while the softmax of tile t computes its
+// exponentials; with two P buffers the softmax never waits for P.V(t-1) (only for P.V(t-2), long done,
+// and for P.V(t-1) when it must rescale O).  No S -> P -> PV -> S dependency chain remains.
+namespace tc3 {
 constexpr int THREADS = 384;  // warps 0-3: K producer, MMA, TMEM alloc, V producer; 4-7, 8-11: softmax M-tiles
-constexpr int KV2 = 2;        // K stages and V stages (independent rings)
-constexpr int JR = 4;         // column-metadata ring
-constexpr uint32_t O_COL2 = 256;
-constexpr int OFF_Q2 = 0;                                   // 2 Q tiles
-constexpr int OFF_K2 = OFF_Q2 + 2 * tc::TILE_BYTES;         // KV2 K tiles
-constexpr int OFF_V2 = OFF_K2 + KV2 * tc::TILE_BYTES;       // KV2 V tiles
-constexpr int OFF_JCOL2 = OFF_V2 + KV2 * tc::TILE_BYTES;    // JR x BN int32
-constexpr int OFF_BAR2 = OFF_JCOL2 + JR * tc::BN * 4 + 64;  // + JR tile flags
-constexpr int N_BARS2 = 1 + 4 * KV2 + 6 + JR;
-constexpr int OFF_TMEM2 = OFF_BAR2 + N_BARS2 * 8;
-constexpr int SMEM2 = OFF_TMEM2 + 16 + 1024;
-}  // namespace tc2
+constexpr int BN = 64;        // keys per KV tile
+constexpr int KVS = 4;        // K stages and V stages (independent rings)
+constexpr int JR = 8;         // column-metadata ring (>= KVS + 2, see the producer)
+constexpr int QT_BYTES = tc::BM * tc::HD * 2;       // one [128][128] Q tile (two SW128 halves of 16 KiB)
+constexpr int QH_BYTES = QT_BYTES / 2;
+constexpr int KT_BYTES = BN * tc::HD * 2;           // one [64][128] K or V tile (two SW128 halves of 8 KiB)
+constexpr int KH_BYTES = KT_BYTES / 2;
+constexpr uint32_t S_COL = 0, P_COL = 128, O_COL = 256;
+constexpr int OFF_Q = 0;
+constexpr int OFF_K = OFF_Q + 2 * QT_BYTES;
+constexpr int OFF_V = OFF_K + KVS * KT_BYTES;
+constexpr int OFF_JCOL = OFF_V + KVS * KT_BYTES;     // JR x BN int32 + JR tile flags
+constexpr int OFF_BAR = OFF_JCOL + JR * BN * 4 + JR * 4;
+constexpr int N_BARS = 1 + 4 * KVS + 12 + JR;
+constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
+constexpr int SMEM = OFF_TMEM + 16 + 1024;
+static_assert(SMEM <= 232448, "shared memory");
+
+// kind::f16 instruction descriptor: bf16 x bf16 -> f32, M = 128, N = n
+__host__ __device__ constexpr uint32_t idesc(int n, bool b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) |
+         ((static_cast<uint32_t>(n) >> 3) << 17) | ((static_cast<uint32_t>(tc::BM) >> 4) << 24);
+}
+}  // namespace tc3
+
+// Development tracing (build with -DKVFS_K2_TRACE, read with tools/k2_trace.py): clock64() stamps of the
+// pipeline events of two CTAs (block 0 and block 296, first and third wave) per KV tile.
+#ifdef KVFS_K2_TRACE
+__device__ unsigned long long g_k2_trace[2][32][512];
+#define K2T(ev, t)                                                                  \
+  do {                                                                              \
+    if (trace_cta >= 0 && (t) < 512) g_k2_trace[trace_cta][ev][t] = clock64();      \
+  } while (0)
+#else
+#define K2T(ev, t) \
+  do {             \
+  } while (0)
+#endif
 
 template <int G>
-__global__ void __launch_bounds__(tc2::THREADS, 1)
+__global__ void __launch_bounds__(tc3::THREADS, 1)
     chunk_attn_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                          const __grid_constant__ CUtensorMap qmap, const ChunkParams p) {
   using namespace tc;
-  using namespace tc2;
+  using namespace tc3;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR2);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
   auto bar = [&](int i) { return smem_u32(bars + i); };
-  // barrier indices
-  constexpr int B_Q = 0, B_KF = 1, B_KE = 1 + KV2, B_VF = 1 + 2 * KV2, B_VE = 1 + 3 * KV2, B_SF = 1 + 4 * KV2,
-                B_PF = B_SF + 2, B_OF = B_PF + 2, B_JF = B_OF + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + OFF_TMEM2);
-  int32_t *jcol_all = reinterpret_cast<int32_t *>(smem + OFF_JCOL2);
+  // barriers: Q; K full/empty, V full/empty rings; per M-tile S full (MMA commit), S consumed (softmax read
+  // S into registers), P full (softmax wrote P); per (M-tile, P buffer) P consumed (PV done: that P buffer
+  // free, O stable; index 2m + b); column metadata
+  // P full is per (M-tile, tile parity) too: it counts one arrival per softmax warp, and a fast warp may
+  // reach tile t+1 (S(t+1) is issued once every warp has READ S(t)) before a slow warp has written P(t);
+  // with one barrier its early arrival would complete the phase of tile t.  Two tiles ahead is impossible
+  // (S(t+2) waits for every warp to read S(t+1), i.e. to finish tile t).
+  constexpr int B_Q = 0, B_KF = 1, B_KE = 1 + KVS, B_VF = 1 + 2 * KVS, B_VE = 1 + 3 * KVS, B_SF = 1 + 4 * KVS,
+                B_SE = B_SF + 2, B_PF = B_SE + 2, B_PE = B_PF + 4, B_JF = B_PE + 4;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + OFF_TMEM);
+  int32_t *jcol_all = reinterpret_cast<int32_t *>(smem + OFF_JCOL);
   int32_t *jflag = jcol_all + JR * BN;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef KVFS_K2_TRACE
+  const int trace_cta = blockIdx.x == 0 ? 0 : (blockIdx.x == 296 ? 1 : -1);
+#endif
   const ChunkUnit u = p.units[blockIdx.x];
   const ChunkDesc cd = p.descs[u.desc];
   const int epb = BN / p.P;  // page entries per KV tile
@@ -205,16 +264,19 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(bar(B_Q), 1);
-    for (int s = 0; s < KV2; ++s) {
+    for (int s = 0; s < KVS; ++s) {
       mbar_init(bar(B_KF + s), 1);
-      mbar_init(bar(B_KE + s), 1);
+      mbar_init(bar(B_KE + s), K2_ISSUERS == 2 ? n_mt : 1);  // one commit per MMA issuer
       mbar_init(bar(B_VF + s), 1);
-      mbar_init(bar(B_VE + s), 1);
+      mbar_init(bar(B_VE + s), K2_ISSUERS == 2 ? n_mt : 1);
     }
     for (int m = 0; m < 2; ++m) {
       mbar_init(bar(B_SF + m), 1);
-      mbar_init(bar(B_PF + m), 4);
-      mbar_init(bar(B_OF + m), 1);
+      mbar_init(bar(B_SE + m), 4);
+      mbar_init(bar(B_PF + 2 * m), 4);
+      mbar_init(bar(B_PF + 2 * m + 1), 4);
+      mbar_init(bar(B_PE + 2 * m), 1);
+      mbar_init(bar(B_PE + 2 * m + 1), 1);
     }
     for (int j = 0; j < JR; ++j) mbar_init(bar(B_JF + j), 1);
     fence_mbar_init();
@@ -238,23 +300,27 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       // ============================================================ K producer (+ Q, + column metadata)
       const uint64_t pol = policy_evict_first();
       if (lane == 0) {
-        mbar_arrive_expect_tx(bar(B_Q), n_mt * TILE_BYTES);
+        mbar_arrive_expect_tx(bar(B_Q), n_mt * QT_BYTES);
         for (int m = 0; m < n_mt; ++m) {
           const int qrow = cd.row0 + ((m0 + m) * BM) / G;
-          tma_load_4d(sbase + OFF_Q2 + m * TILE_BYTES, &qmap, 0, 0, u.g, qrow, bar(B_Q));
-          tma_load_4d(sbase + OFF_Q2 + m * TILE_BYTES + HALF_BYTES, &qmap, 64, 0, u.g, qrow, bar(B_Q));
+          tma_load_4d(sbase + OFF_Q + m * QT_BYTES, &qmap, 0, 0, u.g, qrow, bar(B_Q));
+          tma_load_4d(sbase + OFF_Q + m * QT_BYTES + QH_BYTES, &qmap, 64, 0, u.g, qrow, bar(B_Q));
         }
       }
       // Page-table entries are fetched 32 at a time with one coalesced load (lane i <-> entry 32 blk + i)
       // and handed to the tile's columns by shuffles: no dependent global load on the per-tile path.
       // jbase(e) = j of entry e's first retained token = first_new_lstart - n_old + sum of the popcounts
       // of the entries fne .. e-1 (entries at or after the first new entry hold new tokens).
+      // Ring safety of jcol: the producer writes tile t after K(t - KVS) was released, i.e. after both
+      // softmax groups read S(t - KVS - 1); they read jcol(t') right after S(t'), so slot t % JR (JR >= KVS + 2)
+      // last held tile t - JR <= t - KVS - 2, already consumed.
       uint64_t emask = 0;
       int32_t erow = p.pool_rows, jbase = 0, carry = cd.first_new_lstart - cd.n_old;
       int cached = -1;
       for (int t = 0; t < n_tiles; ++t) {
-        const int s = t % KV2;
-        if (t >= KV2) mbar_wait_sleep(bar(B_KE + s), ((t / KV2) & 1) ^ 1);
+        const int s = t % KVS;
+        if (t >= KVS) mbar_wait_sleep(bar(B_KE + s), ((t / KVS) & 1) ^ 1);
+        if (lane == 0) K2T(0, t);
         const int e0 = t * epb, blk = e0 >> 5;
         if (blk != cached) {
           const int e = blk * 32 + lane;
@@ -299,14 +365,15 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         if (lane == 0) {
           jflag[t % JR] = vis_all ? 1 : 0;
           mbar_arrive(bar(B_JF + t % JR));
-          mbar_arrive_expect_tx(bar(B_KF + s), TILE_BYTES);
+          mbar_arrive_expect_tx(bar(B_KF + s), KT_BYTES);
         }
         __syncwarp();
         if (lane < epb) {  // entry e0 + lane (rows past the table: out-of-bounds box, zero-filled)
           for (int h = 0; h < 2; ++h)
-            tma_load_2d(sbase + OFF_K2 + s * TILE_BYTES + h * HALF_BYTES + lane * p.P * 128, &kmap, h * 64, row,
+            tma_load_2d(sbase + OFF_K + s * KT_BYTES + h * KH_BYTES + lane * p.P * 128, &kmap, h * 64, row,
                         bar(B_KF + s), pol);
         }
+        if (lane == 0) K2T(1, t);
         __syncwarp();
       }
     } else if (warp == 3) {
@@ -315,8 +382,9 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       int32_t erow = p.pool_rows;
       int cached = -1;
       for (int t = 0; t < n_tiles; ++t) {
-        const int s = t % KV2;
-        if (t >= KV2) mbar_wait_sleep(bar(B_VE + s), ((t / KV2) & 1) ^ 1);
+        const int s = t % KVS;
+        if (t >= KVS) mbar_wait_sleep(bar(B_VE + s), ((t / KVS) & 1) ^ 1);
+        if (lane == 0) K2T(2, t);
         const int e0 = t * epb, blk = e0 >> 5;
         if (blk != cached) {
           const int e = blk * 32 + lane;
@@ -324,65 +392,79 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           cached = blk;
         }
         const int32_t row = __shfl_sync(0xffffffffu, erow, (e0 & 31) + (lane % epb));
-        if (lane == 0) mbar_arrive_expect_tx(bar(B_VF + s), TILE_BYTES);
+        if (lane == 0) mbar_arrive_expect_tx(bar(B_VF + s), KT_BYTES);
         __syncwarp();
         if (lane < epb) {
           for (int h = 0; h < 2; ++h)
-            tma_load_2d(sbase + OFF_V2 + s * TILE_BYTES + h * HALF_BYTES + lane * p.P * 128, &vmap, h * 64, row,
+            tma_load_2d(sbase + OFF_V + s * KT_BYTES + h * KH_BYTES + lane * p.P * 128, &vmap, h * 64, row,
                         bar(B_VF + s), pol);
         }
+        if (lane == 0) K2T(3, t);
         __syncwarp();
       }
-    } else if (warp == 1) {
-      // ============================================================ MMA issuer
-      constexpr uint32_t ID_S = idesc_bf16(false), ID_O = idesc_bf16(true);
-      mbar_wait(bar(B_Q), 0);
-      auto issue_s = [&](int t, int m) {
+    } else if (warp == 1 || (warp == 2 && K2_ISSUERS == 2)) {
+      // ============================================================ MMA issuers
+      // K2_ISSUERS == 2: warp 1 + m issues M-tile m; == 1: warp 1 issues both.
+      // Per tile t: S_m(t+1) as soon as softmax m read S_m(t) (and K(t+1) landed), then PV_m(t) as soon as
+      // P_m(t) is written (and V(t) landed).  The tensor pipe runs in order per issuer, so softmax m of
+      // tile t+1 finds S_m(t+1) ready.  K / V stages are released by a commit of each issuer.
+      constexpr uint32_t ID_S = idesc(BN, false), ID_O = idesc(HD, true);
+      const int m_lo = K2_ISSUERS == 2 ? warp - 1 : 0;
+      const int m_hi = K2_ISSUERS == 2 ? min(warp, n_mt) : n_mt;
+      if (m_lo < m_hi) {
+        const uint64_t qd = umma_desc(sbase + OFF_Q, 16, 1024);
+        const uint64_t kd0 = umma_desc(sbase + OFF_K, 16, 1024);
+        const uint64_t vd0 = umma_desc(sbase + OFF_V, KH_BYTES, 1024);
+        constexpr uint64_t STAGE_UNITS = KT_BYTES >> 4, QT_UNITS = QT_BYTES >> 4;
+        mbar_wait(bar(B_Q), 0);
+        mbar_wait(bar(B_KF + 0), 0);
         tc_fence_after();
         if (elect_one()) {
-#pragma unroll
-          for (int k = 0; k < HD / 16; ++k) {
-            const uint32_t koff = (k >> 2) * HALF_BYTES + (k & 3) * 32;
-            mma_bf16(tmem + m * BN, umma_desc(sbase + OFF_Q2 + m * TILE_BYTES + koff, 16, 1024),
-                     umma_desc(sbase + OFF_K2 + (t % KV2) * TILE_BYTES + koff, 16, 1024), ID_S, k > 0);
+          for (int m = m_lo; m < m_hi; ++m) {
+            mma_s_group(tmem + S_COL + m * BN, qd + m * QT_UNITS, kd0, ID_S);
+            mma_commit(bar(B_SF + m));
           }
-          mma_commit(bar(B_SF + m));
+          mma_commit(bar(B_KE + 0));
         }
         __syncwarp();
-      };
-      auto issue_pv = [&](int t, int m) {
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int k = 0; k < BN / 16; ++k)
-            mma_bf16_ts(tmem + O_COL2 + m * HD, tmem + m * BN + k * 8,
-                        umma_desc(sbase + OFF_V2 + (t % KV2) * TILE_BYTES + k * 2048, HALF_BYTES, 1024), ID_O,
-                        (t > 0 || k > 0));
-          mma_commit(bar(B_OF + m));
-        }
-        __syncwarp();
-      };
-      mbar_wait(bar(B_KF + 0), 0);
-      for (int m = 0; m < n_mt; ++m) issue_s(0, m);
-      if (elect_one()) mma_commit(bar(B_KE + 0));
-      __syncwarp();
-      for (int t = 0; t < n_tiles; ++t) {
-        const int s = t % KV2;
-        const bool more = t + 1 < n_tiles;
-        mbar_wait(bar(B_VF + s), (t / KV2) & 1);
-        for (int m = 0; m < n_mt; ++m) {
-          mbar_wait(bar(B_PF + m), t & 1);  // softmax m wrote P(t) into TMEM (and corrected O)
-          issue_pv(t, m);
-          if (more) {                       // in-order after PV(t): S(t+1) may overwrite P(t)'s columns
-            if (m == 0) mbar_wait(bar(B_KF + (t + 1) % KV2), ((t + 1) / KV2) & 1);
-            issue_s(t + 1, m);
+        for (int t = 0; t < n_tiles; ++t) {
+#ifdef KVFS_K2_LOCKSTEP
+          if (K2_ISSUERS == 2 && n_mt == 2) named_bar_sync(14, 64);
+#endif
+          if (t + 1 < n_tiles) {
+            const int s1 = (t + 1) % KVS;
+            mbar_wait(bar(B_KF + s1), ((t + 1) / KVS) & 1);
+            for (int m = m_lo; m < m_hi; ++m) {
+              mbar_wait(bar(B_SE + m), t & 1);  // softmax m holds S_m(t) in registers
+              if (m == 0 && lane == 0) K2T(5, t);
+              tc_fence_after();
+              if (elect_one()) {
+                mma_s_group(tmem + S_COL + m * BN, qd + m * QT_UNITS, kd0 + s1 * STAGE_UNITS, ID_S);
+                mma_commit(bar(B_SF + m));
+              }
+              __syncwarp();
+              if (m == 0 && lane == 0) K2T(6, t);
+            }
+            if (elect_one()) mma_commit(bar(B_KE + s1));
+            __syncwarp();
           }
+          const int s = t % KVS;
+          mbar_wait(bar(B_VF + s), (t / KVS) & 1);
+          for (int m = m_lo; m < m_hi; ++m) {
+            mbar_wait(bar(B_PF + 2 * m + (t & 1)), (t >> 1) & 1);  // softmax m wrote P_m(t) (and corrected O)
+            if (m == 0 && lane == 0) K2T(10, t);
+            tc_fence_after();
+            if (elect_one()) {
+              mma_pv_group(tmem + O_COL + m * HD, tmem + P_COL + (2 * m + (t & 1)) * (BN / 2),
+                           vd0 + s * STAGE_UNITS, ID_O, t > 0 ? 1u : 0u);
+              mma_commit(bar(B_PE + 2 * m + (t & 1)));
+            }
+            __syncwarp();
+            if (m == 0 && lane == 0) K2T(11, t);
+          }
+          if (elect_one()) mma_commit(bar(B_VE + s));
+          __syncwarp();
         }
-        if (elect_one()) {
-          if (more) mma_commit(bar(B_KE + (t + 1) % KV2));
-          mma_commit(bar(B_VE + s));
-        }
-        __syncwarp();
       }
     }
   } else {
@@ -396,11 +478,13 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       const int qi = R / G, h = R % G;
       const bool live = qi < cd.n_q;
       const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
-      const uint32_t s_col = tmem + lane_addr + m * BN;
-      const uint32_t o_col = tmem + lane_addr + O_COL2 + m * HD;
+      const uint32_t s_col = tmem + lane_addr + S_COL + m * BN;
+      const uint32_t p_col = tmem + lane_addr + P_COL + 2 * m * (BN / 2);  // + (t & 1) * (BN / 2)
+      const uint32_t o_col = tmem + lane_addr + O_COL + m * HD;
       float m_run = -CUDART_INF_F, l_run = 0.f;
       for (int t = 0; t < n_tiles; ++t) {
         mbar_wait(bar(B_SF + m), t & 1);
+        if (wq == 0 && lane == 0) K2T(14 + 6 * m, t);
         tc_fence_after();
         float x[BN];
 #pragma unroll
@@ -411,25 +495,36 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           for (int i = 0; i < 32; ++i) x[c * 32 + i] = v[i];
         }
         tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(B_SE + m));  // S_m may now be overwritten by S_m(t+1)
+        if (wq == 0 && lane == 0) K2T(15 + 6 * m, t);
         mbar_wait(bar(B_JF + t % JR), (t / JR) & 1);
         const int32_t *jcol = jcol_all + (t % JR) * BN;
-        // raw-score max (scale > 0 commutes with max); masked columns -> -inf
-        float mx = -CUDART_INF_F;
+        // raw-score max (scale > 0 commutes with max); masked columns -> -inf.  Four independent chains.
+        float mx4[4] = {-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F};
         if (jflag[t % JR]) {
 #pragma unroll
-          for (int c = 0; c < BN; ++c) mx = fmaxf(mx, x[c]);
+          for (int c = 0; c < BN; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], x[c]);
         } else {
 #pragma unroll
           for (int c = 0; c < BN; ++c) {
             if (jcol[c] > qi) x[c] = -CUDART_INF_F;
-            mx = fmaxf(mx, x[c]);
+            mx4[c & 3] = fmaxf(mx4[c & 3], x[c]);
           }
         }
+        float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
         mx = mx == -CUDART_INF_F ? mx : mx * p.scale_log2;
-        if (t > 0) mbar_wait(bar(B_OF + m), (t - 1) & 1);  // PV(t-1) done: O stable
+        if (wq == 0 && lane == 0) K2T(16 + 6 * m, t);
+        // P buffer t & 1 was last read by P.V(t-2): phase (t-2)/2 of its barrier
+        if (t >= 2) mbar_wait(bar(B_PE + 2 * m + (t & 1)), ((t - 2) >> 1) & 1);
         tc_fence_after();
         const bool need = mx > m_run + 8.f;
         if (__any_sync(0xffffffffu, need)) {
+          if (t > 0) {  // O must be stable: P.V(t-1) done (phase (t-1)/2 of buffer (t-1) & 1)
+            mbar_wait(bar(B_PE + 2 * m + ((t - 1) & 1)), ((t - 1) >> 1) & 1);
+            tc_fence_after();
+          }
           const float mn = need ? mx : m_run;
           const float a = (need && m_run != -CUDART_INF_F) ? fast_exp2(m_run - mn) : (need ? 0.f : 1.f);
           if (t > 0) {
@@ -446,35 +541,35 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           l_run *= a;
           m_run = mn;
         }
+        if (wq == 0 && lane == 0) K2T(17 + 6 * m, t);
         const float mref = m_run == -CUDART_INF_F ? 0.f : m_run;
-        // P = exp2(x * scale_log2 - m) -> bf16 pairs into the first 64 columns of this tile's S (the A
-        // operand of P.V); packed fp32x2 FMA for the argument and the row sum
+        // P = exp2(x * scale_log2 - m) -> packed bf16 pairs into P_m (the A operand of P.V)
         const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
         const float2 nm2 = make_float2(-mref, -mref);
-        float2 ls2 = make_float2(0.f, 0.f);
+        float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        float w[BN / 2];
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          float w[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            float2 a = nm2;
-            fma2(a, make_float2(x[c * 64 + 2 * i], x[c * 64 + 2 * i + 1]), sc2);
-            const float2 pp = make_float2(fast_exp2(a.x), fast_exp2(a.y));
-            ls2 = add2(ls2, pp);
-            __nv_bfloat162 pr = __floats2bfloat162_rn(pp.x, pp.y);
-            w[i] = __uint_as_float(*reinterpret_cast<uint32_t *>(&pr));
-          }
-          tmem_st32(s_col + c * 32, w);
+        for (int i = 0; i < BN / 2; ++i) {
+          float2 a = nm2;
+          fma2(a, make_float2(x[2 * i], x[2 * i + 1]), sc2);
+          // EXP_EMU of every 8 pairs go to the FMA pipe (polynomial), the rest to MUFU
+          const float2 pp = ((i & 7) >= 8 - EXP_EMU) ? exp2_poly2(a) : make_float2(fast_exp2(a.x), fast_exp2(a.y));
+          ls2[i & 1] = add2(ls2[i & 1], pp);
+          __nv_bfloat162 pr = __floats2bfloat162_rn(pp.x, pp.y);
+          w[i] = __uint_as_float(*reinterpret_cast<uint32_t *>(&pr));
         }
-        const float ls = ls2.x + ls2.y;
-        l_run += ls;
+        if (wq == 0 && lane == 0) K2T(18 + 6 * m, t);
+        tmem_st32(p_col + (t & 1) * (BN / 2), w);
+        const float2 lsum = add2(ls2[0], ls2[1]);
+        l_run += lsum.x + lsum.y;
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar(B_PF + m));
+        if (lane == 0) mbar_arrive(bar(B_PF + 2 * m + (t & 1)));
+        if (wq == 0 && lane == 0) K2T(19 + 6 * m, t);
       }
       // epilogue: O / l -> bf16 out, lse
-      mbar_wait(bar(B_OF + m), (n_tiles - 1) & 1);
+      mbar_wait(bar(B_PE + 2 * m + ((n_tiles - 1) & 1)), ((n_tiles - 1) >> 1) & 1);
       tc_fence_after();
       const float inv = 1.f / l_run;
       const int64_t orow = (static_cast<int64_t>(cd.row0 + qi) * p.Hq + u.g * G + h) * HD;
@@ -486,13 +581,13 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         if (live) {
 #pragma unroll
           for (int i = 0; i < 32; i += 8) {
-            uint32_t w[4];
+            uint32_t w4[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               __nv_bfloat162 pr = __floats2bfloat162_rn(v[i + 2 * j] * inv, v[i + 2 * j + 1] * inv);
-              w[j] = *reinterpret_cast<uint32_t *>(&pr);
+              w4[j] = *reinterpret_cast<uint32_t *>(&pr);
             }
-            *reinterpret_cast<uint4 *>(p.out + orow + c * 32 + i) = make_uint4(w[0], w[1], w[2], w[3]);
+            *reinterpret_cast<uint4 *>(p.out + orow + c * 32 + i) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
           }
         }
       }
@@ -539,7 +634,14 @@ cudaError_t launch_scatter_rows(const int32_t *dst, int T, const __nv_bfloat16 *
   return cudaGetLastError();
 }
 
-int chunk_smem_bytes() { return tc2::SMEM2; }
+int chunk_smem_bytes() { return tc3::SMEM; }
+
+#ifdef KVFS_K2_TRACE
+extern "C" int kvfs_debug_k2_trace(void *host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, g_k2_trace, bytes < sizeof(g_k2_trace) ? bytes : sizeof(g_k2_trace)) ==
+                 cudaSuccess ? 0 : -1;
+}
+#endif
 
 template <int G>
 static cudaError_t launch_chunk_g(const CUtensorMap &km, const CUtensorMap &vm, const CUtensorMap &qm,
@@ -547,11 +649,11 @@ static cudaError_t launch_chunk_g(const CUtensorMap &km, const CUtensorMap &vm, 
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(chunk_attn_tc_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         tc2::SMEM2);
+                                         tc3::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  chunk_attn_tc_kernel<G><<<n_units, tc2::THREADS, tc2::SMEM2, s>>>(km, vm, qm, p);
+  chunk_attn_tc_kernel<G><<<n_units, tc3::THREADS, tc3::SMEM, s>>>(km, vm, qm, p);
   return cudaGetLastError();
 }
 

@@ -134,6 +134,14 @@ __device__ __forceinline__ float2 add2(const float2 a, const float2 b) {
   return *reinterpret_cast<float2 *>(&dd);
 }
 
+__device__ __forceinline__ float2 sub2(const float2 a, const float2 b) {
+  unsigned long long dd;
+  const unsigned long long aa = *reinterpret_cast<const unsigned long long *>(&a);
+  const unsigned long long bb = *reinterpret_cast<const unsigned long long *>(&b);
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(dd) : "l"(aa), "l"(bb));
+  return *reinterpret_cast<float2 *>(&dd);
+}
+
 // bf16 pair (little-endian u32: element 0 in the low half) -> fp32 pair, exact.
 __device__ __forceinline__ float2 bf2_to_f2(uint32_t w) {
   return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
@@ -143,6 +151,28 @@ __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^a for a pair on the FMA/ALU pipes instead of MUFU (offloads the SFU in the tensor-core softmax):
+// round-to-nearest split a = j + f (f in [-0.5, 0.5]) with the 1.5 * 2^23 trick, 2^f by a degree-3
+// polynomial (relative error 7.7e-5, far below bf16's 2^-9 rounding of P), then j added to the exponent
+// field: bits(r) << 23 == j << 23 (mod 2^32) because bits(1.5 * 2^23) << 23 == 0 (mod 2^32).
+// Inputs are clamped at -126, so masked (-inf) columns give <= 2^-126 (not exactly 0; negligible).
+__device__ __forceinline__ float2 exp2_poly2(float2 a) {
+  a.x = fmaxf(a.x, -126.f);
+  a.y = fmaxf(a.y, -126.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 r = add2(a, magic);
+  const float2 f = sub2(a, sub2(r, magic));  // exact: r - magic is the integer j
+  float2 q = make_float2(0.05508868f, 0.05508868f);
+  float2 t = make_float2(0.24260405f, 0.24260405f);
+  fma2(t, q, f);
+  q = make_float2(0.6932762f, 0.6932762f);
+  fma2(q, t, f);
+  t = make_float2(0.99992895f, 0.99992895f);
+  fma2(t, q, f);
+  return make_float2(__uint_as_float((__float_as_uint(r.x) << 23) + __float_as_uint(t.x)),
+                     __uint_as_float((__float_as_uint(r.y) << 23) + __float_as_uint(t.y)));
 }
 
 // Position of the r-th (0-based) set bit of m (precondition: popc(m) > r).

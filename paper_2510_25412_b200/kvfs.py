@@ -14,7 +14,8 @@ from typing import Iterable, List, Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkvfs.so")
+# KVFS_LIB_PATH: an alternative in-tree build (tuning experiments); the default is the product library
+LIB_PATH = os.environ.get("KVFS_LIB_PATH") or os.path.join(_HERE, "libkvfs.so")
 
 OK, ENOENT, EIO, EBADF, ENOMEM, EBUSY, EEXIST, EINVAL, ENOSPC, ERANGE, ENOSYS = \
     0, -2, -5, -9, -12, -16, -17, -22, -28, -34, -38

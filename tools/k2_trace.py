@@ -1,0 +1,55 @@
+"""Development tool: per-tile pipeline timeline of the K2 chunk kernel (cfg4 workload).
+
+    python -c 'from paper_2510_25412_b200 import build as b; b.build(defines=("KVFS_K2_TRACE",),
+               lib="build_var/trace/libkvfs.so", out_dir="build_var/trace")'
+    KVFS_LIB_PATH=build_var/trace/libkvfs.so python tools/k2_trace.py
+
+Prints, for two CTAs, the median over tiles of every event's time relative to softmax 0's S-ready of the
+same tile, and the median tile period."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2510_25412_b200 import kvfs  # noqa: E402
+from paper_2510_25412_b200.workloads import DecodeWorkload  # noqa: E402
+
+NAMES = ["K:empty", "K:issued", "V:empty", "V:issued", "M:K(t+1)", "M:SE0", "M:S0 iss", "M:SE1", "M:S1 iss",
+         "M:V(t)", "M:PF0", "M:PV0 iss", "M:PF1", "M:PV1 iss"] + \
+        [f"S{m}:{e}" for m in range(2) for e in ("S rdy", "S read", "max", "PE/resc", "exp done", "PF arr")]
+
+
+def main():
+    wl = DecodeWorkload(os.environ.get("CFG", "cfg4"), steps_total=4)
+    kv = wl.kv
+    T = wl.n_files * wl.n_q
+    s = wl.shape
+    out = torch.empty((T, s.Hq, s.D), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((T, s.Hq), dtype=torch.float32, device="cuda")
+    for i in range(2):
+        q, k, v = wl.make_inputs(i)
+        wl.pre_step()
+        kv.pred_attn_batch(wl.descs, wl.positions(), q, k, v, out, lse)
+        wl.advance()
+    torch.cuda.synchronize()
+    buf = np.zeros((2, 32, 512), dtype=np.uint64)
+    fn = kvfs.lib().kvfs_debug_k2_trace
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+    assert fn(buf.ctypes.data, buf.nbytes) == 0
+    for c in range(2):
+        tr = buf[c].astype(np.int64)
+        n = int((tr[14] > 0).sum())
+        ref = tr[14, :n]
+        print(f"--- CTA {'0' if c == 0 else '296'}: {n} tiles, median period {np.median(np.diff(ref[5:n - 5])):.0f} clk")
+        for e, name in enumerate(NAMES):
+            d = tr[e, 5:n - 5] - ref[5:n - 5]
+            if (tr[e, 5:n - 5] == 0).all():
+                continue
+            print(f"  {name:12s} {np.median(d):8.0f}  p10 {np.percentile(d, 10):8.0f}  p90 {np.percentile(d, 90):8.0f}")
+
+
+if __name__ == "__main__":
+    main()
