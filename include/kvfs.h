@@ -230,7 +230,14 @@ typedef enum {
   KVFS_OPT_DECODE_CTAS = 1,     /* grid size of the decode kernel; 0 = auto (SM count x occupancy) */
   KVFS_OPT_CHUNK_CUTOVER = 2,   /* n_q at or above which the tcgen05 chunk kernel is used (head_dim 128);
                                    0 = never; default 8 */
-  KVFS_OPT_DETERMINISTIC = 3    /* reserved (the kernels are deterministic for a fixed grid) */
+  KVFS_OPT_DETERMINISTIC = 3,   /* reserved (the kernels are deterministic for a fixed grid) */
+  KVFS_OPT_CASCADE_MIN_ENTRIES = 4 /* shared-prefix ("cascade") decode for CoW fork families (§4.2
+                                   P:223 fork shares pages): decode descriptors (n_q
+                                   below the chunk cut-over) whose files share a leading run of at least this
+                                   many identical (page, mask) entries, all before their new tokens, have
+                                   that run attended ONCE per batch by the tcgen05 kernel over all sharers'
+                                   query rows, and the per-file rest by the decode kernel, merged exactly
+                                   (log-sum-exp).  0 = off; default 16 (head_dim 128 only) */
 } kvfs_option;
 int kvfs_set_option(kvfs_ctx *ctx, int option, int64_t value);
 
@@ -239,7 +246,9 @@ typedef enum {
   KVFS_CTR_H2D_BYTES = 2,       /* bytes of host->device metadata uploads */
   KVFS_CTR_PAGE_COPIES = 3,     /* whole-page copies (copy-on-write + fork tails), per page */
   KVFS_CTR_LAST_DECODE_CTAS = 4, /* grid (virtual CTAs = rings) of the last decode launch */
-  KVFS_CTR_LAST_CHUNK_UNITS = 5  /* CTAs of the last tcgen05 chunk launch (0: none) */
+  KVFS_CTR_LAST_CHUNK_UNITS = 5, /* CTAs of the last tcgen05 chunk launch (0: none) */
+  KVFS_CTR_LAST_PREFIX_UNITS = 6,  /* CTAs of the last shared-prefix (cascade) launch (0: none) */
+  KVFS_CTR_LAST_PREFIX_GROUPS = 7  /* fork families (groups) the last pred batch attended as shared prefixes */
 } kvfs_counter;
 int kvfs_get_counter(kvfs_ctx *ctx, int counter, int64_t *value);
 

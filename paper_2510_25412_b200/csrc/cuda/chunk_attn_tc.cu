@@ -197,7 +197,11 @@ __device__ unsigned long long g_k2_trace[2][32][512];
   } while (0)
 #endif
 
-template <int G>
+// PREFIX = shared-prefix (cascade) mode: a unit is (fork family + key split, kv head, M-tile pair); the
+// rows are the family's query tokens x the G heads of the kv head (gathered from Q by the softmax warps
+// into the 128B-swizzled layout), every key is an old retained token (no causal part), and the output is
+// the unnormalised partial (O, m, l) per (row, head) that the decode kernel merges.
+template <int G, bool PREFIX>
 __global__ void __launch_bounds__(tc2::THREADS, 1)
     chunk_attn_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                          const __grid_constant__ CUtensorMap qmap, const ChunkParams p) {
@@ -220,7 +224,13 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   const int trace_cta = blockIdx.x == 0 ? 0 : (blockIdx.x == 296 ? 1 : -1);
 #endif
   const ChunkUnit u = p.units[blockIdx.x];
-  const ChunkDesc cd = p.descs[u.desc];
+  ChunkDesc cd;
+  if constexpr (PREFIX) {
+    const PrefixDesc pd = p.pdescs[u.desc];
+    cd = ChunkDesc{pd.slab_off, pd.n_entries, 0, pd.n_rows, pd.row0, pd.n_entries, 0, 0};
+  } else {
+    cd = p.descs[u.desc];
+  }
   const int epb = BN / p.P;  // page entries per KV tile
   const int n_tiles = (cd.n_entries + epb - 1) / epb;
   const int rows_total = cd.n_q * G;
@@ -228,7 +238,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   const int n_mt = min(2, (rows_total + BM - 1) / BM - m0);  // 1 or 2 M-tiles
 
   if (threadIdx.x == 0) {
-    mbar_init(bar(B_Q), 1);
+    mbar_init(bar(B_Q), PREFIX ? 4 * n_mt : 1);  // prefix: one arrival per softmax warp that gathers Q
     for (int s = 0; s < KV2; ++s) {
       mbar_init(bar(B_KF + s), 1);
       mbar_init(bar(B_KE + s), 1);
@@ -261,7 +271,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
     if (warp == 0) {
       // ============================================================ K producer (+ Q, + column metadata)
       const uint64_t pol = policy_evict_first();
-      if (lane == 0) {
+      if (!PREFIX && lane == 0) {
         mbar_arrive_expect_tx(bar(B_Q), n_mt * TILE_BYTES);
         for (int m = 0; m < n_mt; ++m) {
           const int qrow = cd.row0 + ((m0 + m) * BM) / G;
@@ -425,6 +435,27 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
       const uint32_t s_col = tmem + lane_addr + m * BN;
       const uint32_t o_col = tmem + lane_addr + O_COL2 + m * HD;
+      if constexpr (PREFIX) {
+        // thread r gathers its row (family token qi, head h) of Q into the K-major SW128 tile: 16-byte
+        // chunk cc of row r of a 64-column half lands at chunk cc ^ (r % 8) of the row's 128-byte line
+        uint8_t *qt = smem + OFF_Q2 + m * TILE_BYTES;
+        uint4 v[16];
+        if (live) {
+          const PrefixRow pr = p.prows[cd.row0 + qi];
+          const uint4 *src = reinterpret_cast<const uint4 *>(p.q + (static_cast<int64_t>(pr.t) * p.Hq + u.g * G + h) * HD);
+#pragma unroll
+          for (int c = 0; c < 16; ++c) v[c] = __ldg(src + c);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) v[c] = make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          *reinterpret_cast<uint4 *>(qt + (c >> 3) * HALF_BYTES + r * 128 + (((c & 7) ^ (r & 7)) << 4)) = v[c];
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(B_Q));
+      }
       float m_run = -CUDART_INF_F, l_run = 0.f;
       for (int t = 0; t < n_tiles; ++t) {
         mbar_wait(bar(B_SF + m), t & 1);
@@ -509,9 +540,30 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         if (lane == 0) mbar_arrive(bar(B_PF + m));
         if (wq == 0 && lane == 0) K2T(19 + 6 * m, t);
       }
-      // epilogue: O / l -> bf16 out, lse
+      // epilogue: O / l -> bf16 out, lse   (prefix mode: the partial O, m, l of the split)
       mbar_wait(bar(B_OF + m), (n_tiles - 1) & 1);
       tc_fence_after();
+      if constexpr (PREFIX) {
+        float *dst = nullptr;
+        if (live) {
+          const PrefixRow pr = p.prows[cd.row0 + qi];
+          const PrefixDesc pd = p.pdescs[u.desc];
+          const int64_t idx = pr.pref_base + static_cast<int64_t>(u.g * pr.n_q + pr.qi) * pd.n_splits + pd.split;
+          dst = p.ppart + idx * (G * (HD + 2)) + h * (HD + 2);
+        }
+#pragma unroll
+        for (int c = 0; c < HD / 32; ++c) {
+          float v[32];
+          tmem_ld32(o_col + c * 32, v);
+          tmem_wait_ld();
+          if (live) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 2)
+              *reinterpret_cast<float2 *>(dst + c * 32 + i) = make_float2(v[i], v[i + 1]);
+          }
+        }
+        if (live) *reinterpret_cast<float2 *>(dst + HD) = make_float2(m_run, l_run);
+      } else {
       const float inv = 1.f / l_run;
       const int64_t orow = (static_cast<int64_t>(cd.row0 + qi) * p.Hq + u.g * G + h) * HD;
 #pragma unroll
@@ -535,6 +587,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       if (live && p.lse)
         p.lse[static_cast<int64_t>(cd.row0 + qi) * p.Hq + u.g * G + h] =
             (m_run + __log2f(l_run)) * 0.69314718055994531f;
+      }
     }
   }
   tc_fence_before();
@@ -584,29 +637,40 @@ extern "C" int kvfs_debug_k2_trace(void *host, size_t bytes) {
 }
 #endif
 
-template <int G>
+template <int G, bool PREFIX>
 static cudaError_t launch_chunk_g(const CUtensorMap &km, const CUtensorMap &vm, const CUtensorMap &qm,
                                   const ChunkParams &p, int n_units, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(chunk_attn_tc_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         tc2::SMEM2);
+    cudaError_t e = cudaFuncSetAttribute(chunk_attn_tc_kernel<G, PREFIX>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM2);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  chunk_attn_tc_kernel<G><<<n_units, tc2::THREADS, tc2::SMEM2, s>>>(km, vm, qm, p);
+  chunk_attn_tc_kernel<G, PREFIX><<<n_units, tc2::THREADS, tc2::SMEM2, s>>>(km, vm, qm, p);
   return cudaGetLastError();
+}
+
+template <bool PREFIX>
+static cudaError_t launch_mode(const CUtensorMap &km, const CUtensorMap &vm, const CUtensorMap &qm,
+                               const ChunkParams &p, int n_units, int G, cudaStream_t s) {
+  switch (G) {
+    case 1: return launch_chunk_g<1, PREFIX>(km, vm, qm, p, n_units, s);
+    case 2: return launch_chunk_g<2, PREFIX>(km, vm, qm, p, n_units, s);
+    case 4: return launch_chunk_g<4, PREFIX>(km, vm, qm, p, n_units, s);
+    case 8: return launch_chunk_g<8, PREFIX>(km, vm, qm, p, n_units, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_chunk(const CUtensorMap &km, const CUtensorMap &vm, const CUtensorMap &qm, const ChunkParams &p,
                          int n_units, int G, cudaStream_t s) {
-  switch (G) {
-    case 1: return launch_chunk_g<1>(km, vm, qm, p, n_units, s);
-    case 2: return launch_chunk_g<2>(km, vm, qm, p, n_units, s);
-    case 4: return launch_chunk_g<4>(km, vm, qm, p, n_units, s);
-    case 8: return launch_chunk_g<8>(km, vm, qm, p, n_units, s);
-    default: return cudaErrorInvalidValue;
-  }
+  return launch_mode<false>(km, vm, qm, p, n_units, G, s);
+}
+
+cudaError_t launch_prefix(const CUtensorMap &km, const CUtensorMap &vm, const CUtensorMap &qm, const ChunkParams &p,
+                          int n_units, int G, cudaStream_t s) {
+  return launch_mode<true>(km, vm, qm, p, n_units, G, s);
 }
 
 }  // namespace dev

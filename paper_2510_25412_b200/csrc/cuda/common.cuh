@@ -27,7 +27,9 @@ struct Desc {  // == kvfs::DevDesc
   int32_t tail_lstart;
   int32_t first_new_entry;
   int32_t first_new_lstart;
-  int32_t pad0, pad1, pad2;
+  int32_t skip;         // leading entries attended by the shared-prefix kernel
+  int32_t pref_splits;  // shared-prefix partials per unit (0: none)
+  int32_t pref_base;    // partial of unit (g, qi), split s: pref_base + (g * n_q + qi) * pref_splits + s
 };
 
 struct SlabRun {

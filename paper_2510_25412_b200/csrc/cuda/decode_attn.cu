@@ -179,18 +179,20 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
         int64_t off = 0;
         int lo = 0, nrows = 0;
         const int st = sg.st0 + base + lane;
+        const int n_os = dd.n_old_entries - dd.skip;  // old-entry stages (the shared prefix is skipped)
         if (lane < n) {
-          if (st < dd.n_old_entries) {
-            const Entry e = p.slab[dd.slab_off + st];
+          if (st < n_os) {
+            const int ent = st + dd.skip;
+            const Entry e = p.slab[dd.slab_off + ent];
             mask = e.mask;
             // only the last old entry can also hold new tokens (the device lstart is not maintained)
-            if (st == dd.n_old_entries - 1) mask = lowest_bits(mask, dd.n_old - dd.tail_lstart);
+            if (ent == dd.n_old_entries - 1) mask = lowest_bits(mask, dd.n_old - dd.tail_lstart);
             lo = __ffsll(static_cast<long long>(mask)) - 1;
             const int hi = 63 - __clzll(static_cast<long long>(mask));
             nrows = hi - lo + 1;
             off = ((static_cast<int64_t>(e.page) * p.Hkv + sg.g) * P + lo) * D;
           } else {
-            const int v0 = (st - dd.n_old_entries) * P;
+            const int v0 = (st - n_os) * P;
             const int r_end = min(dd.n_q, v0 + P);
             const int vis_end = min(r_end, sg.qi + 1);  // causal: row qi sees new rows <= qi
             const int n_vis = vis_end > v0 ? vis_end - v0 : 0;
@@ -392,7 +394,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
       // fused append: the new-row stage of unit qi = 0 writes K_new / V_new into the reserved slots
       if (m.kind == 1 && sg.qi == 0) {
         const int st = sg.st0 + i;
-        const int v0 = (st - dd.n_old_entries) * P;
+        const int v0 = (st - (dd.n_old_entries - dd.skip)) * P;
         constexpr int CPR = D / 8;  // 16-byte chunks per row
         for (int idx = lane; idx < m.nrows * CPR; idx += 32) {
           const int r = idx / CPR, cc = idx % CPR;
@@ -441,12 +443,18 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
     const int tid = warp * 32 + lane;  // 0 .. NW*32-1 within the ring
     const int unit = dd.unit_base + sg.g * dd.n_q + sg.qi;
     const int64_t row = dd.row0 + sg.qi;
+    // shared-prefix partials of this unit (written by the prefix kernel earlier on the stream)
+    const float *pref = dd.pref_splits
+                            ? p.ppart + (static_cast<int64_t>(dd.pref_base) +
+                                         static_cast<int64_t>(sg.g * dd.n_q + sg.qi) * dd.pref_splits) * C::PART
+                            : nullptr;
     if (whole) {
       for (int e = tid; e < G * D / 2; e += NW * 32) {
         const int h = e / (D / 2), dim = (e % (D / 2)) * 2;
         float M = -CUDART_INF_F;
 #pragma unroll
         for (int w = 0; w < NW; ++w) M = fmaxf(M, comb[w * C::PART + h * (D + 2) + D]);
+        for (int s = 0; s < dd.pref_splits; ++s) M = fmaxf(M, __ldcg(pref + s * C::PART + h * (D + 2) + D));
         float L = 0.f, ox = 0.f, oy = 0.f;
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
@@ -455,6 +463,15 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
           L += cwp[D + 1] * f;
           ox += cwp[dim] * f;
           oy += cwp[dim + 1] * f;
+        }
+        for (int s = 0; s < dd.pref_splits; ++s) {
+          const float *pc = pref + s * C::PART + h * (D + 2);
+          const float2 ml = __ldcg(reinterpret_cast<const float2 *>(pc + D));
+          const float2 o = __ldcg(reinterpret_cast<const float2 *>(pc + dim));
+          const float f = (ml.x == -CUDART_INF_F) ? 0.f : fast_exp2(ml.x - M);
+          L += ml.y * f;
+          ox += o.x * f;
+          oy += o.y * f;
         }
         const float inv = 1.f / L;
         const int64_t oidx = (row * p.Hq + sg.g * G + h) * D + dim;
@@ -506,7 +523,17 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
             const float *pc = p.partials + (static_cast<int64_t>(c) * 2 + wh) * C::PART + h * (D + 2);
             M = fmaxf(M, __ldcg(pc + D));
           }
+          for (int s = 0; s < dd.pref_splits; ++s) M = fmaxf(M, __ldcg(pref + s * C::PART + h * (D + 2) + D));
           float L = 0.f, ox = 0.f, oy = 0.f;
+          for (int s = 0; s < dd.pref_splits; ++s) {
+            const float *pc = pref + s * C::PART + h * (D + 2);
+            const float2 ml = __ldcg(reinterpret_cast<const float2 *>(pc + D));
+            const float2 o = __ldcg(reinterpret_cast<const float2 *>(pc + dim));
+            const float f = (ml.x == -CUDART_INF_F) ? 0.f : fast_exp2(ml.x - M);
+            L += ml.y * f;
+            ox += o.x * f;
+            oy += o.y * f;
+          }
           for (int c = c0; c <= c1; ++c) {
             const int wh = (cta_start(c, p.total, p.ncta) >= ua) ? 0 : 1;
             const float *pc = p.partials + (static_cast<int64_t>(c) * 2 + wh) * C::PART + h * (D + 2);

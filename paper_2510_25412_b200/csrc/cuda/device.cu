@@ -22,7 +22,8 @@ constexpr int kMaxCtas = 2048;
 size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
 struct WsLayout {
-  size_t slab = 0, upload = 0, counters = 0, partials = 0, ptrs = 0, total = 0, upload_cap = 0;
+  size_t slab = 0, upload = 0, counters = 0, partials = 0, ptrs = 0, prefix = 0, total = 0, upload_cap = 0;
+  int64_t prefix_cap = 0;  // shared-prefix partials (PART floats each)
 };
 
 WsLayout ws_layout(const kvfs_config &c) {
@@ -43,6 +44,12 @@ WsLayout ws_layout(const kvfs_config &c) {
   off = align256(off + static_cast<size_t>(kMaxCtas) * 2 * part);
   w.ptrs = off;
   off = align256(off + static_cast<size_t>(c.n_layers) * 2 * sizeof(void *));
+  // shared-prefix (cascade) partials: up to 16 key splits per decode unit, capped at 16384 partials
+  w.prefix_cap = c.head_dim == 128
+                     ? std::min<int64_t>(static_cast<int64_t>(c.max_batch_rows) * c.n_kv_heads * 16, 16384)
+                     : 0;
+  w.prefix = off;
+  off = align256(off + static_cast<size_t>(w.prefix_cap) * part);
   w.total = off;
   return w;
 }
@@ -213,6 +220,7 @@ class CudaDevice final : public Device {
     upload_ = ws + lay_.upload;
     counters_ = reinterpret_cast<int *>(ws + lay_.counters);
     partials_ = reinterpret_cast<float *>(ws + lay_.partials);
+    ppart_ = reinterpret_cast<float *>(ws + lay_.prefix);
     kptrs_ = reinterpret_cast<bf16 **>(ws + lay_.ptrs);
     vptrs_ = kptrs_ + cfg.n_layers;
     std::vector<void *> ptrs(c_.kpool);
@@ -316,7 +324,11 @@ class CudaDevice final : public Device {
     d_cdescs_ = push(pl.chunk_descs.data(), pl.chunk_descs.size() * sizeof(ChunkDesc));
     d_cunits_ = push(pl.chunk_units.data(), pl.chunk_units.size() * sizeof(ChunkUnit));
     d_cdst_ = push(pl.chunk_dst.data(), pl.chunk_dst.size() * sizeof(int32_t));
-    if (!d_runs_ || !d_run_entries_ || !d_copies_ || !d_descs_ || !d_dst_ || !d_cdescs_ || !d_cunits_ || !d_cdst_)
+    d_pdescs_ = push(pl.prefix_descs.data(), pl.prefix_descs.size() * sizeof(PrefixDesc));
+    d_punits_ = push(pl.prefix_units.data(), pl.prefix_units.size() * sizeof(ChunkUnit));
+    d_prows_ = push(pl.prefix_rows.data(), pl.prefix_rows.size() * sizeof(PrefixRow));
+    if (!d_runs_ || !d_run_entries_ || !d_copies_ || !d_descs_ || !d_dst_ || !d_cdescs_ || !d_cunits_ || !d_cdst_ ||
+        !d_pdescs_ || !d_punits_ || !d_prows_)
       return KVFS_ENOMEM;
     if (!send(s)) return KVFS_EIO;
     if (pl.runs.empty() && pl.copies.empty()) return KVFS_OK;
@@ -328,11 +340,17 @@ class CudaDevice final : public Device {
   int pred_layer(const PredPlan &pl, int layer, const void *q, const void *k_new, const void *v_new, void *out,
                  float *lse, float scale, kvfs_stream_t s) override {
     c_.ctr.last_chunk_units = static_cast<int64_t>(pl.chunk_units.size());
+    c_.ctr.last_prefix_units = static_cast<int64_t>(pl.prefix_units.size());
+    c_.ctr.last_prefix_groups = pl.prefix_groups;
     if (!pl.chunk_units.empty()) {
       const int rc = chunk_layer(pl, layer, q, k_new, v_new, out, lse, scale, s);
       if (rc != KVFS_OK) return rc;
     }
     if (pl.descs.empty()) return KVFS_OK;
+    if (!pl.prefix_units.empty()) {
+      const int rc = prefix_layer(pl, layer, q, scale, s);
+      if (rc != KVFS_OK) return rc;
+    }
     const kvfs_config &cfg = c_.cfg;
     dev::DecodeParams p{};
     p.descs = static_cast<const dev::Desc *>(d_descs_);
@@ -353,6 +371,7 @@ class CudaDevice final : public Device {
     p.vpool = static_cast<bf16 *>(c_.vpool[layer]);
     p.scale_log2 = scale * 1.4426950408889634f;
     p.partials = partials_;
+    p.ppart = ppart_;
     p.counters = counters_;
     p.Hq = cfg.n_q_heads;
     p.Hkv = cfg.n_kv_heads;
@@ -363,6 +382,32 @@ class CudaDevice final : public Device {
   }
 
   int sync() override { return cudaDeviceSynchronize() == cudaSuccess ? KVFS_OK : KVFS_EIO; }
+  int sms() const override { return sms_; }
+  int64_t prefix_partial_capacity() const override { return lay_.prefix_cap; }
+
+  // Shared-prefix (cascade) attention of the fork families (tcgen05 kernel in prefix mode): partials
+  // (O, m, l) per (member row, head, key split) into the workspace, merged by the decode kernel.
+  int prefix_layer(const PredPlan &pl, int layer, const void *q, float scale, kvfs_stream_t s) {
+    const kvfs_config &cfg = c_.cfg;
+    const int G = cfg.n_q_heads / cfg.n_kv_heads;
+    dev::ChunkParams p{};
+    p.units = static_cast<const dev::ChunkUnit *>(d_punits_);
+    p.descs = nullptr;
+    p.slab = slab_;
+    p.scale_log2 = scale * 1.4426950408889634f;
+    p.P = cfg.page_size;
+    p.Hkv = cfg.n_kv_heads;
+    p.Hq = cfg.n_q_heads;
+    p.pool_rows = static_cast<int>(cfg.n_pages * cfg.n_kv_heads * cfg.page_size);
+    p.pdescs = static_cast<const dev::PrefixDesc *>(d_pdescs_);
+    p.prows = static_cast<const dev::PrefixRow *>(d_prows_);
+    p.q = static_cast<const bf16 *>(q);
+    p.ppart = ppart_;
+    const cudaError_t e = dev::launch_prefix(kmaps_[layer], vmaps_[layer], kmaps_[layer], p,
+                                             static_cast<int>(pl.prefix_units.size()), G, cs(s));
+    ++c_.ctr.launches;
+    return e == cudaSuccess ? KVFS_OK : KVFS_EIO;
+  }
 
   int pack_pages(const std::vector<uint32_t> &pages, void *buf, kvfs_stream_t s) override {
     return pack_impl(pages, buf, 0, s);
@@ -538,6 +583,7 @@ class CudaDevice final : public Device {
   char *upload_ = nullptr;
   int *counters_ = nullptr;
   float *partials_ = nullptr;
+  float *ppart_ = nullptr;
   bf16 **kptrs_ = nullptr, **vptrs_ = nullptr;
   int sms_ = 148;
   int per_sm_ = 0;
@@ -546,7 +592,8 @@ class CudaDevice final : public Device {
   size_t used_ = 0;
   std::vector<Pending> pending_;
   const void *d_runs_ = nullptr, *d_run_entries_ = nullptr, *d_copies_ = nullptr, *d_descs_ = nullptr,
-             *d_dst_ = nullptr, *d_cdescs_ = nullptr, *d_cunits_ = nullptr, *d_cdst_ = nullptr;
+             *d_dst_ = nullptr, *d_cdescs_ = nullptr, *d_cunits_ = nullptr, *d_cdst_ = nullptr,
+             *d_pdescs_ = nullptr, *d_punits_ = nullptr, *d_prows_ = nullptr;
   PFN_cuTensorMapEncodeTiled_v12000 encode_ = nullptr;
   std::vector<CUtensorMap> kmaps_, vmaps_;
 };

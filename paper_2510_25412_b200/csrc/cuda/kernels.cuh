@@ -20,6 +20,7 @@ struct DecodeParams {
   __nv_bfloat16 *kpool, *vpool;
   float scale_log2;  // scale * log2(e)
   float *partials;   // [ncta][2][PART]
+  const float *ppart;  // shared-prefix partials [..][PART] (Desc::pref_*)
   int *counters;     // [n_units]
   int Hq, Hkv;
 };
@@ -32,6 +33,12 @@ struct ChunkDesc {  // == kvfs::ChunkDesc
 struct ChunkUnit {  // == kvfs::ChunkUnit
   int32_t desc, g, m, pad;
 };
+struct PrefixDesc {  // == kvfs::PrefixDesc
+  int32_t slab_off, n_entries, n_rows, row0, split, n_splits, pad0, pad1;
+};
+struct PrefixRow {  // == kvfs::PrefixRow
+  int32_t t, pref_base, n_q, qi;
+};
 struct ChunkParams {
   const ChunkUnit *units;
   const ChunkDesc *descs;
@@ -41,12 +48,20 @@ struct ChunkParams {
   float scale_log2;
   int P, Hkv, Hq;
   int pool_rows;  // n_pages * Hkv * P: a row coordinate out of the pool tensor (zero-filled TMA box)
+  // shared-prefix mode only: units index pdescs; Q rows gathered through prows; partials -> ppart
+  const PrefixDesc *pdescs;
+  const PrefixRow *prows;
+  const __nv_bfloat16 *q;
+  float *ppart;
 };
 cudaError_t launch_chunk(const CUtensorMap &km, const CUtensorMap &vm, const CUtensorMap &qm, const ChunkParams &p,
                          int n_units, int G, cudaStream_t s);
 cudaError_t launch_scatter_rows(const int32_t *dst, int T, const __nv_bfloat16 *k, const __nv_bfloat16 *v,
                                 __nv_bfloat16 *kp, __nv_bfloat16 *vp, int Hkv, int D, int P, int sms, cudaStream_t s);
 int chunk_smem_bytes();
+// Shared-prefix (cascade) attention: same kernel in prefix mode (no causal part, partial (O, m, l) output).
+cudaError_t launch_prefix(const CUtensorMap &km, const CUtensorMap &vm, const CUtensorMap &qm, const ChunkParams &p,
+                          int n_units, int G, cudaStream_t s);
 
 // resident decode CTAs per SM for this shape (occupancy query; the default grid is SMs x this)
 int decode_ctas_per_sm(int D, int G, int P);

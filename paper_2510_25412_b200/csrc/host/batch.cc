@@ -3,6 +3,7 @@
 // descriptor list, per-row destination slots of the append, copy-on-write copies, and the slab
 // updates (table deltas) of the files in the batch.
 #include <algorithm>
+#include <unordered_map>
 
 #include "kvfs_impl.h"
 
@@ -35,6 +36,12 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
   pl.chunk_descs.clear();
   pl.chunk_units.clear();
   pl.chunk_dst.clear();
+  pl.desc_files.clear();
+  pl.prefix_descs.clear();
+  pl.prefix_units.clear();
+  pl.prefix_rows.clear();
+  pl.prefix_partials = 0;
+  pl.prefix_groups = 0;
   std::vector<int32_t> dst;
   int64_t row = 0;
   bool partial = false;
@@ -91,6 +98,7 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
           d.first_new_entry = static_cast<int32_t>(fne);
           d.first_new_lstart = f->table[fne].lstart;
           pl.descs.push_back(d);
+          pl.desc_files.push_back(f);
           pl.total_cost += static_cast<int64_t>(Hkv) * nq * d.stages_per_unit;
           pl.n_units += Hkv * nq;
           pl.max_nq = std::max(pl.max_nq, nq);
@@ -136,9 +144,11 @@ void pred_split(const Ctx &c, int64_t cutover, PredPlan *plan) {
   if (cutover <= 0 || c.cfg.head_dim != 128) return;
   const int P = c.cfg.page_size, Hkv = c.cfg.n_kv_heads, G = c.cfg.n_q_heads / c.cfg.n_kv_heads;
   std::vector<DevDesc> keep;
+  std::vector<File *> keep_files;
   int64_t cost = 0;
   int32_t units = 0;
-  for (const DevDesc &d : pl.descs) {
+  for (size_t i = 0; i < pl.descs.size(); ++i) {
+    const DevDesc &d = pl.descs[i];
     if (d.n_q >= cutover) {
       if (pl.chunk_dst.empty()) pl.chunk_dst.assign(static_cast<size_t>(pl.T), -1);
       ChunkDesc cd{d.slab_off, d.n_entries, d.n_old, d.n_q, d.row0, d.first_new_entry, d.first_new_lstart, 0};
@@ -156,11 +166,115 @@ void pred_split(const Ctx &c, int64_t cutover, PredPlan *plan) {
     cost += static_cast<int64_t>(Hkv) * d.n_q * d.stages_per_unit;
     units += Hkv * d.n_q;
     keep.push_back(k);
+    keep_files.push_back(pl.desc_files[i]);
   }
   (void)P;
   pl.descs.swap(keep);
+  pl.desc_files.swap(keep_files);
   pl.total_cost = cost;
   pl.n_units = units;
+}
+
+}  // namespace kvfs
+
+namespace kvfs {
+
+// Shared-prefix (cascade) planning, SURVEY §8(f) NEXT-1.  Fork shares pages without copying them (PAPER.md
+// §4.2, `fig:example` P:177); a batch of decode steps of a fork family then reads the same leading
+// pages once per member.  Here the run of identical leading (page, mask) entries common to a family is
+// attended once per (family, kv head, key split) with all members' query rows as the M dimension of the
+// tcgen05 kernel, and every member's decode unit starts after the run and merges the prefix partials
+// (exact: softmax over a disjoint union of key sets = log-sum-exp merge of the parts).
+void pred_cascade(const Ctx &c, int64_t min_entries, int sms, int64_t max_partials, PredPlan *plan) {
+  PredPlan &pl = *plan;
+  pl.prefix_descs.clear();
+  pl.prefix_units.clear();
+  pl.prefix_rows.clear();
+  pl.prefix_partials = 0;
+  pl.prefix_groups = 0;
+  const int P = c.cfg.page_size, Hkv = c.cfg.n_kv_heads, G = c.cfg.n_q_heads / c.cfg.n_kv_heads;
+  if (min_entries <= 0 || c.cfg.head_dim != 128 || pl.descs.size() < 2) return;
+  const int epb = 128 / P;  // page entries per 128-key tile
+  // families: descriptors keyed by their first page (shared: refcount >= 2), in first-appearance order
+  std::unordered_map<uint32_t, int> gid;
+  std::vector<std::vector<int>> fam;
+  for (size_t i = 0; i < pl.descs.size(); ++i) {
+    const File *f = pl.desc_files[i];
+    if (pl.descs[i].first_new_entry < min_entries || f->table.empty()) continue;
+    const uint32_t p0 = f->table[0].page;
+    if (c.pool->refcnt(p0) < 2) continue;
+    auto it = gid.find(p0);
+    if (it == gid.end()) {
+      gid.emplace(p0, static_cast<int>(fam.size()));
+      fam.push_back({static_cast<int>(i)});
+    } else {
+      fam[it->second].push_back(static_cast<int>(i));
+    }
+  }
+  struct Fam {
+    int idx, E, rows, tiles, mpairs, S;
+  };
+  std::vector<Fam> use;
+  for (size_t k = 0; k < fam.size(); ++k) {
+    const std::vector<int> &m = fam[k];
+    if (m.size() < 2) continue;
+    const File *lf = pl.desc_files[m[0]];
+    int E = pl.descs[m[0]].first_new_entry;
+    for (size_t j = 1; j < m.size() && E > 0; ++j) {
+      const File *f = pl.desc_files[m[j]];
+      const int lim = std::min(E, pl.descs[m[j]].first_new_entry);
+      int e = 0;
+      while (e < lim && f->table[e].page == lf->table[e].page && f->table[e].mask == lf->table[e].mask) ++e;
+      E = e;
+    }
+    if (E < min_entries) continue;
+    int rows = 0;
+    for (int i : m) rows += pl.descs[i].n_q;
+    const int mt = (rows * G + 127) / 128;
+    use.push_back({static_cast<int>(k), E, rows, (E + epb - 1) / epb, (mt + 1) / 2, 1});
+  }
+  if (use.empty()) return;
+  // key splits: about one CTA per SM over all families, at most 16 and at most one tile each
+  int64_t units_per_split = 0, rows_all = 0;
+  for (const Fam &u : use) {
+    units_per_split += static_cast<int64_t>(Hkv) * u.mpairs;
+    rows_all += u.rows;
+  }
+  int S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(16, sms / std::max<int64_t>(1, units_per_split))));
+  while (S > 1 && rows_all * Hkv * S > max_partials) --S;
+  if (rows_all * Hkv * S > max_partials) return;  // workspace too small: no cascade
+  for (Fam &u : use) {
+    const int want = std::min(S, u.tiles);
+    const int tps = (u.tiles + want - 1) / want;  // tiles per split
+    u.S = (u.tiles + tps - 1) / tps;              // no empty split
+    const std::vector<int> &m = fam[u.idx];
+    const int row0 = static_cast<int>(pl.prefix_rows.size());
+    for (int i : m) {
+      DevDesc &d = pl.descs[i];
+      d.skip = u.E;
+      d.pref_splits = u.S;
+      d.pref_base = pl.prefix_partials;
+      pl.prefix_partials += Hkv * d.n_q * u.S;
+      d.stages_per_unit = (d.n_old_entries - u.E) + (d.n_q + P - 1) / P;
+      for (int qi = 0; qi < d.n_q; ++qi) pl.prefix_rows.push_back({d.row0 + qi, d.pref_base, d.n_q, qi});
+    }
+    const DevDesc &lead = pl.descs[m[0]];
+    for (int sp = 0; sp < u.S; ++sp) {
+      const int e0 = sp * tps * epb, e1 = std::min(u.E, (sp + 1) * tps * epb);
+      const int32_t di = static_cast<int32_t>(pl.prefix_descs.size());
+      pl.prefix_descs.push_back({lead.slab_off + e0, e1 - e0, u.rows, row0, sp, u.S, 0, 0});
+      for (int g = 0; g < Hkv; ++g)
+        for (int mp = 0; mp < u.mpairs; ++mp) pl.prefix_units.push_back({di, g, mp, 0});
+    }
+    ++pl.prefix_groups;
+  }
+  // the members' decode work shrank: re-pack the K1 stage ranges
+  int64_t cost = 0;
+  for (DevDesc &d : pl.descs) {
+    d.cost_begin = cost;
+    cost += static_cast<int64_t>(Hkv) * d.n_q * d.stages_per_unit;
+  }
+  pl.total_cost = cost;
 }
 
 }  // namespace kvfs

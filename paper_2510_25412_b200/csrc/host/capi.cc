@@ -229,7 +229,10 @@ int pred_step_begin(kvfs_ctx *ctx, const pred_desc *descs, int n_desc, const int
   if (c.dev && c.poisoned) return KVFS_EIO;
   const int rc = pred_reserve(c, descs, n_desc, pos, status, &c.plan);
   if (rc != KVFS_OK && rc != KVFS_EPARTIAL) return rc;
-  if (c.dev) pred_split(c, c.opt_chunk_cutover, &c.plan);
+  if (c.dev) {
+    pred_split(c, c.opt_chunk_cutover, &c.plan);
+    pred_cascade(c, c.opt_cascade_min_entries, c.dev->sms(), c.dev->prefix_partial_capacity(), &c.plan);
+  }
   if (c.dev) {
     const int drc = c.dev->pred_begin(c.plan, stream);
     if (drc != KVFS_OK) {
@@ -416,6 +419,10 @@ int kvfs_set_option(kvfs_ctx *ctx, int option, int64_t value) {
       return KVFS_OK;
     case KVFS_OPT_DETERMINISTIC:
       return KVFS_OK;
+    case KVFS_OPT_CASCADE_MIN_ENTRIES:
+      if (value < 0) return KVFS_EINVAL;
+      c.opt_cascade_min_entries = value;
+      return KVFS_OK;
     default:
       return KVFS_EINVAL;
   }
@@ -431,6 +438,8 @@ int kvfs_get_counter(kvfs_ctx *ctx, int counter, int64_t *value) {
     case KVFS_CTR_PAGE_COPIES: *value = c.ctr.page_copies; return KVFS_OK;
     case KVFS_CTR_LAST_DECODE_CTAS: *value = c.ctr.last_decode_ctas; return KVFS_OK;
     case KVFS_CTR_LAST_CHUNK_UNITS: *value = c.ctr.last_chunk_units; return KVFS_OK;
+    case KVFS_CTR_LAST_PREFIX_UNITS: *value = c.ctr.last_prefix_units; return KVFS_OK;
+    case KVFS_CTR_LAST_PREFIX_GROUPS: *value = c.ctr.last_prefix_groups; return KVFS_OK;
     default: return KVFS_EINVAL;
   }
 }

@@ -70,7 +70,10 @@ struct DevDesc {
   int32_t tail_lstart;       // logical index of the first token of entry n_old_entries - 1
   int32_t first_new_entry;   // entry holding logical token n_old (the first new token)
   int32_t first_new_lstart;  // logical index of that entry's first token
-  int32_t pad0, pad1, pad2;
+  int32_t skip;              // leading entries attended by the shared-prefix kernel (0: none)
+  int32_t pref_splits;       // shared-prefix partials per unit (0: none)
+  int32_t pref_base;         // first shared-prefix partial of unit (g = 0, qi = 0): unit (g, qi) split s is
+                             // partial pref_base + (g * n_q + qi) * pref_splits + s
 };
 static_assert(sizeof(DevDesc) == 64, "DevDesc must be 64 bytes");
 
@@ -88,6 +91,21 @@ struct ChunkDesc {
 struct ChunkUnit {
   int32_t desc, g, m, pad;
 };
+// Shared-prefix (cascade) work: one record per (fork family, key split); the family's query rows are
+// listed in PrefixRow order (row0 .. row0 + n_rows - 1).
+struct PrefixDesc {
+  int32_t slab_off;   // slab index of the split's first entry (in the leader file's table)
+  int32_t n_entries;  // entries of this split
+  int32_t n_rows;     // query rows (tokens) of the family
+  int32_t row0;       // first PrefixRow of the family
+  int32_t split, n_splits, pad0, pad1;
+};
+struct PrefixRow {
+  int32_t t;          // packed row (Q row) of the query token
+  int32_t pref_base;  // DevDesc::pref_base of its descriptor
+  int32_t n_q;        // n_q of its descriptor
+  int32_t qi;         // row within its descriptor
+};
 
 struct PredPlan {
   std::vector<DevDesc> descs;       // successful descriptors with n_q > 0, in order
@@ -103,12 +121,20 @@ struct PredPlan {
   std::vector<ChunkDesc> chunk_descs;
   std::vector<ChunkUnit> chunk_units;
   std::vector<int32_t> chunk_dst;  // [T] dst slot of rows of K2 descriptors, -1 otherwise
+  std::vector<File *> desc_files;   // file of every descriptor in `descs` (host only)
+  // shared-prefix (cascade) plan (pred_cascade)
+  std::vector<PrefixDesc> prefix_descs;
+  std::vector<ChunkUnit> prefix_units;
+  std::vector<PrefixRow> prefix_rows;
+  int32_t prefix_partials = 0;  // partials the prefix kernel writes (PART floats each)
+  int32_t prefix_groups = 0;
 };
 
 class Device;  // data plane (csrc/cuda), absent for a host-only ctx
 
 struct CtxCounters {
-  int64_t launches = 0, h2d_bytes = 0, page_copies = 0, last_decode_ctas = 0, last_chunk_units = 0;
+  int64_t launches = 0, h2d_bytes = 0, page_copies = 0, last_decode_ctas = 0, last_chunk_units = 0,
+          last_prefix_units = 0, last_prefix_groups = 0;
 };
 
 struct Ctx {
@@ -125,6 +151,7 @@ struct Ctx {
   int64_t batch_counter = 0;
   int64_t opt_decode_ctas = 0;
   int64_t opt_chunk_cutover = 8;
+  int64_t opt_cascade_min_entries = 16;
   CtxCounters ctr;
   PredPlan plan;  // the open step's plan
   std::vector<int> step_status;
@@ -159,6 +186,10 @@ int unpack_files(Ctx &c, const void *hdr, size_t hdr_bytes, const char *const *n
 int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos, int *status, PredPlan *plan);
 // Move descriptors with n_q >= cutover (0: none) from the K1 list to the K2 list (D = 128 only).
 void pred_split(const Ctx &c, int64_t cutover, PredPlan *plan);
+// Shared-prefix plan for the K1 list (KVFS_OPT_CASCADE_MIN_ENTRIES): groups descriptors whose files start
+// with the same run of (page, mask) entries, sets their skip / pref_* fields and emits the prefix work.
+// `sms` sizes the key splits, `max_partials` is the workspace capacity in partials.
+void pred_cascade(const Ctx &c, int64_t min_entries, int sms, int64_t max_partials, PredPlan *plan);
 
 // ---- data plane interface (implemented in csrc/cuda/device.cu)
 class Device {
@@ -176,6 +207,8 @@ class Device {
   virtual int pack_pages(const std::vector<uint32_t> &pages, void *buf, kvfs_stream_t s) = 0;
   virtual int unpack_pages(const std::vector<uint32_t> &pages, const void *buf, kvfs_stream_t s) = 0;
   virtual int sync() = 0;
+  virtual int sms() const = 0;
+  virtual int64_t prefix_partial_capacity() const = 0;
 };
 
 size_t device_workspace_bytes(const kvfs_config &cfg);

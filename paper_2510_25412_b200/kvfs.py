@@ -22,8 +22,9 @@ OK, ENOENT, EIO, EBADF, ENOMEM, EBUSY, EEXIST, EINVAL, ENOSPC, ERANGE, ENOSYS = 
 EPOS, EPARTIAL = -1001, -1002
 O_CREAT, O_EXCL = 1, 2
 EVICT_COMPACT = 1
-OPT_DECODE_CTAS, OPT_CHUNK_CUTOVER, OPT_DETERMINISTIC = 1, 2, 3
+OPT_DECODE_CTAS, OPT_CHUNK_CUTOVER, OPT_DETERMINISTIC, OPT_CASCADE_MIN_ENTRIES = 1, 2, 3, 4
 CTR_KERNEL_LAUNCHES, CTR_H2D_BYTES, CTR_PAGE_COPIES, CTR_LAST_DECODE_CTAS, CTR_LAST_CHUNK_UNITS = 1, 2, 3, 4, 5
+CTR_LAST_PREFIX_UNITS, CTR_LAST_PREFIX_GROUPS = 6, 7
 
 # every symbol include/kvfs.h declares (tests check the library exports all of them)
 EXPORTS = [

@@ -1,0 +1,105 @@
+"""Shared-prefix ("cascade") decode for CoW fork families (§4.2: fork
+shares pages without duplicating tensors, `fig:example` P:177 forks a generation into branches).
+
+The leading run of (page, mask) entries a fork family shares is attended once per batch by the tcgen05
+kernel in prefix mode and merged (log-sum-exp) into each member's decode result.  The results must equal
+the oracle's dense attention over every file's retained tokens (rule R10), exactly as without the cascade;
+the counters prove the cascade path actually ran."""
+import random
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from gpu_harness import Harness  # noqa: E402
+
+from paper_2510_25412_b200 import kvfs as K  # noqa: E402
+
+
+def _family(h, root, n_root, kids, tail_lens, evict_root=None):
+    h.open(root)
+    h.append(root, list(range(n_root)))
+    if evict_root:
+        h.evict(root, evict_root)
+    for i, (kid, n) in enumerate(zip(kids, tail_lens)):
+        h.fork(root, kid)
+        last = h.o.stat(h.fds[kid][1])[2]
+        if n:
+            h.append(kid, list(range(last + 1, last + 1 + n)))
+
+
+def _decode_rows(h, names, nq=None):
+    rows = []
+    for i, name in enumerate(names):
+        n = 1 if nq is None else nq[i]
+        last = h.o.stat(h.fds[name][1])[2]
+        rows.append((name, list(range(last + 1, last + 1 + n))))
+    return rows
+
+
+@pytest.mark.parametrize("P,Hq,Hkv", [(16, 32, 8), (32, 16, 8), (64, 16, 2), (16, 8, 8)])
+def test_cascade_fork_family_decode(P, Hq, Hkv):
+    h = Harness(4000, P, Hq, Hkv, 128, seed=P * 7 + Hq)
+    h.c.set_option(K.OPT_CASCADE_MIN_ENTRIES, 4)
+    kids = [f"k{i}" for i in range(9)]
+    # root of 1500 tokens with holes (evicted before the fork: the shared masks carry them), 9 branches
+    _family(h, "root", 1500, kids, [0, 5, 40, 300, 1, 17, 160, 64, 2], evict_root=[(3, 9), (700, 760)])
+    h.evict("k3", [(1600, 1650)])            # a hole in a private suffix
+    h.open("solo")
+    h.append("solo", list(range(333)))
+    for step in range(3):
+        names = kids + ["root", "solo"]
+        nq = [1] * len(names)
+        if step == 1:
+            nq[2], nq[5] = 3, 7              # short speculative drafts stay on the decode path
+        st, *_ = h.pred(_decode_rows(h, names, nq), qstd=4.0 if step == 2 else 1.0)
+        assert st == [0] * len(names)
+        assert h.c.counter(K.CTR_LAST_PREFIX_GROUPS) == 1
+        assert h.c.counter(K.CTR_LAST_PREFIX_UNITS) > 0
+    h.check_meta()
+    h.check_data()
+
+
+def test_cascade_equals_no_cascade_and_two_families():
+    """Two families + a member truncated back into the shared run (the family's common run shrinks to it);
+    the same batch with the cascade disabled gives the same attention (both within tolerance of the oracle,
+    and within 2 bf16 ulps-ish of each other)."""
+    h = Harness(3000, 16, 32, 8, 128, seed=11)
+    h.c.set_option(K.OPT_CASCADE_MIN_ENTRIES, 2)
+    _family(h, "A", 900, ["a0", "a1", "a2", "a3"], [10, 0, 33, 120])
+    _family(h, "B", 2048, ["b0", "b1"], [16, 1])
+    h.truncate("a2", 500)                   # shares only 500 tokens (31 full entries) with the others
+    names = ["a0", "a1", "a2", "a3", "b0", "b1", "A"]
+    st, ob_on, *_ = h.pred(_decode_rows(h, names))
+    assert st == [0] * len(names)
+    assert h.c.counter(K.CTR_LAST_PREFIX_GROUPS) == 2
+    # same step once more with the cascade off: compare with the oracle again (independent path)
+    h.c.set_option(K.OPT_CASCADE_MIN_ENTRIES, 0)
+    st, *_ = h.pred(_decode_rows(h, names))
+    assert st == [0] * len(names)
+    assert h.c.counter(K.CTR_LAST_PREFIX_UNITS) == 0
+    h.check_meta()
+
+
+def test_cascade_random_families():
+    """Random families, random tails, random evictions in branches, several steps; every result vs oracle."""
+    rnd = random.Random(2510)
+    h = Harness(6000, 16, 32, 8, 128, seed=5)
+    h.c.set_option(K.OPT_CASCADE_MIN_ENTRIES, 3)
+    names = []
+    for f in range(3):
+        kids = [f"f{f}k{i}" for i in range(rnd.randint(2, 12))]
+        _family(h, f"f{f}", rnd.randint(100, 1200), kids, [rnd.randint(0, 200) for _ in kids])
+        names += kids
+    for step in range(4):
+        for n in rnd.sample(names, 3):
+            ln = h.o.stat(h.fds[n][1])[0]
+            if ln > 40:
+                a = rnd.randint(ln // 2, ln - 20)
+                h.evict(n, [(a, a + 5)])
+        batch = rnd.sample(names, max(2, len(names) - 2))
+        st, *_ = h.pred(_decode_rows(h, batch))
+        assert st == [0] * len(batch)
+    h.check_meta()
+    h.check_data()
