@@ -114,6 +114,33 @@ __device__ __forceinline__ Segment make_segment(const Desc *descs, int n_desc, i
   return s;
 }
 
+// Shared-prefix partials of one (unit, head): (m, l) and the dims (dim, dim + 1) of every key split, all
+// loads in flight at once (S <= kMaxPrefixSplits); absent splits read as m = -inf (weight 0).
+__device__ __forceinline__ void load_prefix(const float *pref, int S, int part, int hoff, int D, int dim,
+                                            float2 (&pml)[kMaxPrefixSplits], float2 (&po)[kMaxPrefixSplits]) {
+#pragma unroll
+  for (int s = 0; s < kMaxPrefixSplits; ++s) {
+    pml[s] = make_float2(-CUDART_INF_F, 0.f);
+    po[s] = make_float2(0.f, 0.f);
+    if (s < S) {
+      const float *pc = pref + s * part + hoff;
+      pml[s] = __ldcg(reinterpret_cast<const float2 *>(pc + D));
+      po[s] = __ldcg(reinterpret_cast<const float2 *>(pc + dim));
+    }
+  }
+}
+
+__device__ __forceinline__ void fold_prefix(const float2 (&pml)[kMaxPrefixSplits], const float2 (&po)[kMaxPrefixSplits],
+                                            float M, float &L, float &ox, float &oy) {
+#pragma unroll
+  for (int s = 0; s < kMaxPrefixSplits; ++s) {
+    const float f = (pml[s].x == -CUDART_INF_F) ? 0.f : fast_exp2(pml[s].x - M);
+    L += pml[s].y * f;
+    ox += po[s].x * f;
+    oy += po[s].y * f;
+  }
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const DecodeParams p) {
   constexpr int D = C::D, G = C::G, P = C::P, NW = C::NW, NSTAGES = C::NSTAGES;
@@ -454,7 +481,10 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
         float M = -CUDART_INF_F;
 #pragma unroll
         for (int w = 0; w < NW; ++w) M = fmaxf(M, comb[w * C::PART + h * (D + 2) + D]);
-        for (int s = 0; s < dd.pref_splits; ++s) M = fmaxf(M, __ldcg(pref + s * C::PART + h * (D + 2) + D));
+        float2 pml[kMaxPrefixSplits], po[kMaxPrefixSplits];
+        load_prefix(pref, dd.pref_splits, C::PART, h * (D + 2), D, dim, pml, po);
+#pragma unroll
+        for (int s = 0; s < kMaxPrefixSplits; ++s) M = fmaxf(M, pml[s].x);
         float L = 0.f, ox = 0.f, oy = 0.f;
 #pragma unroll
         for (int w = 0; w < NW; ++w) {
@@ -464,15 +494,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
           ox += cwp[dim] * f;
           oy += cwp[dim + 1] * f;
         }
-        for (int s = 0; s < dd.pref_splits; ++s) {
-          const float *pc = pref + s * C::PART + h * (D + 2);
-          const float2 ml = __ldcg(reinterpret_cast<const float2 *>(pc + D));
-          const float2 o = __ldcg(reinterpret_cast<const float2 *>(pc + dim));
-          const float f = (ml.x == -CUDART_INF_F) ? 0.f : fast_exp2(ml.x - M);
-          L += ml.y * f;
-          ox += o.x * f;
-          oy += o.y * f;
-        }
+        fold_prefix(pml, po, M, L, ox, oy);
         const float inv = 1.f / L;
         const int64_t oidx = (row * p.Hq + sg.g * G + h) * D + dim;
         *reinterpret_cast<__nv_bfloat162 *>(p.out + oidx) = __floats2bfloat162_rn(ox * inv, oy * inv);
@@ -523,17 +545,12 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
             const float *pc = p.partials + (static_cast<int64_t>(c) * 2 + wh) * C::PART + h * (D + 2);
             M = fmaxf(M, __ldcg(pc + D));
           }
-          for (int s = 0; s < dd.pref_splits; ++s) M = fmaxf(M, __ldcg(pref + s * C::PART + h * (D + 2) + D));
+          float2 pml[kMaxPrefixSplits], po[kMaxPrefixSplits];
+          load_prefix(pref, dd.pref_splits, C::PART, h * (D + 2), D, dim, pml, po);
+#pragma unroll
+          for (int s = 0; s < kMaxPrefixSplits; ++s) M = fmaxf(M, pml[s].x);
           float L = 0.f, ox = 0.f, oy = 0.f;
-          for (int s = 0; s < dd.pref_splits; ++s) {
-            const float *pc = pref + s * C::PART + h * (D + 2);
-            const float2 ml = __ldcg(reinterpret_cast<const float2 *>(pc + D));
-            const float2 o = __ldcg(reinterpret_cast<const float2 *>(pc + dim));
-            const float f = (ml.x == -CUDART_INF_F) ? 0.f : fast_exp2(ml.x - M);
-            L += ml.y * f;
-            ox += o.x * f;
-            oy += o.y * f;
-          }
+          fold_prefix(pml, po, M, L, ox, oy);
           for (int c = c0; c <= c1; ++c) {
             const int wh = (cta_start(c, p.total, p.ncta) >= ua) ? 0 : 1;
             const float *pc = p.partials + (static_cast<int64_t>(c) * 2 + wh) * C::PART + h * (D + 2);

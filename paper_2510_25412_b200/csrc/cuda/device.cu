@@ -44,9 +44,9 @@ WsLayout ws_layout(const kvfs_config &c) {
   off = align256(off + static_cast<size_t>(kMaxCtas) * 2 * part);
   w.ptrs = off;
   off = align256(off + static_cast<size_t>(c.n_layers) * 2 * sizeof(void *));
-  // shared-prefix (cascade) partials: up to 16 key splits per decode unit, capped at 16384 partials
+  // shared-prefix (cascade) partials: up to kMaxPrefixSplits key splits per decode unit, capped at 16384
   w.prefix_cap = c.head_dim == 128
-                     ? std::min<int64_t>(static_cast<int64_t>(c.max_batch_rows) * c.n_kv_heads * 16, 16384)
+                     ? std::min<int64_t>(static_cast<int64_t>(c.max_batch_rows) * c.n_kv_heads * kMaxPrefixSplits, 16384)
                      : 0;
   w.prefix = off;
   off = align256(off + static_cast<size_t>(w.prefix_cap) * part);

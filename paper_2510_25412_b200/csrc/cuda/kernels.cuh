@@ -7,6 +7,8 @@
 namespace kvfs {
 namespace dev {
 
+constexpr int kMaxPrefixSplits = 8;  // == kvfs::kMaxPrefixSplits (key splits of a shared prefix)
+
 struct DecodeParams {
   const Desc *descs;
   int n_desc;

@@ -234,13 +234,13 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int sms, int64_t max_partia
     use.push_back({static_cast<int>(k), E, rows, (E + epb - 1) / epb, (mt + 1) / 2, 1});
   }
   if (use.empty()) return;
-  // key splits: about one CTA per SM over all families, at most 16 and at most one tile each
+  // key splits: about one CTA per SM over all families, at most kMaxPrefixSplits and at most one per tile
   int64_t units_per_split = 0, rows_all = 0;
   for (const Fam &u : use) {
     units_per_split += static_cast<int64_t>(Hkv) * u.mpairs;
     rows_all += u.rows;
   }
-  int S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(16, sms / std::max<int64_t>(1, units_per_split))));
+  int S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kMaxPrefixSplits, sms / std::max<int64_t>(1, units_per_split))));
   while (S > 1 && rows_all * Hkv * S > max_partials) --S;
   if (rows_all * Hkv * S > max_partials) return;  // workspace too small: no cascade
   for (Fam &u : use) {

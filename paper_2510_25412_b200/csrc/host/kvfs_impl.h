@@ -91,6 +91,7 @@ struct ChunkDesc {
 struct ChunkUnit {
   int32_t desc, g, m, pad;
 };
+constexpr int kMaxPrefixSplits = 8;  // key splits of one shared prefix (the decode merge unrolls over them)
 // Shared-prefix (cascade) work: one record per (fork family, key split); the family's query rows are
 // listed in PrefixRow order (row0 .. row0 + n_rows - 1).
 struct PrefixDesc {
