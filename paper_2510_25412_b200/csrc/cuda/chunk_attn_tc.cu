@@ -237,6 +237,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   const int m0 = 2 * u.m;                                     // first M-tile of this CTA
   const int n_mt = min(2, (rows_total + BM - 1) / BM - m0);  // 1 or 2 M-tiles
 
+  if (threadIdx.x == 0) K2T(24, 0);
   if (threadIdx.x == 0) {
     mbar_init(bar(B_Q), PREFIX ? 4 * n_mt : 1);  // prefix: one arrival per softmax warp that gathers Q
     for (int s = 0; s < KV2; ++s) {
@@ -371,6 +372,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       // ============================================================ MMA issuer
       constexpr uint32_t ID_S = idesc_bf16(false), ID_O = idesc_bf16(true);
       mbar_wait(bar(B_Q), 0);
+      if (lane == 0) K2T(25, 0);
       auto issue_s = [&](int t, int m) {
         tc_fence_after();
         if (elect_one()) {
@@ -542,8 +544,13 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       }
       // epilogue: O / l -> bf16 out, lse   (prefix mode: the partial O, m, l of the split)
       mbar_wait(bar(B_OF + m), (n_tiles - 1) & 1);
+      if (m == 0 && wq == 0 && lane == 0) K2T(26, 0);
       tc_fence_after();
       if constexpr (PREFIX) {
+        // Coalesced partial stores: each 32-column chunk of the warp's 32 rows is transposed through a
+        // per-warp 32 x 33 float buffer in this M-tile's (consumed) Q tile, then 16 lanes write one row's
+        // 128 contiguous bytes: 2 rows per store instead of 32 scattered 8-byte pieces.
+        float *buf = reinterpret_cast<float *>(smem + OFF_Q2 + m * TILE_BYTES) + wq * (32 * 33);
         float *dst = nullptr;
         if (live) {
           const PrefixRow pr = p.prows[cd.row0 + qi];
@@ -551,16 +558,21 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           const int64_t idx = pr.pref_base + static_cast<int64_t>(u.g * pr.n_q + pr.qi) * pd.n_splits + pd.split;
           dst = p.ppart + idx * (G * (HD + 2)) + h * (HD + 2);
         }
-#pragma unroll
+#pragma unroll 1
         for (int c = 0; c < HD / 32; ++c) {
           float v[32];
           tmem_ld32(o_col + c * 32, v);
           tmem_wait_ld();
-          if (live) {
 #pragma unroll
-            for (int i = 0; i < 32; i += 2)
-              *reinterpret_cast<float2 *>(dst + c * 32 + i) = make_float2(v[i], v[i + 1]);
+          for (int i = 0; i < 32; ++i) buf[lane * 33 + i] = v[i];
+          __syncwarp();
+#pragma unroll
+          for (int it = 0; it < 16; ++it) {  // (D + 2)-float rows are 8-byte aligned: float2, 2 rows per store
+            const int rr = it * 2 + (lane >> 4), j = (lane & 15) * 2;
+            float *d = reinterpret_cast<float *>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dst), rr));
+            if (d) *reinterpret_cast<float2 *>(d + c * 32 + j) = make_float2(buf[rr * 33 + j], buf[rr * 33 + j + 1]);
           }
+          __syncwarp();
         }
         if (live) *reinterpret_cast<float2 *>(dst + HD) = make_float2(m_run, l_run);
       } else {
@@ -592,6 +604,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) K2T(27, 0);
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));

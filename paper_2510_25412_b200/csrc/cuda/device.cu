@@ -358,6 +358,14 @@ class CudaDevice final : public Device {
     p.total = pl.total_cost;
     if (per_sm_ == 0) per_sm_ = dev::decode_ctas_per_sm(cfg.head_dim, cfg.n_q_heads / cfg.n_kv_heads, cfg.page_size);
     int64_t ncta = c_.opt_decode_ctas > 0 ? c_.opt_decode_ctas : static_cast<int64_t>(sms_) * per_sm_;
+    if (c_.opt_decode_ctas <= 0 && pl.n_units > 0 && pl.n_units <= ncta) {
+      // Few units (e.g. the short private suffixes of a fork family after the shared prefix went to the
+      // cascade): one ring per unit when the units are about equally long, so no unit is cut by a range
+      // boundary and none pays the cross-ring partial merge.
+      int32_t spu_max = 0;
+      for (const DevDesc &d : pl.descs) spu_max = std::max(spu_max, d.stages_per_unit);
+      if (4 * static_cast<int64_t>(spu_max) * pl.n_units <= 5 * pl.total_cost) ncta = pl.n_units;
+    }
     ncta = std::min<int64_t>(std::min<int64_t>(ncta, kMaxCtas), pl.total_cost);
     p.ncta = static_cast<int>(ncta);
     p.slab = slab_;

@@ -138,5 +138,9 @@ class DecodeWorkload:
         return int(sum(4 * s.Hq * s.D * (n * int(ln) + n * (n + 1) // 2) for ln in self.lens))
 
     def dominant_kernel(self) -> str:
-        return ("chunk_attn_tc_kernel (K2, tcgen05 QK^T / PV with TMEM accumulators)" if self.n_q >= 8
-                else "decode_attn_kernel (K1, fused append + split-KV attention)")
+        if self.n_q >= 8:
+            return "chunk_attn_tc_kernel (K2, tcgen05 QK^T / PV with TMEM accumulators)"
+        if self.prefix_len:
+            return ("chunk_attn_tc_kernel<G, prefix> (shared prefix once per batch, tcgen05) + decode_attn_kernel "
+                    "(K1, private suffixes + log-sum-exp merge); time = both launches of the step")
+        return "decode_attn_kernel (K1, fused append + split-KV attention)"

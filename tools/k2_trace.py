@@ -39,6 +39,10 @@ def main():
     fn = kvfs.lib().kvfs_debug_k2_trace
     fn.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
     assert fn(buf.ctypes.data, buf.nbytes) == 0
+    t0 = buf[0, 24, 0].astype(np.int64)
+    if t0:
+        print("CTA 0 one-off events (clk from kernel start): Q ready %d, first S ready %d, last O %d, end %d"
+              % tuple(int(buf[0, e, 0]) - t0 if buf[0, e, 0] else -1 for e in (25, 14, 26, 27)))
     for c in range(2):
         tr = buf[c].astype(np.int64)
         n = int((tr[14] > 0).sum())
