@@ -225,6 +225,26 @@ int kvfs_pack(kvfs_ctx *ctx, const int *fds, int n_fds, void *buf_dev, size_t bu
 int kvfs_unpack(kvfs_ctx *ctx, const void *buf_dev, const void *hdr, size_t hdr_bytes, const char *const *names,
                 int *fds_out, kvfs_stream_t stream);
 
+/* ---------------------------------------------------------------- new files from existing ones
+ * PAPER.md §4.2: LIPs "create new files from existing ones by extracting specific token indices with
+ * extract, or merging existing files into one with merge".  Both build a NEW file whose
+ * pages are rebuilt (no sharing: a selection or an interleaving breaks page alignment): k tokens go to
+ * ceil(k/P) fresh pages allocated smallest-free first in the new file's logical order (rule R1), token i
+ * at (page i / P, slot i % P), every retained token keeping its original absolute position.  The K/V bits
+ * of every layer are gathered on `stream` (device; a host-only ctx builds the metadata only).  The sources
+ * are unchanged.  Atomic: a failing call changes nothing.
+ *
+ * kvfs_extract: indices[n] = LOGICAL token indices of src, strictly increasing (EINVAL otherwise), each in
+ *   [0, len) (ERANGE); n = 0 gives an empty file.  Errors: EBADF, EINVAL, ERANGE, EEXIST (name exists),
+ *   ENOSPC (not enough free pages), in that order of checking.
+ * kvfs_merge: the union of the parts' retained tokens sorted by position; two tokens with the same
+ *   position (in one or in different parts) are EPOS (overlap semantics are undefined in the
+ *   paper, so they are rejected); a part listed twice is EBUSY.  Errors: EBADF, EBUSY, EPOS, EEXIST, ENOSPC.
+ * *fd receives the new file's fd (open, like kvfs_open). */
+int kvfs_extract(kvfs_ctx *ctx, int src_fd, const int64_t *indices, int64_t n, const char *name, int *fd,
+                 kvfs_stream_t stream);
+int kvfs_merge(kvfs_ctx *ctx, const int *fds, int n_fds, const char *name, int *fd, kvfs_stream_t stream);
+
 /* ---------------------------------------------------------------- knobs and counters */
 typedef enum {
   KVFS_OPT_DECODE_CTAS = 1,     /* grid size of the decode kernel; 0 = auto (SM count x occupancy) */

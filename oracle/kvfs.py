@@ -21,6 +21,13 @@ Rules (readings of a silent paper; numbers as in SURVEY.md
   R9 unlink/close   unlink releases every entry and the name; close releases the fd
   R11 batch      descriptors in order; per descriptor EBADF / EBUSY (file repeated) / EPOS / ENOSPC,
                  isolated failures, EPARTIAL overall
+  R13 extract    P:225 "create new files from existing ones by extracting specific token indices": a new
+                 file holding the selected logical tokens (strictly increasing indices, EINVAL; < len,
+                 ERANGE) in order with their original positions, in ceil(k/P) fresh pages allocated by R1
+                 in logical order (pages rebuilt, no sharing); the source is unchanged
+  R14 merge      P:225 "merging existing files into one": a new file holding every part's retained tokens
+                 sorted by position (duplicate positions: EPOS, SPEC S:100-106), pages rebuilt as in R13;
+                 a part listed twice is EBUSY; the parts are unchanged
 Pinned by tests/test_oracle_kvfs.py: SPEC worked examples S:62, S:70, S:78, S:79, S:87, S:88, S:89,
 S:608; the golden trace tests/golden/c7_trace.json; a deep-copy shadow model on
 random op sequences; invariants I1-I5 after every op.
@@ -412,6 +419,53 @@ class Oracle:
         f.table.append([new_pages[-1], (1 << (length - (k - 1) * self.P)) - 1])
         for page, _ in old:
             self._release(page)
+
+    # ------------------------------------------------------------------ R13 extract, R14 merge
+    def _build(self, name: str, src: List[Tuple[int, int]], pos: List[int]) -> int:
+        """New file `name` whose token i is a copy of pool slot src[i] = (page, slot), position pos[i]:
+        ceil(k/P) fresh pages allocated one at a time (R1), token i -> (new[i // P], i % P)."""
+        if name in self.names:
+            raise KvfsError(EEXIST, name)
+        k = len(src)
+        n_new = -(-k // self.P)
+        if n_new > self.free_count():
+            raise KvfsError(ENOSPC, "extract/merge")
+        new_pages = [self._alloc() for _ in range(n_new)]
+        if self.store:
+            for i, (page, slot) in enumerate(src):
+                dp, ds = new_pages[i // self.P], i % self.P
+                self.K[:, dp, :, ds, :] = self.K[:, page, :, slot, :]
+                self.V[:, dp, :, ds, :] = self.V[:, page, :, slot, :]
+        f = _File(name)
+        full = (1 << self.P) - 1
+        for j, p in enumerate(new_pages):
+            cnt = min(self.P, k - j * self.P)
+            f.table.append([p, full if cnt == self.P else (1 << cnt) - 1])
+        f.pos = list(pos)
+        self.names[name] = f
+        return self._new_fd(f)
+
+    def extract(self, src_fd: int, indices: Sequence[int], name: str) -> int:
+        f = self._file(src_fd)
+        idx = list(indices)
+        if any(b <= a for a, b in zip(idx, idx[1:])):
+            raise KvfsError(EINVAL, "indices not strictly increasing")
+        if idx and (idx[0] < 0 or idx[-1] >= f.length()):
+            raise KvfsError(ERANGE, "index out of range")
+        lg = f.logical()
+        return self._build(name, [lg[i] for i in idx], [f.pos[i] for i in idx])
+
+    def merge(self, fds: Sequence[int], name: str) -> int:
+        files = [self._file(fd) for fd in fds]
+        if len(set(map(id, files))) != len(files):
+            raise KvfsError(EBUSY, "a part appears twice")
+        toks = []
+        for f in files:
+            toks.extend(zip(f.pos, f.logical()))
+        toks.sort(key=lambda t: t[0])
+        if any(a[0] == b[0] for a, b in zip(toks, toks[1:])):
+            raise KvfsError(EPOS, "duplicate position across parts")
+        return self._build(name, [t[1] for t in toks], [t[0] for t in toks])
 
     # ------------------------------------------------------------------ R11 batched pred (+ R10)
     def pred_reserve(self, descs: Sequence[Tuple[int, int]], pos: Sequence[int]):

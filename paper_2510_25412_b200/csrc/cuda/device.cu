@@ -101,6 +101,30 @@ __global__ void append_rows_kernel(const int32_t *dst, int64_t n, int64_t row_ba
   }
 }
 
+// extract / merge (R13, R14): token i of the new file <- pool slot src[i] (page * P + slot), into
+// (new_pages[i / P], i % P), every layer, K and V.  One CTA per (destination page, layer), 16-byte vectors.
+__global__ void __launch_bounds__(256) gather_kernel(const int32_t *src, int64_t n, const uint32_t *new_pages,
+                                                     bf16 *const *kp, bf16 *const *vp, int Hkv, int D, int P) {
+  const int j = blockIdx.x, l = blockIdx.y;
+  const int64_t i0 = static_cast<int64_t>(j) * P;
+  const int ntok = static_cast<int>(n - i0 < P ? n - i0 : static_cast<int64_t>(P));
+  bf16 *kk = kp[l];
+  bf16 *vv = vp[l];
+  const int cpr = D / 8;
+  const int total = Hkv * ntok * cpr;
+  const int64_t dpage = new_pages[j];
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    const int c = idx % cpr, r = idx / cpr, t = r % ntok, g = r / ntok;
+    const int32_t sl = src[i0 + t];
+    const int64_t so = ((static_cast<int64_t>(sl / P) * Hkv + g) * P + sl % P) * D + c * 8;
+    const int64_t po = ((dpage * Hkv + g) * P + t) * D + c * 8;
+    const uint4 a = *reinterpret_cast<const uint4 *>(kk + so);
+    const uint4 b = *reinterpret_cast<const uint4 *>(vv + so);
+    *reinterpret_cast<uint4 *>(kk + po) = a;
+    *reinterpret_cast<uint4 *>(vv + po) = b;
+  }
+}
+
 __device__ __forceinline__ int find_entry(const dev::Entry *t, int n, int64_t i) {
   int lo = 0, hi = n - 1;
   while (lo < hi) {
@@ -293,6 +317,22 @@ class CudaDevice final : public Device {
     compact_kernel<<<grid, 256, 0, cs(s)>>>(static_cast<const dev::Entry *>(dt), static_cast<int>(old_table.size()),
                                             static_cast<const uint32_t *>(dp), len, kptrs_, vptrs_, cfg.n_layers,
                                             cfg.n_kv_heads, cfg.head_dim, cfg.page_size);
+    ++c_.ctr.launches;
+    return cudaGetLastError() == cudaSuccess ? KVFS_OK : KVFS_EIO;
+  }
+
+  int gather(const std::vector<int32_t> &src_slots, const std::vector<uint32_t> &new_pages,
+             kvfs_stream_t s) override {
+    begin_packet();
+    const void *ds = push(src_slots.data(), src_slots.size() * sizeof(int32_t));
+    const void *dp = push(new_pages.data(), new_pages.size() * sizeof(uint32_t));
+    if (!ds || !dp) return KVFS_ENOMEM;
+    if (!send(s)) return KVFS_EIO;
+    const kvfs_config &cfg = c_.cfg;
+    const dim3 grid(static_cast<unsigned>(new_pages.size()), static_cast<unsigned>(cfg.n_layers));
+    gather_kernel<<<grid, 256, 0, cs(s)>>>(static_cast<const int32_t *>(ds), static_cast<int64_t>(src_slots.size()),
+                                           static_cast<const uint32_t *>(dp), kptrs_, vptrs_, cfg.n_kv_heads,
+                                           cfg.head_dim, cfg.page_size);
     ++c_.ctr.launches;
     return cudaGetLastError() == cudaSuccess ? KVFS_OK : KVFS_EIO;
   }

@@ -195,6 +195,37 @@ int kvfs_compact(kvfs_ctx *ctx, int fd, kvfs_stream_t stream) {
   return rc;
 }
 
+int kvfs_extract(kvfs_ctx *ctx, int src_fd, const int64_t *indices, int64_t n, const char *name, int *fd,
+                 kvfs_stream_t stream) {
+  KVFS_LOCK_OR(ctx);
+  if (c.dev && c.poisoned) return KVFS_EIO;
+  File *f = get_file(c, src_fd);
+  if (!f) return KVFS_EBADF;
+  std::vector<int32_t> src;
+  std::vector<uint32_t> pages;
+  int rc = extract_file(c, *f, indices, n, name, fd, &src, &pages);
+  if (rc != KVFS_OK) return rc;
+  if (c.dev && !src.empty()) {
+    rc = c.dev->gather(src, pages, stream);
+    if (rc != KVFS_OK) c.poisoned = true;
+  }
+  return rc;
+}
+
+int kvfs_merge(kvfs_ctx *ctx, const int *fds, int n_fds, const char *name, int *fd, kvfs_stream_t stream) {
+  KVFS_LOCK_OR(ctx);
+  if (c.dev && c.poisoned) return KVFS_EIO;
+  std::vector<int32_t> src;
+  std::vector<uint32_t> pages;
+  int rc = merge_files(c, fds, n_fds, name, fd, &src, &pages);
+  if (rc != KVFS_OK) return rc;
+  if (c.dev && !src.empty()) {
+    rc = c.dev->gather(src, pages, stream);
+    if (rc != KVFS_OK) c.poisoned = true;
+  }
+  return rc;
+}
+
 int kvfs_append(kvfs_ctx *ctx, int fd, int64_t n, const int32_t *pos, const void *k, const void *v,
                 kvfs_stream_t stream) {
   KVFS_LOCK_OR(ctx);

@@ -12,6 +12,11 @@ namespace {
 
 inline int popc(uint64_t m) { return __builtin_popcountll(m); }
 inline int hi_slot(uint64_t m) { return 63 - __builtin_clzll(m); }  // m != 0
+// Slot of the r-th (0-based) set bit of m (precondition: popc(m) > r).
+inline int select_bit(uint64_t m, int r) {
+  for (; r > 0; --r) m &= m - 1;
+  return __builtin_ctzll(m);
+}
 
 // Mask keeping only the set bits of m whose rank (0-based, ascending slots) is in [r0, r1).
 uint64_t rank_range_bits(uint64_t m, int r0, int r1) {
@@ -361,6 +366,89 @@ int evict_file(Ctx &c, File &f, const int64_t *ranges, int n_ranges, int flags, 
   }
   if (compact) compact_commit(c, f, old_table, new_pages);
   return KVFS_OK;
+}
+
+// R13 / R14 common tail: a new file `name` whose token i copies pool slot src[i] (page * P + slot), at
+// position pos[i]; ceil(k/P) fresh pages allocated one at a time (R1), token i -> (new[i/P], i % P).
+static int build_file(Ctx &c, const char *name, const std::vector<int32_t> &src, const std::vector<int32_t> &pos,
+                      int *fd, std::vector<uint32_t> *new_pages) {
+  const int P = c.cfg.page_size;
+  if (!name || !*name || !fd) return KVFS_EINVAL;
+  if (c.names.count(name)) return KVFS_EEXIST;
+  const int64_t k = static_cast<int64_t>(src.size());
+  const int64_t np = (k + P - 1) / P;
+  if (np > c.pool->n_free()) return KVFS_ENOSPC;
+  auto f = std::make_shared<File>();
+  f->name = name;
+  const uint64_t full = P == 64 ? ~0ull : ((1ull << P) - 1);
+  new_pages->resize(static_cast<size_t>(np));
+  f->table.resize(static_cast<size_t>(np));
+  f->spos.assign(static_cast<size_t>(np) * P, 0);
+  for (int64_t j = 0; j < np; ++j) {
+    (*new_pages)[j] = c.pool->alloc();
+    const int64_t cnt = std::min<int64_t>(P, k - j * P);
+    f->table[j] = {(*new_pages)[j], static_cast<int32_t>(j * P), cnt == P ? full : ((1ull << cnt) - 1)};
+  }
+  std::copy(pos.begin(), pos.end(), f->spos.begin());
+  f->len = k;
+  c.names.emplace(f->name, f);
+  *fd = static_cast<int>(new_fd(c, f));
+  return KVFS_OK;
+}
+
+int extract_file(Ctx &c, File &src, const int64_t *idx, int64_t n, const char *name, int *fd,
+                 std::vector<int32_t> *src_slots, std::vector<uint32_t> *new_pages) {
+  const int P = c.cfg.page_size;
+  if (n < 0 || (n > 0 && !idx)) return KVFS_EINVAL;
+  for (int64_t i = 1; i < n; ++i)
+    if (idx[i] <= idx[i - 1]) return KVFS_EINVAL;
+  if (n > 0 && (idx[0] < 0 || idx[n - 1] >= src.len)) return KVFS_ERANGE;
+  std::vector<int32_t> pos(static_cast<size_t>(n));
+  src_slots->resize(static_cast<size_t>(n));
+  // walk the table once: logical index -> (entry, slot)
+  size_t e = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    while (src.table[e].lstart + popc(src.table[e].mask) <= idx[i]) ++e;
+    const int slot = select_bit(src.table[e].mask, static_cast<int>(idx[i] - src.table[e].lstart));
+    (*src_slots)[i] = static_cast<int32_t>(src.table[e].page) * P + slot;
+    pos[i] = src.spos[e * P + slot];
+  }
+  return build_file(c, name, *src_slots, pos, fd, new_pages);
+}
+
+int merge_files(Ctx &c, const int *fds, int n, const char *name, int *fd, std::vector<int32_t> *src_slots,
+                std::vector<uint32_t> *new_pages) {
+  const int P = c.cfg.page_size;
+  if (n < 0 || (n > 0 && !fds)) return KVFS_EINVAL;
+  std::vector<File *> parts;
+  for (int i = 0; i < n; ++i) {
+    File *f = get_file(c, fds[i]);
+    if (!f) return KVFS_EBADF;
+    parts.push_back(f);
+  }
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < i; ++j)
+      if (parts[i] == parts[j]) return KVFS_EBUSY;
+  std::vector<std::pair<int32_t, int32_t>> toks;  // (position, pool slot)
+  for (File *f : parts)
+    for (size_t e = 0; e < f->table.size(); ++e)
+      for (uint64_t m = f->table[e].mask; m; m &= m - 1) {
+        const int slot = __builtin_ctzll(m);
+        toks.emplace_back(f->spos[e * P + slot], static_cast<int32_t>(f->table[e].page) * P + slot);
+      }
+  std::stable_sort(toks.begin(), toks.end(),
+                   [](const std::pair<int32_t, int32_t> &a, const std::pair<int32_t, int32_t> &b) {
+                     return a.first < b.first;
+                   });
+  for (size_t i = 1; i < toks.size(); ++i)
+    if (toks[i].first == toks[i - 1].first) return KVFS_EPOS;
+  std::vector<int32_t> pos(toks.size());
+  src_slots->resize(toks.size());
+  for (size_t i = 0; i < toks.size(); ++i) {
+    pos[i] = toks[i].first;
+    (*src_slots)[i] = toks[i].second;
+  }
+  return build_file(c, name, *src_slots, pos, fd, new_pages);
 }
 
 int compact_file(Ctx &c, File &f, std::vector<Entry> *old_table, std::vector<uint32_t> *new_pages) {

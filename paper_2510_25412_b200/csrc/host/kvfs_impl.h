@@ -172,6 +172,12 @@ int truncate_file(Ctx &c, File &f, int64_t n);
 int evict_file(Ctx &c, File &f, const int64_t *ranges, int n_ranges, int flags, std::vector<Entry> *old_table,
                std::vector<uint32_t> *new_pages);
 int compact_file(Ctx &c, File &f, std::vector<Entry> *old_table, std::vector<uint32_t> *new_pages);
+// R13 / R14: new file from selected tokens / from the union of parts; src_slots[i] = page * P + slot of the
+// source of token i, new_pages = the file's pages (token i -> (new_pages[i / P], i % P)).  Atomic.
+int extract_file(Ctx &c, File &src, const int64_t *idx, int64_t n, const char *name, int *fd,
+                 std::vector<int32_t> *src_slots, std::vector<uint32_t> *new_pages);
+int merge_files(Ctx &c, const int *fds, int n, const char *name, int *fd, std::vector<int32_t> *src_slots,
+                std::vector<uint32_t> *new_pages);
 void recompute_lstart(File &f, size_t from);
 int32_t last_pos(const Ctx &c, const File &f);
 void file_positions(const Ctx &c, const File &f, std::vector<int32_t> *out);
@@ -200,6 +206,8 @@ class Device {
   virtual int append_rows(const std::vector<int32_t> &dst, const void *k, const void *v, kvfs_stream_t s) = 0;
   virtual int compact(const std::vector<Entry> &old_table, const std::vector<uint32_t> &new_pages, int64_t len,
                       kvfs_stream_t s) = 0;
+  virtual int gather(const std::vector<int32_t> &src_slots, const std::vector<uint32_t> &new_pages,
+                     kvfs_stream_t s) = 0;
   virtual int read(const std::vector<Entry> &table, int layer, int64_t begin, int64_t end, void *k_out,
                    void *v_out, kvfs_stream_t s) = 0;
   virtual int pred_begin(PredPlan &plan, kvfs_stream_t s) = 0;

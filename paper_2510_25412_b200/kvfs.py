@@ -32,7 +32,8 @@ EXPORTS = [
     "kvfs_unlink", "kvfs_fork", "kvfs_truncate", "kvfs_evict", "kvfs_compact", "kvfs_append",
     "pred_attn_batch", "pred_step_begin", "pred_attn_layer", "pred_step_end", "kvfs_stat",
     "kvfs_get_table", "kvfs_get_positions", "kvfs_get_refcounts", "kvfs_free_pages", "kvfs_read",
-    "kvfs_audit", "kvfs_set_option", "kvfs_get_counter", "kvfs_pack", "kvfs_unpack",
+    "kvfs_audit", "kvfs_set_option", "kvfs_get_counter", "kvfs_pack", "kvfs_unpack", "kvfs_extract",
+    "kvfs_merge",
 ]
 
 
@@ -81,6 +82,8 @@ def lib():
             "kvfs_truncate": (cint, [vp, cint, i64]),
             "kvfs_evict": (cint, [vp, cint, P(i64), cint, cint, vp]),
             "kvfs_compact": (cint, [vp, cint, vp]),
+            "kvfs_extract": (cint, [vp, cint, P(ctypes.c_int64), i64, ctypes.c_char_p, P(cint), vp]),
+            "kvfs_merge": (cint, [vp, P(cint), cint, ctypes.c_char_p, P(cint), vp]),
             "kvfs_append": (cint, [vp, cint, i64, P(i32), vp, vp, vp]),
             "pred_attn_batch": (cint, [vp, P(PredDesc), cint, P(i32), vp, vp, vp, vp, vp, ctypes.c_float,
                                        P(cint), vp]),
@@ -230,6 +233,24 @@ class KVFS:
     def compact(self, fd: int, stream=None) -> None:
         st = _stream(stream) if self.device >= 0 else None
         _check(lib().kvfs_compact(self._h, fd, st), "compact")
+
+    def extract(self, src_fd: int, indices, name: str, stream=None) -> int:
+        """New file `name` with the logical tokens `indices` of src (kvfs_extract)."""
+        idx = np.ascontiguousarray(np.asarray(list(indices), dtype=np.int64))
+        fd = ctypes.c_int()
+        st = _stream(stream) if self.device >= 0 else None
+        _check(lib().kvfs_extract(self._h, src_fd, _ptr(idx, ctypes.c_int64), idx.shape[0], name.encode(),
+                                  ctypes.byref(fd), st), f"extract {name}")
+        return fd.value
+
+    def merge(self, fds, name: str, stream=None) -> int:
+        """New file `name` with every part's tokens sorted by position (kvfs_merge)."""
+        arr = np.ascontiguousarray(np.asarray(list(fds), dtype=np.int32))
+        fd = ctypes.c_int()
+        st = _stream(stream) if self.device >= 0 else None
+        _check(lib().kvfs_merge(self._h, _ptr(arr, ctypes.c_int32), arr.shape[0], name.encode(),
+                                ctypes.byref(fd), st), f"merge {name}")
+        return fd.value
 
     def append(self, fd: int, pos, k=None, v=None, stream=None) -> None:
         """pos: host int sequence; k, v: device bf16 tensors [L][n][Hkv][D] (None on a host-only ctx)."""

@@ -123,7 +123,7 @@ def run_random(seed, n_ops=200):
     for step in range(n_ops):
         names = list(pr.fds)
         op = rnd.choice(["open", "append", "append", "fork", "truncate", "evict", "evictc", "compact", "unlink",
-                         "pred", "pred", "close_reopen", "bad"])
+                         "pred", "pred", "close_reopen", "bad", "extract", "merge"])
         if op == "open" or not names:
             name = f"n{step}"
             rc, ro, e = pr.both(lambda: c.open(name), lambda: o.open(name))
@@ -181,6 +181,28 @@ def run_random(seed, n_ops=200):
             name = rnd.choice(names)
             cfd, ofd = pr.fds[name]
             pr.both(lambda: c.compact(cfd), lambda: o.compact(ofd))
+        elif op == "extract":
+            src = rnd.choice(names)
+            cfd, ofd = pr.fds[src]
+            ln = o.stat(ofd)[0]
+            idx = sorted(rnd.sample(range(ln), rnd.randint(0, min(ln, 3 * P)))) if ln else []
+            if rnd.random() < 0.1 and len(idx) > 1:
+                idx = idx[::-1]  # EINVAL
+            elif rnd.random() < 0.05:
+                idx = idx + [ln]  # ERANGE
+            name = f"n{step}" if rnd.random() > 0.05 else src  # EEXIST
+            rc, ro, e = pr.both(lambda: c.extract(cfd, idx, name), lambda: o.extract(ofd, idx, name))
+            if e is None:
+                assert rc == ro
+                pr.fds[name] = (rc, ro)
+        elif op == "merge":
+            parts = [rnd.choice(names) for _ in range(rnd.randint(1, 3))]  # repeats -> EBUSY
+            name = f"n{step}"
+            rc, ro, e = pr.both(lambda: c.merge([pr.fds[p][0] for p in parts], name),
+                                lambda: o.merge([pr.fds[p][1] for p in parts], name))
+            if e is None:
+                assert rc == ro
+                pr.fds[name] = (rc, ro)
         elif op == "unlink":
             name = rnd.choice(names)
             cfd, ofd = pr.fds.pop(name)

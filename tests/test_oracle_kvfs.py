@@ -404,7 +404,7 @@ def test_shadow_model_random_ops(seed):
     for step in range(200):
         names = list(sh.files)
         op = rnd.choice(["open", "append", "append", "append", "fork", "truncate", "evict", "evictc",
-                         "compact", "unlink", "pred"])
+                         "compact", "unlink", "pred", "extract", "merge"])
         snap = (list(o.refcnt), {n: o.table(fds[n]) for n in names})
         err = None
         expect = None
@@ -454,6 +454,21 @@ def test_shadow_model_random_ops(seed):
             elif op == "compact":
                 name = rnd.choice(names)
                 o.compact(fds[name])
+            elif op == "extract":  # R13: the selected entries, positions kept
+                src = rnd.choice(names)
+                ln = sh.length(src)
+                idx = sorted(rnd.sample(range(ln), rnd.randint(0, min(ln, 40)))) if ln else []
+                name = f"n{step}"
+                fds[name] = o.extract(fds[src], idx, name)
+                sh.files[name] = [sh.files[src][i] for i in idx]
+            elif op == "merge":  # R14: union sorted by position; duplicates -> EPOS
+                parts = rnd.sample(names, min(len(names), rnd.randint(1, 3)))
+                toks = sorted((e for p in parts for e in sh.files[p]), key=lambda e: e[0])
+                dup = any(a[0] == b[0] for a, b in zip(toks, toks[1:]))
+                expect = EPOS if dup else None
+                name = f"n{step}"
+                fds[name] = o.merge([fds[p] for p in parts], name)
+                sh.files[name] = toks
             elif op == "unlink":
                 name = rnd.choice(names)
                 o.unlink(name)
