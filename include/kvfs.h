@@ -245,6 +245,34 @@ int kvfs_extract(kvfs_ctx *ctx, int src_fd, const int64_t *indices, int64_t n, c
                  kvfs_stream_t stream);
 int kvfs_merge(kvfs_ctx *ctx, const int *fds, int n_fds, const char *name, int *fd, kvfs_stream_t stream);
 
+/* ---------------------------------------------------------------- inference scheduler: batch formation
+ * PAPER.md §4.4: the inference scheduler "aggregates multiple pred system calls into a single
+ * batch"; executing too early under-uses the GPU, too late makes threads wait; Symphony "dynamically adjusts
+ * batch size according to the average frequency of system calls, leveraging models like Poisson process".
+ * Reading (S1): lam = EWMA of 1/dt over enqueue gaps (first enqueue: 1/dt_default;
+ * dt floored at 1e-9); target B* = clamp(round(lam * w_max), 1, b_max) = expected arrivals within w_max;
+ * a batch is due when >= B* requests wait or the oldest waited >= w_max; it is the waiting requests in FIFO
+ * order, at most b_max, a request whose fd is already in the batch staying queued (one pred per file per
+ * batch).  Times are caller-supplied seconds (any monotonic clock).  Host only; no device work. */
+typedef struct kvfs_sched kvfs_sched;
+typedef struct {
+  double w_max;      /* max wait of the oldest request (s), > 0 */
+  int b_max;         /* max batch size (descriptors), >= 1 */
+  double alpha;      /* EWMA weight in (0, 1] */
+  double dt_default; /* initial mean gap (s), > 0 */
+} kvfs_sched_config;
+int kvfs_sched_create(const kvfs_sched_config *cfg, kvfs_sched **out); /* EINVAL for a bad config */
+int kvfs_sched_destroy(kvfs_sched *s);
+/* Queue one pred request: fd, its n_q positions (host, copied). */
+int kvfs_sched_enqueue(kvfs_sched *s, int fd, int n_q, const int32_t *pos, double now);
+/* Current rate estimate lam (1/s) and target B*. */
+int kvfs_sched_state(kvfs_sched *s, double *lambda, int *target, int *n_waiting);
+/* If a batch is due at `now`: write its descriptors and packed positions (rows in descriptor order, the
+ * layout pred_attn_batch takes), remove them from the queue and return 1; else return 0 and write nothing.
+ * ENOMEM (nothing removed) if desc_cap / pos_cap are too small for the batch. */
+int kvfs_sched_form(kvfs_sched *s, double now, pred_desc *descs, int desc_cap, int32_t *pos, int64_t pos_cap,
+                    int *n_desc, int64_t *n_rows);
+
 /* ---------------------------------------------------------------- knobs and counters */
 typedef enum {
   KVFS_OPT_DECODE_CTAS = 1,     /* grid size of the decode kernel; 0 = auto (SM count x occupancy) */

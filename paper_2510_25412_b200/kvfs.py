@@ -33,8 +33,14 @@ EXPORTS = [
     "pred_attn_batch", "pred_step_begin", "pred_attn_layer", "pred_step_end", "kvfs_stat",
     "kvfs_get_table", "kvfs_get_positions", "kvfs_get_refcounts", "kvfs_free_pages", "kvfs_read",
     "kvfs_audit", "kvfs_set_option", "kvfs_get_counter", "kvfs_pack", "kvfs_unpack", "kvfs_extract",
-    "kvfs_merge",
+    "kvfs_merge", "kvfs_sched_create", "kvfs_sched_destroy", "kvfs_sched_enqueue", "kvfs_sched_state",
+    "kvfs_sched_form",
 ]
+
+
+class SchedConfig(ctypes.Structure):
+    _fields_ = [("w_max", ctypes.c_double), ("b_max", ctypes.c_int), ("alpha", ctypes.c_double),
+                ("dt_default", ctypes.c_double)]
 
 
 class KvfsConfig(ctypes.Structure):
@@ -84,6 +90,11 @@ def lib():
             "kvfs_compact": (cint, [vp, cint, vp]),
             "kvfs_extract": (cint, [vp, cint, P(ctypes.c_int64), i64, ctypes.c_char_p, P(cint), vp]),
             "kvfs_merge": (cint, [vp, P(cint), cint, ctypes.c_char_p, P(cint), vp]),
+            "kvfs_sched_create": (cint, [P(SchedConfig), P(vp)]),
+            "kvfs_sched_destroy": (cint, [vp]),
+            "kvfs_sched_enqueue": (cint, [vp, cint, cint, P(i32), ctypes.c_double]),
+            "kvfs_sched_state": (cint, [vp, P(ctypes.c_double), P(cint), P(cint)]),
+            "kvfs_sched_form": (cint, [vp, ctypes.c_double, vp, cint, P(i32), i64, P(cint), P(i64)]),
             "kvfs_append": (cint, [vp, cint, i64, P(i32), vp, vp, vp]),
             "pred_attn_batch": (cint, [vp, P(PredDesc), cint, P(i32), vp, vp, vp, vp, vp, ctypes.c_float,
                                        P(cint), vp]),
@@ -382,3 +393,41 @@ class KVFS:
         v = ctypes.c_int64()
         _check(lib().kvfs_get_counter(self._h, which, ctypes.byref(v)), "get_counter")
         return v.value
+
+
+class Scheduler:
+    """Inference scheduler batch formation (kvfs_sched_*, §4.4): Poisson-rate-sized
+    FIFO batches of pred requests.  Host only."""
+
+    def __init__(self, w_max: float = 0.010, b_max: int = 64, alpha: float = 0.2, dt_default: float = 0.1):
+        cfg = SchedConfig(w_max, b_max, alpha, dt_default)
+        h = ctypes.c_void_p()
+        _check(lib().kvfs_sched_create(ctypes.byref(cfg), ctypes.byref(h)), "sched_create")
+        self._h = h
+        self.b_max = b_max
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().kvfs_sched_destroy(self._h)
+            self._h = None
+
+    def enqueue(self, fd: int, pos, now: float) -> None:
+        p = _i32(pos)
+        _check(lib().kvfs_sched_enqueue(self._h, fd, p.shape[0], _ptr(p, ctypes.c_int32), now), "sched_enqueue")
+
+    def state(self):
+        lam, tgt, n = ctypes.c_double(), ctypes.c_int(), ctypes.c_int()
+        _check(lib().kvfs_sched_state(self._h, ctypes.byref(lam), ctypes.byref(tgt), ctypes.byref(n)), "sched_state")
+        return lam.value, tgt.value, n.value
+
+    def form(self, now: float, pos_cap: int = 1 << 16):
+        """None if no batch is due, else ([(fd, n_q)], positions)."""
+        descs = (PredDesc * self.b_max)()
+        pos = np.zeros(pos_cap, dtype=np.int32)
+        nd, nr = ctypes.c_int(), ctypes.c_int64()
+        rc = lib().kvfs_sched_form(self._h, now, ctypes.cast(descs, ctypes.c_void_p), self.b_max,
+                                   _ptr(pos, ctypes.c_int32), pos_cap, ctypes.byref(nd), ctypes.byref(nr))
+        if rc == 0:
+            return None
+        _check(rc if rc < 0 else 0, "sched_form")
+        return [(descs[i].fd, descs[i].n_q) for i in range(nd.value)], pos[:nr.value].tolist()
