@@ -180,6 +180,20 @@ int pred_step_begin(kvfs_ctx *ctx, const pred_desc *descs, int n_desc, const int
 int pred_attn_layer(kvfs_ctx *ctx, pred_step *step, int layer, const void *q, const void *k_new,
                     const void *v_new, void *out, float *lse, float scale, kvfs_stream_t stream);
 int pred_step_end(kvfs_ctx *ctx, pred_step *step);
+/* Attention-score accumulation for heavy-hitter (H2O-style) replacement policies (§6: the
+ * key finer-grained interface is attention-level access, e.g. H2O; §4.2 P:225 the LIP then evicts the
+ * "unimportant tokens").  After pred_attn_layer(step, layer, ... lse ...) of an open
+ * step, for every successful descriptor d with n_q > 0 and every token k of its file after the append
+ * (logical order, len_after = kvfs_stat len), writes
+ *     scores[score_off[d] + k] = sum over the descriptor's query rows i and the Hq query heads h of
+ *                                softmax_{i,h}(k)      (0 for a key row i cannot see; rule R10's weights)
+ * i.e. exp(scale <q_ih, k_g(h)> - lse_ih) summed, from the SAME q and the lse that pred_attn_layer wrote.
+ * q: device [T][Hq][D] bf16; lse: device [T][Hq] fp32 (as written by pred_attn_layer); scores: device fp32,
+ * caller-owned; score_off: host [n_desc] (entries of failed or n_q = 0 descriptors are ignored).  Costs one
+ * extra read of the files' K rows of that layer (HBM-bound, kernel K9).  EINVAL if lse or scores is NULL
+ * or no step is open. */
+int pred_attn_scores(kvfs_ctx *ctx, pred_step *step, int layer, const void *q, const float *lse, float scale,
+                     float *scores, const int64_t *score_off, kvfs_stream_t stream);
 
 /* ---------------------------------------------------------------- introspection (tests, policies) */
 typedef struct {

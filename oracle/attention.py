@@ -46,6 +46,26 @@ def gqa_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, scale: float):
     return out, lse
 
 
+def attention_scores(q: np.ndarray, k: np.ndarray, scale: float) -> np.ndarray:
+    """NEXT-2 (H2O, §6): per retained key k (logical order) the softmax weight of R10 summed
+    over the query rows i and the Hq heads (0 where row i cannot see k).  q [n_q][Hq][D], k [len][Hkv][D]
+    float64.  Pinned by tests/test_oracle_pins.py: Q = 0 closed form (uniform weights 1/|vis(i)|), the
+    total = n_q * Hq, and torch.softmax over an explicitly masked dense score matrix."""
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    n_q, hq, d = q.shape
+    length, hkv, _ = k.shape
+    group = hq // hkv
+    acc = np.zeros(length, dtype=np.float64)
+    for i in range(n_q):
+        n_vis = length - n_q + i + 1
+        for h in range(hq):
+            s = scale * (k[:n_vis, h // group, :] @ q[i, h, :])
+            p = np.exp(s - s.max())
+            acc[:n_vis] += p / p.sum()
+    return acc
+
+
 def attention_over_file(q_bits: np.ndarray, k_bits: np.ndarray, v_bits: np.ndarray, scale: float):
     """Same as gqa_attention on bf16 bit-pattern inputs (uint16)."""
     return gqa_attention(bf16_to_f64(q_bits), bf16_to_f64(k_bits), bf16_to_f64(v_bits), scale)

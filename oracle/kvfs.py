@@ -39,7 +39,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from .attention import gqa_attention
+from .attention import attention_scores, gqa_attention
 from .bf16 import bf16_to_f64
 
 OK = 0
@@ -504,7 +504,7 @@ class Oracle:
         return status, slot_lists
 
     def pred_batch(self, descs: Sequence[Tuple[int, int]], pos: Sequence[int], q, k_new, v_new,
-                   scale: float):
+                   scale: float, scores: bool = False):
         """Batched pred: q [L][T][Hq][D], k_new/v_new [L][T][Hkv][D] bf16 bits (rows packed in descriptor
         order). Returns (status, out [L][T][Hq][D] float64 (NaN rows for failed descriptors), lse)."""
         q = np.asarray(q)
@@ -534,4 +534,13 @@ class Oracle:
                                      bf16_to_f64(vv), scale)
                 out[layer, r0:r0 + nq] = o
                 lse[layer, r0:r0 + nq] = s
+        if scores:  # per descriptor (None if failed / n_q = 0): layer-0 accumulated weights (NEXT-2)
+            sc = []
+            for fd, r0, nq, st, slots in fd_of:
+                if st != OK or nq == 0:
+                    sc.append(None)
+                    continue
+                kk, _ = self.read(fd, 0, 0, self.fds[fd].length())
+                sc.append(attention_scores(bf16_to_f64(q[0, r0:r0 + nq]), bf16_to_f64(kk), scale))
+            return status, out, lse, sc
         return status, out, lse

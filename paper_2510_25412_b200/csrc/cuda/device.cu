@@ -321,6 +321,22 @@ class CudaDevice final : public Device {
     return cudaGetLastError() == cudaSuccess ? KVFS_OK : KVFS_EIO;
   }
 
+  int scores(const std::vector<ScoreDesc> &descs, const std::vector<ScoreUnit> &units, int layer, const void *q,
+             const float *lse, float scale, float *out, kvfs_stream_t s) override {
+    begin_packet();
+    const void *dd = push(descs.data(), descs.size() * sizeof(ScoreDesc));
+    const void *du = push(units.data(), units.size() * sizeof(ScoreUnit));
+    if (!dd || !du) return KVFS_ENOMEM;
+    if (!send(s)) return KVFS_EIO;
+    const kvfs_config &cfg = c_.cfg;
+    const cudaError_t e = dev::launch_scores(
+        static_cast<const dev::ScoreUnit *>(du), static_cast<int>(units.size()), static_cast<const dev::ScoreDesc *>(dd),
+        slab_, static_cast<const bf16 *>(q), lse, static_cast<const bf16 *>(c_.kpool[layer]),
+        scale * 1.4426950408889634f, out, cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, cfg.page_size, cs(s));
+    ++c_.ctr.launches;
+    return e == cudaSuccess ? KVFS_OK : KVFS_EIO;
+  }
+
   int gather(const std::vector<int32_t> &src_slots, const std::vector<uint32_t> &new_pages,
              kvfs_stream_t s) override {
     begin_packet();

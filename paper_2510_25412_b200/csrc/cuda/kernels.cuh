@@ -41,6 +41,16 @@ struct PrefixDesc {  // == kvfs::PrefixDesc
 struct PrefixRow {  // == kvfs::PrefixRow
   int32_t t, pref_base, n_q, qi;
 };
+struct ScoreDesc {  // == kvfs::ScoreDesc
+  int32_t slab_off, n_q, row0, len_after;
+  int64_t out_off;
+};
+struct ScoreUnit {  // == kvfs::ScoreUnit
+  int32_t desc, e0, e1, l0;
+};
+cudaError_t launch_scores(const ScoreUnit *units, int n_units, const ScoreDesc *descs, const Entry *slab,
+                          const __nv_bfloat16 *q, const float *lse, const __nv_bfloat16 *kpool, float scale_log2,
+                          float *out, int Hq, int Hkv, int D, int P, cudaStream_t s);
 struct ChunkParams {
   const ChunkUnit *units;
   const ChunkDesc *descs;

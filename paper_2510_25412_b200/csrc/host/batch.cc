@@ -37,6 +37,7 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
   pl.chunk_units.clear();
   pl.chunk_dst.clear();
   pl.desc_files.clear();
+  pl.score_src.clear();
   pl.prefix_descs.clear();
   pl.prefix_units.clear();
   pl.prefix_rows.clear();
@@ -99,6 +100,7 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
           d.first_new_lstart = f->table[fne].lstart;
           pl.descs.push_back(d);
           pl.desc_files.push_back(f);
+          pl.score_src.push_back({i, d.slab_off, nq, d.row0, f});
           pl.total_cost += static_cast<int64_t>(Hkv) * nq * d.stages_per_unit;
           pl.n_units += Hkv * nq;
           pl.max_nq = std::max(pl.max_nq, nq);

@@ -291,6 +291,31 @@ int pred_attn_layer(kvfs_ctx *ctx, pred_step *step, int layer, const void *q, co
   return rc;
 }
 
+int pred_attn_scores(kvfs_ctx *ctx, pred_step *step, int layer, const void *q, const float *lse, float scale,
+                     float *scores, const int64_t *score_off, kvfs_stream_t stream) {
+  if (!ctx) return KVFS_EINVAL;
+  Lock lk(ctx);
+  Ctx &c = *lk.c;
+  if (!c.step_open || step != reinterpret_cast<pred_step *>(&c.plan)) return KVFS_EINVAL;
+  if (!c.dev) return KVFS_ENOSYS;
+  if (c.poisoned) return KVFS_EIO;
+  if (layer < 0 || layer >= c.cfg.n_layers || !(scale > 0.f)) return KVFS_EINVAL;
+  if (c.plan.score_src.empty()) return KVFS_OK;
+  if (!q || !lse || !scores || !score_off) return KVFS_EINVAL;
+  std::vector<ScoreDesc> sd;
+  std::vector<ScoreUnit> su;
+  for (const ScoreSrc &x : c.plan.score_src) {
+    const File &f = *x.file;
+    const int32_t di = static_cast<int32_t>(sd.size());
+    sd.push_back({x.slab_off, x.n_q, x.row0, static_cast<int32_t>(f.len), score_off[x.batch_idx]});
+    const int32_t ne = static_cast<int32_t>(f.table.size());
+    for (int32_t e0 = 0; e0 < ne; e0 += 32) su.push_back({di, e0, std::min(ne, e0 + 32), f.table[e0].lstart});
+  }
+  const int rc = c.dev->scores(sd, su, layer, q, lse, scale, scores, stream);
+  if (rc != KVFS_OK) c.poisoned = true;
+  return rc;
+}
+
 int pred_step_end(kvfs_ctx *ctx, pred_step *step) {
   if (!ctx) return KVFS_EINVAL;
   Lock lk(ctx);

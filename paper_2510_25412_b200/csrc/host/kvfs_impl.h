@@ -101,6 +101,19 @@ struct PrefixDesc {
   int32_t row0;       // first PrefixRow of the family
   int32_t split, n_splits, pad0, pad1;
 };
+// NEXT-2 attention-score accumulation (pred_attn_scores): every successful descriptor of the step, and
+// the work units (descriptor, entry chunk of <= 32 entries, logical index of the chunk's first token).
+struct ScoreDesc {
+  int32_t slab_off, n_q, row0, len_after;
+  int64_t out_off;  // caller's offset of the descriptor's scores
+};
+struct ScoreUnit {
+  int32_t desc, e0, e1, l0;
+};
+struct ScoreSrc {
+  int32_t batch_idx, slab_off, n_q, row0;
+  File *file;
+};
 struct PrefixRow {
   int32_t t;          // packed row (Q row) of the query token
   int32_t pref_base;  // DevDesc::pref_base of its descriptor
@@ -128,6 +141,7 @@ struct PredPlan {
   std::vector<ChunkUnit> prefix_units;
   std::vector<PrefixRow> prefix_rows;
   int32_t prefix_partials = 0;  // partials the prefix kernel writes (PART floats each)
+  std::vector<ScoreSrc> score_src;  // every successful descriptor with n_q > 0 (batch order)
   int32_t prefix_groups = 0;
 };
 
@@ -213,6 +227,8 @@ class Device {
   virtual int pred_begin(PredPlan &plan, kvfs_stream_t s) = 0;
   virtual int pred_layer(const PredPlan &plan, int layer, const void *q, const void *k_new, const void *v_new,
                          void *out, float *lse, float scale, kvfs_stream_t s) = 0;
+  virtual int scores(const std::vector<ScoreDesc> &descs, const std::vector<ScoreUnit> &units, int layer,
+                     const void *q, const float *lse, float scale, float *out, kvfs_stream_t s) = 0;
   virtual int pack_pages(const std::vector<uint32_t> &pages, void *buf, kvfs_stream_t s) = 0;
   virtual int unpack_pages(const std::vector<uint32_t> &pages, const void *buf, kvfs_stream_t s) = 0;
   virtual int sync() = 0;

@@ -34,7 +34,7 @@ EXPORTS = [
     "kvfs_get_table", "kvfs_get_positions", "kvfs_get_refcounts", "kvfs_free_pages", "kvfs_read",
     "kvfs_audit", "kvfs_set_option", "kvfs_get_counter", "kvfs_pack", "kvfs_unpack", "kvfs_extract",
     "kvfs_merge", "kvfs_sched_create", "kvfs_sched_destroy", "kvfs_sched_enqueue", "kvfs_sched_state",
-    "kvfs_sched_form",
+    "kvfs_sched_form", "pred_attn_scores",
 ]
 
 
@@ -91,6 +91,7 @@ def lib():
             "kvfs_extract": (cint, [vp, cint, P(ctypes.c_int64), i64, ctypes.c_char_p, P(cint), vp]),
             "kvfs_merge": (cint, [vp, P(cint), cint, ctypes.c_char_p, P(cint), vp]),
             "kvfs_sched_create": (cint, [P(SchedConfig), P(vp)]),
+            "pred_attn_scores": (cint, [vp, vp, cint, vp, vp, ctypes.c_float, vp, P(i64), vp]),
             "kvfs_sched_destroy": (cint, [vp]),
             "kvfs_sched_enqueue": (cint, [vp, cint, cint, P(i32), ctypes.c_double]),
             "kvfs_sched_state": (cint, [vp, P(ctypes.c_double), P(cint), P(cint)]),
@@ -314,6 +315,14 @@ class KVFS:
 
     def pred_step_end(self, step) -> None:
         _check(lib().pred_step_end(self._h, step), "pred_step_end")
+
+    def pred_attn_scores(self, step, layer, q, lse, scores, score_off, scale=None, stream=None) -> None:
+        """Accumulated softmax weight per retained token (H2O; include/kvfs.h pred_attn_scores): after
+        pred_attn_layer of the same step with the same q and the lse it wrote."""
+        scale = float(scale if scale is not None else self.D ** -0.5)
+        off = np.ascontiguousarray(np.asarray(score_off, dtype=np.int64))
+        _check(lib().pred_attn_scores(self._h, step, layer, _dptr(q), _dptr(lse), scale, _dptr(scores),
+                                      _ptr(off, ctypes.c_int64), _stream(stream)), "pred_attn_scores")
 
     # ------------------------------------------------------------------ introspection
     def stat(self, fd: int) -> Tuple[int, int, int]:

@@ -1,0 +1,65 @@
+"""NEXT-2 attention-score accumulation (H2O; §6) on the GPU path: pred_attn_scores after
+pred_attn_layer equals the oracle's per-token softmax weight summed over query rows and heads, for decode,
+drafts and chunk descriptors, files with holes, forks sharing a prefix (cascade on), a failed descriptor."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from gpu_harness import Harness, assert_close, to_bits, to_dev  # noqa: E402
+
+from paper_2510_25412_b200 import kvfs as K  # noqa: E402
+
+
+@pytest.mark.parametrize("P,Hq,Hkv,D", [(16, 32, 8, 128), (32, 8, 2, 64), (64, 16, 2, 128)])
+def test_scores_match_oracle(P, Hq, Hkv, D):
+    h = Harness(4000, P, Hq, Hkv, D, seed=P + Hq + D)
+    h.c.set_option(K.OPT_CASCADE_MIN_ENTRIES, 2)
+    h.open("r")
+    h.append("r", list(range(700)))
+    h.evict("r", [(5, 40), (300, 333)])
+    for i in range(3):
+        h.fork("r", f"k{i}")
+        last = h.o.stat(h.fds[f"k{i}"][1])[2]
+        h.append(f"k{i}", list(range(last + 1, last + 1 + 50 * i + 3)))
+    h.open("big")
+    h.append("big", list(range(2000)))
+    rows = []
+    for name, nq in (("k0", 1), ("k1", 1), ("k2", 3), ("big", 20 if D == 128 else 5), ("r", 1)):
+        last = h.o.stat(h.fds[name][1])[2]
+        rows.append((name, list(range(last + 1, last + 1 + nq))))
+    rows.append(("k0", [99999]))  # EBUSY: ignored by the scores
+    descs_c = [(h.fds[n][0], len(p)) for n, p in rows]
+    descs_o = [(h.fds[n][1], len(p)) for n, p in rows]
+    pos = [x for _, p in rows for x in p]
+    T = len(pos)
+    k, v = h._kv(T)
+    q = h._q(T, 2.0)
+    scale = D ** -0.5
+    out = torch.empty((T, Hq, D), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((T, Hq), dtype=torch.float32, device="cuda")
+    lens = [h.c.stat(fd)[0] + n for fd, n in descs_c]  # length after the append (stat is refused mid-step)
+    lens[-1] = 0                                        # the EBUSY descriptor: no scores
+    step, st = h.c.pred_step_begin(descs_c, pos)
+    qd = to_dev(q[0])
+    h.c.pred_attn_layer(step, 0, qd, to_dev(k[0]), to_dev(v[0]), out, lse, scale)
+    off = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+    scores = torch.full((int(sum(lens)),), float("nan"), dtype=torch.float32, device="cuda")
+    h.c.pred_attn_scores(step, 0, qd, lse, scores, off, scale)
+    h.c.pred_step_end(step)
+    torch.cuda.synchronize()
+    st_o, out_o, lse_o, sc_o = h.o.pred_batch(descs_o, pos, q, k, v, scale, scores=True)
+    assert st == st_o and st[-1] == -16
+    sc = scores.cpu().numpy()
+    r = 0
+    for i, ((name, p), s) in enumerate(zip(rows, st)):
+        if s == 0:
+            assert_close(to_bits(out)[r:r + len(p)], out_o[0, r:r + len(p)], name)
+            got = sc[off[i]:off[i] + lens[i]]
+            ref = sc_o[i]
+            assert got.shape == ref.shape
+            assert np.abs(got - ref).max() <= 2e-3 * len(p) * Hq ** 0.5, name
+            assert abs(got.sum() - len(p) * Hq) <= 1e-3 * len(p) * Hq, name  # weights of each row-head sum to 1
+        r += len(p)
+    assert len(sc) == off[-1]  # nothing was written past the successful descriptors' ranges

@@ -110,3 +110,37 @@ def test_bf16_roundtrip_and_rne():
     x32 = np.concatenate([x32, ties])
     ref = torch.from_numpy(x32).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
     np.testing.assert_array_equal(f64_to_bf16_rne(x32.astype(np.float64)), ref)
+
+
+# ------------------------------------------------------------------ NEXT-2 attention-score accumulation
+from oracle.attention import attention_scores  # noqa: E402
+
+
+def test_scores_zero_query_closed_form():
+    """Q = 0: every visible key of row i has weight 1/|vis(i)| in each of the Hq heads."""
+    n_q, length, hq, hkv, d = 3, 11, 4, 2, 8
+    k = np.random.default_rng(0).normal(size=(length, hkv, d))
+    sc = attention_scores(np.zeros((n_q, hq, d)), k, 0.3)
+    ref = np.zeros(length)
+    for i in range(n_q):
+        nv = length - n_q + i + 1
+        ref[:nv] += hq / nv
+    assert np.allclose(sc, ref, rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("n_q,length,hq,hkv", [(1, 50, 8, 2), (4, 33, 4, 4), (7, 64, 8, 1)])
+def test_scores_match_torch_softmax_of_masked_matrix(n_q, length, hq, hkv):
+    rng = np.random.default_rng(n_q * 100 + length)
+    d = 16
+    q = rng.normal(size=(n_q, hq, d))
+    k = rng.normal(size=(length, hkv, d))
+    scale = d ** -0.5
+    qt = torch.from_numpy(q).permute(1, 0, 2)                      # [Hq][n_q][D]
+    kt = torch.from_numpy(k).permute(1, 0, 2).repeat_interleave(hq // hkv, dim=0)  # [Hq][len][D]
+    s = scale * qt @ kt.transpose(1, 2)                             # [Hq][n_q][len]
+    mask = torch.ones(n_q, length, dtype=torch.bool).tril(diagonal=length - n_q)  # bottom-right causal
+    w = torch.softmax(s.masked_fill(~mask, float("-inf")), dim=-1)
+    ref = w.sum(dim=(0, 1)).numpy()
+    sc = attention_scores(q, k, scale)
+    assert np.allclose(sc, ref, rtol=0, atol=1e-12)
+    assert math.isclose(sc.sum(), n_q * hq, rel_tol=1e-12)         # every (row, head) distribution sums to 1
