@@ -38,6 +38,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scores", action="store_true",
+                    help="also run pred_attn_scores (NEXT-2, H2O score accumulation) every timed step")
     return ap.parse_args()
 
 
@@ -216,6 +218,10 @@ def run_ours(args):
     barrier()
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(Kst)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(Kst)]
+    ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(Kst)] if args.scores else None
+    scores_buf = None
+    if args.scores:
+        scores_buf = torch.empty(int((wl.lens + wl.n_q).sum()) + T + 16, dtype=torch.float32, device="cuda")
     alg_bytes, alg_flops, logical = [], [], []
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
@@ -231,6 +237,10 @@ def run_ours(args):
         ev0[i].record()
         kv.pred_attn_layer(step, 0, q, k, v, out, lse)
         ev1[i].record()
+        if args.scores:
+            la = wl.lens + wl.n_q
+            kv.pred_attn_scores(step, 0, q, lse, scores_buf, np.concatenate([[0], np.cumsum(la)[:-1]]))
+            ev2[i].record()
         kv.pred_step_end(step)
         wl.advance()
     t_end.record()
@@ -336,6 +346,14 @@ def run_ours(args):
                   "h2d_metadata_bytes_per_step": h2d / Kst,
                   "decode_ctas": kv.counter(K.CTR_LAST_DECODE_CTAS)},
     }
+    if args.scores:
+        sc_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev1, ev2))
+        k_bytes = statistics.mean(logical) / 2
+        line["extra"]["scores"] = {
+            "kernel": "scores_kernel (K9, H2O attention-score accumulation, second pass over K)",
+            "ms_mean": sc_ms, "k_bytes_per_step": k_bytes, "gbs": k_bytes / (sc_ms / 1000.0) / 1e9,
+            "frac_of_peak": k_bytes / (sc_ms / 1000.0) / 1e9 / peak,
+            "overhead_vs_attention": sc_ms / k_ms}
     if e2e:
         line["e2e"] = e2e
     if world == 1 and not args.no_cpu_baseline:

@@ -3,9 +3,7 @@
 //   scores[off_d + k] = sum_{rows i of d, heads h} exp2(scale_log2 <q_ih, K_k,g(h)> - lse_ih log2 e)
 // for every retained token k visible to row i (logical k <= len_after - n_q + i), exactly the softmax
 // weights of rule R10 given the lse the attention kernels wrote.
-// One CTA per (descriptor, chunk of <= 32 page entries); thread = (entry, kv head, slot) with the slot
-// fastest (a warp reads two contiguous (page, head) blocks); Q rows (bf16) and lse (log2 domain) of up to
-// QB query rows staged in shared memory; per-key sums over heads in shared-memory atomics.
+// One CTA per (descriptor, chunk of <= 32 page entries).
 #include <cuda_bf16.h>
 
 #include "kernels.cuh"
@@ -13,127 +11,161 @@
 namespace kvfs {
 namespace dev {
 
-constexpr int QB = 8;  // query rows per pass over the chunk's keys
-
+// Layout per CTA (256 threads = 8 warps): warp w takes kv head g = w % Hkv and every (8 / Hkv)-th group
+// of 4 keys (Hkv < 8) of the unit's entries; in a warp, 8 lanes share a key (D / 8 dims each, loaded as
+// 16-byte vectors: the 8 lanes read the key's contiguous row), 4 keys per step, UNR steps in flight.  The
+// lane's slice of q (G heads of the current query row) stays in registers; the G partial dot products
+// are reduced by xor-shuffles over the 8 lanes; lane 0 of the key adds sum_h exp2(s - lse2) into the
+// key's shared-memory accumulator.  Query rows are processed one after another (decode: one row).
+template <int D, int G>
 __global__ void __launch_bounds__(256) scores_kernel(const ScoreUnit *units, const ScoreDesc *descs,
                                                      const Entry *slab, const __nv_bfloat16 *q, const float *lse,
                                                      const __nv_bfloat16 *kpool, float scale_log2, float *out,
-                                                     int Hq, int Hkv, int D, int P) {
-  extern __shared__ __align__(16) uint8_t sm[];
-  __shared__ float acc[32 * 64];      // [entry][slot]
+                                                     int Hkv, int P) {
+  constexpr int DPL = D / 8;   // dims per lane
+  constexpr int CH = DPL / 8;  // 16-byte chunks per lane
+  constexpr int UNR = 4;       // warp steps (4 keys each) in flight
+  __shared__ float acc[32 * 64];  // [entry][slot]
   __shared__ uint64_t emask[32];
   __shared__ uint32_t epage[32];
-  __shared__ int32_t elog[32];        // logical index of the entry's first retained token
+  __shared__ int32_t elog[32];
+  __shared__ int16_t kslot[32 * 64];  // retained keys of the unit: (entry << 8) | slot, logical order
+  __shared__ int nkeys;
   const ScoreUnit u = units[blockIdx.x];
   const ScoreDesc d = descs[u.desc];
   const int ne = u.e1 - u.e0;
-  const int G = Hq / Hkv;
-  __nv_bfloat16 *qs = reinterpret_cast<__nv_bfloat16 *>(sm);  // [QB][Hq][D]
-  float *ls = reinterpret_cast<float *>(qs + QB * Hq * D);     // [QB][Hq]
-  if (threadIdx.x < 32) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
     uint64_t m = 0;
     uint32_t pg = 0;
-    if (static_cast<int>(threadIdx.x) < ne) {
-      const Entry e = slab[d.slab_off + u.e0 + threadIdx.x];
+    if (lane < ne) {
+      const Entry e = slab[d.slab_off + u.e0 + lane];
       m = e.mask;
       pg = e.page;
     }
-    int cnt = __popcll(m), incl = cnt;
+    const int cnt = __popcll(m);
+    int incl = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (static_cast<int>(threadIdx.x) >= o) incl += y;
+      if (lane >= o) incl += y;
     }
-    emask[threadIdx.x] = m;
-    epage[threadIdx.x] = pg;
-    elog[threadIdx.x] = u.l0 + incl - cnt;
+    emask[lane] = m;
+    epage[lane] = pg;
+    elog[lane] = incl - cnt;  // unit-relative
+    int w = incl - cnt;
+    for (uint64_t mm = m; mm; mm &= mm - 1) kslot[w++] = static_cast<int16_t>((lane << 8) | __ffsll(mm) - 1);
+    if (lane == 31) nkeys = incl;
   }
   for (int i = threadIdx.x; i < 32 * 64; i += blockDim.x) acc[i] = 0.f;
-  const int base = d.len_after - d.n_q;  // row i sees logical keys <= base + i
-  const int pairs = ne * Hkv * P;
-  for (int qb = 0; qb < d.n_q; qb += QB) {
-    const int nr = min(QB, d.n_q - qb);
-    __syncthreads();
-    for (int i = threadIdx.x; i < nr * Hq * D / 8; i += blockDim.x)
-      reinterpret_cast<uint4 *>(qs)[i] =
-          reinterpret_cast<const uint4 *>(q + static_cast<int64_t>(d.row0 + qb) * Hq * D)[i];
-    for (int i = threadIdx.x; i < nr * Hq; i += blockDim.x)
-      ls[i] = lse[static_cast<int64_t>(d.row0 + qb) * Hq + i] * 1.4426950408889634f;
-    __syncthreads();
-    for (int t = threadIdx.x; t < pairs; t += blockDim.x) {
-      const int slot = t % P, g = (t / P) % Hkv, e = t / (P * Hkv);
-      const uint64_t m = emask[e];
-      if (!((m >> slot) & 1ull)) continue;
-      const int key = elog[e] + __popcll(m & ((1ull << slot) - 1ull));
-      if (key > base + qb + nr - 1) continue;  // no row of this block sees it
-      const uint4 *kr = reinterpret_cast<const uint4 *>(
-          kpool + ((static_cast<int64_t>(epage[e]) * Hkv + g) * P + slot) * D);
-      float dot[QB][8];
+  __syncthreads();
+  const int n = nkeys;
+  const int g = warp % Hkv, kset = warp / Hkv, nsets = 8 / Hkv;  // Hkv in {1, 2, 4, 8}
+  const int kg = lane >> 3, sub = lane & 7;
+  const int base = d.len_after - d.n_q - u.l0;  // row i sees unit-relative keys <= base + i
+  for (int r = 0; r < d.n_q; ++r) {
+    const int row = d.row0 + r;
+    float2 qf[G][DPL / 2];
 #pragma unroll
-      for (int r = 0; r < QB; ++r)
+    for (int h = 0; h < G; ++h) {
+      const uint4 *qs = reinterpret_cast<const uint4 *>(q + (static_cast<int64_t>(row) * (Hkv * G) + g * G + h) * D) +
+                        sub * CH;
 #pragma unroll
-        for (int h = 0; h < 8; ++h) dot[r][h] = 0.f;
-      for (int c = 0; c < D / 8; ++c) {
-        const uint4 w = __ldg(kr + c);
+      for (int c = 0; c < CH; ++c) {
+        const uint4 w = __ldg(qs + c);
         const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-        float kf[8];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const float2 f = bf2_to_f2(ws[j]);
-          kf[2 * j] = f.x;
-          kf[2 * j + 1] = f.y;
+          qf[h][c * 4 + j] = make_float2(f.x * scale_log2, f.y * scale_log2);
         }
+      }
+    }
+    float l2[G];
 #pragma unroll
-        for (int r = 0; r < QB; ++r) {
-          if (r < nr) {
+    for (int h = 0; h < G; ++h) l2[h] = lse[static_cast<int64_t>(row) * (Hkv * G) + g * G + h] * 1.4426950408889634f;
+    const int vis = min(n, base + r + 1);  // unit-relative keys visible to this row
+    for (int k0 = kset * 4; k0 < vis; k0 += nsets * 4 * UNR) {
+      uint4 kr[UNR][CH];
 #pragma unroll
-            for (int h = 0; h < 8; ++h) {
-              if (h < G) {
-                const uint4 qw = reinterpret_cast<const uint4 *>(qs + (r * Hq + g * G + h) * D)[c];
-                const uint32_t qq[4] = {qw.x, qw.y, qw.z, qw.w};
+      for (int s = 0; s < UNR; ++s) {
+        const int key = k0 + s * nsets * 4 + kg;
+        if (key < vis) {
+          const int ks = kslot[key], e = ks >> 8, slot = ks & 255;
+          const uint4 *src = reinterpret_cast<const uint4 *>(
+                                 kpool + ((static_cast<int64_t>(epage[e]) * Hkv + g) * P + slot) * D) + sub * CH;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  const float2 f = bf2_to_f2(qq[j]);
-                  dot[r][h] = fmaf(f.x, kf[2 * j], fmaf(f.y, kf[2 * j + 1], dot[r][h]));
-                }
-              }
+          for (int c = 0; c < CH; ++c) kr[s][c] = __ldg(src + c);
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < UNR; ++s) {
+        const int key = k0 + s * nsets * 4 + kg;
+        float dot[G];
+#pragma unroll
+        for (int h = 0; h < G; ++h) dot[h] = 0.f;
+        if (key < vis) {
+#pragma unroll
+          for (int c = 0; c < CH; ++c) {
+            const uint32_t ws[4] = {kr[s][c].x, kr[s][c].y, kr[s][c].z, kr[s][c].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 kf = bf2_to_f2(ws[j]);
+#pragma unroll
+              for (int h = 0; h < G; ++h) dot[h] = fmaf(qf[h][c * 4 + j].x, kf.x, fmaf(qf[h][c * 4 + j].y, kf.y, dot[h]));
             }
           }
         }
+#pragma unroll
+        for (int h = 0; h < G; ++h)
+#pragma unroll
+          for (int o = 1; o < 8; o <<= 1) dot[h] += __shfl_xor_sync(0xffffffffu, dot[h], o);
+        if (sub == 0 && key < vis) {
+          float sum = 0.f;
+#pragma unroll
+          for (int h = 0; h < G; ++h) sum += exp2f(dot[h] - l2[h]);
+          const int ks = kslot[key];
+          atomicAdd(&acc[(ks >> 8) * 64 + (ks & 255)], sum);
+        }
       }
-      float sum = 0.f;
-#pragma unroll
-      for (int r = 0; r < QB; ++r)
-        if (r < nr && key <= base + qb + r)
-#pragma unroll
-          for (int h = 0; h < 8; ++h)
-            if (h < G) sum += exp2f(dot[r][h] * scale_log2 - ls[r * Hq + g * G + h]);
-      atomicAdd(&acc[e * 64 + slot], sum);
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < ne * P; t += blockDim.x) {
-    const int e = t / P, slot = t % P;
-    const uint64_t m = emask[e];
-    if ((m >> slot) & 1ull) out[d.out_off + elog[e] + __popcll(m & ((1ull << slot) - 1ull))] = acc[e * 64 + slot];
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    const int ks = kslot[t];
+    out[d.out_off + u.l0 + t] = acc[(ks >> 8) * 64 + (ks & 255)];
   }
+  (void)elog;
 }
 
-size_t scores_smem_bytes(int Hq, int D) { return static_cast<size_t>(QB) * Hq * D * 2 + QB * Hq * 4; }
+template <int D, int G>
+static cudaError_t launch_scores_t(const ScoreUnit *units, int n_units, const ScoreDesc *descs, const Entry *slab,
+                                   const __nv_bfloat16 *q, const float *lse, const __nv_bfloat16 *kpool,
+                                   float scale_log2, float *out, int Hkv, int P, cudaStream_t s) {
+  scores_kernel<D, G><<<n_units, 256, 0, s>>>(units, descs, slab, q, lse, kpool, scale_log2, out, Hkv, P);
+  return cudaGetLastError();
+}
+
+template <int D>
+static cudaError_t launch_scores_d(const ScoreUnit *units, int n_units, const ScoreDesc *descs, const Entry *slab,
+                                   const __nv_bfloat16 *q, const float *lse, const __nv_bfloat16 *kpool,
+                                   float scale_log2, float *out, int G, int Hkv, int P, cudaStream_t s) {
+  switch (G) {
+    case 1: return launch_scores_t<D, 1>(units, n_units, descs, slab, q, lse, kpool, scale_log2, out, Hkv, P, s);
+    case 2: return launch_scores_t<D, 2>(units, n_units, descs, slab, q, lse, kpool, scale_log2, out, Hkv, P, s);
+    case 4: return launch_scores_t<D, 4>(units, n_units, descs, slab, q, lse, kpool, scale_log2, out, Hkv, P, s);
+    case 8: return launch_scores_t<D, 8>(units, n_units, descs, slab, q, lse, kpool, scale_log2, out, Hkv, P, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 cudaError_t launch_scores(const ScoreUnit *units, int n_units, const ScoreDesc *descs, const Entry *slab,
                           const __nv_bfloat16 *q, const float *lse, const __nv_bfloat16 *kpool, float scale_log2,
                           float *out, int Hq, int Hkv, int D, int P, cudaStream_t s) {
-  const size_t smem = scores_smem_bytes(Hq, D);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && attr < smem) {
-    const cudaError_t e = cudaFuncSetAttribute(scores_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
-  scores_kernel<<<n_units, 256, smem, s>>>(units, descs, slab, q, lse, kpool, scale_log2, out, Hq, Hkv, D, P);
-  return cudaGetLastError();
+  if (Hkv > 8 || 8 % Hkv) return cudaErrorInvalidValue;
+  if (D == 64) return launch_scores_d<64>(units, n_units, descs, slab, q, lse, kpool, scale_log2, out, Hq / Hkv, Hkv, P, s);
+  if (D == 128) return launch_scores_d<128>(units, n_units, descs, slab, q, lse, kpool, scale_log2, out, Hq / Hkv, Hkv, P, s);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace dev
