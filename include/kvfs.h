@@ -69,7 +69,8 @@ typedef enum {
   KVFS_ERANGE = -34,     /* index / length out of range */
   KVFS_ENOSYS = -38,     /* data operation on a host-only ctx */
   KVFS_EPOS = -1001,     /* positions not strictly increasing / not > last retained (SPEC PositionConflict) */
-  KVFS_EPARTIAL = -1002  /* pred batch: some descriptors failed, see status[] */
+  KVFS_EPARTIAL = -1002, /* pred batch: some descriptors failed, see status[] */
+  KVFS_EOFFLOAD = -1003  /* the file is offloaded to the host tier (kvfs_offload): restore it first */
 } kvfs_err;
 
 enum { KVFS_O_CREAT = 1, KVFS_O_EXCL = 2 };   /* kvfs_open flags (R2) */
@@ -259,6 +260,22 @@ int kvfs_extract(kvfs_ctx *ctx, int src_fd, const int64_t *indices, int64_t n, c
                  kvfs_stream_t stream);
 int kvfs_merge(kvfs_ctx *ctx, const int *fds, int n_fds, const char *name, int *fd, kvfs_stream_t stream);
 
+/* ---------------------------------------------------------------- host tier: offload / restore
+ * PAPER.md §4.3: while a thread waits on I/O, Symphony "offloads their KV caches from the GPU to the
+ * CPU and restores them upon I/O completion".  Rule R15: kvfs_offload moves every page the
+ * file owns EXCLUSIVELY (refcount 1) to a pinned host buffer owned by the ctx (bits of every layer, K and V,
+ * copied by the page-pack kernel writing through the mapped host pointer on `stream`) and frees it on the
+ * device; pages shared with other files stay (another file may need them).  In the table such an entry's
+ * page reads KVFS_HOST_PAGE | host slot (slots in table order).  kvfs_restore allocates device pages
+ * smallest-free first in table order for those entries (ENOSPC, atomic, if too few are free), copies the
+ * bits back and SYNCHRONIZES `stream` before releasing the host buffer.  While offloaded the file is
+ * EOFFLOAD for append / pred (per-descriptor status) / fork / truncate / evict / compact / extract / merge /
+ * read / pack; stat, tables, positions, close and unlink work (unlink drops the host copy).  kvfs_offload of
+ * an offloaded file, or kvfs_restore of one that is not, is EINVAL.  *moved (nullable) = pages moved. */
+#define KVFS_HOST_PAGE 0x80000000u
+int kvfs_offload(kvfs_ctx *ctx, int fd, int64_t *moved, kvfs_stream_t stream);
+int kvfs_restore(kvfs_ctx *ctx, int fd, int64_t *moved, kvfs_stream_t stream);
+
 /* ---------------------------------------------------------------- inference scheduler: batch formation
  * PAPER.md §4.4: the inference scheduler "aggregates multiple pred system calls into a single
  * batch"; executing too early under-uses the GPU, too late makes threads wait; Symphony "dynamically adjusts
@@ -310,7 +327,8 @@ typedef enum {
   KVFS_CTR_LAST_DECODE_CTAS = 4, /* grid (virtual CTAs = rings) of the last decode launch */
   KVFS_CTR_LAST_CHUNK_UNITS = 5, /* CTAs of the last tcgen05 chunk launch (0: none) */
   KVFS_CTR_LAST_PREFIX_UNITS = 6,  /* CTAs of the last shared-prefix (cascade) launch (0: none) */
-  KVFS_CTR_LAST_PREFIX_GROUPS = 7  /* fork families (groups) the last pred batch attended as shared prefixes */
+  KVFS_CTR_LAST_PREFIX_GROUPS = 7, /* fork families (groups) the last pred batch attended as shared prefixes */
+  KVFS_CTR_HOST_PAGES = 8          /* pages currently in the host tier (kvfs_offload) */
 } kvfs_counter;
 int kvfs_get_counter(kvfs_ctx *ctx, int counter, int64_t *value);
 

@@ -18,7 +18,7 @@ DESIGN.md "Oracle pins". Nothing here is parity-unpinned.
 from .kvfs import (  # noqa: F401
     Oracle,
     KvfsError,
-    OK, ENOENT, EBADF, EBUSY, EEXIST, EINVAL, ENOSPC, ERANGE, EPOS, EPARTIAL, EIO,
+    OK, ENOENT, EBADF, EBUSY, EEXIST, EINVAL, ENOSPC, ERANGE, EPOS, EPARTIAL, EIO, EOFFLOAD, HOST,
     O_CREAT, O_EXCL, EVICT_COMPACT,
 )
 from .attention import gqa_attention, attention_over_file  # noqa: F401

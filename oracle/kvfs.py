@@ -25,6 +25,13 @@ Rules (readings of a silent paper; numbers as in SURVEY.md
                  file holding the selected logical tokens (strictly increasing indices, EINVAL; < len,
                  ERANGE) in order with their original positions, in ceil(k/P) fresh pages allocated by R1
                  in logical order (pages rebuilt, no sharing); the source is unchanged
+  R15 offload    P:233 "offloads their KV caches from the GPU to the CPU and restores them upon I/O
+                 completion": offload moves every EXCLUSIVELY owned page (refcount 1) of the file to the
+                 host tier (entry page := HOST | host slot, in table order) and frees it on the device;
+                 shared pages stay.  restore allocates device pages by R1 in table order
+                 for the host entries (ENOSPC atomic) and copies the bits back.  While offloaded, every op
+                 touching the file's pages (append / pred / fork / truncate / evict / compact / extract /
+                 merge / read) is EOFFLOAD; stat, tables, close and unlink are allowed
   R14 merge      P:225 "merging existing files into one": a new file holding every part's retained tokens
                  sorted by position (duplicate positions: EPOS, SPEC S:100-106), pages rebuilt as in R13;
                  a part listed twice is EBUSY; the parts are unchanged
@@ -53,6 +60,8 @@ ENOSPC = -28
 ERANGE = -34
 EPOS = -1001
 EPARTIAL = -1002
+EOFFLOAD = -1003  # the file's exclusive pages are in the host tier (R15): restore it first
+HOST = 1 << 31    # table page field of an entry whose page lives in the host tier: HOST | host slot
 
 O_CREAT = 1
 O_EXCL = 2
@@ -74,13 +83,14 @@ def _hi(mask: int) -> int:
 
 
 class _File:
-    __slots__ = ("name", "table", "pos", "alive")
+    __slots__ = ("name", "table", "pos", "alive", "host")
 
     def __init__(self, name: str):
         self.name = name
         self.table: List[List[int]] = []  # [[page, mask], ...]
         self.pos: List[int] = []
         self.alive = True
+        self.host = None  # R15: list of saved (K, V) page bits per host slot while offloaded
 
     def length(self) -> int:
         return sum(_popcount(m) for _, m in self.table)
@@ -147,6 +157,13 @@ class Oracle:
             raise KvfsError(EBADF, f"bad fd {fd}")
         return f
 
+    def _live(self, fd: int) -> _File:
+        """A file whose pages are on the device (R15)."""
+        f = self._file(fd)
+        if f.host is not None:
+            raise KvfsError(EOFFLOAD, "offloaded")
+        return f
+
     def _new_fd(self, f: _File) -> int:
         fd = 0
         while fd in self.fds:
@@ -178,9 +195,11 @@ class Oracle:
         if f is None:
             raise KvfsError(ENOENT, name)
         for page, _ in f.table:
-            self._release(page)
+            if not page & HOST:
+                self._release(page)
         f.table = []
         f.pos = []
+        f.host = None
         f.alive = False
         del self.names[name]
 
@@ -197,7 +216,7 @@ class Oracle:
 
     def read(self, fd: int, layer: int, begin: int, end: int):
         """bf16 bits of logical tokens [begin, end): k, v of shape [n][Hkv][D]."""
-        f = self._file(fd)
+        f = self._live(fd)
         assert self.store
         if not (0 <= begin <= end <= f.length()):
             raise KvfsError(ERANGE, "read range")
@@ -219,6 +238,9 @@ class Oracle:
                 assert mask < (1 << self.P)
                 assert page not in seen, "I2: page twice in one file"
                 seen.add(page)
+                if page & HOST:
+                    assert f.host is not None and (page & ~HOST) < len(f.host), "host entry of a live file"
+                    continue
                 count[page] += 1
             assert len(f.pos) == f.length(), "positions vs length"
             assert all(a < b for a, b in zip(f.pos, f.pos[1:])), "I4: positions not increasing"
@@ -283,7 +305,7 @@ class Oracle:
         self.V[:, pages, :, sl, :] = np.asarray(v_rows).transpose(1, 0, 2, 3)
 
     def append(self, fd: int, pos: Sequence[int], k_rows=None, v_rows=None) -> None:
-        f = self._file(fd)
+        f = self._live(fd)
         if len(pos) == 0:
             return
         self._append_plan(f, pos)
@@ -293,7 +315,7 @@ class Oracle:
 
     # ------------------------------------------------------------------ R4 fork
     def fork(self, src_fd: int, dst_name: str) -> int:
-        src = self._file(src_fd)
+        src = self._live(src_fd)
         if not dst_name:
             raise KvfsError(EINVAL, "empty name")
         if dst_name in self.names:
@@ -317,7 +339,7 @@ class Oracle:
 
     # ------------------------------------------------------------------ R5 truncate
     def truncate(self, fd: int, n: int) -> None:
-        f = self._file(fd)
+        f = self._live(fd)
         length = f.length()
         if n < 0 or n > length:
             raise KvfsError(ERANGE, "truncate length")
@@ -357,7 +379,7 @@ class Oracle:
             prev_b = b
 
     def evict(self, fd: int, ranges: Sequence[Tuple[int, int]], flags: int = 0) -> None:
-        f = self._file(fd)
+        f = self._live(fd)
         self._check_ranges(f, ranges)
         drop = set()
         for a, b in ranges:
@@ -393,7 +415,7 @@ class Oracle:
             self._compact_commit(f)
 
     def compact(self, fd: int) -> None:
-        f = self._file(fd)
+        f = self._live(fd)
         length = f.length()
         if length == 0:
             return
@@ -419,6 +441,42 @@ class Oracle:
         f.table.append([new_pages[-1], (1 << (length - (k - 1) * self.P)) - 1])
         for page, _ in old:
             self._release(page)
+
+    # ------------------------------------------------------------------ R15 offload / restore
+    def host_pages(self) -> int:
+        return sum(len(f.host) for f in self.names.values() if f.host is not None)
+
+    def offload(self, fd: int) -> int:
+        """Returns the number of pages moved to the host tier."""
+        f = self._file(fd)
+        if f.host is not None:
+            raise KvfsError(EINVAL, "already offloaded")
+        f.host = []
+        for e in f.table:
+            page = e[0]
+            if self.refcnt[page] == 1:
+                f.host.append((self.K[:, page].copy(), self.V[:, page].copy()) if self.store else None)
+                e[0] = HOST | (len(f.host) - 1)
+                self._release(page)
+        return len(f.host)
+
+    def restore(self, fd: int) -> int:
+        f = self._file(fd)
+        if f.host is None:
+            raise KvfsError(EINVAL, "not offloaded")
+        n = sum(1 for page, _ in f.table if page & HOST)
+        if n > self.free_count():
+            raise KvfsError(ENOSPC, "restore")
+        for e in f.table:
+            if e[0] & HOST:
+                q = self._alloc()
+                if self.store:
+                    kk, vv = f.host[e[0] & ~HOST]
+                    self.K[:, q] = kk
+                    self.V[:, q] = vv
+                e[0] = q
+        f.host = None
+        return n
 
     # ------------------------------------------------------------------ R13 extract, R14 merge
     def _build(self, name: str, src: List[Tuple[int, int]], pos: List[int]) -> int:
@@ -446,7 +504,7 @@ class Oracle:
         return self._new_fd(f)
 
     def extract(self, src_fd: int, indices: Sequence[int], name: str) -> int:
-        f = self._file(src_fd)
+        f = self._live(src_fd)
         idx = list(indices)
         if any(b <= a for a, b in zip(idx, idx[1:])):
             raise KvfsError(EINVAL, "indices not strictly increasing")
@@ -456,7 +514,7 @@ class Oracle:
         return self._build(name, [lg[i] for i in idx], [f.pos[i] for i in idx])
 
     def merge(self, fds: Sequence[int], name: str) -> int:
-        files = [self._file(fd) for fd in fds]
+        files = [self._live(fd) for fd in fds]
         if len(set(map(id, files))) != len(files):
             raise KvfsError(EBUSY, "a part appears twice")
         toks = []
@@ -489,6 +547,10 @@ class Oracle:
                 slot_lists.append(None)
                 continue
             seen.add(id(f))
+            if f.host is not None:
+                status.append(EOFFLOAD)
+                slot_lists.append(None)
+                continue
             if nq == 0:
                 status.append(OK)
                 slot_lists.append([])

@@ -446,6 +446,18 @@ class CudaDevice final : public Device {
   }
 
   int sync() override { return cudaDeviceSynchronize() == cudaSuccess ? KVFS_OK : KVFS_EIO; }
+  int host_alloc(size_t bytes, void **host, void **dev) override {
+    if (cudaHostAlloc(host, bytes, cudaHostAllocMapped) != cudaSuccess) return KVFS_ENOMEM;
+    if (cudaHostGetDevicePointer(dev, *host, 0) != cudaSuccess) {
+      cudaFreeHost(*host);
+      return KVFS_EIO;
+    }
+    return KVFS_OK;
+  }
+  void host_free(void *host) override { cudaFreeHost(host); }
+  int stream_sync(kvfs_stream_t s) override {
+    return cudaStreamSynchronize(cs(s)) == cudaSuccess ? KVFS_OK : KVFS_EIO;
+  }
   int sms() const override { return sms_; }
   int64_t prefix_partial_capacity() const override { return lay_.prefix_cap; }
 

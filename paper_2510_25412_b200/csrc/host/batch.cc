@@ -56,6 +56,9 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
       st = KVFS_EBADF;
     } else if (f->batch_tag == tag) {
       st = KVFS_EBUSY;
+    } else if (f->offloaded) {
+      f->batch_tag = tag;
+      st = KVFS_EOFFLOAD;
     } else {
       f->batch_tag = tag;
       if (nq > 0) {

@@ -54,6 +54,7 @@ const char *kvfs_strerror(int err) {
     case KVFS_ENOSYS: return "data operation on a host-only ctx";
     case KVFS_EPOS: return "position conflict";
     case KVFS_EPARTIAL: return "some batch descriptors failed";
+    case KVFS_EOFFLOAD: return "file is offloaded to the host tier (restore it first)";
     default: return "unknown error";
   }
 }
@@ -112,6 +113,8 @@ int kvfs_destroy(kvfs_ctx *ctx) {
   Ctx *c = reinterpret_cast<Ctx *>(ctx);
   if (c->dev) {
     c->dev->sync();
+    for (auto &kv : c->names)
+      if (kv.second->host_buf) c->dev->host_free(kv.second->host_buf);
     delete c->dev;
   }
   delete c;
@@ -144,6 +147,7 @@ int kvfs_fork(kvfs_ctx *ctx, int src_fd, const char *dst_name, int *dst_fd, kvfs
   if (c.dev && c.poisoned) return KVFS_EIO;
   File *src = get_file(c, src_fd);
   if (!src) return KVFS_EBADF;
+  if (src->offloaded) return KVFS_EOFFLOAD;
   std::vector<PageCopy> copies;
   int rc = fork_file(c, *src, dst_name, dst_fd, &copies);
   if (rc != KVFS_OK) return rc;
@@ -159,6 +163,7 @@ int kvfs_truncate(kvfs_ctx *ctx, int fd, int64_t new_len) {
   KVFS_LOCK_OR(ctx);
   File *f = get_file(c, fd);
   if (!f) return KVFS_EBADF;
+  if (f->offloaded) return KVFS_EOFFLOAD;
   return truncate_file(c, *f, new_len);
 }
 
@@ -167,6 +172,7 @@ int kvfs_evict(kvfs_ctx *ctx, int fd, const int64_t *ranges, int n_ranges, int f
   if (c.dev && c.poisoned) return KVFS_EIO;
   File *f = get_file(c, fd);
   if (!f) return KVFS_EBADF;
+  if (f->offloaded) return KVFS_EOFFLOAD;
   if (flags & ~KVFS_EVICT_COMPACT) return KVFS_EINVAL;
   std::vector<Entry> old_table;
   std::vector<uint32_t> new_pages;
@@ -184,6 +190,7 @@ int kvfs_compact(kvfs_ctx *ctx, int fd, kvfs_stream_t stream) {
   if (c.dev && c.poisoned) return KVFS_EIO;
   File *f = get_file(c, fd);
   if (!f) return KVFS_EBADF;
+  if (f->offloaded) return KVFS_EOFFLOAD;
   std::vector<Entry> old_table;
   std::vector<uint32_t> new_pages;
   int rc = compact_file(c, *f, &old_table, &new_pages);
@@ -201,6 +208,7 @@ int kvfs_extract(kvfs_ctx *ctx, int src_fd, const int64_t *indices, int64_t n, c
   if (c.dev && c.poisoned) return KVFS_EIO;
   File *f = get_file(c, src_fd);
   if (!f) return KVFS_EBADF;
+  if (f->offloaded) return KVFS_EOFFLOAD;
   std::vector<int32_t> src;
   std::vector<uint32_t> pages;
   int rc = extract_file(c, *f, indices, n, name, fd, &src, &pages);
@@ -209,6 +217,57 @@ int kvfs_extract(kvfs_ctx *ctx, int src_fd, const int64_t *indices, int64_t n, c
     rc = c.dev->gather(src, pages, stream);
     if (rc != KVFS_OK) c.poisoned = true;
   }
+  return rc;
+}
+
+int kvfs_offload(kvfs_ctx *ctx, int fd, int64_t *moved, kvfs_stream_t stream) {
+  KVFS_LOCK_OR(ctx);
+  if (c.dev && c.poisoned) return KVFS_EIO;
+  File *f = get_file(c, fd);
+  if (!f) return KVFS_EBADF;
+  if (f->offloaded) return KVFS_EINVAL;
+  // host buffer first (nothing changes if it cannot be had)
+  int64_t n_ex = 0;
+  for (const Entry &e : f->table) n_ex += c.pool->refcnt(e.page) == 1;
+  const size_t page_bytes = static_cast<size_t>(c.cfg.n_kv_heads) * c.cfg.page_size * c.cfg.head_dim * 2;
+  void *hb = nullptr, *hd = nullptr;
+  if (c.dev && n_ex > 0) {
+    const int rc = c.dev->host_alloc(static_cast<size_t>(n_ex) * c.cfg.n_layers * 2 * page_bytes, &hb, &hd);
+    if (rc != KVFS_OK) return rc;
+  }
+  std::vector<uint32_t> pages;
+  int rc = offload_file(c, *f, &pages);
+  if (rc != KVFS_OK) {
+    if (hb) c.dev->host_free(hb);
+    return rc;
+  }
+  f->host_buf = hb;
+  f->host_dev = hd;
+  if (moved) *moved = static_cast<int64_t>(pages.size());
+  if (c.dev && !pages.empty()) {
+    rc = c.dev->pack_pages(pages, hd, stream);  // device pages -> host tier (mapped pinned memory)
+    if (rc != KVFS_OK) c.poisoned = true;
+  }
+  return rc;
+}
+
+int kvfs_restore(kvfs_ctx *ctx, int fd, int64_t *moved, kvfs_stream_t stream) {
+  KVFS_LOCK_OR(ctx);
+  if (c.dev && c.poisoned) return KVFS_EIO;
+  File *f = get_file(c, fd);
+  if (!f) return KVFS_EBADF;
+  void *hb = f->host_buf, *hd = f->host_dev;
+  std::vector<uint32_t> pages;
+  int rc = restore_file(c, *f, &pages);
+  if (rc != KVFS_OK) return rc;
+  f->host_buf = f->host_dev = nullptr;
+  if (moved) *moved = static_cast<int64_t>(pages.size());
+  if (c.dev && !pages.empty()) {
+    rc = c.dev->unpack_pages(pages, hd, stream);  // host tier -> fresh device pages
+    if (rc == KVFS_OK) rc = c.dev->stream_sync(stream);
+    if (rc != KVFS_OK) c.poisoned = true;
+  }
+  if (c.dev && hb) c.dev->host_free(hb);
   return rc;
 }
 
@@ -232,6 +291,7 @@ int kvfs_append(kvfs_ctx *ctx, int fd, int64_t n, const int32_t *pos, const void
   if (c.dev && c.poisoned) return KVFS_EIO;
   File *f = get_file(c, fd);
   if (!f) return KVFS_EBADF;
+  if (f->offloaded) return KVFS_EOFFLOAD;
   if (n < 0 || (n > 0 && !pos)) return KVFS_EINVAL;
   if (n == 0) return KVFS_OK;
   if (n >= (int64_t{1} << 30)) return KVFS_EINVAL;
@@ -407,6 +467,7 @@ int kvfs_read(kvfs_ctx *ctx, int fd, int layer, int64_t begin, int64_t end, void
   KVFS_LOCK_OR(ctx);
   File *f = get_file(c, fd);
   if (!f) return KVFS_EBADF;
+  if (f->offloaded) return KVFS_EOFFLOAD;
   if (!c.dev) return KVFS_ENOSYS;
   if (c.poisoned) return KVFS_EIO;
   if (layer < 0 || layer >= c.cfg.n_layers) return KVFS_EINVAL;
@@ -496,6 +557,7 @@ int kvfs_get_counter(kvfs_ctx *ctx, int counter, int64_t *value) {
     case KVFS_CTR_LAST_CHUNK_UNITS: *value = c.ctr.last_chunk_units; return KVFS_OK;
     case KVFS_CTR_LAST_PREFIX_UNITS: *value = c.ctr.last_prefix_units; return KVFS_OK;
     case KVFS_CTR_LAST_PREFIX_GROUPS: *value = c.ctr.last_prefix_groups; return KVFS_OK;
+    case KVFS_CTR_HOST_PAGES: *value = c.ctr.host_pages; return KVFS_OK;
     default: return KVFS_EINVAL;
   }
 }

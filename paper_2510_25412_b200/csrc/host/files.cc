@@ -142,7 +142,18 @@ int unlink_file(Ctx &c, const char *name) {
   auto it = c.names.find(name);
   if (it == c.names.end()) return KVFS_ENOENT;
   File &f = *it->second;
-  for (const Entry &e : f.table) c.pool->release(e.page);
+  for (const Entry &e : f.table)
+    if (!(e.page & KVFS_HOST_PAGE)) c.pool->release(e.page);
+  if (f.offloaded) {
+    c.ctr.host_pages -= f.n_host;
+    if (c.dev && f.host_buf) {
+      c.dev->sync();  // an offload copy may still be writing the buffer
+      c.dev->host_free(f.host_buf);
+    }
+    f.host_buf = f.host_dev = nullptr;
+    f.offloaded = false;
+    f.n_host = 0;
+  }
   f.table.clear();
   f.spos.clear();
   f.len = 0;
@@ -424,6 +435,7 @@ int merge_files(Ctx &c, const int *fds, int n, const char *name, int *fd, std::v
   for (int i = 0; i < n; ++i) {
     File *f = get_file(c, fds[i]);
     if (!f) return KVFS_EBADF;
+    if (f->offloaded) return KVFS_EOFFLOAD;
     parts.push_back(f);
   }
   for (int i = 0; i < n; ++i)
@@ -451,6 +463,40 @@ int merge_files(Ctx &c, const int *fds, int n, const char *name, int *fd, std::v
   return build_file(c, name, *src_slots, pos, fd, new_pages);
 }
 
+int offload_file(Ctx &c, File &f, std::vector<uint32_t> *pages) {
+  if (f.offloaded) return KVFS_EINVAL;
+  pages->clear();
+  for (Entry &e : f.table) {
+    if (c.pool->refcnt(e.page) != 1) continue;
+    pages->push_back(e.page);
+    c.pool->release(e.page);
+    e.page = KVFS_HOST_PAGE | static_cast<uint32_t>(pages->size() - 1);
+  }
+  f.offloaded = true;
+  f.n_host = static_cast<int64_t>(pages->size());
+  c.ctr.host_pages += f.n_host;
+  mark_dirty_from(f, 0);
+  return KVFS_OK;
+}
+
+int restore_file(Ctx &c, File &f, std::vector<uint32_t> *new_pages) {
+  if (!f.offloaded) return KVFS_EINVAL;
+  if (f.n_host > c.pool->n_free()) return KVFS_ENOSPC;
+  new_pages->assign(static_cast<size_t>(f.n_host), 0u);
+  for (Entry &e : f.table) {
+    if (!(e.page & KVFS_HOST_PAGE)) continue;
+    const uint32_t slot = e.page & ~KVFS_HOST_PAGE;
+    const uint32_t q = c.pool->alloc();
+    (*new_pages)[slot] = q;
+    e.page = q;
+  }
+  c.ctr.host_pages -= f.n_host;
+  f.offloaded = false;
+  f.n_host = 0;
+  mark_dirty_from(f, 0);
+  return KVFS_OK;
+}
+
 int compact_file(Ctx &c, File &f, std::vector<Entry> *old_table, std::vector<uint32_t> *new_pages) {
   const int P = c.cfg.page_size;
   if (f.len == 0) return KVFS_OK;
@@ -473,6 +519,11 @@ int audit(Ctx &c) {
       if (e.lstart != acc) return KVFS_EINVAL;
       acc += popc(e.mask);
       pages.push_back(e.page);
+      if (e.page & KVFS_HOST_PAGE) {
+        if (!f.offloaded || static_cast<int64_t>(e.page & ~KVFS_HOST_PAGE) >= f.n_host) return KVFS_EINVAL;
+        continue;
+      }
+      if (e.page >= static_cast<uint32_t>(c.pool->n_pages())) return KVFS_EINVAL;
       ++cnt[e.page];
     }
     std::sort(pages.begin(), pages.end());

@@ -34,6 +34,11 @@ struct File {
   size_t dirty_from = 0;
   std::vector<uint32_t> dirty_pts;
   int64_t batch_tag = -1;  // pred batch id that last used the file (EBUSY detection)
+  // R15 host tier: while offloaded, entries with page & KVFS_HOST_PAGE live in host_buf (pinned, mapped;
+  // host_dev = its device address), slot order = table order
+  bool offloaded = false;
+  int64_t n_host = 0;
+  void *host_buf = nullptr, *host_dev = nullptr;
 };
 using FilePtr = std::shared_ptr<File>;
 
@@ -149,7 +154,7 @@ class Device;  // data plane (csrc/cuda), absent for a host-only ctx
 
 struct CtxCounters {
   int64_t launches = 0, h2d_bytes = 0, page_copies = 0, last_decode_ctas = 0, last_chunk_units = 0,
-          last_prefix_units = 0, last_prefix_groups = 0;
+          last_prefix_units = 0, last_prefix_groups = 0, host_pages = 0;
 };
 
 struct Ctx {
@@ -197,6 +202,10 @@ int32_t last_pos(const Ctx &c, const File &f);
 void file_positions(const Ctx &c, const File &f, std::vector<int32_t> *out);
 void release_file_slab(Ctx &c, File &f);
 int audit(Ctx &c);
+// R15: mark the file's exclusive entries as host entries (in table order), release their device pages;
+// `pages` = the device pages to copy out, in host-slot order.  restore: allocate (R1, table order).
+int offload_file(Ctx &c, File &f, std::vector<uint32_t> *pages);
+int restore_file(Ctx &c, File &f, std::vector<uint32_t> *new_pages);
 
 // ---- migration (migrate.cc)
 int pack_files(Ctx &c, const int *fds, int n, std::vector<uint32_t> *pages, std::vector<uint8_t> *hdr);
@@ -229,6 +238,10 @@ class Device {
                          void *out, float *lse, float scale, kvfs_stream_t s) = 0;
   virtual int scores(const std::vector<ScoreDesc> &descs, const std::vector<ScoreUnit> &units, int layer,
                      const void *q, const float *lse, float scale, float *out, kvfs_stream_t s) = 0;
+  // pinned, device-mapped host memory for the host tier (R15)
+  virtual int host_alloc(size_t bytes, void **host, void **dev) = 0;
+  virtual void host_free(void *host) = 0;
+  virtual int stream_sync(kvfs_stream_t s) = 0;
   virtual int pack_pages(const std::vector<uint32_t> &pages, void *buf, kvfs_stream_t s) = 0;
   virtual int unpack_pages(const std::vector<uint32_t> &pages, const void *buf, kvfs_stream_t s) = 0;
   virtual int sync() = 0;

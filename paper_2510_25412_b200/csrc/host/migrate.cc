@@ -42,6 +42,7 @@ int pack_files(Ctx &c, const int *fds, int n, std::vector<uint32_t> *pages, std:
   for (int i = 0; i < n; ++i) {
     File *f = get_file(c, fds[i]);
     if (!f) return KVFS_EBADF;
+    if (f->offloaded) return KVFS_EOFFLOAD;
     if (!seen.insert(f).second) return KVFS_EBUSY;
     files.push_back(f);
   }

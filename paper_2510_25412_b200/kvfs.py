@@ -19,12 +19,13 @@ LIB_PATH = os.environ.get("KVFS_LIB_PATH") or os.path.join(_HERE, "libkvfs.so")
 
 OK, ENOENT, EIO, EBADF, ENOMEM, EBUSY, EEXIST, EINVAL, ENOSPC, ERANGE, ENOSYS = \
     0, -2, -5, -9, -12, -16, -17, -22, -28, -34, -38
-EPOS, EPARTIAL = -1001, -1002
+EPOS, EPARTIAL, EOFFLOAD = -1001, -1002, -1003
+HOST_PAGE = 0x80000000
 O_CREAT, O_EXCL = 1, 2
 EVICT_COMPACT = 1
 OPT_DECODE_CTAS, OPT_CHUNK_CUTOVER, OPT_DETERMINISTIC, OPT_CASCADE_MIN_ENTRIES = 1, 2, 3, 4
 CTR_KERNEL_LAUNCHES, CTR_H2D_BYTES, CTR_PAGE_COPIES, CTR_LAST_DECODE_CTAS, CTR_LAST_CHUNK_UNITS = 1, 2, 3, 4, 5
-CTR_LAST_PREFIX_UNITS, CTR_LAST_PREFIX_GROUPS = 6, 7
+CTR_LAST_PREFIX_UNITS, CTR_LAST_PREFIX_GROUPS, CTR_HOST_PAGES = 6, 7, 8
 
 # every symbol include/kvfs.h declares (tests check the library exports all of them)
 EXPORTS = [
@@ -34,7 +35,7 @@ EXPORTS = [
     "kvfs_get_table", "kvfs_get_positions", "kvfs_get_refcounts", "kvfs_free_pages", "kvfs_read",
     "kvfs_audit", "kvfs_set_option", "kvfs_get_counter", "kvfs_pack", "kvfs_unpack", "kvfs_extract",
     "kvfs_merge", "kvfs_sched_create", "kvfs_sched_destroy", "kvfs_sched_enqueue", "kvfs_sched_state",
-    "kvfs_sched_form", "pred_attn_scores",
+    "kvfs_sched_form", "pred_attn_scores", "kvfs_offload", "kvfs_restore",
 ]
 
 
@@ -92,6 +93,8 @@ def lib():
             "kvfs_merge": (cint, [vp, P(cint), cint, ctypes.c_char_p, P(cint), vp]),
             "kvfs_sched_create": (cint, [P(SchedConfig), P(vp)]),
             "pred_attn_scores": (cint, [vp, vp, cint, vp, vp, ctypes.c_float, vp, P(i64), vp]),
+            "kvfs_offload": (cint, [vp, cint, P(i64), vp]),
+            "kvfs_restore": (cint, [vp, cint, P(i64), vp]),
             "kvfs_sched_destroy": (cint, [vp]),
             "kvfs_sched_enqueue": (cint, [vp, cint, cint, P(i32), ctypes.c_double]),
             "kvfs_sched_state": (cint, [vp, P(ctypes.c_double), P(cint), P(cint)]),
@@ -263,6 +266,20 @@ class KVFS:
         _check(lib().kvfs_merge(self._h, _ptr(arr, ctypes.c_int32), arr.shape[0], name.encode(),
                                 ctypes.byref(fd), st), f"merge {name}")
         return fd.value
+
+    def offload(self, fd: int, stream=None) -> int:
+        """Move the file's exclusively owned pages to the host tier (R15). Returns pages moved."""
+        n = ctypes.c_int64()
+        st = _stream(stream) if self.device >= 0 else None
+        _check(lib().kvfs_offload(self._h, fd, ctypes.byref(n), st), "offload")
+        return n.value
+
+    def restore(self, fd: int, stream=None) -> int:
+        """Bring an offloaded file's host pages back into fresh device pages (R15). Returns pages moved."""
+        n = ctypes.c_int64()
+        st = _stream(stream) if self.device >= 0 else None
+        _check(lib().kvfs_restore(self._h, fd, ctypes.byref(n), st), "restore")
+        return n.value
 
     def append(self, fd: int, pos, k=None, v=None, stream=None) -> None:
         """pos: host int sequence; k, v: device bf16 tensors [L][n][Hkv][D] (None on a host-only ctx)."""

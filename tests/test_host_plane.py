@@ -123,7 +123,7 @@ def run_random(seed, n_ops=200):
     for step in range(n_ops):
         names = list(pr.fds)
         op = rnd.choice(["open", "append", "append", "fork", "truncate", "evict", "evictc", "compact", "unlink",
-                         "pred", "pred", "close_reopen", "bad", "extract", "merge"])
+                         "pred", "pred", "close_reopen", "bad", "extract", "merge", "offload", "restore"])
         if op == "open" or not names:
             name = f"n{step}"
             rc, ro, e = pr.both(lambda: c.open(name), lambda: o.open(name))
@@ -195,6 +195,16 @@ def run_random(seed, n_ops=200):
             if e is None:
                 assert rc == ro
                 pr.fds[name] = (rc, ro)
+        elif op in ("offload", "restore"):  # R15 (metadata on a host-only ctx)
+            name = rnd.choice(names)
+            cfd, ofd = pr.fds[name]
+            if op == "offload":
+                rc, ro, e = pr.both(lambda: c.offload(cfd), lambda: o.offload(ofd))
+            else:
+                rc, ro, e = pr.both(lambda: c.restore(cfd), lambda: o.restore(ofd))
+            if e is None:
+                assert rc == ro
+            assert c.counter(K.CTR_HOST_PAGES) == o.host_pages()
         elif op == "merge":
             parts = [rnd.choice(names) for _ in range(rnd.randint(1, 3))]  # repeats -> EBUSY
             name = f"n{step}"
