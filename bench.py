@@ -467,12 +467,62 @@ def run_heavy_hitter(args):
     print(json.dumps(line), flush=True)
 
 
+def run_offload(args):
+    """NEXT-3 host tier (R15): offload then restore 32 LIPs x 8192-token files of the 8B
+    attention shape (32 MiB of K+V each, exclusively owned), through the C ABI.  One JSON line: GB/s each way."""
+    import numpy as np
+    import torch
+
+    from paper_2510_25412_b200 import kvfs as K
+    from synth.configs import Shape
+    from synth.workloads import TAG_K, TAG_V, rows_torch
+
+    torch.cuda.set_device(0)
+    s, n_files, n, seed = Shape(32, 8, 128, 16), 32, 8192, 1006
+    kv = K.KVFS(1, s.Hq, s.Hkv, s.D, s.P, n_files * (n // 16) + 64, device=0)
+    dev = torch.device("cuda", 0)
+    fds = []
+    for f in range(n_files):
+        fd = kv.open(f"o{f}")
+        k = rows_torch(seed, TAG_K, 0, f, 0, n, s.Hkv * s.D, device=dev).view(1, n, s.Hkv, s.D)
+        v = rows_torch(seed, TAG_V, 0, f, 0, n, s.Hkv * s.D, device=dev).view(1, n, s.Hkv, s.D)
+        kv.append(fd, list(range(n)), k, v)
+        fds.append(fd)
+    torch.cuda.synchronize()
+    nbytes = n_files * n * s.Hkv * s.D * 2 * 2
+    res = {"offload": [], "restore": []}
+    for it in range(args.warmup + max(1, min(args.steps, 5))):
+        for what in ("offload", "restore"):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e0.record()
+            for fd in fds:
+                getattr(kv, what)(fd)
+            e1.record()
+            torch.cuda.synchronize()
+            if it >= args.warmup:
+                res[what].append((e0.elapsed_time(e1), 1000 * (time.perf_counter() - t0)))
+    off_ms = statistics.median(a for a, _ in res["offload"])
+    res_ms = statistics.median(max(a, b) for a, b in res["restore"])  # restore syncs its stream
+    line = {"metric": "KVFS host-tier offload / restore GB/s (PAPER.md P:233)", "value": nbytes / (off_ms / 1000) / 1e9,
+            "unit": "GB/s", "n_gpus": 1, "steps": len(res["offload"]), "warmup": args.warmup, "higher_is_better": True,
+            "dtype": "bf16", "data": "synthetic (seed 1006)",
+            "config": {"workload": "32 files x 8192 tokens (8B attention shape, 32 MiB K+V each), kvfs_offload then "
+                                   "kvfs_restore of every file", "bytes_each_way": nbytes},
+            "extra": {"offload_ms": off_ms, "offload_gbs": nbytes / (off_ms / 1000) / 1e9,
+                      "restore_ms": res_ms, "restore_gbs": nbytes / (res_ms / 1000) / 1e9,
+                      "path": "page-pack kernel writing / reading pinned host memory through its mapped device address"}}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "cfg5hh":
         run_heavy_hitter(args)
+    elif args.config == "offload":
+        run_offload(args)
     else:
         run_ours(args)
 

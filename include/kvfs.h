@@ -263,12 +263,12 @@ int kvfs_merge(kvfs_ctx *ctx, const int *fds, int n_fds, const char *name, int *
 /* ---------------------------------------------------------------- host tier: offload / restore
  * PAPER.md §4.3: while a thread waits on I/O, Symphony "offloads their KV caches from the GPU to the
  * CPU and restores them upon I/O completion".  Rule R15: kvfs_offload moves every page the
- * file owns EXCLUSIVELY (refcount 1) to a pinned host buffer owned by the ctx (bits of every layer, K and V,
+ * file owns EXCLUSIVELY (refcount 1) to a pinned host buffer owned by the ctx (recycled between files) (bits of every layer, K and V,
  * copied by the page-pack kernel writing through the mapped host pointer on `stream`) and frees it on the
  * device; pages shared with other files stay (another file may need them).  In the table such an entry's
  * page reads KVFS_HOST_PAGE | host slot (slots in table order).  kvfs_restore allocates device pages
  * smallest-free first in table order for those entries (ENOSPC, atomic, if too few are free), copies the
- * bits back and SYNCHRONIZES `stream` before releasing the host buffer.  While offloaded the file is
+ * bits back on `stream` (the host buffer is recycled once that copy is done; no host wait).  While offloaded the file is
  * EOFFLOAD for append / pred (per-descriptor status) / fork / truncate / evict / compact / extract / merge /
  * read / pack; stat, tables, positions, close and unlink work (unlink drops the host copy).  kvfs_offload of
  * an offloaded file, or kvfs_restore of one that is not, is EINVAL.  *moved (nullable) = pages moved. */

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <unordered_map>
 #include <vector>
 
 #include "../host/kvfs_impl.h"
@@ -232,6 +233,11 @@ class CudaDevice final : public Device {
       if (s.ev) cudaEventDestroy(s.ev);
       if (s.host) cudaFreeHost(s.host);
     }
+    for (auto &b : host_cache_) {
+      if (b.ev) cudaEventDestroy(b.ev);
+      cudaFreeHost(b.host);
+    }
+    for (auto &kv : host_sizes_) cudaFreeHost(kv.first);
   }
 
   int init() {
@@ -446,15 +452,53 @@ class CudaDevice final : public Device {
   }
 
   int sync() override { return cudaDeviceSynchronize() == cudaSuccess ? KVFS_OK : KVFS_EIO; }
+  // Host tier buffers are recycled: a released buffer is cached with an event recorded on the releasing
+  // stream (the restore that reads it may still be running) and handed out again, after that event, to an
+  // offload needing between half and all of its size.  cudaHostAlloc of pinned memory costs milliseconds.
   int host_alloc(size_t bytes, void **host, void **dev) override {
+    size_t best = host_cache_.size();
+    for (size_t i = 0; i < host_cache_.size(); ++i) {
+      const HostBuf &b = host_cache_[i];
+      if (b.bytes >= bytes && b.bytes <= 2 * bytes && (best == host_cache_.size() || b.bytes < host_cache_[best].bytes))
+        best = i;
+    }
+    if (best < host_cache_.size()) {
+      HostBuf b = host_cache_[best];
+      host_cache_.erase(host_cache_.begin() + static_cast<long>(best));
+      if (b.ev) {
+        cudaEventSynchronize(b.ev);
+        cudaEventDestroy(b.ev);
+      }
+      cached_bytes_ -= b.bytes;
+      *host = b.host;
+      *dev = b.dev;
+      host_sizes_[b.host] = b.bytes;
+      return KVFS_OK;
+    }
     if (cudaHostAlloc(host, bytes, cudaHostAllocMapped) != cudaSuccess) return KVFS_ENOMEM;
     if (cudaHostGetDevicePointer(dev, *host, 0) != cudaSuccess) {
       cudaFreeHost(*host);
       return KVFS_EIO;
     }
+    host_sizes_[*host] = bytes;
     return KVFS_OK;
   }
-  void host_free(void *host) override { cudaFreeHost(host); }
+  void host_free(void *host) override { host_release(host, nullptr); }
+  void host_release(void *host, kvfs_stream_t s) override {
+    auto it = host_sizes_.find(host);
+    if (it == host_sizes_.end()) return;
+    HostBuf b{host, nullptr, it->second, nullptr};
+    host_sizes_.erase(it);
+    cudaHostGetDevicePointer(&b.dev, host, 0);
+    if (cached_bytes_ + b.bytes > (size_t{8} << 30)) {  // keep at most 8 GiB cached
+      if (s) cudaStreamSynchronize(cs(s));
+      cudaFreeHost(host);
+      return;
+    }
+    if (s && cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming) == cudaSuccess) cudaEventRecord(b.ev, cs(s));
+    cached_bytes_ += b.bytes;
+    host_cache_.push_back(b);
+  }
   int stream_sync(kvfs_stream_t s) override {
     return cudaStreamSynchronize(cs(s)) == cudaSuccess ? KVFS_OK : KVFS_EIO;
   }
@@ -652,6 +696,14 @@ class CudaDevice final : public Device {
     const void *data;
     size_t bytes, off;
   };
+  struct HostBuf {
+    void *host, *dev;
+    size_t bytes;
+    cudaEvent_t ev;
+  };
+  std::vector<HostBuf> host_cache_;
+  std::unordered_map<void *, size_t> host_sizes_;
+  size_t cached_bytes_ = 0;
 
   Ctx &c_;
   WsLayout lay_;

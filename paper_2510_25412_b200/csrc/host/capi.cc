@@ -264,10 +264,9 @@ int kvfs_restore(kvfs_ctx *ctx, int fd, int64_t *moved, kvfs_stream_t stream) {
   if (moved) *moved = static_cast<int64_t>(pages.size());
   if (c.dev && !pages.empty()) {
     rc = c.dev->unpack_pages(pages, hd, stream);  // host tier -> fresh device pages
-    if (rc == KVFS_OK) rc = c.dev->stream_sync(stream);
     if (rc != KVFS_OK) c.poisoned = true;
   }
-  if (c.dev && hb) c.dev->host_free(hb);
+  if (c.dev && hb) c.dev->host_release(hb, stream);  // recycled once the copy on `stream` is done
   return rc;
 }
 

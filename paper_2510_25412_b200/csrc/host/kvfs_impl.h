@@ -241,6 +241,8 @@ class Device {
   // pinned, device-mapped host memory for the host tier (R15)
   virtual int host_alloc(size_t bytes, void **host, void **dev) = 0;
   virtual void host_free(void *host) = 0;
+  // return a host buffer once the work queued on `s` (reading it) is done; no host wait
+  virtual void host_release(void *host, kvfs_stream_t s) = 0;
   virtual int stream_sync(kvfs_stream_t s) = 0;
   virtual int pack_pages(const std::vector<uint32_t> &pages, void *buf, kvfs_stream_t s) = 0;
   virtual int unpack_pages(const std::vector<uint32_t> &pages, const void *buf, kvfs_stream_t s) = 0;
