@@ -208,7 +208,9 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   using namespace tc;
   using namespace tc2;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned (128B-swizzle atoms) by pointer arithmetic on the shared array itself, so the compiler
+  // keeps the shared address space (LDS / STS, not generic LD / ST)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sbase = smem_u32(smem);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR2);
   auto bar = [&](int i) { return smem_u32(bars + i); };
@@ -238,6 +240,11 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   const int n_mt = min(2, (rows_total + BM - 1) / BM - m0);  // 1 or 2 M-tiles
 
   if (threadIdx.x == 0) K2T(24, 0);
+#ifdef KVFS_K2_TRACE
+  unsigned long long gt0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
+  if (threadIdx.x == 0 && blockIdx.x < 512) g_k2_trace[1][30][blockIdx.x] = gt0;
+#endif
   if (threadIdx.x == 0) {
     mbar_init(bar(B_Q), PREFIX ? 4 * n_mt : 1);  // prefix: one arrival per softmax warp that gathers Q
     for (int s = 0; s < KV2; ++s) {
@@ -570,11 +577,17 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           for (int it = 0; it < 16; ++it) {  // (D + 2)-float rows are 8-byte aligned: float2, 2 rows per store
             const int rr = it * 2 + (lane >> 4), j = (lane & 15) * 2;
             float *d = reinterpret_cast<float *>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dst), rr));
+#ifndef KVFS_K2_NOSTORE
             if (d) *reinterpret_cast<float2 *>(d + c * 32 + j) = make_float2(buf[rr * 33 + j], buf[rr * 33 + j + 1]);
+#else
+            if (d && buf[rr * 33 + j] == 12345.f) *reinterpret_cast<float2 *>(d + c * 32 + j) = make_float2(1.f, 2.f);
+#endif
           }
           __syncwarp();
+          if (m == 0 && wq == 0 && lane == 0) K2T(28, c);
         }
         if (live) *reinterpret_cast<float2 *>(dst + HD) = make_float2(m_run, l_run);
+        if (m == 0 && wq == 0 && lane == 0) K2T(28, 4);
       } else {
       const float inv = 1.f / l_run;
       const int64_t orow = (static_cast<int64_t>(cd.row0 + qi) * p.Hq + u.g * G + h) * HD;
@@ -605,6 +618,16 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) K2T(27, 0);
+#ifdef KVFS_K2_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 512) {
+    unsigned long long gt1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
+    g_k2_trace[1][31][blockIdx.x] = gt1;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_k2_trace[1][29][blockIdx.x] = smid;
+  }
+#endif
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));

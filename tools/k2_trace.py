@@ -43,6 +43,16 @@ def main():
     if t0:
         print("CTA 0 one-off events (clk from kernel start): Q ready %d, first S ready %d, last O %d, end %d"
               % tuple(int(buf[0, e, 0]) - t0 if buf[0, e, 0] else -1 for e in (25, 14, 26, 27)))
+    if t0:
+        print("epilogue stamps (clk from start):", [int(buf[0, 28, c]) - t0 for c in range(5)])
+    st, en, sm = buf[1, 30].astype(np.int64), buf[1, 31].astype(np.int64), buf[1, 29].astype(np.int64)
+    nb = int((en > 0).sum())
+    if nb and os.environ.get("CTA_TIMES"):
+        t0 = st[:nb].min()
+        print("per-CTA start/end (us from the first start), sm:")
+        for b in range(nb):
+            print(f"  cta {b:4d} sm {sm[b]:3d} start {(st[b] - t0) / 1e3:8.2f} end {(en[b] - t0) / 1e3:8.2f} dur {(en[b] - st[b]) / 1e3:7.2f}")
+        return
     for c in range(2):
         tr = buf[c].astype(np.int64)
         n = int((tr[14] > 0).sum())
