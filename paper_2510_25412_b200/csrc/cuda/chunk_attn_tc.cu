@@ -180,7 +180,7 @@ constexpr int OFF_K2 = OFF_Q2 + 2 * tc::TILE_BYTES;         // KV2 K tiles
 constexpr int OFF_V2 = OFF_K2 + KV2 * tc::TILE_BYTES;       // KV2 V tiles
 constexpr int OFF_JCOL2 = OFF_V2 + KV2 * tc::TILE_BYTES;    // JR x BN int32
 constexpr int OFF_BAR2 = OFF_JCOL2 + JR * tc::BN * 4 + 64;  // + JR tile flags
-constexpr int N_BARS2 = 1 + 4 * KV2 + 6 + JR;
+constexpr int N_BARS2 = 1 + 4 * KV2 + 8 + JR;
 constexpr int OFF_TMEM2 = OFF_BAR2 + N_BARS2 * 8;
 constexpr int SMEM2 = OFF_TMEM2 + 16 + 1024;
 }  // namespace tc2
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   auto bar = [&](int i) { return smem_u32(bars + i); };
   // barrier indices
   constexpr int B_Q = 0, B_KF = 1, B_KE = 1 + KV2, B_VF = 1 + 2 * KV2, B_VE = 1 + 3 * KV2, B_SF = 1 + 4 * KV2,
-                B_PF = B_SF + 2, B_OF = B_PF + 2, B_JF = B_OF + 2;
+                B_PF = B_SF + 2, B_OF = B_PF + 4, B_JF = B_OF + 2;  // B_PF + 2m + half
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + OFF_TMEM2);
   int32_t *jcol_all = reinterpret_cast<int32_t *>(smem + OFF_JCOL2);
   int32_t *jflag = jcol_all + JR * BN;
@@ -255,7 +255,8 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
     }
     for (int m = 0; m < 2; ++m) {
       mbar_init(bar(B_SF + m), 1);
-      mbar_init(bar(B_PF + m), 4);
+      mbar_init(bar(B_PF + 2 * m), 4);      // P keys 0..63 written
+      mbar_init(bar(B_PF + 2 * m + 1), 4);  // P keys 64..127 written
       mbar_init(bar(B_OF + m), 1);
     }
     for (int j = 0; j < JR; ++j) mbar_init(bar(B_JF + j), 1);
@@ -393,15 +394,19 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         }
         __syncwarp();
       };
-      auto issue_pv = [&](int t, int m) {
+      // P.V in two halves of 64 keys: the first half runs on the tensor pipe while the softmax computes
+      // the exponentials of the second
+      auto issue_pv = [&](int t, int m, int half) {
         tc_fence_after();
         if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BN / 16; ++k)
+          for (int kk = 0; kk < BN / 32; ++kk) {
+            const int k = half * (BN / 32) + kk;
             mma_bf16_ts(tmem + O_COL2 + m * HD, tmem + m * BN + k * 8,
                         umma_desc(sbase + OFF_V2 + (t % KV2) * TILE_BYTES + k * 2048, HALF_BYTES, 1024), ID_O,
                         (t > 0 || k > 0));
-          mma_commit(bar(B_OF + m));
+          }
+          if (half) mma_commit(bar(B_OF + m));
         }
         __syncwarp();
       };
@@ -415,9 +420,11 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         mbar_wait(bar(B_VF + s), (t / KV2) & 1);
         if (lane == 0) K2T(9, t);
         for (int m = 0; m < n_mt; ++m) {
-          mbar_wait(bar(B_PF + m), t & 1);  // softmax m wrote P(t) into TMEM (and corrected O)
+          mbar_wait(bar(B_PF + 2 * m), t & 1);  // softmax m wrote P(t) keys 0..63 (and corrected O)
+          issue_pv(t, m, 0);
+          mbar_wait(bar(B_PF + 2 * m + 1), t & 1);  // keys 64..127
           if (lane == 0) K2T(10 + 2 * m, t);
-          issue_pv(t, m);
+          issue_pv(t, m, 1);
           if (more) {                       // in-order after PV(t): S(t+1) may overwrite P(t)'s columns
             if (m == 0) mbar_wait(bar(B_KF + (t + 1) % KV2), ((t + 1) / KV2) & 1);
             issue_s(t + 1, m);
@@ -467,6 +474,11 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       }
       float m_run = -CUDART_INF_F, l_run = 0.f;
       for (int t = 0; t < n_tiles; ++t) {
+        // The column metadata of tile t is ready long before S(t): its (~150 clk) barrier wait is taken
+        // while the tensor pipe is still computing S(t), off the critical path.
+        mbar_wait(bar(B_JF + t % JR), (t / JR) & 1);
+        const int32_t *jcol = jcol_all + (t % JR) * BN;
+        const bool vis_all = jflag[t % JR] != 0;
         mbar_wait(bar(B_SF + m), t & 1);
         if (wq == 0 && lane == 0) K2T(14 + 6 * m, t);
         tc_fence_after();
@@ -480,11 +492,10 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         }
         tmem_wait_ld();
         if (wq == 0 && lane == 0) K2T(15 + 6 * m, t);
-        mbar_wait(bar(B_JF + t % JR), (t / JR) & 1);
-        const int32_t *jcol = jcol_all + (t % JR) * BN;
+        if (m == 0 && wq == 0 && lane == 0) K2T(29, t);
         // raw-score max (scale > 0 commutes with max); masked columns -> -inf.  Four independent chains.
         float mx4[4] = {-CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F, -CUDART_INF_F};
-        if (jflag[t % JR]) {
+        if (vis_all) {
 #pragma unroll
           for (int c = 0; c < BN; ++c) mx4[c & 3] = fmaxf(mx4[c & 3], x[c]);
         } else {
@@ -497,8 +508,8 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
         mx = mx == -CUDART_INF_F ? mx : mx * p.scale_log2;
         if (wq == 0 && lane == 0) K2T(16 + 6 * m, t);
-        if (t > 0) mbar_wait(bar(B_OF + m), (t - 1) & 1);  // PV(t-1) done: O stable
-        tc_fence_after();
+        // O is stable here without waiting on B_OF: S(t) was committed after P.V(t-1) by the same thread, and a
+        // tcgen05.commit arrives only when all of that thread's earlier tcgen05 ops are complete.
         const bool need = mx > m_run + 8.f;
         if (__any_sync(0xffffffffu, need)) {
           const float mn = need ? mx : m_run;
@@ -538,15 +549,15 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
             w[i] = __uint_as_float(*reinterpret_cast<uint32_t *>(&pr));
           }
           tmem_st32(s_col + c * 32, w);
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar(B_PF + 2 * m + c));
         }
         if (wq == 0 && lane == 0) K2T(18 + 6 * m, t);
         const float2 ls2 = add2(ls4[0], ls4[1]);
         const float ls = ls2.x + ls2.y;
         l_run += ls;
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar(B_PF + m));
         if (wq == 0 && lane == 0) K2T(19 + 6 * m, t);
       }
       // epilogue: O / l -> bf16 out, lse   (prefix mode: the partial O, m, l of the split)

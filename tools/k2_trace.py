@@ -17,6 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2510_25412_b200 import kvfs  # noqa: E402
 from paper_2510_25412_b200.workloads import DecodeWorkload  # noqa: E402
 
+NAMES_EXTRA = {29: "S0:JF waited"}
 NAMES = ["K:empty", "K:issued", "V:empty", "V:issued", "M:K(t+1)", "M:SE0", "M:S0 iss", "M:SE1", "M:S1 iss",
          "M:V(t)", "M:PF0", "M:PV0 iss", "M:PF1", "M:PV1 iss"] + \
         [f"S{m}:{e}" for m in range(2) for e in ("S rdy", "S read", "max", "PE/resc", "exp done", "PF arr")]
@@ -58,7 +59,7 @@ def main():
         n = int((tr[14] > 0).sum())
         ref = tr[14, :n]
         print(f"--- CTA {'0' if c == 0 else '296'}: {n} tiles, median period {np.median(np.diff(ref[5:n - 5])):.0f} clk")
-        for e, name in enumerate(NAMES):
+        for e, name in list(enumerate(NAMES)) + list(NAMES_EXTRA.items()):
             d = tr[e, 5:n - 5] - ref[5:n - 5]
             if (tr[e, 5:n - 5] == 0).all():
                 continue
