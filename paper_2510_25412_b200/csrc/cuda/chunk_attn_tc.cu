@@ -41,7 +41,7 @@ constexpr int HALF_BYTES = BM * 64 * 2;  // one 64-column half of a [128][64] bf
 constexpr int TILE_BYTES = 2 * HALF_BYTES;  // [128][128] bf16 = 32 KiB
 constexpr int KV_STAGES = 2;
 #ifndef KVFS_EXP_EMU
-#define KVFS_EXP_EMU 3
+#define KVFS_EXP_EMU 2
 #endif
 constexpr int EXP_EMU = KVFS_EXP_EMU;  // of every 8 exp2 pairs in the softmax, how many run as a polynomial on the FMA pipe
 constexpr int THREADS = 256;
