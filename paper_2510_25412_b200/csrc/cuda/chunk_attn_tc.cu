@@ -228,6 +228,9 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   const ChunkUnit u = p.units[blockIdx.x];
   ChunkDesc cd;
   if constexpr (PREFIX) {
+    // the decode kernel that merges these partials may start now (programmatic dependent launch): it only
+    // reads them after griddepcontrol.wait, i.e. after this grid completed
+    asm volatile("griddepcontrol.launch_dependents;");
     const PrefixDesc pd = p.pdescs[u.desc];
     cd = ChunkDesc{pd.slab_off, pd.n_entries, 0, pd.n_rows, pd.row0, pd.n_entries, 0, 0};
   } else {

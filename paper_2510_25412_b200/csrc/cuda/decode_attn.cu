@@ -470,7 +470,10 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
     const int tid = warp * 32 + lane;  // 0 .. NW*32-1 within the ring
     const int unit = dd.unit_base + sg.g * dd.n_q + sg.qi;
     const int64_t row = dd.row0 + sg.qi;
-    // shared-prefix partials of this unit (written by the prefix kernel earlier on the stream)
+    // shared-prefix partials of this unit (written by the prefix kernel earlier on the stream; with a
+    // programmatic dependent launch this kernel may be running alongside it: wait for its completion here,
+    // after streaming this unit's own keys)
+    if (dd.pref_splits) asm volatile("griddepcontrol.wait;" ::: "memory");
     const float *pref = dd.pref_splits
                             ? p.ppart + (static_cast<int64_t>(dd.pref_base) +
                                          static_cast<int64_t>(sg.g * dd.n_q + sg.qi) * dd.pref_splits) * C::PART
@@ -582,7 +585,7 @@ static size_t decode_smem_bytes() {
 }
 
 template <int D, int G, int P>
-static cudaError_t launch_decode_t(const DecodeParams &p, cudaStream_t s, int *per_sm) {
+static cudaError_t launch_decode_t(const DecodeParams &p, cudaStream_t s, int *per_sm, bool pdl) {
   using C = DecodeCfg<D, G, P>;
   const size_t smem = decode_smem_bytes<C>();
   static int occ = -1;
@@ -599,42 +602,51 @@ static cudaError_t launch_decode_t(const DecodeParams &p, cudaStream_t s, int *p
     *per_sm = occ;
     return cudaSuccess;
   }
-  decode_attn_kernel<C><<<(p.ncta + C::R - 1) / C::R, C::THREADS, smem, s>>>(p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((p.ncta + C::R - 1) / C::R);
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, decode_attn_kernel<C>, p);
 }
 
 template <int D, int G>
-static cudaError_t launch_decode_p(const DecodeParams &p, int P, cudaStream_t s, int *per_sm) {
+static cudaError_t launch_decode_p(const DecodeParams &p, int P, cudaStream_t s, int *per_sm, bool pdl) {
   switch (P) {
-    case 16: return launch_decode_t<D, G, 16>(p, s, per_sm);
-    case 32: return launch_decode_t<D, G, 32>(p, s, per_sm);
-    case 64: return launch_decode_t<D, G, 64>(p, s, per_sm);
+    case 16: return launch_decode_t<D, G, 16>(p, s, per_sm, pdl);
+    case 32: return launch_decode_t<D, G, 32>(p, s, per_sm, pdl);
+    case 64: return launch_decode_t<D, G, 64>(p, s, per_sm, pdl);
     default: return cudaErrorInvalidValue;
   }
 }
 
 template <int D>
-static cudaError_t launch_decode_g(const DecodeParams &p, int G, int P, cudaStream_t s, int *per_sm) {
+static cudaError_t launch_decode_g(const DecodeParams &p, int G, int P, cudaStream_t s, int *per_sm, bool pdl) {
   switch (G) {
-    case 1: return launch_decode_p<D, 1>(p, P, s, per_sm);
-    case 2: return launch_decode_p<D, 2>(p, P, s, per_sm);
-    case 4: return launch_decode_p<D, 4>(p, P, s, per_sm);
-    case 8: return launch_decode_p<D, 8>(p, P, s, per_sm);
+    case 1: return launch_decode_p<D, 1>(p, P, s, per_sm, pdl);
+    case 2: return launch_decode_p<D, 2>(p, P, s, per_sm, pdl);
+    case 4: return launch_decode_p<D, 4>(p, P, s, per_sm, pdl);
+    case 8: return launch_decode_p<D, 8>(p, P, s, per_sm, pdl);
     default: return cudaErrorInvalidValue;
   }
 }
 
-cudaError_t launch_decode(const DecodeParams &p, int D, int G, int P, cudaStream_t s) {
-  if (D == 64) return launch_decode_g<64>(p, G, P, s, nullptr);
-  if (D == 128) return launch_decode_g<128>(p, G, P, s, nullptr);
+cudaError_t launch_decode(const DecodeParams &p, int D, int G, int P, cudaStream_t s, bool pdl) {
+  if (D == 64) return launch_decode_g<64>(p, G, P, s, nullptr, pdl);
+  if (D == 128) return launch_decode_g<128>(p, G, P, s, nullptr, pdl);
   return cudaErrorInvalidValue;
 }
 
 int decode_ctas_per_sm(int D, int G, int P) {
   int o = 1;
   DecodeParams dummy{};
-  if (D == 64) launch_decode_g<64>(dummy, G, P, nullptr, &o);
-  if (D == 128) launch_decode_g<128>(dummy, G, P, nullptr, &o);
+  if (D == 64) launch_decode_g<64>(dummy, G, P, nullptr, &o, false);
+  if (D == 128) launch_decode_g<128>(dummy, G, P, nullptr, &o, false);
   return o;
 }
 

@@ -445,7 +445,8 @@ class CudaDevice final : public Device {
     p.counters = counters_;
     p.Hq = cfg.n_q_heads;
     p.Hkv = cfg.n_kv_heads;
-    const cudaError_t e = dev::launch_decode(p, cfg.head_dim, cfg.n_q_heads / cfg.n_kv_heads, cfg.page_size, cs(s));
+    const cudaError_t e = dev::launch_decode(p, cfg.head_dim, cfg.n_q_heads / cfg.n_kv_heads, cfg.page_size, cs(s),
+                                             !pl.prefix_units.empty());
     ++c_.ctr.launches;
     c_.ctr.last_decode_ctas = ncta;
     return e == cudaSuccess ? KVFS_OK : KVFS_EIO;

@@ -27,7 +27,8 @@ struct DecodeParams {
   int Hq, Hkv;
 };
 
-cudaError_t launch_decode(const DecodeParams &p, int D, int G, int P, cudaStream_t s);
+// pdl: programmatic dependent launch after the shared-prefix kernel (the kernel waits for it before merging)
+cudaError_t launch_decode(const DecodeParams &p, int D, int G, int P, cudaStream_t s, bool pdl = false);
 // ---- K2 (tcgen05 chunk attention, D = 128)
 struct ChunkDesc {  // == kvfs::ChunkDesc
   int32_t slab_off, n_entries, n_old, n_q, row0, first_new_entry, first_new_lstart, pad;
