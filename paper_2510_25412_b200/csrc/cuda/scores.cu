@@ -24,17 +24,19 @@ __global__ void __launch_bounds__(256) scores_kernel(const ScoreUnit *units, con
                                                      int Hkv, int P) {
   constexpr int DPL = D / 8;   // dims per lane
   constexpr int CH = DPL / 8;  // 16-byte chunks per lane
-  constexpr int UNR = 4;       // warp steps (4 keys each) in flight
+  constexpr int NS = 8;        // ring stages per warp (4 key rows each)
   __shared__ float acc[32 * 64];  // [entry][slot]
   __shared__ uint64_t emask[32];
   __shared__ uint32_t epage[32];
   __shared__ int32_t elog[32];
   __shared__ int16_t kslot[32 * 64];  // retained keys of the unit: (entry << 8) | slot, logical order
   __shared__ int nkeys;
+  extern __shared__ __align__(16) uint32_t ring_all[];  // [8 warps][NS][32 lanes][DPL bf16]
   const ScoreUnit u = units[blockIdx.x];
   const ScoreDesc d = descs[u.desc];
   const int ne = u.e1 - u.e0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t *ring = ring_all + warp * NS * 32 * (DPL * 2 / 4);
   if (warp == 0) {
     uint64_t m = 0;
     uint32_t pg = 0;
@@ -85,50 +87,63 @@ __global__ void __launch_bounds__(256) scores_kernel(const ScoreUnit *units, con
 #pragma unroll
     for (int h = 0; h < G; ++h) l2[h] = lse[static_cast<int64_t>(row) * (Hkv * G) + g * G + h] * 1.4426950408889634f;
     const int vis = min(n, base + r + 1);  // unit-relative keys visible to this row
-    for (int k0 = kset * 4; k0 < vis; k0 += nsets * 4 * UNR) {
-      uint4 kr[UNR][CH];
-#pragma unroll
-      for (int s = 0; s < UNR; ++s) {
-        const int key = k0 + s * nsets * 4 + kg;
+    // warp-private ring of NS stages of 4 key rows (cp.async, 16 B per lane per chunk): NS - 1 steps in
+    // flight while one is computed
+    const int n_steps = vis > kset * 4 ? (vis - kset * 4 + nsets * 4 - 1) / (nsets * 4) : 0;
+    auto issue = [&](int step) {
+      if (step < n_steps) {
+        const int key = kset * 4 + step * nsets * 4 + kg;
         if (key < vis) {
           const int ks = kslot[key], e = ks >> 8, slot = ks & 255;
-          const uint4 *src = reinterpret_cast<const uint4 *>(
-                                 kpool + ((static_cast<int64_t>(epage[e]) * Hkv + g) * P + slot) * D) + sub * CH;
+          const char *src = reinterpret_cast<const char *>(
+              kpool + ((static_cast<int64_t>(epage[e]) * Hkv + g) * P + slot) * D + sub * DPL);
+          const uint32_t dst = smem_u32(ring + ((step % NS) * 32 + lane) * (DPL * 2 / 4));
 #pragma unroll
-          for (int c = 0; c < CH; ++c) kr[s][c] = __ldg(src + c);
+          for (int c = 0; c < CH; ++c)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 16), "l"(src + c * 16) : "memory");
         }
       }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
 #pragma unroll
-      for (int s = 0; s < UNR; ++s) {
-        const int key = k0 + s * nsets * 4 + kg;
-        float dot[G];
+    for (int st = 0; st < NS - 1; ++st) issue(st);
+    for (int step = 0; step < n_steps; ++step) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2) : "memory");
+      __syncwarp();
+      const int key = kset * 4 + step * nsets * 4 + kg;
+      float dot[G];
 #pragma unroll
-        for (int h = 0; h < G; ++h) dot[h] = 0.f;
-        if (key < vis) {
+      for (int h = 0; h < G; ++h) dot[h] = 0.f;
+      if (key < vis) {
+        const uint4 *kr = reinterpret_cast<const uint4 *>(ring + ((step % NS) * 32 + lane) * (DPL * 2 / 4));
 #pragma unroll
-          for (int c = 0; c < CH; ++c) {
-            const uint32_t ws[4] = {kr[s][c].x, kr[s][c].y, kr[s][c].z, kr[s][c].w};
+        for (int c = 0; c < CH; ++c) {
+          const uint4 w = kr[c];
+          const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float2 kf = bf2_to_f2(ws[j]);
+          for (int j = 0; j < 4; ++j) {
+            const float2 kf = bf2_to_f2(ws[j]);
 #pragma unroll
-              for (int h = 0; h < G; ++h) dot[h] = fmaf(qf[h][c * 4 + j].x, kf.x, fmaf(qf[h][c * 4 + j].y, kf.y, dot[h]));
-            }
+            for (int h = 0; h < G; ++h) dot[h] = fmaf(qf[h][c * 4 + j].x, kf.x, fmaf(qf[h][c * 4 + j].y, kf.y, dot[h]));
           }
         }
+      }
+      __syncwarp();  // the stage is consumed: it may be refilled
+      issue(step + NS - 1);
 #pragma unroll
-        for (int h = 0; h < G; ++h)
+      for (int h = 0; h < G; ++h)
 #pragma unroll
-          for (int o = 1; o < 8; o <<= 1) dot[h] += __shfl_xor_sync(0xffffffffu, dot[h], o);
-        if (sub == 0 && key < vis) {
-          float sum = 0.f;
+        for (int o = 1; o < 8; o <<= 1) dot[h] += __shfl_xor_sync(0xffffffffu, dot[h], o);
+      if (sub == 0 && key < vis) {
+        float sum = 0.f;
 #pragma unroll
-          for (int h = 0; h < G; ++h) sum += exp2f(dot[h] - l2[h]);
-          const int ks = kslot[key];
-          atomicAdd(&acc[(ks >> 8) * 64 + (ks & 255)], sum);
-        }
+        for (int h = 0; h < G; ++h) sum += exp2f(dot[h] - l2[h]);
+        const int ks = kslot[key];
+        atomicAdd(&acc[(ks >> 8) * 64 + (ks & 255)], sum);
       }
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
   }
   __syncthreads();
   for (int t = threadIdx.x; t < n; t += blockDim.x) {
@@ -142,7 +157,14 @@ template <int D, int G>
 static cudaError_t launch_scores_t(const ScoreUnit *units, int n_units, const ScoreDesc *descs, const Entry *slab,
                                    const __nv_bfloat16 *q, const float *lse, const __nv_bfloat16 *kpool,
                                    float scale_log2, float *out, int Hkv, int P, cudaStream_t s) {
-  scores_kernel<D, G><<<n_units, 256, 0, s>>>(units, descs, slab, q, lse, kpool, scale_log2, out, Hkv, P);
+  constexpr int smem = 8 * 8 * 32 * (D / 8) * 2;  // 8 warps x NS stages x 32 lanes x DPL bf16
+  static bool attr = false;
+  if (!attr && smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(scores_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  scores_kernel<D, G><<<n_units, 256, smem, s>>>(units, descs, slab, q, lse, kpool, scale_log2, out, Hkv, P);
   return cudaGetLastError();
 }
 
