@@ -46,6 +46,13 @@ constexpr int KV_STAGES = 2;
 constexpr int EXP_EMU = KVFS_EXP_EMU;  // of every 8 exp2 pairs in the softmax, how many run as a polynomial on the FMA pipe
 constexpr int THREADS = 256;
 constexpr uint32_t TMEM_COLS = 512;
+#ifndef KVFS_K2_SELF_ISSUE
+#define KVFS_K2_SELF_ISSUE 0
+#endif
+// 1 = each softmax group's warp 0 issues its own MMAs after a group barrier (no MMA warp): measured slower
+// (period 4.5k vs 3.2k clk, tools/k2_trace.py) because the two groups fall into phase and the ping-pong of
+// softmax and tensor work between the M-tiles is lost; kept as a switch for the record.
+constexpr bool K2_SELF_ISSUE = KVFS_K2_SELF_ISSUE != 0;
 constexpr uint32_t S_COL0 = 0, O_COL = 256;
 
 // shared memory layout (all tiles 1024-B aligned for the 128B swizzle)
@@ -252,9 +259,9 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
     mbar_init(bar(B_Q), PREFIX ? 4 * n_mt : 1);  // prefix: one arrival per softmax warp that gathers Q
     for (int s = 0; s < KV2; ++s) {
       mbar_init(bar(B_KF + s), 1);
-      mbar_init(bar(B_KE + s), 1);
+      mbar_init(bar(B_KE + s), K2_SELF_ISSUE ? n_mt : 1);
       mbar_init(bar(B_VF + s), 1);
-      mbar_init(bar(B_VE + s), 1);
+      mbar_init(bar(B_VE + s), K2_SELF_ISSUE ? n_mt : 1);
     }
     for (int m = 0; m < 2; ++m) {
       mbar_init(bar(B_SF + m), 1);
@@ -278,6 +285,38 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   if (*tmem_slot != 0u) __trap();
   constexpr uint32_t tmem = 0;
 
+  // MMA issue helpers (one elected lane of the calling warp; K2_SELF_ISSUE: warp 0 of each softmax group
+  // issues its own M-tile's MMAs right after a group barrier, instead of signalling a separate MMA warp)
+  constexpr uint32_t ID_S = idesc_bf16(false), ID_O = idesc_bf16(true);
+    auto issue_s = [&](int t, int m) {
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int k = 0; k < HD / 16; ++k) {
+          const uint32_t koff = (k >> 2) * HALF_BYTES + (k & 3) * 32;
+          mma_bf16(tmem + m * BN, umma_desc(sbase + OFF_Q2 + m * TILE_BYTES + koff, 16, 1024),
+                   umma_desc(sbase + OFF_K2 + (t % KV2) * TILE_BYTES + koff, 16, 1024), ID_S, k > 0);
+        }
+        mma_commit(bar(B_SF + m));
+      }
+      __syncwarp();
+    };
+    // P.V in two halves of 64 keys: the first half runs on the tensor pipe while the softmax computes
+    // the exponentials of the second
+    auto issue_pv = [&](int t, int m, int half) {
+      tc_fence_after();
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < BN / 32; ++kk) {
+          const int k = half * (BN / 32) + kk;
+          mma_bf16_ts(tmem + O_COL2 + m * HD, tmem + m * BN + k * 8,
+                      umma_desc(sbase + OFF_V2 + (t % KV2) * TILE_BYTES + k * 2048, HALF_BYTES, 1024), ID_O,
+                      (t > 0 || k > 0));
+        }
+        if (half) mma_commit(bar(B_OF + m));
+      }
+      __syncwarp();
+    };
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
     if (warp == 0) {
@@ -379,40 +418,10 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         }
         __syncwarp();
       }
-    } else if (warp == 1) {
+    } else if (warp == 1 && !K2_SELF_ISSUE) {
       // ============================================================ MMA issuer
-      constexpr uint32_t ID_S = idesc_bf16(false), ID_O = idesc_bf16(true);
       mbar_wait(bar(B_Q), 0);
       if (lane == 0) K2T(25, 0);
-      auto issue_s = [&](int t, int m) {
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int k = 0; k < HD / 16; ++k) {
-            const uint32_t koff = (k >> 2) * HALF_BYTES + (k & 3) * 32;
-            mma_bf16(tmem + m * BN, umma_desc(sbase + OFF_Q2 + m * TILE_BYTES + koff, 16, 1024),
-                     umma_desc(sbase + OFF_K2 + (t % KV2) * TILE_BYTES + koff, 16, 1024), ID_S, k > 0);
-          }
-          mma_commit(bar(B_SF + m));
-        }
-        __syncwarp();
-      };
-      // P.V in two halves of 64 keys: the first half runs on the tensor pipe while the softmax computes
-      // the exponentials of the second
-      auto issue_pv = [&](int t, int m, int half) {
-        tc_fence_after();
-        if (elect_one()) {
-#pragma unroll
-          for (int kk = 0; kk < BN / 32; ++kk) {
-            const int k = half * (BN / 32) + kk;
-            mma_bf16_ts(tmem + O_COL2 + m * HD, tmem + m * BN + k * 8,
-                        umma_desc(sbase + OFF_V2 + (t % KV2) * TILE_BYTES + k * 2048, HALF_BYTES, 1024), ID_O,
-                        (t > 0 || k > 0));
-          }
-          if (half) mma_commit(bar(B_OF + m));
-        }
-        __syncwarp();
-      };
       mbar_wait(bar(B_KF + 0), 0);
       for (int m = 0; m < n_mt; ++m) issue_s(0, m);
       if (elect_one()) mma_commit(bar(B_KE + 0));
@@ -476,6 +485,13 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         if (lane == 0) mbar_arrive(bar(B_Q));
       }
       float m_run = -CUDART_INF_F, l_run = 0.f;
+      if (K2_SELF_ISSUE && wq == 0) {
+        mbar_wait(bar(B_Q), 0);
+        mbar_wait(bar(B_KF + 0), 0);
+        issue_s(0, m);
+        if (elect_one()) mma_commit(bar(B_KE + 0));
+        __syncwarp();
+      }
       for (int t = 0; t < n_tiles; ++t) {
         // The column metadata of tile t is ready long before S(t): its (~150 clk) barrier wait is taken
         // while the tensor pipe is still computing S(t), off the critical path.
@@ -554,8 +570,31 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           tmem_st32(s_col + c * 32, w);
           tmem_wait_st();
           tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(bar(B_PF + 2 * m + c));
+          if constexpr (K2_SELF_ISSUE) {
+            named_bar_sync(1 + m, 128);  // the group's P half is in TMEM
+            if (wq == 0) {
+              const int s = t % KV2;
+              if (c == 0) {
+                mbar_wait(bar(B_VF + s), (t / KV2) & 1);
+                issue_pv(t, m, 0);
+              } else {
+                issue_pv(t, m, 1);
+                const bool more = t + 1 < n_tiles;
+                if (more) {  // in order after P.V(t): S(t+1) may overwrite P(t)'s columns
+                  mbar_wait(bar(B_KF + (t + 1) % KV2), ((t + 1) / KV2) & 1);
+                  issue_s(t + 1, m);
+                }
+                if (elect_one()) {
+                  if (more) mma_commit(bar(B_KE + (t + 1) % KV2));
+                  mma_commit(bar(B_VE + s));
+                }
+                __syncwarp();
+              }
+            }
+          } else {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(bar(B_PF + 2 * m + c));
+          }
         }
         if (wq == 0 && lane == 0) K2T(18 + 6 * m, t);
         const float2 ls2 = add2(ls4[0], ls4[1]);
