@@ -53,6 +53,12 @@ constexpr uint32_t TMEM_COLS = 512;
 // (period 4.5k vs 3.2k clk, tools/k2_trace.py) because the two groups fall into phase and the ping-pong of
 // softmax and tensor work between the M-tiles is lost; kept as a switch for the record.
 constexpr bool K2_SELF_ISSUE = KVFS_K2_SELF_ISSUE != 0;
+// waits on the softmax <-> MMA handoff barriers: plain try_wait loop, or with a suspend-time hint
+#ifdef KVFS_K2_SLEEPWAIT
+#define K2_WAIT(b, ph) mbar_wait_sleep(b, ph)
+#else
+#define K2_WAIT(b, ph) mbar_wait(b, ph)
+#endif
 constexpr uint32_t S_COL0 = 0, O_COL = 256;
 
 // shared memory layout (all tiles 1024-B aligned for the 128B swizzle)
@@ -432,9 +438,9 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         mbar_wait(bar(B_VF + s), (t / KV2) & 1);
         if (lane == 0) K2T(9, t);
         for (int m = 0; m < n_mt; ++m) {
-          mbar_wait(bar(B_PF + 2 * m), t & 1);  // softmax m wrote P(t) keys 0..63 (and corrected O)
+          K2_WAIT(bar(B_PF + 2 * m), t & 1);  // softmax m wrote P(t) keys 0..63 (and corrected O)
           issue_pv(t, m, 0);
-          mbar_wait(bar(B_PF + 2 * m + 1), t & 1);  // keys 64..127
+          K2_WAIT(bar(B_PF + 2 * m + 1), t & 1);  // keys 64..127
           if (lane == 0) K2T(10 + 2 * m, t);
           issue_pv(t, m, 1);
           if (more) {                       // in-order after PV(t): S(t+1) may overwrite P(t)'s columns
@@ -498,7 +504,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         mbar_wait(bar(B_JF + t % JR), (t / JR) & 1);
         const int32_t *jcol = jcol_all + (t % JR) * BN;
         const bool vis_all = jflag[t % JR] != 0;
-        mbar_wait(bar(B_SF + m), t & 1);
+        K2_WAIT(bar(B_SF + m), t & 1);
         if (wq == 0 && lane == 0) K2T(14 + 6 * m, t);
         tc_fence_after();
         float x[BN];
