@@ -135,7 +135,7 @@ class DecodeWorkload:
     def flops(self) -> int:
         s = self.shape
         n = self.n_q
-        return int(sum(4 * s.Hq * s.D * (n * int(ln) + n * (n + 1) // 2) for ln in self.lens))
+        return int(4 * s.Hq * s.D * (n * int(self.lens.sum()) + self.n_files * (n * (n + 1) // 2)))
 
     def dominant_kernel(self) -> str:
         if self.n_q >= 8:
