@@ -241,9 +241,6 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   const ChunkUnit u = p.units[blockIdx.x];
   ChunkDesc cd;
   if constexpr (PREFIX) {
-    // the decode kernel that merges these partials may start now (programmatic dependent launch): it only
-    // reads them after griddepcontrol.wait, i.e. after this grid completed
-    asm volatile("griddepcontrol.launch_dependents;");
     const PrefixDesc pd = p.pdescs[u.desc];
     cd = ChunkDesc{pd.slab_off, pd.n_entries, 0, pd.n_rows, pd.row0, pd.n_entries, 0, 0};
   } else {
@@ -289,6 +286,14 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   // The CTA owns all 512 TMEM columns (one CTA per SM), so the allocation starts at lane 0, column 0.  The
   // constant keeps every tcgen05 operand a compile-time uniform value (no R2UR waterfall per MMA).
   if (*tmem_slot != 0u) __trap();
+  if constexpr (PREFIX) {
+    // Programmatic dependent launch: this grid may start while the table-delta prologue still runs (the
+    // setup above overlaps it); wait for it before any page-table read, then let the decode kernel that
+    // merges these partials start (it reads them only after its own griddepcontrol.wait, i.e. after this
+    // grid completed; the prologue's writes are complete and visible by then)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+  }
   constexpr uint32_t tmem = 0;
 
   // MMA issue helpers (one elected lane of the calling warp; K2_SELF_ISSUE: warp 0 of each softmax group
@@ -742,8 +747,17 @@ static cudaError_t launch_chunk_g(const CUtensorMap &km, const CUtensorMap &vm, 
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  chunk_attn_tc_kernel<G, PREFIX><<<n_units, tc2::THREADS, tc2::SMEM2, s>>>(km, vm, qm, p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(n_units);
+  cfg.blockDim = dim3(tc2::THREADS);
+  cfg.dynamicSmemBytes = tc2::SMEM2;
+  cfg.stream = s;
+  cudaLaunchAttribute la[1];
+  la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[0].val.programmaticStreamSerializationAllowed = PREFIX ? 1 : 0;  // prefix mode waits in-kernel
+  cfg.attrs = la;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, chunk_attn_tc_kernel<G, PREFIX>, km, vm, qm, p);
 }
 
 template <bool PREFIX>

@@ -178,6 +178,9 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
     fence_mbar_init();
   }
   __syncthreads();
+  // launched programmatically after the table-delta prologue (no shared-prefix kernel in between): the
+  // setup above overlapped its tail; wait for it before reading the page tables
+  if (p.wait_at_start) asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t beg = cta < p.ncta ? cta_start(cta, p.total, p.ncta) : 0;
   const int64_t end = cta < p.ncta ? cta_start(cta + 1, p.total, p.ncta) : 0;
 

@@ -62,6 +62,9 @@ using bf16 = __nv_bfloat16;
 __global__ void prologue_kernel(const dev::SlabRun *runs, int n_runs, const dev::Entry *run_entries,
                                 dev::Entry *slab, const dev::PageCopy *copies, int n_copies, bf16 *const *kp,
                                 bf16 *const *vp, int L, int64_t page_elems) {
+  // the next kernel (decode / shared-prefix, launched programmatically) may start its setup now; it waits
+  // (griddepcontrol.wait) for this grid's completion before reading the tables
+  asm volatile("griddepcontrol.launch_dependents;");
   const int run_blocks = (n_runs + 7) / 8;
   if (static_cast<int>(blockIdx.x) < run_blocks) {
     const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
@@ -442,11 +445,14 @@ class CudaDevice final : public Device {
     p.scale_log2 = scale * 1.4426950408889634f;
     p.partials = partials_;
     p.ppart = ppart_;
+    p.wait_at_start = pl.prefix_units.empty() ? 1 : 0;
     p.counters = counters_;
     p.Hq = cfg.n_q_heads;
     p.Hkv = cfg.n_kv_heads;
+    // always a programmatic dependent launch: after the prologue (waits at start) or after the shared-prefix
+    // kernel (which waited for the prologue itself; waits before merging)
     const cudaError_t e = dev::launch_decode(p, cfg.head_dim, cfg.n_q_heads / cfg.n_kv_heads, cfg.page_size, cs(s),
-                                             !pl.prefix_units.empty());
+                                             true);
     ++c_.ctr.launches;
     c_.ctr.last_decode_ctas = ncta;
     return e == cudaSuccess ? KVFS_OK : KVFS_EIO;

@@ -23,6 +23,7 @@ struct DecodeParams {
   float scale_log2;  // scale * log2(e)
   float *partials;   // [ncta][2][PART]
   const float *ppart;  // shared-prefix partials [..][PART] (Desc::pref_*)
+  int wait_at_start;   // 1: griddepcontrol.wait before reading the tables (programmatic launch after the prologue)
   int *counters;     // [n_units]
   int Hq, Hkv;
 };
