@@ -39,12 +39,10 @@ constexpr int BN = 128;   // keys per KV tile
 constexpr int HD = 128;   // head dim (K2 is specialised for D = 128)
 constexpr int HALF_BYTES = BM * 64 * 2;  // one 64-column half of a [128][64] bf16 SW128 tile = 16 KiB
 constexpr int TILE_BYTES = 2 * HALF_BYTES;  // [128][128] bf16 = 32 KiB
-constexpr int KV_STAGES = 2;
 #ifndef KVFS_EXP_EMU
 #define KVFS_EXP_EMU 2
 #endif
 constexpr int EXP_EMU = KVFS_EXP_EMU;  // of every 8 exp2 pairs in the softmax, how many run as a polynomial on the FMA pipe
-constexpr int THREADS = 256;
 constexpr uint32_t TMEM_COLS = 512;
 #ifndef KVFS_K2_SELF_ISSUE
 #define KVFS_K2_SELF_ISSUE 0
@@ -59,20 +57,6 @@ constexpr bool K2_SELF_ISSUE = KVFS_K2_SELF_ISSUE != 0;
 #else
 #define K2_WAIT(b, ph) mbar_wait(b, ph)
 #endif
-constexpr uint32_t S_COL0 = 0, O_COL = 256;
-
-// shared memory layout (all tiles 1024-B aligned for the 128B swizzle)
-constexpr int OFF_Q = 0;
-constexpr int OFF_P = OFF_Q + TILE_BYTES;
-constexpr int OFF_K = OFF_P + TILE_BYTES;                  // [KV_STAGES] K tiles
-constexpr int OFF_V = OFF_K + KV_STAGES * TILE_BYTES;      // [KV_STAGES] V tiles
-constexpr int OFF_JCOL = OFF_V + KV_STAGES * TILE_BYTES;   // [KV_STAGES][BN] int32 column metadata
-constexpr int OFF_BAR = OFF_JCOL + KV_STAGES * BN * 4;
-// barriers: q_full, kv_full[S], kv_empty[S], s_full[2], s_empty[2], p_full, o_full
-constexpr int N_BARS = 1 + 2 * KV_STAGES + 2 + 2 + 1 + 1;
-constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
-constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + alignment slack
-
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
