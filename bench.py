@@ -259,38 +259,70 @@ def run_ours(args):
     ms_step = ms_max / Kst
     value = world * T * Kst / (ms_max / 1000.0)
 
-    # ---- end to end: host (pinned) inputs -> H2D -> pred through the C ABI -> D2H of out + lse, every step
+    # ---- end to end: host (pinned) inputs -> H2D -> pred through the C ABI -> D2H of out + lse, every step.
+    # Pipelined like a serving loop: the H2D of step i+1 (copy stream) and the D2H of step i-1 (second copy
+    # stream) overlap the pred of step i (compute stream); double-buffered device inputs / outputs, ordered
+    # by events.  Every step still moves its full inputs in and its full result out inside the timed region.
     e2e = None
     if n_e2e:
         ring = [tuple(x.cpu().pin_memory() for x in inputs[i % len(inputs)]) for i in range(4)]
-        qd, kd, vd = (torch.empty_like(x) for x in inputs[0])
-        out_h = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
-        lse_h = torch.empty(lse.shape, dtype=lse.dtype, pin_memory=True)
+        dev_in = [tuple(torch.empty_like(x) for x in inputs[0]) for _ in range(2)]
+        dev_out = [(torch.empty_like(out), torch.empty_like(lse)) for _ in range(2)]
+        host_out = [(torch.empty(out.shape, dtype=out.dtype, pin_memory=True),
+                     torch.empty(lse.shape, dtype=lse.dtype, pin_memory=True)) for _ in range(2)]
+        cs = torch.cuda.current_stream()
+        h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
+        ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "used", "done", "d2h")}
         torch.cuda.synchronize()
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
+        e0.record(cs)
+        h2d_s.wait_stream(cs)
+        d2h_s.wait_stream(cs)
+
+        def issue_h2d(i):
+            b = i % 2
+            with torch.cuda.stream(h2d_s):
+                if i >= 2:
+                    h2d_s.wait_event(ev["used"][b])  # pred i-2 finished reading buffer b
+                for d, hsrc in zip(dev_in[b], ring[i % 4]):
+                    d.copy_(hsrc, non_blocking=True)
+                ev["in"][b].record(h2d_s)
+
+        issue_h2d(0)
         for i in range(n_e2e):
-            hq, hk, hv = ring[i % 4]
+            b = i % 2
+            if i + 1 < n_e2e:
+                issue_h2d(i + 1)
+            cs.wait_event(ev["in"][b])
+            if i >= 2:
+                cs.wait_event(ev["d2h"][b])  # the D2H of step i-2 has read output buffer b
             wl.pre_step()
-            qd.copy_(hq, non_blocking=True)
-            kd.copy_(hk, non_blocking=True)
-            vd.copy_(hv, non_blocking=True)
-            kv.pred_attn_batch(wl.descs, wl.positions(), qd, kd, vd, out, lse)
-            out_h.copy_(out, non_blocking=True)
-            lse_h.copy_(lse, non_blocking=True)
+            qd, kd, vd = dev_in[b]
+            kv.pred_attn_batch(wl.descs, wl.positions(), qd, kd, vd, dev_out[b][0], dev_out[b][1])
+            ev["used"][b].record(cs)
+            ev["done"][b].record(cs)
+            with torch.cuda.stream(d2h_s):
+                d2h_s.wait_event(ev["done"][b])
+                host_out[b][0].copy_(dev_out[b][0], non_blocking=True)
+                host_out[b][1].copy_(dev_out[b][1], non_blocking=True)
+                ev["d2h"][b].record(d2h_s)
             wl.advance()
-        e1.record()
+        cs.wait_stream(d2h_s)
+        cs.wait_stream(h2d_s)
+        e1.record(cs)
         torch.cuda.synchronize()
         et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         h2d_b = sum(x.numel() * x.element_size() for x in ring[0])
-        d2h_b = out_h.numel() * out_h.element_size() + lse_h.numel() * lse_h.element_size()
+        d2h_b = sum(x.numel() * x.element_size() for x in host_out[0])
         e2e = {"value": world * T * n_e2e / (float(et.item()) / 1000.0), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b, "steps": n_e2e,
-               "note": "pinned host Q/K_new/V_new -> device, pred_attn_batch via the C ABI, out+lse -> pinned host"}
+               "note": "pinned host Q/K_new/V_new -> device (copy stream), pred_attn_batch via the C ABI "
+                       "(compute stream), out+lse -> pinned host (second copy stream); steps pipelined with "
+                       "double-buffered device inputs / outputs"}
 
     if rank != 0:
         if world > 1:
