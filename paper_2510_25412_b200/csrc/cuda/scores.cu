@@ -107,39 +107,57 @@ __global__ void __launch_bounds__(256) scores_kernel(const ScoreUnit *units, con
     };
 #pragma unroll
     for (int st = 0; st < NS - 1; ++st) issue(st);
-    for (int step = 0; step < n_steps; ++step) {
-      asm volatile("cp.async.wait_group %0;" ::"n"(NS - 2) : "memory");
+    // two steps per iteration (independent dot chains), packed fp32x2 FMAs
+    for (int step = 0; step < n_steps; step += 2) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(NS - 3) : "memory");
       __syncwarp();
-      const int key = kset * 4 + step * nsets * 4 + kg;
-      float dot[G];
+      float2 dot2[2][G];
+      int keys[2];
 #pragma unroll
-      for (int h = 0; h < G; ++h) dot[h] = 0.f;
-      if (key < vis) {
-        const uint4 *kr = reinterpret_cast<const uint4 *>(ring + ((step % NS) * 32 + lane) * (DPL * 2 / 4));
+      for (int u2 = 0; u2 < 2; ++u2) {
+        keys[u2] = (step + u2 < n_steps) ? kset * 4 + (step + u2) * nsets * 4 + kg : vis;
 #pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          const uint4 w = kr[c];
-          const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        for (int h = 0; h < G; ++h) dot2[u2][h] = make_float2(0.f, 0.f);
+      }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float2 kf = bf2_to_f2(ws[j]);
+      for (int c = 0; c < CH; ++c) {
+        uint4 w[2];
 #pragma unroll
-            for (int h = 0; h < G; ++h) dot[h] = fmaf(qf[h][c * 4 + j].x, kf.x, fmaf(qf[h][c * 4 + j].y, kf.y, dot[h]));
+        for (int u2 = 0; u2 < 2; ++u2)
+          w[u2] = keys[u2] < vis
+                      ? reinterpret_cast<const uint4 *>(ring + (((step + u2) % NS) * 32 + lane) * (DPL * 2 / 4))[c]
+                      : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+          for (int u2 = 0; u2 < 2; ++u2) {
+            const uint32_t wv = j == 0 ? w[u2].x : (j == 1 ? w[u2].y : (j == 2 ? w[u2].z : w[u2].w));
+            const float2 kf = bf2_to_f2(wv);
+#pragma unroll
+            for (int h = 0; h < G; ++h) fma2(dot2[u2][h], qf[h][c * 4 + j], kf);
           }
         }
       }
-      __syncwarp();  // the stage is consumed: it may be refilled
+      __syncwarp();  // both stages are consumed: they may be refilled
       issue(step + NS - 1);
+      issue(step + NS);
 #pragma unroll
-      for (int h = 0; h < G; ++h)
+      for (int u2 = 0; u2 < 2; ++u2) {
+        float dot[G];
 #pragma unroll
-        for (int o = 1; o < 8; o <<= 1) dot[h] += __shfl_xor_sync(0xffffffffu, dot[h], o);
-      if (sub == 0 && key < vis) {
-        float sum = 0.f;
+        for (int h = 0; h < G; ++h) dot[h] = dot2[u2][h].x + dot2[u2][h].y;
 #pragma unroll
-        for (int h = 0; h < G; ++h) sum += exp2f(dot[h] - l2[h]);
-        const int ks = kslot[key];
-        atomicAdd(&acc[(ks >> 8) * 64 + (ks & 255)], sum);
+        for (int h = 0; h < G; ++h)
+#pragma unroll
+          for (int o = 1; o < 8; o <<= 1) dot[h] += __shfl_xor_sync(0xffffffffu, dot[h], o);
+        const int key = keys[u2];
+        if (sub == 0 && key < vis) {
+          float sum = 0.f;
+#pragma unroll
+          for (int h = 0; h < G; ++h) sum += exp2f(dot[h] - l2[h]);
+          const int ks = kslot[key];
+          atomicAdd(&acc[(ks >> 8) * 64 + (ks & 255)], sum);
+        }
       }
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
