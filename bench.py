@@ -121,6 +121,57 @@ def dist_env():
 
 
 # ------------------------------------------------------------------------------------------ CPU oracle
+def host_op_costs(wl, reps: int = 200):
+    """SURVEY §8(d) host-op cost: microseconds per KVFS host operation and per pred planning call, measured
+    on a host-only ctx (the C++ control plane alone, through the C ABI) holding the workload's file shape:
+    n_files x file_len tokens.  The device-side cost of the same calls is inside the timed step."""
+    import numpy as np
+
+    from paper_2510_25412_b200 import kvfs as K
+
+    s = wl.shape
+    n_files = min(wl.n_files, 256)
+    L0 = wl.file_len + wl.prefix_len
+    per = -(-L0 // s.P) + 8
+    c = K.KVFS(1, s.Hq, s.Hkv, s.D, s.P, n_files * per + 4 * per + 64, max_batch_rows=max(16, n_files * wl.n_q),
+               max_batch_descs=max(16, n_files), device=-1)
+    pos = np.arange(L0, dtype=np.int32)
+    fds = []
+    for f in range(n_files):
+        fd = c.open(f"h{f}")
+        c.append(fd, pos)
+        fds.append(fd)
+    out = {}
+
+    def timed(fn, n):
+        t0 = time.perf_counter()
+        for i in range(n):
+            fn(i)
+        return 1e6 * (time.perf_counter() - t0) / n
+
+    descs = np.array([[fd, wl.n_q] for fd in fds], dtype=np.int32)
+    nxt = np.full(n_files, L0, dtype=np.int64)
+    offs = np.arange(wl.n_q, dtype=np.int64)
+
+    def plan(i):
+        step, _ = c.pred_step_begin(descs, (nxt[:, None] + offs[None, :]).reshape(-1).astype(np.int32))
+        c.pred_step_end(step)
+        nxt[:] += wl.n_q
+
+    out["pred_planning_per_step"] = timed(plan, reps)
+    out["pred_planning_per_descriptor"] = out["pred_planning_per_step"] / n_files
+    out["truncate"] = timed(lambda i: c.truncate(fds[i % n_files], int(L0 - 1 - (i // n_files))), reps)
+    out["evict_1_token_at_4"] = timed(lambda i: c.evict(fds[i % n_files], [(4, 5)]), reps)
+    out["fork"] = timed(lambda i: c.fork(fds[i % n_files], f"fk{i}"), min(reps, 64))
+    out["offload_meta"] = timed(lambda i: c.offload(fds[i]), min(reps, n_files // 2))
+    out["restore_meta"] = timed(lambda i: c.restore(fds[i]), min(reps, n_files // 2))
+    sch = K.Scheduler(w_max=0.01, b_max=64)
+    out["sched_enqueue"] = timed(lambda i: sch.enqueue(fds[i % n_files], [i], 1e-5 * i), reps)
+    out["sched_form"] = timed(lambda i: sch.form(1.0 + i), 20)
+    return {"unit": "us", "ctx": f"host-only, {n_files} files x {L0} tokens, n_q {wl.n_q}",
+            **{k: round(v, 2) for k, v in out.items()}}
+
+
 def oracle_sample(cfg_name: str, seconds: float, max_steps: int = None, n_sample: int = 8):
     """Time the oracle (as it stands) on a bounded sample of the workload: n_sample of the LIPs with their
     full files and per-step policies, one pred per step, repeated until `seconds` elapse (or max_steps)."""
@@ -376,7 +427,8 @@ def run_ours(args):
                   "logical_gbs_kernel": statistics.mean(logical) / (k_ms / 1000.0) / 1e9,
                   "tok_s_32_layer_equiv": value / 32.0, "host_s_per_step": host_s / Kst,
                   "h2d_metadata_bytes_per_step": h2d / Kst,
-                  "decode_ctas": kv.counter(K.CTR_LAST_DECODE_CTAS)},
+                  "decode_ctas": kv.counter(K.CTR_LAST_DECODE_CTAS),
+                  "host_ops_us": host_op_costs(wl)},
     }
     if args.scores:
         sc_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev1, ev2))
