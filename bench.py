@@ -38,6 +38,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--real-scores", action="store_true",
+                    help="cfg5hh: pick the evicted tokens by the H2O scores of a decode step (pred_attn_scores) "
+                         "instead of synthetic Exp(1) scores")
     ap.add_argument("--scores", action="store_true",
                     help="also run pred_attn_scores (NEXT-2, H2O score accumulation) every timed step")
     return ap.parse_args()
@@ -490,11 +493,50 @@ def run_heavy_hitter(args):
         fds.append(fd)
         del k, v
     torch.cuda.synchronize()
-    for f, fd in enumerate(fds):
-        kv.evict(fd, evict_ranges_heavy_hitter(seed, f, L0, L0 // 2))
     descs = np.array([[fd, 1] for fd in fds], dtype=np.int32)
-    next_pos = np.full(n_files, L0, dtype=np.int64)
-    lens = np.full(n_files, L0 // 2, dtype=np.int64)
+    scores_info = None
+    if args.real_scores:
+        # NEXT-2 in use: one decode step with H2O score accumulation (pred_attn_scores), then evict the L0 / 2
+        # lowest-score tokens of every file (first 4 and last 1024 protected; ties -> lower index)
+        own = STEP_OWNER + 10 ** 6
+        q, k1, v1 = (rows_torch(seed, t, 0, own, 0, n_files, w, device=dev).view(n_files, -1, s.D)
+                     for t, w in ((TAG_Q, s.Hq * s.D), (TAG_K, s.Hkv * s.D), (TAG_V, s.Hkv * s.D)))
+        out0 = torch.empty((n_files, s.Hq, s.D), dtype=torch.bfloat16, device=dev)
+        lse0 = torch.empty((n_files, s.Hq), dtype=torch.float32, device=dev)
+        n1 = L0 + 1
+        sc = torch.empty(n_files * n1, dtype=torch.float32, device=dev)
+        step, st = kv.pred_step_begin(descs, np.full(n_files, L0, dtype=np.int32))
+        assert st == [0] * n_files
+        kv.pred_attn_layer(step, 0, q, k1, v1, out0, lse0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        kv.pred_attn_scores(step, 0, q, lse0, sc, np.arange(n_files, dtype=np.int64) * n1)
+        e1.record()
+        kv.pred_step_end(step)
+        torch.cuda.synchronize()
+        scores_ms = e0.elapsed_time(e1)
+        sch = sc.view(n_files, n1).cpu().numpy().astype(np.float64)
+        t0 = time.perf_counter()
+        for f, fd in enumerate(fds):
+            x = sch[f].copy()
+            x[:4] = np.inf
+            x[n1 - 1024:] = np.inf
+            idx = np.sort(np.argsort(x, kind="stable")[:L0 // 2])
+            brk = np.nonzero(np.diff(idx) != 1)[0]
+            rg = np.stack([np.concatenate([[idx[0]], idx[brk + 1]]), np.concatenate([idx[brk], [idx[-1]]]) + 1], 1)
+            kv.evict(fd, rg.astype(np.int64))
+        host_sel_s = time.perf_counter() - t0
+        scores_info = {"kernel": "scores_kernel (K9) over 128 x 65537 tokens", "scores_ms": scores_ms,
+                       "k_gbs": n_files * n1 * s.Hkv * s.D * 2 / (scores_ms / 1000) / 1e9,
+                       "host_select_and_evict_s": host_sel_s,
+                       "score_sum_check": float(sch.sum() / (n_files * s.Hq))}  # = 1 (softmax weights)
+        next_pos = np.full(n_files, L0 + 1, dtype=np.int64)
+        lens = np.full(n_files, L0 + 1 - L0 // 2, dtype=np.int64)
+    else:
+        for f, fd in enumerate(fds):
+            kv.evict(fd, evict_ranges_heavy_hitter(seed, f, L0, L0 // 2))
+        next_pos = np.full(n_files, L0, dtype=np.int64)
+        lens = np.full(n_files, L0 // 2, dtype=np.int64)
     out = torch.empty((n_files, s.Hq, s.D), dtype=torch.bfloat16, device=dev)
     row_kv = s.Hkv * s.D * 2
 
@@ -546,8 +588,11 @@ def run_heavy_hitter(args):
         "extra": {"decode_ms_holes": ms_before, "decode_gbs_holes": alg_before / (ms_before / 1000.0) / 1e9,
                   "decode_ms_compacted": ms_after, "decode_gbs_compacted": alg_after / (ms_after / 1000.0) / 1e9,
                   "compact_ms_all_files": ms_compact, "compact_bytes": compact_bytes,
-                  "retained_tokens": retained},
+                  "retained_tokens": retained, "h2o_scores": scores_info},
     }
+    if args.real_scores:
+        line["config"]["workload"] = line["config"]["workload"].replace(
+            "lowest Exp(1) scores", "lowest H2O scores of a decode step (pred_attn_scores)")
     print(json.dumps(line), flush=True)
 
 
