@@ -644,6 +644,67 @@ def run_offload(args):
     print(json.dumps(line), flush=True)
 
 
+def run_migrate(args):
+    """SURVEY §8(e) migration data path on one GPU: kvfs_pack of 32 files x 32768 tokens (8B attention shape,
+    128 MiB of K+V each, the cfg5 file size) into one contiguous device buffer (K6 gather), then kvfs_unpack
+    into a second ctx (K6 scatter into R1 pages).  The NVLink send/recv between the two (NCCL over NVSwitch)
+    needs two GPUs and is not measured here.  One JSON line: pack / unpack GB/s against the HBM peak."""
+    import numpy as np
+    import torch
+
+    from paper_2510_25412_b200 import kvfs as K
+    from synth.configs import Shape
+    from synth.workloads import TAG_K, TAG_V, rows_torch
+
+    torch.cuda.set_device(0)
+    s, n_files, n, seed = Shape(32, 8, 128, 16), 32, 32768, 1007
+    n_pages = n_files * (n // 16) + 64
+    src = K.KVFS(1, s.Hq, s.Hkv, s.D, s.P, n_pages, device=0)
+    dst = K.KVFS(1, s.Hq, s.Hkv, s.D, s.P, n_pages, device=0)
+    dev = torch.device("cuda", 0)
+    fds = []
+    for f in range(n_files):
+        fd = src.open(f"m{f}")
+        k = rows_torch(seed, TAG_K, 0, f, 0, n, s.Hkv * s.D, device=dev).view(1, n, s.Hkv, s.D)
+        v = rows_torch(seed, TAG_V, 0, f, 0, n, s.Hkv * s.D, device=dev).view(1, n, s.Hkv, s.D)
+        src.append(fd, np.arange(n, dtype=np.int32), k, v)
+        fds.append(fd)
+        del k, v
+    torch.cuda.synchronize()
+    nbytes = n_files * n * s.Hkv * s.D * 2 * 2
+    pk, up = [], []
+    for it in range(args.warmup + max(1, min(args.steps, 5))):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record()
+        hdr, buf = src.pack(fds)
+        e[1].record()
+        new = dst.unpack(hdr, buf, [f"r{it}_{f}" for f in range(n_files)])
+        e[2].record()
+        torch.cuda.synchronize()
+        for nm in [f"r{it}_{f}" for f in range(n_files)]:
+            dst.unlink(nm)
+        for fd in new:
+            dst.close(fd)
+        del buf
+        if it >= args.warmup:
+            pk.append(e[0].elapsed_time(e[1]))
+            up.append(e[1].elapsed_time(e[2]))
+    peak, peak_src = peaks()
+    pk_ms, up_ms = statistics.median(pk), statistics.median(up)
+    gbs = lambda ms: 2 * nbytes / (ms / 1000) / 1e9  # read + write
+    line = {"metric": "KV-file migration pack / unpack GB/s (SURVEY 8(e); one GPU, NVLink leg not measured)",
+            "value": gbs(pk_ms), "unit": "GB/s", "n_gpus": 1, "steps": len(pk), "warmup": args.warmup,
+            "higher_is_better": True, "dtype": "bf16", "data": "synthetic (seed 1007)",
+            "config": {"workload": "32 files x 32768 tokens (128 MiB K+V each, 4 GiB total): kvfs_pack into one "
+                                   "device buffer, kvfs_unpack into a second ctx", "bytes_moved_each": nbytes},
+            "roofline": {"bound": "hbm", "achieved": gbs(pk_ms), "peak": peak, "unit": "GB/s",
+                         "frac": gbs(pk_ms) / peak, "kernel": "pack_kernel (K6)", "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": 2 * nbytes},
+            "extra": {"pack_ms": pk_ms, "unpack_ms": up_ms, "pack_gbs": gbs(pk_ms), "unpack_gbs": gbs(up_ms),
+                      "note": "includes the host side of kvfs_pack / kvfs_unpack (page lists, R1 allocation)"}}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -652,6 +713,8 @@ def main():
         run_heavy_hitter(args)
     elif args.config == "offload":
         run_offload(args)
+    elif args.config == "migrate":
+        run_migrate(args)
     else:
         run_ours(args)
 

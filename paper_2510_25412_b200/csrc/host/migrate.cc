@@ -46,14 +46,20 @@ int pack_files(Ctx &c, const int *fds, int n, std::vector<uint32_t> *pages, std:
     if (!seen.insert(f).second) return KVFS_EBUSY;
     files.push_back(f);
   }
-  std::set<uint32_t> uniq;
+  // distinct pages of the set, ascending source page id (vector sort + unique; O(pages log pages))
+  pages->clear();
   for (File *f : files)
-    for (const Entry &e : f->table) uniq.insert(e.page);
-  pages->assign(uniq.begin(), uniq.end());  // ascending source page id
-  std::map<uint32_t, uint32_t> local;
+    for (const Entry &e : f->table) pages->push_back(e.page);
+  std::sort(pages->begin(), pages->end());
+  pages->erase(std::unique(pages->begin(), pages->end()), pages->end());
+  std::vector<uint32_t> local(static_cast<size_t>(c.pool->n_pages()), 0u);
   for (size_t j = 0; j < pages->size(); ++j) local[(*pages)[j]] = static_cast<uint32_t>(j);
   const kvfs_config &cfg = c.cfg;
+  // header size first, then one pass of bulk writes
+  size_t bytes = 8 * 4 + 8;
+  for (File *f : files) bytes += 8 + f->table.size() * 16 + static_cast<size_t>(f->len) * 4;
   hdr->clear();
+  hdr->reserve(bytes);
   put<uint32_t>(hdr, kMagic);
   put<uint32_t>(hdr, 1);
   put<uint32_t>(hdr, static_cast<uint32_t>(n));
@@ -64,16 +70,21 @@ int pack_files(Ctx &c, const int *fds, int n, std::vector<uint32_t> *pages, std:
   put<uint32_t>(hdr, static_cast<uint32_t>(cfg.head_dim));
   put<uint64_t>(hdr, static_cast<uint64_t>(cfg.n_kv_heads) * cfg.page_size * cfg.head_dim * 2);
   std::vector<int32_t> lp;
+  std::vector<uint8_t> ent;
   for (File *f : files) {
     file_positions(c, *f, &lp);
     put<uint32_t>(hdr, static_cast<uint32_t>(f->table.size()));
     put<uint32_t>(hdr, static_cast<uint32_t>(lp.size()));
-    for (const Entry &e : f->table) {
-      put<uint32_t>(hdr, local[e.page]);
-      put<uint32_t>(hdr, 0);
-      put<uint64_t>(hdr, e.mask);
+    ent.resize(f->table.size() * 16);
+    for (size_t e = 0; e < f->table.size(); ++e) {
+      const uint32_t loc = local[f->table[e].page], pad = 0;
+      std::memcpy(ent.data() + e * 16, &loc, 4);
+      std::memcpy(ent.data() + e * 16 + 4, &pad, 4);
+      std::memcpy(ent.data() + e * 16 + 8, &f->table[e].mask, 8);
     }
-    for (int32_t p : lp) put<int32_t>(hdr, p);
+    hdr->insert(hdr->end(), ent.begin(), ent.end());
+    const uint8_t *pb = reinterpret_cast<const uint8_t *>(lp.data());
+    hdr->insert(hdr->end(), pb, pb + lp.size() * 4);
   }
   return KVFS_OK;
 }
