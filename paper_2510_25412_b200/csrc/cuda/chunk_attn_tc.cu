@@ -51,6 +51,10 @@ constexpr uint32_t TMEM_COLS = 512;
 // (period 4.5k vs 3.2k clk, tools/k2_trace.py) because the two groups fall into phase and the ping-pong of
 // softmax and tensor work between the M-tiles is lost; kept as a switch for the record.
 constexpr bool K2_SELF_ISSUE = KVFS_K2_SELF_ISSUE != 0;
+#ifndef KVFS_K2_ISSUERS
+#define KVFS_K2_ISSUERS 1
+#endif
+constexpr int K2_ISSUERS = KVFS_K2_ISSUERS;  // MMA-issuing warps (2: one per M-tile)
 // waits on the softmax <-> MMA handoff barriers: plain try_wait loop, or with a suspend-time hint
 #ifdef KVFS_K2_SLEEPWAIT
 #define K2_WAIT(b, ph) mbar_wait_sleep(b, ph)
@@ -246,9 +250,9 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
     mbar_init(bar(B_Q), PREFIX ? 4 * n_mt : 1);  // prefix: one arrival per softmax warp that gathers Q
     for (int s = 0; s < KV2; ++s) {
       mbar_init(bar(B_KF + s), 1);
-      mbar_init(bar(B_KE + s), K2_SELF_ISSUE ? n_mt : 1);
+      mbar_init(bar(B_KE + s), (K2_SELF_ISSUE || K2_ISSUERS == 2) ? n_mt : 1);
       mbar_init(bar(B_VF + s), 1);
-      mbar_init(bar(B_VE + s), K2_SELF_ISSUE ? n_mt : 1);
+      mbar_init(bar(B_VE + s), (K2_SELF_ISSUE || K2_ISSUERS == 2) ? n_mt : 1);
     }
     for (int m = 0; m < 2; ++m) {
       mbar_init(bar(B_SF + m), 1);
@@ -413,12 +417,17 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         }
         __syncwarp();
       }
-    } else if (warp == 1 && !K2_SELF_ISSUE) {
-      // ============================================================ MMA issuer
+    } else if ((warp == 1 || (warp == 2 && K2_ISSUERS == 2)) && !K2_SELF_ISSUE) {
+      // ============================================================ MMA issuer(s)
+      // K2_ISSUERS == 2: warp 1 + m issues M-tile m, so a tcgen05.mma issue blocked on a full tensor queue
+      // delays only its own M-tile; the K / V stage releases then take one commit per issuer.
+      const int m_lo = K2_ISSUERS == 2 ? warp - 1 : 0;
+      const int m_hi = K2_ISSUERS == 2 ? min(warp, n_mt) : n_mt;
+      if (m_lo < m_hi) {
       mbar_wait(bar(B_Q), 0);
       if (lane == 0) K2T(25, 0);
       mbar_wait(bar(B_KF + 0), 0);
-      for (int m = 0; m < n_mt; ++m) issue_s(0, m);
+      for (int m = m_lo; m < m_hi; ++m) issue_s(0, m);
       if (elect_one()) mma_commit(bar(B_KE + 0));
       __syncwarp();
       for (int t = 0; t < n_tiles; ++t) {
@@ -426,14 +435,14 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         const bool more = t + 1 < n_tiles;
         mbar_wait(bar(B_VF + s), (t / KV2) & 1);
         if (lane == 0) K2T(9, t);
-        for (int m = 0; m < n_mt; ++m) {
+        for (int m = m_lo; m < m_hi; ++m) {
           K2_WAIT(bar(B_PF + 2 * m), t & 1);  // softmax m wrote P(t) keys 0..63 (and corrected O)
           issue_pv(t, m, 0);
           K2_WAIT(bar(B_PF + 2 * m + 1), t & 1);  // keys 64..127
           if (lane == 0) K2T(10 + 2 * m, t);
           issue_pv(t, m, 1);
           if (more) {                       // in-order after PV(t): S(t+1) may overwrite P(t)'s columns
-            if (m == 0) mbar_wait(bar(B_KF + (t + 1) % KV2), ((t + 1) / KV2) & 1);
+            if (m == m_lo) mbar_wait(bar(B_KF + (t + 1) % KV2), ((t + 1) / KV2) & 1);
             issue_s(t + 1, m);
           }
           if (lane == 0) K2T(11 + 2 * m, t);
@@ -443,6 +452,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           mma_commit(bar(B_VE + s));
         }
         __syncwarp();
+      }
       }
     }
   } else {
