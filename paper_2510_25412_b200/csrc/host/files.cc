@@ -3,6 +3,9 @@
 // SURVEY.md §8(c) C3 (restated in DESIGN.md "Readings").
 #include <algorithm>
 #include <cstring>
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
 
 #include "kvfs_impl.h"
 
@@ -282,22 +285,61 @@ int truncate_file(Ctx &c, File &f, int64_t n) {
 }
 
 // ------------------------------------------------------------------------------------------ R6-R8
+// Compacts the retained slots of a partial mask m (P slots at sp + r) to sp + w, w <= r.  Group by group:
+// the group is loaded before anything is stored, and a store never reaches past the group being read.
+static size_t compress_slots_scalar(int32_t *sp, size_t w, size_t r, uint64_t m, int P) {
+  for (uint64_t b = m; b; b &= b - 1) sp[w++] = sp[r + static_cast<size_t>(__builtin_ctzll(b))];
+  return w;
+}
+
+#if defined(__x86_64__)
+__attribute__((target("avx512f"))) static size_t compress_slots_avx512(int32_t *sp, size_t w, size_t r, uint64_t m,
+                                                                         int P) {
+  for (int g = 0; g < P; g += 16) {
+    const __mmask16 k = static_cast<__mmask16>(m >> g);
+    if (!k) continue;
+    const __m512i v = _mm512_loadu_si512(sp + r + g);
+    _mm512_storeu_si512(sp + w, _mm512_maskz_compress_epi32(k, v));
+    w += static_cast<size_t>(__builtin_popcount(k));
+  }
+  return w;
+}
+static const bool kHaveAvx512 = __builtin_cpu_supports("avx512f");
+#endif
+
+static size_t compress_slots(int32_t *sp, size_t w, size_t r, uint64_t m, int P) {
+#if defined(__x86_64__)
+  if (kHaveAvx512) return compress_slots_avx512(sp, w, r, m, P);
+#endif
+  return compress_slots_scalar(sp, w, r, m, P);
+}
+
 static void compact_commit(Ctx &c, File &f, std::vector<Entry> *old_table, std::vector<uint32_t> *new_pages) {
   const int P = c.cfg.page_size;
   const int64_t len = f.len;
   if (len == 0) return;
   const int64_t k = (len + P - 1) / P;
   std::vector<uint32_t> np(static_cast<size_t>(k));
-  for (int64_t j = 0; j < k; ++j) np[j] = c.pool->alloc();  // old pages still held: never destinations
-  // positions in logical order, written straight into the new per-slot array: token i -> (new[i/P], i%P)
-  std::vector<int32_t> nspos(static_cast<size_t>(k) * P, 0);
+  c.pool->alloc_n(k, np.data());  // old pages still held: never destinations
+  // positions in logical order, token i -> slot (new[i/P], i%P), compacted in place: the write cursor
+  // (retained tokens before a slot) never passes the slot being read
+  const uint64_t full = P == 64 ? ~0ull : ((1ull << P) - 1);
+  int32_t *sp = f.spos.data();
   size_t w = 0;
-  for (size_t e = 0; e < f.table.size(); ++e)
-    for (uint64_t m = f.table[e].mask; m; m &= m - 1) nspos[w++] = f.spos[e * P + __builtin_ctzll(m)];
+  for (size_t e = 0; e < f.table.size(); ++e) {
+    const uint64_t m = f.table[e].mask;
+    const size_t r = e * static_cast<size_t>(P);
+    if (m == full) {
+      if (w != r) std::memmove(sp + w, sp + r, sizeof(int32_t) * static_cast<size_t>(P));
+      w += static_cast<size_t>(P);
+    } else {
+      w = compress_slots(sp, w, r, m, P);
+    }
+  }
+  f.spos.resize(static_cast<size_t>(k) * P);
+  std::fill(f.spos.begin() + static_cast<std::ptrdiff_t>(w), f.spos.end(), 0);
   std::vector<Entry> old;
   old.swap(f.table);
-  f.spos.swap(nspos);
-  const uint64_t full = P == 64 ? ~0ull : ((1ull << P) - 1);
   f.table.resize(static_cast<size_t>(k));
   for (int64_t j = 0; j < k; ++j) {
     const int64_t cnt = std::min<int64_t>(P, len - j * P);

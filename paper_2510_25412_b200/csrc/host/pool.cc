@@ -43,6 +43,28 @@ uint32_t PagePool::alloc() {
   return 0;
 }
 
+void PagePool::alloc_n(int64_t n, uint32_t *out) {
+  assert(n_free_ >= n);
+  int64_t got = 0;
+  for (size_t i = hint_; got < n && i < l1_.size(); ++i) {
+    while (got < n && l1_[i]) {
+      const size_t w = i * 64 + static_cast<size_t>(__builtin_ctzll(l1_[i]));
+      uint64_t bits = l0_[w];
+      while (got < n && bits) {
+        const uint32_t p = static_cast<uint32_t>(w * 64 + static_cast<size_t>(__builtin_ctzll(bits)));
+        bits &= bits - 1;
+        ref_[p] = 1;
+        out[got++] = p;
+      }
+      l0_[w] = bits;
+      if (!bits) l1_[i] &= ~(1ull << (w & 63));
+    }
+    if (!l1_[i]) hint_ = i + 1;
+  }
+  assert(got == n);
+  n_free_ -= n;
+}
+
 void PagePool::release(uint32_t p) {
   assert(ref_[p] > 0);
   if (--ref_[p] == 0) {

@@ -19,6 +19,9 @@ class PagePool {
 
   // Smallest free page id, refcount set to 1.  Precondition: n_free() > 0.
   uint32_t alloc();
+  // n smallest free page ids in increasing order into out[0..n), each refcount 1 (the same pages n calls of
+  // alloc() return, found by one scan of the bitmaps).  Precondition: n_free() >= n.
+  void alloc_n(int64_t n, uint32_t *out);
   // refcount++ of an allocated page.
   void incref(uint32_t p) { ++ref_[p]; }
   // refcount--; the page becomes free at 0.
