@@ -112,6 +112,15 @@ void recompute_lstart(File &f, size_t from) {
   f.len = f.table.empty() ? 0 : f.table.back().lstart + popc(f.table.back().mask);
 }
 
+// lstart of entries [from, to) from entry from - 1 (len is not touched)
+static void recompute_lstart_span(File &f, size_t from, size_t to) {
+  int64_t acc = from > 0 ? f.table[from - 1].lstart + popc(f.table[from - 1].mask) : 0;
+  for (size_t i = from; i < to; ++i) {
+    f.table[i].lstart = static_cast<int32_t>(acc);
+    acc += popc(f.table[i].mask);
+  }
+}
+
 File *get_file(Ctx &c, int fd) {
   if (fd < 0 || static_cast<size_t>(fd) >= c.fds.size() || !c.fds[fd] || !c.fds[fd]->alive) return nullptr;
   return c.fds[fd].get();
@@ -369,7 +378,21 @@ int evict_file(Ctx &c, File &f, const int64_t *ranges, int n_ranges, int flags, 
   for (int r = 0; r < n_ranges; ++r) {
     const int64_t a = ranges[2 * r], b = ranges[2 * r + 1];
     evicted += b - a;
-    while (ei < f.table.size() && f.table[ei].lstart + popc(f.table[ei].mask) <= a) ++ei;
+    // first entry ending after a (entry ends are non-decreasing in table order): galloping search from
+    // the previous range's entry, O(log distance)
+    {
+      auto before = [&](size_t i) { return f.table[i].lstart + popc(f.table[i].mask) <= a; };
+      size_t lo = ei, step = 1;
+      while (lo + step < f.table.size() && before(lo + step)) {
+        lo += step;
+        step <<= 1;
+      }
+      const size_t hi = std::min(f.table.size(), lo + step);
+      ei = static_cast<size_t>(
+          std::partition_point(f.table.begin() + static_cast<std::ptrdiff_t>(lo), f.table.begin() + static_cast<std::ptrdiff_t>(hi),
+                               [a](const Entry &e) { return e.lstart + popc(e.mask) <= a; }) -
+          f.table.begin());
+    }
     for (size_t i = ei; i < f.table.size() && f.table[i].lstart < b; ++i) {
       const int64_t ls = f.table[i].lstart;
       const int r0 = static_cast<int>(std::max<int64_t>(0, a - ls));
@@ -414,8 +437,15 @@ int evict_file(Ctx &c, File &f, const int64_t *ranges, int n_ranges, int flags, 
       mark_dirty_from(f, touched.front().first);
       f.table.resize(w);
       f.spos.resize(w * P);
+      recompute_lstart(f, touched.front().first);
+    } else {
+      // offsets change inside the touched span; every later entry moves down by the evicted count
+      const size_t last = touched.back().first;
+      recompute_lstart_span(f, touched.front().first, last + 1);
+      const int32_t ev = static_cast<int32_t>(evicted);
+      for (size_t i = last + 1; i < f.table.size(); ++i) f.table[i].lstart -= ev;
+      f.len -= evicted;
     }
-    recompute_lstart(f, touched.front().first);
   }
   if (compact) compact_commit(c, f, old_table, new_pages);
   return KVFS_OK;
