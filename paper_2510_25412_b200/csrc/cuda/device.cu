@@ -269,18 +269,26 @@ class CudaDevice final : public Device {
       if (cudaMemset(c_.kpool[l], 0, pool_bytes) != cudaSuccess) return KVFS_EIO;
       if (cudaMemset(c_.vpool[l], 0, pool_bytes) != cudaSuccess) return KVFS_EIO;
     }
-    if (cfg.head_dim == 128) {
+    {
       void *fn = nullptr;
       cudaDriverEntryPointQueryResult q;
       if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
           q != cudaDriverEntryPointSuccess || !fn)
         return KVFS_EIO;
       encode_ = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    if (cfg.head_dim == 128) {
       kmaps_.resize(cfg.n_layers);
       vmaps_.resize(cfg.n_layers);
       for (int l = 0; l < cfg.n_layers; ++l) {
-        if (!pool_map(c_.kpool[l], &kmaps_[l]) || !pool_map(c_.vpool[l], &vmaps_[l])) return KVFS_EIO;
+        if (!pool_map(c_.kpool[l], &kmaps_[l], cfg.page_size) || !pool_map(c_.vpool[l], &vmaps_[l], cfg.page_size))
+          return KVFS_EIO;
       }
+    }
+    if (cfg.head_dim == 64 || cfg.head_dim == 128) {  // K9: 16-row tiles of the K pool
+      smaps_.resize(cfg.n_layers);
+      for (int l = 0; l < cfg.n_layers; ++l)
+        if (!pool_map(c_.kpool[l], &smaps_[l], 16)) return KVFS_EIO;
     }
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device);
@@ -338,10 +346,11 @@ class CudaDevice final : public Device {
     if (!dd || !du) return KVFS_ENOMEM;
     if (!send(s)) return KVFS_EIO;
     const kvfs_config &cfg = c_.cfg;
+    if (smaps_.empty()) return KVFS_EINVAL;
     const cudaError_t e = dev::launch_scores(
-        static_cast<const dev::ScoreUnit *>(du), static_cast<int>(units.size()), static_cast<const dev::ScoreDesc *>(dd),
-        slab_, static_cast<const bf16 *>(q), lse, static_cast<const bf16 *>(c_.kpool[layer]),
-        scale * 1.4426950408889634f, out, cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, cfg.page_size, cs(s));
+        smaps_[layer], static_cast<const dev::ScoreUnit *>(du), static_cast<int>(units.size()),
+        static_cast<const dev::ScoreDesc *>(dd), slab_, static_cast<const bf16 *>(q), lse, scale * 1.4426950408889634f,
+        out, cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim, cfg.page_size, cs(s));
     ++c_.ctr.launches;
     return e == cudaSuccess ? KVFS_OK : KVFS_EIO;
   }
@@ -687,12 +696,13 @@ class CudaDevice final : public Device {
     return cudaGetLastError() == cudaSuccess ? KVFS_OK : KVFS_EIO;
   }
 
-  bool pool_map(void *pool, CUtensorMap *m) {
+  // the pool as [n_pages * Hkv * P rows][D] bf16, box 64 dims x box_rows rows, 128-byte swizzle
+  bool pool_map(void *pool, CUtensorMap *m, int box_rows) {
     const kvfs_config &cfg = c_.cfg;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cfg.head_dim),
                                 static_cast<cuuint64_t>(cfg.n_pages) * cfg.n_kv_heads * cfg.page_size};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cfg.head_dim) * 2};
-    const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(cfg.page_size)};
+    const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
     const cuuint32_t es[2] = {1, 1};
     return encode_(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, pool, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -730,7 +740,7 @@ class CudaDevice final : public Device {
              *d_dst_ = nullptr, *d_cdescs_ = nullptr, *d_cunits_ = nullptr, *d_cdst_ = nullptr,
              *d_pdescs_ = nullptr, *d_punits_ = nullptr, *d_prows_ = nullptr;
   PFN_cuTensorMapEncodeTiled_v12000 encode_ = nullptr;
-  std::vector<CUtensorMap> kmaps_, vmaps_;
+  std::vector<CUtensorMap> kmaps_, vmaps_, smaps_;  // smaps_: K pool in 16-row boxes (K9)
 };
 
 }  // namespace

@@ -50,9 +50,10 @@ struct ScoreDesc {  // == kvfs::ScoreDesc
 struct ScoreUnit {  // == kvfs::ScoreUnit
   int32_t desc, e0, e1, l0;
 };
-cudaError_t launch_scores(const ScoreUnit *units, int n_units, const ScoreDesc *descs, const Entry *slab,
-                          const __nv_bfloat16 *q, const float *lse, const __nv_bfloat16 *kpool, float scale_log2,
-                          float *out, int Hq, int Hkv, int D, int P, cudaStream_t s);
+// kmap: the layer's K pool as a 2-D map [n_pages * Hkv * P rows][D], box 64 dims x 16 rows, 128-byte swizzle
+cudaError_t launch_scores(const CUtensorMap &kmap, const ScoreUnit *units, int n_units, const ScoreDesc *descs,
+                          const Entry *slab, const __nv_bfloat16 *q, const float *lse, float scale_log2, float *out,
+                          int Hq, int Hkv, int D, int P, cudaStream_t s);
 struct ChunkParams {
   const ChunkUnit *units;
   const ChunkDesc *descs;

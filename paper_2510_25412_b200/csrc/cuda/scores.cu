@@ -3,7 +3,7 @@
 //   scores[off_d + k] = sum_{rows i of d, heads h} exp2(scale_log2 <q_ih, K_k,g(h)> - lse_ih log2 e)
 // for every retained token k visible to row i (logical k <= len_after - n_q + i), exactly the softmax
 // weights of rule R10 given the lse the attention kernels wrote.
-// One CTA per (descriptor, chunk of <= 32 page entries).
+// One CTA per (descriptor, chunk of <= 32 page entries).  Tensor-core contraction of 16-key tiles (below).
 #include <cuda_bf16.h>
 
 #include "kernels.cuh"
@@ -11,32 +11,52 @@
 namespace kvfs {
 namespace dev {
 
-// Layout per CTA (256 threads = 8 warps): warp w takes kv head g = w % Hkv and every (8 / Hkv)-th group
-// of 4 keys (Hkv < 8) of the unit's entries; in a warp, 8 lanes share a key (D / 8 dims each, loaded as
-// 16-byte vectors: the 8 lanes read the key's contiguous row), 4 keys per step, UNR steps in flight.  The
-// lane's slice of q (G heads of the current query row) stays in registers; the G partial dot products
-// are reduced by xor-shuffles over the 8 lanes; lane 0 of the key adds sum_h exp2(s - lse2) into the
-// key's shared-memory accumulator.  Query rows are processed one after another (decode: one row).
-template <int D, int G>
-__global__ void __launch_bounds__(256) scores_kernel(const ScoreUnit *units, const ScoreDesc *descs,
-                                                     const Entry *slab, const __nv_bfloat16 *q, const float *lse,
-                                                     const __nv_bfloat16 *kpool, float scale_log2, float *out,
-                                                     int Hkv, int P) {
-  constexpr int DPL = D / 8;   // dims per lane
-  constexpr int CH = DPL / 8;  // 16-byte chunks per lane
-  constexpr int NS = 8;        // ring stages per warp (4 key rows each)
-  __shared__ float acc[32 * 64];  // [entry][slot]
+// Layout per CTA (256 threads = 8 warps, two CTAs per SM): warp w takes kv head g = w % Hkv and every
+// (8 / Hkv)-th 16-slot tile of the unit's entries that holds a retained slot.  Each warp streams its tiles
+// through a private ring of NS stages with 2-D TMA (16 rows x 64 dims per box, 128-byte swizzle; lane 0
+// issues, completion on the stage's mbarrier) and contracts them on the tensor cores: S^T = K_tile Q^T as
+// mma.m16n8k16 (A = 16 keys x 16 dims from ldmatrix, B = 16 dims x 8 columns, a column = one (query row,
+// head) pair of the descriptor, G <= 8 heads per kv head, n_q * G columns in tiles of 8).  The epilogue of a
+// tile is exp2(s * scale_log2 - lse_col * log2 e) for the visible (key, row) pairs, summed over the lane's
+// columns, reduced over the 4 lanes of a row, and added into the key's shared-memory accumulator.
+// Holes of a partially retained tile are read (one TMA box) and masked out of the sums.
+constexpr int kScoreStages = 3;
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t &a0, uint32_t &a1, uint32_t &a2, uint32_t &a3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+               : "r"(addr)
+               : "memory");
+}
+
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int D>
+__global__ void __launch_bounds__(256, 2)
+    scores_kernel(const __grid_constant__ CUtensorMap kmap, const ScoreUnit *units, const ScoreDesc *descs,
+                  const Entry *slab, const __nv_bfloat16 *q, const float *lse, float scale_log2, float *out, int Hkv,
+                  int G, int P) {
+  constexpr int NS = kScoreStages;
+  constexpr int NB = D / 64;          // 64-dim TMA boxes per tile
+  constexpr int TILE = 16 * D * 2;    // bytes of one 16-key tile
+  constexpr int KS = D / 16;          // mma k-steps
+  __shared__ float acc[32 * 64];      // [entry][slot]
   __shared__ uint64_t emask[32];
   __shared__ uint32_t epage[32];
   __shared__ int32_t elog[32];
-  __shared__ int16_t kslot[32 * 64];  // retained keys of the unit: (entry << 8) | slot, logical order
-  __shared__ int nkeys;
-  extern __shared__ __align__(16) uint32_t ring_all[];  // [8 warps][NS][32 lanes][DPL bf16]
+  __shared__ __align__(8) uint64_t fullb[8][NS];
+  extern __shared__ __align__(16) uint8_t dyn[];
+  const uint32_t ring0 = (smem_u32(dyn) + 1023u) & ~1023u;
   const ScoreUnit u = units[blockIdx.x];
   const ScoreDesc d = descs[u.desc];
   const int ne = u.e1 - u.e0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t *ring = ring_all + warp * NS * 32 * (DPL * 2 / 4);
   if (warp == 0) {
     uint64_t m = 0;
     uint32_t pg = 0;
@@ -54,157 +74,151 @@ __global__ void __launch_bounds__(256) scores_kernel(const ScoreUnit *units, con
     }
     emask[lane] = m;
     epage[lane] = pg;
-    elog[lane] = incl - cnt;  // unit-relative
-    int w = incl - cnt;
-    for (uint64_t mm = m; mm; mm &= mm - 1) kslot[w++] = static_cast<int16_t>((lane << 8) | __ffsll(mm) - 1);
-    if (lane == 31) nkeys = incl;
+    elog[lane] = incl - cnt;  // unit-relative logical index of the entry's first retained slot
   }
+  if (lane < NS) mbar_init(smem_u32(&fullb[warp][lane]), 1);
   for (int i = threadIdx.x; i < 32 * 64; i += blockDim.x) acc[i] = 0.f;
+  fence_mbar_init();
   __syncthreads();
-  const int n = nkeys;
-  const int g = warp % Hkv, kset = warp / Hkv, nsets = 8 / Hkv;  // Hkv in {1, 2, 4, 8}
-  const int kg = lane >> 3, sub = lane & 7;
-  const int base = d.len_after - d.n_q - u.l0;  // row i sees unit-relative keys <= base + i
-  for (int r = 0; r < d.n_q; ++r) {
-    const int row = d.row0 + r;
-    float2 qf[G][DPL / 2];
-#pragma unroll
-    for (int h = 0; h < G; ++h) {
-      const uint4 *qs = reinterpret_cast<const uint4 *>(q + (static_cast<int64_t>(row) * (Hkv * G) + g * G + h) * D) +
-                        sub * CH;
-#pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        const uint4 w = __ldg(qs + c);
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 f = bf2_to_f2(ws[j]);
-          qf[h][c * 4 + j] = make_float2(f.x * scale_log2, f.y * scale_log2);
-        }
-      }
-    }
-    float l2[G];
-#pragma unroll
-    for (int h = 0; h < G; ++h) l2[h] = lse[static_cast<int64_t>(row) * (Hkv * G) + g * G + h] * 1.4426950408889634f;
-    const int vis = min(n, base + r + 1);  // unit-relative keys visible to this row
-    // warp-private ring of NS stages of 4 key rows (cp.async, 16 B per lane per chunk): NS - 1 steps in
-    // flight while one is computed
-    const int n_steps = vis > kset * 4 ? (vis - kset * 4 + nsets * 4 - 1) / (nsets * 4) : 0;
-    auto issue = [&](int step) {
-      if (step < n_steps) {
-        const int key = kset * 4 + step * nsets * 4 + kg;
-        if (key < vis) {
-          const int ks = kslot[key], e = ks >> 8, slot = ks & 255;
-          const char *src = reinterpret_cast<const char *>(
-              kpool + ((static_cast<int64_t>(epage[e]) * Hkv + g) * P + slot) * D + sub * DPL);
-          const uint32_t dst = smem_u32(ring + ((step % NS) * 32 + lane) * (DPL * 2 / 4));
-#pragma unroll
-          for (int c = 0; c < CH; ++c)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + c * 16), "l"(src + c * 16) : "memory");
-        }
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-#pragma unroll
-    for (int st = 0; st < NS - 1; ++st) issue(st);
-    // two steps per iteration (independent dot chains), packed fp32x2 FMAs
-    for (int step = 0; step < n_steps; step += 2) {
-      asm volatile("cp.async.wait_group %0;" ::"n"(NS - 3) : "memory");
-      __syncwarp();
-      float2 dot2[2][G];
-      int keys[2];
-#pragma unroll
-      for (int u2 = 0; u2 < 2; ++u2) {
-        keys[u2] = (step + u2 < n_steps) ? kset * 4 + (step + u2) * nsets * 4 + kg : vis;
-#pragma unroll
-        for (int h = 0; h < G; ++h) dot2[u2][h] = make_float2(0.f, 0.f);
-      }
-#pragma unroll
-      for (int c = 0; c < CH; ++c) {
-        uint4 w[2];
-#pragma unroll
-        for (int u2 = 0; u2 < 2; ++u2)
-          w[u2] = keys[u2] < vis
-                      ? reinterpret_cast<const uint4 *>(ring + (((step + u2) % NS) * 32 + lane) * (DPL * 2 / 4))[c]
-                      : make_uint4(0, 0, 0, 0);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-#pragma unroll
-          for (int u2 = 0; u2 < 2; ++u2) {
-            const uint32_t wv = j == 0 ? w[u2].x : (j == 1 ? w[u2].y : (j == 2 ? w[u2].z : w[u2].w));
-            const float2 kf = bf2_to_f2(wv);
-#pragma unroll
-            for (int h = 0; h < G; ++h) fma2(dot2[u2][h], qf[h][c * 4 + j], kf);
-          }
-        }
-      }
-      __syncwarp();  // both stages are consumed: they may be refilled
-      issue(step + NS - 1);
-      issue(step + NS);
-#pragma unroll
-      for (int u2 = 0; u2 < 2; ++u2) {
-        float dot[G];
-#pragma unroll
-        for (int h = 0; h < G; ++h) dot[h] = dot2[u2][h].x + dot2[u2][h].y;
-#pragma unroll
-        for (int h = 0; h < G; ++h)
-#pragma unroll
-          for (int o = 1; o < 8; o <<= 1) dot[h] += __shfl_xor_sync(0xffffffffu, dot[h], o);
-        const int key = keys[u2];
-        if (sub == 0 && key < vis) {
-          float sum = 0.f;
-#pragma unroll
-          for (int h = 0; h < G; ++h) sum += exp2f(dot[h] - l2[h]);
-          const int ks = kslot[key];
-          atomicAdd(&acc[(ks >> 8) * 64 + (ks & 255)], sum);
-        }
-      }
-    }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncwarp();
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < n; t += blockDim.x) {
-    const int ks = kslot[t];
-    out[d.out_off + u.l0 + t] = acc[(ks >> 8) * 64 + (ks & 255)];
-  }
-  (void)elog;
-}
 
-template <int D, int G>
-static cudaError_t launch_scores_t(const ScoreUnit *units, int n_units, const ScoreDesc *descs, const Entry *slab,
-                                   const __nv_bfloat16 *q, const float *lse, const __nv_bfloat16 *kpool,
-                                   float scale_log2, float *out, int Hkv, int P, cudaStream_t s) {
-  constexpr int smem = 8 * 8 * 32 * (D / 8) * 2;  // 8 warps x NS stages x 32 lanes x DPL bf16
-  static bool attr = false;
-  if (!attr && smem > 48 * 1024) {
-    const cudaError_t e = cudaFuncSetAttribute(scores_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
+  const int g = warp % Hkv, kset = warp / Hkv, nsets = 8 / Hkv;  // Hkv in {1, 2, 4, 8}
+  const int tpe = P >> 4, ntiles = ne * tpe;
+  const uint32_t ring = ring0 + static_cast<uint32_t>(warp * NS * TILE);
+  const uint64_t pol = policy_evict_first();
+  auto tmask = [&](int t) -> uint32_t { return static_cast<uint32_t>(emask[t / tpe] >> ((t % tpe) * 16)) & 0xffffu; };
+  auto next = [&](int t) {
+    while (t < ntiles && !tmask(t)) t += nsets;
+    return t;
+  };
+  auto issue = [&](int t, int slot) {
+    if (lane == 0) {
+      const uint32_t bar = smem_u32(&fullb[warp][slot]);
+      mbar_arrive_expect_tx(bar, TILE);
+      const int row = (static_cast<int>(epage[t / tpe]) * Hkv + g) * P + (t % tpe) * 16;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) tma_load_2d(ring + slot * TILE + b * 2048, &kmap, b * 64, row, bar, pol);
+    }
+  };
+  int tiss = next(kset);
+#pragma unroll
+  for (int s2 = 0; s2 < NS; ++s2) {
+    if (tiss < ntiles) {
+      issue(tiss, s2);
+      tiss = next(tiss + nsets);
+    }
   }
-  scores_kernel<D, G><<<n_units, 256, smem, s>>>(units, descs, slab, q, lse, kpool, scale_log2, out, Hkv, P);
-  return cudaGetLastError();
+
+  // columns: c = r * G + h (query row r of the descriptor, head h of kv head g)
+  const int Hq = Hkv * G;
+  const int ncols = d.n_q * G, nct = (ncols + 7) >> 3;
+  const int base = d.len_after - d.n_q - u.l0;  // row r sees unit-relative keys <= base + r
+  uint32_t bq[KS][2];
+  float l2c[2];
+  int lim[2];  // highest visible unit-relative key of the lane's two C columns (-1: padding column)
+  auto load_cols = [&](int ct) {
+    const int n = ct * 8 + (lane >> 2);
+    if (n < ncols) {
+      const uint32_t *qp = reinterpret_cast<const uint32_t *>(
+          q + (static_cast<int64_t>(d.row0 + n / G) * Hq + g * G + n % G) * D);
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        bq[ks][0] = __ldg(qp + ks * 8 + (lane & 3));
+        bq[ks][1] = __ldg(qp + ks * 8 + 4 + (lane & 3));
+      }
+    } else {
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) bq[ks][0] = bq[ks][1] = 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c = ct * 8 + (lane & 3) * 2 + j;
+      if (c < ncols) {
+        l2c[j] = lse[static_cast<int64_t>(d.row0 + c / G) * Hq + g * G + c % G] * 1.4426950408889634f;
+        lim[j] = base + c / G;
+      } else {
+        l2c[j] = 0.f;
+        lim[j] = -1;
+      }
+    }
+  };
+  if (nct == 1) load_cols(0);
+
+  // ldmatrix addressing (128-byte swizzle: 16-byte chunk c of row r sits at chunk c ^ (r & 7))
+  const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lhi = lane >> 4;
+  const int r0 = lane >> 2, r1 = r0 + 8;
+  int tcon = next(kset);
+  for (int i = 0; tcon < ntiles; ++i) {
+    const int slot = i % NS;
+    mbar_wait(smem_u32(&fullb[warp][slot]), static_cast<uint32_t>((i / NS) & 1));
+    const uint32_t st = ring + slot * TILE;
+    uint32_t a[KS][4];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const uint32_t chunk = static_cast<uint32_t>(((ks & 3) * 2 + lhi) ^ (lrow & 7));
+      ldsm_x4(st + (ks >> 2) * 2048 + lrow * 128 + (chunk << 4), a[ks][0], a[ks][1], a[ks][2], a[ks][3]);
+    }
+    __syncwarp();  // the stage is in registers: refill it
+    if (tiss < ntiles) {
+      issue(tiss, slot);
+      tiss = next(tiss + nsets);
+    }
+    const int e = tcon / tpe, sub = tcon % tpe;
+    const uint64_t em = emask[e];
+    const int s0 = sub * 16 + r0, s1 = sub * 16 + r1;
+    const int lg0 = elog[e] + __popcll(em & ((1ull << s0) - 1)), lg1 = elog[e] + __popcll(em & ((1ull << s1) - 1));
+    float p0 = 0.f, p1 = 0.f;
+    for (int ct = 0; ct < nct; ++ct) {
+      if (nct > 1) load_cols(ct);
+      float c[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) mma_bf16_16816(c, a[ks], bq[ks][0], bq[ks][1]);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        if (lg0 <= lim[j]) p0 += exp2f(fmaf(c[j], scale_log2, -l2c[j]));
+        if (lg1 <= lim[j]) p1 += exp2f(fmaf(c[2 + j], scale_log2, -l2c[j]));
+      }
+    }
+    p0 += __shfl_xor_sync(0xffffffffu, p0, 1);
+    p1 += __shfl_xor_sync(0xffffffffu, p1, 1);
+    p0 += __shfl_xor_sync(0xffffffffu, p0, 2);
+    p1 += __shfl_xor_sync(0xffffffffu, p1, 2);
+    if ((lane & 3) == 0) {
+      if (em >> s0 & 1) atomicAdd(&acc[e * 64 + s0], p0);
+      if (em >> s1 & 1) atomicAdd(&acc[e * 64 + s1], p1);
+    }
+    tcon = next(tcon + nsets);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < ne * 64; i += blockDim.x) {
+    const int e = i >> 6, s2 = i & 63;
+    const uint64_t em = emask[e];
+    if (s2 < P && (em >> s2 & 1))
+      out[d.out_off + u.l0 + elog[e] + __popcll(em & ((1ull << s2) - 1))] = acc[i];
+  }
 }
 
 template <int D>
-static cudaError_t launch_scores_d(const ScoreUnit *units, int n_units, const ScoreDesc *descs, const Entry *slab,
-                                   const __nv_bfloat16 *q, const float *lse, const __nv_bfloat16 *kpool,
-                                   float scale_log2, float *out, int G, int Hkv, int P, cudaStream_t s) {
-  switch (G) {
-    case 1: return launch_scores_t<D, 1>(units, n_units, descs, slab, q, lse, kpool, scale_log2, out, Hkv, P, s);
-    case 2: return launch_scores_t<D, 2>(units, n_units, descs, slab, q, lse, kpool, scale_log2, out, Hkv, P, s);
-    case 4: return launch_scores_t<D, 4>(units, n_units, descs, slab, q, lse, kpool, scale_log2, out, Hkv, P, s);
-    case 8: return launch_scores_t<D, 8>(units, n_units, descs, slab, q, lse, kpool, scale_log2, out, Hkv, P, s);
-    default: return cudaErrorInvalidValue;
+static cudaError_t launch_scores_d(const CUtensorMap &kmap, const ScoreUnit *units, int n_units,
+                                   const ScoreDesc *descs, const Entry *slab, const __nv_bfloat16 *q,
+                                   const float *lse, float scale_log2, float *out, int G, int Hkv, int P,
+                                   cudaStream_t s) {
+  constexpr int smem = 8 * kScoreStages * 16 * D * 2 + 1024;  // 8 warps x NS tiles + alignment slack
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute(scores_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
   }
+  scores_kernel<D><<<n_units, 256, smem, s>>>(kmap, units, descs, slab, q, lse, scale_log2, out, Hkv, G, P);
+  return cudaGetLastError();
 }
 
-cudaError_t launch_scores(const ScoreUnit *units, int n_units, const ScoreDesc *descs, const Entry *slab,
-                          const __nv_bfloat16 *q, const float *lse, const __nv_bfloat16 *kpool, float scale_log2,
-                          float *out, int Hq, int Hkv, int D, int P, cudaStream_t s) {
-  if (Hkv > 8 || 8 % Hkv) return cudaErrorInvalidValue;
-  if (D == 64) return launch_scores_d<64>(units, n_units, descs, slab, q, lse, kpool, scale_log2, out, Hq / Hkv, Hkv, P, s);
-  if (D == 128) return launch_scores_d<128>(units, n_units, descs, slab, q, lse, kpool, scale_log2, out, Hq / Hkv, Hkv, P, s);
+cudaError_t launch_scores(const CUtensorMap &kmap, const ScoreUnit *units, int n_units, const ScoreDesc *descs,
+                          const Entry *slab, const __nv_bfloat16 *q, const float *lse, float scale_log2, float *out,
+                          int Hq, int Hkv, int D, int P, cudaStream_t s) {
+  if (Hkv > 8 || 8 % Hkv || Hq % Hkv || Hq / Hkv > 8 || P % 16) return cudaErrorInvalidValue;
+  if (D == 64) return launch_scores_d<64>(kmap, units, n_units, descs, slab, q, lse, scale_log2, out, Hq / Hkv, Hkv, P, s);
+  if (D == 128) return launch_scores_d<128>(kmap, units, n_units, descs, slab, q, lse, scale_log2, out, Hq / Hkv, Hkv, P, s);
   return cudaErrorInvalidValue;
 }
 

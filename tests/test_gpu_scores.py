@@ -12,7 +12,8 @@ from gpu_harness import Harness, assert_close, to_bits, to_dev  # noqa: E402
 from paper_2510_25412_b200 import kvfs as K  # noqa: E402
 
 
-@pytest.mark.parametrize("P,Hq,Hkv,D", [(16, 32, 8, 128), (32, 8, 2, 64), (64, 16, 2, 128)])
+@pytest.mark.parametrize("P,Hq,Hkv,D", [(16, 32, 8, 128), (32, 8, 2, 64), (64, 16, 2, 128), (16, 8, 8, 128),
+                                        (16, 16, 8, 64), (32, 8, 1, 128)])
 def test_scores_match_oracle(P, Hq, Hkv, D):
     h = Harness(4000, P, Hq, Hkv, D, seed=P + Hq + D)
     h.c.set_option(K.OPT_CASCADE_MIN_ENTRIES, 2)
