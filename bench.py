@@ -41,6 +41,10 @@ def parse():
     ap.add_argument("--real-scores", action="store_true",
                     help="cfg5hh: pick the evicted tokens by the H2O scores of a decode step (pred_attn_scores) "
                          "instead of synthetic Exp(1) scores")
+    ap.add_argument("--prefix-splits", type=int, default=0,
+                    help="cascade tuning: key splits per shared run (KVFS_OPT_PREFIX_SPLITS; 0 = auto)")
+    ap.add_argument("--decode-ctas", type=int, default=0,
+                    help="tuning: decode-kernel ring count (KVFS_OPT_DECODE_CTAS; 0 = auto)")
     ap.add_argument("--scores", action="store_true",
                     help="also run pred_attn_scores (NEXT-2, H2O score accumulation) every timed step")
     return ap.parse_args()
@@ -245,6 +249,10 @@ def run_ours(args):
     W, Kst = args.warmup, args.steps
     n_e2e = 0 if args.no_e2e else Kst
     wl = DecodeWorkload(args.config, steps_total=W + Kst + n_e2e + 1, device=local)
+    if args.prefix_splits:
+        wl.kv.set_option(K.OPT_PREFIX_SPLITS, args.prefix_splits)
+    if args.decode_ctas:
+        wl.kv.set_option(K.OPT_DECODE_CTAS, args.decode_ctas)
     s = wl.shape
     kv = wl.kv
     T = wl.n_files * wl.n_q

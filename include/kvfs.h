@@ -316,7 +316,8 @@ typedef enum {
                                    many identical (page, mask) entries, all before their new tokens, have
                                    that run attended ONCE per batch by the tcgen05 kernel over all sharers'
                                    query rows, and the per-file rest by the decode kernel, merged exactly
-                                   (log-sum-exp).  0 = off; default 16 (head_dim 128 only) */
+                                   (log-sum-exp).  0 = off; default 16 (head_dim 128 only) */,
+  KVFS_OPT_PREFIX_SPLITS = 5    /* key splits of each shared run in the cascade (1..8); 0 = auto */
 } kvfs_option;
 int kvfs_set_option(kvfs_ctx *ctx, int option, int64_t value);
 

@@ -190,7 +190,7 @@ namespace kvfs {
 // attended once per (family, kv head, key split) with all members' query rows as the M dimension of the
 // tcgen05 kernel, and every member's decode unit starts after the run and merges the prefix partials
 // (exact: softmax over a disjoint union of key sets = log-sum-exp merge of the parts).
-void pred_cascade(const Ctx &c, int64_t min_entries, int sms, int64_t max_partials, PredPlan *plan) {
+void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, int64_t max_partials, PredPlan *plan) {
   PredPlan &pl = *plan;
   pl.prefix_descs.clear();
   pl.prefix_units.clear();
@@ -246,6 +246,7 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int sms, int64_t max_partia
     rows_all += u.rows;
   }
   int S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kMaxPrefixSplits, sms / std::max<int64_t>(1, units_per_split))));
+  if (force_splits > 0) S = std::min(force_splits, kMaxPrefixSplits);
   while (S > 1 && rows_all * Hkv * S > max_partials) --S;
   if (rows_all * Hkv * S > max_partials) return;  // workspace too small: no cascade
   for (Fam &u : use) {

@@ -321,7 +321,8 @@ int pred_step_begin(kvfs_ctx *ctx, const pred_desc *descs, int n_desc, const int
   if (rc != KVFS_OK && rc != KVFS_EPARTIAL) return rc;
   if (c.dev) {
     pred_split(c, c.opt_chunk_cutover, &c.plan);
-    pred_cascade(c, c.opt_cascade_min_entries, c.dev->sms(), c.dev->prefix_partial_capacity(), &c.plan);
+    pred_cascade(c, c.opt_cascade_min_entries, c.opt_prefix_splits, c.dev->sms(), c.dev->prefix_partial_capacity(),
+                 &c.plan);
   }
   if (c.dev) {
     const int drc = c.dev->pred_begin(c.plan, stream);
@@ -538,6 +539,10 @@ int kvfs_set_option(kvfs_ctx *ctx, int option, int64_t value) {
     case KVFS_OPT_CASCADE_MIN_ENTRIES:
       if (value < 0) return KVFS_EINVAL;
       c.opt_cascade_min_entries = value;
+      return KVFS_OK;
+    case KVFS_OPT_PREFIX_SPLITS:
+      if (value < 0 || value > kMaxPrefixSplits) return KVFS_EINVAL;
+      c.opt_prefix_splits = static_cast<int>(value);
       return KVFS_OK;
     default:
       return KVFS_EINVAL;

@@ -172,6 +172,7 @@ struct Ctx {
   int64_t opt_decode_ctas = 0;
   int64_t opt_chunk_cutover = 8;
   int64_t opt_cascade_min_entries = 16;
+  int opt_prefix_splits = 0;  // 0 = auto
   CtxCounters ctr;
   PredPlan plan;  // the open step's plan
   std::vector<int> step_status;
@@ -219,7 +220,8 @@ void pred_split(const Ctx &c, int64_t cutover, PredPlan *plan);
 // Shared-prefix plan for the K1 list (KVFS_OPT_CASCADE_MIN_ENTRIES): groups descriptors whose files start
 // with the same run of (page, mask) entries, sets their skip / pref_* fields and emits the prefix work.
 // `sms` sizes the key splits, `max_partials` is the workspace capacity in partials.
-void pred_cascade(const Ctx &c, int64_t min_entries, int sms, int64_t max_partials, PredPlan *plan);
+// force_splits > 0: key splits per shared run (else chosen from the SM count)
+void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, int64_t max_partials, PredPlan *plan);
 
 // ---- data plane interface (implemented in csrc/cuda/device.cu)
 class Device {

@@ -23,7 +23,7 @@ EPOS, EPARTIAL, EOFFLOAD = -1001, -1002, -1003
 HOST_PAGE = 0x80000000
 O_CREAT, O_EXCL = 1, 2
 EVICT_COMPACT = 1
-OPT_DECODE_CTAS, OPT_CHUNK_CUTOVER, OPT_DETERMINISTIC, OPT_CASCADE_MIN_ENTRIES = 1, 2, 3, 4
+OPT_DECODE_CTAS, OPT_CHUNK_CUTOVER, OPT_DETERMINISTIC, OPT_CASCADE_MIN_ENTRIES, OPT_PREFIX_SPLITS = 1, 2, 3, 4, 5
 CTR_KERNEL_LAUNCHES, CTR_H2D_BYTES, CTR_PAGE_COPIES, CTR_LAST_DECODE_CTAS, CTR_LAST_CHUNK_UNITS = 1, 2, 3, 4, 5
 CTR_LAST_PREFIX_UNITS, CTR_LAST_PREFIX_GROUPS, CTR_HOST_PAGES = 6, 7, 8
 
