@@ -614,13 +614,17 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           const int64_t idx = pr.pref_base + static_cast<int64_t>(u.g * pr.n_q + pr.qi) * pd.n_splits + pd.split;
           dst = p.ppart + idx * (G * (HD + 2)) + h * (HD + 2);
         }
-#pragma unroll 1
+        // the TMEM load of chunk c + 1 is in flight while chunk c is stored
+        float va[32], vb[32];
+        tmem_ld32(o_col, va);
+#pragma unroll
         for (int c = 0; c < HD / 32; ++c) {
-          float v[32];
-          tmem_ld32(o_col + c * 32, v);
+          float(&v)[32] = (c & 1) ? vb : va;
+          float(&vn)[32] = (c & 1) ? va : vb;
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 32; ++i) buf[lane * 33 + i] = v[i];
+          if (c + 1 < HD / 32) tmem_ld32(o_col + (c + 1) * 32, vn);
           __syncwarp();
 #pragma unroll
           for (int it = 0; it < 16; ++it) {  // (D + 2)-float rows are 8-byte aligned: float2, 2 rows per store

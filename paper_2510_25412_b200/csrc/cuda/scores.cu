@@ -20,7 +20,13 @@ namespace dev {
 // tile is exp2(s * scale_log2 - lse_col * log2 e) for the visible (key, row) pairs, summed over the lane's
 // columns, reduced over the 4 lanes of a row, and added into the key's shared-memory accumulator.
 // Holes of a partially retained tile are read (one TMA box) and masked out of the sums.
-constexpr int kScoreStages = 3;
+#ifndef KVFS_K9_NS
+#define KVFS_K9_NS 2
+#endif
+#ifndef KVFS_K9_MINB
+#define KVFS_K9_MINB 3
+#endif
+constexpr int kScoreStages = KVFS_K9_NS;  // ring stages per warp (2 x 4 KB x 8 warps: three CTAs per SM)
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t &a0, uint32_t &a1, uint32_t &a2, uint32_t &a3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
@@ -38,7 +44,7 @@ __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a
 }
 
 template <int D>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, KVFS_K9_MINB)
     scores_kernel(const __grid_constant__ CUtensorMap kmap, const ScoreUnit *units, const ScoreDesc *descs,
                   const Entry *slab, const __nv_bfloat16 *q, const float *lse, float scale_log2, float *out, int Hkv,
                   int G, int P) {
