@@ -622,16 +622,19 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           float(&v)[32] = (c & 1) ? vb : va;
           float(&vn)[32] = (c & 1) ? va : vb;
           tmem_wait_ld();
+          if (m == 0 && wq == 0 && lane == 0) K2T(30, c);
 #pragma unroll
           for (int i = 0; i < 32; ++i) buf[lane * 33 + i] = v[i];
           if (c + 1 < HD / 32) tmem_ld32(o_col + (c + 1) * 32, vn);
           __syncwarp();
+          if (m == 0 && wq == 0 && lane == 0) K2T(31, c);
 #pragma unroll
           for (int it = 0; it < 16; ++it) {  // (D + 2)-float rows are 8-byte aligned: float2, 2 rows per store
             const int rr = it * 2 + (lane >> 4), j = (lane & 15) * 2;
             float *d = reinterpret_cast<float *>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dst), rr));
 #ifndef KVFS_K2_NOSTORE
-            if (d) *reinterpret_cast<float2 *>(d + c * 32 + j) = make_float2(buf[rr * 33 + j], buf[rr * 33 + j + 1]);
+            // st.global: a generic store could alias buf and serialised the loop (~70 clk per iteration)
+            if (d) __stcg(reinterpret_cast<float2 *>(d + c * 32 + j), make_float2(buf[rr * 33 + j], buf[rr * 33 + j + 1]));
 #else
             if (d && buf[rr * 33 + j] == 12345.f) *reinterpret_cast<float2 *>(d + c * 32 + j) = make_float2(1.f, 2.f);
 #endif

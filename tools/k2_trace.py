@@ -46,6 +46,9 @@ def main():
               % tuple(int(buf[0, e, 0]) - t0 if buf[0, e, 0] else -1 for e in (25, 14, 26, 27)))
     if t0:
         print("epilogue stamps (clk from start):", [int(buf[0, 28, c]) - t0 for c in range(5)])
+        if buf[0, 30, 0]:
+            print("  prefix epilogue per chunk: TMEM data ready", [int(buf[0, 30, c]) - t0 for c in range(4)],
+                  "staged", [int(buf[0, 31, c]) - t0 for c in range(4)])
     st, en, sm = buf[1, 30].astype(np.int64), buf[1, 31].astype(np.int64), buf[1, 29].astype(np.int64)
     nb = int((en > 0).sum())
     if nb and os.environ.get("CTA_TIMES"):
