@@ -5,6 +5,10 @@
 
 #include "kvfs_impl.h"
 
+#ifndef KVFS_SCORE_UNIT_ENTRIES
+#define KVFS_SCORE_UNIT_ENTRIES 32  // page entries per K9 CTA (<= 32: the kernel's accumulator rows)
+#endif
+
 using namespace kvfs;
 
 namespace {
@@ -369,7 +373,8 @@ int pred_attn_scores(kvfs_ctx *ctx, pred_step *step, int layer, const void *q, c
     const int32_t di = static_cast<int32_t>(sd.size());
     sd.push_back({x.slab_off, x.n_q, x.row0, static_cast<int32_t>(f.len), score_off[x.batch_idx]});
     const int32_t ne = static_cast<int32_t>(f.table.size());
-    for (int32_t e0 = 0; e0 < ne; e0 += 32) su.push_back({di, e0, std::min(ne, e0 + 32), f.table[e0].lstart});
+    for (int32_t e0 = 0; e0 < ne; e0 += KVFS_SCORE_UNIT_ENTRIES)
+      su.push_back({di, e0, std::min(ne, e0 + KVFS_SCORE_UNIT_ENTRIES), f.table[e0].lstart});
   }
   const int rc = c.dev->scores(sd, su, layer, q, lse, scale, scores, stream);
   if (rc != KVFS_OK) c.poisoned = true;
