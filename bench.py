@@ -325,13 +325,32 @@ def run_ours(args):
     # Pipelined like a serving loop: the H2D of step i+1 (copy stream) and the D2H of step i-1 (second copy
     # stream) overlap the pred of step i (compute stream); double-buffered device inputs / outputs, ordered
     # by events.  Every step still moves its full inputs in and its full result out inside the timed region.
+    # A step's Q / K_new / V_new live in one packed buffer (one H2D copy) and its out / lse in another (one
+    # D2H copy); the C ABI takes views into them.
     e2e = None
     if n_e2e:
-        ring = [tuple(x.cpu().pin_memory() for x in inputs[i % len(inputs)]) for i in range(4)]
-        dev_in = [tuple(torch.empty_like(x) for x in inputs[0]) for _ in range(2)]
-        dev_out = [(torch.empty_like(out), torch.empty_like(lse)) for _ in range(2)]
-        host_out = [(torch.empty(out.shape, dtype=out.dtype, pin_memory=True),
-                     torch.empty(lse.shape, dtype=lse.dtype, pin_memory=True)) for _ in range(2)]
+        def packed(shapes_dtypes, pin):
+            sizes = [int(np.prod(sh)) * torch.empty((), dtype=dt).element_size() for sh, dt in shapes_dtypes]
+            offs = np.concatenate([[0], np.cumsum([(z + 255) // 256 * 256 for z in sizes])]).astype(int)
+            buf = (torch.empty(int(offs[-1]), dtype=torch.uint8, pin_memory=True) if pin
+                   else torch.empty(int(offs[-1]), dtype=torch.uint8, device="cuda"))
+            views = tuple(buf[o:o + z].view(dt).view(sh) for (sh, dt), o, z in zip(shapes_dtypes, offs, sizes))
+            return buf, views
+
+        in_sd = [(tuple(x.shape), x.dtype) for x in inputs[0]]
+        out_sd = [(tuple(out.shape), out.dtype), (tuple(lse.shape), lse.dtype)]
+        ring_p = []
+        for i in range(4):
+            buf, views = packed(in_sd, True)
+            for dst, src in zip(views, inputs[i % len(inputs)]):
+                dst.copy_(src.cpu())
+            ring_p.append(buf)
+        dev_in_p = [packed(in_sd, False) for _ in range(2)]
+        dev_out_p = [packed(out_sd, False) for _ in range(2)]
+        host_out_p = [packed(out_sd, True) for _ in range(2)]
+        dev_in = [v for _, v in dev_in_p]
+        dev_out = [v for _, v in dev_out_p]
+        host_out = [v for _, v in host_out_p]
         cs = torch.cuda.current_stream()
         h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
         ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "used", "done", "d2h")}
@@ -348,8 +367,7 @@ def run_ours(args):
             with torch.cuda.stream(h2d_s):
                 if i >= 2:
                     h2d_s.wait_event(ev["used"][b])  # pred i-2 finished reading buffer b
-                for d, hsrc in zip(dev_in[b], ring[i % 4]):
-                    d.copy_(hsrc, non_blocking=True)
+                dev_in_p[b][0].copy_(ring_p[i % 4], non_blocking=True)
                 ev["in"][b].record(h2d_s)
 
         issue_h2d(0)
@@ -367,8 +385,7 @@ def run_ours(args):
             ev["done"][b].record(cs)
             with torch.cuda.stream(d2h_s):
                 d2h_s.wait_event(ev["done"][b])
-                host_out[b][0].copy_(dev_out[b][0], non_blocking=True)
-                host_out[b][1].copy_(dev_out[b][1], non_blocking=True)
+                host_out_p[b][0].copy_(dev_out_p[b][0], non_blocking=True)
                 ev["d2h"][b].record(d2h_s)
             wl.advance()
         cs.wait_stream(d2h_s)
@@ -378,13 +395,13 @@ def run_ours(args):
         et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        h2d_b = sum(x.numel() * x.element_size() for x in ring[0])
-        d2h_b = sum(x.numel() * x.element_size() for x in host_out[0])
+        h2d_b = int(ring_p[0].numel())
+        d2h_b = int(host_out_p[0][0].numel())
         e2e = {"value": world * T * n_e2e / (float(et.item()) / 1000.0), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b, "steps": n_e2e,
-               "note": "pinned host Q/K_new/V_new -> device (copy stream), pred_attn_batch via the C ABI "
-                       "(compute stream), out+lse -> pinned host (second copy stream); steps pipelined with "
-                       "double-buffered device inputs / outputs"}
+               "note": "pinned host Q/K_new/V_new (one packed buffer) -> device (copy stream), pred_attn_batch "
+                       "via the C ABI on views of it (compute stream), out+lse (one packed buffer) -> pinned host "
+                       "(second copy stream); steps pipelined with double-buffered device inputs / outputs"}
 
     if rank != 0:
         if world > 1:
