@@ -111,31 +111,34 @@ class DecodeWorkload:
         self.step += 1
 
     # ------------------------------------------------------------------ accounting
-    def logical_kv_bytes(self) -> int:
+    def logical_kv_bytes(self, lens=None) -> int:
         s = self.shape
-        return int(2 * self.lens.sum() * s.Hkv * s.D * 2)
+        lens = self.lens if lens is None else lens
+        return int(2 * lens.sum() * s.Hkv * s.D * 2)
 
-    def unique_kv_bytes(self) -> int:
+    def unique_kv_bytes(self, lens=None) -> int:
         """K/V bytes of the distinct retained rows the batch reads (a CoW-shared prefix counted once)."""
         s = self.shape
+        lens = self.lens if lens is None else lens
         row_kv = s.Hkv * s.D * 2
         if not self.prefix_len:
-            return int(2 * self.lens.sum() * row_kv)
-        return int(2 * (self.prefix_len + (self.lens - self.prefix_len).sum()) * row_kv)
+            return int(2 * lens.sum() * row_kv)
+        return int(2 * (self.prefix_len + (lens - self.prefix_len).sum()) * row_kv)
 
-    def algorithmic_bytes(self) -> int:
+    def algorithmic_bytes(self, lens=None) -> int:
         """Bytes one pred step must move: every unique retained K/V row read once (the old tokens; the new
         rows come from K_new), Q read, out + lse written, new K/V read once and written once."""
         s = self.shape
         row_kv = s.Hkv * s.D * 2
         T = self.n_files * self.n_q
-        return (self.unique_kv_bytes() + T * s.Hq * s.D * 2 + T * s.Hq * s.D * 2 + T * s.Hq * 4
+        return (self.unique_kv_bytes(lens) + T * s.Hq * s.D * 2 + T * s.Hq * s.D * 2 + T * s.Hq * 4
                 + 2 * 2 * T * row_kv)
 
-    def flops(self) -> int:
+    def flops(self, lens=None) -> int:
         s = self.shape
         n = self.n_q
-        return int(4 * s.Hq * s.D * (n * int(self.lens.sum()) + self.n_files * (n * (n + 1) // 2)))
+        lens = self.lens if lens is None else lens
+        return int(4 * s.Hq * s.D * (n * int(lens.sum()) + self.n_files * (n * (n + 1) // 2)))
 
     def dominant_kernel(self) -> str:
         if self.n_q >= 8:
