@@ -3,6 +3,7 @@
 // descriptor list, per-row destination slots of the append, copy-on-write copies, and the slab
 // updates (table deltas) of the files in the batch.
 #include <algorithm>
+#include <cstring>
 #include <unordered_map>
 
 #include "kvfs_impl.h"
@@ -223,13 +224,18 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, 
   for (size_t k = 0; k < fam.size(); ++k) {
     const std::vector<int> &m = fam[k];
     if (m.size() < 2) continue;
-    const File *lf = pl.desc_files[m[0]];
+    const Entry *lead = pl.desc_files[m[0]]->table.data();
     int E = pl.descs[m[0]].first_new_entry;
     for (size_t j = 1; j < m.size() && E > 0; ++j) {
-      const File *f = pl.desc_files[m[j]];
+      const Entry *b = pl.desc_files[m[j]]->table.data();
       const int lim = std::min(E, pl.descs[m[j]].first_new_entry);
-      int e = 0;
-      while (e < lim && f->table[e].page == lf->table[e].page && f->table[e].mask == lf->table[e].mask) ++e;
+      // a shared run has identical entries (page, mask and so the logical start): one memcmp in the common
+      // case, the (page, mask) scan only when it differs somewhere
+      int e = lim;
+      if (std::memcmp(lead, b, static_cast<size_t>(lim) * sizeof(Entry)) != 0) {
+        e = 0;
+        while (e < lim && b[e].page == lead[e].page && b[e].mask == lead[e].mask) ++e;
+      }
       E = e;
     }
     if (E < min_entries) continue;
