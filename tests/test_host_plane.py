@@ -73,6 +73,22 @@ class Pair:
         self.o.audit()
 
 
+def test_options_validate():
+    """kvfs_set_option: every knob accepts its documented range and rejects the rest (include/kvfs.h)."""
+    k = K.KVFS(1, 8, 2, 64, 16, 32, device=-1)
+    for opt, good, bad in ((K.OPT_DECODE_CTAS, [0, 1, 4096], [-1, 4097]),
+                           (K.OPT_CHUNK_CUTOVER, [0, 8, 1 << 20], [-1]),
+                           (K.OPT_CASCADE_MIN_ENTRIES, [0, 16], [-1]),
+                           (K.OPT_PREFIX_SPLITS, [0, 1, 8], [-1, 9])):
+        for v in good:
+            k.set_option(opt, v)
+        for v in bad:
+            with pytest.raises(K.KvfsError):
+                k.set_option(opt, v)
+    with pytest.raises(K.KvfsError):
+        k.set_option(99, 0)
+
+
 def test_golden_trace_c7_host_plane():
     g = json.load(open(os.path.join(ROOT, "tests", "golden", "c7_trace.json")))
     c = K.KVFS(1, 8, 2, 64, 16, 96, device=-1)
