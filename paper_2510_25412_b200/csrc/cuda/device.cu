@@ -148,15 +148,16 @@ __device__ __forceinline__ int find_entry(const dev::Entry *t, int n, int64_t i)
 }
 
 // K5: token i of the old table (logical order) -> (new_pages[i / P], i % P), every layer, K and V.
-// One CTA per (destination page, layer): the P source (page, slot) pairs are resolved once into shared
-// memory, then the CTA streams the page's Hkv x P rows of K and V with 16-byte vectors (4 loads in flight
+// A CTA per (destination page, layer), grid-stride over the pages: the P source (page, slot) pairs are
+// resolved once into shared memory, then the CTA streams the page's Hkv x P rows of K and V with 16-byte vectors (4 loads in flight
 // per thread before the stores).
 __global__ void __launch_bounds__(256) compact_kernel(const dev::Entry *old, int n_old, const uint32_t *new_pages,
-                                                      int64_t len, bf16 *const *kp, bf16 *const *vp, int L, int Hkv,
-                                                      int D, int P) {
+                                                      int n_new, int64_t len, bf16 *const *kp, bf16 *const *vp, int L,
+                                                      int Hkv, int D, int P) {
   __shared__ uint32_t src_page[64];
   __shared__ int src_slot[64];
-  const int j = blockIdx.x, l = blockIdx.y;
+  const int l = blockIdx.y;
+  for (int j = blockIdx.x; j < n_new; j += gridDim.x) {  // grid-stride over destination pages
   const int64_t i0 = static_cast<int64_t>(j) * P;
   const int ntok = static_cast<int>(len - i0 < P ? len - i0 : static_cast<int64_t>(P));
   if (threadIdx.x < ntok) {
@@ -195,6 +196,8 @@ __global__ void __launch_bounds__(256) compact_kernel(const dev::Entry *old, int
         *reinterpret_cast<uint4 *>(vd + po[u]) = vr[u];
       }
     }
+  }
+  __syncthreads();  // src_page / src_slot are rewritten for the next destination page
   }
 }
 
@@ -339,10 +342,14 @@ class CudaDevice final : public Device {
     if (!dt || !dp) return KVFS_ENOMEM;
     if (!send(s)) return KVFS_EIO;
     const kvfs_config &cfg = c_.cfg;
-    const dim3 grid(static_cast<unsigned>(new_pages.size()), static_cast<unsigned>(cfg.n_layers));
+    // one wave: up to 8 resident CTAs per SM, each looping over destination pages (a file of ~2k pages
+    // was 1.7 waves of one-page CTAs)
+    const int64_t per_layer = std::max<int64_t>(1, static_cast<int64_t>(sms_) * 8 / cfg.n_layers);
+    const dim3 grid(static_cast<unsigned>(std::min<int64_t>(static_cast<int64_t>(new_pages.size()), per_layer)),
+                    static_cast<unsigned>(cfg.n_layers));
     compact_kernel<<<grid, 256, 0, cs(s)>>>(static_cast<const dev::Entry *>(dt), static_cast<int>(old_table.size()),
-                                            static_cast<const uint32_t *>(dp), len, kptrs_, vptrs_, cfg.n_layers,
-                                            cfg.n_kv_heads, cfg.head_dim, cfg.page_size);
+                                            static_cast<const uint32_t *>(dp), static_cast<int>(new_pages.size()), len,
+                                            kptrs_, vptrs_, cfg.n_layers, cfg.n_kv_heads, cfg.head_dim, cfg.page_size);
     ++c_.ctr.launches;
     return cudaGetLastError() == cudaSuccess ? KVFS_OK : KVFS_EIO;
   }

@@ -3,6 +3,9 @@
 #include <cstring>
 #include <new>
 
+#include <thread>
+#include <atomic>
+#include <algorithm>
 #include "kvfs_impl.h"
 
 #ifndef KVFS_SCORE_UNIT_ENTRIES
@@ -203,6 +206,62 @@ int kvfs_compact(kvfs_ctx *ctx, int fd, kvfs_stream_t stream) {
     rc = c.dev->compact(old_table, new_pages, f->len, stream);
     if (rc != KVFS_OK) c.poisoned = true;
   }
+  return rc;
+}
+
+int kvfs_compact_files(kvfs_ctx *ctx, const int *fds, int n, int *n_done, kvfs_stream_t stream) {
+  KVFS_LOCK_OR(ctx);
+  if (n_done) *n_done = 0;
+  if (n < 0 || (n > 0 && !fds)) return KVFS_EINVAL;
+  if (c.dev && c.poisoned) return KVFS_EIO;
+  std::vector<File *> files(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) {
+    File *f = get_file(c, fds[i]);
+    if (!f) return KVFS_EBADF;
+    if (f->offloaded) return KVFS_EOFFLOAD;
+    files[i] = f;
+  }
+  {  // one file twice would race its deferred position pass
+    std::vector<File *> u(files);
+    std::sort(u.begin(), u.end());
+    if (std::adjacent_find(u.begin(), u.end()) != u.end()) return KVFS_EINVAL;
+  }
+  // pages and tables in order (R1: each file's allocation sees the previous files' releases), each file's
+  // device gather enqueued as it goes; the host position passes afterwards, on worker threads
+  std::vector<std::vector<Entry>> olds(static_cast<size_t>(n));
+  int rc = KVFS_OK, done = 0;
+  for (int i = 0; i < n; ++i) {
+    std::vector<uint32_t> np;
+    rc = compact_file_tables(c, *files[i], &olds[i], &np);
+    if (rc != KVFS_OK) break;
+    ++done;
+    // the device gather of this file before the next file's (stream order): R1 hands the next file the
+    // pages this one just released, so its destinations may be this file's sources
+    if (c.dev && !np.empty()) {
+      rc = c.dev->compact(olds[i], np, files[i]->len, stream);
+      if (rc != KVFS_OK) {
+        c.poisoned = true;
+        break;
+      }
+    }
+  }
+  const int P = c.cfg.page_size;
+  const int nt = static_cast<int>(std::min<unsigned>(8u, std::max(1u, std::thread::hardware_concurrency())));
+  if (done < 4 || nt == 1) {
+    for (int i = 0; i < done; ++i)
+      if (!olds[i].empty()) compact_positions(*files[i], olds[i], P);
+  } else {
+    std::atomic<int> next{0};
+    auto work = [&]() {
+      for (int i = next++; i < done; i = next++)
+        if (!olds[i].empty()) compact_positions(*files[i], olds[i], P);
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto &t : pool) t.join();
+  }
+  if (n_done) *n_done = done;
   return rc;
 }
 

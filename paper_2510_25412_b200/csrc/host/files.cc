@@ -323,20 +323,35 @@ static size_t compress_slots(int32_t *sp, size_t w, size_t r, uint64_t m, int P)
   return compress_slots_scalar(sp, w, r, m, P);
 }
 
-static void compact_commit(Ctx &c, File &f, std::vector<Entry> *old_table, std::vector<uint32_t> *new_pages) {
+// R7 metadata except the positions: ceil(len/P) fresh pages (smallest free first, while the old pages are
+// still held), the new table, the old entries released.  f.spos still follows `old` afterwards.
+static void compact_tables(Ctx &c, File &f, std::vector<Entry> *old, std::vector<uint32_t> *np) {
   const int P = c.cfg.page_size;
   const int64_t len = f.len;
-  if (len == 0) return;
   const int64_t k = (len + P - 1) / P;
-  std::vector<uint32_t> np(static_cast<size_t>(k));
-  c.pool->alloc_n(k, np.data());  // old pages still held: never destinations
-  // positions in logical order, token i -> slot (new[i/P], i%P), compacted in place: the write cursor
-  // (retained tokens before a slot) never passes the slot being read
+  np->resize(static_cast<size_t>(k));
+  c.pool->alloc_n(k, np->data());  // old pages still held: never destinations
+  const uint64_t full = P == 64 ? ~0ull : ((1ull << P) - 1);
+  old->clear();
+  old->swap(f.table);
+  f.table.resize(static_cast<size_t>(k));
+  for (int64_t j = 0; j < k; ++j) {
+    const int64_t cnt = std::min<int64_t>(P, len - j * P);
+    f.table[j] = {(*np)[j], static_cast<int32_t>(j * P), cnt == P ? full : ((1ull << cnt) - 1)};
+  }
+  for (const Entry &e : *old) c.pool->release(e.page);
+  mark_dirty_from(f, 0);
+}
+
+// The positions of a compaction: token i -> slot (new[i/P], i%P), compacted in place from the layout of
+// `old` (the write cursor, retained tokens before a slot, never passes the slot being read).
+void compact_positions(File &f, const std::vector<Entry> &old, int P) {
+  const int64_t k = (f.len + P - 1) / P;
   const uint64_t full = P == 64 ? ~0ull : ((1ull << P) - 1);
   int32_t *sp = f.spos.data();
   size_t w = 0;
-  for (size_t e = 0; e < f.table.size(); ++e) {
-    const uint64_t m = f.table[e].mask;
+  for (size_t e = 0; e < old.size(); ++e) {
+    const uint64_t m = old[e].mask;
     const size_t r = e * static_cast<size_t>(P);
     if (m == full) {
       if (w != r) std::memmove(sp + w, sp + r, sizeof(int32_t) * static_cast<size_t>(P));
@@ -347,16 +362,14 @@ static void compact_commit(Ctx &c, File &f, std::vector<Entry> *old_table, std::
   }
   f.spos.resize(static_cast<size_t>(k) * P);
   std::fill(f.spos.begin() + static_cast<std::ptrdiff_t>(w), f.spos.end(), 0);
+}
+
+static void compact_commit(Ctx &c, File &f, std::vector<Entry> *old_table, std::vector<uint32_t> *new_pages) {
+  if (f.len == 0) return;
   std::vector<Entry> old;
-  old.swap(f.table);
-  f.table.resize(static_cast<size_t>(k));
-  for (int64_t j = 0; j < k; ++j) {
-    const int64_t cnt = std::min<int64_t>(P, len - j * P);
-    f.table[j] = {np[j], static_cast<int32_t>(j * P), cnt == P ? full : ((1ull << cnt) - 1)};
-  }
-  for (const Entry &e : old) c.pool->release(e.page);
-  mark_dirty_from(f, 0);
-  f.len = len;
+  std::vector<uint32_t> np;
+  compact_tables(c, f, &old, &np);
+  compact_positions(f, old, c.cfg.page_size);
   if (old_table) old_table->swap(old);
   if (new_pages) new_pages->swap(np);
 }
@@ -574,6 +587,16 @@ int compact_file(Ctx &c, File &f, std::vector<Entry> *old_table, std::vector<uin
   if (f.len == 0) return KVFS_OK;
   if ((f.len + P - 1) / P > c.pool->n_free()) return KVFS_ENOSPC;
   compact_commit(c, f, old_table, new_pages);
+  return KVFS_OK;
+}
+
+int compact_file_tables(Ctx &c, File &f, std::vector<Entry> *old_table, std::vector<uint32_t> *new_pages) {
+  const int P = c.cfg.page_size;
+  old_table->clear();
+  new_pages->clear();
+  if (f.len == 0) return KVFS_OK;
+  if ((f.len + P - 1) / P > c.pool->n_free()) return KVFS_ENOSPC;
+  compact_tables(c, f, old_table, new_pages);
   return KVFS_OK;
 }
 

@@ -192,6 +192,10 @@ int truncate_file(Ctx &c, File &f, int64_t n);
 int evict_file(Ctx &c, File &f, const int64_t *ranges, int n_ranges, int flags, std::vector<Entry> *old_table,
                std::vector<uint32_t> *new_pages);
 int compact_file(Ctx &c, File &f, std::vector<Entry> *old_table, std::vector<uint32_t> *new_pages);
+// Batched compaction, split in two: the page / table part (sequential: R1 allocation order), then the
+// positions (per file, independent: may run on worker threads) with the old table it returned.
+int compact_file_tables(Ctx &c, File &f, std::vector<Entry> *old_table, std::vector<uint32_t> *new_pages);
+void compact_positions(File &f, const std::vector<Entry> &old, int P);
 // R13 / R14: new file from selected tokens / from the union of parts; src_slots[i] = page * P + slot of the
 // source of token i, new_pages = the file's pages (token i -> (new_pages[i / P], i % P)).  Atomic.
 int extract_file(Ctx &c, File &src, const int64_t *idx, int64_t n, const char *name, int *fd,

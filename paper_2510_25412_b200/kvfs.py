@@ -30,7 +30,8 @@ CTR_LAST_PREFIX_UNITS, CTR_LAST_PREFIX_GROUPS, CTR_HOST_PAGES = 6, 7, 8
 # every symbol include/kvfs.h declares (tests check the library exports all of them)
 EXPORTS = [
     "kvfs_workspace_bytes", "kvfs_init", "kvfs_destroy", "kvfs_strerror", "kvfs_open", "kvfs_close",
-    "kvfs_unlink", "kvfs_fork", "kvfs_truncate", "kvfs_evict", "kvfs_compact", "kvfs_append",
+    "kvfs_unlink", "kvfs_fork", "kvfs_truncate", "kvfs_evict", "kvfs_compact", "kvfs_compact_files",
+    "kvfs_append",
     "pred_attn_batch", "pred_step_begin", "pred_attn_layer", "pred_step_end", "kvfs_stat",
     "kvfs_get_table", "kvfs_get_positions", "kvfs_get_refcounts", "kvfs_free_pages", "kvfs_read",
     "kvfs_audit", "kvfs_set_option", "kvfs_get_counter", "kvfs_pack", "kvfs_unpack", "kvfs_extract",
@@ -89,6 +90,7 @@ def lib():
             "kvfs_truncate": (cint, [vp, cint, i64]),
             "kvfs_evict": (cint, [vp, cint, P(i64), cint, cint, vp]),
             "kvfs_compact": (cint, [vp, cint, vp]),
+            "kvfs_compact_files": (cint, [vp, P(cint), cint, P(cint), vp]),
             "kvfs_extract": (cint, [vp, cint, P(ctypes.c_int64), i64, ctypes.c_char_p, P(cint), vp]),
             "kvfs_merge": (cint, [vp, P(cint), cint, ctypes.c_char_p, P(cint), vp]),
             "kvfs_sched_create": (cint, [P(SchedConfig), P(vp)]),
@@ -248,6 +250,17 @@ class KVFS:
     def compact(self, fd: int, stream=None) -> None:
         st = _stream(stream) if self.device >= 0 else None
         _check(lib().kvfs_compact(self._h, fd, st), "compact")
+
+    def compact_files(self, fds, stream=None) -> int:
+        """kvfs_compact of every fd in order (one call; host position passes on worker threads).  Returns
+        the number of files compacted; raises on an error (files before the failing one stay compacted)."""
+        a = np.ascontiguousarray(np.asarray(list(fds), dtype=np.int32))
+        done = ctypes.c_int(0)
+        st = _stream(stream) if self.device >= 0 else None
+        rc = lib().kvfs_compact_files(self._h, _ptr(a, ctypes.c_int), a.shape[0], ctypes.byref(done), st)
+        if rc != OK:
+            raise KvfsError(rc, f"compact_files ({done.value} done)")
+        return done.value
 
     def extract(self, src_fd: int, indices, name: str, stream=None) -> int:
         """New file `name` with the logical tokens `indices` of src (kvfs_extract)."""

@@ -278,3 +278,33 @@ def test_migration_pack_unpack_two_ctx():
     _, ref, _ = h.o.pred_batch([(h.fds[n][1], 1) for n in names], [r[1][0] for r in rows], q, k_new, v_new,
                                128 ** -0.5)
     assert_close(to_bits(out), ref[0], "migrated decode")
+
+
+def test_compact_files_batched():
+    """kvfs_compact_files = kvfs_compact of each file in order (pages, tables, positions; K/V bit-exact),
+    including forks sharing pages and a two-layer pool."""
+    from paper_2510_25412_b200 import kvfs as K
+    rnd = random.Random(77)
+    h = Harness(3000, 16, 8, 2, 128, seed=77, L=2)
+    names = []
+    for i in range(6):
+        nm = f"f{i}"
+        h.open(nm)
+        h.append(nm, list(range(rnd.randint(40, 500))))
+        names.append(nm)
+    h.fork("f0", "g0")
+    h.fork("f3", "g3")
+    names += ["g0", "g3"]
+    for nm in names:
+        ln = h.o.stat(h.fds[nm][1])[0]
+        a = rnd.randint(0, ln // 2)
+        h.evict(nm, [(a, a + rnd.randint(1, ln // 3))])
+    sel = ["f3", "g0", "f0", "f5", "g3", "f1"]
+    done = h.c.compact_files([h.fds[nm][0] for nm in sel])
+    assert done == len(sel)
+    for nm in sel:
+        h.o.compact(h.fds[nm][1])
+    h.check_meta()
+    h.check_data()
+    with pytest.raises(K.KvfsError):
+        h.c.compact_files([h.fds["f1"][0], h.fds["f1"][0]])

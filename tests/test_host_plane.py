@@ -9,6 +9,7 @@ import re
 import pytest
 
 from oracle import EVICT_COMPACT, KvfsError as OErr, Oracle
+from oracle.kvfs import EOFFLOAD
 from paper_2510_25412_b200 import kvfs as K
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -138,7 +139,8 @@ def run_random(seed, n_ops=200):
     serial = 0
     for step in range(n_ops):
         names = list(pr.fds)
-        op = rnd.choice(["open", "append", "append", "fork", "truncate", "evict", "evictc", "compact", "unlink",
+        op = rnd.choice(["open", "append", "append", "fork", "truncate", "evict", "evictc", "compact", "compact_files",
+                         "unlink",
                          "pred", "pred", "close_reopen", "bad", "extract", "merge", "offload", "restore"])
         if op == "open" or not names:
             name = f"n{step}"
@@ -197,6 +199,20 @@ def run_random(seed, n_ops=200):
             name = rnd.choice(names)
             cfd, ofd = pr.fds[name]
             pr.both(lambda: c.compact(cfd), lambda: o.compact(ofd))
+        elif op == "compact_files":
+            # kvfs_compact_files == kvfs_compact of each file in order, stopping at the first failure
+            sel = rnd.sample(names, rnd.randint(1, len(names)))
+            cfds = [pr.fds[nm][0] for nm in sel]
+
+            def oracle_seq():
+                # include/kvfs.h: an offloaded file fails the whole call before anything is done
+                for nm in sel:
+                    if o._file(pr.fds[nm][1]).host is not None:
+                        raise OErr(EOFFLOAD, "offloaded")
+                for nm in sel:
+                    o.compact(pr.fds[nm][1])
+                return len(sel)
+            pr.both(lambda: c.compact_files(cfds), oracle_seq)
         elif op == "extract":
             src = rnd.choice(names)
             cfd, ofd = pr.fds[src]
