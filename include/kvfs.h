@@ -143,12 +143,13 @@ int kvfs_evict(kvfs_ctx *ctx, int fd, const int64_t *ranges, int n_ranges, int f
  * the file is empty. */
 int kvfs_compact(kvfs_ctx *ctx, int fd, kvfs_stream_t stream);
 
-/* kvfs_compact of fds[0..n) in that order (the same pages, tables and positions as n calls: R1 allocation
- * sees each earlier file's releases), each file's device gather enqueued on `stream` in that order (the
- * next file's destinations may be the pages this one released), then the host position passes on worker
- * threads.  EBADF / EOFFLOAD (nothing done) if an fd is invalid or
- * offloaded, EINVAL if a file appears twice; ENOSPC stops at the first file whose pages are not free, the
- * files before it being compacted.  *n_done (may be NULL) = files compacted. */
+/* Batched compaction (R7 for many files, e.g. a policy compacting every LIP after an eviction sweep,
+ * P:225): kvfs_compact of fds[0..n) in that order (the same pages, tables and positions as n calls: R1
+ * allocation sees each earlier file's releases), each file's device gather enqueued on `stream` in that
+ * order (the next file's destinations may be the pages this one released), then the host position passes
+ * on worker threads.  fds: host [n].  EBADF / EOFFLOAD (nothing done) if an fd is invalid or offloaded,
+ * EINVAL if a file appears twice; ENOSPC stops at the first file whose pages are not free, the files
+ * before it being compacted.  *n_done (host, may be NULL) = files compacted. */
 int kvfs_compact_files(kvfs_ctx *ctx, const int *fds, int n, int *n_done, kvfs_stream_t stream);
 
 /* Append n tokens (R3) without attention (e.g. a prefilled prompt, "fills the file with the KV
