@@ -147,6 +147,10 @@ __device__ __forceinline__ int find_entry(const dev::Entry *t, int n, int64_t i)
   return lo;
 }
 
+#ifndef KVFS_K5_U
+#define KVFS_K5_U 4  // 16-byte K and V loads in flight per thread
+#endif
+
 // K5: token i of the old table (logical order) -> (new_pages[i / P], i % P), every layer, K and V.
 // A CTA per (destination page, layer), grid-stride over the pages: the P source (page, slot) pairs are
 // resolved once into shared memory, then the CTA streams the page's Hkv x P rows of K and V with 16-byte vectors (4 loads in flight
@@ -174,7 +178,7 @@ __global__ void __launch_bounds__(256) compact_kernel(const dev::Entry *old, int
   const int cpr = D / 8;
   const int total = Hkv * ntok * cpr;
   const int64_t dpage = new_pages[j];
-  constexpr int U = 4;
+  constexpr int U = KVFS_K5_U;
   for (int base = threadIdx.x; base < total; base += U * blockDim.x) {
     uint4 kr[U], vr[U];
     int64_t po[U];
