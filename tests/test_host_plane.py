@@ -90,6 +90,40 @@ def test_options_validate():
         k.set_option(99, 0)
 
 
+def test_compact_files_errors():
+    """kvfs_compact_files: a file twice is EINVAL and a bad fd EBADF with nothing done; ENOSPC stops at the
+    first file whose pages are not free, the earlier files compacted (include/kvfs.h)."""
+    P = 16
+    c = K.KVFS(1, 8, 2, 64, P, 10, device=-1)
+    o = Oracle(10, P, store_data=False)
+    fds = {}
+    for nm in ("a", "c"):
+        fds[nm] = (c.open(nm), o.open(nm))
+        c.append(fds[nm][0], list(range(40)))
+        o.append(fds[nm][1], list(range(40)))
+    fds["b"] = (c.fork(fds["a"][0], "b"), o.fork(fds["a"][1], "b"))  # shares a's two full pages
+    for fc, fo in fds.values():
+        c.evict(fc, [(1, 3)])
+        o.evict(fo, [(1, 3)], 0)
+    for bad, code in (([fds["a"][0], fds["a"][0]], K.EINVAL), ([fds["a"][0], 999], K.EBADF)):
+        with pytest.raises(K.KvfsError) as e:
+            c.compact_files(bad)
+        assert e.value.code == code
+    assert c.table(fds["a"][0]) == o.table(fds["a"][1])  # nothing done
+    # 7 of 10 pages in use: a fits (3 new pages) but frees only its own tail page (b still holds the two
+    # shared ones), so b (3 pages) hits ENOSPC; c is not reached
+    with pytest.raises(K.KvfsError) as e:
+        c.compact_files([fds[nm][0] for nm in ("a", "b", "c")])
+    assert e.value.code == K.ENOSPC
+    o.compact(fds["a"][1])
+    with pytest.raises(OErr):
+        o.compact(fds["b"][1])
+    for fc, fo in fds.values():
+        assert c.table(fc) == o.table(fo)
+        assert c.positions(fc) == o.positions(fo)
+    assert c.refcounts() == o.refcnt
+
+
 def test_golden_trace_c7_host_plane():
     g = json.load(open(os.path.join(ROOT, "tests", "golden", "c7_trace.json")))
     c = K.KVFS(1, 8, 2, 64, 16, 96, device=-1)
