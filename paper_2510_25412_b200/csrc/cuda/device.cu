@@ -147,6 +147,9 @@ __device__ __forceinline__ int find_entry(const dev::Entry *t, int n, int64_t i)
   return lo;
 }
 
+#ifndef KVFS_K5_MINB
+#define KVFS_K5_MINB 1  // resident CTAs per SM the register budget is sized for
+#endif
 #ifndef KVFS_K5_U
 #define KVFS_K5_U 4  // 16-byte K and V loads in flight per thread
 #endif
@@ -155,7 +158,7 @@ __device__ __forceinline__ int find_entry(const dev::Entry *t, int n, int64_t i)
 // A CTA per (destination page, layer), grid-stride over the pages: the P source (page, slot) pairs are
 // resolved once into shared memory, then the CTA streams the page's Hkv x P rows of K and V with 16-byte vectors (4 loads in flight
 // per thread before the stores).
-__global__ void __launch_bounds__(256) compact_kernel(const dev::Entry *old, int n_old, const uint32_t *new_pages,
+__global__ void __launch_bounds__(256, KVFS_K5_MINB) compact_kernel(const dev::Entry *old, int n_old, const uint32_t *new_pages,
                                                       int n_new, int64_t len, bf16 *const *kp, bf16 *const *vp, int L,
                                                       int Hkv, int D, int P) {
   __shared__ uint32_t src_page[64];
@@ -348,7 +351,7 @@ class CudaDevice final : public Device {
     const kvfs_config &cfg = c_.cfg;
     // one wave: up to 8 resident CTAs per SM, each looping over destination pages (a file of ~2k pages
     // was 1.7 waves of one-page CTAs)
-    const int64_t per_layer = std::max<int64_t>(1, static_cast<int64_t>(sms_) * 8 / cfg.n_layers);
+    const int64_t per_layer = std::max<int64_t>(1, static_cast<int64_t>(sms_) * 8 / cfg.n_layers);  // >= resident
     const dim3 grid(static_cast<unsigned>(std::min<int64_t>(static_cast<int64_t>(new_pages.size()), per_layer)),
                     static_cast<unsigned>(cfg.n_layers));
     compact_kernel<<<grid, 256, 0, cs(s)>>>(static_cast<const dev::Entry *>(dt), static_cast<int>(old_table.size()),
