@@ -34,6 +34,11 @@
  *     No CUDA call is ever made; calls that need data (pred_attn_batch, pred_attn_layer, kvfs_read)
  *     return KVFS_ENOSYS; kvfs_append / fork / evict / compact update metadata only.
  *   - A CUDA error poisons the ctx: that call and every later data call return KVFS_EIO.
+ *   - No C++ exception crosses this ABI.  If one is raised inside a call (a host allocation failure:
+ *     std::bad_alloc from a table, position or plan vector; std::system_error from a worker thread), the
+ *     call returns KVFS_ENOMEM (allocation) or KVFS_EIO (anything else) and the ctx becomes BROKEN: the
+ *     failed call may have been half-applied, so every later call on that ctx returns KVFS_EIO except
+ *     kvfs_destroy, which still frees it.  (KVFS_OPT_FAULT_INJECT exercises this path in the tests.)
  *
  * Data layout (device)
  *   K and V pools, one pair per layer: [n_pages][n_kv_heads][page_size][head_dim] bf16 ("HND" pages):
@@ -147,8 +152,9 @@ int kvfs_compact(kvfs_ctx *ctx, int fd, kvfs_stream_t stream);
  * P:225): kvfs_compact of fds[0..n) in that order (the same pages, tables and positions as n calls: R1
  * allocation sees each earlier file's releases), each file's device gather enqueued on `stream` in that
  * order (the next file's destinations may be the pages this one released), then the host position passes
- * on worker threads.  fds: host [n].  EBADF / EOFFLOAD (nothing done) if an fd is invalid or offloaded,
- * EINVAL if a file appears twice; ENOSPC stops at the first file whose pages are not free, the files
+ * on worker threads (on the calling thread if none can be started).  fds: host [n].  EBADF / EOFFLOAD
+ * (nothing done) if an fd is invalid or offloaded, EBUSY if a file appears twice (as in a pred batch,
+ * kvfs_merge and kvfs_pack); ENOSPC stops at the first file whose pages are not free, the files
  * before it being compacted.  *n_done (host, may be NULL) = files compacted. */
 int kvfs_compact_files(kvfs_ctx *ctx, const int *fds, int n, int *n_done, kvfs_stream_t stream);
 
@@ -244,10 +250,13 @@ int kvfs_pack(kvfs_ctx *ctx, const int *fds, int n_fds, void *buf_dev, size_t bu
               void *hdr, size_t hdr_cap, size_t *hdr_used, kvfs_stream_t stream);
 /* Create files names[i] from a packed set: n_unique pages are allocated smallest-free first in packed order
  * (R1), buf_dev is scattered into them (device, on `stream`), tables and positions are rebuilt and the
- * refcounts count the sharing within the set.  fds_out[i] receives the new fds.  EINVAL for a malformed
- * header or a shape mismatch, EEXIST if a name exists, ENOSPC if the pages are not free (atomic). */
-int kvfs_unpack(kvfs_ctx *ctx, const void *buf_dev, const void *hdr, size_t hdr_bytes, const char *const *names,
-                int *fds_out, kvfs_stream_t stream);
+ * refcounts count the sharing within the set.  fds_out[i] receives the new fds.  buf_bytes = the size of
+ * buf_dev as received (device ctx: EINVAL, nothing done, if it is smaller than the header's n_unique x
+ * L x 2 x page bytes, e.g. a truncated transfer or a header from another pack; ignored by a host-only
+ * ctx).  EINVAL for a malformed header or a shape mismatch, EEXIST if a name exists, ENOSPC if the
+ * pages are not free (atomic). */
+int kvfs_unpack(kvfs_ctx *ctx, const void *buf_dev, size_t buf_bytes, const void *hdr, size_t hdr_bytes,
+                const char *const *names, int *fds_out, kvfs_stream_t stream);
 
 /* ---------------------------------------------------------------- new files from existing ones
  * PAPER.md §4.2: LIPs "create new files from existing ones by extracting specific token indices with
@@ -326,7 +335,11 @@ typedef enum {
                                    that run attended ONCE per batch by the tcgen05 kernel over all sharers'
                                    query rows, and the per-file rest by the decode kernel, merged exactly
                                    (log-sum-exp).  0 = off; default 16 (head_dim 128 only) */,
-  KVFS_OPT_PREFIX_SPLITS = 5    /* key splits of each shared run in the cascade (1..8); 0 = auto */
+  KVFS_OPT_PREFIX_SPLITS = 5,   /* key splits of each shared run in the cascade (1..8); 0 = auto */
+  KVFS_OPT_FAULT_INJECT = 6     /* tests only: value n > 0 makes the n-th following pass through an
+                                   injection point (mid-way through a pred reservation, after the first
+                                   descriptor is committed; fork; open) throw std::bad_alloc inside the
+                                   library, to exercise the no-exception guarantee above; 0 = off */
 } kvfs_option;
 int kvfs_set_option(kvfs_ctx *ctx, int option, int64_t value);
 

@@ -24,6 +24,7 @@ size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 
 struct WsLayout {
   size_t slab = 0, upload = 0, counters = 0, partials = 0, ptrs = 0, prefix = 0, total = 0, upload_cap = 0;
+  size_t scratch = 0, scratch_cap = 0;  // second upload area: packets sent while a pred step is open
   int64_t prefix_cap = 0;  // shared-prefix partials (PART floats each)
 };
 
@@ -39,6 +40,14 @@ WsLayout ws_layout(const kvfs_config &c) {
                           static_cast<size_t>(c.max_batch_descs) * 96 + static_cast<size_t>(c.max_batch_rows) * 8 +
                           (1u << 20));
   off = align256(off + w.upload_cap);
+  // The open step's plan (descriptors, destination slots, chunk / prefix records) stays in the upload area
+  // until pred_step_end; the only call allowed between the layers of an open step that uploads anything is
+  // pred_attn_scores (every other op is EBUSY), so its packet goes here instead: ScoreDesc (24 B) per
+  // descriptor + one ScoreUnit (16 B) per <= 8..32 table entries of the batch's files (<= table_capacity).
+  w.scratch = off;
+  w.scratch_cap = align256(static_cast<size_t>(c.max_batch_descs) * 48 + static_cast<size_t>(c.table_capacity) * 2 +
+                           (size_t{1} << 16));
+  off = align256(off + w.scratch_cap);
   w.counters = off;
   off = align256(off + static_cast<size_t>(c.max_batch_rows) * c.n_kv_heads * 4);
   w.partials = off;
@@ -363,7 +372,7 @@ class CudaDevice final : public Device {
 
   int scores(const std::vector<ScoreDesc> &descs, const std::vector<ScoreUnit> &units, int layer, const void *q,
              const float *lse, float scale, float *out, kvfs_stream_t s) override {
-    begin_packet();
+    begin_packet(/*scratch=*/true);  // the open step's plan in the upload area must survive (later layers)
     const void *dd = push(descs.data(), descs.size() * sizeof(ScoreDesc));
     const void *du = push(units.data(), units.size() * sizeof(ScoreUnit));
     if (!dd || !du) return KVFS_ENOMEM;
@@ -662,7 +671,11 @@ class CudaDevice final : public Device {
     return true;
   }
 
-  void begin_packet() {
+  // scratch: the packet goes to the second upload area (see WsLayout::scratch), leaving an open step's plan
+  // in the first one intact
+  void begin_packet(bool scratch = false) {
+    area_ = scratch ? upload_ + (lay_.scratch - lay_.upload) : upload_;
+    area_cap_ = scratch ? lay_.scratch_cap : lay_.upload_cap;
     cur_ = (cur_ + 1) % 4;
     Staging &s = stg_[cur_];
     if (s.pending) {
@@ -677,10 +690,10 @@ class CudaDevice final : public Device {
   // pinned buffer at send().
   const void *push(const void *data, size_t bytes) {
     const size_t off = (used_ + 15) & ~static_cast<size_t>(15);
-    if (off + bytes > lay_.upload_cap) return nullptr;
+    if (off + bytes > area_cap_) return nullptr;
     pending_.push_back({data, bytes, off});
     used_ = off + bytes;
-    return upload_ + off;
+    return area_ + off;
   }
 
   bool send(kvfs_stream_t s) {
@@ -694,11 +707,11 @@ class CudaDevice final : public Device {
     // ones by DMA, whose fixed cost is lower (cfg3's 9 KB packet: the extra launch cost ~3 us per step)
     if (n16 * 16 <= st.cap && used_ >= (size_t{16} << 10) && used_ <= (size_t{1} << 20)) {
       const int grid = static_cast<int>(std::min<size_t>((n16 + 255) / 256, 64));
-      upload_kernel<<<grid, 256, 0, cs(s)>>>(reinterpret_cast<uint4 *>(upload_), reinterpret_cast<const uint4 *>(st.dev),
+      upload_kernel<<<grid, 256, 0, cs(s)>>>(reinterpret_cast<uint4 *>(area_), reinterpret_cast<const uint4 *>(st.dev),
                                              static_cast<int64_t>(n16));
       ++c_.ctr.launches;
       if (cudaGetLastError() != cudaSuccess) return false;
-    } else if (cudaMemcpyAsync(upload_, st.host, used_, cudaMemcpyHostToDevice, cs(s)) != cudaSuccess) {
+    } else if (cudaMemcpyAsync(area_, st.host, used_, cudaMemcpyHostToDevice, cs(s)) != cudaSuccess) {
       return false;
     }
     if (cudaEventRecord(st.ev, cs(s)) != cudaSuccess) return false;
@@ -764,6 +777,8 @@ class CudaDevice final : public Device {
   WsLayout lay_;
   dev::Entry *slab_ = nullptr;
   char *upload_ = nullptr;
+  char *area_ = nullptr;  // upload area of the current packet (upload_ or the scratch area)
+  size_t area_cap_ = 0;
   int *counters_ = nullptr;
   float *partials_ = nullptr;
   float *ppart_ = nullptr;

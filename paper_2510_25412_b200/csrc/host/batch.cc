@@ -84,6 +84,7 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
           const int64_t n_old = f->len;
           dst.clear();
           append_commit(c, *f, nq, pos + row0, &dst, &pl.copies);
+          fault_point(c);  // tests: an exception mid-way through a batch (KVFS_OPT_FAULT_INJECT)
           std::copy(dst.begin(), dst.end(), pl.dst_slot.begin() + row0);
           int64_t idx = static_cast<int64_t>(f->table.size()) - 1;
           while (idx >= 0 && f->table[idx].lstart >= n_old) --idx;

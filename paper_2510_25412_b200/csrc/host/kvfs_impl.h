@@ -1,8 +1,10 @@
 // Host control plane of KVFS (no CUDA dependency): files, page tables, the batched-pred reserve and
 // the plan handed to the device data plane.  Rules R1-R11 as in SURVEY.md §8(c) C3 / DESIGN.md.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <memory>
+#include <new>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -167,6 +169,8 @@ struct Ctx {
   Slab slab;
   Device *dev = nullptr;
   bool poisoned = false;
+  std::atomic<bool> broken{false};  // a C++ exception escaped a call (capi.cc guarded): every call is EIO
+  int64_t fault_countdown = 0;       // KVFS_OPT_FAULT_INJECT (tests)
   bool step_open = false;
   int64_t batch_counter = 0;
   int64_t opt_decode_ctas = 0;
@@ -177,6 +181,11 @@ struct Ctx {
   PredPlan plan;  // the open step's plan
   std::vector<int> step_status;
 };
+
+// KVFS_OPT_FAULT_INJECT: the n-th pass through an injection point throws (tests of the no-exception ABI)
+inline void fault_point(Ctx &c) {
+  if (c.fault_countdown > 0 && --c.fault_countdown == 0) throw std::bad_alloc();
+}
 
 // ---- host operations (files.cc); return kvfs_err codes, atomic on failure
 int open_file(Ctx &c, const char *name, int flags, int *fd);

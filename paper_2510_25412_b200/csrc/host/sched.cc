@@ -50,9 +50,13 @@ int kvfs_sched_destroy(kvfs_sched *s) {
   return KVFS_OK;
 }
 
-int kvfs_sched_enqueue(kvfs_sched *s, int fd, int n_q, const int32_t *pos, double now) {
+// No exception crosses the C ABI (include/kvfs.h conventions): the allocating steps run first, inside a
+// function-try-block, and the queue is changed only after they succeeded (strong guarantee).
+int kvfs_sched_enqueue(kvfs_sched *s, int fd, int n_q, const int32_t *pos, double now) try {
   if (!s || n_q < 0 || (n_q > 0 && !pos)) return KVFS_EINVAL;
+  kvfs_sched::Req req{fd, std::vector<int32_t>(pos, pos + n_q), now};
   std::lock_guard<std::mutex> lk(s->mu);
+  s->pool.push_back(std::move(req));  // may throw (strong guarantee): before the rate changes
   if (!s->has_rate) {
     s->lam = 1.0 / s->cfg.dt_default;
     s->has_rate = true;
@@ -61,8 +65,9 @@ int kvfs_sched_enqueue(kvfs_sched *s, int fd, int n_q, const int32_t *pos, doubl
     s->lam = (1.0 - s->cfg.alpha) * s->lam + s->cfg.alpha / dt;
   }
   s->t_prev = now;
-  s->pool.push_back({fd, std::vector<int32_t>(pos, pos + n_q), now});
   return KVFS_OK;
+} catch (...) {  // std::bad_alloc building or queueing the request: nothing changed
+  return KVFS_ENOMEM;
 }
 
 int kvfs_sched_state(kvfs_sched *s, double *lambda, int *target, int *n_waiting) {
@@ -75,7 +80,7 @@ int kvfs_sched_state(kvfs_sched *s, double *lambda, int *target, int *n_waiting)
 }
 
 int kvfs_sched_form(kvfs_sched *s, double now, pred_desc *descs, int desc_cap, int32_t *pos, int64_t pos_cap,
-                    int *n_desc, int64_t *n_rows) {
+                    int *n_desc, int64_t *n_rows) try {
   if (!s || !n_desc || !n_rows) return KVFS_EINVAL;
   std::lock_guard<std::mutex> lk(s->mu);
   if (s->pool.empty()) return 0;
@@ -107,12 +112,14 @@ int kvfs_sched_form(kvfs_sched *s, double now, pred_desc *descs, int desc_cap, i
       ++k;
       continue;
     }
-    rest.push_back(std::move(s->pool[i]));
+    rest.push_back(s->pool[i]);  // a copy: if it throws, the queue is intact
   }
   s->pool.swap(rest);
   *n_desc = static_cast<int>(take.size());
   *n_rows = rows;
   return 1;
+} catch (...) {
+  return KVFS_ENOMEM;
 }
 
 }  // extern "C"

@@ -24,6 +24,7 @@ HOST_PAGE = 0x80000000
 O_CREAT, O_EXCL = 1, 2
 EVICT_COMPACT = 1
 OPT_DECODE_CTAS, OPT_CHUNK_CUTOVER, OPT_DETERMINISTIC, OPT_CASCADE_MIN_ENTRIES, OPT_PREFIX_SPLITS = 1, 2, 3, 4, 5
+OPT_FAULT_INJECT = 6
 CTR_KERNEL_LAUNCHES, CTR_H2D_BYTES, CTR_PAGE_COPIES, CTR_LAST_DECODE_CTAS, CTR_LAST_CHUNK_UNITS = 1, 2, 3, 4, 5
 CTR_LAST_PREFIX_UNITS, CTR_LAST_PREFIX_GROUPS, CTR_HOST_PAGES = 6, 7, 8
 
@@ -118,7 +119,7 @@ def lib():
             "kvfs_get_counter": (cint, [vp, cint, P(i64)]),
             "kvfs_pack": (cint, [vp, P(cint), cint, vp, ctypes.c_size_t, P(ctypes.c_size_t), vp, ctypes.c_size_t,
                                  P(ctypes.c_size_t), vp]),
-            "kvfs_unpack": (cint, [vp, vp, vp, ctypes.c_size_t, P(ctypes.c_char_p), P(cint), vp]),
+            "kvfs_unpack": (cint, [vp, vp, ctypes.c_size_t, vp, ctypes.c_size_t, P(ctypes.c_char_p), P(cint), vp]),
         }
         for name, (res, args) in sigs.items():
             f = getattr(L, name)
@@ -425,7 +426,8 @@ class KVFS:
         nm = (ctypes.c_char_p * max(1, n))(*[x.encode() for x in names])
         fds = (ctypes.c_int * max(1, n))()
         st = _stream(stream) if self.device >= 0 else None
-        _check(lib().kvfs_unpack(self._h, _dptr(buf), hdr, len(hdr), nm, fds, st), "unpack")
+        nbuf = 0 if buf is None else buf.numel() * buf.element_size()
+        _check(lib().kvfs_unpack(self._h, _dptr(buf), nbuf, hdr, len(hdr), nm, fds, st), "unpack")
         return list(fds[:n])
 
     def counter(self, which: int) -> int:

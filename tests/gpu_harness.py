@@ -141,3 +141,23 @@ class Harness:
                 ko, vo = self.o.read(ofd, layer, 0, n)
                 assert np.array_equal(to_bits(kk), ko), name
                 assert np.array_equal(to_bits(vv), vo), name
+
+
+def scores_rtol(q_f64: np.ndarray, k_f64: np.ndarray, lse_gpu: np.ndarray, lse_ref: np.ndarray, scale: float):
+    """Per-key relative error bound of the K9 scores of one descriptor.
+
+    score_k = sum_{i,h} w_{k,i,h}, w = exp(s - lse), every term positive.  The kernel takes the SAME bf16 Q/K
+    bits as the oracle and the lse that the attention kernel wrote, so each w carries at most
+      |d lse_{i,h}|                    (the attention kernel's lse error: measured here, <= 2e-3 by the lse check)
+    + gamma_D * scale * |q_{i,h}| |k|  (fp32 accumulation of the D-term dot product, Cauchy-Schwarz bound;
+                                        gamma_D = D * 2^-24)
+    + 2^-21                            (MUFU ex2.approx relative error, incl. the fp32 log2(e) folding)
+    of relative error in the exponent, and the fp32 sum of n_q * Hq positive terms adds n_q * Hq * 2^-24
+    relative.  So |got_k - ref_k| <= rtol * ref_k with the rtol returned here (first order; expm1 keeps it
+    an upper bound).  q_f64 [n_q][Hq][D], k_f64 [len][Hkv][D]; lse_* [n_q][Hq]."""
+    n_q, hq, d = q_f64.shape
+    dlse = float(np.abs(np.asarray(lse_gpu, np.float64) - np.asarray(lse_ref, np.float64)).max())
+    qn = float(np.sqrt((q_f64 ** 2).sum(-1)).max())
+    kn = float(np.sqrt((k_f64 ** 2).sum(-1)).max())
+    ds = d * 2.0 ** -24 * scale * qn * kn
+    return float(np.expm1(dlse + ds + 2.0 ** -21) + n_q * hq * 2.0 ** -24)

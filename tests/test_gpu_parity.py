@@ -252,6 +252,10 @@ def test_migration_pack_unpack_two_ctx():
     hdr, buf = h.c.pack([h.fds[n][0] for n in names])
     dst = K.KVFS(1, 32, 8, 128, 16, 500, device=0)
     dst.open("pre-existing")  # the destination allocates smallest-free pages around its own state
+    free0 = dst.free_pages()
+    with pytest.raises(K.KvfsError) as e:  # a truncated transfer: EINVAL, nothing created, nothing read
+        dst.unpack(hdr, buf[:buf.numel() - 4096], names)
+    assert e.value.code == K.EINVAL and dst.free_pages() == free0
     fds = dst.unpack(hdr, buf, names)
     torch.cuda.synchronize()
     dst.audit()
@@ -306,5 +310,6 @@ def test_compact_files_batched():
         h.o.compact(h.fds[nm][1])
     h.check_meta()
     h.check_data()
-    with pytest.raises(K.KvfsError):
+    with pytest.raises(K.KvfsError) as e:
         h.c.compact_files([h.fds["f1"][0], h.fds["f1"][0]])
+    assert e.value.code == K.EBUSY

@@ -7,7 +7,10 @@ import torch
 
 pytestmark = pytest.mark.gpu
 
-from gpu_harness import Harness, assert_close, to_bits, to_dev  # noqa: E402
+from gpu_harness import Harness, assert_close, scores_rtol, to_bits, to_dev  # noqa: E402
+
+from oracle.attention import attention_scores  # noqa: E402
+from oracle.bf16 import bf16_to_f64  # noqa: E402
 
 from paper_2510_25412_b200 import kvfs as K  # noqa: E402
 
@@ -60,7 +63,72 @@ def test_scores_match_oracle(P, Hq, Hkv, D):
             got = sc[off[i]:off[i] + lens[i]]
             ref = sc_o[i]
             assert got.shape == ref.shape
-            assert np.abs(got - ref).max() <= 2e-3 * len(p) * Hq ** 0.5, name
+            kk = bf16_to_f64(h.o.read(h.fds[name][1], 0, 0, lens[i])[0])
+            rtol = scores_rtol(bf16_to_f64(q[0, r:r + len(p)]), kk, lse.cpu().numpy()[r:r + len(p)],
+                               lse_o[0, r:r + len(p)], scale)
+            assert rtol < 5e-3, (name, rtol)
+            assert (np.abs(got - ref) <= rtol * ref + 1e-30).all(), (name, rtol, np.abs(got - ref).max())
             assert abs(got.sum() - len(p) * Hq) <= 1e-3 * len(p) * Hq, name  # weights of each row-head sum to 1
         r += len(p)
     assert len(sc) == off[-1]  # nothing was written past the successful descriptors' ranges
+
+
+@pytest.mark.parametrize("P,Hq,Hkv,D", [(16, 32, 8, 128), (32, 8, 2, 64)])
+def test_scores_between_layers(P, Hq, Hkv, D):
+    """pred_attn_scores after layer l of an OPEN multi-layer step, then pred_attn_layer for
+    layer l + 1 (the per-layer H2O order).  The scores packet must not overwrite the step's uploaded plan
+    (descriptors, destination slots): every layer's output, lse, scores and pool bits equal the oracle's."""
+    L = 3
+    h = Harness(3000, P, Hq, Hkv, D, L=L, seed=11 + P + D)
+    h.c.set_option(K.OPT_CASCADE_MIN_ENTRIES, 2)
+    h.open("r")
+    h.append("r", list(range(500)))
+    h.evict("r", [(7, 29)])
+    for i in range(2):
+        h.fork("r", f"k{i}")
+    h.open("big")
+    h.append("big", list(range(700)))
+    rows = []
+    for name, nq in (("k0", 1), ("big", 24 if D == 128 else 5), ("k1", 3), ("r", 1)):
+        last = h.o.stat(h.fds[name][1])[2]
+        rows.append((name, list(range(last + 1, last + 1 + nq))))
+    descs_c = [(h.fds[n][0], len(p)) for n, p in rows]
+    descs_o = [(h.fds[n][1], len(p)) for n, p in rows]
+    pos = [x for _, p in rows for x in p]
+    T = len(pos)
+    k, v = h._kv(T)
+    q = h._q(T, 2.0)
+    scale = D ** -0.5
+    lens = [h.c.stat(fd)[0] + n for fd, n in descs_c]
+    off = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+    step, st = h.c.pred_step_begin(descs_c, pos)
+    res = []
+    for layer in range(L):
+        qd = to_dev(q[layer])
+        out = torch.full((T, Hq, D), float("nan"), dtype=torch.bfloat16, device="cuda")
+        lse = torch.full((T, Hq), float("nan"), dtype=torch.float32, device="cuda")
+        h.c.pred_attn_layer(step, layer, qd, to_dev(k[layer]), to_dev(v[layer]), out, lse, scale)
+        sc = torch.full((int(sum(lens)),), float("nan"), dtype=torch.float32, device="cuda")
+        h.c.pred_attn_scores(step, layer, qd, lse, sc, off, scale)
+        res.append((out, lse, sc))
+    h.c.pred_step_end(step)
+    torch.cuda.synchronize()
+    st_o, out_o, lse_o = h.o.pred_batch(descs_o, pos, q, k, v, scale)
+    assert st == st_o == [0] * len(rows)
+    for layer, (out, lse, sc) in enumerate(res):
+        assert_close(to_bits(out), out_o[layer], f"layer {layer}")
+        lg = lse.cpu().numpy()
+        np.testing.assert_allclose(lg, lse_o[layer], atol=2e-3, rtol=0)
+        scn = sc.cpu().numpy()
+        r = 0
+        for i, (name, p) in enumerate(rows):
+            n = len(p)
+            kk = bf16_to_f64(h.o.read(h.fds[name][1], layer, 0, lens[i])[0])
+            qq = bf16_to_f64(q[layer, r:r + n])
+            ref = attention_scores(qq, kk, scale)
+            rtol = scores_rtol(qq, kk, lg[r:r + n], lse_o[layer, r:r + n], scale)
+            got = scn[off[i]:off[i] + lens[i]]
+            assert (np.abs(got - ref) <= rtol * ref + 1e-30).all(), (layer, name, rtol)
+            r += n
+    h.check_meta()
+    h.check_data()  # every layer's appended K/V bits landed in the reserved slots

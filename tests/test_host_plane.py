@@ -91,7 +91,7 @@ def test_options_validate():
 
 
 def test_compact_files_errors():
-    """kvfs_compact_files: a file twice is EINVAL and a bad fd EBADF with nothing done; ENOSPC stops at the
+    """kvfs_compact_files: a file twice is EBUSY and a bad fd EBADF with nothing done; ENOSPC stops at the
     first file whose pages are not free, the earlier files compacted (include/kvfs.h)."""
     P = 16
     c = K.KVFS(1, 8, 2, 64, P, 10, device=-1)
@@ -105,7 +105,7 @@ def test_compact_files_errors():
     for fc, fo in fds.values():
         c.evict(fc, [(1, 3)])
         o.evict(fo, [(1, 3)], 0)
-    for bad, code in (([fds["a"][0], fds["a"][0]], K.EINVAL), ([fds["a"][0], 999], K.EBADF)):
+    for bad, code in (([fds["a"][0], fds["a"][0]], K.EBUSY), ([fds["a"][0], 999], K.EBADF)):
         with pytest.raises(K.KvfsError) as e:
             c.compact_files(bad)
         assert e.value.code == code
@@ -315,3 +315,57 @@ def test_host_plane_matches_oracle_random(seed):
 def test_host_plane_matches_oracle_random_many(block):
     for seed in range(1000 + block * 500, 1000 + (block + 1) * 500):
         run_random(seed, n_ops=100)
+
+
+def test_no_exception_crosses_the_abi():
+    """include/kvfs.h: "No C++ exception crosses this ABI".  KVFS_OPT_FAULT_INJECT makes a std::bad_alloc
+    fly from inside the library (mid-way through a pred reservation, after the first descriptor committed;
+    in fork; in open): the call returns KVFS_ENOMEM instead of terminating the process, the possibly
+    half-applied ctx is BROKEN (every later call KVFS_EIO), and kvfs_destroy still frees it."""
+    for where in ("pred", "fork", "open"):
+        c = K.KVFS(1, 8, 2, 64, 16, 64, device=-1)
+        a = c.open("a")
+        b = c.open("b")
+        c.append(a, list(range(20)))
+        c.append(b, list(range(20)))
+        c.set_option(K.OPT_FAULT_INJECT, 1)
+        with pytest.raises(K.KvfsError) as e:
+            if where == "pred":
+                c.pred_step_begin([(a, 1), (b, 1)], [20, 20])
+            elif where == "fork":
+                c.fork(a, "a2")
+            else:
+                c.open("z")
+        assert e.value.code == K.ENOMEM, where
+        for call in (lambda: c.open("q"), lambda: c.stat(a), lambda: c.truncate(a, 3), lambda: c.audit(),
+                     lambda: c.pred_step_begin([(a, 1)], [99]), lambda: c.set_option(K.OPT_FAULT_INJECT, 0)):
+            with pytest.raises(K.KvfsError) as e:
+                call()
+            assert e.value.code == K.EIO, where
+        c.close_ctx()  # kvfs_destroy of a broken ctx
+    # countdown: the injection fires on the n-th pass only; earlier calls are unaffected
+    c = K.KVFS(1, 8, 2, 64, 16, 64, device=-1)
+    c.set_option(K.OPT_FAULT_INJECT, 3)
+    c.open("x")
+    c.open("y")
+    with pytest.raises(K.KvfsError) as e:
+        c.open("w")
+    assert e.value.code == K.ENOMEM
+
+
+def test_unpack_checks_the_header_on_a_host_ctx():
+    """kvfs_unpack takes the received buffer size; on a host-only ctx only the header matters, and a
+    truncated or foreign header is EINVAL with nothing created (atomic)."""
+    c = K.KVFS(1, 8, 2, 64, 16, 64, device=-1)
+    a = c.open("a")
+    c.append(a, list(range(40)))
+    hdr, buf = c.pack([a])
+    assert buf is None
+    d = K.KVFS(1, 8, 2, 64, 16, 64, device=-1)
+    for bad in (hdr[:10], hdr[:-4], b"\0" * len(hdr)):
+        with pytest.raises(K.KvfsError) as e:
+            d.unpack(bad, None, ["a"])
+        assert e.value.code == K.EINVAL
+    assert d.free_pages() == 64
+    (fd,) = d.unpack(hdr, None, ["a"])
+    assert d.table(fd) == c.table(a) and d.positions(fd) == c.positions(a)
