@@ -47,7 +47,30 @@ def parse():
                     help="tuning: decode-kernel ring count (KVFS_OPT_DECODE_CTAS; 0 = auto)")
     ap.add_argument("--scores", action="store_true",
                     help="also run pred_attn_scores (NEXT-2, H2O score accumulation) every timed step")
+    ap.add_argument("--migrate", action="store_true",
+                    help="cfg5 at N > 1: skewed 160/96 LIP placement on even/odd ranks, one rebalance round "
+                         "(kvfs_pack -> NCCL send/recv -> kvfs_unpack), then the timed decode steps")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="functional multi-process run on ONE GPU (every rank on cuda:0, gloo with host staging); "
+                         "not a measurement")
     return ap.parse_args()
+
+
+def relaunch_distributed(args) -> int:
+    """`bench.py --gpus N` started without torchrun: re-execute this script under torch.distributed.run with
+    N processes (one per GPU, rendezvous on 127.0.0.1) and return its exit code.  Rank 0 prints the line."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "4")
+    print(f"[bench] relaunching under torch.distributed.run: {args.gpus} ranks", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
 
 
 def tensor_peak():
@@ -125,6 +148,91 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def dist_setup(args):
+    """One process per GPU (torchrun env).  NCCL for N > 1; --share-gpu: every rank on cuda:0 over gloo."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        print(f"[bench] warning: --gpus {args.gpus} but WORLD_SIZE={world}; using {world}", file=sys.stderr)
+    devi = 0 if args.share_gpu else local
+    torch.cuda.set_device(devi)
+    if world > 1:
+        if args.share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", devi))
+    return world, rank, local, devi
+
+
+def all_max(x: float, world: int) -> float:
+    """Max over ranks (CPU tensor under gloo, device tensor under NCCL)."""
+    if world == 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+
+    dev = "cpu" if dist.get_backend() == "gloo" else "cuda"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def gather_rank_info(world: int, info: dict):
+    if world == 1:
+        return [info]
+    import torch.distributed as dist
+
+    out = [None] * world
+    dist.all_gather_object(out, info)
+    return out
+
+
+NVLINK_GBS = 900.0  # NVLink 5 per direction per GPU (B200_PROFILING.md / SURVEY §8(e))
+
+
+def migration_summary(per_rank):
+    """Per pair of the rebalance: bytes moved, device-timed pack (K6 gather) / transfer / unpack (K6 scatter)
+    and their GB/s (pack / unpack: read + write of the page bytes against the HBM peak; transfer against
+    NVLink 5's ~900 GB/s per direction)."""
+    peak, _ = peaks()
+    pairs = []
+    by_rank = {x["rank"]: x for x in per_rank}
+    for x in per_rank:
+        if x.get("role") != "send":
+            continue
+        r = by_rank.get(x.get("peer"), {})
+        b = x.get("buf_bytes") or 0
+        xfer = max(v for v in (x.get("send_ms"), r.get("recv_ms"), 1e-9) if v is not None)
+        p = {"src": x["rank"], "dst": x.get("peer"), "files": x.get("files"), "moved": x.get("moved"),
+             "bytes": b, "pack_ms": x.get("pack_ms"), "pack_host_ms": x.get("pack_host_ms"),
+             "send_ms": x.get("send_ms"), "recv_ms": r.get("recv_ms"), "unpack_ms": r.get("unpack_ms"),
+             "unpack_host_ms": r.get("unpack_host_ms")}
+        if b and x.get("pack_ms"):
+            p["pack_gbs"] = 2 * b / (x["pack_ms"] / 1000) / 1e9
+            p["pack_frac_hbm"] = p["pack_gbs"] / peak
+        if b:
+            p["xfer_gbs"] = b / (xfer / 1000) / 1e9
+            p["xfer_frac_nvlink"] = p["xfer_gbs"] / NVLINK_GBS
+        if b and r.get("unpack_ms"):
+            p["unpack_gbs"] = 2 * b / (r["unpack_ms"] / 1000) / 1e9
+            p["unpack_frac_hbm"] = p["unpack_gbs"] / peak
+        pairs.append(p)
+    return {"pairs": pairs, "per_rank": per_rank, "nvlink_gbs_ref": NVLINK_GBS,
+            "note": "device-timed (CUDA events; the host part of kvfs_pack / kvfs_unpack is reported separately as "
+                    "*_host_ms); transfer = max(sender send, receiver recv) event time of the page buffer"}
+
+
+def pci_bus_id(devi: int):
+    try:
+        import torch
+
+        return torch.cuda.get_device_properties(devi).pci_bus_id
+    except Exception:
+        return None
 
 
 # ------------------------------------------------------------------------------------------ CPU oracle
@@ -241,14 +349,37 @@ def run_ours(args):
     from paper_2510_25412_b200 import kvfs as K
     from paper_2510_25412_b200.workloads import DecodeWorkload
 
-    world, rank, local = dist_env()
-    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    world, rank, local, devi = dist_setup(args)
     W, Kst = args.warmup, args.steps
     n_e2e = 0 if args.no_e2e else Kst
-    wl = DecodeWorkload(args.config, steps_total=W + Kst + n_e2e + 1, device=local)
+    # rank r holds its own LIPs (generator owners r * n_files ...) and its own step inputs: weak scaling
+    n_files0 = DecodeWorkload.config_files(args.config)
+    migration = None
+    if args.migrate and world > 1:
+        # SURVEY §8(d) cfg5 "Migration": skewed placement, n + n/4 LIPs on even ranks and n - n/4 on odd ranks
+        # (160 / 96 at cfg5's 128 per GPU; an odd last rank keeps n), then one rebalance round moves n/4
+        # files even -> odd over NCCL (kvfs_pack -> send / recv -> kvfs_unpack, ACKed); the timed steps run
+        # on the balanced placement
+        skew = n_files0 // 4
+        odd_last = world % 2 == 1 and rank == world - 1
+        n_mine = n_files0 if odd_last else (n_files0 + skew if rank % 2 == 0 else n_files0 - skew)
+        wl = DecodeWorkload(args.config, steps_total=W + Kst + n_e2e + 1, device=devi, n_files=n_mine,
+                            owner_base=rank * (n_files0 + skew), room_files=0 if rank % 2 == 0 else skew + 2,
+                            step_owner_base=rank * 100_000)
+        from paper_2510_25412_b200.parallel import rebalance
+
+        torch.cuda.synchronize()
+        dist.barrier()
+        mstats = {}
+        files = rebalance(wl.kv, wl.file_map(), stats=mstats)
+        torch.cuda.synchronize()
+        wl.set_files(files)
+        mstats["lips_after"] = wl.n_files
+        mstats["moved_files"] = len(mstats.get("moved_files", []))
+        migration = gather_rank_info(world, dict(mstats, rank=rank, lips_before=n_mine))
+    else:
+        wl = DecodeWorkload(args.config, steps_total=W + Kst + n_e2e + 1, device=devi, owner_base=rank * n_files0,
+                            step_owner_base=rank * 100_000)
     if args.prefix_splits:
         wl.kv.set_option(K.OPT_PREFIX_SPLITS, args.prefix_splits)
     if args.decode_ctas:
@@ -274,7 +405,7 @@ def run_ours(args):
     barrier()
     launches0 = kv.counter(K.CTR_KERNEL_LAUNCHES)
     h2d0 = kv.counter(K.CTR_H2D_BYTES)
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(devi)
     sampler.start()
     torch.cuda.synchronize()
     barrier()
@@ -317,10 +448,7 @@ def run_ours(args):
     kernel_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
     launches = kv.counter(K.CTR_KERNEL_LAUNCHES) - launches0
     h2d = kv.counter(K.CTR_H2D_BYTES) - h2d0
-    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = all_max(ms_total, world)
     ms_step = ms_max / Kst
     value = world * T * Kst / (ms_max / 1000.0)
 
@@ -395,17 +523,19 @@ def run_ours(args):
         cs.wait_stream(h2d_s)
         e1.record(cs)
         torch.cuda.synchronize()
-        et = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        et = all_max(e0.elapsed_time(e1), world)
         h2d_b = int(ring_p[0].numel())
         d2h_b = int(host_out_p[0][0].numel())
-        e2e = {"value": world * T * n_e2e / (float(et.item()) / 1000.0), "unit": "tokens/s",
+        e2e = {"value": world * T * n_e2e / (et / 1000.0), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b, "steps": n_e2e,
                "note": "pinned host Q/K_new/V_new (one packed buffer) -> device (copy stream), pred_attn_batch "
                        "via the C ABI on views of it (compute stream), out+lse (one packed buffer) -> pinned host "
                        "(second copy stream); steps pipelined with double-buffered device inputs / outputs"}
 
+    ranks = gather_rank_info(world, {
+        "rank": rank, "device": devi, "pci_bus_id": pci_bus_id(devi), "lips": wl.n_files, "ms_total": ms_total,
+        "kernel_ms_mean": statistics.mean(kernel_ms), "clocks": sampler.summary(),
+        "e2e_value": None if e2e is None else e2e["value"]})
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -443,7 +573,9 @@ def run_ours(args):
         "data": "synthetic (counter-based generator seed %d, DESIGN.md input recipe)" % wl.seed,
         "config": {"workload": wl.desc, "lips_per_gpu": wl.n_files, "file_len_start": wl.file_len + wl.prefix_len,
                    "n_q": wl.n_q, "n_q_heads": s.Hq, "n_kv_heads": s.Hkv, "head_dim": s.D, "page_size": s.P,
-                   "layers_per_step": 1, "parallelism": f"dp{world} (LIPs partitioned by process, no collective)",
+                   "layers_per_step": 1,
+                   "parallelism": f"dp{world} (LIPs partitioned by process, no collective)"
+                   + (" [--share-gpu: every rank on cuda:0, functional run, not a measurement]" if args.share_gpu else ""),
                    "l2": ("inputs larger than L2 (K/V read per step %.2f GB > 126 MB L2)" % (logical[0] / 1e9)
                           if logical[0] > 126e6 * 4 else
                           "unique K/V %.0f MB per step; the CoW-shared prefix is L2-resident by design" % (alg_bytes[0] / 1e6))},
@@ -453,6 +585,7 @@ def run_ours(args):
                          algorithmic_flops_per_launch=flops_mean),
         "gpu_launches": launches,
         "clocks": sampler.summary(),
+        "ranks": ranks if world > 1 else None,
         "extra": {"kv_attn_gbs_step": statistics.mean(alg_bytes) / (ms_step / 1000.0) / 1e9,
                   "logical_kv_bytes_per_step": statistics.mean(logical),
                   "logical_gbs_kernel": statistics.mean(logical) / (k_ms / 1000.0) / 1e9,
@@ -461,6 +594,11 @@ def run_ours(args):
                   "decode_ctas": kv.counter(K.CTR_LAST_DECODE_CTAS),
                   "host_ops_us": host_op_costs(wl)},
     }
+    if migration is not None:
+        line["migration"] = migration_summary(migration)
+        line["config"]["workload"] += (" | migration: skewed %d/%d LIPs on even/odd ranks, one rebalance round "
+                                       "(kvfs_pack, NCCL send/recv, kvfs_unpack) before the timed steps"
+                                       % (n_files0 + n_files0 // 4, n_files0 - n_files0 // 4))
     if args.scores:
         sc_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev1, ev2))
         k_bytes = statistics.mean(logical) / 2
@@ -481,18 +619,9 @@ def run_ours(args):
 def evict_ranges_heavy_hitter(seed: int, f: int, n: int, drop: int, sink: int = 4, recent: int = 1024):
     """cfg5(ii) policy: evict the `drop` lowest Exp(1) synthetic scores of file f, protecting
     the first `sink` and last `recent` tokens; ties -> lower index. Returns sorted disjoint [a, b) ranges."""
-    import numpy as np
+    from synth.workloads import heavy_hitter_ranges
 
-    from synth import exp1_scores_np, stream_key
-
-    sc = exp1_scores_np(stream_key(seed, 4, 0, f), 0, n)
-    sc[:sink] = np.inf
-    sc[n - recent:] = np.inf
-    idx = np.sort(np.argsort(sc, kind="stable")[:drop])
-    brk = np.nonzero(np.diff(idx) != 1)[0]
-    starts = np.concatenate([[idx[0]], idx[brk + 1]])
-    ends = np.concatenate([idx[brk], [idx[-1]]]) + 1
-    return np.stack([starts, ends], axis=1).astype(np.int64)
+    return heavy_hitter_ranges(seed, f, n, drop, sink, recent)
 
 
 def run_heavy_hitter(args):
@@ -545,14 +674,10 @@ def run_heavy_hitter(args):
         scores_ms = e0.elapsed_time(e1)
         sch = sc.view(n_files, n1).cpu().numpy().astype(np.float64)
         t0 = time.perf_counter()
+        from synth.workloads import lowest_score_ranges
+
         for f, fd in enumerate(fds):
-            x = sch[f].copy()
-            x[:4] = np.inf
-            x[n1 - 1024:] = np.inf
-            idx = np.sort(np.argsort(x, kind="stable")[:L0 // 2])
-            brk = np.nonzero(np.diff(idx) != 1)[0]
-            rg = np.stack([np.concatenate([[idx[0]], idx[brk + 1]]), np.concatenate([idx[brk], [idx[-1]]]) + 1], 1)
-            kv.evict(fd, rg.astype(np.int64))
+            kv.evict(fd, lowest_score_ranges(sch[f], L0 // 2))
         host_sel_s = time.perf_counter() - t0
         scores_info = {"kernel": "scores_kernel (K9) over 128 x 65537 tokens", "scores_ms": scores_ms,
                        "k_gbs": n_files * n1 * s.Hkv * s.D * 2 / (scores_ms / 1000) / 1e9,
@@ -734,13 +859,15 @@ def run_migrate(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args))
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "cfg5hh":
         run_heavy_hitter(args)
     elif args.config == "offload":
         run_offload(args)
-    elif args.config == "migrate":
+    elif args.config == "migrate" or (args.migrate and args.gpus == 1):
         run_migrate(args)
     else:
         run_ours(args)

@@ -156,65 +156,145 @@ __device__ __forceinline__ int find_entry(const dev::Entry *t, int n, int64_t i)
   return lo;
 }
 
-#ifndef KVFS_K5_MINB
-#define KVFS_K5_MINB 1  // resident CTAs per SM the register budget is sized for
-#endif
-#ifndef KVFS_K5_U
-#define KVFS_K5_U 4  // 16-byte K and V loads in flight per thread
-#endif
+// K5: compaction gather (R7).  Token i of the old table (logical order) -> (new_pages[i / P], i % P), every
+// layer, K and V.  The unit of work is a destination BLOCK = one (page, layer, K|V, kv head): P rows of D bf16,
+// contiguous in the pool (P * D * 2 bytes, 4 KiB at the 8B shape).  Blocks are ordered (page, layer, K|V,
+// head) and cut into 32 KiB stages; each CTA takes a contiguous range of stages (so a contiguous range of
+// destination pages) and pipelines them through kK5Stages shared-memory buffers:
+//   * sources: every row is a 256-byte (D = 128) scattered read (holes): the 256 threads issue 16-byte
+//     cp.async (LDGSTS) copies straight into the stage buffer, laid out as the destination blocks -- the
+//     bytes in flight live in shared memory, not in registers (the round-1 register-held copy kept only
+//     ~128 B per thread in flight: 0.46 eligible warps per scheduler, 3.9 TB/s);
+//   * destinations: one 1-D TMA bulk store (cp.async.bulk.global.shared::cta) per block, issued by one
+//     lane per block of warp 0 -- whole 4 KiB contiguous writes.
+// Source (page, slot) of every token of the CTA's pages is resolved once per chunk of pages into shared
+// memory from `first_entry[j]` (host: the old entry holding token j * P), walking forward <= P entries.
+// Programmatic dependent launch (kvfs_compact_files chains one launch per file, R1 order): the grid reads
+// its own sources at once (a later file's sources were held while earlier files compacted, so no earlier
+// grid writes them) and executes griddepcontrol.wait before its first store (its destinations may be the
+// pages the previous file just released, i.e. the previous grid's sources).
+constexpr int kK5Threads = 256;
+constexpr int kK5StageBytes = 32768;
+constexpr int kK5Stages = 3;
+constexpr int kK5SrcCap = 1024;  // tokens whose sources are resolved at a time
+constexpr int kK5MaxBps = 16;    // blocks per stage (block >= 2 KiB)
+struct K5Block {                 // one destination block of a stage (shared memory)
+  const bf16 *src_pool;          // the layer's K or V pool
+  bf16 *dst;                     // destination block (page new_pages[j], kv head g, slot 0)
+  int32_t gP;                    // g * P (row offset of the head inside a page)
+  int32_t k0;                    // index of the block's first token in the resolved chunk
+  int32_t ntok;                  // rows (P, or fewer on the last page; 0: past the end)
+  int32_t pad;
+};
+constexpr int kK5Smem = kK5Stages * kK5StageBytes + kK5SrcCap * 8 + kK5Stages * kK5MaxBps * 32 + 128;
 
-// K5: token i of the old table (logical order) -> (new_pages[i / P], i % P), every layer, K and V.
-// A CTA per (destination page, layer), grid-stride over the pages: the P source (page, slot) pairs are
-// resolved once into shared memory, then the CTA streams the page's Hkv x P rows of K and V with 16-byte vectors (4 loads in flight
-// per thread before the stores).
-__global__ void __launch_bounds__(256, KVFS_K5_MINB) compact_kernel(const dev::Entry *old, int n_old, const uint32_t *new_pages,
-                                                      int n_new, int64_t len, bf16 *const *kp, bf16 *const *vp, int L,
-                                                      int Hkv, int D, int P) {
-  __shared__ uint32_t src_page[64];
-  __shared__ int src_slot[64];
-  const int l = blockIdx.y;
-  for (int j = blockIdx.x; j < n_new; j += gridDim.x) {  // grid-stride over destination pages
-  const int64_t i0 = static_cast<int64_t>(j) * P;
-  const int ntok = static_cast<int>(len - i0 < P ? len - i0 : static_cast<int64_t>(P));
-  if (threadIdx.x < ntok) {
-    const int64_t i = i0 + threadIdx.x;
-    const dev::Entry e = old[find_entry(old, n_old, i)];
-    src_page[threadIdx.x] = e.page;
-    src_slot[threadIdx.x] = dev::select_bit64(e.mask, static_cast<int>(i - e.lstart));
-  }
-  __syncthreads();
-  const bf16 *ks = kp[l];
-  const bf16 *vs = vp[l];
-  bf16 *kd = kp[l];
-  bf16 *vd = vp[l];
-  const int cpr = D / 8;
-  const int total = Hkv * ntok * cpr;
-  const int64_t dpage = new_pages[j];
-  constexpr int U = KVFS_K5_U;
-  for (int base = threadIdx.x; base < total; base += U * blockDim.x) {
-    uint4 kr[U], vr[U];
-    int64_t po[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int idx = base + u * blockDim.x;
-      if (idx < total) {
-        const int c = idx % cpr, r = idx / cpr, t = r % ntok, g = r / ntok;
-        const int64_t so = ((static_cast<int64_t>(src_page[t]) * Hkv + g) * P + src_slot[t]) * D + c * 8;
-        po[u] = ((dpage * Hkv + g) * P + t) * D + c * 8;
-        kr[u] = *reinterpret_cast<const uint4 *>(ks + so);
-        vr[u] = *reinterpret_cast<const uint4 *>(vs + so);
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void *g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+
+__global__ void __launch_bounds__(kK5Threads, 2)
+compact_kernel(const dev::Entry *old, int n_old, const uint32_t *new_pages, const int32_t *first_entry, int n_new,
+               int64_t len, bf16 *const *kp, bf16 *const *vp, int L, int Hkv, int lgD, int lgP) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  extern __shared__ __align__(128) unsigned char k5_smem[];
+  unsigned char *stage_base = k5_smem;
+  uint32_t *src_page = reinterpret_cast<uint32_t *>(k5_smem + kK5Stages * kK5StageBytes);
+  int32_t *src_slot = reinterpret_cast<int32_t *>(src_page + kK5SrcCap);
+  K5Block *blk = reinterpret_cast<K5Block *>(src_slot + kK5SrcCap);  // [kK5Stages][kK5MaxBps]
+  const int tid = threadIdx.x;
+  const int P = 1 << lgP, D = 1 << lgD;
+  const int lg_cpr = lgD - 3;                            // 16-byte chunks per row: D / 8
+  const int lg_blk_chunks = lgP + lg_cpr;                // chunks per block
+  const int bps = kK5StageBytes >> (lg_blk_chunks + 4);  // blocks per stage
+  const int bpp = L * 2 * Hkv;                           // blocks per destination page
+  const int64_t nb = static_cast<int64_t>(n_new) * bpp;
+  const int64_t n_stages = (nb + bps - 1) / bps;
+  const int64_t q0 = n_stages * blockIdx.x / gridDim.x, q1 = n_stages * (blockIdx.x + 1) / gridDim.x;
+  if (q0 >= q1) return;
+  const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(stage_base));
+  const int chunk_pages = kK5SrcCap >> lgP;
+  int64_t cj0 = -1;  // first page of the resolved chunk
+
+  // resolve the sources of pages [j0, j0 + chunk_pages) into src_page / src_slot (all threads)
+  auto resolve = [&](int64_t j0) {
+    __syncthreads();  // every thread is done computing addresses from the previous chunk
+    const int64_t i_begin = j0 << lgP;
+    const int64_t i_end = min(len, i_begin + kK5SrcCap);
+    for (int64_t i = i_begin + tid; i < i_end; i += kK5Threads) {
+      int e = first_entry[i >> lgP];
+      dev::Entry en = old[e];
+      while (e + 1 < n_old && en.lstart + __popcll(en.mask) <= i) en = old[++e];
+      src_page[i - i_begin] = en.page;
+      src_slot[i - i_begin] = dev::select_bit64(en.mask, static_cast<int>(i - en.lstart));
+    }
+    cj0 = j0;
+    __syncthreads();
+  };
+  // issue the cp.async copies of stage q into buffer `buf` (one commit group per call, possibly empty)
+  auto issue = [&](int64_t q, int buf) {
+    if (q < q1) {  // uniform
+      const int64_t b0 = q * bps;
+      const int64_t jf = b0 / bpp;
+      const int r0 = static_cast<int>(b0 - jf * bpp);
+      const int64_t jl = min(nb - 1, b0 + bps - 1) / bpp;  // last page of the stage
+      if (cj0 < 0 || jl >= cj0 + chunk_pages) resolve(jf);
+      K5Block *bd = blk + buf * kK5MaxBps;
+      if (tid < bps) {  // the stage's block descriptors (also read by the stores, kK5Stages - 1 iterations later)
+        const int rr = r0 + tid;
+        const int64_t j = jf + rr / bpp;
+        const int r = rr % bpp;
+        const int g = r % Hkv, kv = (r / Hkv) & 1, l = r / (2 * Hkv);
+        K5Block d{};
+        if (b0 + tid < nb) {
+          bf16 *pool = kv ? vp[l] : kp[l];
+          d.src_pool = pool;
+          d.dst = pool + ((static_cast<int64_t>(new_pages[j]) * Hkv + g) << (lgP + lgD));
+          d.gP = g << lgP;
+          d.k0 = static_cast<int32_t>((j - cj0) << lgP);
+          d.ntok = static_cast<int32_t>(min(static_cast<int64_t>(P), len - (j << lgP)));
+        }
+        bd[tid] = d;
+      }
+      __syncthreads();
+      const uint32_t sb = sbase + buf * kK5StageBytes;
+      const int HkvP = Hkv << lgP;
+      // kK5StageBytes / 16 chunks per stage = (block, row, 16-byte chunk), chunk fastest (coalesced rows)
+#pragma unroll 4
+      for (int x = tid; x < kK5StageBytes / 16; x += kK5Threads) {
+        const K5Block &d = bd[x >> lg_blk_chunks];
+        const int t = (x >> lg_cpr) & (P - 1);
+        if (t >= d.ntok) continue;
+        const int k = d.k0 + t;
+        const int64_t row = static_cast<int64_t>(src_page[k]) * HkvP + d.gP + src_slot[k];
+        cp_async16(sb + (x << 4), d.src_pool + (row << lgD) + ((x & ((1 << lg_cpr) - 1)) << 3));
       }
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (base + u * static_cast<int>(blockDim.x) < total) {
-        *reinterpret_cast<uint4 *>(kd + po[u]) = kr[u];
-        *reinterpret_cast<uint4 *>(vd + po[u]) = vr[u];
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  for (int k = 0; k < kK5Stages - 1; ++k) issue(q0 + k, k);
+  for (int64_t q = q0; q < q1; ++q) {
+    const int buf = static_cast<int>((q - q0) % kK5Stages);
+    asm volatile("cp.async.wait_group %0;" ::"n"(kK5Stages - 2) : "memory");  // this thread's part of stage q
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the async (TMA) proxy
+    __syncthreads();
+    if (tid < 32) {
+      if (q == q0) asm volatile("griddepcontrol.wait;" ::: "memory");  // before the first write (see above)
+      const K5Block &d = blk[buf * kK5MaxBps + (tid < bps ? tid : 0)];
+      if (tid < bps && d.ntok > 0) {
+        const uint32_t src = sbase + buf * kK5StageBytes + (tid << (lg_blk_chunks + 4));
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d.dst), "r"(src),
+                     "r"(d.ntok << (lgD + 1))
+                     : "memory");
       }
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      // the buffer refilled next held stage q - 1: its bulk stores must have finished reading it
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
     }
+    __syncthreads();
+    issue(q + kK5Stages - 1, static_cast<int>((q - q0 + kK5Stages - 1) % kK5Stages));
   }
-  __syncthreads();  // src_page / src_slot are rewritten for the next destination page
-  }
+  if (tid < 32) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // writes performed before exit
 }
 
 // K6: whole pages <-> a packed buffer [L][K, V][n][page_elems] (migration pack / unpack).
@@ -350,24 +430,63 @@ class CudaDevice final : public Device {
     return KVFS_OK;
   }
 
-  int compact(const std::vector<Entry> &old_table, const std::vector<uint32_t> &new_pages, int64_t len,
-              kvfs_stream_t s) override {
-    begin_packet();
-    const void *dt = push(old_table.data(), old_table.size() * sizeof(Entry));
-    const void *dp = push(new_pages.data(), new_pages.size() * sizeof(uint32_t));
-    if (!dt || !dp) return KVFS_ENOMEM;
-    if (!send(s)) return KVFS_EIO;
+  int compact(const std::vector<CompactJob> &jobs, kvfs_stream_t s) override {
+    // one packet for every file (old tables, new pages, first entries), then one K5 launch per file in
+    // order, each after the first a programmatic dependent launch of the previous one (see compact_kernel)
     const kvfs_config &cfg = c_.cfg;
-    // one wave: up to 8 resident CTAs per SM, each looping over destination pages (a file of ~2k pages
-    // was 1.7 waves of one-page CTAs)
-    const int64_t per_layer = std::max<int64_t>(1, static_cast<int64_t>(sms_) * 8 / cfg.n_layers);  // >= resident
-    const dim3 grid(static_cast<unsigned>(std::min<int64_t>(static_cast<int64_t>(new_pages.size()), per_layer)),
-                    static_cast<unsigned>(cfg.n_layers));
-    compact_kernel<<<grid, 256, 0, cs(s)>>>(static_cast<const dev::Entry *>(dt), static_cast<int>(old_table.size()),
-                                            static_cast<const uint32_t *>(dp), static_cast<int>(new_pages.size()), len,
-                                            kptrs_, vptrs_, cfg.n_layers, cfg.n_kv_heads, cfg.head_dim, cfg.page_size);
-    ++c_.ctr.launches;
-    return cudaGetLastError() == cudaSuccess ? KVFS_OK : KVFS_EIO;
+    const int P = cfg.page_size;
+    std::vector<std::vector<int32_t>> fe(jobs.size());
+    std::vector<const void *> dt(jobs.size()), dp(jobs.size()), df(jobs.size());
+    begin_packet();
+    for (size_t f = 0; f < jobs.size(); ++f) {
+      const std::vector<Entry> &old = *jobs[f].old_table;
+      const size_t n_new = jobs[f].new_pages->size();
+      fe[f].resize(n_new);
+      size_t e = 0;
+      for (size_t j = 0; j < n_new; ++j) {  // the old entry holding logical token j * P
+        const int64_t i = static_cast<int64_t>(j) * P;
+        while (e + 1 < old.size() && old[e + 1].lstart <= i) ++e;
+        fe[f][j] = static_cast<int32_t>(e);
+      }
+      dt[f] = push(old.data(), old.size() * sizeof(Entry));
+      dp[f] = push(jobs[f].new_pages->data(), n_new * sizeof(uint32_t));
+      df[f] = push(fe[f].data(), n_new * sizeof(int32_t));
+      if (!dt[f] || !dp[f] || !df[f]) return KVFS_ENOMEM;
+    }
+    if (!send(s)) return KVFS_EIO;
+    if (k5_grid_ == 0) {
+      if (cudaFuncSetAttribute(compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kK5Smem) != cudaSuccess)
+        return KVFS_EIO;
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, compact_kernel, kK5Threads, kK5Smem);
+      k5_grid_ = sms_ * std::max(1, per_sm);  // one wave of resident CTAs (2 per SM)
+    }
+    const int lgD = cfg.head_dim == 128 ? 7 : 6;
+    const int lgP = __builtin_ctz(static_cast<unsigned>(P));
+    for (size_t f = 0; f < jobs.size(); ++f) {
+      const int64_t n_new = static_cast<int64_t>(jobs[f].new_pages->size());
+      if (n_new == 0) continue;
+      const int64_t stages = (n_new * cfg.n_layers * 2 * cfg.n_kv_heads * P * cfg.head_dim * 2 + kK5StageBytes - 1) /
+                             kK5StageBytes;
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(k5_grid_, stages)));
+      lc.blockDim = dim3(kK5Threads);
+      lc.dynamicSmemBytes = kK5Smem;
+      lc.stream = cs(s);
+      cudaLaunchAttribute la[1];
+      la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      la[0].val.programmaticStreamSerializationAllowed = f > 0 ? 1 : 0;  // the first waits for everything before
+      lc.attrs = la;
+      lc.numAttrs = 1;
+      const cudaError_t e = cudaLaunchKernelEx(&lc, compact_kernel, static_cast<const dev::Entry *>(dt[f]),
+                                               static_cast<int>(jobs[f].old_table->size()),
+                                               static_cast<const uint32_t *>(dp[f]), static_cast<const int32_t *>(df[f]),
+                                               static_cast<int>(n_new), jobs[f].len, kptrs_, vptrs_, cfg.n_layers,
+                                               cfg.n_kv_heads, lgD, lgP);
+      ++c_.ctr.launches;
+      if (e != cudaSuccess) return KVFS_EIO;
+    }
+    return KVFS_OK;
   }
 
   int scores(const std::vector<ScoreDesc> &descs, const std::vector<ScoreUnit> &units, int layer, const void *q,
@@ -785,6 +904,7 @@ class CudaDevice final : public Device {
   bf16 **kptrs_ = nullptr, **vptrs_ = nullptr;
   int sms_ = 148;
   int per_sm_ = 0;
+  int64_t k5_grid_ = 0;
   Staging stg_[4];
   int cur_ = 0;
   size_t used_ = 0;

@@ -214,7 +214,7 @@ int kvfs_evict(kvfs_ctx *ctx, int fd, const int64_t *ranges, int n_ranges, int f
     int rc = evict_file(c, *f, ranges, n_ranges, flags, &old_table, &new_pages);
     if (rc != KVFS_OK) return rc;
     if (c.dev && !new_pages.empty()) {
-      rc = c.dev->compact(old_table, new_pages, f->len, stream);
+      rc = c.dev->compact({CompactJob{&old_table, &new_pages, f->len}}, stream);
       if (rc != KVFS_OK) c.poisoned = true;
     }
     return rc;
@@ -233,7 +233,7 @@ int kvfs_compact(kvfs_ctx *ctx, int fd, kvfs_stream_t stream) {
     int rc = compact_file(c, *f, &old_table, &new_pages);
     if (rc != KVFS_OK) return rc;
     if (c.dev && !new_pages.empty()) {
-      rc = c.dev->compact(old_table, new_pages, f->len, stream);
+      rc = c.dev->compact({CompactJob{&old_table, &new_pages, f->len}}, stream);
       if (rc != KVFS_OK) c.poisoned = true;
     }
     return rc;
@@ -261,19 +261,24 @@ int kvfs_compact_files(kvfs_ctx *ctx, const int *fds, int n, int *n_done, kvfs_s
     // pages and tables in order (R1: each file's allocation sees the previous files' releases), each file's
     // device gather enqueued as it goes; the host position passes afterwards, on worker threads
     std::vector<std::vector<Entry>> olds(static_cast<size_t>(n));
+    std::vector<std::vector<uint32_t>> nps(static_cast<size_t>(n));
     int rc = KVFS_OK, done = 0;
     for (int i = 0; i < n; ++i) {
-      std::vector<uint32_t> np;
-      rc = compact_file_tables(c, *files[i], &olds[i], &np);
+      rc = compact_file_tables(c, *files[i], &olds[i], &nps[i]);
       if (rc != KVFS_OK) break;
       ++done;
-      // the device gather of this file before the next file's (stream order): R1 hands the next file the
-      // pages this one just released, so its destinations may be this file's sources
-      if (c.dev && !np.empty()) {
-        rc = c.dev->compact(olds[i], np, files[i]->len, stream);
-        if (rc != KVFS_OK) {
+    }
+    // the device gathers of the committed files, in order (R1 hands the next file the pages this one just
+    // released, so its destinations may be this file's sources: the data plane chains them)
+    if (c.dev && done > 0) {
+      std::vector<CompactJob> jobs;
+      for (int i = 0; i < done; ++i)
+        if (!nps[i].empty()) jobs.push_back({&olds[i], &nps[i], files[i]->len});
+      if (!jobs.empty()) {
+        const int drc = c.dev->compact(jobs, stream);
+        if (drc != KVFS_OK) {
           c.poisoned = true;
-          break;
+          rc = drc;
         }
       }
     }

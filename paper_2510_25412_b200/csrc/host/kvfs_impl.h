@@ -154,6 +154,13 @@ struct PredPlan {
 
 class Device;  // data plane (csrc/cuda), absent for a host-only ctx
 
+// one file's compaction gather (R7): token i of old_table (logical order) -> (new_pages[i / P], i % P)
+struct CompactJob {
+  const std::vector<Entry> *old_table;
+  const std::vector<uint32_t> *new_pages;
+  int64_t len;
+};
+
 struct CtxCounters {
   int64_t launches = 0, h2d_bytes = 0, page_copies = 0, last_decode_ctas = 0, last_chunk_units = 0,
           last_prefix_units = 0, last_prefix_groups = 0, host_pages = 0;
@@ -242,8 +249,8 @@ class Device {
   virtual ~Device() = default;
   virtual int copy_pages(const std::vector<PageCopy> &copies, kvfs_stream_t s) = 0;
   virtual int append_rows(const std::vector<int32_t> &dst, const void *k, const void *v, kvfs_stream_t s) = 0;
-  virtual int compact(const std::vector<Entry> &old_table, const std::vector<uint32_t> &new_pages, int64_t len,
-                      kvfs_stream_t s) = 0;
+  // the files' gathers in order (a later file's destinations may be an earlier file's sources)
+  virtual int compact(const std::vector<CompactJob> &jobs, kvfs_stream_t s) = 0;
   virtual int gather(const std::vector<int32_t> &src_slots, const std::vector<uint32_t> &new_pages,
                      kvfs_stream_t s) = 0;
   virtual int read(const std::vector<Entry> &table, int layer, int64_t begin, int64_t end, void *k_out,

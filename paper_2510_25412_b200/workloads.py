@@ -29,7 +29,15 @@ class DecodeWorkload:
     step (autocompletion); `evict_sink` evicts logical [sink, sink+1) (attention sink + sliding
     window); `prefix_len` builds every file as a fork of one shared prefix."""
 
-    def __init__(self, name: str, steps_total: int, device: int = 0, n_files: int = None):
+    @staticmethod
+    def config_files(name: str) -> int:
+        return CONFIGS[name]["n_files"]
+
+    def __init__(self, name: str, steps_total: int, device: int = 0, n_files: int = None, owner_base: int = 0,
+                 room_files: int = 0, step_owner_base: int = 0):
+        """owner_base: the first file's generator owner id (and name "lip<owner>"), so the ranks of a multi-GPU
+        run hold distinct LIPs; room_files: pool room for that many more files (migration targets);
+        step_owner_base: offset of the per-step input owners (distinct inputs per rank)."""
         c = CONFIGS[name]
         self.name = name
         self.desc = c["workload"]
@@ -46,10 +54,12 @@ class DecodeWorkload:
         self.dev = torch.device("cuda", device)
         grow = 0 if self.rewind else steps_total * self.n_q
         per_file = math.ceil((self.file_len + grow + s.P) / s.P) + 2
-        self.n_pages = self.n_files * per_file + math.ceil(self.prefix_len / s.P) + 64
-        rows = self.n_files * self.n_q
+        self.n_pages = (self.n_files + room_files) * per_file + math.ceil(self.prefix_len / s.P) + 64
+        self.step_owner_base = step_owner_base
+        self.per_file_pages = per_file
+        rows = (self.n_files + room_files) * self.n_q
         self.kv = KVFS(1, s.Hq, s.Hkv, s.D, s.P, self.n_pages, max_batch_rows=max(rows, 16),
-                       max_batch_descs=max(self.n_files, 16), device=device)
+                       max_batch_descs=max(self.n_files + room_files, 16), device=device)
         width = s.Hkv * s.D
         fds = []
         self.prefix_fd = None
@@ -59,8 +69,10 @@ class DecodeWorkload:
             v = rows_torch(self.seed, TAG_V, 0, PREFIX_OWNER, 0, self.prefix_len, width, device=self.dev)
             self.kv.append(self.prefix_fd, list(range(self.prefix_len)), k.view(1, -1, s.Hkv, s.D),
                            v.view(1, -1, s.Hkv, s.D))
-        for f in range(self.n_files):
+        self.names = []
+        for f in range(owner_base, owner_base + self.n_files):
             fd = self.kv.fork(self.prefix_fd, f"lip{f}") if self.prefix_fd is not None else self.kv.open(f"lip{f}")
+            self.names.append(f"lip{f}")
             k = rows_torch(self.seed, TAG_K, 0, f, 0, self.file_len, width, device=self.dev)
             v = rows_torch(self.seed, TAG_V, 0, f, 0, self.file_len, width, device=self.dev)
             p0 = self.prefix_len
@@ -75,12 +87,28 @@ class DecodeWorkload:
         self._offs = np.arange(self.n_q, dtype=np.int64)
         self.step = 0
 
+    # ------------------------------------------------------------------ migration (parallel.rebalance)
+    def file_map(self):
+        return dict(zip(self.names, self.fds))
+
+    def set_files(self, files) -> None:
+        """Adopt the file set after a rebalance ({name: fd}; moved-in files continue at their own last
+        retained position; files are kept in name order so the batch is deterministic)."""
+        items = sorted(files.items(), key=lambda x: (len(x[0]), x[0]))
+        self.names = [n for n, _ in items]
+        self.fds = [fd for _, fd in items]
+        st = [self.kv.stat(fd) for fd in self.fds]
+        self.n_files = len(self.fds)
+        self.lens = np.array([x[0] for x in st], dtype=np.int64)
+        self.next_pos = np.array([x[2] + 1 for x in st], dtype=np.int64)
+        self.descs = np.array([[fd, self.n_q] for fd in self.fds], dtype=np.int32)
+
     # ------------------------------------------------------------------ per step
     def make_inputs(self, step: int) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
         """Device Q [T][Hq][D], K_new/V_new [T][Hkv][D] of step `step`."""
         s = self.shape
         T = self.n_files * self.n_q
-        owner = STEP_OWNER + step
+        owner = STEP_OWNER + self.step_owner_base + step
         q = rows_torch(self.seed, TAG_Q, 0, owner, 0, T, s.Hq * s.D, device=self.dev).view(T, s.Hq, s.D)
         k = rows_torch(self.seed, TAG_K, 0, owner, 0, T, s.Hkv * s.D, device=self.dev).view(T, s.Hkv, s.D)
         v = rows_torch(self.seed, TAG_V, 0, owner, 0, T, s.Hkv * s.D, device=self.dev).view(T, s.Hkv, s.D)

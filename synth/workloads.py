@@ -28,3 +28,31 @@ def rows_torch(seed: int, tag: int, layer: int, owner: int, s0: int, s1: int, wi
     t = normal_bf16_torch(key, s0 * width, (s1 - s0) * width, std, device=device,
                           out=None if out is None else out.reshape(-1))
     return t.view(s1 - s0, width) if out is None else out
+
+
+# ------------------------------------------------------------------ cfg5(ii) LIP eviction policy (inputs)
+# a heavy-hitter-like replacement policy evicts the `drop` lowest-score tokens of a
+# file, protecting the first `sink` and the last `recent` ones, ties to the lower index.  The scores are
+# either synthetic (Exp(1), seeded) or a decode step's H2O scores; choosing the ranges from them is the LIP's
+# policy (an INPUT to kvfs_evict), not KVFS arithmetic.
+TAG_SCORE = 4
+
+
+def lowest_score_ranges(scores, drop: int, sink: int = 4, recent: int = 1024) -> np.ndarray:
+    """Sorted disjoint half-open logical ranges [a, b) covering the `drop` lowest scores (int64 [n][2])."""
+    sc = np.array(scores, dtype=np.float64, copy=True)
+    n = sc.shape[0]
+    sc[:sink] = np.inf
+    sc[max(0, n - recent):] = np.inf
+    idx = np.sort(np.argsort(sc, kind="stable")[:drop])
+    brk = np.nonzero(np.diff(idx) != 1)[0]
+    starts = np.concatenate([[idx[0]], idx[brk + 1]])
+    ends = np.concatenate([idx[brk], [idx[-1]]]) + 1
+    return np.stack([starts, ends], axis=1).astype(np.int64)
+
+
+def heavy_hitter_ranges(seed: int, f: int, n: int, drop: int, sink: int = 4, recent: int = 1024) -> np.ndarray:
+    """cfg5(ii) with synthetic scores: Exp(1) per token of file f (stream (seed, TAG_SCORE, 0, f))."""
+    from .gen import exp1_scores_np
+
+    return lowest_score_ranges(exp1_scores_np(stream_key(seed, TAG_SCORE, 0, f), 0, n), drop, sink, recent)
