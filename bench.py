@@ -711,21 +711,42 @@ def run_heavy_hitter(args):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / steps
 
+    sampler = ClockSampler(0)
+    sampler.start()
     decode(W, 0)
     alg_before = 2 * int(lens.sum()) * row_kv
     ms_before = decode(Kst, W)
     retained = int(lens.sum())
+    # kvfs_compact_files of all files: (1) as the caller sees it (CUDA events around the call: the host R1 /
+    # table work and the device gathers, overlapped by file groups) and (2) the device work alone (the
+    # library's own events around each group's upload + K5 launches, KVFS_OPT_TIMING)
+    kv.set_option(K.OPT_TIMING, 1)
+    torch.cuda.synchronize()
     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_host0 = time.perf_counter()
     c0.record()
     kv.compact_files(fds)  # one call: page / table work in order, host position passes on worker threads
     c1.record()
+    host_ms = 1000 * (time.perf_counter() - t_host0)
     torch.cuda.synchronize()
-    ms_compact = c0.elapsed_time(c1)
+    ms_call = c0.elapsed_time(c1)
+    ms_compact = kv.counter(K.CTR_COMPACT_DEVICE_NS) / 1e6
+    kv.set_option(K.OPT_TIMING, 0)
     compact_bytes = 2 * 2 * retained * row_kv  # K and V of every retained token: read + write
     decode(W, W + Kst)
     alg_after = 2 * int(lens.sum()) * row_kv
     ms_after = decode(Kst, 2 * W + Kst)
+    sampler.stop()
     peak, peak_src = peaks()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "decode_traffic.json")
+    tinfo = {}
+    if os.path.exists(tp):
+        try:
+            tinfo = json.load(open(tp)).get("cfg5hh", {})
+            traffic = tinfo.get("k5_traffic_bytes_per_file")
+        except Exception:
+            tinfo = {}
     line = {
         "metric": METRIC, "value": n_files / (ms_after / 1000.0), "unit": "tokens/s", "n_gpus": 1, "steps": Kst,
         "warmup": W, "ms_per_step": ms_after, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -735,17 +756,46 @@ def run_heavy_hitter(args):
                                "kvfs_compact", "l2": "inputs larger than L2"},
         "roofline": {"bound": "hbm", "achieved": compact_bytes / (ms_compact / 1000.0) / 1e9, "peak": peak,
                      "unit": "GB/s", "frac": compact_bytes / (ms_compact / 1000.0) / 1e9 / peak,
-                     "kernel": "compact_kernel (K5, evict-compact gather, all files)", "peak_source": peak_src,
-                     "traffic": None, "algorithmic_bytes_per_launch": compact_bytes / n_files},
+                     "kernel": "compact_kernel (K5, evict-compact gather, all 128 files, device time only)",
+                     "peak_source": peak_src, "traffic": traffic, "traffic_source": tinfo.get("source"),
+                     "algorithmic_bytes_per_launch": compact_bytes / n_files},
+        "clocks": sampler.summary(),
         "extra": {"decode_ms_holes": ms_before, "decode_gbs_holes": alg_before / (ms_before / 1000.0) / 1e9,
+                  "decode_holes_traffic_ratio": tinfo.get("holes_decode_traffic_over_algorithmic"),
                   "decode_ms_compacted": ms_after, "decode_gbs_compacted": alg_after / (ms_after / 1000.0) / 1e9,
-                  "compact_ms_all_files": ms_compact, "compact_bytes": compact_bytes,
+                  "compact_ms_device": ms_compact, "compact_ms_call": ms_call, "compact_call_host_ms": host_ms,
+                  "compact_bytes": compact_bytes,
                   "retained_tokens": retained, "h2o_scores": scores_info},
     }
     if args.real_scores:
         line["config"]["workload"] = line["config"]["workload"].replace(
             "lowest Exp(1) scores", "lowest H2O scores of a decode step (pred_attn_scores)")
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = oracle_compaction_sample(s, seed)
     print(json.dumps(line), flush=True)
+
+
+def oracle_compaction_sample(s, seed: int):
+    """cpu_baseline for cfg5(ii): the oracle's R7 compaction (oracle.Oracle.compact, NumPy) of ONE 65536-token
+    file with the same Exp(1) eviction, timed on the host cores; reported in the K5 roofline's unit (GB/s of
+    algorithmic compaction bytes)."""
+    import numpy as np
+
+    from oracle import Oracle
+    from synth.workloads import TAG_K, TAG_V, heavy_hitter_ranges, rows_np
+
+    L0, w = 65536, s.Hkv * s.D
+    o = Oracle(L0 // 16 * 2 + 64, s.P, 1, s.Hkv, s.D)
+    fd = o.open("x")
+    o.append(fd, list(range(L0)), rows_np(seed, TAG_K, 0, 0, 0, L0, w).reshape(1, L0, s.Hkv, s.D),
+             rows_np(seed, TAG_V, 0, 0, 0, L0, w).reshape(1, L0, s.Hkv, s.D))
+    o.evict(fd, [tuple(r) for r in heavy_hitter_ranges(seed, 0, L0, L0 // 2).tolist()])
+    t0 = time.perf_counter()
+    o.compact(fd)
+    el = time.perf_counter() - t0
+    nbytes = 2 * 2 * (L0 // 2) * w * 2
+    return {"value": nbytes / el / 1e9, "unit": "GB/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+            "sample": f"oracle.Oracle.compact of 1 of 128 files (32768 retained tokens, 50% random holes) in {el:.2f} s"}
 
 
 def run_offload(args):

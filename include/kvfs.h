@@ -336,6 +336,10 @@ typedef enum {
                                    query rows, and the per-file rest by the decode kernel, merged exactly
                                    (log-sum-exp).  0 = off; default 16 (head_dim 128 only) */,
   KVFS_OPT_PREFIX_SPLITS = 5,   /* key splits of each shared run in the cascade (1..8); 0 = auto */
+  KVFS_OPT_TIMING = 7,          /* 1: kvfs_compact_files records CUDA events around its device work (file
+                                   groups: upload + gathers) and, before returning, waits for them and
+                                   stores their summed device time in KVFS_CTR_COMPACT_DEVICE_NS (the host
+                                   R1 / table work that overlaps it excluded); 0 = off (default) */
   KVFS_OPT_FAULT_INJECT = 6     /* tests only: value n > 0 makes the n-th following pass through an
                                    injection point (mid-way through a pred reservation, after the first
                                    descriptor is committed; fork; open) throw std::bad_alloc inside the
@@ -351,7 +355,8 @@ typedef enum {
   KVFS_CTR_LAST_CHUNK_UNITS = 5, /* CTAs of the last tcgen05 chunk launch (0: none) */
   KVFS_CTR_LAST_PREFIX_UNITS = 6,  /* CTAs of the last shared-prefix (cascade) launch (0: none) */
   KVFS_CTR_LAST_PREFIX_GROUPS = 7, /* fork families (groups) the last pred batch attended as shared prefixes */
-  KVFS_CTR_HOST_PAGES = 8          /* pages currently in the host tier (kvfs_offload) */
+  KVFS_CTR_HOST_PAGES = 8,         /* pages currently in the host tier (kvfs_offload) */
+  KVFS_CTR_COMPACT_DEVICE_NS = 9   /* KVFS_OPT_TIMING: device time of the last kvfs_compact_files (ns) */
 } kvfs_counter;
 int kvfs_get_counter(kvfs_ctx *ctx, int counter, int64_t *value);
 

@@ -434,6 +434,13 @@ class CudaDevice final : public Device {
     // one packet for every file (old tables, new pages, first entries), then one K5 launch per file in
     // order, each after the first a programmatic dependent launch of the previous one (see compact_kernel)
     const kvfs_config &cfg = c_.cfg;
+    cudaEvent_t ev_end = nullptr;
+    if (c_.opt_timing) {  // device time of this group: upload + gathers (KVFS_CTR_COMPACT_DEVICE_NS)
+      cudaEvent_t e0 = nullptr;
+      if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&ev_end) != cudaSuccess) return KVFS_EIO;
+      cudaEventRecord(e0, cs(s));
+      timing_.push_back({e0, ev_end});
+    }
     const int P = cfg.page_size;
     std::vector<std::vector<int32_t>> fe(jobs.size());
     std::vector<const void *> dt(jobs.size()), dp(jobs.size()), df(jobs.size());
@@ -486,7 +493,22 @@ class CudaDevice final : public Device {
       ++c_.ctr.launches;
       if (e != cudaSuccess) return KVFS_EIO;
     }
+    if (ev_end) cudaEventRecord(ev_end, cs(s));
     return KVFS_OK;
+  }
+
+  // Sum of the recorded device intervals (each: a compact group's upload + gathers), then forget them.
+  int64_t take_device_ns() override {
+    double ms = 0;
+    for (auto &t : timing_) {
+      float x = 0.f;
+      if (cudaEventSynchronize(t.second) == cudaSuccess && cudaEventElapsedTime(&x, t.first, t.second) == cudaSuccess)
+        ms += x;
+      cudaEventDestroy(t.first);
+      cudaEventDestroy(t.second);
+    }
+    timing_.clear();
+    return static_cast<int64_t>(ms * 1e6);
   }
 
   int scores(const std::vector<ScoreDesc> &descs, const std::vector<ScoreUnit> &units, int layer, const void *q,
@@ -904,6 +926,7 @@ class CudaDevice final : public Device {
   bf16 **kptrs_ = nullptr, **vptrs_ = nullptr;
   int sms_ = 148;
   int per_sm_ = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timing_;
   int64_t k5_grid_ = 0;
   Staging stg_[4];
   int cur_ = 0;

@@ -258,29 +258,39 @@ int kvfs_compact_files(kvfs_ctx *ctx, const int *fds, int n, int *n_done, kvfs_s
       std::sort(u.begin(), u.end());
       if (std::adjacent_find(u.begin(), u.end()) != u.end()) return KVFS_EBUSY;
     }
-    // pages and tables in order (R1: each file's allocation sees the previous files' releases), each file's
-    // device gather enqueued as it goes; the host position passes afterwards, on worker threads
     std::vector<std::vector<Entry>> olds(static_cast<size_t>(n));
     std::vector<std::vector<uint32_t>> nps(static_cast<size_t>(n));
     int rc = KVFS_OK, done = 0;
-    for (int i = 0; i < n; ++i) {
-      rc = compact_file_tables(c, *files[i], &olds[i], &nps[i]);
-      if (rc != KVFS_OK) break;
-      ++done;
-    }
-    // the device gathers of the committed files, in order (R1 hands the next file the pages this one just
-    // released, so its destinations may be this file's sources: the data plane chains them)
-    if (c.dev && done > 0) {
-      std::vector<CompactJob> jobs;
-      for (int i = 0; i < done; ++i)
-        if (!nps[i].empty()) jobs.push_back({&olds[i], &nps[i], files[i]->len});
-      if (!jobs.empty()) {
-        const int drc = c.dev->compact(jobs, stream);
-        if (drc != KVFS_OK) {
-          c.poisoned = true;
-          rc = drc;
-        }
+    // Pages and tables in order (R1: each file's allocation sees the previous files' releases); the device
+    // gathers are handed to the data plane in groups of files as the host goes, so the host table work of
+    // the next group overlaps the GPU copying this one.  Inside a group the data plane chains the files
+    // (a file's destinations may be the previous file's sources); consecutive groups are stream-ordered.
+    constexpr int kGroup = 8;
+    std::vector<CompactJob> jobs;
+    auto flush = [&]() {
+      if (jobs.empty() || !c.dev || rc == KVFS_EIO) return;
+      const int drc = c.dev->compact(jobs, stream);
+      jobs.clear();
+      if (drc != KVFS_OK) {
+        c.poisoned = true;
+        rc = drc;
       }
+    };
+    for (int i = 0; i < n; ++i) {
+      const int trc = compact_file_tables(c, *files[i], &olds[i], &nps[i]);
+      if (trc != KVFS_OK) {
+        rc = trc;
+        break;
+      }
+      ++done;
+      if (!nps[i].empty()) jobs.push_back({&olds[i], &nps[i], files[i]->len});
+      if (static_cast<int>(jobs.size()) == kGroup) flush();
+      if (rc != KVFS_OK) break;
+    }
+    {
+      const int keep = rc;
+      flush();  // the committed files' gathers (also after an ENOSPC stop)
+      if (rc == KVFS_OK) rc = keep;
     }
     const int P = c.cfg.page_size;
     // Position passes: independent per file, on worker threads; a thread that cannot be started (resource
@@ -303,6 +313,7 @@ int kvfs_compact_files(kvfs_ctx *ctx, const int *fds, int n, int *n_done, kvfs_s
     work();
     for (auto &t : pool) t.join();
     if (n_done) *n_done = done;
+    if (c.dev && c.opt_timing) c.last_compact_device_ns = c.dev->take_device_ns();
     return rc;
   });
 }
@@ -701,6 +712,10 @@ int kvfs_set_option(kvfs_ctx *ctx, int option, int64_t value) {
         if (value < 0 || value > kMaxPrefixSplits) return KVFS_EINVAL;
         c.opt_prefix_splits = static_cast<int>(value);
         return KVFS_OK;
+      case KVFS_OPT_TIMING:
+        if (value < 0 || value > 1) return KVFS_EINVAL;
+        c.opt_timing = value != 0;
+        return KVFS_OK;
       case KVFS_OPT_FAULT_INJECT:
         if (value < 0) return KVFS_EINVAL;
         c.fault_countdown = value;
@@ -726,6 +741,7 @@ int kvfs_get_counter(kvfs_ctx *ctx, int counter, int64_t *value) {
       case KVFS_CTR_LAST_PREFIX_UNITS: *value = c.ctr.last_prefix_units; return KVFS_OK;
       case KVFS_CTR_LAST_PREFIX_GROUPS: *value = c.ctr.last_prefix_groups; return KVFS_OK;
       case KVFS_CTR_HOST_PAGES: *value = c.ctr.host_pages; return KVFS_OK;
+      case KVFS_CTR_COMPACT_DEVICE_NS: *value = c.last_compact_device_ns; return KVFS_OK;
       default: return KVFS_EINVAL;
     }
   });

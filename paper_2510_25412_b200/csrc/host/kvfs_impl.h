@@ -184,6 +184,8 @@ struct Ctx {
   int64_t opt_chunk_cutover = 8;
   int64_t opt_cascade_min_entries = 16;
   int opt_prefix_splits = 0;  // 0 = auto
+  bool opt_timing = false;    // KVFS_OPT_TIMING
+  int64_t last_compact_device_ns = 0;
   CtxCounters ctr;
   PredPlan plan;  // the open step's plan
   std::vector<int> step_status;
@@ -271,6 +273,8 @@ class Device {
   virtual int sync() = 0;
   virtual int sms() const = 0;
   virtual int64_t prefix_partial_capacity() const = 0;
+  // KVFS_OPT_TIMING: device time (ns) of the intervals recorded since the last call (waits for them)
+  virtual int64_t take_device_ns() = 0;
 };
 
 size_t device_workspace_bytes(const kvfs_config &cfg);
