@@ -43,6 +43,9 @@ def parse():
                          "instead of synthetic Exp(1) scores")
     ap.add_argument("--prefix-splits", type=int, default=0,
                     help="cascade tuning: key splits per shared run (KVFS_OPT_PREFIX_SPLITS; 0 = auto)")
+    ap.add_argument("--cutover", type=int, default=-1,
+                    help="tuning: n_q at or above which the tcgen05 chunk kernel runs (KVFS_OPT_CHUNK_CUTOVER; "
+                         "-1 = library default 8)")
     ap.add_argument("--decode-ctas", type=int, default=0,
                     help="tuning: decode-kernel ring count (KVFS_OPT_DECODE_CTAS; 0 = auto)")
     ap.add_argument("--scores", action="store_true",
@@ -384,6 +387,8 @@ def run_ours(args):
         wl.kv.set_option(K.OPT_PREFIX_SPLITS, args.prefix_splits)
     if args.decode_ctas:
         wl.kv.set_option(K.OPT_DECODE_CTAS, args.decode_ctas)
+    if args.cutover >= 0:
+        wl.kv.set_option(K.OPT_CHUNK_CUTOVER, args.cutover)
     s = wl.shape
     kv = wl.kv
     T = wl.n_files * wl.n_q
@@ -549,7 +554,7 @@ def run_ours(args):
     t_bytes = statistics.mean(alg_bytes) / (peak * 1e9)
     t_flops = flops_mean / (tc_peak * 1e12)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak}
-    if wl.n_q >= 8 and t_flops > 0.5 * t_bytes:
+    if t_flops > 0.5 * t_bytes:
         # chunk workloads sit at the ridge: report the binding roof (the larger ideal time)
         ach_tf = flops_mean / (k_ms / 1000.0) / 1e12
         if t_flops >= t_bytes:
@@ -579,7 +584,7 @@ def run_ours(args):
                    "l2": ("inputs larger than L2 (K/V read per step %.2f GB > 126 MB L2)" % (logical[0] / 1e9)
                           if logical[0] > 126e6 * 4 else
                           "unique K/V %.0f MB per step; the CoW-shared prefix is L2-resident by design" % (alg_bytes[0] / 1e6))},
-        "roofline": dict(roof, traffic=traffic, traffic_source=traffic_src, kernel=wl.dominant_kernel(),
+        "roofline": dict(roof, traffic=traffic, traffic_source=traffic_src, kernel=wl.dominant_kernel(args.cutover if args.cutover >= 0 else 8),
                          kernel_ms_mean=k_ms, peak_source=peak_src,
                          algorithmic_bytes_per_launch=statistics.mean(alg_bytes),
                          algorithmic_flops_per_launch=flops_mean),

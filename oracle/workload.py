@@ -26,7 +26,7 @@ class OracleWorkload:
         self.n_q = c["n_q"]
         s = self.s
         prefix = c.get("prefix_len", 0)
-        grow = 0 if c.get("rewind") else max_steps * self.n_q
+        grow = max_steps * max(0, self.n_q - c.get("rewind", 0))
         per_file = math.ceil((c["file_len"] + grow + s.P) / s.P) + 2
         self.o = Oracle(len(self.lips) * per_file + math.ceil(prefix / s.P) + 8, s.P, 1, s.Hkv, s.D)
         w = s.Hkv * s.D

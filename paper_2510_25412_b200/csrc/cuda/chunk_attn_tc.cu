@@ -3,26 +3,26 @@
 // rule R10 of SURVEY.md §8(c): each of the n_q new tokens attends to the file's retained tokens with
 // logical index <= len - n_q + i).
 //
-// Unit = (descriptor, kv head g, M-tile m): 128 query rows R = 128 m + r, row R <-> (qi = R / G, h = R % G),
-// so Q of the unit is a [rows][D] K-major tile loaded by one 4-D TMA box per 64-column half.
-// KV tiles = 128 keys = 128 / P consecutive page entries of the file (K and V blocks of the (page, g) pairs
-// loaded with 2-D TMA boxes of {64 cols, P rows}, 128-byte swizzle); the new tokens were scattered into the
-// pool by scatter_rows_kernel before this launch, so every key is read from the pool.
+// CTA = (descriptor, kv head g, pair of 128-row M-tiles) sharing every K/V tile.  Rows R = 128 m + r,
+// row R <-> (qi = R / G, h = R % G), so Q of an M-tile is a [rows][D] K-major tile loaded by one 4-D TMA box
+// per 64-column half.  KV tiles = 128 keys = 128 / P consecutive page entries of the file (K and V blocks of
+// the (page, g) pairs loaded with 2-D TMA boxes of {64 cols, P rows}, 128-byte swizzle); the new tokens were
+// scattered into the pool by scatter_rows_kernel before this launch, so every key is read from the pool.
 //   S  = Q K^T      tcgen05.mma kind::f16, M = 128, N = 128, K = 16 x 8, A = Q (smem, K-major),
-//                   B = K tile (smem, K-major), D = S in TMEM (double-buffered: columns 0 / 128)
-//   softmax         4 warps, thread = row: tcgen05.ld of the S row, masks (retained slots, causality from
-//                   per-column "new-token index" metadata written by the TMA warp), online softmax in the
-//                   log2 domain with lazy rescale of O (tcgen05.ld/st, only when the row max grows > 8),
-//                   P -> bf16 into smem in the 128B-swizzled K-major layout
-//   O += P V        M = 128, N = 128 (D), K = 16 x 8, A = P (smem, K-major), B = V tile (smem, MN-major),
-//                   D = O in TMEM (columns 256..383)
-// Warp roles (v2 below): 0 = K producer (+ Q, column metadata), 1 = MMA issuer (elect.sync lane),
-// 2 = TMEM allocator, 3 = V producer, 4..7 / 8..11 = softmax + epilogue of M-tile 0 / 1.
-// Measured per-128-key-tile timeline (tools/k2_trace.py, cfg4): softmax ~1.9k clk (max ~0.4k, exp2 ~1.1k
-// with 3/8 of the pairs on the FMA pipe), then P.V + S(t+1) of that M-tile ~1.0k on the tensor pipe:
-// period ~3.3k clk, tensor pipe ~63% busy.  A variant with P in separate TMEM columns and 64-key tiles
-// (S(t+1) overlapping the softmax; tools/chunk_attn_tc_v4_sep_p_experiment.cu.txt) measured 8% slower:
-// twice the per-tile fixed costs, both softmax groups in phase on the MUFU.
+//                   B = K tile (smem, K-major), D = S in TMEM (S0 / S1 at columns 0 / 128, one per M-tile)
+//   softmax         one warpgroup per M-tile, thread = row: tcgen05.ld of the S row, masks (retained slots,
+//                   causality from per-column "new-token index" metadata written by the K producer), online
+//                   softmax in the log2 domain with lazy rescale of O (tcgen05.ld/st, only when the row max
+//                   grows by > 8), P -> bf16 pairs written back into TMEM over the first 64 columns of S
+//   O += P V        M = 128, N = 128 (D), K = 16 x 8, A = P (TMEM, the .kind::f16 [a_tmem] form), B = V tile
+//                   (smem, MN-major), D = O in TMEM (O0 / O1 at columns 256 / 384), in two 64-key halves
+// Warp roles: 0 = K producer (+ Q, column metadata), 1 = MMA issuer (elect.sync lane), 2 = TMEM allocator,
+// 3 = V producer, 4..7 / 8..11 = softmax + epilogue of M-tile 0 / 1.
+// Measured per-128-key-tile timeline (tools/k2_trace.py, cfg4): softmax ~1.65k clk (MUFU floor ~0.77k with
+// EXP_EMU of 8 exp2 pairs on the FMA pipe), MMA-warp reaction ~0.26k, P.V(second half) + S(t+1) ~0.77k on
+// the tensor pipe, wake-up ~0.3k: period ~3.1k clk, tensor pipe ~64% busy.  Variants measured slower and
+// removed (git history): P in separate TMEM columns with 64-key tiles,
+// softmax groups issuing their own MMAs, one MMA warp per M-tile, split-column softmax, suspend-hint waits.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <math_constants.h>
@@ -44,23 +44,7 @@ constexpr int TILE_BYTES = 2 * HALF_BYTES;  // [128][128] bf16 = 32 KiB
 #endif
 constexpr int EXP_EMU = KVFS_EXP_EMU;  // of every 8 exp2 pairs in the softmax, how many run as a polynomial on the FMA pipe
 constexpr uint32_t TMEM_COLS = 512;
-#ifndef KVFS_K2_SELF_ISSUE
-#define KVFS_K2_SELF_ISSUE 0
-#endif
-// 1 = each softmax group's warp 0 issues its own MMAs after a group barrier (no MMA warp): measured slower
-// (period 4.5k vs 3.2k clk, tools/k2_trace.py) because the two groups fall into phase and the ping-pong of
-// softmax and tensor work between the M-tiles is lost; kept as a switch for the record.
-constexpr bool K2_SELF_ISSUE = KVFS_K2_SELF_ISSUE != 0;
-#ifndef KVFS_K2_ISSUERS
-#define KVFS_K2_ISSUERS 1
-#endif
-constexpr int K2_ISSUERS = KVFS_K2_ISSUERS;  // MMA-issuing warps (2: one per M-tile)
-// waits on the softmax <-> MMA handoff barriers: plain try_wait loop, or with a suspend-time hint
-#ifdef KVFS_K2_SLEEPWAIT
-#define K2_WAIT(b, ph) mbar_wait_sleep(b, ph)
-#else
 #define K2_WAIT(b, ph) mbar_wait(b, ph)
-#endif
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
   uint64_t d = 0;
   d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
@@ -241,9 +225,9 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
     mbar_init(bar(B_Q), PREFIX ? 4 * n_mt : 1);  // prefix: one arrival per softmax warp that gathers Q
     for (int s = 0; s < KV2; ++s) {
       mbar_init(bar(B_KF + s), 1);
-      mbar_init(bar(B_KE + s), (K2_SELF_ISSUE || K2_ISSUERS == 2) ? n_mt : 1);
+      mbar_init(bar(B_KE + s), 1);
       mbar_init(bar(B_VF + s), 1);
-      mbar_init(bar(B_VE + s), (K2_SELF_ISSUE || K2_ISSUERS == 2) ? n_mt : 1);
+      mbar_init(bar(B_VE + s), 1);
     }
     for (int m = 0; m < 2; ++m) {
       mbar_init(bar(B_SF + m), 1);
@@ -275,8 +259,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   }
   constexpr uint32_t tmem = 0;
 
-  // MMA issue helpers (one elected lane of the calling warp; K2_SELF_ISSUE: warp 0 of each softmax group
-  // issues its own M-tile's MMAs right after a group barrier, instead of signalling a separate MMA warp)
+  // MMA issue helpers (one elected lane of the MMA warp)
   constexpr uint32_t ID_S = idesc_bf16(false), ID_O = idesc_bf16(true);
     auto issue_s = [&](int t, int m) {
       tc_fence_after();
@@ -303,7 +286,9 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
                       umma_desc(sbase + OFF_V2 + (t % KV2) * TILE_BYTES + k * 2048, HALF_BYTES, 1024), ID_O,
                       (t > 0 || k > 0));
         }
-        if (half) mma_commit(bar(B_OF + m));
+        // O complete: one commit after the last tile's P.V only (the softmax waits for it once, in the
+        // epilogue; a commit per tile left phases nobody waits on, which compute-sanitizer synccheck reports)
+        if (half && t == n_tiles - 1) mma_commit(bar(B_OF + m));
       }
       __syncwarp();
     };
@@ -408,17 +393,12 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         }
         __syncwarp();
       }
-    } else if ((warp == 1 || (warp == 2 && K2_ISSUERS == 2)) && !K2_SELF_ISSUE) {
-      // ============================================================ MMA issuer(s)
-      // K2_ISSUERS == 2: warp 1 + m issues M-tile m, so a tcgen05.mma issue blocked on a full tensor queue
-      // delays only its own M-tile; the K / V stage releases then take one commit per issuer.
-      const int m_lo = K2_ISSUERS == 2 ? warp - 1 : 0;
-      const int m_hi = K2_ISSUERS == 2 ? min(warp, n_mt) : n_mt;
-      if (m_lo < m_hi) {
+    } else if (warp == 1) {
+      // ============================================================ MMA issuer
       mbar_wait(bar(B_Q), 0);
       if (lane == 0) K2T(25, 0);
       mbar_wait(bar(B_KF + 0), 0);
-      for (int m = m_lo; m < m_hi; ++m) issue_s(0, m);
+      for (int m = 0; m < n_mt; ++m) issue_s(0, m);
       if (elect_one()) mma_commit(bar(B_KE + 0));
       __syncwarp();
       for (int t = 0; t < n_tiles; ++t) {
@@ -426,14 +406,14 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         const bool more = t + 1 < n_tiles;
         mbar_wait(bar(B_VF + s), (t / KV2) & 1);
         if (lane == 0) K2T(9, t);
-        for (int m = m_lo; m < m_hi; ++m) {
+        for (int m = 0; m < n_mt; ++m) {
           K2_WAIT(bar(B_PF + 2 * m), t & 1);  // softmax m wrote P(t) keys 0..63 (and corrected O)
           issue_pv(t, m, 0);
           K2_WAIT(bar(B_PF + 2 * m + 1), t & 1);  // keys 64..127
           if (lane == 0) K2T(10 + 2 * m, t);
           issue_pv(t, m, 1);
           if (more) {                       // in-order after PV(t): S(t+1) may overwrite P(t)'s columns
-            if (m == m_lo) mbar_wait(bar(B_KF + (t + 1) % KV2), ((t + 1) / KV2) & 1);
+            if (m == 0) mbar_wait(bar(B_KF + (t + 1) % KV2), ((t + 1) / KV2) & 1);
             issue_s(t + 1, m);
           }
           if (lane == 0) K2T(11 + 2 * m, t);
@@ -443,7 +423,6 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           mma_commit(bar(B_VE + s));
         }
         __syncwarp();
-      }
       }
     }
   } else {
@@ -481,13 +460,6 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         if (lane == 0) mbar_arrive(bar(B_Q));
       }
       float m_run = -CUDART_INF_F, l_run = 0.f;
-      if (K2_SELF_ISSUE && wq == 0) {
-        mbar_wait(bar(B_Q), 0);
-        mbar_wait(bar(B_KF + 0), 0);
-        issue_s(0, m);
-        if (elect_one()) mma_commit(bar(B_KE + 0));
-        __syncwarp();
-      }
       for (int t = 0; t < n_tiles; ++t) {
         // The column metadata of tile t is ready long before S(t): its (~150 clk) barrier wait is taken
         // while the tensor pipe is still computing S(t), off the critical path.
@@ -566,31 +538,8 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           tmem_st32(s_col + c * 32, w);
           tmem_wait_st();
           tc_fence_before();
-          if constexpr (K2_SELF_ISSUE) {
-            named_bar_sync(1 + m, 128);  // the group's P half is in TMEM
-            if (wq == 0) {
-              const int s = t % KV2;
-              if (c == 0) {
-                mbar_wait(bar(B_VF + s), (t / KV2) & 1);
-                issue_pv(t, m, 0);
-              } else {
-                issue_pv(t, m, 1);
-                const bool more = t + 1 < n_tiles;
-                if (more) {  // in order after P.V(t): S(t+1) may overwrite P(t)'s columns
-                  mbar_wait(bar(B_KF + (t + 1) % KV2), ((t + 1) / KV2) & 1);
-                  issue_s(t + 1, m);
-                }
-                if (elect_one()) {
-                  if (more) mma_commit(bar(B_KE + (t + 1) % KV2));
-                  mma_commit(bar(B_VE + s));
-                }
-                __syncwarp();
-              }
-            }
-          } else {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar(B_PF + 2 * m + c));
-          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(bar(B_PF + 2 * m + c));
         }
         if (wq == 0 && lane == 0) K2T(18 + 6 * m, t);
         const float2 ls2 = add2(ls4[0], ls4[1]);
@@ -599,7 +548,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         if (wq == 0 && lane == 0) K2T(19 + 6 * m, t);
       }
       // epilogue: O / l -> bf16 out, lse   (prefix mode: the partial O, m, l of the split)
-      mbar_wait(bar(B_OF + m), (n_tiles - 1) & 1);
+      mbar_wait(bar(B_OF + m), 0);
       if (m == 0 && wq == 0 && lane == 0) K2T(26, 0);
       tc_fence_after();
       if constexpr (PREFIX) {
@@ -632,12 +581,8 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           for (int it = 0; it < 16; ++it) {  // (D + 2)-float rows are 8-byte aligned: float2, 2 rows per store
             const int rr = it * 2 + (lane >> 4), j = (lane & 15) * 2;
             float *d = reinterpret_cast<float *>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dst), rr));
-#ifndef KVFS_K2_NOSTORE
             // st.global: a generic store could alias buf and serialised the loop (~70 clk per iteration)
             if (d) __stcg(reinterpret_cast<float2 *>(d + c * 32 + j), make_float2(buf[rr * 33 + j], buf[rr * 33 + j + 1]));
-#else
-            if (d && buf[rr * 33 + j] == 12345.f) *reinterpret_cast<float2 *>(d + c * 32 + j) = make_float2(1.f, 2.f);
-#endif
           }
           __syncwarp();
           if (m == 0 && wq == 0 && lane == 0) K2T(28, c);

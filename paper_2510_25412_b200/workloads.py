@@ -52,7 +52,7 @@ class DecodeWorkload:
         self.steps_total = steps_total
         s = self.shape
         self.dev = torch.device("cuda", device)
-        grow = 0 if self.rewind else steps_total * self.n_q
+        grow = steps_total * max(0, self.n_q - self.rewind)  # net growth per step (drafts: n_q - rewind)
         per_file = math.ceil((self.file_len + grow + s.P) / s.P) + 2
         self.n_pages = (self.n_files + room_files) * per_file + math.ceil(self.prefix_len / s.P) + 64
         self.step_owner_base = step_owner_base
@@ -168,8 +168,8 @@ class DecodeWorkload:
         lens = self.lens if lens is None else lens
         return int(4 * s.Hq * s.D * (n * int(lens.sum()) + self.n_files * (n * (n + 1) // 2)))
 
-    def dominant_kernel(self) -> str:
-        if self.n_q >= 8:
+    def dominant_kernel(self, cutover: int = 8) -> str:
+        if cutover > 0 and self.n_q >= cutover:
             return "chunk_attn_tc_kernel (K2, tcgen05 QK^T / PV with TMEM accumulators)"
         if self.prefix_len:
             return ("chunk_attn_tc_kernel<G, prefix> (shared prefix once per batch, tcgen05) + decode_attn_kernel "

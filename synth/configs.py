@@ -25,6 +25,13 @@ CONFIGS: Dict[str, dict] = {
     "cfg2": dict(workload="cfg2: Llama-3-8B attn (32q/8kv, hd128, bf16, P=16), 256 LIPs decode (n_q=1) "
                           "from 2048-token KVFS files, 1 layer per step",
                  shape=Shape(32, 8, 128, 16), n_files=256, file_len=2048, n_q=1, seed=1002),
+    # PAPER.md §4.1 P:217 speculative drafts on the cfg2 shape: every step a LIP appends 4 draft tokens
+    # (n_q = 4: 2 <= n_q < the chunk cut-over), the verifier keeps the first, the rest is truncated before
+    # the next step (rewind 3): files grow by one token per step
+    "cfg2d": dict(workload="cfg2d: speculative drafts on the cfg2 shape, 256 LIPs x 2048-token files (32q/8kv, hd128, "
+                           "P=16), each step truncates the 3 rejected drafts of the previous step and appends 4 draft "
+                           "tokens (n_q=4)",
+                  shape=Shape(32, 8, 128, 16), n_files=256, file_len=2048, n_q=4, seed=1012, rewind=3),
     # BASELINE.json configs[2]: tree-of-thought fan-out, 64 forks of a 4096-token CoW prefix + 512-token branches
     "cfg3": dict(workload="cfg3: ToT fan-out, 64 LIPs forked from one 4096-token prefix file (CoW, 0 tail copies) "
                           "+ 512-token private branches, decode n_q=1 (32q/8kv, hd128, P=16)",

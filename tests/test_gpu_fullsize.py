@@ -17,14 +17,20 @@ from oracle.workload import OracleWorkload  # noqa: E402
 from paper_2510_25412_b200.workloads import DecodeWorkload  # noqa: E402
 
 
-@pytest.mark.parametrize("cfg,steps,lips", [
-    ("cfg2", 3, [0, 1, 37, 127, 128, 200, 254, 255]),
-    ("cfg3", 3, [0, 31, 63]),
-    ("cfg4", 2, [0, 77, 127]),
-    ("cfg5", 2, [5]),
+@pytest.mark.parametrize("cfg,steps,lips,cutover", [
+    ("cfg2", 3, [0, 1, 37, 127, 128, 200, 254, 255], None),
+    ("cfg2d", 3, [0, 99, 255], None),   # drafts (n_q = 4) through K1
+    ("cfg2d", 3, [0, 99, 255], 2),      # ... and through the tcgen05 chunk kernel (cut-over 2)
+    ("cfg3", 3, [0, 31, 63], None),
+    ("cfg4", 2, [0, 77, 127], None),
+    ("cfg5", 2, [5], None),
 ])
-def test_full_size_sampled_parity(cfg, steps, lips):
+def test_full_size_sampled_parity(cfg, steps, lips, cutover):
+    from paper_2510_25412_b200 import kvfs as K
+
     wl = DecodeWorkload(cfg, steps_total=steps + 1)
+    if cutover is not None:
+        wl.kv.set_option(K.OPT_CHUNK_CUTOVER, cutover)
     s = wl.shape
     T = wl.n_files * wl.n_q
     out = torch.empty((T, s.Hq, s.D), dtype=torch.bfloat16, device="cuda")
