@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--cutover", type=int, default=-1,
                     help="tuning: n_q at or above which the tcgen05 chunk kernel runs (KVFS_OPT_CHUNK_CUTOVER; "
                          "-1 = library default 8)")
+    ap.add_argument("--decode-chunks", type=int, default=-1,
+                    help="tuning: dynamic decode scheduling with this many chunks (KVFS_OPT_DECODE_CHUNKS; 0 = static; "
+                         "-1 = library default)")
     ap.add_argument("--decode-ctas", type=int, default=0,
                     help="tuning: decode-kernel ring count (KVFS_OPT_DECODE_CTAS; 0 = auto)")
     ap.add_argument("--scores", action="store_true",
@@ -389,6 +392,8 @@ def run_ours(args):
         wl.kv.set_option(K.OPT_DECODE_CTAS, args.decode_ctas)
     if args.cutover >= 0:
         wl.kv.set_option(K.OPT_CHUNK_CUTOVER, args.cutover)
+    if args.decode_chunks >= 0:
+        wl.kv.set_option(K.OPT_DECODE_CHUNKS, args.decode_chunks)
     s = wl.shape
     kv = wl.kv
     T = wl.n_files * wl.n_q

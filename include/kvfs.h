@@ -336,6 +336,11 @@ typedef enum {
                                    query rows, and the per-file rest by the decode kernel, merged exactly
                                    (log-sum-exp).  0 = off; default 16 (head_dim 128 only) */,
   KVFS_OPT_PREFIX_SPLITS = 5,   /* key splits of each shared run in the cascade (1..8); 0 = auto */
+  KVFS_OPT_DECODE_CHUNKS = 8,   /* decode-kernel scheduling: 0 = static (ring r streams the r-th of
+                                   KVFS_OPT_DECODE_CTAS equal contiguous stage ranges; default); n in 1..2048 =
+                                   dynamic: the batch's stages are cut into n equal ranges that at most one
+                                   wave of rings takes from a device counter as they finish (load balance when
+                                   some SMs are busy, e.g. with the cascade's shared-prefix kernel) */
   KVFS_OPT_TIMING = 7,          /* 1: kvfs_compact_files records CUDA events around its device work (file
                                    groups: upload + gathers) and, before returning, waits for them and
                                    stores their summed device time in KVFS_CTR_COMPACT_DEVICE_NS (the host

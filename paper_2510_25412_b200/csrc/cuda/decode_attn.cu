@@ -53,7 +53,7 @@ struct DecodeCfg {
   static constexpr int NQ = 4;                   // Q ring slots
   static constexpr int PART = G * (D + 2);       // floats per partial (o, m, l per head)
   static constexpr int RING_BYTES_RAW = NSTAGES * STAGE_BYTES + NQ * G * D * 2 + NW * PART * 4 + NSTAGES * 16 +
-                                        (2 * NSTAGES + 2 * NQ) * 8 + 16;
+                                        (2 * NSTAGES + 2 * NQ + 4) * 8 + 16 + 16;
   static constexpr int RING_BYTES = (RING_BYTES_RAW + 127) / 128 * 128;
   static constexpr int R_RAW = 232448 / RING_BYTES;  // 227 KB of dynamic shared memory per CTA
   static constexpr int R = R_RAW > 4 ? 4 : R_RAW;    // rings per CTA
@@ -155,14 +155,21 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
   __nv_bfloat16 *qring = reinterpret_cast<__nv_bfloat16 *>(smem + NSTAGES * C::STAGE_BYTES);  // [NQ][G][D]
   float *comb = reinterpret_cast<float *>(qring + C::NQ * G * D);                // [NW][PART]
   StageMeta *meta = reinterpret_cast<StageMeta *>(comb + NW * C::PART);          // [NSTAGES]
-  uint64_t *bars = reinterpret_cast<uint64_t *>(meta + NSTAGES);                 // full, empty, qfull, qempty
-  int *flag = reinterpret_cast<int *>(bars + 2 * NSTAGES + 2 * C::NQ);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(meta + NSTAGES);  // full, empty, qfull, qempty, cfull, cempty
+  int *flag = reinterpret_cast<int *>(bars + 2 * NSTAGES + 2 * C::NQ + 4);
+  int *chunk_slot = flag + 4;                                        // [2] chunk ids (dynamic scheduling)
 
-  const int cta = blockIdx.x * C::R + ring;  // virtual CTA: one contiguous stage range per ring
+  // Physical ring pr processes "chunks" = virtual CTAs (contiguous stage ranges, p.ncta of them): static
+  // scheduling gives ring pr chunk pr; dynamic scheduling (p.dynamic) lets the ring's producer take chunk
+  // after chunk from a global counter and hand each id to its consumers through a 2-slot chunk ring, so
+  // rings whose SM frees up early (e.g. next to the shared-prefix kernel of a cascade) do more of the work.
+  const int pr = blockIdx.x * C::R + ring;
   auto full_bar = [&](int s) { return smem_u32(bars + s); };
   auto empty_bar = [&](int s) { return smem_u32(bars + NSTAGES + s); };
   auto qfull_bar = [&](int s) { return smem_u32(bars + 2 * NSTAGES + s); };
   auto qempty_bar = [&](int s) { return smem_u32(bars + 2 * NSTAGES + C::NQ + s); };
+  auto cfull_bar = [&](int s) { return smem_u32(bars + 2 * NSTAGES + 2 * C::NQ + s); };
+  auto cempty_bar = [&](int s) { return smem_u32(bars + 2 * NSTAGES + 2 * C::NQ + 2 + s); };
 
   if (threadIdx.x < C::R) {  // thread r initialises ring r's barriers
     uint64_t *rb = reinterpret_cast<uint64_t *>(
@@ -175,24 +182,46 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
       mbar_init(smem_u32(rb + 2 * NSTAGES + s), 1);
       mbar_init(smem_u32(rb + 2 * NSTAGES + C::NQ + s), NW);
     }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(smem_u32(rb + 2 * NSTAGES + 2 * C::NQ + s), 1);
+      mbar_init(smem_u32(rb + 2 * NSTAGES + 2 * C::NQ + 2 + s), NW);
+    }
     fence_mbar_init();
   }
   __syncthreads();
   // launched programmatically after the table-delta prologue (no shared-prefix kernel in between): the
   // setup above overlapped its tail; wait for it before reading the page tables
   if (p.wait_at_start) asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int64_t beg = cta < p.ncta ? cta_start(cta, p.total, p.ncta) : 0;
-  const int64_t end = cta < p.ncta ? cta_start(cta + 1, p.total, p.ncta) : 0;
+  const bool ring_live = ring < C::R && pr < p.n_rings;
 
   if (is_producer) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::PRODUCER_REGS));
-    if (ring >= C::R || beg >= end) return;
+    if (!ring_live) return;
     // ================================================================ producer warp
     // Lanes prepare up to 32 stages at once (one coalesced load of their page-table entries), then lane 0
     // issues them in order: wait for the ring slot, publish the stage meta, arm the barrier, 1-D TMA.
     const uint64_t pol = policy_evict_first();
-    int64_t x = beg;
     int local = 0, segi = 0;
+    for (int k = 0;; ++k) {
+    int cta = (k == 0) ? pr : p.ncta;  // static: one chunk per ring
+    if (p.dynamic) {
+      if (lane == 0) {
+        cta = atomicAdd(p.work, 1);
+        if (k >= 2) mbar_wait_sleep(cempty_bar(k & 1), ((k >> 1) & 1) ^ 1);
+        chunk_slot[k & 1] = cta;
+        mbar_arrive(cfull_bar(k & 1));  // release: the id is visible to the consumers
+        // the last ring to run out of chunks resets the counters for the next launch (every ring's final
+        // fetch happened before its increment of the second counter)
+        if (cta >= p.ncta && atomicAdd(p.work + 1, 1) == p.n_rings - 1) {
+          p.work[0] = 0;
+          p.work[1] = 0;
+        }
+      }
+      cta = __shfl_sync(0xffffffffu, cta, 0);
+    }
+    if (cta >= p.ncta) break;
+    const int64_t beg = cta_start(cta, p.total, p.ncta), end = cta_start(cta + 1, p.total, p.ncta);
+    int64_t x = beg;
     while (x < end) {
       const Segment sg = make_segment(p.descs, p.n_desc, x, end, p.Hkv);
       const Desc dd = p.descs[sg.d];
@@ -274,11 +303,12 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
       x += sg.nst;
       ++segi;
     }
+    }
     return;
   }
 
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::CONSUMER_REGS));
-  if (ring >= C::R || beg >= end) return;
+  if (!ring_live) return;
   // ================================================================ consumers
   // Lane (kg, sub): key group kg = lane / LPK scores key kg of every warp step; sub = lane % LPK owns
   // dims {(c*LPK + sub)*8 .. +8} for c < CH.  After the transposing xor-reduction of the G partial dot
@@ -288,8 +318,18 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
   constexpr int SPH = LPK / G;  // lanes per head within a key group
   const int kg = lane / LPK, sub = lane % LPK;
   const int hm = sub / SPH;
-  int64_t x = beg;
   int local0 = 0, segi = 0;
+  for (int k = 0;; ++k) {
+  int cta = (k == 0) ? pr : p.ncta;
+  if (p.dynamic) {
+    mbar_wait(cfull_bar(k & 1), (k >> 1) & 1);
+    cta = chunk_slot[k & 1];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(cempty_bar(k & 1));
+  }
+  if (cta >= p.ncta) break;
+  const int64_t beg = cta_start(cta, p.total, p.ncta), end = cta_start(cta + 1, p.total, p.ncta);
+  int64_t x = beg;
   bool first_seg = true;
   while (x < end) {
     const Segment sg = make_segment(p.descs, p.n_desc, x, end, p.Hkv);
@@ -579,6 +619,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
     ++segi;
     first_seg = false;
   }
+  }
 }
 
 template <class C>
@@ -606,7 +647,7 @@ static cudaError_t launch_decode_t(const DecodeParams &p, cudaStream_t s, int *p
     return cudaSuccess;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((p.ncta + C::R - 1) / C::R);
+  cfg.gridDim = dim3((p.n_rings + C::R - 1) / C::R);
   cfg.blockDim = dim3(C::THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;

@@ -25,6 +25,7 @@ size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 struct WsLayout {
   size_t slab = 0, upload = 0, counters = 0, partials = 0, ptrs = 0, prefix = 0, total = 0, upload_cap = 0;
   size_t scratch = 0, scratch_cap = 0;  // second upload area: packets sent while a pred step is open
+  size_t work = 0;                      // [2] int: K1 dynamic-scheduling counters (self-resetting)
   int64_t prefix_cap = 0;  // shared-prefix partials (PART floats each)
 };
 
@@ -50,6 +51,8 @@ WsLayout ws_layout(const kvfs_config &c) {
   off = align256(off + w.scratch_cap);
   w.counters = off;
   off = align256(off + static_cast<size_t>(c.max_batch_rows) * c.n_kv_heads * 4);
+  w.work = off;
+  off = align256(off + 16);
   w.partials = off;
   off = align256(off + static_cast<size_t>(kMaxCtas) * 2 * part);
   w.ptrs = off;
@@ -370,6 +373,8 @@ class CudaDevice final : public Device {
       return KVFS_EIO;
     if (cudaMemset(counters_, 0, static_cast<size_t>(cfg.max_batch_rows) * cfg.n_kv_heads * 4) != cudaSuccess)
       return KVFS_EIO;
+    work_ = reinterpret_cast<int *>(ws + lay_.work);
+    if (cudaMemset(work_, 0, 16) != cudaSuccess) return KVFS_EIO;
     // Zero-fill the pools once: every slot then always holds finite bf16 (only finite rows are ever
     // written), so the tensor-core kernel can multiply masked-out keys' V rows by P = 0 safely.
     const size_t pool_bytes = static_cast<size_t>(cfg.n_pages) * cfg.n_kv_heads * cfg.page_size * cfg.head_dim * 2;
@@ -615,6 +620,17 @@ class CudaDevice final : public Device {
     }
     ncta = std::min<int64_t>(std::min<int64_t>(ncta, kMaxCtas), pl.total_cost);
     p.ncta = static_cast<int>(ncta);
+    p.n_rings = p.ncta;
+    p.dynamic = 0;
+    p.work = work_;
+    if (c_.opt_decode_chunks > 0) {
+      // dynamic scheduling: opt_decode_chunks chunks taken from a counter by at most one wave of rings
+      const int64_t chunks = std::min<int64_t>(std::min<int64_t>(c_.opt_decode_chunks, kMaxCtas), pl.total_cost);
+      p.ncta = static_cast<int>(chunks);
+      p.n_rings = static_cast<int>(std::min<int64_t>(chunks, static_cast<int64_t>(sms_) * per_sm_));
+      p.dynamic = 1;
+      ncta = chunks;
+    }
     p.slab = slab_;
     p.dst_slot = static_cast<const int32_t *>(d_dst_);
     p.q = static_cast<const bf16 *>(q);
@@ -921,6 +937,7 @@ class CudaDevice final : public Device {
   char *area_ = nullptr;  // upload area of the current packet (upload_ or the scratch area)
   size_t area_cap_ = 0;
   int *counters_ = nullptr;
+  int *work_ = nullptr;
   float *partials_ = nullptr;
   float *ppart_ = nullptr;
   bf16 **kptrs_ = nullptr, **vptrs_ = nullptr;

@@ -13,7 +13,10 @@ struct DecodeParams {
   const Desc *descs;
   int n_desc;
   int64_t total;  // total stages
-  int ncta;
+  int ncta;       // chunks (virtual CTAs: contiguous stage ranges)
+  int n_rings;    // physical rings launched (== ncta unless dynamic)
+  int dynamic;    // 1: rings take chunks from the counter `work` (else ring r takes chunk r)
+  int *work;      // [2] self-resetting counters (next chunk, finished rings)
   const Entry *slab;
   const int32_t *dst_slot;
   const __nv_bfloat16 *q, *k_new, *v_new;

@@ -712,6 +712,10 @@ int kvfs_set_option(kvfs_ctx *ctx, int option, int64_t value) {
         if (value < 0 || value > kMaxPrefixSplits) return KVFS_EINVAL;
         c.opt_prefix_splits = static_cast<int>(value);
         return KVFS_OK;
+      case KVFS_OPT_DECODE_CHUNKS:
+        if (value < 0 || value > 2048) return KVFS_EINVAL;
+        c.opt_decode_chunks = value;
+        return KVFS_OK;
       case KVFS_OPT_TIMING:
         if (value < 0 || value > 1) return KVFS_EINVAL;
         c.opt_timing = value != 0;

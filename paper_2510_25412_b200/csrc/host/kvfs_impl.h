@@ -181,6 +181,7 @@ struct Ctx {
   bool step_open = false;
   int64_t batch_counter = 0;
   int64_t opt_decode_ctas = 0;
+  int64_t opt_decode_chunks = 0;  // KVFS_OPT_DECODE_CHUNKS (0: static scheduling)
   int64_t opt_chunk_cutover = 8;
   int64_t opt_cascade_min_entries = 16;
   int opt_prefix_splits = 0;  // 0 = auto

@@ -119,3 +119,20 @@ def test_cascade_forced_splits(splits):
     assert st == [0] * 7
     assert h.c.counter(K.CTR_LAST_PREFIX_GROUPS) == 1
     h.check_meta()
+
+
+@pytest.mark.parametrize("chunks", [64, 700])
+def test_cascade_dynamic_decode(chunks):
+    """The cascade with the dynamic decode scheduling (KVFS_OPT_DECODE_CHUNKS): chunks merge with the
+    shared-prefix partials exactly as the static grid."""
+    h = Harness(3000, 16, 32, 8, 128, seed=60 + chunks)
+    h.c.set_option(K.OPT_CASCADE_MIN_ENTRIES, 4)
+    h.c.set_option(K.OPT_DECODE_CHUNKS, chunks)
+    kids = [f"k{i}" for i in range(9)]
+    _family(h, "root", 1500, kids, [0, 3, 30, 129, 1, 64, 300, 2, 17], evict_root=[(10, 33)])
+    for _ in range(2):
+        st, *_ = h.pred(_decode_rows(h, kids + ["root"]))
+        assert st == [0] * 10
+        assert h.c.counter(K.CTR_LAST_PREFIX_GROUPS) == 1
+    h.check_meta()
+    h.check_data()

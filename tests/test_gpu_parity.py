@@ -115,9 +115,13 @@ def test_closed_forms():
     assert_close(to_bits(out)[0], ref, "mean V")
 
 
-@pytest.mark.parametrize("ctas", [1, 2, 7, 148, 592, 2048])
-def test_split_invariance_and_determinism(ctas):
-    """Forced grid sizes (split counts) agree within tolerance with the oracle; each is bitwise repeatable."""
+@pytest.mark.parametrize("ctas,chunks", [(1, 0), (2, 0), (7, 0), (148, 0), (592, 0), (2048, 0),
+                                         (0, 1), (0, 5), (0, 600), (0, 2048)])
+def test_split_invariance_and_determinism(ctas, chunks):
+    """Forced grid sizes (split counts) agree within tolerance with the oracle; each is bitwise repeatable.
+    chunks > 0: dynamic scheduling (KVFS_OPT_DECODE_CHUNKS): rings take the chunks from a device counter in
+    whatever order they finish; the merge of a unit's pieces is still in chunk order, so the result is
+    bitwise repeatable too, and the counter resets itself between launches (second batch below)."""
     h = Harness(2000, 16, 32, 8, 128, seed=9)
     rows = []
     for i in range(12):
@@ -125,6 +129,7 @@ def test_split_invariance_and_determinism(ctas):
         h.append(f"f{i}", list(range(50 + 97 * i)))
     h.evict("f3", [(5, 200)])
     h.c.set_option(1, ctas)  # KVFS_OPT_DECODE_CTAS
+    h.c.set_option(8, chunks)  # KVFS_OPT_DECODE_CHUNKS
     for i in range(12):
         last = h.o.stat(h.fds[f"f{i}"][1])[2]
         rows.append((f"f{i}", [last + 1] if i % 3 else [last + 1, last + 2, last + 3]))
@@ -136,8 +141,14 @@ def test_split_invariance_and_determinism(ctas):
         h2.append(f"f{i}", list(range(50 + 97 * i)))
     h2.evict("f3", [(5, 200)])
     h2.c.set_option(1, ctas)
+    h2.c.set_option(8, chunks)
     _, ob2, lb2, _, _ = h2.pred(rows, qstd=4.0)
     assert np.array_equal(ob1, ob2) and np.array_equal(lb1, lb2)
+    # a second batch on each (the dynamic counters were reset by the first launch)
+    rows2 = [(n, [p[-1] + 1]) for n, p in rows]
+    _, ob3, lb3, _, _ = h.pred(rows2, qstd=4.0)
+    _, ob4, lb4, _, _ = h2.pred(rows2, qstd=4.0)
+    assert np.array_equal(ob3, ob4) and np.array_equal(lb3, lb4)
 
 
 def test_fork_isolation_bitwise():
