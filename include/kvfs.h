@@ -326,7 +326,9 @@ int kvfs_sched_form(kvfs_sched *s, double now, pred_desc *descs, int desc_cap, i
 typedef enum {
   KVFS_OPT_DECODE_CTAS = 1,     /* grid size of the decode kernel; 0 = auto (SM count x occupancy) */
   KVFS_OPT_CHUNK_CUTOVER = 2,   /* n_q at or above which the tcgen05 chunk kernel is used (head_dim 128);
-                                   0 = never; default 8 */
+                                   0 = never; default 2: the decode kernel streams a file once per query row
+                                   (ncu, cfg2 shape with n_q = 4 drafts: 4.0x the K/V bytes, 1.29 ms), the chunk
+                                   kernel once per (descriptor, kv head) (1.0x, 0.44 ms) */
   KVFS_OPT_DETERMINISTIC = 3,   /* reserved (the kernels are deterministic for a fixed grid) */
   KVFS_OPT_CASCADE_MIN_ENTRIES = 4 /* shared-prefix ("cascade") decode for CoW fork families (§4.2
                                    P:223 fork shares pages): decode descriptors (n_q

@@ -141,6 +141,29 @@ __device__ __forceinline__ void fold_prefix(const float2 (&pml)[kMaxPrefixSplits
   }
 }
 
+#ifdef KVFS_K1_TRACE
+// Development trace (tools/cascade_trace.py): per physical ring, %globaltimer (ns) at kernel start, the
+// producer's first TMA, the consumers' first full stage, the end of streaming and the end of the output.
+__device__ unsigned long long g_k1_trace[6][2048];
+__device__ __forceinline__ unsigned long long k1_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define K1T(ev, r)                                  \
+  do {                                              \
+    if ((r) < 2048) g_k1_trace[ev][r] = k1_now();   \
+  } while (0)
+extern "C" int kvfs_debug_k1_trace(void *host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, g_k1_trace, bytes < sizeof(g_k1_trace) ? bytes : sizeof(g_k1_trace)) ==
+                 cudaSuccess ? 0 : -1;
+}
+#else
+#define K1T(ev, r) \
+  do {             \
+  } while (0)
+#endif
+
 template <class C>
 __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const DecodeParams p) {
   constexpr int D = C::D, G = C::G, P = C::P, NW = C::NW, NSTAGES = C::NSTAGES;
@@ -193,6 +216,14 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
   // setup above overlapped its tail; wait for it before reading the page tables
   if (p.wait_at_start) asm volatile("griddepcontrol.wait;" ::: "memory");
   const bool ring_live = ring < C::R && pr < p.n_rings;
+#ifdef KVFS_K1_TRACE
+  if (is_producer && lane == 0 && ring_live) {
+    K1T(0, pr);
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    if (pr < 2048) g_k1_trace[5][pr] = smid;
+  }
+#endif
 
   if (is_producer) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::PRODUCER_REGS));
@@ -267,6 +298,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
           const int loj = __shfl_sync(0xffffffffu, lo, j);
           const int nrj = __shfl_sync(0xffffffffu, nrows, j);
           if (lane == 0) {
+            if (local == 0) K1T(1, pr);
             const int slot = local % NSTAGES;
             if (local >= NSTAGES) mbar_wait_sleep(empty_bar(slot), ((local / NSTAGES) & 1) ^ 1);
             const uint32_t kdst = smem_u32(stage_data + slot * C::STAGE_BYTES);
@@ -365,6 +397,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
       const int local = local0 + i;
       const int slot = local % NSTAGES;
       mbar_wait(full_bar(slot), (local / NSTAGES) & 1);
+      if (local == 0 && warp == 0 && lane == 0) K1T(2, pr);
       const StageMeta m = meta[slot];
       const __nv_bfloat16 *ks = reinterpret_cast<const __nv_bfloat16 *>(stage_data + slot * C::STAGE_BYTES);
       const __nv_bfloat16 *vs = ks + P * D;
@@ -479,6 +512,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
       if (lane == 0) mbar_arrive(empty_bar(slot));
     }
 
+    if (warp == 0 && lane == 0) K1T(3, pr);
     // ---- combine the warps' (m, l, O) of this segment
 #pragma unroll
     for (int o = LPK; o < 32; o <<= 1) {
@@ -620,6 +654,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
     first_seg = false;
   }
   }
+  if (warp == 0 && lane == 0) K1T(4, pr);
 }
 
 template <class C>

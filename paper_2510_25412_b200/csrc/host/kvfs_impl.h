@@ -182,7 +182,7 @@ struct Ctx {
   int64_t batch_counter = 0;
   int64_t opt_decode_ctas = 0;
   int64_t opt_decode_chunks = 0;  // KVFS_OPT_DECODE_CHUNKS (0: static scheduling)
-  int64_t opt_chunk_cutover = 8;
+  int64_t opt_chunk_cutover = 2;  // measured: cfg2d drafts (n_q 4) K1 1.29 ms / 4.0x HBM traffic, K2 0.44 ms / 1.0x
   int64_t opt_cascade_min_entries = 16;
   int opt_prefix_splits = 0;  // 0 = auto
   bool opt_timing = false;    // KVFS_OPT_TIMING

@@ -38,10 +38,14 @@ def _decode_rows(h, names, nq=None):
     return rows
 
 
-@pytest.mark.parametrize("P,Hq,Hkv", [(16, 32, 8), (32, 16, 8), (64, 16, 2), (16, 8, 8)])
-def test_cascade_fork_family_decode(P, Hq, Hkv):
+@pytest.mark.parametrize("P,Hq,Hkv,cutover", [(16, 32, 8, 8), (32, 16, 8, 8), (64, 16, 2, 8), (16, 8, 8, 8),
+                                               (16, 32, 8, 2), (64, 16, 2, 2)])
+def test_cascade_fork_family_decode(P, Hq, Hkv, cutover):
+    """cutover 8: the draft rows (n_q 3, 7) stay on the decode path and join the family's cascade; cutover 2
+    (the default): they go to the tcgen05 chunk kernel in the same batch, the n_q = 1 members cascade."""
     h = Harness(4000, P, Hq, Hkv, 128, seed=P * 7 + Hq)
     h.c.set_option(K.OPT_CASCADE_MIN_ENTRIES, 4)
+    h.c.set_option(K.OPT_CHUNK_CUTOVER, cutover)
     kids = [f"k{i}" for i in range(9)]
     # root of 1500 tokens with holes (evicted before the fork: the shared masks carry them), 9 branches
     _family(h, "root", 1500, kids, [0, 5, 40, 300, 1, 17, 160, 64, 2], evict_root=[(3, 9), (700, 760)])
@@ -52,7 +56,7 @@ def test_cascade_fork_family_decode(P, Hq, Hkv):
         names = kids + ["root", "solo"]
         nq = [1] * len(names)
         if step == 1:
-            nq[2], nq[5] = 3, 7              # short speculative drafts stay on the decode path
+            nq[2], nq[5] = 3, 7              # short speculative drafts
         st, *_ = h.pred(_decode_rows(h, names, nq), qstd=4.0 if step == 2 else 1.0)
         assert st == [0] * len(names)
         assert h.c.counter(K.CTR_LAST_PREFIX_GROUPS) == 1

@@ -195,7 +195,7 @@ def test_chunk_tcgen05_kernel(P, Hq, Hkv):
     eviction, truncation + re-append (autocompletion), a fresh file, several 128-row M-tiles."""
     D = 128
     h = Harness(3000, P, Hq, Hkv, D, seed=P + Hq + 7)
-    h.c.set_option(2, 8)  # KVFS_OPT_CHUNK_CUTOVER (the default)
+    h.c.set_option(2, 8)  # KVFS_OPT_CHUNK_CUTOVER 8: rows with n_q < 8 on K1 (the default is 2)
     lens = [300, 1000, 77, 513, 0, 2048]
     for i, n in enumerate(lens):
         h.open(f"f{i}")

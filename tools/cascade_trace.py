@@ -1,0 +1,71 @@
+"""Development tool: globaltimer timeline of one cascade step (cfg3): the shared-prefix K2 kernel's CTAs and the
+decode kernel's rings (start, first data, end of streaming, end of output), to see how the two kernels share
+the SMs.
+
+    python -c 'from paper_2510_25412_b200 import build as b; b.build(defines=("KVFS_K1_TRACE", "KVFS_K2_TRACE"),
+               lib="build_var/trace/libkvfs.so", out_dir="build_var/trace")'
+    KVFS_LIB_PATH=build_var/trace/libkvfs.so python tools/cascade_trace.py [extra bench-like options via env]
+"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2510_25412_b200 import kvfs  # noqa: E402
+from paper_2510_25412_b200.workloads import DecodeWorkload  # noqa: E402
+
+
+def main():
+    wl = DecodeWorkload(os.environ.get("CFG", "cfg3"), steps_total=8)
+    kv = wl.kv
+    for k, opt in (("SPLITS", kvfs.OPT_PREFIX_SPLITS), ("CHUNKS", kvfs.OPT_DECODE_CHUNKS),
+                   ("CTAS", kvfs.OPT_DECODE_CTAS)):
+        if os.environ.get(k):
+            kv.set_option(opt, int(os.environ[k]))
+    T = wl.n_files * wl.n_q
+    s = wl.shape
+    out = torch.empty((T, s.Hq, s.D), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((T, s.Hq), dtype=torch.float32, device="cuda")
+    for i in range(4):
+        q, k, v = wl.make_inputs(i)
+        wl.pre_step()
+        kv.pred_attn_batch(wl.descs, wl.positions(), q, k, v, out, lse)
+        wl.advance()
+    torch.cuda.synchronize()
+    t2 = np.zeros((2, 32, 512), dtype=np.uint64)
+    t1 = np.zeros((6, 2048), dtype=np.uint64)
+    L = kvfs.lib()
+    for name, buf in (("kvfs_debug_k2_trace", t2), ("kvfs_debug_k1_trace", t1)):
+        fn = getattr(L, name)
+        fn.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+        assert fn(buf.ctypes.data, buf.nbytes) == 0
+    ps, pe = t2[1, 30].astype(np.int64), t2[1, 31].astype(np.int64)
+    n_p = int((pe > 0).sum())
+    nr = int((t1[4] > 0).sum())
+    t0 = min(ps[:n_p].min() if n_p else 1 << 62, t1[0, :nr].astype(np.int64).min())
+    us = lambda x: (x.astype(np.int64) - t0) / 1e3  # noqa: E731
+    if n_p:
+        d = (pe[:n_p] - ps[:n_p]) / 1e3
+        print(f"prefix kernel: {n_p} CTAs, start {us(ps[:n_p]).min():.2f}..{us(ps[:n_p]).max():.2f} us, "
+              f"end {us(pe[:n_p]).min():.2f}..{us(pe[:n_p]).max():.2f} us, duration median {np.median(d):.2f} us")
+        smp = set(t2[1, 29, :n_p].tolist())
+    else:
+        smp = set()
+    st, tma, fd, se, en, sm = (t1[i, :nr] for i in range(6))
+    print(f"decode kernel: {nr} rings; start {us(st).min():.2f}..{us(st).max():.2f}; first TMA median "
+          f"{np.median(us(tma) - us(st)):.2f} us after start; first data median {np.median(us(fd) - us(st)):.2f}; "
+          f"streaming ends {us(se).min():.2f}..{us(se).max():.2f}; output ends {us(en).min():.2f}..{us(en).max():.2f} us")
+    on_p = np.array([int(x) in smp for x in sm])
+    if on_p.any():
+        print(f"  rings on SMs that ran a prefix CTA: {on_p.sum()}, start median {np.median(us(st[on_p])):.2f} us; "
+              f"others start median {np.median(us(st[~on_p])):.2f} us")
+    dur = us(en) - us(st)
+    print(f"  ring duration median {np.median(dur):.2f} p10 {np.percentile(dur, 10):.2f} p90 {np.percentile(dur, 90):.2f} us; "
+          f"merge part median {np.median(us(en) - us(se)):.2f} us")
+
+
+if __name__ == "__main__":
+    main()
