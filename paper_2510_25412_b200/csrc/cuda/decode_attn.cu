@@ -78,12 +78,33 @@ __device__ __forceinline__ int cta_of(int64_t x, int64_t total, int ncta) {
   return static_cast<int>(c);
 }
 
-// Largest d with descs[d].cost_begin <= x.
-__device__ __forceinline__ int find_desc(const Desc *descs, int n, int64_t x) {
-  int lo = 0, hi = n - 1;
+// Largest d with descs[d].cost_begin <= x (cost_begin is nondecreasing, descs[0].cost_begin = 0).
+// Warp-collective (all 32 lanes, uniform arguments): each round the lanes probe 32 evenly spaced
+// descriptors in one load, so a batch of n descriptors takes ceil(log33 n) dependent loads (2 for 1024)
+// instead of log2 n (a cold ring start used to spend ~3 us in the binary search).  hint >= 0: the caller
+// knows d >= hint (the previous segment's descriptor); a short forward scan from it first.
+__device__ __forceinline__ int find_desc(const Desc *descs, int n, int64_t x, int hint) {
+  const int lane = threadIdx.x & 31;
+  int lo = 0, hi = n - 1;  // the answer is in [lo, hi]
+  if (hint >= 0) {
+    // lanes probe hint + 1 .. hint + 32: the answer is hint + (number of probes <= x), if not past them
+    const int pos = hint + 1 + lane;
+    const bool le = pos < n && descs[pos].cost_begin <= x;
+    const unsigned m = __ballot_sync(0xffffffffu, le);
+    if (m != 0xffffffffu) return hint + __popc(m);
+    lo = hint + 32;
+  }
   while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (descs[mid].cost_begin <= x) lo = mid; else hi = mid - 1;
+    const int64_t span = hi - lo;                                   // candidates lo + 1 .. hi
+    const int pos = lo + 1 + static_cast<int>(span * lane / 32);   // nondecreasing in lane, <= hi
+    const bool le = descs[pos].cost_begin <= x;
+    const unsigned m = __ballot_sync(0xffffffffu, le);
+    if (m == 0) return lo;  // pos(lane 0) = lo + 1 is already past x
+    const int L = 31 - __clz(m);  // last lane whose probe is <= x (probes are monotone)
+    const int newlo = lo + 1 + static_cast<int>(span * L / 32);
+    const int newhi = (L < 31) ? lo + static_cast<int>(span * (L + 1) / 32) : hi;  // pos(L + 1) - 1
+    lo = newlo;
+    hi = newhi;
   }
   return lo;
 }
@@ -96,10 +117,10 @@ struct Segment {
   int64_t ubeg;  // global stage index of the unit's first stage
 };
 
-// Segment containing global stage x (x < total), clipped to [x, end).
-__device__ __forceinline__ Segment make_segment(const Desc *descs, int n_desc, int64_t x, int64_t end, int Hkv) {
+// Segment containing global stage x (x < total), clipped to [x, end).  Warp-collective (find_desc).
+__device__ __forceinline__ Segment make_segment(const Desc *descs, int n_desc, int64_t x, int64_t end, int hint) {
   Segment s;
-  s.d = find_desc(descs, n_desc, x);
+  s.d = find_desc(descs, n_desc, x, hint);
   const Desc &dd = descs[s.d];
   s.spu = dd.stages_per_unit;
   const int64_t rel = x - dd.cost_begin;
@@ -110,7 +131,6 @@ __device__ __forceinline__ Segment make_segment(const Desc *descs, int n_desc, i
   s.ubeg = dd.cost_begin + static_cast<int64_t>(u) * s.spu;
   const int64_t uend = s.ubeg + s.spu;
   s.nst = static_cast<int>((end < uend ? end : uend) - x);
-  (void)Hkv;
   return s;
 }
 
@@ -144,7 +164,7 @@ __device__ __forceinline__ void fold_prefix(const float2 (&pml)[kMaxPrefixSplits
 #ifdef KVFS_K1_TRACE
 // Development trace (tools/cascade_trace.py): per physical ring, %globaltimer (ns) at kernel start, the
 // producer's first TMA, the consumers' first full stage, the end of streaming and the end of the output.
-__device__ unsigned long long g_k1_trace[6][2048];
+__device__ unsigned long long g_k1_trace[8][2048];
 __device__ __forceinline__ unsigned long long k1_now() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -253,8 +273,10 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
     if (cta >= p.ncta) break;
     const int64_t beg = cta_start(cta, p.total, p.ncta), end = cta_start(cta + 1, p.total, p.ncta);
     int64_t x = beg;
+    int dhint = -1;
     while (x < end) {
-      const Segment sg = make_segment(p.descs, p.n_desc, x, end, p.Hkv);
+      const Segment sg = make_segment(p.descs, p.n_desc, x, end, dhint);
+      dhint = sg.d;
       const Desc dd = p.descs[sg.d];
       if (lane == 0) {  // Q rows of this unit -> Q ring
         const int qs = segi % C::NQ;
@@ -363,8 +385,10 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
   const int64_t beg = cta_start(cta, p.total, p.ncta), end = cta_start(cta + 1, p.total, p.ncta);
   int64_t x = beg;
   bool first_seg = true;
+  int dhint = -1;
   while (x < end) {
-    const Segment sg = make_segment(p.descs, p.n_desc, x, end, p.Hkv);
+    const Segment sg = make_segment(p.descs, p.n_desc, x, end, dhint);
+    dhint = sg.d;
     const Desc dd = p.descs[sg.d];
     // ---- Q (scaled into the log2 domain) from the Q ring
     float2 q2[G][DPL / 2];
@@ -550,19 +574,27 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
     // shared-prefix partials of this unit (written by the prefix kernel earlier on the stream; with a
     // programmatic dependent launch this kernel may be running alongside it: wait for its completion here,
     // after streaming this unit's own keys)
+    if (warp == 0 && lane == 0) K1T(6, pr);
     if (dd.pref_splits) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (warp == 0 && lane == 0) K1T(7, pr);
     const float *pref = dd.pref_splits
                             ? p.ppart + (static_cast<int64_t>(dd.pref_base) +
                                          static_cast<int64_t>(sg.g * dd.n_q + sg.qi) * dd.pref_splits) * C::PART
                             : nullptr;
     if (whole) {
+      // the next element's shared-prefix partials are loaded while this one is combined (one L2 round trip
+      // for the whole merge instead of one per element)
+      float2 pml[kMaxPrefixSplits], po[kMaxPrefixSplits], pml_n[kMaxPrefixSplits], po_n[kMaxPrefixSplits];
+      if (tid < G * D / 2)
+        load_prefix(pref, dd.pref_splits, C::PART, (tid / (D / 2)) * (D + 2), D, (tid % (D / 2)) * 2, pml, po);
       for (int e = tid; e < G * D / 2; e += NW * 32) {
         const int h = e / (D / 2), dim = (e % (D / 2)) * 2;
+        const int en = e + NW * 32;
+        if (en < G * D / 2)
+          load_prefix(pref, dd.pref_splits, C::PART, (en / (D / 2)) * (D + 2), D, (en % (D / 2)) * 2, pml_n, po_n);
         float M = -CUDART_INF_F;
 #pragma unroll
         for (int w = 0; w < NW; ++w) M = fmaxf(M, comb[w * C::PART + h * (D + 2) + D]);
-        float2 pml[kMaxPrefixSplits], po[kMaxPrefixSplits];
-        load_prefix(pref, dd.pref_splits, C::PART, h * (D + 2), D, dim, pml, po);
 #pragma unroll
         for (int s = 0; s < kMaxPrefixSplits; ++s) M = fmaxf(M, pml[s].x);
         float L = 0.f, ox = 0.f, oy = 0.f;
@@ -579,6 +611,11 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
         const int64_t oidx = (row * p.Hq + sg.g * G + h) * D + dim;
         *reinterpret_cast<__nv_bfloat162 *>(p.out + oidx) = __floats2bfloat162_rn(ox * inv, oy * inv);
         if (dim == 0 && p.lse) p.lse[row * p.Hq + sg.g * G + h] = (M + __log2f(L)) * 0.69314718055994531f;
+#pragma unroll
+        for (int sp = 0; sp < kMaxPrefixSplits; ++sp) {
+          pml[sp] = pml_n[sp];
+          po[sp] = po_n[sp];
+        }
       }
       named_bar_sync(1 + ring, NW * 32);
     } else {

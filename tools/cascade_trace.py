@@ -36,7 +36,7 @@ def main():
         wl.advance()
     torch.cuda.synchronize()
     t2 = np.zeros((2, 32, 512), dtype=np.uint64)
-    t1 = np.zeros((6, 2048), dtype=np.uint64)
+    t1 = np.zeros((8, 2048), dtype=np.uint64)
     L = kvfs.lib()
     for name, buf in (("kvfs_debug_k2_trace", t2), ("kvfs_debug_k1_trace", t1)):
         fn = getattr(L, name)
@@ -63,6 +63,9 @@ def main():
         print(f"  rings on SMs that ran a prefix CTA: {on_p.sum()}, start median {np.median(us(st[on_p])):.2f} us; "
               f"others start median {np.median(us(st[~on_p])):.2f} us")
     dur = us(en) - us(st)
+    cb, gw = t1[6, :nr], t1[7, :nr]
+    print(f"  after streaming: combine {np.median(us(cb) - us(se)):.2f} us, griddepcontrol.wait "
+          f"{np.median(us(gw) - us(cb)):.2f} us, merge + output {np.median(us(en) - us(gw)):.2f} us (medians)")
     print(f"  ring duration median {np.median(dur):.2f} p10 {np.percentile(dur, 10):.2f} p90 {np.percentile(dur, 90):.2f} us; "
           f"merge part median {np.median(us(en) - us(se)):.2f} us")
 
