@@ -256,6 +256,13 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
     // grid completed; the prologue's writes are complete and visible by then)
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
+#ifdef KVFS_K2_TRACE
+    if (threadIdx.x == 0 && blockIdx.x < 512) {
+      unsigned long long gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      g_k2_trace[1][26][blockIdx.x] = gt;  // prologue dependency satisfied
+    }
+#endif
   }
   constexpr uint32_t tmem = 0;
 
@@ -550,6 +557,13 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       // epilogue: O / l -> bf16 out, lse   (prefix mode: the partial O, m, l of the split)
       mbar_wait(bar(B_OF + m), 0);
       if (m == 0 && wq == 0 && lane == 0) K2T(26, 0);
+#ifdef KVFS_K2_TRACE
+      if (m == 0 && wq == 0 && lane == 0 && blockIdx.x < 512) {
+        unsigned long long gt;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+        g_k2_trace[1][27][blockIdx.x] = gt;  // O complete (main loop done)
+      }
+#endif
       tc_fence_after();
       if constexpr (PREFIX) {
         // Coalesced partial stores: each 32-column chunk of the warp's 32 rows is transposed through a

@@ -21,6 +21,24 @@ def rows_np(seed: int, tag: int, layer: int, owner: int, s0: int, s1: int, width
     return normal_bf16_np(key, s0 * width, (s1 - s0) * width, std).reshape(s1 - s0, width)
 
 
+def outlier_channels(bits: np.ndarray, D: int, channels, e: int) -> np.ndarray:
+    """Outlier-channel inputs (real K caches carry a few channels of much larger magnitude, and Q follows
+    them): multiply channels `channels` of every D-wide head of bf16 bit patterns [..][H*D] by 2^e, EXACTLY,
+    by adding e to the exponent field of the nonzero values (the generator's values are normal and bounded,
+    so nothing overflows or goes subnormal for |e| <= 30).  A power of two is used so both sides see the
+    same bits without any rounding; no method arithmetic here."""
+    b = np.array(bits, dtype=np.uint16, copy=True)
+    w = b.shape[-1]
+    cols = np.array([h * D + c for h in range(w // D) for c in channels], dtype=np.int64)
+    sub = b[..., cols].astype(np.int32)
+    nz = (sub & 0x7FFF) != 0
+    ex = (sub >> 7) & 0xFF
+    assert ((ex[nz] + e) > 0).all() and ((ex[nz] + e) < 255).all(), "outlier scaling leaves the normal range"
+    sub = np.where(nz, (sub & ~(0xFF << 7)) | ((ex + e) << 7), sub)
+    b[..., cols] = sub.astype(np.uint16)
+    return b
+
+
 def rows_torch(seed: int, tag: int, layer: int, owner: int, s0: int, s1: int, width: int,
                std: float = 1.0, device="cpu", out=None):
     """Same bits as rows_np as a torch.bfloat16 tensor [s1 - s0][width] (or written into `out`)."""

@@ -10,7 +10,7 @@ import torch
 from oracle import Oracle
 from oracle.bf16 import bf16_to_f64
 from paper_2510_25412_b200 import kvfs as K
-from synth.workloads import TAG_K, TAG_Q, TAG_V, rows_np
+from synth.workloads import TAG_K, TAG_Q, TAG_V, outlier_channels, rows_np
 
 MAX_ABS = 2e-2   # north-star tolerance (BASELINE.json): max-abs error of bf16 attention outputs
 MEAN_ABS = 2e-3  # and mean-abs error, fp32 accumulation vs the fp64 oracle
@@ -34,7 +34,11 @@ def assert_close(gpu_bf16: np.ndarray, ref: np.ndarray, what=""):
 
 
 class Harness:
-    def __init__(self, n_pages, P=16, Hq=8, Hkv=2, D=64, L=1, seed=0, max_rows=4096, max_descs=1024):
+    def __init__(self, n_pages, P=16, Hq=8, Hkv=2, D=64, L=1, seed=0, max_rows=4096, max_descs=1024,
+                 outliers=None):
+        """outliers = (channels, k_e, q_e, v_e): channels of every head scaled by 2^k_e in K, 2^q_e in Q and
+        2^v_e in V (synth.workloads.outlier_channels; exact, the same bits on both sides)."""
+        self.outliers = outliers
         self.c = K.KVFS(L, Hq, Hkv, D, P, n_pages, max_batch_rows=max_rows, max_batch_descs=max_descs, device=0)
         self.o = Oracle(n_pages, P, L, Hkv, D)
         self.L, self.Hq, self.Hkv, self.D, self.P = L, Hq, Hkv, D, P
@@ -48,12 +52,17 @@ class Harness:
         self.serial += n
         k = np.stack([rows_np(self.seed, TAG_K, l, 0, s0, s0 + n, self.Hkv * self.D) for l in range(self.L)])
         v = np.stack([rows_np(self.seed, TAG_V, l, 0, s0, s0 + n, self.Hkv * self.D) for l in range(self.L)])
+        if self.outliers:
+            ch, ke, _, ve = self.outliers
+            k, v = outlier_channels(k, self.D, ch, ke), outlier_channels(v, self.D, ch, ve)
         return k.reshape(self.L, n, self.Hkv, self.D), v.reshape(self.L, n, self.Hkv, self.D)
 
     def _q(self, n, std=1.0):
         s0 = self.qserial
         self.qserial += n
         q = np.stack([rows_np(self.seed, TAG_Q, l, 0, s0, s0 + n, self.Hq * self.D, std) for l in range(self.L)])
+        if self.outliers:
+            q = outlier_channels(q, self.D, self.outliers[0], self.outliers[2])
         return q.reshape(self.L, n, self.Hq, self.D)
 
     def open(self, name):

@@ -52,6 +52,10 @@ def main():
         print(f"prefix kernel: {n_p} CTAs, start {us(ps[:n_p]).min():.2f}..{us(ps[:n_p]).max():.2f} us, "
               f"end {us(pe[:n_p]).min():.2f}..{us(pe[:n_p]).max():.2f} us, duration median {np.median(d):.2f} us")
         smp = set(t2[1, 29, :n_p].tolist())
+        gw, of = t2[1, 26, :n_p].astype(np.int64), t2[1, 27, :n_p].astype(np.int64)
+        if (gw > 0).all() and (of > 0).all():
+            print(f"  prefix CTA phases (medians): griddepcontrol.wait {np.median(gw - ps[:n_p]) / 1e3:.2f} us, "
+                  f"Q + tiles {np.median(of - gw) / 1e3:.2f} us, epilogue {np.median(pe[:n_p] - of) / 1e3:.2f} us")
     else:
         smp = set()
     st, tma, fd, se, en, sm = (t1[i, :nr] for i in range(6))
