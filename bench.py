@@ -424,8 +424,13 @@ def run_ours(args):
     sampler.start()
     torch.cuda.synchronize()
     barrier()
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(Kst)]
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(Kst)]
+    # The attention layer's device time (first to last kernel of pred_attn_layer: chunk / shared-prefix /
+    # decode) comes from CUDA events the library records on the launching stream around its own launches
+    # (KVFS_OPT_TIMING), so no Python work sits between an event and the kernel it brackets.  Without
+    # --scores a step is one pred_attn_batch call (begin + layer + end inside the library).
+    kv.set_option(K.OPT_TIMING, 1)
+    kv.counter(K.CTR_LAYER_DEVICE_NS)  # start a new sum (the warm-up steps were not timed)
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(Kst)] if args.scores else None
     ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(Kst)] if args.scores else None
     scores_buf = None
     if args.scores:
@@ -440,15 +445,16 @@ def run_ours(args):
         q, k, v = inputs[W + i]
         wl.pre_step()
         lens_seen.append(wl.lens.copy())
-        step, st = kv.pred_step_begin(wl.descs, wl.positions())
-        ev0[i].record()
-        kv.pred_attn_layer(step, 0, q, k, v, out, lse)
-        ev1[i].record()
         if args.scores:
+            step, st = kv.pred_step_begin(wl.descs, wl.positions())
+            kv.pred_attn_layer(step, 0, q, k, v, out, lse)
+            ev1[i].record()
             la = wl.lens + wl.n_q
             kv.pred_attn_scores(step, 0, q, lse, scores_buf, np.concatenate([[0], np.cumsum(la)[:-1]]))
             ev2[i].record()
-        kv.pred_step_end(step)
+            kv.pred_step_end(step)
+        else:
+            kv.pred_attn_batch(wl.descs, wl.positions(), q, k, v, out, lse)
         wl.advance()
     t_end.record()
     host_s = time.perf_counter() - host_t0
@@ -460,7 +466,10 @@ def run_ours(args):
     barrier()
     sampler.stop()
     ms_total = t_start.elapsed_time(t_end)
-    kernel_ms = [a.elapsed_time(b) for a, b in zip(ev0, ev1)]
+    layer_ns = kv.counter(K.CTR_LAYER_DEVICE_NS)
+    assert kv.counter(K.CTR_LAYER_TIMED) == Kst
+    kv.set_option(K.OPT_TIMING, 0)
+    kernel_ms = [layer_ns / 1e6 / Kst] * Kst
     launches = kv.counter(K.CTR_KERNEL_LAUNCHES) - launches0
     h2d = kv.counter(K.CTR_H2D_BYTES) - h2d0
     ms_max = all_max(ms_total, world)
@@ -596,6 +605,9 @@ def run_ours(args):
                           "unique K/V %.0f MB per step; the CoW-shared prefix is L2-resident by design" % (alg_bytes[0] / 1e6))},
         "roofline": dict(roof, traffic=traffic, traffic_source=traffic_src, kernel=wl.dominant_kernel(args.cutover if args.cutover >= 0 else 8),
                          kernel_ms_mean=k_ms, peak_source=peak_src,
+                         kernel_timing="CUDA events the library records on the launching stream before the first "
+                                       "and after the last kernel of each timed pred_attn_layer (KVFS_OPT_TIMING, "
+                                       "KVFS_CTR_LAYER_DEVICE_NS), mean over the timed steps",
                          algorithmic_bytes_per_launch=statistics.mean(alg_bytes),
                          algorithmic_flops_per_launch=flops_mean),
         "gpu_launches": launches,

@@ -337,7 +337,7 @@ typedef enum {
                                    that run attended ONCE per batch by the tcgen05 kernel over all sharers'
                                    query rows, and the per-file rest by the decode kernel, merged exactly
                                    (log-sum-exp).  0 = off; default 16 (head_dim 128 only) */,
-  KVFS_OPT_PREFIX_SPLITS = 5,   /* key splits of each shared run in the cascade (1..8); 0 = auto */
+  KVFS_OPT_PREFIX_SPLITS = 5,   /* key splits of each shared run in the cascade (1..16); 0 = auto */
   KVFS_OPT_DECODE_CHUNKS = 8,   /* decode-kernel scheduling: 0 = static (ring r streams the r-th of
                                    KVFS_OPT_DECODE_CTAS equal contiguous stage ranges; default); n in 1..2048 =
                                    dynamic: the batch's stages are cut into n equal ranges that at most one
@@ -346,7 +346,9 @@ typedef enum {
   KVFS_OPT_TIMING = 7,          /* 1: kvfs_compact_files records CUDA events around its device work (file
                                    groups: upload + gathers) and, before returning, waits for them and
                                    stores their summed device time in KVFS_CTR_COMPACT_DEVICE_NS (the host
-                                   R1 / table work that overlaps it excluded); 0 = off (default) */
+                                   R1 / table work that overlaps it excluded); pred_attn_layer records
+                                   events around its kernels (chunk, shared-prefix, decode), summed by
+                                   KVFS_CTR_LAYER_DEVICE_NS; 0 = off (default) */
   KVFS_OPT_FAULT_INJECT = 6     /* tests only: value n > 0 makes the n-th following pass through an
                                    injection point (mid-way through a pred reservation, after the first
                                    descriptor is committed; fork; open) throw std::bad_alloc inside the
@@ -363,7 +365,20 @@ typedef enum {
   KVFS_CTR_LAST_PREFIX_UNITS = 6,  /* CTAs of the last shared-prefix (cascade) launch (0: none) */
   KVFS_CTR_LAST_PREFIX_GROUPS = 7, /* fork families (groups) the last pred batch attended as shared prefixes */
   KVFS_CTR_HOST_PAGES = 8,         /* pages currently in the host tier (kvfs_offload) */
-  KVFS_CTR_COMPACT_DEVICE_NS = 9   /* KVFS_OPT_TIMING: device time of the last kvfs_compact_files (ns) */
+  KVFS_CTR_COMPACT_DEVICE_NS = 9,  /* KVFS_OPT_TIMING: device time of the last kvfs_compact_files (ns) */
+  KVFS_CTR_LAYER_DEVICE_NS = 10,   /* KVFS_OPT_TIMING: summed device time (ns) of the pred_attn_layer calls
+                                      recorded since the previous read of this counter, from the event
+                                      before a layer's first kernel to the event after its last (reading
+                                      waits for them and starts a new sum) */
+  KVFS_CTR_LAYER_TIMED = 11,       /* KVFS_OPT_TIMING: number of pred_attn_layer calls in the last
+                                      KVFS_CTR_LAYER_DEVICE_NS sum */
+  /* Host time (ns, summed since kvfs_init) of the phases of pred_step_begin / pred_attn_layer: the
+     reservation and plan of the batch (R11), the chunk split + shared-prefix planning, the metadata upload
+     + prologue launch, and pred_attn_layer's kernel launches.  Host-cost observability. */
+  KVFS_CTR_HOST_RESERVE_NS = 12,
+  KVFS_CTR_HOST_SPLIT_NS = 13,
+  KVFS_CTR_HOST_UPLOAD_NS = 14,
+  KVFS_CTR_HOST_LAUNCH_NS = 15
 } kvfs_counter;
 int kvfs_get_counter(kvfs_ctx *ctx, int counter, int64_t *value);
 

@@ -156,7 +156,7 @@ constexpr int OFF_K2 = OFF_Q2 + 2 * tc::TILE_BYTES;         // KV2 K tiles
 constexpr int OFF_V2 = OFF_K2 + KV2 * tc::TILE_BYTES;       // KV2 V tiles
 constexpr int OFF_JCOL2 = OFF_V2 + KV2 * tc::TILE_BYTES;    // JR x BN int32
 constexpr int OFF_BAR2 = OFF_JCOL2 + JR * tc::BN * 4 + 64;  // + JR tile flags
-constexpr int N_BARS2 = 1 + 4 * KV2 + 8 + JR;
+constexpr int N_BARS2 = 1 + 4 * KV2 + 8 + JR + 1;
 constexpr int OFF_TMEM2 = OFF_BAR2 + N_BARS2 * 8;
 constexpr int SMEM2 = OFF_TMEM2 + 16 + 1024;
 }  // namespace tc2
@@ -167,9 +167,21 @@ __device__ unsigned long long g_k2_trace[2][32][512];
   do {                                                                              \
     if (trace_cta >= 0 && (t) < 512) g_k2_trace[trace_cta][ev][t] = clock64();      \
   } while (0)
+// per-CTA globaltimer stamps (prefix-mode phases; tools/cascade_trace.py), slots 20..23 of trace row 1
+#define K2G(slot)                                                                   \
+  do {                                                                              \
+    if (blockIdx.x < 512) {                                                         \
+      unsigned long long gt_;                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));                       \
+      g_k2_trace[1][slot][blockIdx.x] = gt_;                                        \
+    }                                                                               \
+  } while (0)
 #else
 #define K2T(ev, t) \
   do {             \
+  } while (0)
+#define K2G(slot) \
+  do {            \
   } while (0)
 #endif
 
@@ -192,7 +204,8 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   auto bar = [&](int i) { return smem_u32(bars + i); };
   // barrier indices
   constexpr int B_Q = 0, B_KF = 1, B_KE = 1 + KV2, B_VF = 1 + 2 * KV2, B_VE = 1 + 3 * KV2, B_SF = 1 + 4 * KV2,
-                B_PF = B_SF + 2, B_OF = B_PF + 4, B_JF = B_OF + 2;  // B_PF + 2m + half
+                B_PF = B_SF + 2, B_OF = B_PF + 4, B_JF = B_OF + 2,  // B_PF + 2m + half
+                B_X = B_JF + JR;  // prefix mode: the split-exchange loads
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + OFF_TMEM2);
   int32_t *jcol_all = reinterpret_cast<int32_t *>(smem + OFF_JCOL2);
   int32_t *jflag = jcol_all + JR * BN;
@@ -203,9 +216,11 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
 #endif
   const ChunkUnit u = p.units[blockIdx.x];
   ChunkDesc cd;
+  int q_t0 = -1;  // prefix mode: first packed Q row when the family's rows are consecutive (Q by TMA)
   if constexpr (PREFIX) {
     const PrefixDesc pd = p.pdescs[u.desc];
     cd = ChunkDesc{pd.slab_off, pd.n_entries, 0, pd.n_rows, pd.row0, pd.n_entries, 0, 0};
+    q_t0 = pd.q_t0;
   } else {
     cd = p.descs[u.desc];
   }
@@ -222,7 +237,8 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   if (threadIdx.x == 0 && blockIdx.x < 512) g_k2_trace[1][30][blockIdx.x] = gt0;
 #endif
   if (threadIdx.x == 0) {
-    mbar_init(bar(B_Q), PREFIX ? 4 * n_mt : 1);  // prefix: one arrival per softmax warp that gathers Q
+    // prefix mode with gathered rows: one arrival per softmax warp that gathers Q; else one TMA transaction
+    mbar_init(bar(B_Q), (PREFIX && q_t0 < 0) ? 4 * n_mt : 1);
     for (int s = 0; s < KV2; ++s) {
       mbar_init(bar(B_KF + s), 1);
       mbar_init(bar(B_KE + s), 1);
@@ -236,6 +252,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       mbar_init(bar(B_OF + m), 1);
     }
     for (int j = 0; j < JR; ++j) mbar_init(bar(B_JF + j), 1);
+    mbar_init(bar(B_X), 1);
     fence_mbar_init();
   }
   if (warp == 2) {
@@ -304,10 +321,10 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
     if (warp == 0) {
       // ============================================================ K producer (+ Q, + column metadata)
       const uint64_t pol = policy_evict_first();
-      if (!PREFIX && lane == 0) {
+      if ((!PREFIX || q_t0 >= 0) && lane == 0) {
         mbar_arrive_expect_tx(bar(B_Q), n_mt * TILE_BYTES);
         for (int m = 0; m < n_mt; ++m) {
-          const int qrow = cd.row0 + ((m0 + m) * BM) / G;
+          const int qrow = (PREFIX ? q_t0 : cd.row0) + ((m0 + m) * BM) / G;
           tma_load_4d(sbase + OFF_Q2 + m * TILE_BYTES, &qmap, 0, 0, u.g, qrow, bar(B_Q));
           tma_load_4d(sbase + OFF_Q2 + m * TILE_BYTES + HALF_BYTES, &qmap, 64, 0, u.g, qrow, bar(B_Q));
         }
@@ -405,6 +422,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       mbar_wait(bar(B_Q), 0);
       if (lane == 0) K2T(25, 0);
       mbar_wait(bar(B_KF + 0), 0);
+      if (lane == 0) K2G(22);  // first K tile landed
       for (int m = 0; m < n_mt; ++m) issue_s(0, m);
       if (elect_one()) mma_commit(bar(B_KE + 0));
       __syncwarp();
@@ -445,16 +463,19 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       const uint32_t lane_addr = static_cast<uint32_t>(wq * 32) << 16;
       const uint32_t s_col = tmem + lane_addr + m * BN;
       const uint32_t o_col = tmem + lane_addr + O_COL2 + m * HD;
-      if constexpr (PREFIX) {
+      if (PREFIX && q_t0 < 0) {
         // thread r gathers its row (family token qi, head h) of Q into the K-major SW128 tile: 16-byte
         // chunk cc of row r of a 64-column half lands at chunk cc ^ (r % 8) of the row's 128-byte line
         uint8_t *qt = smem + OFF_Q2 + m * TILE_BYTES;
         uint4 v[16];
+        if (m == 0 && wq == 0 && lane == 0) K2G(18);  // softmax warps start the gather
         if (live) {
           const PrefixRow pr = p.prows[cd.row0 + qi];
+          if (m == 0 && wq == 0 && lane == 0) K2G(23);  // row record loaded
           const uint4 *src = reinterpret_cast<const uint4 *>(p.q + (static_cast<int64_t>(pr.t) * p.Hq + u.g * G + h) * HD);
 #pragma unroll
           for (int c = 0; c < 16; ++c) v[c] = __ldg(src + c);
+          if (m == 0 && wq == 0 && lane == 0 && v[15].w != 0x7fffffffu) K2G(19);  // Q loads returned
         } else {
 #pragma unroll
           for (int c = 0; c < 16; ++c) v[c] = make_uint4(0, 0, 0, 0);
@@ -465,6 +486,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(bar(B_Q));
+        if (m == 0 && wq == 0 && lane == 0) K2G(20);  // Q rows gathered
       }
       float m_run = -CUDART_INF_F, l_run = 0.f;
       for (int t = 0; t < n_tiles; ++t) {
@@ -475,6 +497,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         const bool vis_all = jflag[t % JR] != 0;
         K2_WAIT(bar(B_SF + m), t & 1);
         if (wq == 0 && lane == 0) K2T(14 + 6 * m, t);
+        if (PREFIX && t == 0 && m == 0 && wq == 0 && lane == 0) K2G(21);  // first S ready
         tc_fence_after();
         float x[BN];
 #pragma unroll
@@ -566,18 +589,15 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
 #endif
       tc_fence_after();
       if constexpr (PREFIX) {
-        // Coalesced partial stores: each 32-column chunk of the warp's 32 rows is transposed through a
-        // per-warp 32 x 33 float buffer in this M-tile's (consumed) Q tile, then 16 lanes write one row's
-        // 128 contiguous bytes: 2 rows per store instead of 32 scattered 8-byte pieces.
-        float *buf = reinterpret_cast<float *>(smem + OFF_Q2 + m * TILE_BYTES) + wq * (32 * 33);
-        float *dst = nullptr;
-        if (live) {
-          const PrefixRow pr = p.prows[cd.row0 + qi];
-          const PrefixDesc pd = p.pdescs[u.desc];
-          const int64_t idx = pr.pref_base + static_cast<int64_t>(u.g * pr.n_q + pr.qi) * pd.n_splits + pd.split;
-          dst = p.ppart + idx * (G * (HD + 2)) + h * (HD + 2);
-        }
-        // the TMEM load of chunk c + 1 is in flight while chunk c is stored
+        // The partial (o, m, l) rows go out by 1-D TMA bulk stores from a shared-memory image of their global
+        // layout: row R of the pair (qi = R / G, h = R % G) -> staging byte R * 4 (HD + 2), so the G rows of
+        // one query token qi are one contiguous G (HD + 2)-float record, stored with one bulk copy.  The
+        // staging overlays Q, K and V (256 rows x 520 B = 130 KiB): wait for both M-tiles' MMAs first.
+        if (n_mt == 2) mbar_wait(bar(B_OF + (m ^ 1)), 0);
+        tc_fence_after();
+        constexpr int PARTF = part_floats(G, HD);
+        const int Rl = m * BM + r;  // row within the pair: token Rl / G, head Rl % G
+        float *row = reinterpret_cast<float *>(smem + OFF_Q2) + (Rl / G) * PARTF + (Rl % G) * (HD + 2);
         float va[32], vb[32];
         tmem_ld32(o_col, va);
 #pragma unroll
@@ -585,24 +605,32 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           float(&v)[32] = (c & 1) ? vb : va;
           float(&vn)[32] = (c & 1) ? va : vb;
           tmem_wait_ld();
-          if (m == 0 && wq == 0 && lane == 0) K2T(30, c);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) buf[lane * 33 + i] = v[i];
           if (c + 1 < HD / 32) tmem_ld32(o_col + (c + 1) * 32, vn);
-          __syncwarp();
-          if (m == 0 && wq == 0 && lane == 0) K2T(31, c);
 #pragma unroll
-          for (int it = 0; it < 16; ++it) {  // (D + 2)-float rows are 8-byte aligned: float2, 2 rows per store
-            const int rr = it * 2 + (lane >> 4), j = (lane & 15) * 2;
-            float *d = reinterpret_cast<float *>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dst), rr));
-            // st.global: a generic store could alias buf and serialised the loop (~70 clk per iteration)
-            if (d) __stcg(reinterpret_cast<float2 *>(d + c * 32 + j), make_float2(buf[rr * 33 + j], buf[rr * 33 + j + 1]));
-          }
-          __syncwarp();
-          if (m == 0 && wq == 0 && lane == 0) K2T(28, c);
+          for (int i = 0; i < 32; i += 2) *reinterpret_cast<float2 *>(row + c * 32 + i) = make_float2(v[i], v[i + 1]);
         }
-        if (live) *reinterpret_cast<float2 *>(dst + HD) = make_float2(m_run, l_run);
-        if (m == 0 && wq == 0 && lane == 0) K2T(28, 4);
+        *reinterpret_cast<float2 *>(row + HD) = make_float2(m_run, l_run);
+        fence_proxy_async();
+        __syncwarp();
+        // lane j < 32 / G stores the record of the warp's j-th query token
+        if (lane < 32 / G) {
+          const int R = (m0 + m) * BM + wq * 32 + lane * G;  // first row of the token
+          const int tq = R / G;
+          if (tq < cd.n_q) {
+            const PrefixRow pr = p.prows[cd.row0 + tq];
+            const PrefixDesc pd = p.pdescs[u.desc];
+            const int64_t rr = pr.pref_base + static_cast<int64_t>(u.g * pr.n_q + pr.qi);
+            const int64_t idx = pd.n_splits > 1 ? pd.split_off + rr * pd.n_splits + pd.split : rr;
+            const uint32_t src = sbase + OFF_Q2 + static_cast<uint32_t>(((m * BM + wq * 32) / G + lane) * PARTF * 4);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(p.ppart + idx * PARTF),
+                         "r"(src), "r"(static_cast<uint32_t>(PARTF * 4))
+                         : "memory");
+          }
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // performed: visible after the fences below
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        __syncwarp();
       } else {
       const float inv = 1.f / l_run;
       const int64_t orow = (static_cast<int64_t>(cd.row0 + qi) * p.Hq + u.g * G + h) * HD;
@@ -646,6 +674,88 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+  if constexpr (PREFIX) {
+    // Split merge: the S CTAs of a (family, kv head, M-tile pair) group wait for each other (the host makes
+    // such a grid at most one CTA per SM, so all are resident; the decode kernel cannot start before every
+    // CTA of this grid has started), then CTA `split` folds the S split partials of its slice of the pair's
+    // rows into the merged record: (o, m, l) with one (M, L) per row, all loads of up to 8 splits in flight.
+    const PrefixDesc pd = p.pdescs[u.desc];
+    const int S = pd.n_splits;
+    // Arrival counters alternate between two arrays by launch parity: this launch counts in array `parity`
+    // and clears the other one, which the previous launch used (it completed before this one started) and
+    // the next launch will use.
+    {
+      int *clear = p.pgroup + (p.pgroup_parity ^ 1) * kMaxPrefixGroups;
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kMaxPrefixGroups; i += gridDim.x * blockDim.x) clear[i] = 0;
+    }
+    if (S > 1) {
+      int *arrived = p.pgroup + p.pgroup_parity * kMaxPrefixGroups + u.group;
+      __threadfence();  // this CTA's partial records (bulk stores waited for), before the group sees the arrival
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        atomicAdd(arrived, 1);
+        while (ld_acquire_gpu(arrived) < S) {
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // the bulk loads below read what others stored
+        K2G(16);  // the group's partials are all written
+      }
+      __syncthreads();
+      // Owned slice: rows [r0, r1) of the pair = query tokens [t0, t1).  The S split records of token t are
+      // contiguous in global memory (split_off + r * S + s): one bulk copy of S G (HD + 2) floats per token
+      // into shared memory (over the staging area, whose stores were waited for), all in flight at once.
+      constexpr int PARTF = part_floats(G, HD);
+      const int rp = n_mt * BM;
+      const int tpo = ((rp / G) + S - 1) / S;  // tokens per owner
+      const int t0 = m0 * BM / G + pd.split * tpo, t1 = min(m0 * BM / G + rp / G, t0 + tpo);
+      const int nt = max(0, min(t1, cd.n_q) - t0);
+      float *stage = reinterpret_cast<float *>(smem + OFF_Q2);
+      if (threadIdx.x < 32) {
+        const uint32_t xb = bar(B_X);
+        if (threadIdx.x == 0) mbar_arrive_expect_tx(xb, static_cast<uint32_t>(nt * S * PARTF * 4));
+        __syncwarp();
+        for (int j = threadIdx.x; j < nt; j += 32) {
+          const PrefixRow pr = p.prows[cd.row0 + t0 + j];
+          const int64_t rr = pr.pref_base + static_cast<int64_t>(u.g * pr.n_q + pr.qi);
+          bulk_g2s(sbase + OFF_Q2 + static_cast<uint32_t>(j * S * PARTF * 4), p.ppart + (pd.split_off + rr * S) * PARTF,
+                   static_cast<uint32_t>(S * PARTF * 4), xb, policy_evict_first());
+        }
+      }
+      if (nt > 0) mbar_wait(bar(B_X), 0);
+      // fold: item = (token j, head h, 8 dims), the softmax warps (the others run at 56 registers)
+      for (int it = static_cast<int>(threadIdx.x) - 128; it >= 0 && it < nt * G * (HD / 8); it += 256) {
+        const int j = it / (G * (HD / 8)), h = (it / (HD / 8)) % G, d0 = (it % (HD / 8)) * 8;
+        const float *rec = stage + static_cast<int64_t>(j) * S * PARTF + h * (HD + 2);
+        float M = -CUDART_INF_F;
+        for (int sp = 0; sp < S; ++sp) M = fmaxf(M, rec[sp * PARTF + HD]);
+        float L = 0.f, acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        for (int sp = 0; sp < S; ++sp) {
+          const float *x = rec + sp * PARTF;
+          const float f = (x[HD] == -CUDART_INF_F) ? 0.f : fast_exp2(x[HD] - M);
+          L += x[HD + 1] * f;
+#pragma unroll
+          for (int i = 0; i < 8; i += 2) {
+            const float2 v = *reinterpret_cast<const float2 *>(x + d0 + i);
+            acc[i] += v.x * f;
+            acc[i + 1] += v.y * f;
+          }
+        }
+        const PrefixRow pr = p.prows[cd.row0 + t0 + j];
+        const int64_t rr = pr.pref_base + static_cast<int64_t>(u.g * pr.n_q + pr.qi);
+        float *dst = p.ppart + rr * PARTF + h * (HD + 2);
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) __stcg(reinterpret_cast<float2 *>(dst + d0 + i), make_float2(acc[i], acc[i + 1]));
+        if (d0 == 0) __stcg(reinterpret_cast<float2 *>(dst + HD), make_float2(M, L));
+      }
+#ifdef KVFS_K2_TRACE
+      __syncthreads();
+      if (threadIdx.x == 0) K2G(17);  // merged
+#endif
+    }
+#ifdef KVFS_K2_TRACE
+    __syncthreads();
+    if (threadIdx.x == 0) K2G(25);  // CTA done
+#endif
   }
 }
 

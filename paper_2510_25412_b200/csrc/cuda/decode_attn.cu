@@ -51,7 +51,7 @@ struct DecodeCfg {
   static constexpr int THREADS = 12 * 32;        // producer warpgroup (4 warps) + 2 consumer warpgroups
   static constexpr int PRODUCER_REGS = 56, CONSUMER_REGS = 224;
   static constexpr int NQ = 4;                   // Q ring slots
-  static constexpr int PART = G * (D + 2);       // floats per partial (o, m, l per head)
+  static constexpr int PART = part_floats(G, D);  // floats per partial (o, m, l per head, 16-byte padded)
   static constexpr int RING_BYTES_RAW = NSTAGES * STAGE_BYTES + NQ * G * D * 2 + NW * PART * 4 + NSTAGES * 16 +
                                         (2 * NSTAGES + 2 * NQ + 4) * 8 + 16 + 16;
   static constexpr int RING_BYTES = (RING_BYTES_RAW + 127) / 128 * 128;
@@ -68,13 +68,14 @@ struct StageMeta {
 
 
 
-__device__ __forceinline__ int64_t cta_start(int64_t c, int64_t total, int ncta) { return c * total / ncta; }
+__device__ __forceinline__ int64_t cta_start(int64_t c, const DecodeParams &p) { return c * p.total / p.ncta; }
 
-__device__ __forceinline__ int cta_of(int64_t x, int64_t total, int ncta) {
-  int64_t c = x * ncta / total;
-  if (c >= ncta) c = ncta - 1;
-  while (c + 1 < ncta && cta_start(c + 1, total, ncta) <= x) ++c;
-  while (c > 0 && cta_start(c, total, ncta) > x) --c;
+// chunk holding stage x
+__device__ __forceinline__ int cta_of(int64_t x, const DecodeParams &p) {
+  int64_t c = x * p.ncta / p.total;
+  if (c >= p.ncta) c = p.ncta - 1;
+  while (c + 1 < p.ncta && cta_start(c + 1, p) <= x) ++c;
+  while (c > 0 && cta_start(c, p) > x) --c;
   return static_cast<int>(c);
 }
 
@@ -134,31 +135,116 @@ __device__ __forceinline__ Segment make_segment(const Desc *descs, int n_desc, i
   return s;
 }
 
-// Shared-prefix partials of one (unit, head): (m, l) and the dims (dim, dim + 1) of every key split, all
-// loads in flight at once (S <= kMaxPrefixSplits); absent splits read as m = -inf (weight 0).
-__device__ __forceinline__ void load_prefix(const float *pref, int S, int part, int hoff, int D, int dim,
-                                            float2 (&pml)[kMaxPrefixSplits], float2 (&po)[kMaxPrefixSplits]) {
+// Final merge of a unit's output (whole unit, or the last piece of a unit cut by ring boundaries).  Each of
+// the ring's NT = NW * 32 consumer threads owns one head h and DPT consecutive dims d0 .. d0 + DPT of it and
+// folds (o, m, l) partial records into a running (M, L, acc) in the log2 domain.  Global records (other
+// rings' pieces, shared-prefix key splits) are read in groups of SG with every load of a group in flight, so
+// a merge of S prefix splits costs ceil(S / SG) L2 round trips (not one per element and split).
+template <int D, int G, int NT>
+struct MergeMap {
+  static constexpr int TPH = NT / G;  // threads per head
+  static constexpr int DPT = D / TPH;  // dims per thread
+  static constexpr int SG = DPT >= 16 ? 4 : (DPT >= 8 ? 8 : 16);
+  static_assert(NT % G == 0 && D % TPH == 0 && DPT >= 1, "merge map");
+};
+
+template <int DPT>
+__device__ __forceinline__ void ld_dims(const float *p, float (&x)[DPT]) {
+  if constexpr (DPT % 2 == 0) {
 #pragma unroll
-  for (int s = 0; s < kMaxPrefixSplits; ++s) {
-    pml[s] = make_float2(-CUDART_INF_F, 0.f);
-    po[s] = make_float2(0.f, 0.f);
-    if (s < S) {
-      const float *pc = pref + s * part + hoff;
-      pml[s] = __ldcg(reinterpret_cast<const float2 *>(pc + D));
-      po[s] = __ldcg(reinterpret_cast<const float2 *>(pc + dim));
+    for (int i = 0; i < DPT / 2; ++i) {
+      const float2 t = __ldcg(reinterpret_cast<const float2 *>(p) + i);
+      x[2 * i] = t.x;
+      x[2 * i + 1] = t.y;
     }
+  } else {
+#pragma unroll
+    for (int i = 0; i < DPT; ++i) x[i] = __ldcg(p + i);
   }
 }
 
-__device__ __forceinline__ void fold_prefix(const float2 (&pml)[kMaxPrefixSplits], const float2 (&po)[kMaxPrefixSplits],
-                                            float M, float &L, float &ox, float &oy) {
+// Fold n records rec(s) = base + s * stride (s < n) of one head: (o[D], m, l); the thread's dims at d0.
+template <int D, int DPT, int SG>
+__device__ __forceinline__ void fold_records(const float *base, int64_t stride, int n, int d0, float &M, float &L,
+                                             float (&acc)[DPT]) {
+  for (int s0 = 0; s0 < n; s0 += SG) {
+    float2 ml[SG];
+    float o[SG][DPT];
 #pragma unroll
-  for (int s = 0; s < kMaxPrefixSplits; ++s) {
-    const float f = (pml[s].x == -CUDART_INF_F) ? 0.f : fast_exp2(pml[s].x - M);
-    L += pml[s].y * f;
-    ox += po[s].x * f;
-    oy += po[s].y * f;
+    for (int j = 0; j < SG; ++j) {
+      ml[j] = make_float2(-CUDART_INF_F, 0.f);
+#pragma unroll
+      for (int i = 0; i < DPT; ++i) o[j][i] = 0.f;
+      if (s0 + j < n) {
+        const float *r = base + (s0 + j) * stride;
+        ml[j] = __ldcg(reinterpret_cast<const float2 *>(r + D));
+        ld_dims<DPT>(r + d0, o[j]);
+      }
+    }
+    float Mg = M;
+#pragma unroll
+    for (int j = 0; j < SG; ++j) Mg = fmaxf(Mg, ml[j].x);
+    if (Mg == -CUDART_INF_F) continue;
+    const float a = (M == -CUDART_INF_F) ? 0.f : fast_exp2(M - Mg);
+    L *= a;
+#pragma unroll
+    for (int i = 0; i < DPT; ++i) acc[i] *= a;
+#pragma unroll
+    for (int j = 0; j < SG; ++j) {
+      const float f = (ml[j].x == -CUDART_INF_F) ? 0.f : fast_exp2(ml[j].x - Mg);
+      L += ml[j].y * f;
+#pragma unroll
+      for (int i = 0; i < DPT; ++i) acc[i] += o[j][i] * f;
+    }
+    M = Mg;
   }
+}
+
+// The ring's warps' (o, m, l) of this segment from shared memory (comb), head h, dims d0..
+template <int D, int DPT, int NW, int PART>
+__device__ __forceinline__ void fold_comb(const float *comb, int h, int d0, float &M, float &L, float (&acc)[DPT]) {
+  M = -CUDART_INF_F;
+  L = 0.f;
+#pragma unroll
+  for (int i = 0; i < DPT; ++i) acc[i] = 0.f;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) M = fmaxf(M, comb[w * PART + h * (D + 2) + D]);
+  if (M == -CUDART_INF_F) return;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const float *cw = comb + w * PART + h * (D + 2);
+    const float f = (cw[D] == -CUDART_INF_F) ? 0.f : fast_exp2(cw[D] - M);
+    L += cw[D + 1] * f;
+#pragma unroll
+    for (int i = 0; i < DPT; ++i) acc[i] += cw[d0 + i] * f;
+  }
+}
+
+// out[d0 .. d0 + DPT) = acc / L as bf16 (RNE), lse = (M + log2 L) ln 2 by the thread holding d0 = 0
+template <int DPT>
+__device__ __forceinline__ void store_out(__nv_bfloat16 *o, float *lse, int d0, float M, float L,
+                                          const float (&acc)[DPT]) {
+  const float inv = 1.f / L;
+  if constexpr (DPT == 1) {
+    o[0] = __float2bfloat16_rn(acc[0] * inv);
+  } else {
+    uint32_t w[DPT / 2];
+#pragma unroll
+    for (int i = 0; i < DPT / 2; ++i) {
+      __nv_bfloat162 pr = __floats2bfloat162_rn(acc[2 * i] * inv, acc[2 * i + 1] * inv);
+      w[i] = *reinterpret_cast<uint32_t *>(&pr);
+    }
+    if constexpr (DPT == 2) {
+      *reinterpret_cast<uint32_t *>(o) = w[0];
+    } else if constexpr (DPT == 4) {
+      *reinterpret_cast<uint2 *>(o) = make_uint2(w[0], w[1]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < DPT / 8; ++i)
+        reinterpret_cast<uint4 *>(o)[i] = make_uint4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
+    }
+  }
+  if (d0 == 0 && lse) *lse = (M + __log2f(L)) * 0.69314718055994531f;
 }
 
 #ifdef KVFS_K1_TRACE
@@ -271,7 +357,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
       cta = __shfl_sync(0xffffffffu, cta, 0);
     }
     if (cta >= p.ncta) break;
-    const int64_t beg = cta_start(cta, p.total, p.ncta), end = cta_start(cta + 1, p.total, p.ncta);
+    const int64_t beg = cta_start(cta, p), end = cta_start(cta + 1, p);
     int64_t x = beg;
     int dhint = -1;
     while (x < end) {
@@ -382,7 +468,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
     if (lane == 0) mbar_arrive(cempty_bar(k & 1));
   }
   if (cta >= p.ncta) break;
-  const int64_t beg = cta_start(cta, p.total, p.ncta), end = cta_start(cta + 1, p.total, p.ncta);
+  const int64_t beg = cta_start(cta, p), end = cta_start(cta + 1, p);
   int64_t x = beg;
   bool first_seg = true;
   int dhint = -1;
@@ -581,42 +667,14 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
                             ? p.ppart + (static_cast<int64_t>(dd.pref_base) +
                                          static_cast<int64_t>(sg.g * dd.n_q + sg.qi) * dd.pref_splits) * C::PART
                             : nullptr;
+    using MM = MergeMap<D, G, NW * 32>;
+    const int mh = tid / MM::TPH, md0 = (tid % MM::TPH) * MM::DPT;
     if (whole) {
-      // the next element's shared-prefix partials are loaded while this one is combined (one L2 round trip
-      // for the whole merge instead of one per element)
-      float2 pml[kMaxPrefixSplits], po[kMaxPrefixSplits], pml_n[kMaxPrefixSplits], po_n[kMaxPrefixSplits];
-      if (tid < G * D / 2)
-        load_prefix(pref, dd.pref_splits, C::PART, (tid / (D / 2)) * (D + 2), D, (tid % (D / 2)) * 2, pml, po);
-      for (int e = tid; e < G * D / 2; e += NW * 32) {
-        const int h = e / (D / 2), dim = (e % (D / 2)) * 2;
-        const int en = e + NW * 32;
-        if (en < G * D / 2)
-          load_prefix(pref, dd.pref_splits, C::PART, (en / (D / 2)) * (D + 2), D, (en % (D / 2)) * 2, pml_n, po_n);
-        float M = -CUDART_INF_F;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) M = fmaxf(M, comb[w * C::PART + h * (D + 2) + D]);
-#pragma unroll
-        for (int s = 0; s < kMaxPrefixSplits; ++s) M = fmaxf(M, pml[s].x);
-        float L = 0.f, ox = 0.f, oy = 0.f;
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-          const float *cwp = comb + w * C::PART + h * (D + 2);
-          const float f = (cwp[D] == -CUDART_INF_F) ? 0.f : fast_exp2(cwp[D] - M);
-          L += cwp[D + 1] * f;
-          ox += cwp[dim] * f;
-          oy += cwp[dim + 1] * f;
-        }
-        fold_prefix(pml, po, M, L, ox, oy);
-        const float inv = 1.f / L;
-        const int64_t oidx = (row * p.Hq + sg.g * G + h) * D + dim;
-        *reinterpret_cast<__nv_bfloat162 *>(p.out + oidx) = __floats2bfloat162_rn(ox * inv, oy * inv);
-        if (dim == 0 && p.lse) p.lse[row * p.Hq + sg.g * G + h] = (M + __log2f(L)) * 0.69314718055994531f;
-#pragma unroll
-        for (int sp = 0; sp < kMaxPrefixSplits; ++sp) {
-          pml[sp] = pml_n[sp];
-          po[sp] = po_n[sp];
-        }
-      }
+      float M, L, acc[MM::DPT];
+      fold_comb<D, MM::DPT, NW, C::PART>(comb, mh, md0, M, L, acc);
+      if (pref) fold_records<D, MM::DPT, MM::SG>(pref + mh * (D + 2), C::PART, dd.pref_splits, md0, M, L, acc);
+      const int64_t orow = row * p.Hq + sg.g * G + mh;
+      store_out<MM::DPT>(p.out + orow * D + md0, p.lse ? p.lse + orow : nullptr, md0, M, L, acc);
       named_bar_sync(1 + ring, NW * 32);
     } else {
       // partial of this CTA's piece of the unit
@@ -644,7 +702,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
       named_bar_sync(1 + ring, NW * 32);
       if (tid == 0) {
         const int64_t ua = sg.ubeg, ub = sg.ubeg + sg.spu;
-        const int c0 = cta_of(ua, p.total, p.ncta), c1 = cta_of(ub - 1, p.total, p.ncta);
+        const int c0 = cta_of(ua, p), c1 = cta_of(ub - 1, p);
         const int prev = atomicAdd(p.counters + unit, 1);
         *flag = (prev == c1 - c0) ? 1 : 0;
         if (prev == c1 - c0) p.counters[unit] = 0;  // self-cleaning for the next launch
@@ -653,35 +711,18 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
       if (*flag) {
         __threadfence();
         const int64_t ua = sg.ubeg, ub = sg.ubeg + sg.spu;
-        const int c0 = cta_of(ua, p.total, p.ncta), c1 = cta_of(ub - 1, p.total, p.ncta);
-        for (int e = tid; e < G * D / 2; e += NW * 32) {
-          const int h = e / (D / 2), dim = (e % (D / 2)) * 2;
-          float M = -CUDART_INF_F;
-          for (int c = c0; c <= c1; ++c) {
-            const int wh = (cta_start(c, p.total, p.ncta) >= ua) ? 0 : 1;
-            const float *pc = p.partials + (static_cast<int64_t>(c) * 2 + wh) * C::PART + h * (D + 2);
-            M = fmaxf(M, __ldcg(pc + D));
-          }
-          float2 pml[kMaxPrefixSplits], po[kMaxPrefixSplits];
-          load_prefix(pref, dd.pref_splits, C::PART, h * (D + 2), D, dim, pml, po);
+        const int c0 = cta_of(ua, p), c1 = cta_of(ub - 1, p);
+        float M = -CUDART_INF_F, L = 0.f, acc[MM::DPT];
 #pragma unroll
-          for (int s = 0; s < kMaxPrefixSplits; ++s) M = fmaxf(M, pml[s].x);
-          float L = 0.f, ox = 0.f, oy = 0.f;
-          fold_prefix(pml, po, M, L, ox, oy);
-          for (int c = c0; c <= c1; ++c) {
-            const int wh = (cta_start(c, p.total, p.ncta) >= ua) ? 0 : 1;
-            const float *pc = p.partials + (static_cast<int64_t>(c) * 2 + wh) * C::PART + h * (D + 2);
-            const float mc = __ldcg(pc + D);
-            const float f = (mc == -CUDART_INF_F) ? 0.f : fast_exp2(mc - M);
-            L += __ldcg(pc + D + 1) * f;
-            ox += __ldcg(pc + dim) * f;
-            oy += __ldcg(pc + dim + 1) * f;
-          }
-          const float inv = 1.f / L;
-          const int64_t oidx = (row * p.Hq + sg.g * G + h) * D + dim;
-          *reinterpret_cast<__nv_bfloat162 *>(p.out + oidx) = __floats2bfloat162_rn(ox * inv, oy * inv);
-          if (dim == 0 && p.lse) p.lse[row * p.Hq + sg.g * G + h] = (M + __log2f(L)) * 0.69314718055994531f;
+        for (int i = 0; i < MM::DPT; ++i) acc[i] = 0.f;
+        for (int c = c0; c <= c1; ++c) {  // the unit's pieces in range order (deterministic)
+          const int wh = (cta_start(c, p) >= ua) ? 0 : 1;
+          fold_records<D, MM::DPT, 1>(p.partials + (static_cast<int64_t>(c) * 2 + wh) * C::PART + mh * (D + 2), 0, 1,
+                                      md0, M, L, acc);
         }
+        if (pref) fold_records<D, MM::DPT, MM::SG>(pref + mh * (D + 2), C::PART, dd.pref_splits, md0, M, L, acc);
+        const int64_t orow = row * p.Hq + sg.g * G + mh;
+        store_out<MM::DPT>(p.out + orow * D + md0, p.lse ? p.lse + orow : nullptr, md0, M, L, acc);
       }
       named_bar_sync(1 + ring, NW * 32);
     }

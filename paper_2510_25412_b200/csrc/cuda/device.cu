@@ -7,6 +7,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <unordered_map>
 #include <vector>
@@ -26,13 +28,14 @@ struct WsLayout {
   size_t slab = 0, upload = 0, counters = 0, partials = 0, ptrs = 0, prefix = 0, total = 0, upload_cap = 0;
   size_t scratch = 0, scratch_cap = 0;  // second upload area: packets sent while a pred step is open
   size_t work = 0;                      // [2] int: K1 dynamic-scheduling counters (self-resetting)
+  size_t pgroup = 0;                    // [2][kMaxPrefixGroups] int: shared-prefix split-group counters
   int64_t prefix_cap = 0;  // shared-prefix partials (PART floats each)
 };
 
 WsLayout ws_layout(const kvfs_config &c) {
   WsLayout w;
   const int G = c.n_q_heads / c.n_kv_heads;
-  const size_t part = static_cast<size_t>(G) * (c.head_dim + 2) * 4;
+  const size_t part = static_cast<size_t>(dev::part_floats(G, c.head_dim)) * 4;
   size_t off = 0;
   w.slab = off;
   off = align256(off + static_cast<size_t>(c.table_capacity) * 16);
@@ -53,13 +56,17 @@ WsLayout ws_layout(const kvfs_config &c) {
   off = align256(off + static_cast<size_t>(c.max_batch_rows) * c.n_kv_heads * 4);
   w.work = off;
   off = align256(off + 16);
+  w.pgroup = off;
+  off = align256(off + 2 * static_cast<size_t>(kMaxPrefixGroups) * 4);
   w.partials = off;
   off = align256(off + static_cast<size_t>(kMaxCtas) * 2 * part);
   w.ptrs = off;
   off = align256(off + static_cast<size_t>(c.n_layers) * 2 * sizeof(void *));
-  // shared-prefix (cascade) partials: up to kMaxPrefixSplits key splits per decode unit, capped at 16384
+  // shared-prefix (cascade) partials: one merged partial per decode unit + up to kMaxPrefixSplits split
+  // partials, capped at 16384 + the merged ones
   w.prefix_cap = c.head_dim == 128
-                     ? std::min<int64_t>(static_cast<int64_t>(c.max_batch_rows) * c.n_kv_heads * kMaxPrefixSplits, 16384)
+                     ? std::min<int64_t>(static_cast<int64_t>(c.max_batch_rows) * c.n_kv_heads * (kMaxPrefixSplits + 1),
+                                         16384 + static_cast<int64_t>(c.max_batch_rows) * c.n_kv_heads)
                      : 0;
   w.prefix = off;
   off = align256(off + static_cast<size_t>(w.prefix_cap) * part);
@@ -339,6 +346,23 @@ __global__ void read_kernel(const dev::Entry *t, int n_ent, int64_t begin, int64
 }
 
 // ------------------------------------------------------------------------------------------ device
+#ifdef KVFS_HOST_PROFILE
+// Development: host time of the launch-path pieces, printed every 200 layers (build variant only).
+struct HostProf {
+  double t[8] = {0};
+  int64_t n = 0;
+  static double now() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  }
+};
+static HostProf g_hprof;
+#define HP_MARK(var) const double var = HostProf::now()
+#define HP_ADD(i, a, b) g_hprof.t[i] += (b) - (a)
+#else
+#define HP_MARK(var)
+#define HP_ADD(i, a, b)
+#endif
+
 class CudaDevice final : public Device {
  public:
   explicit CudaDevice(Ctx &c) : c_(c) {}
@@ -352,6 +376,11 @@ class CudaDevice final : public Device {
       cudaFreeHost(b.host);
     }
     for (auto &kv : host_sizes_) cudaFreeHost(kv.first);
+    for (auto &t : layer_timing_) {
+      cudaEventDestroy(t.first);
+      cudaEventDestroy(t.second);
+    }
+    for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
   }
 
   int init() {
@@ -375,6 +404,8 @@ class CudaDevice final : public Device {
       return KVFS_EIO;
     work_ = reinterpret_cast<int *>(ws + lay_.work);
     if (cudaMemset(work_, 0, 16) != cudaSuccess) return KVFS_EIO;
+    pgroup_ = reinterpret_cast<int *>(ws + lay_.pgroup);
+    if (cudaMemset(pgroup_, 0, 2 * static_cast<size_t>(kMaxPrefixGroups) * 4) != cudaSuccess) return KVFS_EIO;
     // Zero-fill the pools once: every slot then always holds finite bf16 (only finite rows are ever
     // written), so the tensor-core kernel can multiply masked-out keys' V rows by P = 0 safely.
     const size_t pool_bytes = static_cast<size_t>(cfg.n_pages) * cfg.n_kv_heads * cfg.page_size * cfg.head_dim * 2;
@@ -589,8 +620,45 @@ class CudaDevice final : public Device {
                            static_cast<const dev::PageCopy *>(d_copies_), static_cast<int>(pl.copies.size()), s);
   }
 
+  // KVFS_OPT_TIMING: events on the stream before the layer's first kernel and after its last
   int pred_layer(const PredPlan &pl, int layer, const void *q, const void *k_new, const void *v_new, void *out,
                  float *lse, float scale, kvfs_stream_t s) override {
+    if (!c_.opt_timing) return pred_layer_kernels(pl, layer, q, k_new, v_new, out, lse, scale, s);
+    cudaEvent_t e0 = pooled_event(), e1 = pooled_event();
+    if (!e0 || !e1) return KVFS_EIO;
+    cudaEventRecord(e0, cs(s));
+    const int rc = pred_layer_kernels(pl, layer, q, k_new, v_new, out, lse, scale, s);
+    cudaEventRecord(e1, cs(s));
+    layer_timing_.push_back({e0, e1});
+    return rc;
+  }
+
+  int64_t take_layer_ns(int64_t *n) override {
+    double ms = 0;
+    for (auto &t : layer_timing_) {
+      float x = 0.f;
+      if (cudaEventSynchronize(t.second) == cudaSuccess && cudaEventElapsedTime(&x, t.first, t.second) == cudaSuccess)
+        ms += x;
+      ev_pool_.push_back(t.first);
+      ev_pool_.push_back(t.second);
+    }
+    *n = static_cast<int64_t>(layer_timing_.size());
+    layer_timing_.clear();
+    return static_cast<int64_t>(ms * 1e6);
+  }
+
+  cudaEvent_t pooled_event() {
+    if (!ev_pool_.empty()) {
+      cudaEvent_t e = ev_pool_.back();
+      ev_pool_.pop_back();
+      return e;
+    }
+    cudaEvent_t e = nullptr;
+    return cudaEventCreate(&e) == cudaSuccess ? e : nullptr;
+  }
+
+  int pred_layer_kernels(const PredPlan &pl, int layer, const void *q, const void *k_new, const void *v_new,
+                         void *out, float *lse, float scale, kvfs_stream_t s) {
     c_.ctr.last_chunk_units = static_cast<int64_t>(pl.chunk_units.size());
     c_.ctr.last_prefix_units = static_cast<int64_t>(pl.prefix_units.size());
     c_.ctr.last_prefix_groups = pl.prefix_groups;
@@ -649,10 +717,20 @@ class CudaDevice final : public Device {
     p.Hkv = cfg.n_kv_heads;
     // always a programmatic dependent launch: after the prologue (waits at start) or after the shared-prefix
     // kernel (which waited for the prologue itself; waits before merging)
+    HP_MARK(d0);
     const cudaError_t e = dev::launch_decode(p, cfg.head_dim, cfg.n_q_heads / cfg.n_kv_heads, cfg.page_size, cs(s),
                                              true);
+    HP_MARK(d1);
+    HP_ADD(2, d0, d1);
+#ifdef KVFS_HOST_PROFILE
+    if (++g_hprof.n % 200 == 0) {
+      fprintf(stderr, "[hprof] per layer us: qmap encode %.2f prefix launch %.2f decode launch %.2f\n",
+              g_hprof.t[0] / 200, g_hprof.t[1] / 200, g_hprof.t[2] / 200);
+      for (double &x : g_hprof.t) x = 0;
+    }
+#endif
     ++c_.ctr.launches;
-    c_.ctr.last_decode_ctas = ncta;
+    c_.ctr.last_decode_ctas = p.ncta;
     return e == cudaSuccess ? KVFS_OK : KVFS_EIO;
   }
 
@@ -728,8 +806,17 @@ class CudaDevice final : public Device {
     p.prows = static_cast<const dev::PrefixRow *>(d_prows_);
     p.q = static_cast<const bf16 *>(q);
     p.ppart = ppart_;
-    const cudaError_t e = dev::launch_prefix(kmaps_[layer], vmaps_[layer], kmaps_[layer], p,
+    p.pgroup = pgroup_;
+    p.pgroup_parity = static_cast<int>(prefix_launches_++ & 1);
+    alignas(64) CUtensorMap qmap;
+    HP_MARK(a0);
+    if (!encode_q_map(&qmap, q, pl.T)) return KVFS_EINVAL;
+    HP_MARK(a1);
+    const cudaError_t e = dev::launch_prefix(kmaps_[layer], vmaps_[layer], qmap, p,
                                              static_cast<int>(pl.prefix_units.size()), G, cs(s));
+    HP_MARK(a2);
+    HP_ADD(0, a0, a1);
+    HP_ADD(1, a1, a2);
     ++c_.ctr.launches;
     return e == cudaSuccess ? KVFS_OK : KVFS_EIO;
   }
@@ -757,6 +844,23 @@ class CudaDevice final : public Device {
   }
 
   // K2: scatter the chunk descriptors' new rows into the pool, then tcgen05 attention from the pool.
+  // Q [T][Hq][D] as a 4-D tensor (D, G, Hkv, T), boxes of {64 dims, G heads, 1 kv head, 128 / G rows} with
+  // 128-byte swizzle: one box = one 64-column half of a 128-row M-tile (rows = (token, head), head fastest)
+  bool encode_q_map(CUtensorMap *qmap, const void *q, int64_t T) {
+    const kvfs_config &cfg = c_.cfg;
+    const int G = cfg.n_q_heads / cfg.n_kv_heads;
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(cfg.head_dim), static_cast<cuuint64_t>(G),
+                                static_cast<cuuint64_t>(cfg.n_kv_heads), static_cast<cuuint64_t>(T)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(cfg.head_dim) * 2,
+                                   static_cast<cuuint64_t>(G) * cfg.head_dim * 2,
+                                   static_cast<cuuint64_t>(cfg.n_q_heads) * cfg.head_dim * 2};
+    const cuuint32_t box[4] = {64, static_cast<cuuint32_t>(G), 1, static_cast<cuuint32_t>(128 / G)};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    return encode_(qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(q), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+
   int chunk_layer(const PredPlan &pl, int layer, const void *q, const void *k_new, const void *v_new, void *out,
                   float *lse, float scale, kvfs_stream_t s) {
     const kvfs_config &cfg = c_.cfg;
@@ -768,19 +872,7 @@ class CudaDevice final : public Device {
     if (e != cudaSuccess) return KVFS_EIO;
     const int G = cfg.n_q_heads / cfg.n_kv_heads;
     alignas(64) CUtensorMap qmap;
-    {
-      const cuuint64_t dims[4] = {static_cast<cuuint64_t>(cfg.head_dim), static_cast<cuuint64_t>(G),
-                                  static_cast<cuuint64_t>(cfg.n_kv_heads), static_cast<cuuint64_t>(pl.T)};
-      const cuuint64_t strides[3] = {static_cast<cuuint64_t>(cfg.head_dim) * 2,
-                                     static_cast<cuuint64_t>(G) * cfg.head_dim * 2,
-                                     static_cast<cuuint64_t>(cfg.n_q_heads) * cfg.head_dim * 2};
-      const cuuint32_t box[4] = {64, static_cast<cuuint32_t>(G), 1, static_cast<cuuint32_t>(128 / G)};
-      const cuuint32_t es[4] = {1, 1, 1, 1};
-      if (encode_(&qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(q), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return KVFS_EINVAL;
-    }
+    if (!encode_q_map(&qmap, q, pl.T)) return KVFS_EINVAL;
     dev::ChunkParams p{};
     p.units = static_cast<const dev::ChunkUnit *>(d_cunits_);
     p.descs = static_cast<const dev::ChunkDesc *>(d_cdescs_);
@@ -938,12 +1030,16 @@ class CudaDevice final : public Device {
   size_t area_cap_ = 0;
   int *counters_ = nullptr;
   int *work_ = nullptr;
+  int *pgroup_ = nullptr;
+  uint64_t prefix_launches_ = 0;
   float *partials_ = nullptr;
   float *ppart_ = nullptr;
   bf16 **kptrs_ = nullptr, **vptrs_ = nullptr;
   int sms_ = 148;
   int per_sm_ = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timing_;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> layer_timing_;  // KVFS_OPT_TIMING: per pred layer
+  std::vector<cudaEvent_t> ev_pool_;
   int64_t k5_grid_ = 0;
   Staging stg_[4];
   int cur_ = 0;

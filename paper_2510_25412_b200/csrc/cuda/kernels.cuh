@@ -7,7 +7,10 @@
 namespace kvfs {
 namespace dev {
 
-constexpr int kMaxPrefixSplits = 8;  // == kvfs::kMaxPrefixSplits (key splits of a shared prefix)
+// Floats of one partial record (o, m, l) of a unit's G heads: G (D + 2) rounded up to 16 bytes, so records
+// can be moved by 1-D TMA bulk copies (head h at h (D + 2))
+__host__ __device__ constexpr int part_floats(int G, int D) { return (G * (D + 2) + 3) & ~3; }
+constexpr int kMaxPrefixSplits = 16;  // == kvfs::kMaxPrefixSplits (key splits of a shared prefix)
 
 struct DecodeParams {
   const Desc *descs;
@@ -38,10 +41,11 @@ struct ChunkDesc {  // == kvfs::ChunkDesc
   int32_t slab_off, n_entries, n_old, n_q, row0, first_new_entry, first_new_lstart, pad;
 };
 struct ChunkUnit {  // == kvfs::ChunkUnit
-  int32_t desc, g, m, pad;
+  int32_t desc, g, m, group;
 };
+constexpr int kMaxPrefixGroups = 4096;  // == kvfs::kMaxPrefixGroups
 struct PrefixDesc {  // == kvfs::PrefixDesc
-  int32_t slab_off, n_entries, n_rows, row0, split, n_splits, pad0, pad1;
+  int32_t slab_off, n_entries, n_rows, row0, split, n_splits, q_t0, split_off;
 };
 struct PrefixRow {  // == kvfs::PrefixRow
   int32_t t, pref_base, n_q, qi;
@@ -71,6 +75,8 @@ struct ChunkParams {
   const PrefixRow *prows;
   const __nv_bfloat16 *q;
   float *ppart;
+  int *pgroup;         // [2][kMaxPrefixGroups] arrival counters of the split groups, by launch parity
+  int pgroup_parity;   // 0 / 1: this launch's counter array (the other one is cleared)
 };
 cudaError_t launch_chunk(const CUtensorMap &km, const CUtensorMap &vm, const CUtensorMap &qm, const ChunkParams &p,
                          int n_units, int G, cudaStream_t s);

@@ -225,19 +225,30 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, 
   for (size_t k = 0; k < fam.size(); ++k) {
     const std::vector<int> &m = fam[k];
     if (m.size() < 2) continue;
-    const Entry *lead = pl.desc_files[m[0]]->table.data();
+    const File *lf = pl.desc_files[m[0]];
+    const Entry *lead = lf->table.data();
     int E = pl.descs[m[0]].first_new_entry;
     for (size_t j = 1; j < m.size() && E > 0; ++j) {
-      const Entry *b = pl.desc_files[m[j]]->table.data();
+      File *bf = pl.desc_files[m[j]];
       const int lim = std::min(E, pl.descs[m[j]].first_new_entry);
-      // a shared run has identical entries (page, mask and so the logical start): one memcmp in the common
-      // case, the (page, mask) scan only when it differs somewhere
-      int e = lim;
-      if (std::memcmp(lead, b, static_cast<size_t>(lim) * sizeof(Entry)) != 0) {
-        e = 0;
-        while (e < lim && b[e].page == lead[e].page && b[e].mask == lead[e].mask) ++e;
+      // The number of leading entries identical (page, mask and so the logical start) to the leader's is
+      // cached per member with both files' table stamps: it changes only when one of the tables is changed
+      // in place (a new stamp), not by appends (File::tver).  Otherwise one memcmp over the whole common
+      // length, the (page, mask) scan only when it differs somewhere.
+      if (bf->run_lead != lf || bf->run_lead_tver != lf->tver || bf->run_self_tver != bf->tver) {
+        const Entry *b = bf->table.data();
+        const size_t n = std::min(lf->table.size(), bf->table.size());
+        size_t e = n;
+        if (std::memcmp(lead, b, n * sizeof(Entry)) != 0) {
+          e = 0;
+          while (e < n && b[e].page == lead[e].page && b[e].mask == lead[e].mask) ++e;
+        }
+        bf->run_lead = lf;
+        bf->run_lead_tver = lf->tver;
+        bf->run_self_tver = bf->tver;
+        bf->run_len = static_cast<int64_t>(e);
       }
-      E = e;
+      E = static_cast<int>(std::min<int64_t>(lim, bf->run_len));
     }
     if (E < min_entries) continue;
     int rows = 0;
@@ -246,41 +257,61 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, 
     use.push_back({static_cast<int>(k), E, rows, (E + epb - 1) / epb, (mt + 1) / 2, 1});
   }
   if (use.empty()) return;
-  // key splits: about one CTA per SM over all families, at most kMaxPrefixSplits and at most one per tile
+  // Key splits: about one CTA per SM over all families, at most kMaxPrefixSplits and at most one per tile.
+  // The S split CTAs of a (family, kv head, M-tile pair) group exchange their partials through global memory
+  // and each merges a slice of the group's rows, so the decode kernel folds ONE prefix partial per unit.
+  // Their wait for each other needs every CTA of the grid resident at once (one CTA per SM): with S > 1 the
+  // grid is at most one CTA per SM.
   int64_t units_per_split = 0, rows_all = 0;
   for (const Fam &u : use) {
     units_per_split += static_cast<int64_t>(Hkv) * u.mpairs;
     rows_all += u.rows;
   }
-  int S = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kMaxPrefixSplits, sms / std::max<int64_t>(1, units_per_split))));
-  if (force_splits > 0) S = std::min(force_splits, kMaxPrefixSplits);
-  while (S > 1 && rows_all * Hkv * S > max_partials) --S;
-  if (rows_all * Hkv * S > max_partials) return;  // workspace too small: no cascade
+  const int64_t fit = std::max<int64_t>(1, sms / std::max<int64_t>(1, units_per_split));
+  int S = static_cast<int>(std::min<int64_t>(kMaxPrefixSplits, fit));
+  if (force_splits > 0) S = static_cast<int>(std::min<int64_t>(std::min(force_splits, kMaxPrefixSplits), fit));
+  // workspace: one merged partial per (member row, kv head), plus S split partials when S > 1
+  while (S > 1 && rows_all * Hkv * (S + 1) > max_partials) --S;
+  if (rows_all * Hkv > max_partials) return;  // workspace too small: no cascade
+  int64_t merged = rows_all * Hkv;            // split partials live after the merged ones
+  int64_t split_next = merged;
+  int32_t group = 0;
   for (Fam &u : use) {
-    const int want = std::min(S, u.tiles);
-    const int tps = (u.tiles + want - 1) / want;  // tiles per split
-    u.S = (u.tiles + tps - 1) / tps;              // no empty split
+    u.S = std::min(S, u.tiles);  // splits of the family: tiles spread evenly, none empty
     const std::vector<int> &m = fam[u.idx];
     const int row0 = static_cast<int>(pl.prefix_rows.size());
+    // members whose query rows follow each other in the packed batch (e.g. a family's consecutive decode
+    // descriptors): the prefix kernel loads Q tiles by TMA instead of gathering rows
+    int32_t q_t0 = pl.descs[m[0]].row0;
+    for (size_t j = 1; j < m.size() && q_t0 >= 0; ++j)
+      if (pl.descs[m[j]].row0 != pl.descs[m[j - 1]].row0 + pl.descs[m[j - 1]].n_q) q_t0 = -1;
+    const int32_t merged_base = pl.prefix_partials;
     for (int i : m) {
       DevDesc &d = pl.descs[i];
       d.skip = u.E;
-      d.pref_splits = u.S;
+      d.pref_splits = 1;  // the decode kernel reads the merged partial of unit (g, qi): pref_base + g * n_q + qi
       d.pref_base = pl.prefix_partials;
-      pl.prefix_partials += Hkv * d.n_q * u.S;
+      pl.prefix_partials += Hkv * d.n_q;
       d.stages_per_unit = (d.n_old_entries - u.E) + (d.n_q + P - 1) / P;
       for (int qi = 0; qi < d.n_q; ++qi) pl.prefix_rows.push_back({d.row0 + qi, d.pref_base, d.n_q, qi});
     }
+    // split partial of merged record r, split s: split_off + r * S + s (split_off = split base - merged base * S)
+    const int32_t split_off = static_cast<int32_t>(u.S > 1 ? split_next - static_cast<int64_t>(merged_base) * u.S : 0);
+    if (u.S > 1) split_next += static_cast<int64_t>(pl.prefix_partials - merged_base) * u.S;
     const DevDesc &lead = pl.descs[m[0]];
     for (int sp = 0; sp < u.S; ++sp) {
-      const int e0 = sp * tps * epb, e1 = std::min(u.E, (sp + 1) * tps * epb);
-      const int32_t di = static_cast<int32_t>(pl.prefix_descs.size());
-      pl.prefix_descs.push_back({lead.slab_off + e0, e1 - e0, u.rows, row0, sp, u.S, 0, 0});
-      for (int g = 0; g < Hkv; ++g)
-        for (int mp = 0; mp < u.mpairs; ++mp) pl.prefix_units.push_back({di, g, mp, 0});
+      const int t0 = sp * u.tiles / u.S, t1 = (sp + 1) * u.tiles / u.S;
+      const int e0 = t0 * epb, e1 = std::min(u.E, t1 * epb);
+      pl.prefix_descs.push_back({lead.slab_off + e0, e1 - e0, u.rows, row0, sp, u.S, q_t0, split_off});
     }
+    // CTAs: group (g, M-tile pair) -> its S splits consecutively; ChunkUnit.pad = group id
+    const int32_t d0 = static_cast<int32_t>(pl.prefix_descs.size()) - u.S;
+    for (int g = 0; g < Hkv; ++g)
+      for (int mp = 0; mp < u.mpairs; ++mp, ++group)
+        for (int sp = 0; sp < u.S; ++sp) pl.prefix_units.push_back({d0 + sp, g, mp, group});
     ++pl.prefix_groups;
   }
+  (void)merged;
   // the members' decode work shrank: re-pack the K1 stage ranges
   int64_t cost = 0;
   for (DevDesc &d : pl.descs) {

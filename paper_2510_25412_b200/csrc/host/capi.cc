@@ -7,6 +7,7 @@
 #include <thread>
 #include <atomic>
 #include <algorithm>
+#include <chrono>
 #include "kvfs_impl.h"
 
 #ifndef KVFS_SCORE_UNIT_ENTRIES
@@ -16,6 +17,11 @@
 using namespace kvfs;
 
 namespace {
+
+int64_t now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
 
 bool supported_shape(const kvfs_config &c) {
   if (c.n_layers < 1 || c.n_layers > 1024) return false;
@@ -444,15 +450,19 @@ int pred_step_begin(kvfs_ctx *ctx, const pred_desc *descs, int n_desc, const int
     KVFS_LOCK_OR(ctx);
     if (!step) return KVFS_EINVAL;
     if (c.dev && c.poisoned) return KVFS_EIO;
+    const int64_t t0 = now_ns();
     const int rc = pred_reserve(c, descs, n_desc, pos, status, &c.plan);
+    const int64_t t1 = now_ns();
+    c.ctr.host_reserve_ns += t1 - t0;
     if (rc != KVFS_OK && rc != KVFS_EPARTIAL) return rc;
     if (c.dev) {
       pred_split(c, c.opt_chunk_cutover, &c.plan);
       pred_cascade(c, c.opt_cascade_min_entries, c.opt_prefix_splits, c.dev->sms(), c.dev->prefix_partial_capacity(),
                    &c.plan);
-    }
-    if (c.dev) {
+      const int64_t t2 = now_ns();
+      c.ctr.host_split_ns += t2 - t1;
       const int drc = c.dev->pred_begin(c.plan, stream);
+      c.ctr.host_upload_ns += now_ns() - t2;
       if (drc != KVFS_OK) {
         c.poisoned = true;
         return drc;
@@ -476,7 +486,9 @@ int pred_attn_layer(kvfs_ctx *ctx, pred_step *step, int layer, const void *q, co
     if (c.poisoned) return KVFS_EIO;
     if (layer < 0 || layer >= c.cfg.n_layers || !(scale > 0.f)) return KVFS_EINVAL;
     if (c.plan.T > 0 && (!q || !k_new || !v_new || !out)) return KVFS_EINVAL;
+    const int64_t t0 = now_ns();
     const int rc = c.dev->pred_layer(c.plan, layer, q, k_new, v_new, out, lse, scale, stream);
+    c.ctr.host_launch_ns += now_ns() - t0;
     if (rc != KVFS_OK) c.poisoned = true;
     return rc;
   });
@@ -746,6 +758,17 @@ int kvfs_get_counter(kvfs_ctx *ctx, int counter, int64_t *value) {
       case KVFS_CTR_LAST_PREFIX_GROUPS: *value = c.ctr.last_prefix_groups; return KVFS_OK;
       case KVFS_CTR_HOST_PAGES: *value = c.ctr.host_pages; return KVFS_OK;
       case KVFS_CTR_COMPACT_DEVICE_NS: *value = c.last_compact_device_ns; return KVFS_OK;
+      case KVFS_CTR_LAYER_DEVICE_NS: {
+        int64_t n = 0;
+        *value = c.dev ? c.dev->take_layer_ns(&n) : 0;
+        c.last_layer_timed = n;
+        return KVFS_OK;
+      }
+      case KVFS_CTR_LAYER_TIMED: *value = c.last_layer_timed; return KVFS_OK;
+      case KVFS_CTR_HOST_RESERVE_NS: *value = c.ctr.host_reserve_ns; return KVFS_OK;
+      case KVFS_CTR_HOST_SPLIT_NS: *value = c.ctr.host_split_ns; return KVFS_OK;
+      case KVFS_CTR_HOST_UPLOAD_NS: *value = c.ctr.host_upload_ns; return KVFS_OK;
+      case KVFS_CTR_HOST_LAUNCH_NS: *value = c.ctr.host_launch_ns; return KVFS_OK;
       default: return KVFS_EINVAL;
     }
   });

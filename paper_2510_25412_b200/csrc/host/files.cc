@@ -212,6 +212,7 @@ void append_commit(Ctx &c, File &f, int64_t n, const int32_t *pos, std::vector<i
         copies->push_back({t.page, q});
         c.pool->release(t.page);
         t.page = q;
+        f.tver = next_tver();
       }
       const int take = static_cast<int>(std::min<int64_t>(n, room));
       for (int s = 0; s < take; ++s) {
@@ -270,6 +271,7 @@ int truncate_file(Ctx &c, File &f, int64_t n) {
   const int P = c.cfg.page_size;
   if (n < 0 || n > f.len) return KVFS_ERANGE;
   if (n == f.len) return KVFS_OK;
+  f.tver = next_tver();
   if (n == 0) {
     for (const Entry &e : f.table) c.pool->release(e.page);
     f.table.clear();
@@ -334,6 +336,7 @@ static void compact_tables(Ctx &c, File &f, std::vector<Entry> *old, std::vector
   const uint64_t full = P == 64 ? ~0ull : ((1ull << P) - 1);
   old->clear();
   old->swap(f.table);
+  f.tver = next_tver();
   f.table.resize(static_cast<size_t>(k));
   for (int64_t j = 0; j < k; ++j) {
     const int64_t cnt = std::min<int64_t>(P, len - j * P);
@@ -427,6 +430,7 @@ int evict_file(Ctx &c, File &f, const int64_t *ranges, int n_ranges, int flags, 
   }
   if (!touched.empty()) {
     bool removed = false;
+    f.tver = next_tver();
     for (const auto &t : touched) {
       f.table[t.first].mask = t.second;
       if (t.second == 0) {
@@ -551,6 +555,7 @@ int merge_files(Ctx &c, const int *fds, int n, const char *name, int *fd, std::v
 int offload_file(Ctx &c, File &f, std::vector<uint32_t> *pages) {
   if (f.offloaded) return KVFS_EINVAL;
   pages->clear();
+  f.tver = next_tver();
   for (Entry &e : f.table) {
     if (c.pool->refcnt(e.page) != 1) continue;
     pages->push_back(e.page);
@@ -568,6 +573,7 @@ int restore_file(Ctx &c, File &f, std::vector<uint32_t> *new_pages) {
   if (!f.offloaded) return KVFS_EINVAL;
   if (f.n_host > c.pool->n_free()) return KVFS_ENOSPC;
   new_pages->assign(static_cast<size_t>(f.n_host), 0u);
+  f.tver = next_tver();
   for (Entry &e : f.table) {
     if (!(e.page & KVFS_HOST_PAGE)) continue;
     const uint32_t slot = e.page & ~KVFS_HOST_PAGE;

@@ -23,8 +23,24 @@ struct Entry {
 };
 static_assert(sizeof(Entry) == 16, "Entry must be 16 bytes");
 
+// Table version stamps: globally unique and increasing, so (file, stamp) identifies one state of a table.
+inline uint64_t next_tver() {
+  static std::atomic<uint64_t> clock{0};
+  return ++clock;
+}
+
 struct File {
   std::string name;
+  // Version of the table's existing entries: a new stamp whenever an entry is changed in place or removed
+  // (truncate, evict, compaction, copy-on-write of the tail, offload / restore).  Appends that only add
+  // entries or fill the slots of an unshared tail keep it (an entry identical to another file's entry
+  // holds a shared page, and appending into a shared tail copies it first, i.e. gets a new stamp).
+  uint64_t tver = next_tver();
+  // Cascade planning cache (pred_cascade): the number of leading entries identical to those of file
+  // run_lead, valid while both stamps are unchanged.
+  const File *run_lead = nullptr;
+  uint64_t run_lead_tver = 0, run_self_tver = 0;
+  int64_t run_len = 0;
   bool alive = true;
   std::vector<Entry> table;
   std::vector<int32_t> spos;  // [n_entries * P]: absolute position of the token in (entry, slot)
@@ -80,7 +96,8 @@ struct DevDesc {
   int32_t skip;              // leading entries attended by the shared-prefix kernel (0: none)
   int32_t pref_splits;       // shared-prefix partials per unit (0: none)
   int32_t pref_base;         // first shared-prefix partial of unit (g = 0, qi = 0): unit (g, qi) split s is
-                             // partial pref_base + (g * n_q + qi) * pref_splits + s
+                             // partial pref_base + (g * n_q + qi) * pref_splits + s (the cascade writes one
+                             // merged partial per unit: pref_splits = 1)
 };
 static_assert(sizeof(DevDesc) == 64, "DevDesc must be 64 bytes");
 
@@ -96,9 +113,11 @@ struct ChunkDesc {
   int32_t slab_off, n_entries, n_old, n_q, row0, first_new_entry, first_new_lstart, pad;
 };
 struct ChunkUnit {
-  int32_t desc, g, m, pad;
+  int32_t desc, g, m;
+  int32_t group;  // shared-prefix mode: the (family, kv head, M-tile pair) group whose splits merge together
 };
-constexpr int kMaxPrefixSplits = 8;  // key splits of one shared prefix (the decode merge unrolls over them)
+constexpr int kMaxPrefixGroups = 4096;  // group counters in the workspace (a prefix grid with S > 1 is <= 1 CTA per SM)
+constexpr int kMaxPrefixSplits = 16;  // key splits of one shared prefix (the decode merge folds them in groups)
 // Shared-prefix (cascade) work: one record per (fork family, key split); the family's query rows are
 // listed in PrefixRow order (row0 .. row0 + n_rows - 1).
 struct PrefixDesc {
@@ -106,7 +125,10 @@ struct PrefixDesc {
   int32_t n_entries;  // entries of this split
   int32_t n_rows;     // query rows (tokens) of the family
   int32_t row0;       // first PrefixRow of the family
-  int32_t split, n_splits, pad0, pad1;
+  int32_t split, n_splits;
+  int32_t q_t0;       // >= 0: the family's query rows are the consecutive packed rows q_t0 .. q_t0 + n_rows - 1
+                      // (Q tiles by TMA); -1: rows gathered through the PrefixRow records
+  int32_t split_off;  // n_splits > 1: split partial s of merged record r is split_off + r * n_splits + s
 };
 // NEXT-2 attention-score accumulation (pred_attn_scores): every successful descriptor of the step, and
 // the work units (descriptor, entry chunk of <= 32 entries, logical index of the chunk's first token).
@@ -164,6 +186,7 @@ struct CompactJob {
 struct CtxCounters {
   int64_t launches = 0, h2d_bytes = 0, page_copies = 0, last_decode_ctas = 0, last_chunk_units = 0,
           last_prefix_units = 0, last_prefix_groups = 0, host_pages = 0;
+  int64_t host_reserve_ns = 0, host_split_ns = 0, host_upload_ns = 0, host_launch_ns = 0;
 };
 
 struct Ctx {
@@ -187,6 +210,7 @@ struct Ctx {
   int opt_prefix_splits = 0;  // 0 = auto
   bool opt_timing = false;    // KVFS_OPT_TIMING
   int64_t last_compact_device_ns = 0;
+  int64_t last_layer_timed = 0;
   CtxCounters ctr;
   PredPlan plan;  // the open step's plan
   std::vector<int> step_status;
@@ -276,6 +300,9 @@ class Device {
   virtual int64_t prefix_partial_capacity() const = 0;
   // KVFS_OPT_TIMING: device time (ns) of the intervals recorded since the last call (waits for them)
   virtual int64_t take_device_ns() = 0;
+  // KVFS_OPT_TIMING: summed device time of the pred layers recorded since the last call (waits for them);
+  // *n = how many
+  virtual int64_t take_layer_ns(int64_t *n) = 0;
 };
 
 size_t device_workspace_bytes(const kvfs_config &cfg);

@@ -27,6 +27,8 @@ OPT_DECODE_CTAS, OPT_CHUNK_CUTOVER, OPT_DETERMINISTIC, OPT_CASCADE_MIN_ENTRIES, 
 OPT_FAULT_INJECT, OPT_TIMING, OPT_DECODE_CHUNKS = 6, 7, 8
 CTR_KERNEL_LAUNCHES, CTR_H2D_BYTES, CTR_PAGE_COPIES, CTR_LAST_DECODE_CTAS, CTR_LAST_CHUNK_UNITS = 1, 2, 3, 4, 5
 CTR_LAST_PREFIX_UNITS, CTR_LAST_PREFIX_GROUPS, CTR_HOST_PAGES, CTR_COMPACT_DEVICE_NS = 6, 7, 8, 9
+CTR_LAYER_DEVICE_NS, CTR_LAYER_TIMED = 10, 11
+CTR_HOST_RESERVE_NS, CTR_HOST_SPLIT_NS, CTR_HOST_UPLOAD_NS, CTR_HOST_LAUNCH_NS = 12, 13, 14, 15
 
 # every symbol include/kvfs.h declares (tests check the library exports all of them)
 EXPORTS = [
@@ -103,9 +105,9 @@ def lib():
             "kvfs_sched_state": (cint, [vp, P(ctypes.c_double), P(cint), P(cint)]),
             "kvfs_sched_form": (cint, [vp, ctypes.c_double, vp, cint, P(i32), i64, P(cint), P(i64)]),
             "kvfs_append": (cint, [vp, cint, i64, P(i32), vp, vp, vp]),
-            "pred_attn_batch": (cint, [vp, P(PredDesc), cint, P(i32), vp, vp, vp, vp, vp, ctypes.c_float,
-                                       P(cint), vp]),
-            "pred_step_begin": (cint, [vp, P(PredDesc), cint, P(i32), P(cint), P(vp), vp]),
+            # the per-step calls take plain addresses (ints) for every array: no ctypes pointer objects
+            "pred_attn_batch": (cint, [vp, vp, cint, vp, vp, vp, vp, vp, vp, ctypes.c_float, vp, vp]),
+            "pred_step_begin": (cint, [vp, vp, cint, vp, vp, P(vp), vp]),
             "pred_attn_layer": (cint, [vp, vp, cint, vp, vp, vp, vp, vp, ctypes.c_float, vp]),
             "pred_step_end": (cint, [vp, vp]),
             "kvfs_stat": (cint, [vp, cint, P(KvfsStat)]),
@@ -153,9 +155,11 @@ def _ptr(a: np.ndarray, ct):
     return a.ctypes.data_as(ctypes.POINTER(ct))
 
 
-def _stream(stream):
+def _stream(stream, device: int = -1):
     if stream is None:
         import torch
+        if device >= 0:  # the raw handle of the device's current stream, without a Stream object
+            return torch._C._cuda_getCurrentRawStream(device)
         return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     if isinstance(stream, int):
         return ctypes.c_void_p(stream)
@@ -164,6 +168,10 @@ def _stream(stream):
 
 def _dptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _daddr(t):
+    return None if t is None else t.data_ptr()
 
 
 class KVFS:
@@ -305,44 +313,44 @@ class KVFS:
     # ------------------------------------------------------------------ pred
     @staticmethod
     def _descs(descs):
-        """descs: list of (fd, n_q) or an int32 numpy array [n][2] (fast path, no per-item Python work)."""
+        """descs: list of (fd, n_q) or an int32 numpy array [n][2] (fast path, no per-item Python work).
+        Returns (address of the pred_desc array, n, the array to keep alive)."""
         if isinstance(descs, np.ndarray):
             a = np.ascontiguousarray(descs, dtype=np.int32).reshape(-1, 2)
-            return a.ctypes.data_as(ctypes.POINTER(PredDesc)), a.shape[0], a
-        descs = list(descs)
-        arr = (PredDesc * max(1, len(descs)))()
-        for i, (fd, nq) in enumerate(descs):
-            arr[i].fd, arr[i].n_q = fd, nq
-        return arr, len(descs), None
+        else:
+            a = np.array(list(descs), dtype=np.int32).reshape(-1, 2)
+        return (a.ctypes.data if a.shape[0] else None), a.shape[0], a
 
     def pred_attn_batch(self, descs, pos, q, k_new, v_new, out, lse=None, scale: Optional[float] = None,
                         stream=None) -> List[int]:
         """Batched pred (one layer). Returns the per-descriptor status list; raises on call-level errors."""
         arr, n, _keep = self._descs(descs)
         p = _i32(pos)
-        status = (ctypes.c_int * max(1, n))()
+        status = np.empty(max(1, n), np.int32)
         scale = float(scale if scale is not None else self.D ** -0.5)
-        rc = lib().pred_attn_batch(self._h, arr, n, _ptr(p, ctypes.c_int32), _dptr(q), _dptr(k_new), _dptr(v_new),
-                                   _dptr(out), _dptr(lse), scale, status, _stream(stream))
+        rc = _lib.pred_attn_batch(self._h, arr, n, p.ctypes.data, _daddr(q), _daddr(k_new), _daddr(v_new),
+                                  _daddr(out), _daddr(lse), scale, status.ctypes.data, _stream(stream, self.device))
         if rc not in (OK, EPARTIAL):
             raise KvfsError(rc, "pred_attn_batch")
-        return list(status[:n])
+        return status[:n].tolist()
 
     def pred_step_begin(self, descs, pos, stream=None):
         arr, n, _keep = self._descs(descs)
         p = _i32(pos)
-        status = (ctypes.c_int * max(1, n))()
+        status = np.empty(max(1, n), np.int32)
         step = ctypes.c_void_p()
-        st = _stream(stream) if self.device >= 0 else None
-        rc = lib().pred_step_begin(self._h, arr, n, _ptr(p, ctypes.c_int32), status, ctypes.byref(step), st)
+        st = _stream(stream, self.device) if self.device >= 0 else None
+        rc = _lib.pred_step_begin(self._h, arr, n, p.ctypes.data, status.ctypes.data, ctypes.byref(step), st)
         if rc not in (OK, EPARTIAL):
             raise KvfsError(rc, "pred_step_begin")
-        return step, list(status[:n])
+        return step, status[:n].tolist()
 
     def pred_attn_layer(self, step, layer, q, k_new, v_new, out, lse=None, scale=None, stream=None) -> None:
         scale = float(scale if scale is not None else self.D ** -0.5)
-        _check(lib().pred_attn_layer(self._h, step, layer, _dptr(q), _dptr(k_new), _dptr(v_new), _dptr(out),
-                                     _dptr(lse), scale, _stream(stream)), "pred_attn_layer")
+        rc = _lib.pred_attn_layer(self._h, step, layer, _daddr(q), _daddr(k_new), _daddr(v_new), _daddr(out),
+                                  _daddr(lse), scale, _stream(stream, self.device))
+        if rc != OK:
+            raise KvfsError(rc, "pred_attn_layer")
 
     def pred_step_end(self, step) -> None:
         _check(lib().pred_step_end(self._h, step), "pred_step_end")

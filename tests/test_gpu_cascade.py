@@ -109,16 +109,16 @@ def test_cascade_random_families():
     h.check_data()
 
 
-@pytest.mark.parametrize("splits", [1, 3, 8])
-def test_cascade_forced_splits(splits):
+@pytest.mark.parametrize("splits,n_root", [(1, 1300), (3, 1300), (8, 1300), (16, 1300), (13, 2400), (16, 4200)])
+def test_cascade_forced_splits(splits, n_root):
     """KVFS_OPT_PREFIX_SPLITS: any split count of the shared run gives the oracle's attention."""
     h = Harness(3000, 16, 32, 8, 128, seed=40 + splits)
     h.c.set_option(K.OPT_CASCADE_MIN_ENTRIES, 4)
     h.c.set_option(K.OPT_PREFIX_SPLITS, splits)
     with pytest.raises(Exception):
-        h.c.set_option(K.OPT_PREFIX_SPLITS, 9)
+        h.c.set_option(K.OPT_PREFIX_SPLITS, 17)
     kids = [f"k{i}" for i in range(6)]
-    _family(h, "root", 1300, kids, [0, 3, 30, 129, 1, 64], evict_root=[(100, 117)])
+    _family(h, "root", n_root, kids, [0, 3, 30, 129, 1, 64], evict_root=[(100, 117)])
     st, *_ = h.pred(_decode_rows(h, kids + ["root"]))
     assert st == [0] * 7
     assert h.c.counter(K.CTR_LAST_PREFIX_GROUPS) == 1

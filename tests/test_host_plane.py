@@ -80,7 +80,7 @@ def test_options_validate():
     for opt, good, bad in ((K.OPT_DECODE_CTAS, [0, 1, 4096], [-1, 4097]),
                            (K.OPT_CHUNK_CUTOVER, [0, 8, 1 << 20], [-1]),
                            (K.OPT_CASCADE_MIN_ENTRIES, [0, 16], [-1]),
-                           (K.OPT_PREFIX_SPLITS, [0, 1, 8], [-1, 9])):
+                           (K.OPT_PREFIX_SPLITS, [0, 1, 8, 16], [-1, 17])):
         for v in good:
             k.set_option(opt, v)
         for v in bad:

@@ -54,6 +54,23 @@ def main():
         smp = set(t2[1, 29, :n_p].tolist())
         gw, of = t2[1, 26, :n_p].astype(np.int64), t2[1, 27, :n_p].astype(np.int64)
         if (gw > 0).all() and (of > 0).all():
+            qg, s0, k0 = (t2[1, j, :n_p].astype(np.int64) for j in (20, 21, 22))
+            if (qg > 0).all() and (s0 > 0).all() and (k0 > 0).all():
+                print(f"  prefix start -> Q gathered {np.median(qg - ps[:n_p]) / 1e3:.2f} us, -> first K tile "
+                      f"{np.median(k0 - ps[:n_p]) / 1e3:.2f} us, -> first S ready {np.median(s0 - ps[:n_p]) / 1e3:.2f} us "
+                      f"(medians)")
+            g0, rr, ql = (t2[1, j, :n_p].astype(np.int64) for j in (18, 23, 19))
+            if (g0 > 0).all() and (rr > 0).all() and (ql > 0).all():
+                print(f"  gather: softmax start {np.median(g0 - ps[:n_p]) / 1e3:.2f} us, row record "
+                      f"{np.median(rr - ps[:n_p]) / 1e3:.2f} us, Q loads {np.median(ql - ps[:n_p]) / 1e3:.2f} us")
+            sw, mg = (t2[1, j, :n_p].astype(np.int64) for j in (16, 17))
+            if (sw > 0).all() and (mg > 0).all():
+                print(f"  split merge: group complete {np.median(sw - pe[:n_p]) / 1e3:.2f} us after the CTA's own end "
+                      f"(max {np.max(sw - pe[:n_p]) / 1e3:.2f}), merge {np.median(mg - sw) / 1e3:.2f} us, "
+                      f"last merged at {us(mg).max():.2f} us")
+            dn = t2[1, 25, :n_p].astype(np.int64)
+            if (dn > 0).all():
+                print(f"  prefix CTAs done at {us(dn).min():.2f}..{us(dn).max():.2f} us")
             print(f"  prefix CTA phases (medians): griddepcontrol.wait {np.median(gw - ps[:n_p]) / 1e3:.2f} us, "
                   f"Q + tiles {np.median(of - gw) / 1e3:.2f} us, epilogue {np.median(pe[:n_p] - of) / 1e3:.2f} us")
     else:

@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r2t_tests.log 2>&1; tail -3 gpurun_out/r2t_tests.log
+run() { label=$1; shift; timeout 300 python bench.py --no-cpu-baseline "$@" > gpurun_out/r2t_$label.json 2>gpurun_out/r2t_$label.err; python tools/bench_summary.py $label gpurun_out/r2t_$label.json; }
+run cfg3 --config cfg3
+run cfg2
