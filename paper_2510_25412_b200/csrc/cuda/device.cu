@@ -86,6 +86,37 @@ __global__ void upload_kernel(uint4 *dst, const uint4 *src, int64_t n16) {
     dst[i] = src[i];
 }
 
+// A pred step's metadata packet and its device-table work in ONE launch (replaces a DMA of the packet and
+// a separate prologue launch: the copy engine's latency plus a kernel boundary, ~5 us per step on B200):
+// every CTA copies a slice of the packet from mapped pinned host memory into the device upload area (the
+// later kernels of the step read it there), and the table deltas / copy-on-write pages are applied from
+// the HOST copy of the same packet (no dependency on the device copy inside this grid).
+__global__ void step_prologue_kernel(uint4 *dst, const uint4 *src, int64_t n16, const dev::SlabRun *runs, int n_runs,
+                                     const dev::Entry *run_entries, dev::Entry *slab, const dev::PageCopy *copies,
+                                     int n_copies, bf16 *const *kp, bf16 *const *vp, int L, int64_t page_elems) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n16;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+  const int run_blocks = (n_runs + 7) / 8;
+  if (static_cast<int>(blockIdx.x) < run_blocks) {
+    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (r >= n_runs) return;
+    const dev::SlabRun run = runs[r];
+    for (int i = threadIdx.x & 31; i < run.count; i += 32) slab[run.dst + i] = run_entries[run.src + i];
+    return;
+  }
+  const int b = blockIdx.x - run_blocks;
+  const int ci = b / (2 * L), rem = b % (2 * L), l = rem >> 1, isv = rem & 1;
+  if (ci >= n_copies) return;
+  const dev::PageCopy pc = copies[ci];
+  const bf16 *pool = isv ? vp[l] : kp[l];
+  const uint4 *ps = reinterpret_cast<const uint4 *>(pool + static_cast<int64_t>(pc.src) * page_elems);
+  uint4 *pd = reinterpret_cast<uint4 *>(const_cast<bf16 *>(pool) + static_cast<int64_t>(pc.dst) * page_elems);
+  const int64_t m16 = page_elems / 8;
+  for (int64_t i = threadIdx.x; i < m16; i += blockDim.x) pd[i] = ps[i];
+}
+
 // Table deltas into the slab (one warp per run) and whole-page copies (one CTA per page, layer, K|V).
 __global__ void prologue_kernel(const dev::SlabRun *runs, int n_runs, const dev::Entry *run_entries,
                                 dev::Entry *slab, const dev::PageCopy *copies, int n_copies, bf16 *const *kp,
@@ -602,6 +633,7 @@ class CudaDevice final : public Device {
     d_runs_ = push(pl.runs.data(), pl.runs.size() * sizeof(SlabRun));
     d_run_entries_ = push(pl.run_entries.data(), pl.run_entries.size() * sizeof(Entry));
     d_copies_ = push(pl.copies.data(), pl.copies.size() * sizeof(PageCopy));
+    const size_t off_runs = pending_[0].off, off_entries = pending_[1].off, off_copies = pending_[2].off;
     d_descs_ = push(pl.descs.data(), pl.descs.size() * sizeof(DevDesc));
     d_dst_ = push(pl.dst_slot.data(), pl.dst_slot.size() * sizeof(int32_t));
     d_cdescs_ = push(pl.chunk_descs.data(), pl.chunk_descs.size() * sizeof(ChunkDesc));
@@ -613,11 +645,27 @@ class CudaDevice final : public Device {
     if (!d_runs_ || !d_run_entries_ || !d_copies_ || !d_descs_ || !d_dst_ || !d_cdescs_ || !d_cunits_ || !d_cdst_ ||
         !d_pdescs_ || !d_punits_ || !d_prows_)
       return KVFS_ENOMEM;
-    if (!send(s)) return KVFS_EIO;
-    if (pl.runs.empty() && pl.copies.empty()) return KVFS_OK;
-    return launch_prologue(static_cast<const dev::SlabRun *>(d_runs_), static_cast<int>(pl.runs.size()),
-                           static_cast<const dev::Entry *>(d_run_entries_),
-                           static_cast<const dev::PageCopy *>(d_copies_), static_cast<int>(pl.copies.size()), s);
+    // one launch: packet copy (SM loads over PCIe) + table deltas + copy-on-write pages (step_prologue_kernel)
+    Staging &st = stg_[cur_];
+    if (!gather(st)) return KVFS_EIO;
+    const kvfs_config &cfg = c_.cfg;
+    const int64_t n16 = static_cast<int64_t>((used_ + 15) / 16);
+    const int n_runs = static_cast<int>(pl.runs.size()), n_copies = static_cast<int>(pl.copies.size());
+    const int work = (n_runs + 7) / 8 + n_copies * 2 * cfg.n_layers;
+    const int blocks = std::max<int>(work, static_cast<int>(std::min<int64_t>((n16 + 255) / 256, 64)));
+    if (blocks == 0) return KVFS_OK;
+    const int64_t page_elems = static_cast<int64_t>(cfg.n_kv_heads) * cfg.page_size * cfg.head_dim;
+    step_prologue_kernel<<<blocks, 256, 0, cs(s)>>>(
+        reinterpret_cast<uint4 *>(area_), reinterpret_cast<const uint4 *>(st.dev), n16,
+        reinterpret_cast<const dev::SlabRun *>(st.dev + off_runs), n_runs,
+        reinterpret_cast<const dev::Entry *>(st.dev + off_entries), slab_,
+        reinterpret_cast<const dev::PageCopy *>(st.dev + off_copies), n_copies, kptrs_, vptrs_, cfg.n_layers, page_elems);
+    ++c_.ctr.launches;
+    if (cudaGetLastError() != cudaSuccess) return KVFS_EIO;
+    if (cudaEventRecord(st.ev, cs(s)) != cudaSuccess) return KVFS_EIO;
+    st.pending = true;
+    c_.ctr.h2d_bytes += static_cast<int64_t>(used_);
+    return KVFS_OK;
   }
 
   // KVFS_OPT_TIMING: events on the stream before the layer's first kernel and after its last
@@ -945,11 +993,17 @@ class CudaDevice final : public Device {
     return area_ + off;
   }
 
-  bool send(kvfs_stream_t s) {
-    Staging &st = stg_[cur_];
+  // the packet's pieces into the pinned staging buffer
+  bool gather(Staging &st) {
     if (!grow(st, std::max<size_t>(used_, 16))) return false;
     for (const auto &p : pending_)
       if (p.bytes) std::memcpy(st.host + p.off, p.data, p.bytes);
+    return true;
+  }
+
+  bool send(kvfs_stream_t s) {
+    Staging &st = stg_[cur_];
+    if (!gather(st)) return false;
     if (used_ == 0) return true;
     const size_t n16 = (used_ + 15) / 16;
     // packets of 16 KB .. 1 MB by SM loads (measured: cfg2 / cfg4 / cfg5 steps faster, e2e +10-17%); smaller

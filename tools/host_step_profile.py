@@ -47,6 +47,10 @@ def main():
     print(cfg, "library host us per step:", " ".join(f"{a}={b:.1f}" for a, b in ph.items()))
     print(cfg, "host us per step:", " ".join(f"{a}={b:.1f}" for a, b in zip(names, acc)), f"total={acc.sum():.1f}")
     # the same with one pred_attn_batch call per step
+    from paper_2510_25412_b200 import kvfs as K
+    ctrs = (("reserve", K.CTR_HOST_RESERVE_NS), ("split+cascade", K.CTR_HOST_SPLIT_NS),
+            ("upload+prologue", K.CTR_HOST_UPLOAD_NS), ("layer launches", K.CTR_HOST_LAUNCH_NS))
+    before = {nm: kv.counter(c) for nm, c in ctrs}
     t0 = time.perf_counter()
     for it in range(n):
         q, k, v = inputs[it % 4]
@@ -58,6 +62,8 @@ def main():
     torch.cuda.synchronize()
     dev = (time.perf_counter() - t0) / n * 1e6
     print(cfg, f"pred_attn_batch loop: host {host:.1f} us per step, wall incl. drain {dev:.1f}")
+    print(cfg, "  library host us per step in that loop:",
+          " ".join(f"{nm}={(kv.counter(c) - before[nm]) / 1e3 / n:.1f}" for nm, c in ctrs))
 
 
 if __name__ == "__main__":

@@ -40,7 +40,7 @@ def main():
     rows = [(e.time_range.start, e.time_range.end, e.name[:60]) for e in evs]
     t0 = rows[0][0]
     # steps start at the upload of the step packet (a memcpy or the upload kernel)
-    starts = [i for i, r in enumerate(rows) if "Memcpy" in r[2] or "upload" in r[2]]
+    starts = [i for i, r in enumerate(rows) if "Memcpy" in r[2] or "upload" in r[2] or "step_prologue" in r[2]]
     print(f"{len(rows)} device activities over {(rows[-1][1] - t0):.1f} us for {n} steps: "
           f"{(rows[-1][1] - t0) / n:.1f} us per step")
     for si in range(min(4, len(starts) - 1)):
