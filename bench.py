@@ -957,9 +957,14 @@ def run_offload(args):
     torch.cuda.synchronize()
     nbytes = n_files * n * s.Hkv * s.D * 2 * 2
     res = {"offload": [], "restore": []}
+    kdev = {"offload": [], "restore": []}
+    kv.set_option(K.OPT_TIMING, 1)
+    sampler = ClockSampler(0)
+    sampler.start()
     for it in range(args.warmup + max(1, min(args.steps, 5))):
         for what in ("offload", "restore"):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            kv.counter(K.CTR_COPY_DEVICE_NS)  # new sum
             t0 = time.perf_counter()
             e0.record()
             for fd in fds:
@@ -968,15 +973,31 @@ def run_offload(args):
             torch.cuda.synchronize()
             if it >= args.warmup:
                 res[what].append((e0.elapsed_time(e1), 1000 * (time.perf_counter() - t0)))
+                kdev[what].append(kv.counter(K.CTR_COPY_DEVICE_NS) / 1e6)
+    sampler.stop()
     off_ms = statistics.median(a for a, _ in res["offload"])
     res_ms = statistics.median(max(a, b) for a, b in res["restore"])  # restore syncs its stream
+    k_off, k_res = statistics.median(kdev["offload"]), statistics.median(kdev["restore"])
+    pcie = 63.0  # PCIe Gen5 x16 per direction, nominal (no measured PCIe peak in MEASURED_PEAKS.json)
     line = {"metric": "KVFS host-tier offload / restore GB/s (PAPER.md P:233)", "value": nbytes / (off_ms / 1000) / 1e9,
             "unit": "GB/s", "n_gpus": 1, "steps": len(res["offload"]), "warmup": args.warmup, "higher_is_better": True,
             "dtype": "bf16", "data": "synthetic (seed 1006)",
             "config": {"workload": "32 files x 8192 tokens (8B attention shape, 32 MiB K+V each), kvfs_offload then "
                                    "kvfs_restore of every file", "bytes_each_way": nbytes},
+            "roofline": {"bound": "pcie", "achieved": nbytes / (k_off / 1000) / 1e9, "peak": pcie, "unit": "GB/s",
+                         "frac": nbytes / (k_off / 1000) / 1e9 / pcie, "kernel": "pack_kernel (K6) over mapped host memory",
+                         "peak_source": "nominal PCIe Gen5 x16 per direction (no measured PCIe peak)",
+                         "traffic": None, "kernel_ms": k_off},
+            "clocks": sampler.summary(),
             "extra": {"offload_ms": off_ms, "offload_gbs": nbytes / (off_ms / 1000) / 1e9,
                       "restore_ms": res_ms, "restore_gbs": nbytes / (res_ms / 1000) / 1e9,
+                      "offload_kernel_ms": k_off, "restore_kernel_ms": k_res,
+                      "offload_kernel_gbs": nbytes / (k_off / 1000) / 1e9,
+                      "restore_kernel_gbs": nbytes / (k_res / 1000) / 1e9,
+                      "timing": "call time: CUDA events around the kvfs_offload / kvfs_restore calls (host work "
+                                "included); kernel: events the library records around its K6 launches "
+                                "(KVFS_OPT_TIMING, KVFS_CTR_COPY_DEVICE_NS)",
+                      "cpu_baseline": "not meaningful (a host memcpy, not the method's arithmetic)",
                       "path": "page-pack kernel writing / reading pinned host memory through its mapped device address"}}
     print(json.dumps(line), flush=True)
 
@@ -1009,15 +1030,24 @@ def run_migrate(args):
         del k, v
     torch.cuda.synchronize()
     nbytes = n_files * n * s.Hkv * s.D * 2 * 2
-    pk, up = [], []
+    pk, up, kpk, kup = [], [], [], []
+    src.set_option(K.OPT_TIMING, 1)
+    dst.set_option(K.OPT_TIMING, 1)
+    sampler = ClockSampler(0)
+    sampler.start()
     for it in range(args.warmup + max(1, min(args.steps, 5))):
         e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        src.counter(K.CTR_COPY_DEVICE_NS)
+        dst.counter(K.CTR_COPY_DEVICE_NS)
         e[0].record()
         hdr, buf = src.pack(fds)
         e[1].record()
         new = dst.unpack(hdr, buf, [f"r{it}_{f}" for f in range(n_files)])
         e[2].record()
         torch.cuda.synchronize()
+        if it >= args.warmup:
+            kpk.append(src.counter(K.CTR_COPY_DEVICE_NS) / 1e6)
+            kup.append(dst.counter(K.CTR_COPY_DEVICE_NS) / 1e6)
         for nm in [f"r{it}_{f}" for f in range(n_files)]:
             dst.unlink(nm)
         for fd in new:
@@ -1026,19 +1056,28 @@ def run_migrate(args):
         if it >= args.warmup:
             pk.append(e[0].elapsed_time(e[1]))
             up.append(e[1].elapsed_time(e[2]))
+    sampler.stop()
     peak, peak_src = peaks()
     pk_ms, up_ms = statistics.median(pk), statistics.median(up)
+    kpk_ms, kup_ms = statistics.median(kpk), statistics.median(kup)
     gbs = lambda ms: 2 * nbytes / (ms / 1000) / 1e9  # read + write
     line = {"metric": "KV-file migration pack / unpack GB/s (SURVEY 8(e); one GPU, NVLink leg not measured)",
-            "value": gbs(pk_ms), "unit": "GB/s", "n_gpus": 1, "steps": len(pk), "warmup": args.warmup,
+            "value": gbs(kpk_ms), "unit": "GB/s", "n_gpus": 1, "steps": len(pk), "warmup": args.warmup,
             "higher_is_better": True, "dtype": "bf16", "data": "synthetic (seed 1007)",
             "config": {"workload": "32 files x 32768 tokens (128 MiB K+V each, 4 GiB total): kvfs_pack into one "
                                    "device buffer, kvfs_unpack into a second ctx", "bytes_moved_each": nbytes},
-            "roofline": {"bound": "hbm", "achieved": gbs(pk_ms), "peak": peak, "unit": "GB/s",
-                         "frac": gbs(pk_ms) / peak, "kernel": "pack_kernel (K6)", "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": 2 * nbytes},
-            "extra": {"pack_ms": pk_ms, "unpack_ms": up_ms, "pack_gbs": gbs(pk_ms), "unpack_gbs": gbs(up_ms),
-                      "note": "includes the host side of kvfs_pack / kvfs_unpack (page lists, R1 allocation)"}}
+            "roofline": {"bound": "hbm", "achieved": gbs(kpk_ms), "peak": peak, "unit": "GB/s",
+                         "frac": gbs(kpk_ms) / peak, "kernel": "pack_kernel (K6), device time only",
+                         "peak_source": peak_src, "algorithmic_bytes_per_launch": 2 * nbytes, "traffic": None,
+                         "kernel_ms": kpk_ms},
+            "clocks": sampler.summary(),
+            "extra": {"pack_kernel_ms": kpk_ms, "unpack_kernel_ms": kup_ms, "pack_kernel_gbs": gbs(kpk_ms),
+                      "unpack_kernel_gbs": gbs(kup_ms), "pack_call_ms": pk_ms, "unpack_call_ms": up_ms,
+                      "pack_call_gbs": gbs(pk_ms), "unpack_call_gbs": gbs(up_ms),
+                      "timing": "kernel: events the library records around its K6 launch (KVFS_OPT_TIMING, "
+                                "KVFS_CTR_COPY_DEVICE_NS); call: events around kvfs_pack / kvfs_unpack, host side "
+                                "(page lists, R1 allocation, header) included",
+                      "cpu_baseline": "not meaningful (a memcpy, not the method's arithmetic)"}}
     print(json.dumps(line), flush=True)
 
 

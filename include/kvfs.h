@@ -378,7 +378,10 @@ typedef enum {
   KVFS_CTR_HOST_RESERVE_NS = 12,
   KVFS_CTR_HOST_SPLIT_NS = 13,
   KVFS_CTR_HOST_UPLOAD_NS = 14,
-  KVFS_CTR_HOST_LAUNCH_NS = 15
+  KVFS_CTR_HOST_LAUNCH_NS = 15,
+  KVFS_CTR_COPY_DEVICE_NS = 16     /* KVFS_OPT_TIMING: summed device time (ns) of the whole-page pack /
+                                      unpack kernel launches (kvfs_pack, kvfs_unpack, kvfs_offload,
+                                      kvfs_restore) since the previous read (reading waits for them) */
 } kvfs_counter;
 int kvfs_get_counter(kvfs_ctx *ctx, int counter, int64_t *value);
 

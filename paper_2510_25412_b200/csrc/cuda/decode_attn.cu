@@ -43,11 +43,14 @@ struct DecodeCfg {
   // An SM's TMA bandwidth grows with the number of independent producer streams (tools/bw_probe.cu:
   // 1 stream/SM ~2.5 TB/s, 3-4 streams/SM ~6.4-6.9 TB/s), so the rings are what feeds HBM; one CTA of
   // 12 warps lets setmaxnreg move registers from the 4-warp producer warpgroup to the 8 consumers.
-  static constexpr int NSTAGES_RAW = 49152 / STAGE_BYTES;
-  static constexpr int NSTAGES = NSTAGES_RAW < 2 ? 2 : (NSTAGES_RAW > 8 ? 8 : NSTAGES_RAW);
+#ifndef KVFS_K1_NW
+#define KVFS_K1_NW 2
+#endif
+  static constexpr int NW = KVFS_K1_NW;          // consumer warps per ring (8 / NW rings per CTA)
+  static constexpr int NSTAGES_RAW = 49152 / 2 * NW / STAGE_BYTES;  // 48 KiB of stages per 2 consumer warps
+  static constexpr int NSTAGES = NSTAGES_RAW < NW ? NW : (NSTAGES_RAW > 16 ? 16 : NSTAGES_RAW);
   // NW <= NSTAGES is required: a warp never waits on a ring slot more than one phase ahead (mbarrier
   // parity waits are ambiguous beyond that).
-  static constexpr int NW = 2;                   // consumer warps per ring
   static constexpr int THREADS = 12 * 32;        // producer warpgroup (4 warps) + 2 consumer warpgroups
   static constexpr int PRODUCER_REGS = 56, CONSUMER_REGS = 224;
   static constexpr int NQ = 4;                   // Q ring slots
@@ -56,7 +59,7 @@ struct DecodeCfg {
                                         (2 * NSTAGES + 2 * NQ + 4) * 8 + 16 + 16;
   static constexpr int RING_BYTES = (RING_BYTES_RAW + 127) / 128 * 128;
   static constexpr int R_RAW = 232448 / RING_BYTES;  // 227 KB of dynamic shared memory per CTA
-  static constexpr int R = R_RAW > 4 ? 4 : R_RAW;    // rings per CTA
+  static constexpr int R = R_RAW > 8 / NW ? 8 / NW : R_RAW;  // rings per CTA
   static_assert(LPK * KG == 32 && SUB % KG == 0 && P % SUB == 0 && NW <= NSTAGES && NW * R <= 8 && R >= 1, "layout");
 };
 
@@ -142,7 +145,7 @@ __device__ __forceinline__ Segment make_segment(const Desc *descs, int n_desc, i
 // a merge of S prefix splits costs ceil(S / SG) L2 round trips (not one per element and split).
 template <int D, int G, int NT>
 struct MergeMap {
-  static constexpr int TPH = NT / G;  // threads per head
+  static constexpr int TPH = NT / G > D ? D : NT / G;  // threads per head (threads past G TPH idle)
   static constexpr int DPT = D / TPH;  // dims per thread
   static constexpr int SG = DPT >= 16 ? 4 : (DPT >= 8 ? 8 : 16);
   static_assert(NT % G == 0 && D % TPH == 0 && DPT >= 1, "merge map");
@@ -669,12 +672,15 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
                             : nullptr;
     using MM = MergeMap<D, G, NW * 32>;
     const int mh = tid / MM::TPH, md0 = (tid % MM::TPH) * MM::DPT;
+    const bool mlive = mh < G;
     if (whole) {
       float M, L, acc[MM::DPT];
+      if (mlive) {
       fold_comb<D, MM::DPT, NW, C::PART>(comb, mh, md0, M, L, acc);
       if (pref) fold_records<D, MM::DPT, MM::SG>(pref + mh * (D + 2), C::PART, dd.pref_splits, md0, M, L, acc);
       const int64_t orow = row * p.Hq + sg.g * G + mh;
       store_out<MM::DPT>(p.out + orow * D + md0, p.lse ? p.lse + orow : nullptr, md0, M, L, acc);
+      }
       named_bar_sync(1 + ring, NW * 32);
     } else {
       // partial of this CTA's piece of the unit
@@ -708,7 +714,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
         if (prev == c1 - c0) p.counters[unit] = 0;  // self-cleaning for the next launch
       }
       named_bar_sync(1 + ring, NW * 32);
-      if (*flag) {
+      if (*flag && mlive) {
         __threadfence();
         const int64_t ua = sg.ubeg, ub = sg.ubeg + sg.spu;
         const int c0 = cta_of(ua, p), c1 = cta_of(ub - 1, p);

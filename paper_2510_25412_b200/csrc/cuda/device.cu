@@ -407,10 +407,11 @@ class CudaDevice final : public Device {
       cudaFreeHost(b.host);
     }
     for (auto &kv : host_sizes_) cudaFreeHost(kv.first);
-    for (auto &t : layer_timing_) {
-      cudaEventDestroy(t.first);
-      cudaEventDestroy(t.second);
-    }
+    for (auto *v : {&layer_timing_, &copy_timing_})
+      for (auto &t : *v) {
+        cudaEventDestroy(t.first);
+        cudaEventDestroy(t.second);
+      }
     for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
   }
 
@@ -681,17 +682,20 @@ class CudaDevice final : public Device {
     return rc;
   }
 
-  int64_t take_layer_ns(int64_t *n) override {
+  int64_t take_layer_ns(int64_t *n) override { return take_pairs(layer_timing_, n); }
+  int64_t take_copy_ns(int64_t *n) override { return take_pairs(copy_timing_, n); }
+
+  int64_t take_pairs(std::vector<std::pair<cudaEvent_t, cudaEvent_t>> &v, int64_t *n) {
     double ms = 0;
-    for (auto &t : layer_timing_) {
+    for (auto &t : v) {
       float x = 0.f;
       if (cudaEventSynchronize(t.second) == cudaSuccess && cudaEventElapsedTime(&x, t.first, t.second) == cudaSuccess)
         ms += x;
       ev_pool_.push_back(t.first);
       ev_pool_.push_back(t.second);
     }
-    *n = static_cast<int64_t>(layer_timing_.size());
-    layer_timing_.clear();
+    *n = static_cast<int64_t>(v.size());
+    v.clear();
     return static_cast<int64_t>(ms * 1e6);
   }
 
@@ -883,11 +887,22 @@ class CudaDevice final : public Device {
     const kvfs_config &cfg = c_.cfg;
     const int64_t page_elems = static_cast<int64_t>(cfg.n_kv_heads) * cfg.page_size * cfg.head_dim;
     const int64_t blocks = static_cast<int64_t>(pages.size()) * cfg.n_layers * 2;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c_.opt_timing) {  // KVFS_CTR_COPY_DEVICE_NS: the K6 kernel alone (no host work, no packet upload)
+      e0 = pooled_event();
+      e1 = pooled_event();
+      if (!e0 || !e1) return KVFS_EIO;
+      cudaEventRecord(e0, cs(s));
+    }
     pack_kernel<<<static_cast<unsigned>(blocks), 256, 0, cs(s)>>>(static_cast<const uint32_t *>(dp),
                                                                   static_cast<int>(pages.size()), kptrs_, vptrs_,
                                                                   cfg.n_layers, page_elems, static_cast<bf16 *>(buf),
                                                                   unpack);
     ++c_.ctr.launches;
+    if (e1) {
+      cudaEventRecord(e1, cs(s));
+      copy_timing_.push_back({e0, e1});
+    }
     return cudaGetLastError() == cudaSuccess ? KVFS_OK : KVFS_EIO;
   }
 
@@ -1093,6 +1108,7 @@ class CudaDevice final : public Device {
   int per_sm_ = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timing_;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> layer_timing_;  // KVFS_OPT_TIMING: per pred layer
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> copy_timing_;   // KVFS_OPT_TIMING: per K6 launch
   std::vector<cudaEvent_t> ev_pool_;
   int64_t k5_grid_ = 0;
   Staging stg_[4];

@@ -765,6 +765,11 @@ int kvfs_get_counter(kvfs_ctx *ctx, int counter, int64_t *value) {
         return KVFS_OK;
       }
       case KVFS_CTR_LAYER_TIMED: *value = c.last_layer_timed; return KVFS_OK;
+      case KVFS_CTR_COPY_DEVICE_NS: {
+        int64_t n = 0;
+        *value = c.dev ? c.dev->take_copy_ns(&n) : 0;
+        return KVFS_OK;
+      }
       case KVFS_CTR_HOST_RESERVE_NS: *value = c.ctr.host_reserve_ns; return KVFS_OK;
       case KVFS_CTR_HOST_SPLIT_NS: *value = c.ctr.host_split_ns; return KVFS_OK;
       case KVFS_CTR_HOST_UPLOAD_NS: *value = c.ctr.host_upload_ns; return KVFS_OK;

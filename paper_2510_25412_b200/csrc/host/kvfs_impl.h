@@ -303,6 +303,8 @@ class Device {
   // KVFS_OPT_TIMING: summed device time of the pred layers recorded since the last call (waits for them);
   // *n = how many
   virtual int64_t take_layer_ns(int64_t *n) = 0;
+  // KVFS_OPT_TIMING: summed device time of the page pack / unpack kernels (K6) since the last call
+  virtual int64_t take_copy_ns(int64_t *n) = 0;
 };
 
 size_t device_workspace_bytes(const kvfs_config &cfg);

@@ -29,6 +29,7 @@ CTR_KERNEL_LAUNCHES, CTR_H2D_BYTES, CTR_PAGE_COPIES, CTR_LAST_DECODE_CTAS, CTR_L
 CTR_LAST_PREFIX_UNITS, CTR_LAST_PREFIX_GROUPS, CTR_HOST_PAGES, CTR_COMPACT_DEVICE_NS = 6, 7, 8, 9
 CTR_LAYER_DEVICE_NS, CTR_LAYER_TIMED = 10, 11
 CTR_HOST_RESERVE_NS, CTR_HOST_SPLIT_NS, CTR_HOST_UPLOAD_NS, CTR_HOST_LAUNCH_NS = 12, 13, 14, 15
+CTR_COPY_DEVICE_NS = 16
 
 # every symbol include/kvfs.h declares (tests check the library exports all of them)
 EXPORTS = [
