@@ -51,6 +51,9 @@ def parse():
                          "-1 = library default)")
     ap.add_argument("--decode-ctas", type=int, default=0,
                     help="tuning: decode-kernel ring count (KVFS_OPT_DECODE_CTAS; 0 = auto)")
+    ap.add_argument("--fused-scores", action="store_true",
+                    help="with --scores / --real-scores: the decode kernel writes its logits into a registered buffer "
+                         "(kvfs_set_logits_buffer) and the score pass reads them (K10) instead of K (K9)")
     ap.add_argument("--scores", action="store_true",
                     help="also run pred_attn_scores (NEXT-2, H2O score accumulation) every timed step")
     ap.add_argument("--migrate", action="store_true",
@@ -435,6 +438,8 @@ def run_ours(args):
     scores_buf = None
     if args.scores:
         scores_buf = torch.empty(int((wl.lens + wl.n_q).sum()) + T + 16, dtype=torch.float32, device="cuda")
+        if args.fused_scores:
+            kv.set_logits_buffer(logits_buffer(wl, Kst))
     alg_bytes, alg_flops, logical = [], [], []
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
@@ -629,11 +634,22 @@ def run_ours(args):
     if args.scores:
         sc_ms = statistics.mean(a.elapsed_time(b) for a, b in zip(ev1, ev2))
         k_bytes = statistics.mean(logical) / 2
-        line["extra"]["scores"] = {
-            "kernel": "scores_kernel (K9, H2O attention-score accumulation, second pass over K)",
-            "ms_mean": sc_ms, "k_bytes_per_step": k_bytes, "gbs": k_bytes / (sc_ms / 1000.0) / 1e9,
-            "frac_of_peak": k_bytes / (sc_ms / 1000.0) / 1e9 / peak,
-            "overhead_vs_attention": sc_ms / k_ms}
+        if args.fused_scores:
+            # K10 reads the logits (Hq fp32 per key and row) and the lse; K1 wrote them during the attention
+            n_fused = kv.counter(K.CTR_LAST_FUSED_SCORES)
+            lg_bytes = int(statistics.mean(float((ln + wl.n_q).sum()) for ln in lens_seen)) * wl.n_q * s.Hq * 4
+            line["extra"]["scores"] = {
+                "kernel": "logit_scores_kernel (K10, fused H2O scores from the decode kernel's logits)",
+                "fused_descriptors": n_fused, "ms_mean": sc_ms, "logit_bytes_per_step": lg_bytes,
+                "gbs": lg_bytes / (sc_ms / 1000.0) / 1e9, "frac_of_peak": lg_bytes / (sc_ms / 1000.0) / 1e9 / peak,
+                "overhead_vs_attention": sc_ms / k_ms,
+                "note": "the attention kernel time (roofline.kernel_ms_mean) includes writing the logits"}
+        else:
+            line["extra"]["scores"] = {
+                "kernel": "scores_kernel (K9, H2O attention-score accumulation, second pass over K)",
+                "ms_mean": sc_ms, "k_bytes_per_step": k_bytes, "gbs": k_bytes / (sc_ms / 1000.0) / 1e9,
+                "frac_of_peak": k_bytes / (sc_ms / 1000.0) / 1e9 / peak,
+                "overhead_vs_attention": sc_ms / k_ms}
     if e2e:
         line["e2e"] = e2e
     if world == 1 and not args.no_cpu_baseline:
@@ -641,6 +657,17 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def logits_buffer(wl, steps: int):
+    """Device buffer for the fused scores (include/kvfs.h kvfs_set_logits_buffer): 4 Hq P n_q (entries + ceil(n_q / P))
+    bytes per descriptor, sized for the longest files of the run (`steps` more tokens per file)."""
+    import torch
+
+    s = wl.shape
+    ent = (wl.lens + steps * wl.n_q + s.P - 1) // s.P + 1 + (wl.n_q + s.P - 1) // s.P
+    floats = int((ent * s.P).sum()) * wl.n_q * s.Hq
+    return torch.empty(floats + 64, dtype=torch.float32, device="cuda")
 
 
 def evict_ranges_heavy_hitter(seed: int, f: int, n: int, drop: int, sink: int = 4, recent: int = 1024):
@@ -689,6 +716,9 @@ def run_heavy_hitter(args):
         lse0 = torch.empty((n_files, s.Hq), dtype=torch.float32, device=dev)
         n1 = L0 + 1
         sc = torch.empty(n_files * n1, dtype=torch.float32, device=dev)
+        if args.fused_scores:  # K1 writes the logits, K10 sums them (kvfs_set_logits_buffer)
+            kv.set_logits_buffer(torch.empty(n_files * (L0 // s.P + 2) * s.P * s.Hq + 64, dtype=torch.float32,
+                                             device=dev))
         step, st = kv.pred_step_begin(descs, np.full(n_files, L0, dtype=np.int32))
         assert st == [0] * n_files
         kv.pred_attn_layer(step, 0, q, k1, v1, out0, lse0)
@@ -699,6 +729,8 @@ def run_heavy_hitter(args):
         kv.pred_step_end(step)
         torch.cuda.synchronize()
         scores_ms = e0.elapsed_time(e1)
+        n_fused = kv.counter(K.CTR_LAST_FUSED_SCORES)
+        kv.set_logits_buffer(None)
         sch = sc.view(n_files, n1).cpu().numpy().astype(np.float64)
         t0 = time.perf_counter()
         from synth.workloads import lowest_score_ranges
@@ -706,7 +738,9 @@ def run_heavy_hitter(args):
         for f, fd in enumerate(fds):
             kv.evict(fd, lowest_score_ranges(sch[f], L0 // 2))
         host_sel_s = time.perf_counter() - t0
-        scores_info = {"kernel": "scores_kernel (K9) over 128 x 65537 tokens", "scores_ms": scores_ms,
+        scores_info = {"kernel": ("logit_scores_kernel (K10, fused: the decode kernel's logits)" if n_fused else
+                                  "scores_kernel (K9)") + " over 128 x 65537 tokens", "scores_ms": scores_ms,
+                       "fused_descriptors": n_fused,
                        "k_gbs": n_files * n1 * s.Hkv * s.D * 2 / (scores_ms / 1000) / 1e9,
                        "host_select_and_evict_s": host_sel_s,
                        "score_sum_check": float(sch.sum() / (n_files * s.Hq))}  # = 1 (softmax weights)

@@ -210,6 +210,16 @@ int pred_step_end(kvfs_ctx *ctx, pred_step *step);
  * or no step is open. */
 int pred_attn_scores(kvfs_ctx *ctx, pred_step *step, int layer, const void *q, const float *lse, float scale,
                      float *scores, const int64_t *score_off, kvfs_stream_t stream);
+/* Fused scores (same result as above, ~16x fewer bytes for decode descriptors).  Registers a caller-owned
+ * device buffer (16-byte aligned; NULL or 0 bytes = off).  While registered, every pred_attn_layer's decode
+ * kernel also writes the scaled logit of every key it attends, per head, for each descriptor it attends in
+ * full (not chunk descriptors, not shared-prefix cascade members) that still fits in the buffer: a
+ * descriptor takes 4 * Hq * P * n_q * (entries before the call + ceil(n_q / P)) bytes, in batch order.  A
+ * pred_attn_scores for the most recent pred_attn_layer's layer then sums exp(logit - lse) from the buffer
+ * for those descriptors (kernel K10) and falls back to the pass over K (K9) for the others.  The buffer must
+ * stay valid until pred_step_end.  EBUSY while a step is open; EINVAL for a host-only ctx or a misaligned
+ * buffer. */
+int kvfs_set_logits_buffer(kvfs_ctx *ctx, void *buf, size_t bytes);
 
 /* ---------------------------------------------------------------- introspection (tests, policies) */
 typedef struct {
@@ -379,9 +389,11 @@ typedef enum {
   KVFS_CTR_HOST_SPLIT_NS = 13,
   KVFS_CTR_HOST_UPLOAD_NS = 14,
   KVFS_CTR_HOST_LAUNCH_NS = 15,
-  KVFS_CTR_COPY_DEVICE_NS = 16     /* KVFS_OPT_TIMING: summed device time (ns) of the whole-page pack /
+  KVFS_CTR_COPY_DEVICE_NS = 16,    /* KVFS_OPT_TIMING: summed device time (ns) of the whole-page pack /
                                       unpack kernel launches (kvfs_pack, kvfs_unpack, kvfs_offload,
                                       kvfs_restore) since the previous read (reading waits for them) */
+  KVFS_CTR_LAST_FUSED_SCORES = 17  /* descriptors the last pred_attn_scores served from the decode kernel's
+                                      logits (K10); the rest went through K9 */
 } kvfs_counter;
 int kvfs_get_counter(kvfs_ctx *ctx, int counter, int64_t *value);
 

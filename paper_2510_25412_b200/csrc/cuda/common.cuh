@@ -30,6 +30,9 @@ struct Desc {  // == kvfs::DevDesc
   int32_t skip;         // leading entries attended by the shared-prefix kernel
   int32_t pref_splits;  // shared-prefix partials per unit (0: none)
   int32_t pref_base;    // partial of unit (g, qi), split s: pref_base + (g * n_q + qi) * pref_splits + s
+  int64_t logit_off;    // >= 0: fused-scores logits of unit (g, qi), stage st, slot s, head h at
+                        // logit_off + (((g * n_q + qi) * stages_per_unit + st) * P + s) * G + h; -1: none
+  int64_t pad;
 };
 
 struct SlabRun {

@@ -514,6 +514,12 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
       const StageMeta m = meta[slot];
       const __nv_bfloat16 *ks = reinterpret_cast<const __nv_bfloat16 *>(stage_data + slot * C::STAGE_BYTES);
       const __nv_bfloat16 *vs = ks + P * D;
+      // fused scores: this stage's scaled logits (log2 domain) of every visible key, per head, for the score
+      // pass (pred_attn_scores reads them instead of re-reading K)
+      float *lg = nullptr;
+      if (p.logits != nullptr && dd.logit_off >= 0)
+        lg = p.logits + dd.logit_off +
+             (static_cast<int64_t>(sg.g * dd.n_q + sg.qi) * dd.stages_per_unit + (sg.st0 + i)) * (P * G);
       // one softmax sub-block of SUB slots; FULL = every slot is a visible key (the common case: no
       // per-key predicates or divergent branches)
       auto sub_block = [&](auto full_tag, const uint32_t sbm, const int sb) {
@@ -556,6 +562,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
           float sc = v[0];
 #pragma unroll
           for (int o = SPH / 2; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
+          if (lg != nullptr && valid && (sub % SPH) == 0) lg[slot_k * G + hm] = sc;
           s[it] = FULL ? sc : (valid ? sc : -CUDART_INF_F);
           smax = fmaxf(smax, s[it]);
         }

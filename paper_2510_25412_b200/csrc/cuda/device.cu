@@ -579,6 +579,21 @@ class CudaDevice final : public Device {
     return static_cast<int64_t>(ms * 1e6);
   }
 
+  int logit_scores(const std::vector<LogitDesc> &descs, const std::vector<ScoreUnit> &units, const float *lse,
+                   float *out, kvfs_stream_t s) override {
+    begin_packet(/*scratch=*/true);
+    const void *dd = push(descs.data(), descs.size() * sizeof(LogitDesc));
+    const void *du = push(units.data(), units.size() * sizeof(ScoreUnit));
+    if (!dd || !du) return KVFS_ENOMEM;
+    if (!send(s)) return KVFS_EIO;
+    const kvfs_config &cfg = c_.cfg;
+    const cudaError_t e = dev::launch_logit_scores(static_cast<const dev::ScoreUnit *>(du), static_cast<int>(units.size()),
+                                                   static_cast<const dev::LogitDesc *>(dd), slab_, c_.logits_buf, lse,
+                                                   out, cfg.n_q_heads, cfg.n_kv_heads, cfg.page_size, cs(s));
+    ++c_.ctr.launches;
+    return e == cudaSuccess ? KVFS_OK : KVFS_EIO;
+  }
+
   int scores(const std::vector<ScoreDesc> &descs, const std::vector<ScoreUnit> &units, int layer, const void *q,
              const float *lse, float scale, float *out, kvfs_stream_t s) override {
     begin_packet(/*scratch=*/true);  // the open step's plan in the upload area must survive (later layers)
@@ -765,6 +780,7 @@ class CudaDevice final : public Device {
     p.ppart = ppart_;
     p.wait_at_start = pl.prefix_units.empty() ? 1 : 0;
     p.counters = counters_;
+    p.logits = c_.logits_buf;
     p.Hq = cfg.n_q_heads;
     p.Hkv = cfg.n_kv_heads;
     // always a programmatic dependent launch: after the prologue (waits at start) or after the shared-prefix

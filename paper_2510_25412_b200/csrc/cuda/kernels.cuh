@@ -31,6 +31,7 @@ struct DecodeParams {
   const float *ppart;  // shared-prefix partials [..][PART] (Desc::pref_*)
   int wait_at_start;   // 1: griddepcontrol.wait before reading the tables (programmatic launch after the prologue)
   int *counters;     // [n_units]
+  float *logits;     // fused scores: descriptors with logit_off >= 0 get their logits written here (else null)
   int Hq, Hkv;
 };
 
@@ -57,6 +58,14 @@ struct ScoreDesc {  // == kvfs::ScoreDesc
 struct ScoreUnit {  // == kvfs::ScoreUnit
   int32_t desc, e0, e1, l0;
 };
+struct LogitDesc {  // == kvfs::LogitDesc
+  int64_t out_off, logit_off;
+  int32_t slab_off, n_q, row0, n_old, n_old_entries, stages_per_unit;
+};
+// Fused scores (K10): scores of the descriptors whose keys the decode kernel scored, from its logits.
+cudaError_t launch_logit_scores(const ScoreUnit *units, int n_units, const LogitDesc *descs, const Entry *slab,
+                                const float *logits, const float *lse, float *out, int Hq, int Hkv, int P,
+                                cudaStream_t s);
 // kmap: the layer's K pool as a 2-D map [n_pages * Hkv * P rows][D], box 64 dims x 16 rows, 128-byte swizzle
 cudaError_t launch_scores(const CUtensorMap &kmap, const ScoreUnit *units, int n_units, const ScoreDesc *descs,
                           const Entry *slab, const __nv_bfloat16 *q, const float *lse, float scale_log2, float *out,

@@ -230,3 +230,83 @@ cudaError_t launch_scores(const CUtensorMap &kmap, const ScoreUnit *units, int n
 
 }  // namespace dev
 }  // namespace kvfs
+
+namespace kvfs {
+namespace dev {
+
+// K10: fused scores.  The decode kernel (K1) wrote, for every key it attended, the scaled logit s (log2
+// domain) of each head (DevDesc::logit_off); the score of retained token k of descriptor d is then
+//   sum_{rows qi of d that see k} sum_{kv heads g, heads h of g} exp2(s[g, qi][k][h] - lse[qi][g G + h] log2 e)
+// (rule H1), reading Hq floats per (key, row) instead of the K row (Hkv D bf16): ~16x fewer bytes than K9.
+// One CTA per (descriptor, <= 32 final-table entries); thread per (entry, slot).  The key's place in K1's
+// stage layout: an old token (logical < n_old) sits at stage = its entry, slot = its slot; new row r at stage
+// n_old_entries + r / P, slot r % P, visible to the rows qi >= r.
+__global__ void __launch_bounds__(256) logit_scores_kernel(const ScoreUnit *units, const LogitDesc *descs,
+                                                           const Entry *slab, const float *logits, const float *lse,
+                                                           float *out, int Hq, int Hkv, int P) {
+  __shared__ uint64_t emask[32];
+  __shared__ int32_t elog[32];
+  const ScoreUnit u = units[blockIdx.x];
+  const LogitDesc d = descs[u.desc];
+  const int ne = u.e1 - u.e0, G = Hq / Hkv;
+  if (threadIdx.x < 32) {
+    const int e = threadIdx.x;
+    const uint64_t m = e < ne ? slab[d.slab_off + u.e0 + e].mask : 0ull;
+    const int pc = __popcll(m);
+    int incl = pc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (e >= o) incl += y;
+    }
+    emask[e] = m;
+    elog[e] = u.l0 + incl - pc;
+  }
+  __syncthreads();
+  constexpr float kLog2e = 1.4426950408889634f;
+  for (int j = threadIdx.x; j < ne * P; j += blockDim.x) {
+    const int e = j / P, sl = j % P;
+    const uint64_t m = emask[e];
+    if (!((m >> sl) & 1ull)) continue;
+    const int k = elog[e] + __popcll(m & ((1ull << sl) - 1ull));
+    int st, slot, q0;
+    if (k < d.n_old) {
+      st = u.e0 + e;
+      slot = sl;
+      q0 = 0;
+    } else {
+      const int r = k - d.n_old;
+      st = d.n_old_entries + r / P;
+      slot = r % P;
+      q0 = r;
+    }
+    float acc = 0.f;
+    for (int g = 0; g < Hkv; ++g)
+      for (int qi = q0; qi < d.n_q; ++qi) {
+        const float *lg = logits + d.logit_off +
+                          ((static_cast<int64_t>(g * d.n_q + qi) * d.stages_per_unit + st) * P + slot) * G;
+        const float *ls = lse + static_cast<int64_t>(d.row0 + qi) * Hq + g * G;
+        if ((G & 3) == 0) {
+          for (int h = 0; h < G; h += 4) {  // 16-byte aligned: logit_off and every stride are multiples of 4
+            const float4 x = __ldcs(reinterpret_cast<const float4 *>(lg + h));
+            acc += fast_exp2(x.x - __ldg(ls + h) * kLog2e) + fast_exp2(x.y - __ldg(ls + h + 1) * kLog2e) +
+                   fast_exp2(x.z - __ldg(ls + h + 2) * kLog2e) + fast_exp2(x.w - __ldg(ls + h + 3) * kLog2e);
+          }
+        } else {
+          for (int h = 0; h < G; ++h) acc += fast_exp2(__ldcs(lg + h) - __ldg(ls + h) * kLog2e);
+        }
+      }
+    out[d.out_off + k] = acc;
+  }
+}
+
+cudaError_t launch_logit_scores(const ScoreUnit *units, int n_units, const LogitDesc *descs, const Entry *slab,
+                                const float *logits, const float *lse, float *out, int Hq, int Hkv, int P,
+                                cudaStream_t s) {
+  if (n_units <= 0) return cudaSuccess;
+  logit_scores_kernel<<<n_units, 256, 0, s>>>(units, descs, slab, logits, lse, out, Hq, Hkv, P);
+  return cudaGetLastError();
+}
+
+}  // namespace dev
+}  // namespace kvfs

@@ -91,6 +91,7 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
           int64_t fne = idx < 0 ? 0 : idx;  // entry holding logical token n_old
           if (idx >= 0 && f->table[idx].lstart + __builtin_popcountll(f->table[idx].mask) <= n_old) fne = idx + 1;
           DevDesc d{};
+          d.logit_off = -1;
           d.cost_begin = pl.total_cost;
           d.slab_off = static_cast<int32_t>(f->slab_off);
           d.n_old_entries = static_cast<int32_t>(idx + 1);
@@ -105,6 +106,7 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
           d.first_new_lstart = f->table[fne].lstart;
           pl.descs.push_back(d);
           pl.desc_files.push_back(f);
+          f->score_slot = static_cast<int32_t>(pl.score_src.size());
           pl.score_src.push_back({i, d.slab_off, nq, d.row0, f});
           pl.total_cost += static_cast<int64_t>(Hkv) * nq * d.stages_per_unit;
           pl.n_units += Hkv * nq;
@@ -319,6 +321,36 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, 
     cost += static_cast<int64_t>(Hkv) * d.n_q * d.stages_per_unit;
   }
   pl.total_cost = cost;
+}
+
+}  // namespace kvfs
+
+namespace kvfs {
+
+// Fused scores: logits space in the caller's buffer for every descriptor the decode kernel attends in full
+// (not a chunk descriptor, no shared-prefix skip), in descriptor order while it fits; the others keep the
+// K9 score pass.  Unit (g, qi) of descriptor d takes stages_per_unit * P * G floats.
+void pred_logits(Ctx &c, PredPlan *plan) {
+  PredPlan &pl = *plan;
+  const int P = c.cfg.page_size, Hkv = c.cfg.n_kv_heads, G = c.cfg.n_q_heads / c.cfg.n_kv_heads;
+  int64_t off = 0;
+  for (size_t i = 0; i < pl.descs.size(); ++i) {
+    DevDesc &d = pl.descs[i];
+    d.logit_off = -1;
+    if (!c.logits_buf || d.skip != 0) continue;
+    const int64_t need = static_cast<int64_t>(Hkv) * d.n_q * d.stages_per_unit * P * G;
+    if (off + need > c.logits_cap) continue;
+    d.logit_off = off;
+    off += need;
+    const File *f = pl.desc_files[i];
+    if (f->score_slot >= 0 && f->score_slot < static_cast<int32_t>(pl.score_src.size())) {
+      ScoreSrc &x = pl.score_src[static_cast<size_t>(f->score_slot)];
+      x.logit_off = d.logit_off;
+      x.n_old = d.n_old;
+      x.n_old_entries = d.n_old_entries;
+      x.stages_per_unit = d.stages_per_unit;
+    }
+  }
 }
 
 }  // namespace kvfs

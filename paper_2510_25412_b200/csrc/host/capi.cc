@@ -459,6 +459,7 @@ int pred_step_begin(kvfs_ctx *ctx, const pred_desc *descs, int n_desc, const int
       pred_split(c, c.opt_chunk_cutover, &c.plan);
       pred_cascade(c, c.opt_cascade_min_entries, c.opt_prefix_splits, c.dev->sms(), c.dev->prefix_partial_capacity(),
                    &c.plan);
+      pred_logits(c, &c.plan);
       const int64_t t2 = now_ns();
       c.ctr.host_split_ns += t2 - t1;
       const int drc = c.dev->pred_begin(c.plan, stream);
@@ -487,6 +488,7 @@ int pred_attn_layer(kvfs_ctx *ctx, pred_step *step, int layer, const void *q, co
     if (layer < 0 || layer >= c.cfg.n_layers || !(scale > 0.f)) return KVFS_EINVAL;
     if (c.plan.T > 0 && (!q || !k_new || !v_new || !out)) return KVFS_EINVAL;
     const int64_t t0 = now_ns();
+    c.logits_layer = c.logits_buf ? layer : -1;  // the decode kernel (over)writes this layer's logits
     const int rc = c.dev->pred_layer(c.plan, layer, q, k_new, v_new, out, lse, scale, stream);
     c.ctr.host_launch_ns += now_ns() - t0;
     if (rc != KVFS_OK) c.poisoned = true;
@@ -508,16 +510,30 @@ int pred_attn_scores(kvfs_ctx *ctx, pred_step *step, int layer, const void *q, c
     if (c.plan.score_src.empty()) return KVFS_OK;
     if (!q || !lse || !scores || !score_off) return KVFS_EINVAL;
     std::vector<ScoreDesc> sd;
-    std::vector<ScoreUnit> su;
+    std::vector<ScoreUnit> su, lu;
+    std::vector<LogitDesc> ld;
+    // descriptors whose keys the decode kernel scored for this layer: fused pass over its logits (K10);
+    // the others (chunk descriptors, shared-prefix members, no buffer, another layer): K9 over K
+    const bool fused = c.logits_buf && c.logits_layer == layer;
     for (const ScoreSrc &x : c.plan.score_src) {
       const File &f = *x.file;
+      const int32_t ne = static_cast<int32_t>(f.table.size());
+      if (fused && x.logit_off >= 0) {
+        const int32_t di = static_cast<int32_t>(ld.size());
+        ld.push_back({score_off[x.batch_idx], x.logit_off, x.slab_off, x.n_q, x.row0, x.n_old, x.n_old_entries,
+                      x.stages_per_unit});
+        for (int32_t e0 = 0; e0 < ne; e0 += 32) lu.push_back({di, e0, std::min(ne, e0 + 32), f.table[e0].lstart});
+        continue;
+      }
       const int32_t di = static_cast<int32_t>(sd.size());
       sd.push_back({x.slab_off, x.n_q, x.row0, static_cast<int32_t>(f.len), score_off[x.batch_idx]});
-      const int32_t ne = static_cast<int32_t>(f.table.size());
       for (int32_t e0 = 0; e0 < ne; e0 += KVFS_SCORE_UNIT_ENTRIES)
         su.push_back({di, e0, std::min(ne, e0 + KVFS_SCORE_UNIT_ENTRIES), f.table[e0].lstart});
     }
-    const int rc = c.dev->scores(sd, su, layer, q, lse, scale, scores, stream);
+    int rc = KVFS_OK;
+    c.ctr.last_fused_scores = static_cast<int64_t>(ld.size());
+    if (!ld.empty()) rc = c.dev->logit_scores(ld, lu, lse, scores, stream);
+    if (rc == KVFS_OK && !sd.empty()) rc = c.dev->scores(sd, su, layer, q, lse, scale, scores, stream);
     if (rc != KVFS_OK) c.poisoned = true;
     return rc;
   });
@@ -702,6 +718,19 @@ int kvfs_unpack(kvfs_ctx *ctx, const void *buf_dev, size_t buf_bytes, const void
   });
 }
 
+int kvfs_set_logits_buffer(kvfs_ctx *ctx, void *buf, size_t bytes) {
+  return guarded(ctx, [&]() -> int {
+    KVFS_LOCK_OR(ctx);
+    if (!c.dev) return KVFS_EINVAL;
+    if (c.step_open) return KVFS_EBUSY;
+    if (buf && (reinterpret_cast<uintptr_t>(buf) & 15)) return KVFS_EINVAL;
+    c.logits_buf = (buf && bytes >= 16) ? static_cast<float *>(buf) : nullptr;
+    c.logits_cap = c.logits_buf ? static_cast<int64_t>(bytes / 16) * 4 : 0;
+    c.logits_layer = -1;
+    return KVFS_OK;
+  });
+}
+
 int kvfs_set_option(kvfs_ctx *ctx, int option, int64_t value) {
   return guarded(ctx, [&]() -> int {
     KVFS_LOCK_OR(ctx);
@@ -770,6 +799,7 @@ int kvfs_get_counter(kvfs_ctx *ctx, int counter, int64_t *value) {
         *value = c.dev ? c.dev->take_copy_ns(&n) : 0;
         return KVFS_OK;
       }
+      case KVFS_CTR_LAST_FUSED_SCORES: *value = c.ctr.last_fused_scores; return KVFS_OK;
       case KVFS_CTR_HOST_RESERVE_NS: *value = c.ctr.host_reserve_ns; return KVFS_OK;
       case KVFS_CTR_HOST_SPLIT_NS: *value = c.ctr.host_split_ns; return KVFS_OK;
       case KVFS_CTR_HOST_UPLOAD_NS: *value = c.ctr.host_upload_ns; return KVFS_OK;

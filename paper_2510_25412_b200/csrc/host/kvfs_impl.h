@@ -52,6 +52,7 @@ struct File {
   size_t dirty_from = 0;
   std::vector<uint32_t> dirty_pts;
   int64_t batch_tag = -1;  // pred batch id that last used the file (EBUSY detection)
+  int32_t score_slot = -1; // index of its ScoreSrc in the current pred plan (fused-scores bookkeeping)
   // R15 host tier: while offloaded, entries with page & KVFS_HOST_PAGE live in host_buf (pinned, mapped;
   // host_dev = its device address), slot order = table order
   bool offloaded = false;
@@ -98,8 +99,12 @@ struct DevDesc {
   int32_t pref_base;         // first shared-prefix partial of unit (g = 0, qi = 0): unit (g, qi) split s is
                              // partial pref_base + (g * n_q + qi) * pref_splits + s (the cascade writes one
                              // merged partial per unit: pref_splits = 1)
+  int64_t logit_off;         // >= 0: the decode kernel writes the scaled logits of this descriptor's keys for
+                             // the fused scores (kvfs_set_logits_buffer); unit (g, qi), stage st, slot s, head h
+                             // at logit_off + (((g * n_q + qi) * stages_per_unit + st) * P + s) * G + h.  -1: none
+  int64_t pad;
 };
-static_assert(sizeof(DevDesc) == 64, "DevDesc must be 64 bytes");
+static_assert(sizeof(DevDesc) == 80, "DevDesc must be 80 bytes");
 
 struct SlabRun {
   int64_t dst;    // first slab entry written
@@ -142,6 +147,14 @@ struct ScoreUnit {
 struct ScoreSrc {
   int32_t batch_idx, slab_off, n_q, row0;
   File *file;
+  // fused scores: the decode kernel's logits of this descriptor (logit_off >= 0), with the layout numbers
+  int64_t logit_off = -1;
+  int32_t n_old = 0, n_old_entries = 0, stages_per_unit = 0;
+};
+// Fused-scores pass (pred_attn_scores over the decode kernel's logits, include/kvfs.h kvfs_set_logits_buffer)
+struct LogitDesc {
+  int64_t out_off, logit_off;
+  int32_t slab_off, n_q, row0, n_old, n_old_entries, stages_per_unit;
 };
 struct PrefixRow {
   int32_t t;          // packed row (Q row) of the query token
@@ -187,6 +200,7 @@ struct CtxCounters {
   int64_t launches = 0, h2d_bytes = 0, page_copies = 0, last_decode_ctas = 0, last_chunk_units = 0,
           last_prefix_units = 0, last_prefix_groups = 0, host_pages = 0;
   int64_t host_reserve_ns = 0, host_split_ns = 0, host_upload_ns = 0, host_launch_ns = 0;
+  int64_t last_fused_scores = 0;
 };
 
 struct Ctx {
@@ -202,6 +216,11 @@ struct Ctx {
   std::atomic<bool> broken{false};  // a C++ exception escaped a call (capi.cc guarded): every call is EIO
   int64_t fault_countdown = 0;       // KVFS_OPT_FAULT_INJECT (tests)
   bool step_open = false;
+  // Fused scores (kvfs_set_logits_buffer): caller-owned device buffer for the decode kernel's logits, and the
+  // layer whose logits it holds (pred_attn_scores uses them only for that layer; else the K9 pass)
+  float *logits_buf = nullptr;
+  int64_t logits_cap = 0;  // floats
+  int logits_layer = -1;
   int64_t batch_counter = 0;
   int64_t opt_decode_ctas = 0;
   int64_t opt_decode_chunks = 0;  // KVFS_OPT_DECODE_CHUNKS (0: static scheduling)
@@ -269,6 +288,7 @@ void pred_split(const Ctx &c, int64_t cutover, PredPlan *plan);
 // `sms` sizes the key splits, `max_partials` is the workspace capacity in partials.
 // force_splits > 0: key splits per shared run (else chosen from the SM count)
 void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, int64_t max_partials, PredPlan *plan);
+void pred_logits(Ctx &c, PredPlan *plan);
 
 // ---- data plane interface (implemented in csrc/cuda/device.cu)
 class Device {
@@ -285,6 +305,9 @@ class Device {
   virtual int pred_begin(PredPlan &plan, kvfs_stream_t s) = 0;
   virtual int pred_layer(const PredPlan &plan, int layer, const void *q, const void *k_new, const void *v_new,
                          void *out, float *lse, float scale, kvfs_stream_t s) = 0;
+  // fused scores (K10) of the descriptors whose logits the decode kernel wrote
+  virtual int logit_scores(const std::vector<LogitDesc> &descs, const std::vector<ScoreUnit> &units,
+                           const float *lse, float *out, kvfs_stream_t s) = 0;
   virtual int scores(const std::vector<ScoreDesc> &descs, const std::vector<ScoreUnit> &units, int layer,
                      const void *q, const float *lse, float scale, float *out, kvfs_stream_t s) = 0;
   // pinned, device-mapped host memory for the host tier (R15)

@@ -29,7 +29,7 @@ CTR_KERNEL_LAUNCHES, CTR_H2D_BYTES, CTR_PAGE_COPIES, CTR_LAST_DECODE_CTAS, CTR_L
 CTR_LAST_PREFIX_UNITS, CTR_LAST_PREFIX_GROUPS, CTR_HOST_PAGES, CTR_COMPACT_DEVICE_NS = 6, 7, 8, 9
 CTR_LAYER_DEVICE_NS, CTR_LAYER_TIMED = 10, 11
 CTR_HOST_RESERVE_NS, CTR_HOST_SPLIT_NS, CTR_HOST_UPLOAD_NS, CTR_HOST_LAUNCH_NS = 12, 13, 14, 15
-CTR_COPY_DEVICE_NS = 16
+CTR_COPY_DEVICE_NS, CTR_LAST_FUSED_SCORES = 16, 17
 
 # every symbol include/kvfs.h declares (tests check the library exports all of them)
 EXPORTS = [
@@ -40,7 +40,7 @@ EXPORTS = [
     "kvfs_get_table", "kvfs_get_positions", "kvfs_get_refcounts", "kvfs_free_pages", "kvfs_read",
     "kvfs_audit", "kvfs_set_option", "kvfs_get_counter", "kvfs_pack", "kvfs_unpack", "kvfs_extract",
     "kvfs_merge", "kvfs_sched_create", "kvfs_sched_destroy", "kvfs_sched_enqueue", "kvfs_sched_state",
-    "kvfs_sched_form", "pred_attn_scores", "kvfs_offload", "kvfs_restore",
+    "kvfs_sched_form", "pred_attn_scores", "kvfs_offload", "kvfs_restore", "kvfs_set_logits_buffer",
 ]
 
 
@@ -111,6 +111,7 @@ def lib():
             "pred_step_begin": (cint, [vp, vp, cint, vp, vp, P(vp), vp]),
             "pred_attn_layer": (cint, [vp, vp, cint, vp, vp, vp, vp, vp, ctypes.c_float, vp]),
             "pred_step_end": (cint, [vp, vp]),
+            "kvfs_set_logits_buffer": (cint, [vp, vp, ctypes.c_size_t]),
             "kvfs_stat": (cint, [vp, cint, P(KvfsStat)]),
             "kvfs_get_table": (cint, [vp, cint, P(ctypes.c_uint32), P(ctypes.c_uint64), i64, P(i64)]),
             "kvfs_get_positions": (cint, [vp, cint, P(i32), i64, P(i64)]),
@@ -355,6 +356,14 @@ class KVFS:
 
     def pred_step_end(self, step) -> None:
         _check(lib().pred_step_end(self._h, step), "pred_step_end")
+
+    def set_logits_buffer(self, buf) -> None:
+        """Fused scores (include/kvfs.h kvfs_set_logits_buffer): a device tensor the decode kernel writes its
+        logits into (None = off).  Keep it alive while registered."""
+        self._logits = buf
+        _check(_lib.kvfs_set_logits_buffer(self._h, None if buf is None else buf.data_ptr(),
+                                           0 if buf is None else buf.numel() * buf.element_size()),
+               "set_logits_buffer")
 
     def pred_attn_scores(self, step, layer, q, lse, scores, score_off, scale=None, stream=None) -> None:
         """Accumulated softmax weight per retained token (H2O; include/kvfs.h pred_attn_scores): after

@@ -79,12 +79,16 @@ def test_outlier_channels_every_kernel(D, Hq, Hkv, k_e, q_e, v_e):
     h.check_data()
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("D,Hq,Hkv", [(128, 32, 8), (64, 8, 2)])
-def test_outlier_channels_scores(D, Hq, Hkv):
+def test_outlier_channels_scores(D, Hq, Hkv, fused):
     """K9 under peaked softmaxes: the per-key relative bound of DESIGN.md (tests/gpu_harness.py::scores_rtol)
     still holds when the logits span tens of units."""
     ch = _channels(D)
     h = Harness(3000, 16, Hq, Hkv, D, seed=77 + D, outliers=(ch, 3, 2, 0))
+    if fused:
+        logits = torch.empty(8 << 20, dtype=torch.float32, device="cuda")
+        h.c.set_logits_buffer(logits)
     h.open("a")
     h.append("a", list(range(900)))
     h.evict("a", [(10, 50)])

@@ -15,11 +15,17 @@ from oracle.bf16 import bf16_to_f64  # noqa: E402
 from paper_2510_25412_b200 import kvfs as K  # noqa: E402
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("P,Hq,Hkv,D", [(16, 32, 8, 128), (32, 8, 2, 64), (64, 16, 2, 128), (16, 8, 8, 128),
                                         (16, 16, 8, 64), (32, 8, 1, 128)])
-def test_scores_match_oracle(P, Hq, Hkv, D):
+def test_scores_match_oracle(P, Hq, Hkv, D, fused):
+    """fused: the decode kernel writes its logits (kvfs_set_logits_buffer) and the decode descriptors' scores
+    come from them (K10); chunk descriptors and cascade members still go through K9 in the same call."""
     h = Harness(4000, P, Hq, Hkv, D, seed=P + Hq + D)
     h.c.set_option(K.OPT_CASCADE_MIN_ENTRIES, 2)
+    if fused:
+        logits = torch.empty(16 << 20, dtype=torch.float32, device="cuda")
+        h.c.set_logits_buffer(logits)
     h.open("r")
     h.append("r", list(range(700)))
     h.evict("r", [(5, 40), (300, 333)])
@@ -29,8 +35,11 @@ def test_scores_match_oracle(P, Hq, Hkv, D):
         h.append(f"k{i}", list(range(last + 1, last + 1 + 50 * i + 3)))
     h.open("big")
     h.append("big", list(range(2000)))
+    h.open("solo")
+    h.append("solo", list(range(333)))
+    h.evict("solo", [(30, 41)])
     rows = []
-    for name, nq in (("k0", 1), ("k1", 1), ("k2", 3), ("big", 20 if D == 128 else 5), ("r", 1)):
+    for name, nq in (("k0", 1), ("k1", 1), ("k2", 3), ("big", 20 if D == 128 else 5), ("r", 1), ("solo", 1)):
         last = h.o.stat(h.fds[name][1])[2]
         rows.append((name, list(range(last + 1, last + 1 + nq))))
     rows.append(("k0", [99999]))  # EBUSY: ignored by the scores
@@ -53,6 +62,10 @@ def test_scores_match_oracle(P, Hq, Hkv, D):
     h.c.pred_attn_scores(step, 0, qd, lse, scores, off, scale)
     h.c.pred_step_end(step)
     torch.cuda.synchronize()
+    n_fused = h.c.counter(K.CTR_LAST_FUSED_SCORES)
+    assert (n_fused > 0) == fused, n_fused  # "solo" (and for D 64 every descriptor) is a plain decode descriptor
+    if fused and D == 64:
+        assert n_fused == 6
     st_o, out_o, lse_o, sc_o = h.o.pred_batch(descs_o, pos, q, k, v, scale, scores=True)
     assert st == st_o and st[-1] == -16
     sc = scores.cpu().numpy()
@@ -73,14 +86,18 @@ def test_scores_match_oracle(P, Hq, Hkv, D):
     assert len(sc) == off[-1]  # nothing was written past the successful descriptors' ranges
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("P,Hq,Hkv,D", [(16, 32, 8, 128), (32, 8, 2, 64)])
-def test_scores_between_layers(P, Hq, Hkv, D):
+def test_scores_between_layers(P, Hq, Hkv, D, fused):
     """pred_attn_scores after layer l of an OPEN multi-layer step, then pred_attn_layer for
     layer l + 1 (the per-layer H2O order).  The scores packet must not overwrite the step's uploaded plan
     (descriptors, destination slots): every layer's output, lse, scores and pool bits equal the oracle's."""
     L = 3
     h = Harness(3000, P, Hq, Hkv, D, L=L, seed=11 + P + D)
     h.c.set_option(K.OPT_CASCADE_MIN_ENTRIES, 2)
+    if fused:  # each layer's logits overwrite the previous layer's; scores follow every layer
+        logits = torch.empty(8 << 20, dtype=torch.float32, device="cuda")
+        h.c.set_logits_buffer(logits)
     h.open("r")
     h.append("r", list(range(500)))
     h.evict("r", [(7, 29)])
