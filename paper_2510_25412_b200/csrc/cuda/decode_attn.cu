@@ -55,12 +55,26 @@ struct DecodeCfg {
   static constexpr int PRODUCER_REGS = 56, CONSUMER_REGS = 224;
   static constexpr int NQ = 4;                   // Q ring slots
   static constexpr int PART = part_floats(G, D);  // floats per partial (o, m, l per head, 16-byte padded)
+  static constexpr int KDEF = kDecodeRecSlots;   // workspace records per range; deferred merges per ring
   static constexpr int RING_BYTES_RAW = NSTAGES * STAGE_BYTES + NQ * G * D * 2 + NW * PART * 4 + NSTAGES * 16 +
-                                        (2 * NSTAGES + 2 * NQ + 4) * 8 + 16 + 16;
+                                        (2 * NSTAGES + 2 * NQ + 4) * 8 + 32 + KDEF * 32;
   static constexpr int RING_BYTES = (RING_BYTES_RAW + 127) / 128 * 128;
   static constexpr int R_RAW = 232448 / RING_BYTES;  // 227 KB of dynamic shared memory per CTA
   static constexpr int R = R_RAW > 8 / NW ? 8 / NW : R_RAW;  // rings per CTA
   static_assert(LPK * KG == 32 && SUB % KG == 0 && P % SUB == 0 && NW <= NSTAGES && NW * R <= 8 && R >= 1, "layout");
+};
+
+// A segment of a unit whose final merge waits for the shared-prefix grid (Desc::pref_splits != 0): its record
+// is in the partials workspace, and the arrival count, the merge and the wait run only when the ring has
+// streamed its range (flush_deferred), so the ring never stalls on the prefix kernel (or on a fence) between
+// two of its segments.
+struct Deferred {
+  int64_t ubeg;   // global stage index of the unit's first stage
+  int32_t d;      // descriptor
+  int32_t unit;   // Desc::unit_base + g * n_q + qi
+  int32_t rslot;  // >= 0: a whole unit, its record in slot rslot of the range; -1: a piece (slot 0 / 1)
+  int32_t merge;  // flush: this ring merges the unit
+  int32_t pad[2];
 };
 
 struct StageMeta {
@@ -462,6 +476,18 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
   const int kg = lane / LPK, sub = lane % LPK;
   const int hm = sub / SPH;
   int local0 = 0, segi = 0;
+  // merge map: consumer thread ctid owns head mh, dims md0 .. md0 + DPT of a unit's output
+  const int ctid = warp * 32 + lane;
+  using MM = MergeMap<D, G, NW * 32>;
+  const int mh = ctid / MM::TPH, md0 = (ctid % MM::TPH) * MM::DPT;
+  const bool mlive = mh < G;
+  int *ndef = flag + 2, *ndw = flag + 3;  // deferred merges pending / of which whole-unit records
+  Deferred *dlist = reinterpret_cast<Deferred *>(flag + 8);
+  if (ctid == 0) {
+    *ndef = 0;
+    *ndw = 0;
+  }
+  named_bar_sync(1 + ring, NW * 32);
   for (int k = 0;; ++k) {
   int cta = (k == 0) ? pr : p.ncta;
   if (p.dynamic) {
@@ -472,6 +498,66 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
   }
   if (cta >= p.ncta) break;
   const int64_t beg = cta_start(cta, p), end = cta_start(cta + 1, p);
+  // Final output of one unit (threads with mlive): its record(s) in the workspace -- the whole unit's record
+  // `wrec` (index), or else the pieces of the rings covering it in range order (deterministic) -- then the
+  // shared-prefix record(s), if any.
+  auto merge_unit = [&](int64_t ua, int spu, int64_t row, int g, int64_t wrec, const float *pref, int nsplit) {
+    float M = -CUDART_INF_F, L = 0.f, acc[MM::DPT];
+#pragma unroll
+    for (int i = 0; i < MM::DPT; ++i) acc[i] = 0.f;
+    if (wrec >= 0) {
+      fold_records<D, MM::DPT, 1>(p.partials + wrec * C::PART + mh * (D + 2), 0, 1, md0, M, L, acc);
+    } else {
+      const int c0 = cta_of(ua, p), c1 = cta_of(ua + spu - 1, p);
+      for (int c = c0; c <= c1; ++c) {
+        const int wh = (cta_start(c, p) >= ua) ? 0 : 1;
+        fold_records<D, MM::DPT, 1>(p.partials + (static_cast<int64_t>(c) * C::KDEF + wh) * C::PART + mh * (D + 2),
+                                    0, 1, md0, M, L, acc);
+      }
+    }
+    if (pref) fold_records<D, MM::DPT, MM::SG>(pref + mh * (D + 2), C::PART, nsplit, md0, M, L, acc);
+    const int64_t orow = row * p.Hq + g * G + mh;
+    store_out<MM::DPT>(p.out + orow * D + md0, p.lse ? p.lse + orow : nullptr, md0, M, L, acc);
+  };
+  // The deferred merges (units with a shared prefix): one griddepcontrol.wait for the prefix grid, then each
+  // unit's records + its prefix record.  Called by every consumer thread of the ring (uniform).
+  auto flush_deferred = [&]() {
+    const int n = *ndef;
+    if (n == 0) return;
+    if (ctid == 0) K1T(6, pr);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (ctid == 0) K1T(7, pr);
+    __threadfence();  // this ring's piece records before its arrivals
+    named_bar_sync(1 + ring, NW * 32);
+    if (ctid < n) {  // one thread per entry: the arrivals in parallel
+      Deferred &df = dlist[ctid];
+      df.merge = 1;
+      if (df.rslot < 0) {  // a piece: the last of the unit's rings to arrive merges it
+        const int spu = p.descs[df.d].stages_per_unit;
+        const int c0 = cta_of(df.ubeg, p), c1 = cta_of(df.ubeg + spu - 1, p);
+        const int prev = atomicAdd(p.counters + df.unit, 1);
+        df.merge = (prev == c1 - c0) ? 1 : 0;
+        if (df.merge) p.counters[df.unit] = 0;  // self-cleaning for the next launch
+      }
+      __threadfence();
+    }
+    named_bar_sync(1 + ring, NW * 32);
+    for (int j = 0; j < n; ++j) {
+      const Deferred df = dlist[j];
+      if (!df.merge || !mlive) continue;
+      const Desc &du = p.descs[df.d];
+      const int ui = df.unit - du.unit_base, g = ui / du.n_q, qi = ui - g * du.n_q;
+      const float *pref = p.ppart + (static_cast<int64_t>(du.pref_base) + static_cast<int64_t>(ui) * du.pref_splits) * C::PART;
+      merge_unit(df.ubeg, du.stages_per_unit, du.row0 + qi, g,
+                 df.rslot >= 0 ? static_cast<int64_t>(cta) * C::KDEF + df.rslot : -1, pref, du.pref_splits);
+    }
+    named_bar_sync(1 + ring, NW * 32);
+    if (ctid == 0) {
+      *ndef = 0;
+      *ndw = 0;
+    }
+    named_bar_sync(1 + ring, NW * 32);
+  };
   int64_t x = beg;
   bool first_seg = true;
   int dhint = -1;
@@ -664,35 +750,41 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
     named_bar_sync(1 + ring, NW * 32);
 
     const bool whole = (sg.st0 == 0) && (sg.nst == sg.spu);
-    const int tid = warp * 32 + lane;  // 0 .. NW*32-1 within the ring
+    const int tid = ctid;
     const int unit = dd.unit_base + sg.g * dd.n_q + sg.qi;
-    const int64_t row = dd.row0 + sg.qi;
-    // shared-prefix partials of this unit (written by the prefix kernel earlier on the stream; with a
-    // programmatic dependent launch this kernel may be running alongside it: wait for its completion here,
-    // after streaming this unit's own keys)
-    if (warp == 0 && lane == 0) K1T(6, pr);
-    if (dd.pref_splits) asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (warp == 0 && lane == 0) K1T(7, pr);
-    const float *pref = dd.pref_splits
-                            ? p.ppart + (static_cast<int64_t>(dd.pref_base) +
-                                         static_cast<int64_t>(sg.g * dd.n_q + sg.qi) * dd.pref_splits) * C::PART
-                            : nullptr;
-    using MM = MergeMap<D, G, NW * 32>;
-    const int mh = tid / MM::TPH, md0 = (tid % MM::TPH) * MM::DPT;
-    const bool mlive = mh < G;
-    if (whole) {
+    // A unit with a shared-prefix partial (written by the prefix kernel launched before this one; with a
+    // programmatic dependent launch this kernel runs alongside it) is merged only after griddepcontrol.wait.
+    // Waiting here, between two segments, would stall the ring's streaming until the prefix grid completed,
+    // so the unit's record goes to the workspace and its merge is deferred to the end of the ring's range.
+    // (The range's last segment has nothing streaming behind it: it waits and merges in place.)
+    const bool defer = dd.pref_splits != 0 && x + sg.nst < end;
+    const float *pref = dd.pref_splits ? p.ppart + (static_cast<int64_t>(dd.pref_base) +
+                                                    static_cast<int64_t>(sg.g * dd.n_q + sg.qi) * dd.pref_splits) *
+                                                       C::PART
+                                       : nullptr;
+    if (whole && !defer) {
+      if (pref) {
+        if (ctid == 0) K1T(6, pr);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (ctid == 0) K1T(7, pr);
+      }
       float M, L, acc[MM::DPT];
       if (mlive) {
-      fold_comb<D, MM::DPT, NW, C::PART>(comb, mh, md0, M, L, acc);
-      if (pref) fold_records<D, MM::DPT, MM::SG>(pref + mh * (D + 2), C::PART, dd.pref_splits, md0, M, L, acc);
-      const int64_t orow = row * p.Hq + sg.g * G + mh;
-      store_out<MM::DPT>(p.out + orow * D + md0, p.lse ? p.lse + orow : nullptr, md0, M, L, acc);
+        fold_comb<D, MM::DPT, NW, C::PART>(comb, mh, md0, M, L, acc);
+        if (pref) fold_records<D, MM::DPT, MM::SG>(pref + mh * (D + 2), C::PART, dd.pref_splits, md0, M, L, acc);
+        const int64_t orow = (dd.row0 + sg.qi) * p.Hq + sg.g * G + mh;
+        store_out<MM::DPT>(p.out + orow * D + md0, p.lse ? p.lse + orow : nullptr, md0, M, L, acc);
       }
       named_bar_sync(1 + ring, NW * 32);
     } else {
-      // partial of this CTA's piece of the unit
-      const int which = first_seg ? 0 : 1;
-      float *part = p.partials + (static_cast<int64_t>(cta) * 2 + which) * C::PART;
+      // record of this segment: a piece of a unit cut by a range boundary (slot 0: the range's first segment,
+      // slot 1: its last) or a whole deferred unit (slots 2 ..)
+      int rslot = first_seg ? 0 : 1;
+      if (whole) {
+        if (*ndw == C::KDEF - 2) flush_deferred();  // no free slot: merge what is pending now
+        rslot = 2 + *ndw;
+      }
+      float *part = p.partials + (static_cast<int64_t>(cta) * C::KDEF + rslot) * C::PART;
       for (int e = tid; e < G * (D + 2); e += NW * 32) {
         const int h = e / (D + 2), dim = e % (D + 2);
         float M = -CUDART_INF_F;
@@ -711,39 +803,48 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
         }
         part[e] = acc;
       }
-      __threadfence();
-      named_bar_sync(1 + ring, NW * 32);
-      if (tid == 0) {
-        const int64_t ua = sg.ubeg, ub = sg.ubeg + sg.spu;
-        const int c0 = cta_of(ua, p), c1 = cta_of(ub - 1, p);
-        const int prev = atomicAdd(p.counters + unit, 1);
-        *flag = (prev == c1 - c0) ? 1 : 0;
-        if (prev == c1 - c0) p.counters[unit] = 0;  // self-cleaning for the next launch
-      }
-      named_bar_sync(1 + ring, NW * 32);
-      if (*flag && mlive) {
-        __threadfence();
-        const int64_t ua = sg.ubeg, ub = sg.ubeg + sg.spu;
-        const int c0 = cta_of(ua, p), c1 = cta_of(ub - 1, p);
-        float M = -CUDART_INF_F, L = 0.f, acc[MM::DPT];
-#pragma unroll
-        for (int i = 0; i < MM::DPT; ++i) acc[i] = 0.f;
-        for (int c = c0; c <= c1; ++c) {  // the unit's pieces in range order (deterministic)
-          const int wh = (cta_start(c, p) >= ua) ? 0 : 1;
-          fold_records<D, MM::DPT, 1>(p.partials + (static_cast<int64_t>(c) * 2 + wh) * C::PART + mh * (D + 2), 0, 1,
-                                      md0, M, L, acc);
+      if (defer) {  // record only: arrival, wait and merge at the end of the range (flush_deferred)
+        named_bar_sync(1 + ring, NW * 32);
+        if (tid == 0) {
+          Deferred &df = dlist[*ndef];
+          df.ubeg = sg.ubeg;
+          df.d = sg.d;
+          df.unit = unit;
+          df.rslot = whole ? rslot : -1;
+          *ndef += 1;
+          if (whole) *ndw += 1;
         }
-        if (pref) fold_records<D, MM::DPT, MM::SG>(pref + mh * (D + 2), C::PART, dd.pref_splits, md0, M, L, acc);
-        const int64_t orow = row * p.Hq + sg.g * G + mh;
-        store_out<MM::DPT>(p.out + orow * D + md0, p.lse ? p.lse + orow : nullptr, md0, M, L, acc);
+        named_bar_sync(1 + ring, NW * 32);
+      } else {  // a piece at the end of the range: the last of the unit's rings to arrive merges it now
+        __threadfence();
+        named_bar_sync(1 + ring, NW * 32);
+        if (tid == 0) {
+          const int64_t ua = sg.ubeg, ub = sg.ubeg + sg.spu;
+          const int c0 = cta_of(ua, p), c1 = cta_of(ub - 1, p);
+          const int prev = atomicAdd(p.counters + unit, 1);
+          *flag = (prev == c1 - c0) ? 1 : 0;
+          if (prev == c1 - c0) p.counters[unit] = 0;  // self-cleaning for the next launch
+        }
+        named_bar_sync(1 + ring, NW * 32);
+        if (*flag) {
+          if (pref) {
+            if (ctid == 0) K1T(6, pr);
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            if (ctid == 0) K1T(7, pr);
+          }
+          __threadfence();
+          if (mlive) merge_unit(sg.ubeg, sg.spu, dd.row0 + sg.qi, sg.g, -1, pref, dd.pref_splits);
+        }
+        named_bar_sync(1 + ring, NW * 32);
       }
-      named_bar_sync(1 + ring, NW * 32);
+      if (*ndef == C::KDEF) flush_deferred();
     }
     x += sg.nst;
     local0 += sg.nst;
     ++segi;
     first_seg = false;
   }
+  flush_deferred();
   }
   if (warp == 0 && lane == 0) K1T(4, pr);
 }

@@ -59,7 +59,7 @@ WsLayout ws_layout(const kvfs_config &c) {
   w.pgroup = off;
   off = align256(off + 2 * static_cast<size_t>(kMaxPrefixGroups) * 4);
   w.partials = off;
-  off = align256(off + static_cast<size_t>(kMaxCtas) * 2 * part);
+  off = align256(off + static_cast<size_t>(kMaxCtas) * dev::kDecodeRecSlots * part);
   w.ptrs = off;
   off = align256(off + static_cast<size_t>(c.n_layers) * 2 * sizeof(void *));
   // shared-prefix (cascade) partials: one merged partial per decode unit + up to kMaxPrefixSplits split
@@ -745,6 +745,11 @@ class CudaDevice final : public Device {
     p.total = pl.total_cost;
     if (per_sm_ == 0) per_sm_ = dev::decode_ctas_per_sm(cfg.head_dim, cfg.n_q_heads / cfg.n_kv_heads, cfg.page_size);
     int64_t ncta = c_.opt_decode_ctas > 0 ? c_.opt_decode_ctas : static_cast<int64_t>(sms_) * per_sm_;
+    if (c_.opt_decode_ctas <= 0 && !pl.prefix_units.empty() && pl.decode_sms > 0) {
+      // the shared-prefix grid (one CTA per SM, launched first) holds the other SMs for most of the step: the
+      // decode rings go to the free ones, so none of them starts late (pred_cascade chose the split)
+      ncta = static_cast<int64_t>(pl.decode_sms) * per_sm_;
+    }
     if (c_.opt_decode_ctas <= 0 && pl.n_units > 0 && pl.n_units <= ncta) {
       // Few units (e.g. the short private suffixes of a fork family after the shared prefix went to the
       // cascade): one ring per unit when the units are about equally long, so no unit is cut by a range

@@ -7,6 +7,9 @@
 namespace kvfs {
 namespace dev {
 
+// K1 workspace records per ring range (DecodeCfg::KDEF): 2 cut-unit pieces + 2 deferred whole units
+constexpr int kDecodeRecSlots = 4;
+
 // Floats of one partial record (o, m, l) of a unit's G heads: G (D + 2) rounded up to 16 bytes, so records
 // can be moved by 1-D TMA bulk copies (head h at h (D + 2))
 __host__ __device__ constexpr int part_floats(int G, int D) { return (G * (D + 2) + 3) & ~3; }
@@ -27,7 +30,7 @@ struct DecodeParams {
   float *lse;
   __nv_bfloat16 *kpool, *vpool;
   float scale_log2;  // scale * log2(e)
-  float *partials;   // [ncta][2][PART]
+  float *partials;   // [ncta][kDecodeRecSlots][PART] (K1 records: range pieces, deferred whole units)
   const float *ppart;  // shared-prefix partials [..][PART] (Desc::pref_*)
   int wait_at_start;   // 1: griddepcontrol.wait before reading the tables (programmatic launch after the prologue)
   int *counters;     // [n_units]

@@ -281,21 +281,39 @@ __global__ void __launch_bounds__(256) logit_scores_kernel(const ScoreUnit *unit
       q0 = r;
     }
     float acc = 0.f;
-    for (int g = 0; g < Hkv; ++g)
-      for (int qi = q0; qi < d.n_q; ++qi) {
-        const float *lg = logits + d.logit_off +
-                          ((static_cast<int64_t>(g * d.n_q + qi) * d.stages_per_unit + st) * P + slot) * G;
-        const float *ls = lse + static_cast<int64_t>(d.row0 + qi) * Hq + g * G;
-        if ((G & 3) == 0) {
-          for (int h = 0; h < G; h += 4) {  // 16-byte aligned: logit_off and every stride are multiples of 4
-            const float4 x = __ldcs(reinterpret_cast<const float4 *>(lg + h));
-            acc += fast_exp2(x.x - __ldg(ls + h) * kLog2e) + fast_exp2(x.y - __ldg(ls + h + 1) * kLog2e) +
-                   fast_exp2(x.z - __ldg(ls + h + 2) * kLog2e) + fast_exp2(x.w - __ldg(ls + h + 3) * kLog2e);
+    // unit (g, qi) of the key: its G logits at lg0 + (g * n_q + qi) * ustride
+    const int64_t ustride = static_cast<int64_t>(d.stages_per_unit) * P * G;
+    const float *lg0 = logits + d.logit_off + (static_cast<int64_t>(st) * P + slot) * G;
+    for (int qi = q0; qi < d.n_q; ++qi) {
+      const float *ls = lse + static_cast<int64_t>(d.row0 + qi) * Hq;  // head g G + h of row qi
+      if ((G & 3) == 0) {
+        // the row's Hq logits as Hq / 4 float4 (16-byte aligned: logit_off and every stride are multiples
+        // of 4), 8 loads in flight per thread
+        const int nv = Hq >> 2;
+        for (int j0 = 0; j0 < nv; j0 += 8) {
+          float4 x[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int j = j0 + t, g = (4 * j) / G, h = (4 * j) - g * G;
+            if (j < nv) x[t] = __ldcs(reinterpret_cast<const float4 *>(lg0 + (g * d.n_q + qi) * ustride + h));
           }
-        } else {
-          for (int h = 0; h < G; ++h) acc += fast_exp2(__ldcs(lg + h) - __ldg(ls + h) * kLog2e);
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const int j = j0 + t;
+            if (j < nv) {
+              const float *l = ls + 4 * j;
+              acc += fast_exp2(x[t].x - __ldg(l) * kLog2e) + fast_exp2(x[t].y - __ldg(l + 1) * kLog2e) +
+                     fast_exp2(x[t].z - __ldg(l + 2) * kLog2e) + fast_exp2(x[t].w - __ldg(l + 3) * kLog2e);
+            }
+          }
+        }
+      } else {
+        for (int g = 0; g < Hkv; ++g) {
+          const float *lg = lg0 + (g * d.n_q + qi) * ustride;
+          for (int h = 0; h < G; ++h) acc += fast_exp2(__ldcs(lg + h) - __ldg(ls + g * G + h) * kLog2e);
         }
       }
+    }
     out[d.out_off + k] = acc;
   }
 }

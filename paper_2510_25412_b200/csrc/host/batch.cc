@@ -44,6 +44,7 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
   pl.prefix_rows.clear();
   pl.prefix_partials = 0;
   pl.prefix_groups = 0;
+  pl.decode_sms = 0;
   std::vector<int32_t> dst;
   int64_t row = 0;
   bool partial = false;
@@ -270,11 +271,56 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, 
     rows_all += u.rows;
   }
   const int64_t fit = std::max<int64_t>(1, sms / std::max<int64_t>(1, units_per_split));
-  int S = static_cast<int>(std::min<int64_t>(kMaxPrefixSplits, fit));
-  if (force_splits > 0) S = static_cast<int>(std::min<int64_t>(std::min(force_splits, kMaxPrefixSplits), fit));
+  // The prefix grid (units_per_split * S CTAs, one per SM) is launched first and the decode kernel after it
+  // (programmatic launch).  Either the decode rings take only the SMs the prefix CTAs leave free ("shrink":
+  // they merge the prefix records at the end of their ranges, so the two kernels run side by side), or all
+  // SMs (the rings on the prefix CTAs' SMs start when those finish).  A cost model picks S and the mode:
+  // prefix CTA ~kPrefFixed + kPrefTile per 128-key tile of its split, decode ~kDecFixed + its bytes at
+  // kSmBytesPerUs per SM.  B200 constants measured on cfg3 (tools/cascade_trace.py, ncu): 3.7 us start +
+  // 3.6 us epilogue + 3.3 us split merge + ~2 us exit, 1.8 us per tile of an M-tile pair; the decode kernel
+  // alone on 33-stage units streams ~29 GB/s per SM (profiles/r02_k1_cfg3_ncu.txt).
+  constexpr double kPrefFixed = 12.0, kPrefTile = 1.8, kDecFixed = 5.0, kSmBytesPerUs = 29e3;
+  int max_tiles = 0;
+  for (const Fam &u : use) max_tiles = std::max(max_tiles, u.tiles);
+  double dec_bytes = 0;  // decode-kernel bytes once the runs are skipped
+  {
+    std::vector<int> runE(pl.descs.size(), 0);
+    for (const Fam &u : use)
+      for (int i : fam[u.idx]) runE[static_cast<size_t>(i)] = u.E;
+    for (size_t i = 0; i < pl.descs.size(); ++i) {
+      const DevDesc &d = pl.descs[i];
+      const int spu = (d.n_old_entries - runE[i]) + (d.n_q + P - 1) / P;
+      dec_bytes += static_cast<double>(Hkv) * d.n_q * spu * 2.0 * P * c.cfg.head_dim * 2;
+    }
+  }
+  int S = 1;
+  bool shrink = false;
+  double best = 1e30;
+  auto model = [&](int s, bool shr) {
+    const int64_t free_sms = sms - units_per_split * s;
+    const double tp = kPrefFixed + kPrefTile * ((max_tiles + s - 1) / s);
+    if (!shr) return tp + kDecFixed + dec_bytes / (static_cast<double>(sms) * kSmBytesPerUs);
+    if (free_sms < 1) return 1e30;
+    return std::max(tp, kDecFixed + dec_bytes / (static_cast<double>(free_sms) * kSmBytesPerUs));
+  };
+  for (int s = 1; s <= std::min<int64_t>(kMaxPrefixSplits, fit); ++s)
+    for (bool shr : {false, true}) {
+      const double t = model(s, shr);
+      if (t < best - 1e-9) {
+        best = t;
+        S = s;
+        shrink = shr;
+      }
+    }
+  if (force_splits > 0) {
+    S = static_cast<int>(std::min<int64_t>(std::min(force_splits, kMaxPrefixSplits), fit));
+    shrink = model(S, true) < model(S, false);
+  }
+
   // workspace: one merged partial per (member row, kv head), plus S split partials when S > 1
   while (S > 1 && rows_all * Hkv * (S + 1) > max_partials) --S;
   if (rows_all * Hkv > max_partials) return;  // workspace too small: no cascade
+  pl.decode_sms = shrink ? static_cast<int32_t>(sms - units_per_split * S) : 0;
   int64_t merged = rows_all * Hkv;            // split partials live after the merged ones
   int64_t split_next = merged;
   int32_t group = 0;

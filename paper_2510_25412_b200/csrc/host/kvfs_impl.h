@@ -185,6 +185,7 @@ struct PredPlan {
   int32_t prefix_partials = 0;  // partials the prefix kernel writes (PART floats each)
   std::vector<ScoreSrc> score_src;  // every successful descriptor with n_q > 0 (batch order)
   int32_t prefix_groups = 0;
+  int32_t decode_sms = 0;  // cascade: SMs the decode kernel's rings take (the prefix CTAs hold the rest); 0: all
 };
 
 class Device;  // data plane (csrc/cuda), absent for a host-only ctx

@@ -23,7 +23,7 @@ def main():
     kv = wl.kv
     for k, opt in (("SPLITS", kvfs.OPT_PREFIX_SPLITS), ("CHUNKS", kvfs.OPT_DECODE_CHUNKS),
                    ("CTAS", kvfs.OPT_DECODE_CTAS)):
-        if os.environ.get(k):
+        if os.environ.get(k) and int(os.environ[k]) > 0:
             kv.set_option(opt, int(os.environ[k]))
     T = wl.n_files * wl.n_q
     s = wl.shape
