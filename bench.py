@@ -666,7 +666,7 @@ def logits_buffer(wl, steps: int):
 
     s = wl.shape
     ent = (wl.lens + steps * wl.n_q + s.P - 1) // s.P + 1 + (wl.n_q + s.P - 1) // s.P
-    floats = int((ent * s.P).sum()) * wl.n_q * s.Hq
+    floats = int((ent * s.P).sum()) * wl.n_q * s.Hq + 32 * len(ent)  # + 128-byte alignment per descriptor
     return torch.empty(floats + 64, dtype=torch.float32, device="cuda")
 
 
@@ -717,7 +717,7 @@ def run_heavy_hitter(args):
         n1 = L0 + 1
         sc = torch.empty(n_files * n1, dtype=torch.float32, device=dev)
         if args.fused_scores:  # K1 writes the logits, K10 sums them (kvfs_set_logits_buffer)
-            kv.set_logits_buffer(torch.empty(n_files * (L0 // s.P + 2) * s.P * s.Hq + 64, dtype=torch.float32,
+            kv.set_logits_buffer(torch.empty(n_files * ((L0 // s.P + 2) * s.P * s.Hq + 32) + 64, dtype=torch.float32,
                                              device=dev))
         step, st = kv.pred_step_begin(descs, np.full(n_files, L0, dtype=np.int32))
         assert st == [0] * n_files

@@ -214,7 +214,10 @@ int pred_attn_scores(kvfs_ctx *ctx, pred_step *step, int layer, const void *q, c
  * device buffer (16-byte aligned; NULL or 0 bytes = off).  While registered, every pred_attn_layer's decode
  * kernel also writes the scaled logit of every key it attends, per head, for each descriptor it attends in
  * full (not chunk descriptors, not shared-prefix cascade members) that still fits in the buffer: a
- * descriptor takes 4 * Hq * P * n_q * (entries before the call + ceil(n_q / P)) bytes, in batch order.  A
+ * descriptor takes 4 * Hq * P * n_q * (entries before the call + ceil(n_q / P)) bytes rounded up to 128, in
+ * batch order.  The logits are written with an L2 evict-last policy and, when the buffer is 128-byte aligned
+ * and P * Hq / Hkv is a multiple of 32, the score pass drops their L2 lines after reading them (no write-back):
+ * with a buffer smaller than the L2 they need not reach DRAM at all.  A
  * pred_attn_scores for the most recent pred_attn_layer's layer then sums exp(logit - lse) from the buffer
  * for those descriptors (kernel K10) and falls back to the pass over K (K9) for the others.  The buffer must
  * stay valid until pred_step_end.  EBUSY while a step is open; EINVAL for a host-only ctx or a misaligned

@@ -119,6 +119,17 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 
+// 4-byte global store with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void st_hint(float *a, float v, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(policy) : "memory");
+}
+
+// Invalidate the 128-byte L2 line at a (128-byte aligned) WITHOUT writing it back: for dead data that was
+// written and consumed inside L2 (the fused-scores logits), so it never costs DRAM write bandwidth.
+__device__ __forceinline__ void discard_l2(const void *a) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
+}
+
 __device__ __forceinline__ void named_bar_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }

@@ -476,6 +476,8 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
   const int kg = lane / LPK, sub = lane % LPK;
   const int hm = sub / SPH;
   int local0 = 0, segi = 0;
+  // fused-scores logits stay in L2 (evict_last) until the score pass reads and discards them
+  const uint64_t lpol = policy_evict_last();
   // merge map: consumer thread ctid owns head mh, dims md0 .. md0 + DPT of a unit's output
   const int ctid = warp * 32 + lane;
   using MM = MergeMap<D, G, NW * 32>;
@@ -648,7 +650,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
           float sc = v[0];
 #pragma unroll
           for (int o = SPH / 2; o > 0; o >>= 1) sc += __shfl_xor_sync(0xffffffffu, sc, o);
-          if (lg != nullptr && valid && (sub % SPH) == 0) lg[slot_k * G + hm] = sc;
+          if (lg != nullptr && valid && (sub % SPH) == 0) st_hint(lg + slot_k * G + hm, sc, lpol);
           s[it] = FULL ? sc : (valid ? sc : -CUDART_INF_F);
           smax = fmaxf(smax, s[it]);
         }

@@ -241,6 +241,7 @@ namespace dev {
 // One CTA per (descriptor, <= 32 final-table entries); thread per (entry, slot).  The key's place in K1's
 // stage layout: an old token (logical < n_old) sits at stage = its entry, slot = its slot; new row r at stage
 // n_old_entries + r / P, slot r % P, visible to the rows qi >= r.
+constexpr int kMaxLogitHeads = 1024;
 __global__ void __launch_bounds__(256) logit_scores_kernel(const ScoreUnit *units, const LogitDesc *descs,
                                                            const Entry *slab, const float *logits, const float *lse,
                                                            float *out, int Hq, int Hkv, int P) {
@@ -262,8 +263,14 @@ __global__ void __launch_bounds__(256) logit_scores_kernel(const ScoreUnit *unit
     emask[e] = m;
     elog[e] = u.l0 + incl - pc;
   }
-  __syncthreads();
   constexpr float kLog2e = 1.4426950408889634f;
+  // lse * log2(e) of the descriptor's rows in shared memory when they fit (decode descriptors: one row)
+  __shared__ __align__(16) float lsh[kMaxLogitHeads];
+  const bool lsm = d.n_q * Hq <= kMaxLogitHeads;
+  if (lsm)
+    for (int i = threadIdx.x; i < d.n_q * Hq; i += blockDim.x)
+      lsh[i] = __ldg(lse + static_cast<int64_t>(d.row0) * Hq + i) * kLog2e;
+  __syncthreads();
   for (int j = threadIdx.x; j < ne * P; j += blockDim.x) {
     const int e = j / P, sl = j % P;
     const uint64_t m = emask[e];
@@ -285,7 +292,8 @@ __global__ void __launch_bounds__(256) logit_scores_kernel(const ScoreUnit *unit
     const int64_t ustride = static_cast<int64_t>(d.stages_per_unit) * P * G;
     const float *lg0 = logits + d.logit_off + (static_cast<int64_t>(st) * P + slot) * G;
     for (int qi = q0; qi < d.n_q; ++qi) {
-      const float *ls = lse + static_cast<int64_t>(d.row0 + qi) * Hq;  // head g G + h of row qi
+      const float *ls = lse + static_cast<int64_t>(d.row0 + qi) * Hq;  // head g G + h of row qi (lsm: unscaled)
+      const float *lss = lsh + qi * Hq;                                // (lsm: scaled)
       if ((G & 3) == 0) {
         // the row's Hq logits as Hq / 4 float4 (16-byte aligned: logit_off and every stride are multiples
         // of 4), 8 loads in flight per thread
@@ -294,27 +302,49 @@ __global__ void __launch_bounds__(256) logit_scores_kernel(const ScoreUnit *unit
           float4 x[8];
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
-            const int j = j0 + t, g = (4 * j) / G, h = (4 * j) - g * G;
-            if (j < nv) x[t] = __ldcs(reinterpret_cast<const float4 *>(lg0 + (g * d.n_q + qi) * ustride + h));
+            const int jj = j0 + t, g = (4 * jj) / G, h = (4 * jj) - g * G;
+            if (jj < nv) x[t] = __ldcs(reinterpret_cast<const float4 *>(lg0 + (g * d.n_q + qi) * ustride + h));
           }
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
-            const int j = j0 + t;
-            if (j < nv) {
-              const float *l = ls + 4 * j;
-              acc += fast_exp2(x[t].x - __ldg(l) * kLog2e) + fast_exp2(x[t].y - __ldg(l + 1) * kLog2e) +
-                     fast_exp2(x[t].z - __ldg(l + 2) * kLog2e) + fast_exp2(x[t].w - __ldg(l + 3) * kLog2e);
+            const int jj = j0 + t;
+            if (jj < nv) {
+              float4 l;
+              if (lsm) {
+                l = *reinterpret_cast<const float4 *>(lss + 4 * jj);
+              } else {
+                l = make_float4(__ldg(ls + 4 * jj) * kLog2e, __ldg(ls + 4 * jj + 1) * kLog2e,
+                                __ldg(ls + 4 * jj + 2) * kLog2e, __ldg(ls + 4 * jj + 3) * kLog2e);
+              }
+              acc += fast_exp2(x[t].x - l.x) + fast_exp2(x[t].y - l.y) + fast_exp2(x[t].z - l.z) +
+                     fast_exp2(x[t].w - l.w);
             }
           }
         }
       } else {
         for (int g = 0; g < Hkv; ++g) {
           const float *lg = lg0 + (g * d.n_q + qi) * ustride;
-          for (int h = 0; h < G; ++h) acc += fast_exp2(__ldcs(lg + h) - __ldg(ls + g * G + h) * kLog2e);
+          for (int h = 0; h < G; ++h)
+            acc += fast_exp2(__ldcs(lg + h) - (lsm ? lss[g * G + h] : __ldg(ls + g * G + h) * kLog2e));
         }
       }
     }
     out[d.out_off + k] = acc;
+  }
+  // The logits are dead now: drop their L2 lines without a write-back (they were written with an evict_last
+  // policy by K1, so they never reach DRAM).  Only the old-entry stages of this CTA's entries (each read by
+  // this CTA alone); whole lines only: every unit-stage block is P G floats at a 128-byte aligned offset
+  // (pred_logits aligns logit_off) when P G is a multiple of 32.
+  if ((P * G) % 32 == 0 && (reinterpret_cast<uintptr_t>(logits) & 127) == 0) {
+    __syncthreads();
+    const int n_old_st = max(0, min(u.e1, d.n_old_entries) - u.e0);  // stages u.e0 .. of old entries
+    const int lpb = P * G / 32;                                      // lines per unit-stage block
+    const int n_units = Hkv * d.n_q;
+    const int total = n_units * n_old_st * lpb;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      const int ln = i % lpb, r = i / lpb, st = u.e0 + r % n_old_st, un = r / n_old_st;
+      discard_l2(logits + d.logit_off + (static_cast<int64_t>(un) * d.stages_per_unit + st) * P * G + ln * 32);
+    }
   }
 }
 

@@ -387,7 +387,7 @@ void pred_logits(Ctx &c, PredPlan *plan) {
     const int64_t need = static_cast<int64_t>(Hkv) * d.n_q * d.stages_per_unit * P * G;
     if (off + need > c.logits_cap) continue;
     d.logit_off = off;
-    off += need;
+    off = (off + need + 31) & ~int64_t{31};  // 128-byte aligned regions: the score pass discards whole L2 lines
     const File *f = pl.desc_files[i];
     if (f->score_slot >= 0 && f->score_slot < static_cast<int32_t>(pl.score_src.size())) {
       ScoreSrc &x = pl.score_src[static_cast<size_t>(f->score_slot)];
