@@ -214,6 +214,11 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
 #ifdef KVFS_K2_TRACE
   const int trace_cta = blockIdx.x == 0 ? 0 : (blockIdx.x == 296 ? 1 : -1);
 #endif
+  // Prefix mode is a programmatic dependent launch after the step prologue, which copies this step's packet
+  // (units, prefix descriptors and rows) into the upload area and applies the table deltas: wait for it
+  // before the first read of either.  (Reading the units earlier returned the PREVIOUS step's records
+  // whenever the packet layout changed between steps, e.g. with another split count.)
+  if constexpr (PREFIX) asm volatile("griddepcontrol.wait;" ::: "memory");
   const ChunkUnit u = p.units[blockIdx.x];
   ChunkDesc cd;
   int q_t0 = -1;  // prefix mode: first packed Q row when the family's rows are consecutive (Q by TMA)
@@ -267,11 +272,8 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   // constant keeps every tcgen05 operand a compile-time uniform value (no R2UR waterfall per MMA).
   if (*tmem_slot != 0u) __trap();
   if constexpr (PREFIX) {
-    // Programmatic dependent launch: this grid may start while the table-delta prologue still runs (the
-    // setup above overlaps it); wait for it before any page-table read, then let the decode kernel that
-    // merges these partials start (it reads them only after its own griddepcontrol.wait, i.e. after this
-    // grid completed; the prologue's writes are complete and visible by then)
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // (waited for the step prologue at the top) let the decode kernel that merges these partials start: it
+    // reads them only after its own griddepcontrol.wait, i.e. after this grid completed
     asm volatile("griddepcontrol.launch_dependents;");
 #ifdef KVFS_K2_TRACE
     if (threadIdx.x == 0 && blockIdx.x < 512) {

@@ -140,3 +140,44 @@ def test_cascade_dynamic_decode(chunks):
         assert h.c.counter(K.CTR_LAST_PREFIX_GROUPS) == 1
     h.check_meta()
     h.check_data()
+
+
+def test_cascade_pipelined_steps_with_changing_splits():
+    """Regression: consecutive steps issued WITHOUT a host synchronisation while the key-split count changes
+    from step to step (a different packet layout every step).  The shared-prefix kernel is a programmatic
+    dependent launch after the step prologue that uploads the step's packet; it read its unit records before
+    waiting for that upload and so picked up the previous step's records (illegal address on B200 when the
+    layout changed).  Every step's output must equal the oracle's."""
+    import torch
+
+    from gpu_harness import assert_close, to_bits, to_dev
+
+    h = Harness(4000, 16, 32, 8, 128, seed=5)
+    h.c.set_option(K.OPT_CASCADE_MIN_ENTRIES, 4)
+    kids = [f"k{i}" for i in range(24)]
+    _family(h, "root", 1200, kids, [3 + 5 * i for i in range(24)])
+    splits = [2, 1, 3, 1, 2, 4, 1, 2]
+    outs, refs = [], []
+    for step, sp in enumerate(splits):
+        h.c.set_option(K.OPT_PREFIX_SPLITS, sp)
+        rows = _decode_rows(h, kids)
+        descs_c = [(h.fds[n][0], len(p)) for n, p in rows]
+        descs_o = [(h.fds[n][1], len(p)) for n, p in rows]
+        pos = [x for _, p in rows for x in p]
+        T = len(pos)
+        k, v = h._kv(T)
+        q = h._q(T)
+        out = torch.full((T, h.Hq, h.D), float("nan"), dtype=torch.bfloat16, device="cuda")
+        lse = torch.empty((T, h.Hq), dtype=torch.float32, device="cuda")
+        st = h.c.pred_attn_batch(descs_c, pos, to_dev(q[0]), to_dev(k[0]), to_dev(v[0]), out, lse)  # no sync
+        assert st == [0] * T
+        assert h.c.counter(K.CTR_LAST_PREFIX_GROUPS) == 1
+        st_o, out_o, lse_o = h.o.pred_batch(descs_o, pos, q, k, v, h.D ** -0.5)
+        outs.append((out, lse))
+        refs.append((out_o[0], lse_o[0]))
+    torch.cuda.synchronize()
+    for step, ((out, lse), (ro, rl)) in enumerate(zip(outs, refs)):
+        assert_close(to_bits(out), ro, f"step {step}")
+        np.testing.assert_allclose(lse.cpu().numpy(), rl, atol=2e-3, rtol=0)
+    h.check_meta()
+    h.check_data()

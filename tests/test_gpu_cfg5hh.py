@@ -38,7 +38,9 @@ def _set(ranges):
     return set(np.concatenate([np.arange(a, b) for a, b in ranges]).tolist())
 
 
-def test_cfg5ii_full_size():
+@pytest.mark.parametrize("fused", [False, True])
+def test_cfg5ii_full_size(fused):
+    """fused: the scores come from the decode kernel's logits (kvfs_set_logits_buffer, K10), else K9."""
     s = Shape(32, 8, 128, 16)
     w = s.Hkv * s.D
     dev = torch.device("cuda", 0)
@@ -88,6 +90,9 @@ def test_cfg5ii_full_size():
 
     # ---- step 0: decode + H2O scores (pred_attn_scores), GPU vs oracle selection of the evicted half
     (q, k1, v1), host = step_inputs(0)
+    if fused:
+        logits = torch.empty(N_FILES * ((L0 // s.P + 2) * s.P * s.Hq + 32) + 64, dtype=torch.float32, device=dev)
+        kv.set_logits_buffer(logits)
     out = torch.empty((N_FILES, s.Hq, s.D), dtype=torch.bfloat16, device=dev)
     lse = torch.empty((N_FILES, s.Hq), dtype=torch.float32, device=dev)
     n1 = L0 + 1
@@ -98,6 +103,9 @@ def test_cfg5ii_full_size():
     kv.pred_attn_scores(step, 0, q, lse, sc, np.arange(N_FILES, dtype=np.int64) * n1)
     kv.pred_step_end(step)
     torch.cuda.synchronize()
+    assert kv.counter(K.CTR_LAST_FUSED_SCORES) == (N_FILES if fused else 0)
+    if fused:
+        kv.set_logits_buffer(None)
     lse_o = check_step(out, lse, host, next_pos, "step 0")
     gsc = sc.view(N_FILES, n1).cpu().numpy().astype(np.float64)
     lg = lse.cpu().numpy()
