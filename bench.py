@@ -51,6 +51,10 @@ def parse():
                          "-1 = library default)")
     ap.add_argument("--decode-ctas", type=int, default=0,
                     help="tuning: decode-kernel ring count (KVFS_OPT_DECODE_CTAS; 0 = auto)")
+    ap.add_argument("--hh-drop", type=float, default=0.0,
+                    help="cfg5hh tuning: fraction of each file evicted (default 0.5, the SURVEY workload)")
+    ap.add_argument("--holes-gather", type=int, default=-1,
+                    help="tuning: KVFS_OPT_HOLES_GATHER (1 = TMA gather4 of retained rows in holey pages; -1 = default)")
     ap.add_argument("--fused-scores", action="store_true",
                     help="with --scores / --real-scores: the decode kernel writes its logits into a registered buffer "
                          "(kvfs_set_logits_buffer) and the score pass reads them (K10) instead of K (K9)")
@@ -402,6 +406,8 @@ def run_ours(args):
         wl.kv.set_option(K.OPT_CHUNK_CUTOVER, args.cutover)
     if args.decode_chunks >= 0:
         wl.kv.set_option(K.OPT_DECODE_CHUNKS, args.decode_chunks)
+    if args.holes_gather >= 0:
+        wl.kv.set_option(K.OPT_HOLES_GATHER, args.holes_gather)
     s = wl.shape
     kv = wl.kv
     T = wl.n_files * wl.n_q
@@ -694,6 +700,8 @@ def run_heavy_hitter(args):
     W, Kst = args.warmup, args.steps
     n_pages = n_files * (L0 // 16 + 4) + n_files * (L0 // 32 + 8)
     kv = K.KVFS(1, s.Hq, s.Hkv, s.D, s.P, n_pages, max_batch_rows=n_files, max_batch_descs=n_files, device=0)
+    if args.holes_gather >= 0:
+        kv.set_option(K.OPT_HOLES_GATHER, args.holes_gather)
     dev = torch.device("cuda", 0)
     fds = []
     for f in range(n_files):
@@ -747,10 +755,11 @@ def run_heavy_hitter(args):
         next_pos = np.full(n_files, L0 + 1, dtype=np.int64)
         lens = np.full(n_files, L0 + 1 - L0 // 2, dtype=np.int64)
     else:
+        drop = int(L0 * args.hh_drop) if args.hh_drop > 0 else L0 // 2
         for f, fd in enumerate(fds):
-            kv.evict(fd, evict_ranges_heavy_hitter(seed, f, L0, L0 // 2))
+            kv.evict(fd, evict_ranges_heavy_hitter(seed, f, L0, drop))
         next_pos = np.full(n_files, L0, dtype=np.int64)
-        lens = np.full(n_files, L0 // 2, dtype=np.int64)
+        lens = np.full(n_files, L0 - drop, dtype=np.int64)
     out = torch.empty((n_files, s.Hq, s.D), dtype=torch.bfloat16, device=dev)
     row_kv = s.Hkv * s.D * 2
 

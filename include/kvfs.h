@@ -362,6 +362,10 @@ typedef enum {
                                    R1 / table work that overlaps it excluded); pred_attn_layer records
                                    events around its kernels (chunk, shared-prefix, decode), summed by
                                    KVFS_CTR_LAYER_DEVICE_NS; 0 = off (default) */
+  KVFS_OPT_HOLES_GATHER = 9,    /* decode kernel, page entries whose retained slots fill less than 40% of
+                                   their [lowest, highest] span (heavy lazy eviction): 1 = fetch only the
+                                   retained rows with TMA gather4 (4 rows per copy, packed in shared memory;
+                                   default), 0 = always copy the whole span (reads the holes too) */
   KVFS_OPT_FAULT_INJECT = 6     /* tests only: value n > 0 makes the n-th following pass through an
                                    injection point (mid-way through a pred reservation, after the first
                                    descriptor is committed; fork; open) throw std::bad_alloc inside the

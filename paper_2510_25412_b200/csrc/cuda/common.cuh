@@ -119,6 +119,17 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 
+// TMA tile::gather4: rows r0..r3 (any order, repeats allowed) of a 2-D map with one-row boxes, columns from
+// c0, into 4 consecutive box rows of shared memory; completion counted on the mbarrier
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const void *map, int c0, int r0, int r1, int r2, int r3,
+                                            uint32_t bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(dst),
+      "l"(map), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar), "l"(policy)
+      : "memory");
+}
+
 // 4-byte global store with an L2 eviction-priority policy (createpolicy)
 __device__ __forceinline__ void st_hint(float *a, float v, uint64_t policy) {
   asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(policy) : "memory");

@@ -288,7 +288,7 @@ extern "C" int kvfs_debug_k1_trace(void *host, size_t bytes) {
 #endif
 
 template <class C>
-__global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const DecodeParams p) {
+__global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const __grid_constant__ DecodeParams p) {
   constexpr int D = C::D, G = C::G, P = C::P, NW = C::NW, NSTAGES = C::NSTAGES;
   constexpr int LPK = C::LPK, KG = C::KG, CH = C::CH, DPL = C::DPL, NIT = C::NIT, SUB = C::SUB;
   extern __shared__ __align__(128) uint8_t smem_all[];
@@ -406,6 +406,12 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
             const int hi = 63 - __clzll(static_cast<long long>(mask));
             nrows = hi - lo + 1;
             off = ((static_cast<int64_t>(e.page) * p.Hkv + sg.g) * P + lo) * D;
+            // sparse span (lazy eviction left more than 60% of it as holes): fetch only the retained rows
+            // (gather4), packed from stage row 0; nrows < 0 marks it (-popcount).  Measured on cfg5(ii)
+            // (50% random holes, spans ~57% retained): gather4 of every holey span 7.7 ms = 2.2 TB/s of
+            // retained bytes against 5.7 ms for the span copies (5.3 TB/s raw), so the break-even density is
+            // ~0.42 (gather4 is bound by TMA operations of 4 x 256 B, not by bytes)
+            if (p.gather && mask != 0 && 5 * __popcll(mask) < 2 * nrows) nrows = -__popcll(mask);
           } else {
             const int v0 = (st - n_os) * P;
             const int r_end = min(dd.n_q, v0 + P);
@@ -430,7 +436,34 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const Decode
             const uint32_t vdst = kdst + C::BLOCK_BYTES;
             StageMeta m;
             m.mask = mj;
-            if (loj >= 0) {
+            if (loj >= 0 && nrj < 0) {
+              // gathered stage: the n retained rows of the page's span, in slot order, at stage rows 0 .. n-1
+              // (the consumers see them as slots 0 .. n-1: attention over a set; the fused-scores logits use
+              // the same packed index, K10 recomputes it); 4 rows per gather4, the last group padded by
+              // repeating its last row
+              const int n = -nrj;
+              m.kind = 0;
+              m.nrows = 0;
+              m.mask = (1ull << n) - 1;  // n < P <= 64
+              meta[slot] = m;
+              const int rowb = static_cast<int>(offj / D) - loj;  // pool row of slot 0 of the (page, head)
+              mbar_arrive_expect_tx(full_bar(slot), static_cast<uint32_t>((n + 3) / 4) * 4 * D * 2 * 2);
+              uint64_t mm = mj;
+              for (int gi = 0; gi < n; gi += 4) {
+                int r[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                  if (mm) {
+                    r[t] = rowb + __ffsll(static_cast<long long>(mm)) - 1;
+                    mm &= mm - 1;
+                  } else {
+                    r[t] = r[t > 0 ? t - 1 : 0];
+                  }
+                }
+                tma_gather4(kdst + gi * D * 2, &p.gk, 0, r[0], r[1], r[2], r[3], full_bar(slot), pol);
+                tma_gather4(vdst + gi * D * 2, &p.gv, 0, r[0], r[1], r[2], r[3], full_bar(slot), pol);
+              }
+            } else if (loj >= 0) {
               m.kind = 0;
               m.nrows = 0;
               meta[slot] = m;

@@ -461,6 +461,12 @@ class CudaDevice final : public Device {
           return KVFS_EIO;
       }
     }
+    if (cfg.head_dim == 64 || cfg.head_dim == 128) {  // K1 holes: single rows for TMA gather4
+      gkmaps_.resize(cfg.n_layers);
+      gvmaps_.resize(cfg.n_layers);
+      for (int l = 0; l < cfg.n_layers; ++l)
+        if (!row_map(c_.kpool[l], &gkmaps_[l]) || !row_map(c_.vpool[l], &gvmaps_[l])) return KVFS_EIO;
+    }
     if (cfg.head_dim == 64 || cfg.head_dim == 128) {  // K9: 16-row tiles of the K pool
       smaps_.resize(cfg.n_layers);
       for (int l = 0; l < cfg.n_layers; ++l)
@@ -788,6 +794,11 @@ class CudaDevice final : public Device {
     p.logits = c_.logits_buf;
     p.Hq = cfg.n_q_heads;
     p.Hkv = cfg.n_kv_heads;
+    p.gather = c_.opt_holes_gather && !gkmaps_.empty() ? 1 : 0;
+    if (p.gather) {
+      p.gk = gkmaps_[layer];
+      p.gv = gvmaps_[layer];
+    }
     // always a programmatic dependent launch: after the prologue (waits at start) or after the shared-prefix
     // kernel (which waited for the prologue itself; waits before merging)
     HP_MARK(d0);
@@ -1099,6 +1110,20 @@ class CudaDevice final : public Device {
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
 
+  // the pool as [n_pages * Hkv * P rows][D] with one-row boxes of the whole head dim, no swizzle: the
+  // decode kernel's tile::gather4 copies land rows packed in a [row][D] shared-memory stage
+  bool row_map(void *pool, CUtensorMap *m) {
+    const kvfs_config &cfg = c_.cfg;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cfg.head_dim),
+                                static_cast<cuuint64_t>(cfg.n_pages) * cfg.n_kv_heads * cfg.page_size};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(cfg.head_dim) * 2};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(cfg.head_dim), 1};
+    const cuuint32_t es[2] = {1, 1};
+    return encode_(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, pool, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+
   struct Pending {
     const void *data;
     size_t bytes, off;
@@ -1141,6 +1166,7 @@ class CudaDevice final : public Device {
              *d_pdescs_ = nullptr, *d_punits_ = nullptr, *d_prows_ = nullptr;
   PFN_cuTensorMapEncodeTiled_v12000 encode_ = nullptr;
   std::vector<CUtensorMap> kmaps_, vmaps_, smaps_;  // smaps_: K pool in 16-row boxes (K9)
+  std::vector<CUtensorMap> gkmaps_, gvmaps_;          // single-row boxes (K1 gather4 over holes)
 };
 
 }  // namespace

@@ -36,6 +36,10 @@ struct DecodeParams {
   int *counters;     // [n_units]
   float *logits;     // fused scores: descriptors with logit_off >= 0 get their logits written here (else null)
   int Hq, Hkv;
+  int gather;        // 1: holey page spans are fetched row by row with TMA gather4 (packed stage rows)
+  // the layer's K / V pools as 2-D maps [n_pages * Hkv * P rows][D], box {D, 1}, no swizzle (gather4)
+  alignas(64) CUtensorMap gk;
+  alignas(64) CUtensorMap gv;
 };
 
 // pdl: programmatic dependent launch after the shared-prefix kernel (the kernel waits for it before merging)
@@ -64,6 +68,7 @@ struct ScoreUnit {  // == kvfs::ScoreUnit
 struct LogitDesc {  // == kvfs::LogitDesc
   int64_t out_off, logit_off;
   int32_t slab_off, n_q, row0, n_old, n_old_entries, stages_per_unit;
+  int32_t gather, pad;  // gather: the decode kernel packed holey page spans (DecodeParams::gather)
 };
 // Fused scores (K10): scores of the descriptors whose keys the decode kernel scored, from its logits.
 cudaError_t launch_logit_scores(const ScoreUnit *units, int n_units, const LogitDesc *descs, const Entry *slab,

@@ -281,6 +281,14 @@ __global__ void __launch_bounds__(256) logit_scores_kernel(const ScoreUnit *unit
       st = u.e0 + e;
       slot = sl;
       q0 = 0;
+      if (d.gather) {
+        // the decode kernel's row of this key in the stage: a page whose retained slots (the old ones of the
+        // last old entry) fill less than 40% of their span was gathered packed (DecodeParams::gather; the
+        // same rule as decode_attn.cu)
+        const uint64_t m1 = (st == d.n_old_entries - 1) ? lowest_bits(m, d.n_old - elog[e]) : m;
+        const int lo = __ffsll(static_cast<long long>(m1)) - 1, hi = 63 - __clzll(static_cast<long long>(m1));
+        if (5 * __popcll(m1) < 2 * (hi - lo + 1)) slot = __popcll(m1 & ((1ull << sl) - 1ull));
+      }
     } else {
       const int r = k - d.n_old;
       st = d.n_old_entries + r / P;

@@ -489,6 +489,7 @@ int pred_attn_layer(kvfs_ctx *ctx, pred_step *step, int layer, const void *q, co
     if (c.plan.T > 0 && (!q || !k_new || !v_new || !out)) return KVFS_EINVAL;
     const int64_t t0 = now_ns();
     c.logits_layer = c.logits_buf ? layer : -1;  // the decode kernel (over)writes this layer's logits
+    c.logits_gather = c.opt_holes_gather;         // ... at packed row positions in gathered stages
     const int rc = c.dev->pred_layer(c.plan, layer, q, k_new, v_new, out, lse, scale, stream);
     c.ctr.host_launch_ns += now_ns() - t0;
     if (rc != KVFS_OK) c.poisoned = true;
@@ -521,7 +522,7 @@ int pred_attn_scores(kvfs_ctx *ctx, pred_step *step, int layer, const void *q, c
       if (fused && x.logit_off >= 0) {
         const int32_t di = static_cast<int32_t>(ld.size());
         ld.push_back({score_off[x.batch_idx], x.logit_off, x.slab_off, x.n_q, x.row0, x.n_old, x.n_old_entries,
-                      x.stages_per_unit});
+                      x.stages_per_unit, c.logits_gather, 0});
         for (int32_t e0 = 0; e0 < ne; e0 += 32) lu.push_back({di, e0, std::min(ne, e0 + 32), f.table[e0].lstart});
         continue;
       }
@@ -748,6 +749,10 @@ int kvfs_set_option(kvfs_ctx *ctx, int option, int64_t value) {
       case KVFS_OPT_CASCADE_MIN_ENTRIES:
         if (value < 0) return KVFS_EINVAL;
         c.opt_cascade_min_entries = value;
+        return KVFS_OK;
+      case KVFS_OPT_HOLES_GATHER:
+        if (value < 0 || value > 1) return KVFS_EINVAL;
+        c.opt_holes_gather = static_cast<int>(value);
         return KVFS_OK;
       case KVFS_OPT_PREFIX_SPLITS:
         if (value < 0 || value > kMaxPrefixSplits) return KVFS_EINVAL;

@@ -155,6 +155,7 @@ struct ScoreSrc {
 struct LogitDesc {
   int64_t out_off, logit_off;
   int32_t slab_off, n_q, row0, n_old, n_old_entries, stages_per_unit;
+  int32_t gather, pad;
 };
 struct PrefixRow {
   int32_t t;          // packed row (Q row) of the query token
@@ -222,9 +223,11 @@ struct Ctx {
   float *logits_buf = nullptr;
   int64_t logits_cap = 0;  // floats
   int logits_layer = -1;
+  int logits_gather = 1;  // KVFS_OPT_HOLES_GATHER in force when those logits were written
   int64_t batch_counter = 0;
   int64_t opt_decode_ctas = 0;
   int64_t opt_decode_chunks = 0;  // KVFS_OPT_DECODE_CHUNKS (0: static scheduling)
+  int opt_holes_gather = 1;       // KVFS_OPT_HOLES_GATHER
   int64_t opt_chunk_cutover = 2;  // measured: cfg2d drafts (n_q 4) K1 1.29 ms / 4.0x HBM traffic, K2 0.44 ms / 1.0x
   int64_t opt_cascade_min_entries = 16;
   int opt_prefix_splits = 0;  // 0 = auto

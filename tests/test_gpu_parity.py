@@ -324,3 +324,77 @@ def test_compact_files_batched():
     with pytest.raises(K.KvfsError) as e:
         h.c.compact_files([h.fds["f1"][0], h.fds["f1"][0]])
     assert e.value.code == K.EBUSY
+
+
+@pytest.mark.parametrize("gather", [1, 0])
+@pytest.mark.parametrize("P,Hq,Hkv,D", [(16, 32, 8, 128), (32, 8, 2, 64), (64, 16, 2, 128)])
+def test_heavy_eviction_gather(P, Hq, Hkv, D, gather):
+    """Lazy eviction leaving sparse pages (KVFS_OPT_HOLES_GATHER): most pages keep 1-4 of P slots spread over
+    their span, so the decode kernel fetches their retained rows with TMA gather4 into packed stage rows
+    (gather = 1) or copies the whole spans (0).  Outputs, lse and the fused H2O scores (whose logit index
+    follows the packed rows) equal the oracle's."""
+    import torch
+
+    from gpu_harness import scores_rtol
+
+    from paper_2510_25412_b200 import kvfs as K
+
+    h = Harness(3000, P, Hq, Hkv, D, seed=31 + P + D)
+    h.c.set_option(K.OPT_HOLES_GATHER, gather)
+    h.c.set_option(K.OPT_CASCADE_MIN_ENTRIES, 0)
+    logits = torch.empty(4 << 20, dtype=torch.float32, device="cuda")
+    h.c.set_logits_buffer(logits)
+    rng = random.Random(P * D + gather)
+    for f in range(3):
+        name = f"h{f}"
+        h.open(name)
+        n = 700 + 300 * f
+        h.append(name, list(range(n)))
+        keep = set(rng.sample(range(n), n // 8)) | {0, n - 1}
+        ranges, a = [], None
+        for t in range(n + 1):
+            if t < n and t not in keep:
+                a = t if a is None else a
+            elif a is not None:
+                ranges.append((a, t))
+                a = None
+        h.evict(name, ranges)
+    names = ["h0", "h1", "h2"]
+    rows = []
+    for name in names:
+        last = h.o.stat(h.fds[name][1])[2]
+        rows.append((name, [last + 1]))
+    descs_c = [(h.fds[n][0], 1) for n in names]
+    descs_o = [(h.fds[n][1], 1) for n in names]
+    pos = [p[0] for _, p in rows]
+    k, v = h._kv(3)
+    q = h._q(3, 2.0)
+    scale = D ** -0.5
+    out = torch.empty((3, Hq, D), dtype=torch.bfloat16, device="cuda")
+    lse = torch.empty((3, Hq), dtype=torch.float32, device="cuda")
+    lens = [h.c.stat(fd)[0] + 1 for fd, _ in descs_c]
+    step, st = h.c.pred_step_begin(descs_c, pos)
+    qd = to_dev(q[0])
+    h.c.pred_attn_layer(step, 0, qd, to_dev(k[0]), to_dev(v[0]), out, lse, scale)
+    off = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+    sc = torch.full((int(sum(lens)),), float("nan"), dtype=torch.float32, device="cuda")
+    h.c.pred_attn_scores(step, 0, qd, lse, sc, off, scale)
+    h.c.pred_step_end(step)
+    torch.cuda.synchronize()
+    assert st == [0, 0, 0]
+    assert h.c.counter(K.CTR_LAST_FUSED_SCORES) == 3
+    st_o, out_o, lse_o, sc_o = h.o.pred_batch(descs_o, pos, q, k, v, scale, scores=True)
+    assert st_o == [0, 0, 0]
+    assert_close(to_bits(out), out_o[0], "heavy eviction")
+    lg = lse.cpu().numpy()
+    np.testing.assert_allclose(lg, lse_o[0], atol=2e-3, rtol=0)
+    got = sc.cpu().numpy().astype(np.float64)
+    for i, name in enumerate(names):
+        kk = bf16_to_f64(h.o.read(h.fds[name][1], 0, 0, lens[i])[0])
+        ref = sc_o[i]
+        rtol = scores_rtol(bf16_to_f64(q[0, i:i + 1]), kk, lg[i:i + 1], lse_o[0, i:i + 1], scale)
+        g = got[off[i]:off[i] + lens[i]]
+        assert g.shape == ref.shape
+        assert (np.abs(g - ref) <= rtol * ref + 1e-30).all(), (name, rtol)
+    h.check_meta()
+    h.check_data()
