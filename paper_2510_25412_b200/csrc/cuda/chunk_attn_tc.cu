@@ -222,10 +222,14 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   const ChunkUnit u = p.units[blockIdx.x];
   ChunkDesc cd;
   int q_t0 = -1;  // prefix mode: first packed Q row when the family's rows are consecutive (Q by TMA)
+  int pd_split = 0, pd_nsplits = 1, pd_split_off = 0;  // prefix mode: this CTA's key split (PrefixDesc)
   if constexpr (PREFIX) {
     const PrefixDesc pd = p.pdescs[u.desc];
     cd = ChunkDesc{pd.slab_off, pd.n_entries, 0, pd.n_rows, pd.row0, pd.n_entries, 0, 0};
     q_t0 = pd.q_t0;
+    pd_split = pd.split;
+    pd_nsplits = pd.n_splits;
+    pd_split_off = pd.split_off;
   } else {
     cd = p.descs[u.desc];
   }
@@ -490,6 +494,21 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         if (lane == 0) mbar_arrive(bar(B_Q));
         if (m == 0 && wq == 0 && lane == 0) K2G(20);  // Q rows gathered
       }
+      // prefix mode: lane j < 32 / G of the warp stores the record of the warp's j-th query token in the
+      // epilogue; its destination is resolved now, off the epilogue's critical path
+      int64_t rec_idx = -1;
+      if (PREFIX && lane < 32 / G) {
+        const int tq = ((m0 + m) * BM + wq * 32 + lane * G) / G;
+        if (tq < cd.n_q) {
+          const PrefixRow pr = p.prows[cd.row0 + tq];
+          const int64_t uq = static_cast<int64_t>(u.g * pr.n_q + pr.qi);
+          const int64_t rr = pr.pref_base + uq;
+          // fold mode (split_off < 0): the decode kernel folds the S split records of its unit itself,
+          // record pref_base + (g n_q + qi) S + split; else split records for the in-kernel group merge
+          rec_idx = pd_split_off < 0 ? pr.pref_base + uq * pd_nsplits + pd_split
+                                     : (pd_nsplits > 1 ? pd_split_off + rr * pd_nsplits + pd_split : rr);
+        }
+      }
       float m_run = -CUDART_INF_F, l_run = 0.f;
       for (int t = 0; t < n_tiles; ++t) {
         // The column metadata of tile t is ready long before S(t): its (~150 clk) barrier wait is taken
@@ -596,6 +615,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         // one query token qi are one contiguous G (HD + 2)-float record, stored with one bulk copy.  The
         // staging overlays Q, K and V (256 rows x 520 B = 130 KiB): wait for both M-tiles' MMAs first.
         if (n_mt == 2) mbar_wait(bar(B_OF + (m ^ 1)), 0);
+        if (m == 0 && wq == 0 && lane == 0) K2G(10);  // both M-tiles' O complete
         tc_fence_after();
         constexpr int PARTF = part_floats(G, HD);
         const int Rl = m * BM + r;  // row within the pair: token Rl / G, head Rl % G
@@ -614,25 +634,27 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         *reinterpret_cast<float2 *>(row + HD) = make_float2(m_run, l_run);
         fence_proxy_async();
         __syncwarp();
+        if (m == 0 && wq == 0 && lane == 0) K2G(11);  // staging written
         // lane j < 32 / G stores the record of the warp's j-th query token
         if (lane < 32 / G) {
-          const int R = (m0 + m) * BM + wq * 32 + lane * G;  // first row of the token
-          const int tq = R / G;
-          if (tq < cd.n_q) {
-            const PrefixRow pr = p.prows[cd.row0 + tq];
-            const PrefixDesc pd = p.pdescs[u.desc];
-            const int64_t rr = pr.pref_base + static_cast<int64_t>(u.g * pr.n_q + pr.qi);
-            const int64_t idx = pd.n_splits > 1 ? pd.split_off + rr * pd.n_splits + pd.split : rr;
+          if (rec_idx >= 0) {
             const uint32_t src = sbase + OFF_Q2 + static_cast<uint32_t>(((m * BM + wq * 32) / G + lane) * PARTF * 4);
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(p.ppart + idx * PARTF),
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(p.ppart + rec_idx * PARTF),
                          "r"(src), "r"(static_cast<uint32_t>(PARTF * 4))
                          : "memory");
           }
           asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // performed: visible after the fences below
-          asm volatile("fence.proxy.async.global;" ::: "memory");
+          if (pd_split_off < 0) {
+            // fold mode: only the next grid reads the records (after this grid completed): the staging must
+            // just outlive the copies' shared-memory reads
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          } else {
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // performed: visible after the fences below
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
         }
         __syncwarp();
+        if (m == 0 && wq == 0 && lane == 0) K2G(12);  // records stored
       } else {
       const float inv = 1.f / l_run;
       const int64_t orow = (static_cast<int64_t>(cd.row0 + qi) * p.Hq + u.g * G + h) * HD;
@@ -691,7 +713,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       int *clear = p.pgroup + (p.pgroup_parity ^ 1) * kMaxPrefixGroups;
       for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kMaxPrefixGroups; i += gridDim.x * blockDim.x) clear[i] = 0;
     }
-    if (S > 1) {
+    if (S > 1 && pd.split_off >= 0) {
       int *arrived = p.pgroup + p.pgroup_parity * kMaxPrefixGroups + u.group;
       __threadfence();  // this CTA's partial records (bulk stores waited for), before the group sees the arrival
       __syncthreads();

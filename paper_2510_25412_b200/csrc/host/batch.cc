@@ -279,7 +279,11 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, 
   // kSmBytesPerUs per SM.  B200 constants measured on cfg3 (tools/cascade_trace.py, ncu): 3.7 us start +
   // 3.6 us epilogue + 3.3 us split merge + ~2 us exit, 1.8 us per tile of an M-tile pair; the decode kernel
   // alone on 33-stage units streams ~29 GB/s per SM (profiles/r02_k1_cfg3_ncu.txt).
-  constexpr double kPrefFixed = 12.0, kPrefTile = 1.8, kDecFixed = 5.0, kSmBytesPerUs = 29e3;
+  // With S <= kMaxFoldSplits the split CTAs do not merge: each writes its records and the decode kernel folds
+  // the S records of its unit (all loads of a group of 4 in flight), which drops the group wait, the merge and
+  // the full write-completion wait of the epilogue from the prefix CTA (~12 -> ~6.5 us of fixed cost; cfg3:
+  // 0.0555 -> 0.048 ms of kernels per step, tools/cascade_trace.py).
+  constexpr double kPrefFixed = 12.0, kPrefFixedFold = 6.5, kPrefTile = 2.0, kDecFixed = 5.0, kSmBytesPerUs = 29e3;
   int max_tiles = 0;
   for (const Fam &u : use) max_tiles = std::max(max_tiles, u.tiles);
   double dec_bytes = 0;  // decode-kernel bytes once the runs are skipped
@@ -298,7 +302,7 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, 
   double best = 1e30;
   auto model = [&](int s, bool shr) {
     const int64_t free_sms = sms - units_per_split * s;
-    const double tp = kPrefFixed + kPrefTile * ((max_tiles + s - 1) / s);
+    const double tp = (s > 1 && s <= kMaxFoldSplits ? kPrefFixedFold : kPrefFixed) + kPrefTile * ((max_tiles + s - 1) / s);
     if (!shr) return tp + kDecFixed + dec_bytes / (static_cast<double>(sms) * kSmBytesPerUs);
     if (free_sms < 1) return 1e30;
     return std::max(tp, kDecFixed + dec_bytes / (static_cast<double>(free_sms) * kSmBytesPerUs));
@@ -317,8 +321,11 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, 
     shrink = model(S, true) < model(S, false);
   }
 
-  // workspace: one merged partial per (member row, kv head), plus S split partials when S > 1
-  while (S > 1 && rows_all * Hkv * (S + 1) > max_partials) --S;
+  const bool fold = S > 1 && S <= kMaxFoldSplits;
+  pl.prefix_fold = fold ? 1 : 0;
+  // workspace: one merged partial per (member row, kv head), plus S split partials when S > 1 (fold: S
+  // split partials only)
+  while (S > 1 && rows_all * Hkv * (fold ? S : S + 1) > max_partials) --S;
   if (rows_all * Hkv > max_partials) return;  // workspace too small: no cascade
   pl.decode_sms = shrink ? static_cast<int32_t>(sms - units_per_split * S) : 0;
   int64_t merged = rows_all * Hkv;            // split partials live after the merged ones
@@ -334,18 +341,22 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, 
     for (size_t j = 1; j < m.size() && q_t0 >= 0; ++j)
       if (pl.descs[m[j]].row0 != pl.descs[m[j - 1]].row0 + pl.descs[m[j - 1]].n_q) q_t0 = -1;
     const int32_t merged_base = pl.prefix_partials;
+    const bool ufold = fold && u.S > 1;
     for (int i : m) {
       DevDesc &d = pl.descs[i];
       d.skip = u.E;
-      d.pref_splits = 1;  // the decode kernel reads the merged partial of unit (g, qi): pref_base + g * n_q + qi
+      // the decode kernel reads the merged partial of unit (g, qi): pref_base + g * n_q + qi; fold: the
+      // S split records pref_base + (g * n_q + qi) * S + s
+      d.pref_splits = ufold ? u.S : 1;
       d.pref_base = pl.prefix_partials;
-      pl.prefix_partials += Hkv * d.n_q;
+      pl.prefix_partials += Hkv * d.n_q * (ufold ? u.S : 1);
       d.stages_per_unit = (d.n_old_entries - u.E) + (d.n_q + P - 1) / P;
       for (int qi = 0; qi < d.n_q; ++qi) pl.prefix_rows.push_back({d.row0 + qi, d.pref_base, d.n_q, qi});
     }
     // split partial of merged record r, split s: split_off + r * S + s (split_off = split base - merged base * S)
-    const int32_t split_off = static_cast<int32_t>(u.S > 1 ? split_next - static_cast<int64_t>(merged_base) * u.S : 0);
-    if (u.S > 1) split_next += static_cast<int64_t>(pl.prefix_partials - merged_base) * u.S;
+    const int32_t split_off =
+        ufold ? -1 : static_cast<int32_t>(u.S > 1 ? split_next - static_cast<int64_t>(merged_base) * u.S : 0);
+    if (u.S > 1 && !ufold) split_next += static_cast<int64_t>(pl.prefix_partials - merged_base) * u.S;
     const DevDesc &lead = pl.descs[m[0]];
     for (int sp = 0; sp < u.S; ++sp) {
       const int t0 = sp * u.tiles / u.S, t1 = (sp + 1) * u.tiles / u.S;

@@ -123,6 +123,8 @@ struct ChunkUnit {
 };
 constexpr int kMaxPrefixGroups = 4096;  // group counters in the workspace (a prefix grid with S > 1 is <= 1 CTA per SM)
 constexpr int kMaxPrefixSplits = 16;  // key splits of one shared prefix (the decode merge folds them in groups)
+// Up to this many key splits the decode kernel folds a unit's split records itself (no in-kernel group merge)
+constexpr int kMaxFoldSplits = 4;
 // Shared-prefix (cascade) work: one record per (fork family, key split); the family's query rows are
 // listed in PrefixRow order (row0 .. row0 + n_rows - 1).
 struct PrefixDesc {
@@ -187,6 +189,7 @@ struct PredPlan {
   std::vector<ScoreSrc> score_src;  // every successful descriptor with n_q > 0 (batch order)
   int32_t prefix_groups = 0;
   int32_t decode_sms = 0;  // cascade: SMs the decode kernel's rings take (the prefix CTAs hold the rest); 0: all
+  int32_t prefix_fold = 0;  // cascade: 1 = the decode kernel folds the S split records (no in-kernel merge)
 };
 
 class Device;  // data plane (csrc/cuda), absent for a host-only ctx

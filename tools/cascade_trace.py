@@ -68,6 +68,11 @@ def main():
                 print(f"  split merge: group complete {np.median(sw - pe[:n_p]) / 1e3:.2f} us after the CTA's own end "
                       f"(max {np.max(sw - pe[:n_p]) / 1e3:.2f}), merge {np.median(mg - sw) / 1e3:.2f} us, "
                       f"last merged at {us(mg).max():.2f} us")
+            e1, e2, e3 = (t2[1, j, :n_p].astype(np.int64) for j in (10, 11, 12))
+            if (e1 > 0).all() and (e2 > 0).all() and (e3 > 0).all():
+                print(f"  epilogue (medians): other M-tile's O {np.median(e1 - of) / 1e3:.2f} us, staging "
+                      f"{np.median(e2 - e1) / 1e3:.2f} us, record stores {np.median(e3 - e2) / 1e3:.2f} us, to CTA end "
+                      f"{np.median(pe[:n_p] - e3) / 1e3:.2f} us")
             dn = t2[1, 25, :n_p].astype(np.int64)
             if (dn > 0).all():
                 print(f"  prefix CTAs done at {us(dn).min():.2f}..{us(dn).max():.2f} us")
