@@ -56,12 +56,14 @@ struct DecodeCfg {
   static constexpr int NQ = 4;                   // Q ring slots
   static constexpr int PART = part_floats(G, D);  // floats per partial (o, m, l per head, 16-byte padded)
   static constexpr int KDEF = kDecodeRecSlots;   // workspace records per range; deferred merges per ring
+  static constexpr int SEGMETA_BYTES = 64;       // per Q slot: the producer's resolved segment (struct SegMeta)
   static constexpr int RING_BYTES_RAW = NSTAGES * STAGE_BYTES + NQ * G * D * 2 + NW * PART * 4 + NSTAGES * 16 +
-                                        (2 * NSTAGES + 2 * NQ + 4) * 8 + 32 + KDEF * 32;
+                                        (2 * NSTAGES + 2 * NQ + 4) * 8 + 32 + KDEF * 32 + NQ * SEGMETA_BYTES;
   static constexpr int RING_BYTES = (RING_BYTES_RAW + 127) / 128 * 128;
   static constexpr int R_RAW = 232448 / RING_BYTES;  // 227 KB of dynamic shared memory per CTA
   static constexpr int R = R_RAW > 8 / NW ? 8 / NW : R_RAW;  // rings per CTA
   static_assert(LPK * KG == 32 && SUB % KG == 0 && P % SUB == 0 && NW <= NSTAGES && NW * R <= 8 && R >= 1, "layout");
+  static_assert(!(D == 128 && G == 4 && P == 16 && NW == 2) || R == 4, "the 8B shape keeps 4 rings per CTA");
 };
 
 // A segment of a unit whose final merge waits for the shared-prefix grid (Desc::pref_splits != 0): its record
@@ -152,6 +154,17 @@ __device__ __forceinline__ Segment make_segment(const Desc *descs, int n_desc, i
   return s;
 }
 
+// A segment as the producer resolved it, handed to the ring's consumers with the segment's Q slot (written
+// before the Q slot's arrive, which releases it): the consumers do not repeat the descriptor search and the
+// descriptor load, two dependent global loads at every segment start.
+// (64 bytes: the 4 rings of a CTA then still fit 227 KB of shared memory at the 8B shape)
+struct SegMeta {
+  int64_t ubeg, logit_off;
+  int32_t d, g, qi, st0, nst, spu;
+  int32_t n_os, n_q, row0, unit_base, pref_splits, pref_base;  // n_os = old-entry stages (n_old_entries - skip)
+};
+static_assert(sizeof(SegMeta) == 64, "SegMeta must be DecodeCfg::SEGMETA_BYTES");
+
 // Final merge of a unit's output (whole unit, or the last piece of a unit cut by ring boundaries).  Each of
 // the ring's NT = NW * 32 consumer threads owns one head h and DPT consecutive dims d0 .. d0 + DPT of it and
 // folds (o, m, l) partial records into a running (M, L, acc) in the log2 domain.  Global records (other
@@ -215,6 +228,41 @@ __device__ __forceinline__ void fold_records(const float *base, int64_t stride, 
     }
     M = Mg;
   }
+}
+
+// Fold the n <= N records rec[j] (each (o[D], m, l) of one head; the thread's dims at d0) with every load in
+// flight at once (one L2 round trip for a unit's pieces and shared-prefix splits together).
+template <int D, int DPT, int N>
+__device__ __forceinline__ void fold_ptrs(const float *const (&rec)[N], int n, int d0, float &M, float &L,
+                                          float (&acc)[DPT]) {
+  float2 ml[N];
+  float o[N][DPT];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    ml[j] = make_float2(-CUDART_INF_F, 0.f);
+#pragma unroll
+    for (int i = 0; i < DPT; ++i) o[j][i] = 0.f;
+    if (j < n) {
+      ml[j] = __ldcg(reinterpret_cast<const float2 *>(rec[j] + D));
+      ld_dims<DPT>(rec[j] + d0, o[j]);
+    }
+  }
+  float Mg = M;
+#pragma unroll
+  for (int j = 0; j < N; ++j) Mg = fmaxf(Mg, ml[j].x);
+  if (Mg == -CUDART_INF_F) return;
+  const float a = (M == -CUDART_INF_F) ? 0.f : fast_exp2(M - Mg);
+  L *= a;
+#pragma unroll
+  for (int i = 0; i < DPT; ++i) acc[i] *= a;
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    const float f = (ml[j].x == -CUDART_INF_F) ? 0.f : fast_exp2(ml[j].x - Mg);
+    L += ml[j].y * f;
+#pragma unroll
+    for (int i = 0; i < DPT; ++i) acc[i] += o[j][i] * f;
+  }
+  M = Mg;
 }
 
 // The ring's warps' (o, m, l) of this segment from shared memory (comb), head h, dims d0..
@@ -304,6 +352,7 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const __grid
   uint64_t *bars = reinterpret_cast<uint64_t *>(meta + NSTAGES);  // full, empty, qfull, qempty, cfull, cempty
   int *flag = reinterpret_cast<int *>(bars + 2 * NSTAGES + 2 * C::NQ + 4);
   int *chunk_slot = flag + 4;                                        // [2] chunk ids (dynamic scheduling)
+  SegMeta *segmeta = reinterpret_cast<SegMeta *>(reinterpret_cast<uint8_t *>(flag + 8) + C::KDEF * 32);  // [NQ]
 
   // Physical ring pr processes "chunks" = virtual CTAs (contiguous stage ranges, p.ncta of them): static
   // scheduling gives ring pr chunk pr; dynamic scheduling (p.dynamic) lets the ring's producer take chunk
@@ -381,9 +430,11 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const __grid
       const Segment sg = make_segment(p.descs, p.n_desc, x, end, dhint);
       dhint = sg.d;
       const Desc dd = p.descs[sg.d];
-      if (lane == 0) {  // Q rows of this unit -> Q ring
+      if (lane == 0) {  // Q rows of this unit -> Q ring, with the resolved segment
         const int qs = segi % C::NQ;
         if (segi >= C::NQ) mbar_wait_sleep(qempty_bar(qs), ((segi / C::NQ) & 1) ^ 1);
+        segmeta[qs] = SegMeta{sg.ubeg, dd.logit_off, sg.d, sg.g, sg.qi, sg.st0, sg.nst, sg.spu,
+                              dd.n_old_entries - dd.skip, dd.n_q, dd.row0, dd.unit_base, dd.pref_splits, dd.pref_base};
         const __nv_bfloat16 *src = p.q + (static_cast<int64_t>(dd.row0 + sg.qi) * p.Hq + sg.g * G) * D;
         mbar_arrive_expect_tx(qfull_bar(qs), G * D * 2);
         bulk_g2s(smem_u32(qring + qs * G * D), src, G * D * 2, qfull_bar(qs), pol);
@@ -540,17 +591,36 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const __grid
     float M = -CUDART_INF_F, L = 0.f, acc[MM::DPT];
 #pragma unroll
     for (int i = 0; i < MM::DPT; ++i) acc[i] = 0.f;
-    if (wrec >= 0) {
-      fold_records<D, MM::DPT, 1>(p.partials + wrec * C::PART + mh * (D + 2), 0, 1, md0, M, L, acc);
-    } else {
-      const int c0 = cta_of(ua, p), c1 = cta_of(ua + spu - 1, p);
-      for (int c = c0; c <= c1; ++c) {
-        const int wh = (cta_start(c, p) >= ua) ? 0 : 1;
-        fold_records<D, MM::DPT, 1>(p.partials + (static_cast<int64_t>(c) * C::KDEF + wh) * C::PART + mh * (D + 2),
-                                    0, 1, md0, M, L, acc);
+    // the unit's records (its whole-unit record, or the pieces of the rings covering it in range order) and
+    // its shared-prefix split records: up to 8 folded with all loads in flight
+    const int c0 = wrec >= 0 ? 0 : cta_of(ua, p), c1 = wrec >= 0 ? 0 : cta_of(ua + spu - 1, p);
+    const int npref = pref ? nsplit : 0;
+    if (c1 - c0 + 1 + npref <= 8) {
+      const float *rec[8];
+      int n = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) rec[j] = nullptr;
+      if (wrec >= 0) {
+        rec[n++] = p.partials + wrec * C::PART + mh * (D + 2);
+      } else {
+        for (int c = c0; c <= c1; ++c)
+          rec[n++] = p.partials + (static_cast<int64_t>(c) * C::KDEF + ((cta_start(c, p) >= ua) ? 0 : 1)) * C::PART +
+                     mh * (D + 2);
       }
+      for (int sp = 0; sp < npref; ++sp) rec[n++] = pref + static_cast<int64_t>(sp) * C::PART + mh * (D + 2);
+      fold_ptrs<D, MM::DPT, 8>(rec, n, md0, M, L, acc);
+    } else {
+      if (wrec >= 0) {
+        fold_records<D, MM::DPT, 1>(p.partials + wrec * C::PART + mh * (D + 2), 0, 1, md0, M, L, acc);
+      } else {
+        for (int c = c0; c <= c1; ++c) {
+          const int wh = (cta_start(c, p) >= ua) ? 0 : 1;
+          fold_records<D, MM::DPT, 1>(p.partials + (static_cast<int64_t>(c) * C::KDEF + wh) * C::PART + mh * (D + 2),
+                                      0, 1, md0, M, L, acc);
+        }
+      }
+      if (pref) fold_records<D, MM::DPT, MM::SG>(pref + mh * (D + 2), C::PART, nsplit, md0, M, L, acc);
     }
-    if (pref) fold_records<D, MM::DPT, MM::SG>(pref + mh * (D + 2), C::PART, nsplit, md0, M, L, acc);
     const int64_t orow = row * p.Hq + g * G + mh;
     store_out<MM::DPT>(p.out + orow * D + md0, p.lse ? p.lse + orow : nullptr, md0, M, L, acc);
   };
@@ -595,16 +665,25 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const __grid
   };
   int64_t x = beg;
   bool first_seg = true;
-  int dhint = -1;
   while (x < end) {
-    const Segment sg = make_segment(p.descs, p.n_desc, x, end, dhint);
-    dhint = sg.d;
-    const Desc dd = p.descs[sg.d];
-    // ---- Q (scaled into the log2 domain) from the Q ring
+    // ---- the segment (resolved by the producer) and its Q (scaled into the log2 domain) from the Q ring
     float2 q2[G][DPL / 2];
+    Segment sg;
+    Desc dd;
     {
       const int qs = segi % C::NQ;
       mbar_wait(qfull_bar(qs), (segi / C::NQ) & 1);
+      const SegMeta sm = segmeta[qs];
+      sg = Segment{sm.d, sm.g, sm.qi, sm.st0, sm.nst, sm.spu, sm.ubeg};
+      dd = Desc{};
+      dd.logit_off = sm.logit_off;
+      dd.n_old_entries = sm.n_os;  // (skip stays 0: n_old_entries - skip is what the consumers use)
+      dd.n_q = sm.n_q;
+      dd.row0 = sm.row0;
+      dd.unit_base = sm.unit_base;
+      dd.pref_splits = sm.pref_splits;
+      dd.pref_base = sm.pref_base;
+      dd.stages_per_unit = sm.spu;
 #pragma unroll
       for (int h = 0; h < G; ++h)
 #pragma unroll

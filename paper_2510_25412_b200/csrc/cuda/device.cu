@@ -91,22 +91,27 @@ __global__ void upload_kernel(uint4 *dst, const uint4 *src, int64_t n16) {
 // every CTA copies a slice of the packet from mapped pinned host memory into the device upload area (the
 // later kernels of the step read it there), and the table deltas / copy-on-write pages are applied from
 // the HOST copy of the same packet (no dependency on the device copy inside this grid).
-__global__ void step_prologue_kernel(uint4 *dst, const uint4 *src, int64_t n16, const dev::SlabRun *runs, int n_runs,
-                                     const dev::Entry *run_entries, dev::Entry *slab, const dev::PageCopy *copies,
-                                     int n_copies, bf16 *const *kp, bf16 *const *vp, int L, int64_t page_elems) {
+// Each table delta is (slab index, entry) read independently from host memory, so the deltas cost one
+// PCIe round trip, in parallel with the packet copy (a run list first, then its entries, cost two).
+__global__ void step_prologue_kernel(uint4 *dst, const uint4 *src, int64_t n16, const int64_t *delta_dst,
+                                     int n_deltas, const dev::Entry *delta_entries, dev::Entry *slab,
+                                     const dev::PageCopy *copies, int n_copies, bf16 *const *kp, bf16 *const *vp, int L,
+                                     int64_t page_elems) {
   asm volatile("griddepcontrol.launch_dependents;");
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n16;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    dst[i] = src[i];
-  const int run_blocks = (n_runs + 7) / 8;
-  if (static_cast<int>(blockIdx.x) < run_blocks) {
-    const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
-    if (r >= n_runs) return;
-    const dev::SlabRun run = runs[r];
-    for (int i = threadIdx.x & 31; i < run.count; i += 32) slab[run.dst + i] = run_entries[run.src + i];
+  const int delta_blocks = (n_deltas + 255) / 256;
+  const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  int64_t ddst = -1;
+  dev::Entry de{};
+  if (static_cast<int>(blockIdx.x) < delta_blocks && j < n_deltas) {
+    ddst = delta_dst[j];
+    de = delta_entries[j];
+  }
+  for (int64_t i = j; i < n16; i += static_cast<int64_t>(gridDim.x) * blockDim.x) dst[i] = src[i];
+  if (static_cast<int>(blockIdx.x) < delta_blocks) {
+    if (ddst >= 0) slab[ddst] = de;
     return;
   }
-  const int b = blockIdx.x - run_blocks;
+  const int b = blockIdx.x - delta_blocks;
   const int ci = b / (2 * L), rem = b % (2 * L), l = rem >> 1, isv = rem & 1;
   if (ci >= n_copies) return;
   const dev::PageCopy pc = copies[ci];
@@ -652,7 +657,7 @@ class CudaDevice final : public Device {
 
   int pred_begin(PredPlan &pl, kvfs_stream_t s) override {
     begin_packet();
-    d_runs_ = push(pl.runs.data(), pl.runs.size() * sizeof(SlabRun));
+    d_runs_ = push(pl.run_dst.data(), pl.run_dst.size() * sizeof(int64_t));
     d_run_entries_ = push(pl.run_entries.data(), pl.run_entries.size() * sizeof(Entry));
     d_copies_ = push(pl.copies.data(), pl.copies.size() * sizeof(PageCopy));
     const size_t off_runs = pending_[0].off, off_entries = pending_[1].off, off_copies = pending_[2].off;
@@ -672,14 +677,14 @@ class CudaDevice final : public Device {
     if (!gather(st)) return KVFS_EIO;
     const kvfs_config &cfg = c_.cfg;
     const int64_t n16 = static_cast<int64_t>((used_ + 15) / 16);
-    const int n_runs = static_cast<int>(pl.runs.size()), n_copies = static_cast<int>(pl.copies.size());
-    const int work = (n_runs + 7) / 8 + n_copies * 2 * cfg.n_layers;
+    const int n_deltas = static_cast<int>(pl.run_dst.size()), n_copies = static_cast<int>(pl.copies.size());
+    const int work = (n_deltas + 255) / 256 + n_copies * 2 * cfg.n_layers;
     const int blocks = std::max<int>(work, static_cast<int>(std::min<int64_t>((n16 + 255) / 256, 64)));
     if (blocks == 0) return KVFS_OK;
     const int64_t page_elems = static_cast<int64_t>(cfg.n_kv_heads) * cfg.page_size * cfg.head_dim;
     step_prologue_kernel<<<blocks, 256, 0, cs(s)>>>(
         reinterpret_cast<uint4 *>(area_), reinterpret_cast<const uint4 *>(st.dev), n16,
-        reinterpret_cast<const dev::SlabRun *>(st.dev + off_runs), n_runs,
+        reinterpret_cast<const int64_t *>(st.dev + off_runs), n_deltas,
         reinterpret_cast<const dev::Entry *>(st.dev + off_entries), slab_,
         reinterpret_cast<const dev::PageCopy *>(st.dev + off_copies), n_copies, kptrs_, vptrs_, cfg.n_layers, page_elems);
     ++c_.ctr.launches;

@@ -24,7 +24,7 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
   const bool device = c.dev != nullptr;
   PredPlan &pl = *plan;
   pl.descs.clear();
-  pl.runs.clear();
+  pl.run_dst.clear();
   pl.run_entries.clear();
   pl.copies.clear();
   pl.dst_slot.assign(static_cast<size_t>(T), -1);
@@ -115,24 +115,17 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
           if (device) {
             // device table deltas: in-place point updates below dirty_from, then the dirty suffix
             const size_t n_ent = f->table.size();
+            // (one slab index per entry: the prologue applies each delta with ONE read of host memory)
             for (uint32_t e : f->dirty_pts) {
               if (e >= f->dirty_from || e >= n_ent) continue;
-              if (!pl.runs.empty() && pl.runs.back().dst + pl.runs.back().count == f->slab_off + e &&
-                  pl.runs.back().count < (1 << 30)) {
-                pl.runs.back().count += 1;
-              } else {
-                pl.runs.push_back({f->slab_off + e, static_cast<int32_t>(pl.run_entries.size()), 1});
-              }
+              pl.run_dst.push_back(f->slab_off + e);
               pl.run_entries.push_back(f->table[e]);
             }
             f->dirty_pts.clear();
-            if (f->dirty_from < n_ent) {
-              SlabRun r{f->slab_off + static_cast<int64_t>(f->dirty_from), static_cast<int32_t>(pl.run_entries.size()),
-                        static_cast<int32_t>(n_ent - f->dirty_from)};
-              pl.runs.push_back(r);
+            for (size_t e = f->dirty_from; e < n_ent; ++e) pl.run_dst.push_back(f->slab_off + static_cast<int64_t>(e));
+            if (f->dirty_from < n_ent)
               pl.run_entries.insert(pl.run_entries.end(), f->table.begin() + static_cast<long>(f->dirty_from),
                                     f->table.end());
-            }
             f->dirty_from = n_ent;
           }
         }

@@ -169,7 +169,7 @@ struct PrefixRow {
 struct PredPlan {
   std::vector<DevDesc> descs;       // successful descriptors with n_q > 0, in order
   std::vector<int32_t> dst_slot;    // [T] page * P + slot of every appended row (-1: row not appended)
-  std::vector<SlabRun> runs;        // slab updates
+  std::vector<int64_t> run_dst;     // slab updates: slab index of each run_entries[j]
   std::vector<Entry> run_entries;
   std::vector<PageCopy> copies;     // copy-on-write copies
   int64_t total_cost = 0;
