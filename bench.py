@@ -381,7 +381,7 @@ def run_ours(args):
         skew = n_files0 // 4
         odd_last = world % 2 == 1 and rank == world - 1
         n_mine = n_files0 if odd_last else (n_files0 + skew if rank % 2 == 0 else n_files0 - skew)
-        wl = DecodeWorkload(args.config, steps_total=W + Kst + min(Kst, 20) + n_e2e + 1, device=devi, n_files=n_mine,
+        wl = DecodeWorkload(args.config, steps_total=W + Kst + min(Kst, 20) + n_e2e + 3, device=devi, n_files=n_mine,
                             owner_base=rank * (n_files0 + skew), room_files=0 if rank % 2 == 0 else skew + 2,
                             step_owner_base=rank * 100_000)
         from paper_2510_25412_b200.parallel import rebalance
@@ -396,7 +396,7 @@ def run_ours(args):
         mstats["moved_files"] = len(mstats.get("moved_files", []))
         migration = gather_rank_info(world, dict(mstats, rank=rank, lips_before=n_mine))
     else:
-        wl = DecodeWorkload(args.config, steps_total=W + Kst + min(Kst, 20) + n_e2e + 1, device=devi, owner_base=rank * n_files0,
+        wl = DecodeWorkload(args.config, steps_total=W + Kst + min(Kst, 20) + n_e2e + 3, device=devi, owner_base=rank * n_files0,
                             step_owner_base=rank * 100_000)
     if args.prefix_splits:
         wl.kv.set_option(K.OPT_PREFIX_SPLITS, args.prefix_splits)
@@ -508,85 +508,54 @@ def run_ours(args):
     ms_step = ms_max / Kst
     value = world * T * Kst / (ms_max / 1000.0)
 
-    # ---- end to end: host (pinned) inputs -> H2D -> pred through the C ABI -> D2H of out + lse, every step.
-    # Pipelined like a serving loop: the H2D of step i+1 (copy stream) and the D2H of step i-1 (second copy
-    # stream) overlap the pred of step i (compute stream); double-buffered device inputs / outputs, ordered
-    # by events.  Every step still moves its full inputs in and its full result out inside the timed region.
-    # A step's Q / K_new / V_new live in one packed buffer (one H2D copy) and its out / lse in another (one
-    # D2H copy); the C ABI takes views into them.
+    # ---- end to end: host (pinned) inputs -> device -> pred -> host outputs, every step, through the C ABI's
+    # host-buffer call pred_attn_batch_host (include/kvfs.h): the library copies each step's Q / K_new / V_new
+    # into one of its two device slots on its own copy stream, runs the pred on the compute stream and copies
+    # out + lse back on a second copy stream, so consecutive steps overlap (the input copy of step i+1 and the
+    # output copy of step i-1 run beside the pred of step i).  Every step moves its full inputs in and its
+    # full result out inside the timed region; the region ends after pred_host_fence (all output copies).
     e2e = None
     if n_e2e:
-        def packed(shapes_dtypes, pin):
-            sizes = [int(np.prod(sh)) * torch.empty((), dtype=dt).element_size() for sh, dt in shapes_dtypes]
-            offs = np.concatenate([[0], np.cumsum([(z + 255) // 256 * 256 for z in sizes])]).astype(int)
-            buf = (torch.empty(int(offs[-1]), dtype=torch.uint8, pin_memory=True) if pin
-                   else torch.empty(int(offs[-1]), dtype=torch.uint8, device="cuda"))
-            views = tuple(buf[o:o + z].view(dt).view(sh) for (sh, dt), o, z in zip(shapes_dtypes, offs, sizes))
-            return buf, views
+        def pinned(shapes_dtypes):
+            return [torch.empty(sh, dtype=dt).pin_memory() for sh, dt in shapes_dtypes]
 
         in_sd = [(tuple(x.shape), x.dtype) for x in inputs[0]]
         out_sd = [(tuple(out.shape), out.dtype), (tuple(lse.shape), lse.dtype)]
-        ring_p = []
+        ring_h = []
         for i in range(4):
-            buf, views = packed(in_sd, True)
+            views = pinned(in_sd)
             for dst, src in zip(views, inputs[i % len(inputs)]):
                 dst.copy_(src.cpu())
-            ring_p.append(buf)
-        dev_in_p = [packed(in_sd, False) for _ in range(2)]
-        dev_out_p = [packed(out_sd, False) for _ in range(2)]
-        host_out_p = [packed(out_sd, True) for _ in range(2)]
-        dev_in = [v for _, v in dev_in_p]
-        dev_out = [v for _, v in dev_out_p]
-        host_out = [v for _, v in host_out_p]
+            ring_h.append(views)
+        host_out = [pinned(out_sd) for _ in range(2)]
         cs = torch.cuda.current_stream()
-        h2d_s, d2h_s = torch.cuda.Stream(), torch.cuda.Stream()
-        ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "used", "done", "d2h")}
+        for i in range(2):  # untimed: the library sizes its two device slots on first use
+            wl.pre_step()
+            kv.pred_attn_batch_host(wl.descs, wl.positions(), *ring_h[i], *host_out[i])
+            wl.advance()
+        kv.pred_host_fence()
         torch.cuda.synchronize()
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(cs)
-        h2d_s.wait_stream(cs)
-        d2h_s.wait_stream(cs)
-
-        def issue_h2d(i):
-            b = i % 2
-            with torch.cuda.stream(h2d_s):
-                if i >= 2:
-                    h2d_s.wait_event(ev["used"][b])  # pred i-2 finished reading buffer b
-                dev_in_p[b][0].copy_(ring_p[i % 4], non_blocking=True)
-                ev["in"][b].record(h2d_s)
-
-        issue_h2d(0)
         for i in range(n_e2e):
-            b = i % 2
-            if i + 1 < n_e2e:
-                issue_h2d(i + 1)
-            cs.wait_event(ev["in"][b])
-            if i >= 2:
-                cs.wait_event(ev["d2h"][b])  # the D2H of step i-2 has read output buffer b
+            qh, kh, vh = ring_h[i % 4]
+            oh, lh = host_out[i % 2]
             wl.pre_step()
-            qd, kd, vd = dev_in[b]
-            kv.pred_attn_batch(wl.descs, wl.positions(), qd, kd, vd, dev_out[b][0], dev_out[b][1])
-            ev["used"][b].record(cs)
-            ev["done"][b].record(cs)
-            with torch.cuda.stream(d2h_s):
-                d2h_s.wait_event(ev["done"][b])
-                host_out_p[b][0].copy_(dev_out_p[b][0], non_blocking=True)
-                ev["d2h"][b].record(d2h_s)
+            kv.pred_attn_batch_host(wl.descs, wl.positions(), qh, kh, vh, oh, lh)
             wl.advance()
-        cs.wait_stream(d2h_s)
-        cs.wait_stream(h2d_s)
+        kv.pred_host_fence()
         e1.record(cs)
         torch.cuda.synchronize()
         et = all_max(e0.elapsed_time(e1), world)
-        h2d_b = int(ring_p[0].numel())
-        d2h_b = int(host_out_p[0][0].numel())
+        h2d_b = int(sum(x.numel() * x.element_size() for x in ring_h[0]))
+        d2h_b = int(sum(x.numel() * x.element_size() for x in host_out[0]))
         e2e = {"value": world * T * n_e2e / (et / 1000.0), "unit": "tokens/s",
                "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b, "steps": n_e2e,
-               "note": "pinned host Q/K_new/V_new (one packed buffer) -> device (copy stream), pred_attn_batch "
-                       "via the C ABI on views of it (compute stream), out+lse (one packed buffer) -> pinned host "
-                       "(second copy stream); steps pipelined with double-buffered device inputs / outputs"}
+               "note": "pred_attn_batch_host through the C ABI with pinned host Q/K_new/V_new and out/lse: the "
+                       "library's H2D copy stream, the pred on the compute stream, its D2H copy stream; steps "
+                       "pipelined over two device slots; the timed region ends after pred_host_fence"}
 
     ranks = gather_rank_info(world, {
         "rank": rank, "device": devi, "pci_bus_id": pci_bus_id(devi), "lips": wl.n_files, "ms_total": ms_total,

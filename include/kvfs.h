@@ -187,6 +187,25 @@ int pred_attn_batch(kvfs_ctx *ctx, const pred_desc *descs, int n_desc, const int
                     const void *q, const void *k_new, const void *v_new, void *out, float *lse,
                     float scale, int *status, kvfs_stream_t stream);
 
+/* pred_attn_batch with HOST buffers (the serving loop's end-to-end form: PAPER.md §4.4, the runtime
+ * hands each batch's projected rows to the GPU and reads the attention output back).  Same arguments and
+ * results as pred_attn_batch, except
+ *   q, k_new, v_new  HOST [T][Hq][D] / [T][Hkv][D] bf16 (page-locked memory for asynchronous copies)
+ *   out, lse         HOST [T][Hq][D] bf16 / [T][Hq] fp32 (lse may be NULL)
+ * The library copies the inputs into one of two device slots on its own copy stream, runs the pred on
+ * `stream` once they landed, and copies the rows of the descriptors that succeeded back on a second copy
+ * stream (rows of failed descriptors are not written).  The call returns once this is enqueued: the host
+ * may refill q / k_new / v_new only after the outputs of the same call are complete, and out / lse are
+ * complete after pred_host_fence(ctx, s) followed by a synchronisation of s.  Consecutive calls overlap:
+ * the input copy of call i+1 and the output copy of call i-1 run beside the pred of call i.
+ * Errors: as pred_attn_batch; KVFS_ENOMEM if the device slots cannot grow; after a call-level error
+ * nothing is copied out. */
+int pred_attn_batch_host(kvfs_ctx *ctx, const pred_desc *descs, int n_desc, const int32_t *pos,
+                         const void *q, const void *k_new, const void *v_new, void *out, float *lse,
+                         float scale, int *status, kvfs_stream_t stream);
+/* Make `stream` wait (no host wait) for every output copy pred_attn_batch_host issued so far. */
+int pred_host_fence(kvfs_ctx *ctx, kvfs_stream_t stream);
+
 /* Multi-layer form: pred_step_begin validates + reserves once (host metadata committed, device tables
  * and copy-on-write copies enqueued), then the caller issues pred_attn_layer for EVERY layer (append of
  * that layer's K_new/V_new fused with its attention), then pred_step_end.  Only one step may be open per

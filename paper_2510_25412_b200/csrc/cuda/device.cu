@@ -403,6 +403,18 @@ class CudaDevice final : public Device {
  public:
   explicit CudaDevice(Ctx &c) : c_(c) {}
   ~CudaDevice() override {
+    if (io_h2d_) {
+      cudaStreamSynchronize(io_h2d_);
+      cudaStreamSynchronize(io_d2h_);
+      for (IoSlot &x : io_) {
+        for (cudaEvent_t e : {x.in_ready, x.used, x.out_done})
+          if (e) cudaEventDestroy(e);
+        if (x.in) cudaFree(x.in);
+        if (x.out) cudaFree(x.out);
+      }
+      cudaStreamDestroy(io_h2d_);
+      cudaStreamDestroy(io_d2h_);
+    }
     for (auto &s : stg_) {
       if (s.ev) cudaEventDestroy(s.ev);
       if (s.host) cudaFreeHost(s.host);
@@ -824,6 +836,94 @@ class CudaDevice final : public Device {
   }
 
   int sync() override { return cudaDeviceSynchronize() == cudaSuccess ? KVFS_OK : KVFS_EIO; }
+
+  // ---- host-buffer pred: two device slots, an H2D and a D2H copy stream of the library
+  int io_begin(int64_t T, const void *q, const void *k, const void *v, bool want_lse, kvfs_stream_t s,
+               HostIo *io) override {
+    const kvfs_config &cfg = c_.cfg;
+    if (!io_h2d_) {
+      if (cudaStreamCreateWithFlags(&io_h2d_, cudaStreamNonBlocking) != cudaSuccess ||
+          cudaStreamCreateWithFlags(&io_d2h_, cudaStreamNonBlocking) != cudaSuccess)
+        return KVFS_EIO;
+      for (IoSlot &x : io_)
+        for (cudaEvent_t *e : {&x.in_ready, &x.used, &x.out_done})
+          if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) return KVFS_EIO;
+    }
+    const int b = io_next_;
+    io_next_ ^= 1;
+    IoSlot &x = io_[b];
+    auto al = [](size_t n) { return (n + 255) & ~static_cast<size_t>(255); };
+    io->q_bytes = static_cast<size_t>(T) * cfg.n_q_heads * cfg.head_dim * 2;
+    io->kv_bytes = static_cast<size_t>(T) * cfg.n_kv_heads * cfg.head_dim * 2;
+    io->out_bytes = io->q_bytes;
+    io->lse_bytes = want_lse ? static_cast<size_t>(T) * cfg.n_q_heads * 4 : 0;
+    const size_t need_in = al(io->q_bytes) + 2 * al(io->kv_bytes), need_out = al(io->out_bytes) + al(io->lse_bytes);
+    if (x.in_cap < need_in || x.out_cap < need_out) {
+      // grow: the slot's previous use must be over (its input and output copies and the pred between them)
+      if (x.live && (cudaEventSynchronize(x.used) != cudaSuccess || cudaEventSynchronize(x.out_done) != cudaSuccess))
+        return KVFS_EIO;
+      if (x.in_cap < need_in) {
+        if (x.in) cudaFree(x.in);
+        x.in = nullptr;
+        x.in_cap = 0;
+        if (cudaMalloc(&x.in, need_in) != cudaSuccess) return KVFS_ENOMEM;
+        x.in_cap = need_in;
+      }
+      if (x.out_cap < need_out) {
+        if (x.out) cudaFree(x.out);
+        x.out = nullptr;
+        x.out_cap = 0;
+        if (cudaMalloc(&x.out, need_out) != cudaSuccess) return KVFS_ENOMEM;
+        x.out_cap = need_out;
+      }
+    }
+    char *in = static_cast<char *>(x.in), *out = static_cast<char *>(x.out);
+    io->slot = b;
+    io->q = in;
+    io->k = in + al(io->q_bytes);
+    io->v = in + al(io->q_bytes) + al(io->kv_bytes);
+    io->out = out;
+    io->lse = want_lse ? reinterpret_cast<float *>(out + al(io->out_bytes)) : nullptr;
+    // inputs: after the pred that last read this slot
+    if (x.live && cudaStreamWaitEvent(io_h2d_, x.used, 0) != cudaSuccess) return KVFS_EIO;
+    if (cudaMemcpyAsync(io->q, q, io->q_bytes, cudaMemcpyHostToDevice, io_h2d_) != cudaSuccess ||
+        cudaMemcpyAsync(io->k, k, io->kv_bytes, cudaMemcpyHostToDevice, io_h2d_) != cudaSuccess ||
+        cudaMemcpyAsync(io->v, v, io->kv_bytes, cudaMemcpyHostToDevice, io_h2d_) != cudaSuccess ||
+        cudaEventRecord(x.in_ready, io_h2d_) != cudaSuccess)
+      return KVFS_EIO;
+    // the pred: after its inputs landed and after the slot's previous outputs were copied out
+    if (cudaStreamWaitEvent(cs(s), x.in_ready, 0) != cudaSuccess) return KVFS_EIO;
+    if (x.live && cudaStreamWaitEvent(cs(s), x.out_done, 0) != cudaSuccess) return KVFS_EIO;
+    return KVFS_OK;
+  }
+
+  int io_end(const HostIo &io, void *out, float *lse, const std::vector<std::pair<int64_t, int64_t>> &rows,
+             kvfs_stream_t s) override {
+    IoSlot &x = io_[io.slot];
+    if (cudaEventRecord(x.used, cs(s)) != cudaSuccess || cudaStreamWaitEvent(io_d2h_, x.used, 0) != cudaSuccess)
+      return KVFS_EIO;
+    const size_t orow = static_cast<size_t>(c_.cfg.n_q_heads) * c_.cfg.head_dim * 2, lrow = c_.cfg.n_q_heads * 4;
+    for (const auto &r : rows) {
+      const size_t n = static_cast<size_t>(r.second - r.first);
+      if (cudaMemcpyAsync(static_cast<char *>(out) + r.first * orow, static_cast<const char *>(io.out) + r.first * orow,
+                          n * orow, cudaMemcpyDeviceToHost, io_d2h_) != cudaSuccess)
+        return KVFS_EIO;
+      if (lse && io.lse &&
+          cudaMemcpyAsync(lse + r.first * c_.cfg.n_q_heads, io.lse + r.first * c_.cfg.n_q_heads, n * lrow,
+                          cudaMemcpyDeviceToHost, io_d2h_) != cudaSuccess)
+        return KVFS_EIO;
+    }
+    if (cudaEventRecord(x.out_done, io_d2h_) != cudaSuccess) return KVFS_EIO;
+    x.live = true;
+    return KVFS_OK;
+  }
+
+  int io_fence(kvfs_stream_t s) override {
+    if (!io_d2h_) return KVFS_OK;
+    for (IoSlot &x : io_)
+      if (x.live && cudaStreamWaitEvent(cs(s), x.out_done, 0) != cudaSuccess) return KVFS_EIO;
+    return KVFS_OK;
+  }
   // Host tier buffers are recycled: a released buffer is cached with an event recorded on the releasing
   // stream (the restore that reads it may still be running) and handed out again, after that event, to an
   // offload needing between half and all of its size.  cudaHostAlloc of pinned memory costs milliseconds.
@@ -1157,6 +1257,15 @@ class CudaDevice final : public Device {
   bf16 **kptrs_ = nullptr, **vptrs_ = nullptr;
   int sms_ = 148;
   int per_sm_ = 0;
+  struct IoSlot {  // host-buffer pred: one device slot (inputs, outputs) and its events
+    void *in = nullptr, *out = nullptr;
+    size_t in_cap = 0, out_cap = 0;
+    cudaEvent_t in_ready = nullptr, used = nullptr, out_done = nullptr;
+    bool live = false;  // used before (its events were recorded)
+  };
+  IoSlot io_[2];
+  int io_next_ = 0;
+  cudaStream_t io_h2d_ = nullptr, io_d2h_ = nullptr;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timing_;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> layer_timing_;  // KVFS_OPT_TIMING: per pred layer
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> copy_timing_;   // KVFS_OPT_TIMING: per K6 launch

@@ -578,6 +578,69 @@ int pred_attn_batch(kvfs_ctx *ctx, const pred_desc *descs, int n_desc, const int
   });
 }
 
+int pred_attn_batch_host(kvfs_ctx *ctx, const pred_desc *descs, int n_desc, const int32_t *pos, const void *q,
+                         const void *k_new, const void *v_new, void *out, float *lse, float scale, int *status,
+                         kvfs_stream_t stream) {
+  return guarded(ctx, [&]() -> int {
+    if (!ctx) return KVFS_EINVAL;
+    Device::HostIo io;
+    int64_t T = 0;
+    {
+      Lock lk(ctx);
+      Ctx &c = *lk.c;
+      if (c.broken) return KVFS_EIO;
+      if (c.step_open) return KVFS_EBUSY;
+      if (!c.dev) return KVFS_ENOSYS;
+      if (c.poisoned) return KVFS_EIO;
+      if (c.cfg.n_layers != 1 || !(scale > 0.f) || n_desc < 0 || (n_desc > 0 && !descs)) return KVFS_EINVAL;
+      for (int i = 0; i < n_desc; ++i) {
+        if (descs[i].n_q < 0) return KVFS_EINVAL;
+        T += descs[i].n_q;
+      }
+      if (T > c.cfg.max_batch_rows) return KVFS_EINVAL;
+      if (T > 0 && (!q || !k_new || !v_new || !out)) return KVFS_EINVAL;
+      if (T > 0) {
+        const int rc = c.dev->io_begin(T, q, k_new, v_new, lse != nullptr, stream, &io);
+        if (rc != KVFS_OK) return rc;
+      }
+    }
+    std::vector<int> st_local;
+    int *st = status;
+    if (!st) {
+      st_local.assign(static_cast<size_t>(std::max(1, n_desc)), 0);
+      st = st_local.data();
+    }
+    const int rc = pred_attn_batch(ctx, descs, n_desc, pos, T ? io.q : nullptr, T ? io.k : nullptr,
+                                   T ? io.v : nullptr, T ? io.out : nullptr, T ? io.lse : nullptr, scale, st, stream);
+    if (T == 0) return rc;
+    // copy out the rows of the descriptors that succeeded (failed descriptors' rows stay untouched); after a
+    // call-level error nothing is copied
+    std::vector<std::pair<int64_t, int64_t>> rows;
+    if (rc == KVFS_OK || rc == KVFS_EPARTIAL) {
+      int64_t r = 0;
+      for (int i = 0; i < n_desc; ++i) {
+        const int64_t n = descs[i].n_q;
+        if (n > 0 && st[i] == KVFS_OK) {
+          if (!rows.empty() && rows.back().second == r) rows.back().second = r + n;
+          else rows.push_back({r, r + n});
+        }
+        r += n;
+      }
+    }
+    Lock lk(ctx);
+    const int erc = lk.c->dev->io_end(io, out, lse, rows, stream);
+    return erc != KVFS_OK ? erc : rc;
+  });
+}
+
+int pred_host_fence(kvfs_ctx *ctx, kvfs_stream_t stream) {
+  return guarded(ctx, [&]() -> int {
+    KVFS_LOCK_OR(ctx);
+    if (!c.dev) return KVFS_ENOSYS;
+    return c.dev->io_fence(stream);
+  });
+}
+
 // ------------------------------------------------------------------------------------------ introspection
 int kvfs_stat(kvfs_ctx *ctx, int fd, kvfs_stat_t *st) {
   return guarded(ctx, [&]() -> int {

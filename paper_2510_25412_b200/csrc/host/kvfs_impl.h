@@ -335,6 +335,22 @@ class Device {
   virtual int64_t take_layer_ns(int64_t *n) = 0;
   // KVFS_OPT_TIMING: summed device time of the page pack / unpack kernels (K6) since the last call
   virtual int64_t take_copy_ns(int64_t *n) = 0;
+  // Host-buffer pred (pred_attn_batch_host): io_begin copies the step's inputs from host memory into one of
+  // two device slots (library copy stream) and makes `s` wait for them (and for the slot's previous output
+  // copy); io_end copies the slot's outputs to host memory once `s` has produced them (second copy stream);
+  // io_fence makes `s2` wait for every output copy issued so far.
+  struct HostIo {
+    void *q = nullptr, *k = nullptr, *v = nullptr, *out = nullptr;
+    float *lse = nullptr;
+    int slot = -1;
+    size_t q_bytes = 0, kv_bytes = 0, out_bytes = 0, lse_bytes = 0;
+  };
+  virtual int io_begin(int64_t T, const void *q, const void *k, const void *v, bool want_lse, kvfs_stream_t s,
+                       HostIo *io) = 0;
+  // rows: [begin, end) row ranges to copy out (the rows of the descriptors that succeeded)
+  virtual int io_end(const HostIo &io, void *out, float *lse, const std::vector<std::pair<int64_t, int64_t>> &rows,
+                     kvfs_stream_t s) = 0;
+  virtual int io_fence(kvfs_stream_t s) = 0;
 };
 
 size_t device_workspace_bytes(const kvfs_config &cfg);

@@ -36,7 +36,7 @@ EXPORTS = [
     "kvfs_workspace_bytes", "kvfs_init", "kvfs_destroy", "kvfs_strerror", "kvfs_open", "kvfs_close",
     "kvfs_unlink", "kvfs_fork", "kvfs_truncate", "kvfs_evict", "kvfs_compact", "kvfs_compact_files",
     "kvfs_append",
-    "pred_attn_batch", "pred_step_begin", "pred_attn_layer", "pred_step_end", "kvfs_stat",
+    "pred_attn_batch", "pred_attn_batch_host", "pred_host_fence", "pred_step_begin", "pred_attn_layer", "pred_step_end", "kvfs_stat",
     "kvfs_get_table", "kvfs_get_positions", "kvfs_get_refcounts", "kvfs_free_pages", "kvfs_read",
     "kvfs_audit", "kvfs_set_option", "kvfs_get_counter", "kvfs_pack", "kvfs_unpack", "kvfs_extract",
     "kvfs_merge", "kvfs_sched_create", "kvfs_sched_destroy", "kvfs_sched_enqueue", "kvfs_sched_state",
@@ -108,6 +108,8 @@ def lib():
             "kvfs_append": (cint, [vp, cint, i64, P(i32), vp, vp, vp]),
             # the per-step calls take plain addresses (ints) for every array: no ctypes pointer objects
             "pred_attn_batch": (cint, [vp, vp, cint, vp, vp, vp, vp, vp, vp, ctypes.c_float, vp, vp]),
+            "pred_attn_batch_host": (cint, [vp, vp, cint, vp, vp, vp, vp, vp, vp, ctypes.c_float, vp, vp]),
+            "pred_host_fence": (cint, [vp, vp]),
             "pred_step_begin": (cint, [vp, vp, cint, vp, vp, P(vp), vp]),
             "pred_attn_layer": (cint, [vp, vp, cint, vp, vp, vp, vp, vp, ctypes.c_float, vp]),
             "pred_step_end": (cint, [vp, vp]),
@@ -335,6 +337,25 @@ class KVFS:
         if rc not in (OK, EPARTIAL):
             raise KvfsError(rc, "pred_attn_batch")
         return status[:n].tolist()
+
+    def pred_attn_batch_host(self, descs, pos, q, k_new, v_new, out, lse=None, scale: Optional[float] = None,
+                             stream=None) -> List[int]:
+        """Batched pred with HOST buffers (include/kvfs.h pred_attn_batch_host): q / k_new / v_new / out / lse are
+        pinned CPU tensors; the library stages them through its device slots.  out / lse are complete after
+        pred_host_fence(stream) and a synchronisation of that stream."""
+        arr, n, _keep = self._descs(descs)
+        p = _i32(pos)
+        status = np.empty(max(1, n), np.int32)
+        scale = float(scale if scale is not None else self.D ** -0.5)
+        rc = _lib.pred_attn_batch_host(self._h, arr, n, p.ctypes.data, _daddr(q), _daddr(k_new), _daddr(v_new),
+                                       _daddr(out), _daddr(lse), scale, status.ctypes.data,
+                                       _stream(stream, self.device))
+        if rc not in (OK, EPARTIAL):
+            raise KvfsError(rc, "pred_attn_batch_host")
+        return status[:n].tolist()
+
+    def pred_host_fence(self, stream=None) -> None:
+        _check(_lib.pred_host_fence(self._h, _stream(stream, self.device)), "pred_host_fence")
 
     def pred_step_begin(self, descs, pos, stream=None):
         arr, n, _keep = self._descs(descs)

@@ -20,6 +20,10 @@ def to_dev(bits: np.ndarray) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).cuda().view(torch.bfloat16)
 
 
+def to_host_pinned(bits: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).pin_memory()
+
+
 def to_bits(t: torch.Tensor) -> np.ndarray:
     return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
 
@@ -96,8 +100,9 @@ class Harness:
         self.c.close(cfd)
         self.o.close(ofd)
 
-    def pred(self, rows, qstd=1.0, scale=None, check=True, sentinel=True):
-        """rows: list of (name, positions). Runs the batch on both sides; returns (status, out bits, lse)."""
+    def pred(self, rows, qstd=1.0, scale=None, check=True, sentinel=True, host_io=False):
+        """rows: list of (name, positions). Runs the batch on both sides; returns (status, out bits, lse).
+        host_io: through pred_attn_batch_host with pinned host buffers instead of device tensors."""
         descs_c, descs_o, pos = [], [], []
         for name, ps in rows:
             cfd, ofd = self.fds[name] if name in self.fds else (987, 987)
@@ -109,12 +114,20 @@ class Harness:
         q = self._q(T, qstd)
         scale = scale if scale is not None else self.D ** -0.5
         assert self.L == 1
+        dev = "cpu" if host_io else "cuda"
         out = torch.full((max(T, 1), self.Hq, self.D), float("nan") if sentinel else 0.0, dtype=torch.bfloat16,
-                         device="cuda")
-        lse = torch.full((max(T, 1), self.Hq), float("nan"), dtype=torch.float32, device="cuda")
-        st = self.c.pred_attn_batch(descs_c, pos, to_dev(q[0]) if T else None, to_dev(k[0]) if T else None,
-                                    to_dev(v[0]) if T else None, out if T else None, lse if T else None,
-                                    scale=scale)
+                         device=dev)
+        lse = torch.full((max(T, 1), self.Hq), float("nan"), dtype=torch.float32, device=dev)
+        if host_io:
+            out, lse = out.pin_memory(), lse.pin_memory()
+            qh, kh, vh = (to_host_pinned(x[0]) if T else None for x in (q, k, v))
+            st = self.c.pred_attn_batch_host(descs_c, pos, qh, kh, vh, out if T else None, lse if T else None,
+                                             scale=scale)
+            self.c.pred_host_fence()
+        else:
+            st = self.c.pred_attn_batch(descs_c, pos, to_dev(q[0]) if T else None, to_dev(k[0]) if T else None,
+                                        to_dev(v[0]) if T else None, out if T else None, lse if T else None,
+                                        scale=scale)
         torch.cuda.synchronize()
         st_o, out_o, lse_o = self.o.pred_batch(descs_o, pos, q, k, v, scale)
         assert st == st_o, (st, st_o)
