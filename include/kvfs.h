@@ -385,6 +385,10 @@ typedef enum {
                                    their [lowest, highest] span (heavy lazy eviction): 1 = fetch only the
                                    retained rows with TMA gather4 (4 rows per copy, packed in shared memory;
                                    default), 0 = always copy the whole span (reads the holes too) */
+  KVFS_OPT_PREFIX_PAIRED = 10,  /* cascade: 0 = the cost model may pick the paired partition (the (kv head,
+                                   M-tile pair) lanes of a shared run taken in pairs, 3 key pieces each, 5
+                                   prefix CTAs per pair, one of them running two short pieces in turn; the
+                                   decode kernel folds the 3 records), 1 = never, 2 = whenever possible */
   KVFS_OPT_FAULT_INJECT = 6     /* tests only: value n > 0 makes the n-th following pass through an
                                    injection point (mid-way through a pred reservation, after the first
                                    descriptor is committed; fork; open) throw std::bad_alloc inside the

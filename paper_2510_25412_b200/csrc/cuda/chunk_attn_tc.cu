@@ -189,7 +189,10 @@ __device__ unsigned long long g_k2_trace[2][32][512];
 // rows are the family's query tokens x the G heads of the kv head (gathered from Q by the softmax warps
 // into the 128B-swizzled layout), every key is an old retained token (no causal part), and the output is
 // the unnormalised partial (O, m, l) per (row, head) that the decode kernel merges.
-template <int G, bool PREFIX>
+// MULTI (prefix mode with ChunkParams::cta_units): a CTA runs a list of units in turn.  A separate
+// instantiation, so the one-unit kernels keep their per-unit values constant (no loop-carried state: the
+// loop version measured ~6% slower per tile).
+template <int G, bool PREFIX, bool MULTI = false>
 __global__ void __launch_bounds__(tc2::THREADS, 1)
     chunk_attn_tc_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                          const __grid_constant__ CUtensorMap qmap, const ChunkParams p) {
@@ -219,25 +222,38 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   // before the first read of either.  (Reading the units earlier returned the PREVIOUS step's records
   // whenever the packet layout changed between steps, e.g. with another split count.)
   if constexpr (PREFIX) asm volatile("griddepcontrol.wait;" ::: "memory");
-  const ChunkUnit u = p.units[blockIdx.x];
+  // The CTA's units: unit blockIdx.x, or in prefix mode with p.cta_units the list [first, first + count), run
+  // one after the other (a balanced partition of the shared runs' key tiles over fewer CTAs than pieces).
+  int u_first = blockIdx.x, n_my = 1;
+  if constexpr (PREFIX && MULTI) {
+    const int2 cr = p.cta_units[blockIdx.x];
+    u_first = cr.x;
+    n_my = cr.y;
+  }
+  ChunkUnit u;
   ChunkDesc cd;
   int q_t0 = -1;  // prefix mode: first packed Q row when the family's rows are consecutive (Q by TMA)
-  int pd_split = 0, pd_nsplits = 1, pd_split_off = 0;  // prefix mode: this CTA's key split (PrefixDesc)
-  if constexpr (PREFIX) {
-    const PrefixDesc pd = p.pdescs[u.desc];
-    cd = ChunkDesc{pd.slab_off, pd.n_entries, 0, pd.n_rows, pd.row0, pd.n_entries, 0, 0};
-    q_t0 = pd.q_t0;
-    pd_split = pd.split;
-    pd_nsplits = pd.n_splits;
-    pd_split_off = pd.split_off;
-  } else {
-    cd = p.descs[u.desc];
-  }
+  int pd_split = 0, pd_nsplits = 1, pd_split_off = 0;  // prefix mode: the unit's key split (PrefixDesc)
   const int epb = BN / p.P;  // page entries per KV tile
-  const int n_tiles = (cd.n_entries + epb - 1) / epb;
-  const int rows_total = cd.n_q * G;
-  const int m0 = 2 * u.m;                                     // first M-tile of this CTA
-  const int n_mt = min(2, (rows_total + BM - 1) / BM - m0);  // 1 or 2 M-tiles
+  int n_tiles = 0, m0 = 0, n_mt = 0;
+  auto load_unit = [&](int ui) {
+    u = p.units[ui];
+    if constexpr (PREFIX) {
+      const PrefixDesc pd = p.pdescs[u.desc];
+      cd = ChunkDesc{pd.slab_off, pd.n_entries, 0, pd.n_rows, pd.row0, pd.n_entries, 0, 0};
+      q_t0 = pd.q_t0;
+      pd_split = pd.split;
+      pd_nsplits = pd.n_splits;
+      pd_split_off = pd.split_off;
+    } else {
+      cd = p.descs[u.desc];
+    }
+    n_tiles = (cd.n_entries + epb - 1) / epb;
+    const int rows_total = cd.n_q * G;
+    m0 = 2 * u.m;                                     // first M-tile of this CTA
+    n_mt = min(2, (rows_total + BM - 1) / BM - m0);  // 1 or 2 M-tiles
+  };
+  load_unit(u_first);
 
   if (threadIdx.x == 0) K2T(24, 0);
 #ifdef KVFS_K2_TRACE
@@ -245,7 +261,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
   if (threadIdx.x == 0 && blockIdx.x < 512) g_k2_trace[1][30][blockIdx.x] = gt0;
 #endif
-  if (threadIdx.x == 0) {
+  auto init_bars = [&]() {
     // prefix mode with gathered rows: one arrival per softmax warp that gathers Q; else one TMA transaction
     mbar_init(bar(B_Q), (PREFIX && q_t0 < 0) ? 4 * n_mt : 1);
     for (int s = 0; s < KV2; ++s) {
@@ -263,7 +279,22 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
     for (int j = 0; j < JR; ++j) mbar_init(bar(B_JF + j), 1);
     mbar_init(bar(B_X), 1);
     fence_mbar_init();
-  }
+  };
+  if (threadIdx.x == 0) init_bars();
+  // Between two units of the CTA: every role has finished the previous one (the MMA warp waited for its last
+  // commits' arrivals, the epilogue's bulk stores have read their staging), so the barriers are invalidated
+  // and re-armed for the next unit, whose phases start again at 0.
+  auto next_unit = [&](int j) {
+    tc_fence_before();
+    named_bar_sync(1, THREADS);
+    load_unit(u_first + j);
+    if (threadIdx.x == 0) {
+      for (int i = 0; i <= B_X; ++i) mbar_inval(bar(i));
+      init_bars();
+    }
+    named_bar_sync(1, THREADS);
+    tc_fence_after();
+  };
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(TMEM_COLS));
@@ -324,6 +355,8 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
     };
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
+    for (int j = 0; j < n_my; ++j) {
+    if (j > 0) next_unit(j);
     if (warp == 0) {
       // ============================================================ K producer (+ Q, + column metadata)
       const uint64_t pol = policy_evict_first();
@@ -355,15 +388,17 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
             emask = en.mask;
             erow = (static_cast<int>(en.page) * p.Hkv + u.g) * p.P;
           }
-          const int cnt = (e >= cd.first_new_entry) ? __popcll(emask) : 0;
-          int incl = cnt;
+          if constexpr (!PREFIX) {  // (prefix mode: every key is an old token, no logical index needed)
+            const int cnt = (e >= cd.first_new_entry) ? __popcll(emask) : 0;
+            int incl = cnt;
 #pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
+            for (int o = 1; o < 32; o <<= 1) {
+              const int y = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= o) incl += y;
+            }
+            jbase = carry + incl - cnt;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
           }
-          jbase = carry + incl - cnt;
-          carry += __shfl_sync(0xffffffffu, incl, 31);
           cached = blk;
         }
         // column metadata of tile t: j = logical index - n_old (visible iff j <= qi), INT_MAX = no key;
@@ -376,11 +411,15 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           const int i = c / p.P, slot = c % p.P;
           const int src = (e0 & 31) + i;
           const uint64_t m = __shfl_sync(0xffffffffu, emask, src);
-          const int32_t jb = __shfl_sync(0xffffffffu, jbase, src);
           const int e = e0 + i;
           int32_t j = 0x7fffffff;
-          if (e < cd.n_entries && ((m >> slot) & 1ull))
-            j = (e < cd.first_new_entry) ? -1 : jb + __popcll(m & ((1ull << slot) - 1ull));
+          if constexpr (PREFIX) {
+            if (e < cd.n_entries && ((m >> slot) & 1ull)) j = -1;
+          } else {
+            const int32_t jb = __shfl_sync(0xffffffffu, jbase, src);
+            if (e < cd.n_entries && ((m >> slot) & 1ull))
+              j = (e < cd.first_new_entry) ? -1 : jb + __popcll(m & ((1ull << slot) - 1ull));
+          }
           jcol[c] = j;
           vis_all &= (j < 0);
         }
@@ -455,9 +494,20 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         }
         __syncwarp();
       }
+      if (j + 1 < n_my) {
+        // another unit follows: wait until the arrivals of the last K / V stage commits (nobody else waits
+        // for them) have landed, so the barriers can be re-armed
+        for (int t = max(0, n_tiles - KV2); t < n_tiles; ++t) {
+          mbar_wait(bar(B_KE + t % KV2), (t / KV2) & 1);
+          mbar_wait(bar(B_VE + t % KV2), (t / KV2) & 1);
+        }
+      }
+    }
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    for (int j = 0; j < n_my; ++j) {
+    if (j > 0) next_unit(j);
     // ============================================================ softmax warpgroups (thread = row)
     const int m = (warp - 4) >> 2;          // M-tile of this warpgroup
     const int wq = (warp - 4) & 3;          // TMEM lane quarter
@@ -681,6 +731,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
             (m_run + __log2f(l_run)) * 0.69314718055994531f;
       }
     }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -822,12 +873,12 @@ extern "C" int kvfs_debug_k2_trace(void *host, size_t bytes) {
 }
 #endif
 
-template <int G, bool PREFIX>
-static cudaError_t launch_chunk_g(const CUtensorMap &km, const CUtensorMap &vm, const CUtensorMap &qm,
-                                  const ChunkParams &p, int n_units, cudaStream_t s) {
+template <int G, bool PREFIX, bool MULTI>
+static cudaError_t launch_chunk_gm(const CUtensorMap &km, const CUtensorMap &vm, const CUtensorMap &qm,
+                                   const ChunkParams &p, int n_units, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(chunk_attn_tc_kernel<G, PREFIX>,
+    cudaError_t e = cudaFuncSetAttribute(chunk_attn_tc_kernel<G, PREFIX, MULTI>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM2);
     if (e != cudaSuccess) return e;
     attr = true;
@@ -842,7 +893,16 @@ static cudaError_t launch_chunk_g(const CUtensorMap &km, const CUtensorMap &vm, 
   la[0].val.programmaticStreamSerializationAllowed = PREFIX ? 1 : 0;  // prefix mode waits in-kernel
   cfg.attrs = la;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, chunk_attn_tc_kernel<G, PREFIX>, km, vm, qm, p);
+  return cudaLaunchKernelEx(&cfg, chunk_attn_tc_kernel<G, PREFIX, MULTI>, km, vm, qm, p);
+}
+
+template <int G, bool PREFIX>
+static cudaError_t launch_chunk_g(const CUtensorMap &km, const CUtensorMap &vm, const CUtensorMap &qm,
+                                  const ChunkParams &p, int n_units, cudaStream_t s) {
+  if constexpr (PREFIX) {
+    if (p.cta_units) return launch_chunk_gm<G, true, true>(km, vm, qm, p, n_units, s);
+  }
+  return launch_chunk_gm<G, PREFIX, false>(km, vm, qm, p, n_units, s);
 }
 
 template <bool PREFIX>

@@ -681,8 +681,9 @@ class CudaDevice final : public Device {
     d_pdescs_ = push(pl.prefix_descs.data(), pl.prefix_descs.size() * sizeof(PrefixDesc));
     d_punits_ = push(pl.prefix_units.data(), pl.prefix_units.size() * sizeof(ChunkUnit));
     d_prows_ = push(pl.prefix_rows.data(), pl.prefix_rows.size() * sizeof(PrefixRow));
+    d_pctas_ = push(pl.prefix_cta_units.data(), pl.prefix_cta_units.size() * sizeof(int32_t));
     if (!d_runs_ || !d_run_entries_ || !d_copies_ || !d_descs_ || !d_dst_ || !d_cdescs_ || !d_cunits_ || !d_cdst_ ||
-        !d_pdescs_ || !d_punits_ || !d_prows_)
+        !d_pdescs_ || !d_punits_ || !d_prows_ || !d_pctas_)
       return KVFS_ENOMEM;
     // one launch: packet copy (SM loads over PCIe) + table deltas + copy-on-write pages (step_prologue_kernel)
     Staging &st = stg_[cur_];
@@ -997,12 +998,15 @@ class CudaDevice final : public Device {
     p.ppart = ppart_;
     p.pgroup = pgroup_;
     p.pgroup_parity = static_cast<int>(prefix_launches_++ & 1);
+    p.cta_units = pl.prefix_cta_units.empty() ? nullptr : static_cast<const int2 *>(d_pctas_);
+    const int n_ctas = pl.prefix_cta_units.empty() ? static_cast<int>(pl.prefix_units.size())
+                                                   : static_cast<int>(pl.prefix_cta_units.size() / 2);
     alignas(64) CUtensorMap qmap;
     HP_MARK(a0);
     if (!encode_q_map(&qmap, q, pl.T)) return KVFS_EINVAL;
     HP_MARK(a1);
     const cudaError_t e = dev::launch_prefix(kmaps_[layer], vmaps_[layer], qmap, p,
-                                             static_cast<int>(pl.prefix_units.size()), G, cs(s));
+                                             n_ctas, G, cs(s));
     HP_MARK(a2);
     HP_ADD(0, a0, a1);
     HP_ADD(1, a1, a2);
@@ -1275,6 +1279,7 @@ class CudaDevice final : public Device {
   int cur_ = 0;
   size_t used_ = 0;
   std::vector<Pending> pending_;
+  const void *d_pctas_ = nullptr;
   const void *d_runs_ = nullptr, *d_run_entries_ = nullptr, *d_copies_ = nullptr, *d_descs_ = nullptr,
              *d_dst_ = nullptr, *d_cdescs_ = nullptr, *d_cunits_ = nullptr, *d_cdst_ = nullptr,
              *d_pdescs_ = nullptr, *d_punits_ = nullptr, *d_prows_ = nullptr;

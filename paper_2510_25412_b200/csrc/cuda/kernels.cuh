@@ -94,6 +94,7 @@ struct ChunkParams {
   float *ppart;
   int *pgroup;         // [2][kMaxPrefixGroups] arrival counters of the split groups, by launch parity
   int pgroup_parity;   // 0 / 1: this launch's counter array (the other one is cleared)
+  const int2 *cta_units;  // prefix mode: per CTA (first unit, count), units run in turn; null: unit = CTA
 };
 cudaError_t launch_chunk(const CUtensorMap &km, const CUtensorMap &vm, const CUtensorMap &qm, const ChunkParams &p,
                          int n_units, int G, cudaStream_t s);

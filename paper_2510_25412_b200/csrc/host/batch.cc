@@ -42,6 +42,7 @@ int pred_reserve(Ctx &c, const pred_desc *descs, int n_desc, const int32_t *pos,
   pl.prefix_descs.clear();
   pl.prefix_units.clear();
   pl.prefix_rows.clear();
+  pl.prefix_cta_units.clear();
   pl.prefix_partials = 0;
   pl.prefix_groups = 0;
   pl.decode_sms = 0;
@@ -188,11 +189,13 @@ namespace kvfs {
 // attended once per (family, kv head, key split) with all members' query rows as the M dimension of the
 // tcgen05 kernel, and every member's decode unit starts after the run and merges the prefix partials
 // (exact: softmax over a disjoint union of key sets = log-sum-exp merge of the parts).
-void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, int64_t max_partials, PredPlan *plan) {
+void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int paired_mode, int sms, int64_t max_partials,
+                  PredPlan *plan) {
   PredPlan &pl = *plan;
   pl.prefix_descs.clear();
   pl.prefix_units.clear();
   pl.prefix_rows.clear();
+  pl.prefix_cta_units.clear();
   pl.prefix_partials = 0;
   pl.prefix_groups = 0;
   const int P = c.cfg.page_size, Hkv = c.cfg.n_kv_heads, G = c.cfg.n_q_heads / c.cfg.n_kv_heads;
@@ -276,7 +279,16 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, 
   // the S records of its unit (all loads of a group of 4 in flight), which drops the group wait, the merge and
   // the full write-completion wait of the epilogue from the prefix CTA (~12 -> ~6.5 us of fixed cost; cfg3:
   // 0.0555 -> 0.048 ms of kernels per step, tools/cascade_trace.py).
-  constexpr double kPrefFixed = 12.0, kPrefFixedFold = 6.5, kPrefTile = 2.0, kDecFixed = 5.0, kSmBytesPerUs = 29e3;
+  // Round-2 constants (tools/cascade_trace.py on cfg3): fold-mode prefix CTA ~6.6 us fixed (0.3 wait, 2.6 to
+  // the first S, 3.7 epilogue) + 2.0 us per tile; decode rings stream ~10 GB/s each, 4 per SM, after ~5 us
+  // of start and merge.  In "shrink" mode a ring count between the unit count and 4x it cuts units across
+  // rings, whose extra segment starts and cross-ring merges were measured to cost more than the SMs they
+  // free (cfg3 S = 3: 0.063 ms against 0.050 for S = 2), so such layouts are not considered.
+  constexpr double kPrefFixed = 12.0, kPrefFixedFold = 6.6, kPrefTile = 2.0, kDecFixed = 5.0, kSmBytesPerUs = 40e3;
+  auto rings_ok = [&](int64_t free_sms) {
+    const int64_t rings = free_sms * 4;
+    return pl.n_units <= rings || pl.n_units >= 4 * rings;
+  };
   int max_tiles = 0;
   for (const Fam &u : use) max_tiles = std::max(max_tiles, u.tiles);
   double dec_bytes = 0;  // decode-kernel bytes once the runs are skipped
@@ -297,8 +309,40 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, 
     const int64_t free_sms = sms - units_per_split * s;
     const double tp = (s > 1 && s <= kMaxFoldSplits ? kPrefFixedFold : kPrefFixed) + kPrefTile * ((max_tiles + s - 1) / s);
     if (!shr) return tp + kDecFixed + dec_bytes / (static_cast<double>(sms) * kSmBytesPerUs);
-    if (free_sms < 1) return 1e30;
+    if (free_sms < 1 || !rings_ok(free_sms)) return 1e30;
     return std::max(tp, kDecFixed + dec_bytes / (static_cast<double>(free_sms) * kSmBytesPerUs));
+  };
+  // Paired partition (fold, S = 3): the (kv head, M-tile pair) lanes of a family are taken in pairs (a, b);
+  // lane a is cut into key pieces (x, x, r) and lane b into (r, x, x), r = tiles - 2x, and a pair runs on 5
+  // CTAs: [a0] [a1] [a2 then b0] [b1] [b2] (one CTA runs two short units in turn).  2.5 CTAs per lane
+  // instead of 2 or 3 lets the prefix grid take exactly the SMs the decode rings leave (cfg3: 20 = 148 - 128).
+  int64_t paired_ctas = 0;
+  bool paired_possible = true;
+  double paired_tp = 0;
+  std::vector<int> pair_x(use.size(), 0);
+  for (size_t k = 0; k < use.size(); ++k) {
+    const Fam &u = use[k];
+    const int lanes = Hkv * u.mpairs;
+    if (lanes % 2 != 0 || u.tiles < 3) {
+      paired_possible = false;
+      break;
+    }
+    paired_ctas += static_cast<int64_t>(lanes / 2) * 5;
+    double bt = 1e30;
+    for (int x = 1; 2 * x < u.tiles; ++x) {
+      const int r = u.tiles - 2 * x;
+      const double t = std::max(kPrefFixedFold + kPrefTile * x, 2 * kPrefFixedFold + kPrefTile * 2 * r);
+      if (t < bt) {
+        bt = t;
+        pair_x[k] = x;
+      }
+    }
+    paired_tp = std::max(paired_tp, bt);
+  }
+  auto model_paired = [&]() {
+    const int64_t free_sms = sms - paired_ctas;
+    if (!paired_possible || free_sms < 1 || !rings_ok(free_sms)) return 1e30;
+    return std::max(paired_tp, kDecFixed + dec_bytes / (static_cast<double>(free_sms) * kSmBytesPerUs));
   };
   for (int s = 1; s <= std::min<int64_t>(kMaxPrefixSplits, fit); ++s)
     for (bool shr : {false, true}) {
@@ -309,9 +353,16 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, 
         shrink = shr;
       }
     }
+  bool paired = paired_mode != 1 && model_paired() < best - 1e-9;
   if (force_splits > 0) {
     S = static_cast<int>(std::min<int64_t>(std::min(force_splits, kMaxPrefixSplits), fit));
     shrink = model(S, true) < model(S, false);
+    paired = false;
+  }
+  if (paired_mode == 2 && paired_possible && paired_ctas < sms) paired = true;
+  if (paired) {
+    S = 3;
+    shrink = true;
   }
 
   const bool fold = S > 1 && S <= kMaxFoldSplits;
@@ -320,7 +371,8 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, 
   // split partials only)
   while (S > 1 && rows_all * Hkv * (fold ? S : S + 1) > max_partials) --S;
   if (rows_all * Hkv > max_partials) return;  // workspace too small: no cascade
-  pl.decode_sms = shrink ? static_cast<int32_t>(sms - units_per_split * S) : 0;
+  if (paired && rows_all * Hkv * 3 > max_partials) paired = false, S = 2;
+  pl.decode_sms = shrink ? static_cast<int32_t>(sms - (paired ? paired_ctas : units_per_split * S)) : 0;
   int64_t merged = rows_all * Hkv;            // split partials live after the merged ones
   int64_t split_next = merged;
   int32_t group = 0;
@@ -351,6 +403,38 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, 
         ufold ? -1 : static_cast<int32_t>(u.S > 1 ? split_next - static_cast<int64_t>(merged_base) * u.S : 0);
     if (u.S > 1 && !ufold) split_next += static_cast<int64_t>(pl.prefix_partials - merged_base) * u.S;
     const DevDesc &lead = pl.descs[m[0]];
+    if (paired) {
+      const int x = pair_x[static_cast<size_t>(&u - use.data())], r = u.tiles - 2 * x;
+      // key pieces of the lanes "a" (x, x, r) and "b" (r, x, x): six prefix descriptors, splits 0..2 each
+      const int cuts[2][4] = {{0, x, 2 * x, u.tiles}, {0, r, r + x, u.tiles}};
+      const int32_t d0 = static_cast<int32_t>(pl.prefix_descs.size());
+      for (int par = 0; par < 2; ++par)
+        for (int sp = 0; sp < 3; ++sp) {
+          const int e0 = cuts[par][sp] * epb, e1 = std::min(u.E, cuts[par][sp + 1] * epb);
+          pl.prefix_descs.push_back({lead.slab_off + e0, e1 - e0, u.rows, row0, sp, 3, q_t0, -1});
+        }
+      std::vector<std::pair<int, int>> lanes;  // (kv head, M-tile pair)
+      for (int g = 0; g < Hkv; ++g)
+        for (int mp = 0; mp < u.mpairs; ++mp) lanes.push_back({g, mp});
+      auto unit = [&](int par, int sp, const std::pair<int, int> &ln) {
+        return ChunkUnit{d0 + par * 3 + sp, ln.first, ln.second, group};
+      };
+      auto cta = [&](std::initializer_list<ChunkUnit> us) {
+        pl.prefix_cta_units.push_back(static_cast<int32_t>(pl.prefix_units.size()));
+        pl.prefix_cta_units.push_back(static_cast<int32_t>(us.size()));
+        for (const ChunkUnit &cu : us) pl.prefix_units.push_back(cu);
+      };
+      for (size_t l = 0; l + 1 < lanes.size(); l += 2, ++group) {
+        const auto &a = lanes[l], &b = lanes[l + 1];
+        cta({unit(0, 0, a)});
+        cta({unit(0, 1, a)});
+        cta({unit(0, 2, a), unit(1, 0, b)});
+        cta({unit(1, 1, b)});
+        cta({unit(1, 2, b)});
+      }
+      ++pl.prefix_groups;
+      continue;
+    }
     for (int sp = 0; sp < u.S; ++sp) {
       const int t0 = sp * u.tiles / u.S, t1 = (sp + 1) * u.tiles / u.S;
       const int e0 = t0 * epb, e1 = std::min(u.E, t1 * epb);

@@ -457,7 +457,7 @@ int pred_step_begin(kvfs_ctx *ctx, const pred_desc *descs, int n_desc, const int
     if (rc != KVFS_OK && rc != KVFS_EPARTIAL) return rc;
     if (c.dev) {
       pred_split(c, c.opt_chunk_cutover, &c.plan);
-      pred_cascade(c, c.opt_cascade_min_entries, c.opt_prefix_splits, c.dev->sms(), c.dev->prefix_partial_capacity(),
+      pred_cascade(c, c.opt_cascade_min_entries, c.opt_prefix_splits, c.opt_prefix_paired, c.dev->sms(), c.dev->prefix_partial_capacity(),
                    &c.plan);
       pred_logits(c, &c.plan);
       const int64_t t2 = now_ns();
@@ -820,6 +820,10 @@ int kvfs_set_option(kvfs_ctx *ctx, int option, int64_t value) {
       case KVFS_OPT_PREFIX_SPLITS:
         if (value < 0 || value > kMaxPrefixSplits) return KVFS_EINVAL;
         c.opt_prefix_splits = static_cast<int>(value);
+        return KVFS_OK;
+      case KVFS_OPT_PREFIX_PAIRED:
+        if (value < 0 || value > 2) return KVFS_EINVAL;
+        c.opt_prefix_paired = static_cast<int>(value);
         return KVFS_OK;
       case KVFS_OPT_DECODE_CHUNKS:
         if (value < 0 || value > 2048) return KVFS_EINVAL;

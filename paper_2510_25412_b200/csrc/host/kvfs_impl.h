@@ -185,6 +185,7 @@ struct PredPlan {
   std::vector<PrefixDesc> prefix_descs;
   std::vector<ChunkUnit> prefix_units;
   std::vector<PrefixRow> prefix_rows;
+  std::vector<int32_t> prefix_cta_units;  // paired cascade: per CTA (first unit, count); empty: one unit per CTA
   int32_t prefix_partials = 0;  // partials the prefix kernel writes (PART floats each)
   std::vector<ScoreSrc> score_src;  // every successful descriptor with n_q > 0 (batch order)
   int32_t prefix_groups = 0;
@@ -234,6 +235,7 @@ struct Ctx {
   int64_t opt_chunk_cutover = 2;  // measured: cfg2d drafts (n_q 4) K1 1.29 ms / 4.0x HBM traffic, K2 0.44 ms / 1.0x
   int64_t opt_cascade_min_entries = 16;
   int opt_prefix_splits = 0;  // 0 = auto
+  int opt_prefix_paired = 0;  // 0 = auto, 1 = off, 2 = on when possible
   bool opt_timing = false;    // KVFS_OPT_TIMING
   int64_t last_compact_device_ns = 0;
   int64_t last_layer_timed = 0;
@@ -294,7 +296,9 @@ void pred_split(const Ctx &c, int64_t cutover, PredPlan *plan);
 // with the same run of (page, mask) entries, sets their skip / pref_* fields and emits the prefix work.
 // `sms` sizes the key splits, `max_partials` is the workspace capacity in partials.
 // force_splits > 0: key splits per shared run (else chosen from the SM count)
-void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int sms, int64_t max_partials, PredPlan *plan);
+// paired_mode: 0 = the cost model decides, 1 = never the paired partition, 2 = paired whenever possible
+void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int paired_mode, int sms, int64_t max_partials,
+                  PredPlan *plan);
 void pred_logits(Ctx &c, PredPlan *plan);
 
 // ---- data plane interface (implemented in csrc/cuda/device.cu)

@@ -24,7 +24,7 @@ HOST_PAGE = 0x80000000
 O_CREAT, O_EXCL = 1, 2
 EVICT_COMPACT = 1
 OPT_DECODE_CTAS, OPT_CHUNK_CUTOVER, OPT_DETERMINISTIC, OPT_CASCADE_MIN_ENTRIES, OPT_PREFIX_SPLITS = 1, 2, 3, 4, 5
-OPT_FAULT_INJECT, OPT_TIMING, OPT_DECODE_CHUNKS, OPT_HOLES_GATHER = 6, 7, 8, 9
+OPT_FAULT_INJECT, OPT_TIMING, OPT_DECODE_CHUNKS, OPT_HOLES_GATHER, OPT_PREFIX_PAIRED = 6, 7, 8, 9, 10
 CTR_KERNEL_LAUNCHES, CTR_H2D_BYTES, CTR_PAGE_COPIES, CTR_LAST_DECODE_CTAS, CTR_LAST_CHUNK_UNITS = 1, 2, 3, 4, 5
 CTR_LAST_PREFIX_UNITS, CTR_LAST_PREFIX_GROUPS, CTR_HOST_PAGES, CTR_COMPACT_DEVICE_NS = 6, 7, 8, 9
 CTR_LAYER_DEVICE_NS, CTR_LAYER_TIMED = 10, 11

@@ -181,3 +181,25 @@ def test_cascade_pipelined_steps_with_changing_splits():
         np.testing.assert_allclose(lse.cpu().numpy(), rl, atol=2e-3, rtol=0)
     h.check_meta()
     h.check_data()
+
+
+@pytest.mark.parametrize("P,Hq,Hkv,n_root,nq", [(16, 32, 8, 1300, None), (16, 32, 8, 4200, None), (32, 16, 8, 700, None),
+                                                  (16, 32, 8, 1300, [1, 2, 1, 3, 1, 1, 1, 1]), (16, 16, 2, 2500, None)])
+def test_cascade_paired_partition(P, Hq, Hkv, n_root, nq):
+    """KVFS_OPT_PREFIX_PAIRED = 2: lanes in pairs, 3 key pieces each, one CTA per pair running two pieces of
+    different kv heads in turn (barriers re-armed between them); the decode kernel folds the 3 records."""
+    h = Harness(3000, P, Hq, Hkv, 128, seed=90 + n_root + Hkv)
+    h.c.set_option(K.OPT_CASCADE_MIN_ENTRIES, 4)
+    h.c.set_option(K.OPT_PREFIX_PAIRED, 2)
+    with pytest.raises(Exception):
+        h.c.set_option(K.OPT_PREFIX_PAIRED, 3)
+    kids = [f"k{i}" for i in range(7)]
+    _family(h, "root", n_root, kids, [0, 3, 30, 129, 1, 64, 5], evict_root=[(100, 117)])
+    for _ in range(3):
+        st, *_ = h.pred(_decode_rows(h, kids + ["root"], nq))
+        assert st == [0] * 8
+        assert h.c.counter(K.CTR_LAST_PREFIX_GROUPS) == 1
+        # 3 pieces per lane, 5 CTAs per lane pair: 3 * Hkv units
+        assert h.c.counter(K.CTR_LAST_PREFIX_UNITS) == 3 * Hkv
+    h.check_meta()
+    h.check_data()
