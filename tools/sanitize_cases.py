@@ -93,6 +93,25 @@ def main():
         h.c.pred_step_end(step)
         torch.cuda.synchronize()
         assert abs(float(sc.sum()) - Hq) < 1e-2
+        if D == 128:
+            # cascade variants of round 2: folded split records (S = 2) and the paired partition (a CTA running
+            # two prefix units in turn), then the host-buffer pred
+            h.open("r")
+            h.append("r", list(range(700)))
+            for kid in ("r1", "r2", "r3"):
+                h.fork("r", kid)
+            for splits, paired in ((2, 0), (0, 2)):
+                h.c.set_option(K.OPT_PREFIX_SPLITS, splits)
+                h.c.set_option(K.OPT_PREFIX_PAIRED, paired)
+                rows = []
+                for nm in ("r", "r1", "r2", "r3"):
+                    rows.append((nm, [h.o.stat(h.fds[nm][1])[2] + 1]))
+                h.pred(rows)
+            h.c.set_option(K.OPT_PREFIX_SPLITS, 0)
+            h.c.set_option(K.OPT_PREFIX_PAIRED, 0)
+            h.pred([(nm, [h.o.stat(h.fds[nm][1])[2] + 1]) for nm in ("r", "r1", "a")], host_io=True)
+            h.check_meta()
+            h.check_data()
     print("sanitize cases ok")
 
 
