@@ -387,6 +387,9 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const __grid
   // launched programmatically after the table-delta prologue (no shared-prefix kernel in between): the
   // setup above overlapped its tail; wait for it before reading the page tables
   if (p.wait_at_start) asm volatile("griddepcontrol.wait;" ::: "memory");
+  // The next step's prologue (a programmatic launch that waits for this grid before touching anything) may be
+  // launched now: its launch latency then overlaps this kernel instead of following it.
+  asm volatile("griddepcontrol.launch_dependents;");
   const bool ring_live = ring < C::R && pr < p.n_rings;
 #ifdef KVFS_K1_TRACE
   if (is_producer && lane == 0 && ring_live) {

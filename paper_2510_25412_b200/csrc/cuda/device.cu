@@ -98,15 +98,29 @@ __global__ void step_prologue_kernel(uint4 *dst, const uint4 *src, int64_t n16, 
                                      const dev::PageCopy *copies, int n_copies, bf16 *const *kp, bf16 *const *vp, int L,
                                      int64_t page_elems) {
   asm volatile("griddepcontrol.launch_dependents;");
+  // Launched programmatically after the previous step's last kernel, whose trigger comes early: this grid's
+  // launch and its host-memory reads (the packet and the deltas live in this step's pinned staging buffer,
+  // which no running grid reads) overlap that kernel's tail; the stores into the upload area and the slab,
+  // which it reads, wait for it (griddepcontrol.wait).
   const int delta_blocks = (n_deltas + 255) / 256;
   const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   int64_t ddst = -1;
   dev::Entry de{};
   if (static_cast<int>(blockIdx.x) < delta_blocks && j < n_deltas) {
     ddst = delta_dst[j];
     de = delta_entries[j];
   }
-  for (int64_t i = j; i < n16; i += static_cast<int64_t>(gridDim.x) * blockDim.x) dst[i] = src[i];
+  constexpr int PRE = 4;  // packet vectors per thread loaded before the wait
+  uint4 pv[PRE];
+#pragma unroll
+  for (int k = 0; k < PRE; ++k)
+    if (j + k * stride < n16) pv[k] = src[j + k * stride];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#pragma unroll
+  for (int k = 0; k < PRE; ++k)
+    if (j + k * stride < n16) dst[j + k * stride] = pv[k];
+  for (int64_t i = j + PRE * stride; i < n16; i += stride) dst[i] = src[i];
   if (static_cast<int>(blockIdx.x) < delta_blocks) {
     if (ddst >= 0) slab[ddst] = de;
     return;
@@ -695,13 +709,25 @@ class CudaDevice final : public Device {
     const int blocks = std::max<int>(work, static_cast<int>(std::min<int64_t>((n16 + 255) / 256, 64)));
     if (blocks == 0) return KVFS_OK;
     const int64_t page_elems = static_cast<int64_t>(cfg.n_kv_heads) * cfg.page_size * cfg.head_dim;
-    step_prologue_kernel<<<blocks, 256, 0, cs(s)>>>(
-        reinterpret_cast<uint4 *>(area_), reinterpret_cast<const uint4 *>(st.dev), n16,
-        reinterpret_cast<const int64_t *>(st.dev + off_runs), n_deltas,
-        reinterpret_cast<const dev::Entry *>(st.dev + off_entries), slab_,
-        reinterpret_cast<const dev::PageCopy *>(st.dev + off_copies), n_copies, kptrs_, vptrs_, cfg.n_layers, page_elems);
+    {
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(static_cast<unsigned>(blocks));
+      lc.blockDim = dim3(256);
+      lc.stream = cs(s);
+      cudaLaunchAttribute la[1];
+      la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      la[0].val.programmaticStreamSerializationAllowed = 1;
+      lc.attrs = la;
+      lc.numAttrs = 1;
+      if (cudaLaunchKernelEx(&lc, step_prologue_kernel, reinterpret_cast<uint4 *>(area_),
+                             reinterpret_cast<const uint4 *>(st.dev), static_cast<int64_t>(n16),
+                             reinterpret_cast<const int64_t *>(st.dev + off_runs), n_deltas,
+                             reinterpret_cast<const dev::Entry *>(st.dev + off_entries), slab_,
+                             reinterpret_cast<const dev::PageCopy *>(st.dev + off_copies), n_copies, kptrs_, vptrs_,
+                             cfg.n_layers, page_elems) != cudaSuccess)
+        return KVFS_EIO;
+    }
     ++c_.ctr.launches;
-    if (cudaGetLastError() != cudaSuccess) return KVFS_EIO;
     if (cudaEventRecord(st.ev, cs(s)) != cudaSuccess) return KVFS_EIO;
     st.pending = true;
     c_.ctr.h2d_bytes += static_cast<int64_t>(used_);

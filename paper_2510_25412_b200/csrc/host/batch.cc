@@ -360,6 +360,7 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int paire
     paired = false;
   }
   if (paired_mode == 2 && paired_possible && paired_ctas < sms) paired = true;
+  if (rows_all * Hkv * 3 > max_partials) paired = false;  // its 3 records per (member row, kv head) must fit
   if (paired) {
     S = 3;
     shrink = true;
@@ -371,7 +372,6 @@ void pred_cascade(const Ctx &c, int64_t min_entries, int force_splits, int paire
   // split partials only)
   while (S > 1 && rows_all * Hkv * (fold ? S : S + 1) > max_partials) --S;
   if (rows_all * Hkv > max_partials) return;  // workspace too small: no cascade
-  if (paired && rows_all * Hkv * 3 > max_partials) paired = false, S = 2;
   pl.decode_sms = shrink ? static_cast<int32_t>(sms - (paired ? paired_ctas : units_per_split * S)) : 0;
   int64_t merged = rows_all * Hkv;            // split partials live after the merged ones
   int64_t split_next = merged;
