@@ -663,9 +663,12 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         // The partial (o, m, l) rows go out by 1-D TMA bulk stores from a shared-memory image of their global
         // layout: row R of the pair (qi = R / G, h = R % G) -> staging byte R * 4 (HD + 2), so the G rows of
         // one query token qi are one contiguous G (HD + 2)-float record, stored with one bulk copy.  The
-        // staging overlays Q, K and V (256 rows x 520 B = 130 KiB): wait for both M-tiles' MMAs first.
-        if (n_mt == 2) mbar_wait(bar(B_OF + (m ^ 1)), 0);
-        if (m == 0 && wq == 0 && lane == 0) K2G(10);  // both M-tiles' O complete
+        // staging overlays Q, K and V (256 rows x 520 B = 130 KiB).  Each M-tile stages as soon as its own O
+        // is complete: M-tile 0's half (bytes 0 .. 66.5 KiB: Q and the first 2.5 KiB of K stage 0) is dead
+        // then, because the tensor pipe runs in issue order and the MMA warp issued the last S of M-tile 1
+        // before the last P.V of M-tile 0; M-tile 1's half (66.5 .. 133 KiB: K and the first 5 KiB of V stage
+        // 0) is dead once its own last P.V, issued after M-tile 0's, completed.
+        if (m == 0 && wq == 0 && lane == 0) K2G(10);  // this M-tile's O complete
         tc_fence_after();
         constexpr int PARTF = part_floats(G, HD);
         const int Rl = m * BM + r;  // row within the pair: token Rl / G, head Rl % G
