@@ -148,17 +148,23 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
 // TMEM: S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512); P_m aliases the first 64 columns of S_m.
 namespace tc2 {
 constexpr int THREADS = 384;  // warps 0-3: K producer, MMA, TMEM alloc, V producer; 4-7, 8-11: softmax M-tiles
-constexpr int KV2 = 2;        // K stages and V stages (independent rings)
+// K and V stages (independent rings).  3 V stages (with JR = 3 to stay inside 227 KB) measured the same as 2:
+// the MMA warp's wait for V(t) (tools/k2_trace.py) is where it arrives after issuing the previous M-tile's
+// P.V and S MMAs, whose issue the tensor pipe throttles, not a late TMA.
+constexpr int KS2 = 2;
+constexpr int VS2 = 2;
 constexpr int JR = 4;         // column-metadata ring
 constexpr uint32_t O_COL2 = 256;
 constexpr int OFF_Q2 = 0;                                   // 2 Q tiles
-constexpr int OFF_K2 = OFF_Q2 + 2 * tc::TILE_BYTES;         // KV2 K tiles
-constexpr int OFF_V2 = OFF_K2 + KV2 * tc::TILE_BYTES;       // KV2 V tiles
-constexpr int OFF_JCOL2 = OFF_V2 + KV2 * tc::TILE_BYTES;    // JR x BN int32
+constexpr int OFF_K2 = OFF_Q2 + 2 * tc::TILE_BYTES;         // KS2 K tiles
+constexpr int OFF_V2 = OFF_K2 + KS2 * tc::TILE_BYTES;       // VS2 V tiles
+constexpr int OFF_JCOL2 = OFF_V2 + VS2 * tc::TILE_BYTES;    // JR x BN int32
 constexpr int OFF_BAR2 = OFF_JCOL2 + JR * tc::BN * 4 + 64;  // + JR tile flags
-constexpr int N_BARS2 = 1 + 4 * KV2 + 8 + JR + 1;
+constexpr int N_BARS2 = 1 + 2 * KS2 + 2 * VS2 + 8 + JR + 1;
 constexpr int OFF_TMEM2 = OFF_BAR2 + N_BARS2 * 8;
 constexpr int SMEM2 = OFF_TMEM2 + 16 + 1024;
+static_assert(SMEM2 <= 232448, "227 KB of dynamic shared memory per CTA");
+static_assert(256 * part_floats(1, 128) * 4 <= OFF_JCOL2, "prefix-mode record staging (256 rows, G = 1 worst case) overlays Q, K and V");
 }  // namespace tc2
 
 #ifdef KVFS_K2_TRACE
@@ -206,7 +212,8 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR2);
   auto bar = [&](int i) { return smem_u32(bars + i); };
   // barrier indices
-  constexpr int B_Q = 0, B_KF = 1, B_KE = 1 + KV2, B_VF = 1 + 2 * KV2, B_VE = 1 + 3 * KV2, B_SF = 1 + 4 * KV2,
+  constexpr int B_Q = 0, B_KF = 1, B_KE = 1 + KS2, B_VF = 1 + 2 * KS2, B_VE = 1 + 2 * KS2 + VS2,
+                B_SF = 1 + 2 * KS2 + 2 * VS2,
                 B_PF = B_SF + 2, B_OF = B_PF + 4, B_JF = B_OF + 2,  // B_PF + 2m + half
                 B_X = B_JF + JR;  // prefix mode: the split-exchange loads
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + OFF_TMEM2);
@@ -264,9 +271,11 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
   auto init_bars = [&]() {
     // prefix mode with gathered rows: one arrival per softmax warp that gathers Q; else one TMA transaction
     mbar_init(bar(B_Q), (PREFIX && q_t0 < 0) ? 4 * n_mt : 1);
-    for (int s = 0; s < KV2; ++s) {
+    for (int s = 0; s < KS2; ++s) {
       mbar_init(bar(B_KF + s), 1);
       mbar_init(bar(B_KE + s), 1);
+    }
+    for (int s = 0; s < VS2; ++s) {
       mbar_init(bar(B_VF + s), 1);
       mbar_init(bar(B_VE + s), 1);
     }
@@ -329,7 +338,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         for (int k = 0; k < HD / 16; ++k) {
           const uint32_t koff = (k >> 2) * HALF_BYTES + (k & 3) * 32;
           mma_bf16(tmem + m * BN, umma_desc(sbase + OFF_Q2 + m * TILE_BYTES + koff, 16, 1024),
-                   umma_desc(sbase + OFF_K2 + (t % KV2) * TILE_BYTES + koff, 16, 1024), ID_S, k > 0);
+                   umma_desc(sbase + OFF_K2 + (t % KS2) * TILE_BYTES + koff, 16, 1024), ID_S, k > 0);
         }
         mma_commit(bar(B_SF + m));
       }
@@ -344,7 +353,7 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
         for (int kk = 0; kk < BN / 32; ++kk) {
           const int k = half * (BN / 32) + kk;
           mma_bf16_ts(tmem + O_COL2 + m * HD, tmem + m * BN + k * 8,
-                      umma_desc(sbase + OFF_V2 + (t % KV2) * TILE_BYTES + k * 2048, HALF_BYTES, 1024), ID_O,
+                      umma_desc(sbase + OFF_V2 + (t % VS2) * TILE_BYTES + k * 2048, HALF_BYTES, 1024), ID_O,
                       (t > 0 || k > 0));
         }
         // O complete: one commit after the last tile's P.V only (the softmax waits for it once, in the
@@ -376,8 +385,8 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       int32_t erow = p.pool_rows, jbase = 0, carry = cd.first_new_lstart - cd.n_old;
       int cached = -1;
       for (int t = 0; t < n_tiles; ++t) {
-        const int s = t % KV2;
-        if (t >= KV2) mbar_wait_sleep(bar(B_KE + s), ((t / KV2) & 1) ^ 1);
+        const int s = t % KS2;
+        if (t >= KS2) mbar_wait_sleep(bar(B_KE + s), ((t / KS2) & 1) ^ 1);
         const int e0 = t * epb, blk = e0 >> 5;
         if (blk != cached) {
           const int e = blk * 32 + lane;
@@ -444,8 +453,8 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       int32_t erow = p.pool_rows;
       int cached = -1;
       for (int t = 0; t < n_tiles; ++t) {
-        const int s = t % KV2;
-        if (t >= KV2) mbar_wait_sleep(bar(B_VE + s), ((t / KV2) & 1) ^ 1);
+        const int s = t % VS2;
+        if (t >= VS2) mbar_wait_sleep(bar(B_VE + s), ((t / VS2) & 1) ^ 1);
         const int e0 = t * epb, blk = e0 >> 5;
         if (blk != cached) {
           const int e = blk * 32 + lane;
@@ -472,9 +481,9 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       if (elect_one()) mma_commit(bar(B_KE + 0));
       __syncwarp();
       for (int t = 0; t < n_tiles; ++t) {
-        const int s = t % KV2;
+        const int s = t % VS2;  // V stage of tile t
         const bool more = t + 1 < n_tiles;
-        mbar_wait(bar(B_VF + s), (t / KV2) & 1);
+        mbar_wait(bar(B_VF + s), (t / VS2) & 1);
         if (lane == 0) K2T(9, t);
         for (int m = 0; m < n_mt; ++m) {
           K2_WAIT(bar(B_PF + 2 * m), t & 1);  // softmax m wrote P(t) keys 0..63 (and corrected O)
@@ -483,13 +492,13 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
           if (lane == 0) K2T(10 + 2 * m, t);
           issue_pv(t, m, 1);
           if (more) {                       // in-order after PV(t): S(t+1) may overwrite P(t)'s columns
-            if (m == 0) mbar_wait(bar(B_KF + (t + 1) % KV2), ((t + 1) / KV2) & 1);
+            if (m == 0) mbar_wait(bar(B_KF + (t + 1) % KS2), ((t + 1) / KS2) & 1);
             issue_s(t + 1, m);
           }
           if (lane == 0) K2T(11 + 2 * m, t);
         }
         if (elect_one()) {
-          if (more) mma_commit(bar(B_KE + (t + 1) % KV2));
+          if (more) mma_commit(bar(B_KE + (t + 1) % KS2));
           mma_commit(bar(B_VE + s));
         }
         __syncwarp();
@@ -497,10 +506,8 @@ __global__ void __launch_bounds__(tc2::THREADS, 1)
       if (j + 1 < n_my) {
         // another unit follows: wait until the arrivals of the last K / V stage commits (nobody else waits
         // for them) have landed, so the barriers can be re-armed
-        for (int t = max(0, n_tiles - KV2); t < n_tiles; ++t) {
-          mbar_wait(bar(B_KE + t % KV2), (t / KV2) & 1);
-          mbar_wait(bar(B_VE + t % KV2), (t / KV2) & 1);
-        }
+        for (int t = max(0, n_tiles - KS2); t < n_tiles; ++t) mbar_wait(bar(B_KE + t % KS2), (t / KS2) & 1);
+        for (int t = max(0, n_tiles - VS2); t < n_tiles; ++t) mbar_wait(bar(B_VE + t % VS2), (t / VS2) & 1);
       }
     }
     }
