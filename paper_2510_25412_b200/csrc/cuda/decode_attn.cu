@@ -335,6 +335,19 @@ extern "C" int kvfs_debug_k1_trace(void *host, size_t bytes) {
   } while (0)
 #endif
 
+// Position of the k-th (0-based) set bit of a 16-bit mask (k < popc(m)): a 4-step popcount search.
+__device__ __forceinline__ int kth_set_bit16(uint32_t m, int k) {
+  int pos = 0;
+  int c = __popc(m & 0xFFu);
+  if (k >= c) { k -= c; pos += 8; m >>= 8; }
+  c = __popc(m & 0xFu);
+  if (k >= c) { k -= c; pos += 4; m >>= 4; }
+  c = __popc(m & 0x3u);
+  if (k >= c) { k -= c; pos += 2; m >>= 2; }
+  if (k >= static_cast<int>(m & 1u)) pos += 1;
+  return pos;
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const __grid_constant__ DecodeParams p) {
   constexpr int D = C::D, G = C::G, P = C::P, NW = C::NW, NSTAGES = C::NSTAGES;
@@ -727,12 +740,25 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const __grid
       // per-key predicates or divergent branches)
       auto sub_block = [&](auto full_tag, const uint32_t sbm, const int sb) {
         constexpr bool FULL = decltype(full_tag)::value;
+        // A partial sub-block (lazy-eviction holes, a gathered stage, the last page) walks its retained keys
+        // packed: warp step `it` scores the (it KG + kg)-th set bit of the mask, and steps past the retained
+        // count are skipped (warp-uniform), so a half-empty page costs about half the consumer work.
+        const int nk = FULL ? SUB : __popc(sbm);
+        int kslot[NIT];  // the lane's key slot per warp step (packed retained keys in a partial sub-block)
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+          const int kidx = it * KG + kg;
+          kslot[it] = FULL ? kidx : (kidx < nk ? kth_set_bit16(sbm, kidx) : 0);
+        }
         float s[NIT];
         float smax = -CUDART_INF_F;
 #pragma unroll
         for (int it = 0; it < NIT; ++it) {
-          const int slot_k = sb * SUB + it * KG + kg;
-          const bool valid = FULL || ((sbm >> (it * KG + kg)) & 1u);
+          s[it] = -CUDART_INF_F;
+          if (!FULL && it * KG >= nk) continue;  // warp-uniform
+          const int kidx = it * KG + kg;
+          const bool valid = FULL || kidx < nk;
+          const int slot_k = sb * SUB + kslot[it];
           float2 acc[G];
 #pragma unroll
           for (int h = 0; h < G; ++h) acc[h] = make_float2(0.f, 0.f);
@@ -789,8 +815,10 @@ __global__ void __launch_bounds__(C::THREADS, 1) decode_attn_kernel(const __grid
         // P.V
 #pragma unroll
         for (int it = 0; it < NIT; ++it) {
-          const int slot_k = sb * SUB + it * KG + kg;
-          const bool valid = FULL || ((sbm >> (it * KG + kg)) & 1u);
+          if (!FULL && it * KG >= nk) continue;  // warp-uniform
+          const int kidx = it * KG + kg;
+          const bool valid = FULL || kidx < nk;
+          const int slot_k = sb * SUB + kslot[it];
           const float pown = FULL ? fast_exp2(s[it] - m_own) : (valid ? fast_exp2(s[it] - m_own) : 0.f);
           l_own += pown;
           float pw[G];
