@@ -381,7 +381,7 @@ def run_ours(args):
         skew = n_files0 // 4
         odd_last = world % 2 == 1 and rank == world - 1
         n_mine = n_files0 if odd_last else (n_files0 + skew if rank % 2 == 0 else n_files0 - skew)
-        wl = DecodeWorkload(args.config, steps_total=W + Kst + min(Kst, 20) + n_e2e + 3, device=devi, n_files=n_mine,
+        wl = DecodeWorkload(args.config, steps_total=W + Kst + n_e2e + 3, device=devi, n_files=n_mine,
                             owner_base=rank * (n_files0 + skew), room_files=0 if rank % 2 == 0 else skew + 2,
                             step_owner_base=rank * 100_000)
         from paper_2510_25412_b200.parallel import rebalance
@@ -396,7 +396,7 @@ def run_ours(args):
         mstats["moved_files"] = len(mstats.get("moved_files", []))
         migration = gather_rank_info(world, dict(mstats, rank=rank, lips_before=n_mine))
     else:
-        wl = DecodeWorkload(args.config, steps_total=W + Kst + min(Kst, 20) + n_e2e + 3, device=devi, owner_base=rank * n_files0,
+        wl = DecodeWorkload(args.config, steps_total=W + Kst + n_e2e + 3, device=devi, owner_base=rank * n_files0,
                             step_owner_base=rank * 100_000)
     if args.prefix_splits:
         wl.kv.set_option(K.OPT_PREFIX_SPLITS, args.prefix_splits)
@@ -433,16 +433,14 @@ def run_ours(args):
     sampler.start()
     torch.cuda.synchronize()
     barrier()
-    # The timed steps run as a serving loop would: no instrumentation inside the library.  The attention
-    # layer's device time (first to last kernel of pred_attn_layer: chunk / shared-prefix / decode) is
-    # measured in a second pass of Kst steps (below) with the CUDA events the library records on the
-    # launching stream around its own launches (KVFS_OPT_TIMING): two event records per step cost ~16 us of
-    # host time and break the programmatic-launch chain prologue -> kernels, which on a short step (cfg3)
-    # made the timed loop itself host-bound (0.059 instead of 0.050 ms per step).  With --scores the events
-    # stay in the timed loop (the score pass is timed by Python events around its call).
-    layer_timing_in_loop = bool(args.scores)
-    n_kpass = min(Kst, 20)
-    kv.set_option(K.OPT_TIMING, 1 if layer_timing_in_loop else 0)
+    # The attention layer's device time (first to last kernel of pred_attn_layer: chunk / shared-prefix /
+    # decode) comes from CUDA events the library records on the launching stream around its own launches
+    # (KVFS_OPT_TIMING) inside the timed loop, on every `every`-th step only: two event records cost ~16 us of
+    # host time and break the programmatic-launch chain of the step, which on a short step (cfg3) made a fully
+    # instrumented loop host-bound (0.059 instead of 0.050 ms per step).  ~20 sampled steps per run; with
+    # --scores every step is instrumented (the score pass is timed by Python events around its call).
+    every = 1 if args.scores else max(1, Kst // 20)
+    kv.set_option(K.OPT_TIMING, every)
     kv.counter(K.CTR_LAYER_DEVICE_NS)  # start a new sum (the warm-up steps were not timed)
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(Kst)] if args.scores else None
     ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(Kst)] if args.scores else None
@@ -484,24 +482,12 @@ def run_ours(args):
     ms_total = t_start.elapsed_time(t_end)
     launches = kv.counter(K.CTR_KERNEL_LAUNCHES) - launches0
     h2d = kv.counter(K.CTR_H2D_BYTES) - h2d0
-    kernel_bytes, kernel_flops = alg_bytes, alg_flops
-    if not layer_timing_in_loop:
-        # second pass: min(Kst, 20) more steps with the library's per-layer events (kernel time for the
-        # roofline; the files keep growing by n_q per step, so the pass is short and its bytes are its own)
-        kv.set_option(K.OPT_TIMING, 1)
-        kv.counter(K.CTR_LAYER_DEVICE_NS)
-        kernel_bytes, kernel_flops = [], []
-        for i in range(n_kpass):
-            q, k, v = inputs[W + i]
-            wl.pre_step()
-            kernel_bytes.append(wl.algorithmic_bytes(wl.lens.copy()))
-            kernel_flops.append(wl.flops(wl.lens.copy()))
-            kv.pred_attn_batch(wl.descs, wl.positions(), q, k, v, out, lse)
-            wl.advance()
-        torch.cuda.synchronize()
+    # the sampled steps' own byte / flop counts (the files grow by n_q per step)
+    kernel_bytes = [b for i, b in enumerate(alg_bytes) if i % every == 0]
+    kernel_flops = [f for i, f in enumerate(alg_flops) if i % every == 0]
     layer_ns = kv.counter(K.CTR_LAYER_DEVICE_NS)
-    n_timed = Kst if layer_timing_in_loop else n_kpass
-    assert kv.counter(K.CTR_LAYER_TIMED) == n_timed
+    n_timed = len(kernel_bytes)
+    assert kv.counter(K.CTR_LAYER_TIMED) == n_timed, (kv.counter(K.CTR_LAYER_TIMED), n_timed)
     kv.set_option(K.OPT_TIMING, 0)
     kernel_ms = [layer_ns / 1e6 / n_timed] * n_timed
     ms_max = all_max(ms_total, world)
@@ -608,10 +594,8 @@ def run_ours(args):
                          kernel_ms_mean=k_ms, peak_source=peak_src,
                          kernel_timing="CUDA events the library records on the launching stream before the first "
                                        "and after the last kernel of each pred_attn_layer (KVFS_OPT_TIMING, "
-                                       "KVFS_CTR_LAYER_DEVICE_NS), mean over "
-                                       + ("the timed steps" if layer_timing_in_loop else
-                                          "a second pass of the same number of steps after the timed loop (the "
-                                          "timed loop itself runs without them)"),
+                                       "KVFS_CTR_LAYER_DEVICE_NS), mean over every %d-th step of the timed loop "
+                                       "(%d steps; algorithmic bytes of those steps)" % (every, len(kernel_bytes)),
                          algorithmic_bytes_per_launch=statistics.mean(kernel_bytes),
                          algorithmic_flops_per_launch=flops_mean),
         "gpu_launches": launches,

@@ -380,7 +380,9 @@ typedef enum {
                                    stores their summed device time in KVFS_CTR_COMPACT_DEVICE_NS (the host
                                    R1 / table work that overlaps it excluded); pred_attn_layer records
                                    events around its kernels (chunk, shared-prefix, decode), summed by
-                                   KVFS_CTR_LAYER_DEVICE_NS; 0 = off (default) */
+                                   KVFS_CTR_LAYER_DEVICE_NS; n > 1: only every n-th pred_attn_layer call
+                                   (counted from this setting; the first is timed) records them
+                                   (KVFS_CTR_LAYER_TIMED counts the timed calls); 0 = off (default) */
   KVFS_OPT_HOLES_GATHER = 9,    /* decode kernel, page entries whose retained slots fill less than 40% of
                                    their [lowest, highest] span (heavy lazy eviction): 1 = fetch only the
                                    retained rows with TMA gather4 (4 rows per copy, packed in shared memory;

@@ -737,7 +737,8 @@ class CudaDevice final : public Device {
   // KVFS_OPT_TIMING: events on the stream before the layer's first kernel and after its last
   int pred_layer(const PredPlan &pl, int layer, const void *q, const void *k_new, const void *v_new, void *out,
                  float *lse, float scale, kvfs_stream_t s) override {
-    if (!c_.opt_timing) return pred_layer_kernels(pl, layer, q, k_new, v_new, out, lse, scale, s);
+    if (!c_.opt_timing || (c_.layer_calls++ % c_.opt_timing_every) != 0)
+      return pred_layer_kernels(pl, layer, q, k_new, v_new, out, lse, scale, s);
     cudaEvent_t e0 = pooled_event(), e1 = pooled_event();
     if (!e0 || !e1) return KVFS_EIO;
     cudaEventRecord(e0, cs(s));

@@ -830,8 +830,10 @@ int kvfs_set_option(kvfs_ctx *ctx, int option, int64_t value) {
         c.opt_decode_chunks = value;
         return KVFS_OK;
       case KVFS_OPT_TIMING:
-        if (value < 0 || value > 1) return KVFS_EINVAL;
+        if (value < 0 || value > 1000000) return KVFS_EINVAL;
         c.opt_timing = value != 0;
+        c.opt_timing_every = value > 1 ? value : 1;
+        c.layer_calls = 0;
         return KVFS_OK;
       case KVFS_OPT_FAULT_INJECT:
         if (value < 0) return KVFS_EINVAL;

@@ -237,6 +237,8 @@ struct Ctx {
   int opt_prefix_splits = 0;  // 0 = auto
   int opt_prefix_paired = 0;  // 0 = auto, 1 = off, 2 = on when possible
   bool opt_timing = false;    // KVFS_OPT_TIMING
+  int64_t opt_timing_every = 1;  // KVFS_OPT_TIMING = n: every n-th pred_attn_layer call is timed
+  int64_t layer_calls = 0;        // pred_attn_layer calls since KVFS_OPT_TIMING was set
   int64_t last_compact_device_ns = 0;
   int64_t last_layer_timed = 0;
   CtxCounters ctr;
