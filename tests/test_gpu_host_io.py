@@ -84,3 +84,43 @@ def test_host_io_failed_rows_untouched_and_errors():
     h.c.pred_host_fence()
     torch.cuda.synchronize()
     assert torch.isnan(out.float()).all()
+
+
+def test_host_io_packed_buffers_one_copy_layout():
+    """Q / K_new / V_new (and out / lse) as views of one pinned buffer at 256-byte aligned offsets (how a serving
+    loop packs a step) give the oracle's results."""
+    h = Harness(800, 16, 8, 2, 64, seed=74)
+    for i in range(3):
+        h.open(f"p{i}")
+        h.append(f"p{i}", list(range(120 + 40 * i)))
+    descs_c = [(h.fds[f"p{i}"][0], 1 + i) for i in range(3)]
+    descs_o = [(h.fds[f"p{i}"][1], 1 + i) for i in range(3)]
+    pos = [p for i in range(3) for p in range(1000, 1001 + i)]
+    T = len(pos)
+    k, v = h._kv(T)
+    q = h._q(T, 2.0)
+
+    def packed(arrays):
+        sizes = [a.nbytes for a in arrays]
+        offs = np.concatenate([[0], np.cumsum([(z + 255) // 256 * 256 for z in sizes])]).astype(int)
+        buf = torch.full((int(offs[-1]),), 0x7F, dtype=torch.uint8).pin_memory()
+        views = []
+        for a, o, z in zip(arrays, offs, sizes):
+            t = buf[o:o + z]
+            t.copy_(torch.from_numpy(np.ascontiguousarray(a).view(np.uint8).reshape(-1)))
+            views.append(t)
+        return buf, views
+
+    _, (qb, kb, vb) = packed([q[0], k[0], v[0]])
+    qh, kh, vh = (x.view(torch.bfloat16) for x in (qb, kb, vb))
+    outbuf, (ob, lb) = packed([np.zeros((T, h.Hq, h.D), np.uint16), np.zeros((T, h.Hq), np.float32)])
+    out, lse = ob.view(torch.bfloat16).view(T, h.Hq, h.D), lb.view(torch.float32).view(T, h.Hq)
+    st = h.c.pred_attn_batch_host(descs_c, pos, qh, kh, vh, out, lse)
+    h.c.pred_host_fence()
+    torch.cuda.synchronize()
+    st_o, out_o, lse_o = h.o.pred_batch(descs_o, pos, q, k, v, h.D ** -0.5)
+    assert st == st_o == [0, 0, 0]
+    assert_close(to_bits(out), out_o[0], "packed host buffers")
+    np.testing.assert_allclose(lse.numpy(), lse_o[0], atol=2e-3, rtol=0)
+    h.check_meta()
+    h.check_data()
