@@ -184,7 +184,8 @@ def test_cascade_pipelined_steps_with_changing_splits():
 
 
 @pytest.mark.parametrize("P,Hq,Hkv,n_root,nq", [(16, 32, 8, 1300, None), (16, 32, 8, 4200, None), (32, 16, 8, 700, None),
-                                                  (16, 32, 8, 1300, [1, 2, 1, 3, 1, 1, 1, 1]), (16, 16, 2, 2500, None)])
+                                                  (16, 32, 8, 1300, [1, 2, 1, 3, 1, 1, 1, 1]), (16, 16, 2, 2500, None),
+                                                  (16, 8, 8, 1500, None)])
 def test_cascade_paired_partition(P, Hq, Hkv, n_root, nq):
     """KVFS_OPT_PREFIX_PAIRED = 2: lanes in pairs, 3 key pieces each, one CTA per pair running two pieces of
     different kv heads in turn (barriers re-armed between them); the decode kernel folds the 3 records."""

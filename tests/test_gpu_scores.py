@@ -21,8 +21,20 @@ from paper_2510_25412_b200 import kvfs as K  # noqa: E402
 def test_scores_match_oracle(P, Hq, Hkv, D, fused):
     """fused: the decode kernel writes its logits (kvfs_set_logits_buffer) and the decode descriptors' scores
     come from them (K10); chunk descriptors and cascade members still go through K9 in the same call."""
+    _scores_case(P, Hq, Hkv, D, fused)
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_scores_paired_cascade(fused):
+    """The same batch with the cascade's paired partition forced (KVFS_OPT_PREFIX_PAIRED = 2): the members'
+    attention folds 3 prefix records, their scores (K9) and the others' are unchanged."""
+    _scores_case(16, 32, 8, 128, fused, paired=2)
+
+
+def _scores_case(P, Hq, Hkv, D, fused, paired=0):
     h = Harness(4000, P, Hq, Hkv, D, seed=P + Hq + D)
     h.c.set_option(K.OPT_CASCADE_MIN_ENTRIES, 2)
+    h.c.set_option(K.OPT_PREFIX_PAIRED, paired)
     if fused:
         logits = torch.empty(16 << 20, dtype=torch.float32, device="cuda")
         h.c.set_logits_buffer(logits)
@@ -62,6 +74,8 @@ def test_scores_match_oracle(P, Hq, Hkv, D, fused):
     h.c.pred_attn_scores(step, 0, qd, lse, scores, off, scale)
     h.c.pred_step_end(step)
     torch.cuda.synchronize()
+    if paired:
+        assert h.c.counter(K.CTR_LAST_PREFIX_UNITS) == 3 * Hkv  # the paired partition ran
     n_fused = h.c.counter(K.CTR_LAST_FUSED_SCORES)
     assert (n_fused > 0) == fused, n_fused  # "solo" (and for D 64 every descriptor) is a plain decode descriptor
     if fused and D == 64:
