@@ -204,3 +204,22 @@ def test_cascade_paired_partition(P, Hq, Hkv, n_root, nq):
         assert h.c.counter(K.CTR_LAST_PREFIX_UNITS) == 3 * Hkv
     h.check_meta()
     h.check_data()
+
+
+def test_cascade_paired_two_families_and_holes():
+    """The paired partition over two families of different run lengths (one truncated member shrinks family A's
+    run), holes in the shared run, several steps: every result vs the oracle."""
+    h = Harness(3000, 16, 32, 8, 128, seed=12)
+    h.c.set_option(K.OPT_CASCADE_MIN_ENTRIES, 2)
+    h.c.set_option(K.OPT_PREFIX_PAIRED, 2)
+    _family(h, "A", 900, ["a0", "a1", "a2", "a3"], [10, 0, 33, 120], evict_root=[(40, 77), (300, 301)])
+    _family(h, "B", 2048, ["b0", "b1"], [16, 1])
+    h.truncate("a2", 500)
+    names = ["a0", "a1", "a2", "a3", "b0", "b1", "A"]
+    for _ in range(3):
+        st, *_ = h.pred(_decode_rows(h, names))
+        assert st == [0] * len(names)
+        assert h.c.counter(K.CTR_LAST_PREFIX_GROUPS) == 2
+        assert h.c.counter(K.CTR_LAST_PREFIX_UNITS) == 2 * 3 * 8
+    h.check_meta()
+    h.check_data()
